@@ -1,0 +1,853 @@
+/*
+ * cavac_oracle.c -- CPU restatement of the reference hot path, in plain C99.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library, and
+ * only as the checker.  The product path (paper_2112_00087_b200) never links
+ * or calls it.
+ *
+ * Parity is PINNED: tests/test_oracle_golden.py solves the reference's golden
+ * system (proj/tests/golden/system.mtx + rhs.csv) and requires 246
+ * iterations, the recorded final/true relres bit for bit and a byte-identical
+ * solution.csv.  Every function below cites the reference function it
+ * restates (paths relative to /root/reference).
+ *
+ * Numerics follow the reference object code: no FMA contraction (build with
+ * -ffp-contract=off), sequential left-to-right sums, complex multiply as
+ * (ac-bd, ad+bc) and complex division through libgcc __divdc3 -- the same
+ * helper std::complex<double> uses.  C99 `double complex` reaches both.
+ *
+ * GMRES(m) is NOT in the reference (krylov.cpp:377-384 rejects "gmres"); the
+ * restatement here is the beyond-reference oracle for the device GMRES and is
+ * parity-unpinned except through the solution of the same system.
+ */
+#define _POSIX_C_SOURCE 200809L
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+typedef double complex cplx;
+
+/* breakdown codes shared with include/cavac_b200.h */
+enum {
+    ORC_BRK_NONE = 0,
+    ORC_BRK_RHO = 1,        /* "rho breakdown" */
+    ORC_BRK_SHADOW_V = 2,   /* "stagnation in <shadow, v>" */
+    ORC_BRK_OMEGA = 3,      /* "omega breakdown" */
+    ORC_BRK_SHADOW_U = 4,   /* "stagnation in <shadow, u>" */
+    ORC_BRK_MR = 5,         /* "degenerate least-squares in MR step" */
+    ORC_BRK_SIGMA = 6,      /* "sigma breakdown" */
+    ORC_BRK_ARNOLDI = 7     /* "arnoldi breakdown" (gmres, beyond reference) */
+};
+
+typedef struct {
+    int32_t converged;
+    int32_t breakdown;
+    int64_t iterations;
+    double final_relres;
+    double true_relres;
+    double wall_time_s;
+    double *history;
+    int64_t history_cap;
+    int64_t history_len;
+} orc_report;
+
+typedef struct {
+    double tol;
+    int64_t max_iter;
+    int64_t l;
+    int64_t m;
+    int32_t record_history;
+    int32_t pad;
+} orc_opts;
+
+typedef struct {
+    int64_t n;
+    const int64_t *rp;
+    const int64_t *ci;
+    const cplx *v;
+} orc_csr;
+
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static void hist_push(orc_report *rep, const orc_opts *o, double v) {
+    if (!o->record_history) return;
+    if (rep->history && rep->history_len < rep->history_cap)
+        rep->history[rep->history_len] = v;
+    rep->history_len++;
+}
+
+/* ---------------- numkit (proj/core/src/numkit.cpp) ---------------- */
+
+/* csr_from_triplets numkit.cpp:41-75: range check, stable sort by (row, col),
+ * duplicates summed in input order, prefix-summed offsets.  Stable counting
+ * sort by row, then stable insertion/merge by column within each row.
+ * Returns -1 - k for the first out-of-range triplet k, else nnz. Output arrays
+ * must hold ntrip entries (upper bound). */
+static void merge_sort_cols(int64_t *idx, int64_t *tmp, int64_t n, const int64_t *col) {
+    if (n < 2) return;
+    if (n <= 16) {
+        for (int64_t i = 1; i < n; ++i) {
+            int64_t t = idx[i], j = i;
+            while (j > 0 && col[idx[j - 1]] > col[t]) { idx[j] = idx[j - 1]; --j; }
+            idx[j] = t;
+        }
+        return;
+    }
+    int64_t h = n / 2;
+    merge_sort_cols(idx, tmp, h, col);
+    merge_sort_cols(idx + h, tmp, n - h, col);
+    int64_t a = 0, b = h, k = 0;
+    while (a < h && b < n) tmp[k++] = (col[idx[b]] < col[idx[a]]) ? idx[b++] : idx[a++];
+    while (a < h) tmp[k++] = idx[a++];
+    while (b < n) tmp[k++] = idx[b++];
+    memcpy(idx, tmp, (size_t)n * sizeof(int64_t));
+}
+
+int64_t orc_csr_from_triplets(int64_t ntrip, const int64_t *row, const int64_t *col,
+                              const cplx *val, int64_t nrows, int64_t ncols,
+                              int64_t *rp, int64_t *ci, cplx *v) {
+    for (int64_t k = 0; k < ntrip; ++k)
+        if (row[k] < 0 || row[k] >= nrows || col[k] < 0 || col[k] >= ncols) return -1 - k;
+    int64_t *cnt = calloc((size_t)nrows + 1, sizeof(int64_t));
+    int64_t *order = malloc((size_t)(ntrip ? ntrip : 1) * sizeof(int64_t));
+    int64_t *tmp = malloc((size_t)(ntrip ? ntrip : 1) * sizeof(int64_t));
+    for (int64_t k = 0; k < ntrip; ++k) cnt[row[k] + 1]++;
+    for (int64_t i = 0; i < nrows; ++i) cnt[i + 1] += cnt[i];
+    int64_t *pos = malloc(((size_t)nrows + 1) * sizeof(int64_t));
+    memcpy(pos, cnt, ((size_t)nrows + 1) * sizeof(int64_t));
+    for (int64_t k = 0; k < ntrip; ++k) order[pos[row[k]]++] = k;
+    int64_t nnz = 0;
+    rp[0] = 0;
+    for (int64_t i = 0; i < nrows; ++i) {
+        int64_t b = cnt[i], e = cnt[i + 1];
+        merge_sort_cols(order + b, tmp, e - b, col);
+        for (int64_t k = b; k < e;) {
+            int64_t j = k + 1;
+            cplx sum = val[order[k]];
+            while (j < e && col[order[j]] == col[order[k]]) { sum += val[order[j]]; ++j; }
+            ci[nnz] = col[order[k]];
+            v[nnz] = sum;
+            ++nnz;
+            k = j;
+        }
+        rp[i + 1] = nnz;
+    }
+    free(cnt); free(order); free(tmp); free(pos);
+    return nnz;
+}
+
+/* spmv numkit.cpp:88-105: y_i = sum_k A[k] x[col[k]], left to right from 0. */
+void orc_spmv(const orc_csr *A, const cplx *x, cplx *y) {
+    for (int64_t i = 0; i < A->n; ++i) {
+        cplx acc = 0.0;
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) acc += A->v[k] * x[A->ci[k]];
+        y[i] = acc;
+    }
+}
+
+/* dot_hermitian numkit.cpp:113-119: sum conj(x_i) y_i, sequential. */
+cplx orc_dot(int64_t n, const cplx *x, const cplx *y) {
+    cplx acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += conj(x[i]) * y[i];
+    return acc;
+}
+
+/* norm2 numkit.cpp:121-125: sqrt(sum re^2 + im^2), sequential. */
+double orc_norm2(int64_t n, const cplx *x) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double a = creal(x[i]), b = cimag(x[i]);
+        acc += a * a + b * b;
+    }
+    return sqrt(acc);
+}
+
+/* axpy_inplace numkit.cpp:135-146: y += alpha x. */
+void orc_axpy(int64_t n, cplx alpha, const cplx *x, cplx *y) {
+    for (int64_t i = 0; i < n; ++i) y[i] += alpha * x[i];
+}
+
+/* xpay_inplace numkit.cpp:148-159: x = alpha x + y. */
+void orc_xpay(int64_t n, cplx alpha, cplx *x, const cplx *y) {
+    for (int64_t i = 0; i < n; ++i) x[i] = alpha * x[i] + y[i];
+}
+
+/* axpy (copying) numkit.cpp:127-133: z = y; z += alpha x. */
+static void axpy_copy(int64_t n, cplx alpha, const cplx *x, const cplx *y, cplx *z) {
+    memcpy(z, y, (size_t)n * sizeof(cplx));
+    orc_axpy(n, alpha, x, z);
+}
+
+/* ---------------- krylov (proj/core/src/krylov.cpp) ---------------- */
+
+/* jacobi krylov.cpp:31-55: first stored entry with col == i, inverse by
+ * 1.0 / d (complex division, __divdc3).  Returns -1 on success or the first
+ * row with a missing/zero diagonal. */
+int64_t orc_jacobi(const orc_csr *A, cplx *inv_diag) {
+    for (int64_t i = 0; i < A->n; ++i) {
+        cplx d = 0.0;
+        int found = 0;
+        for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k)
+            if (A->ci[k] == i) { d = A->v[k]; found = 1; break; }
+        if (!found || d == 0.0) return i;
+        inv_diag[i] = CMPLX(1.0, 0.0) / d;
+    }
+    return -1;
+}
+
+/* Preconditioned operator op(v) = M^{-1}(A v) (krylov.cpp:66); M given as an
+ * inverse diagonal, or NULL for the identity preconditioner (krylov.cpp:27). */
+typedef struct {
+    const orc_csr *A;
+    const cplx *dinv;
+} orc_op;
+
+static void prec_apply(const orc_op *op, const cplx *in, cplx *out) {
+    int64_t n = op->A->n;
+    if (!op->dinv) { if (out != in) memcpy(out, in, (size_t)n * sizeof(cplx)); return; }
+    for (int64_t i = 0; i < n; ++i) out[i] = op->dinv[i] * in[i];
+}
+
+static void op_apply(const orc_op *op, const cplx *in, cplx *out, cplx *scratch) {
+    orc_spmv(op->A, in, scratch);
+    prec_apply(op, scratch, out);
+}
+
+/* true_relative_residual krylov.cpp:17-23. */
+double orc_true_relres(const orc_csr *A, const cplx *b, const cplx *x) {
+    int64_t n = A->n;
+    cplx *r = malloc((size_t)n * sizeof(cplx));
+    orc_spmv(A, x, r);
+    for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+    double bn = orc_norm2(n, b);
+    double rn = orc_norm2(n, r);
+    free(r);
+    return bn > 0 ? rn / bn : rn;
+}
+
+static cplx *cvec(int64_t n) { return calloc((size_t)(n ? n : 1), sizeof(cplx)); }
+
+/* bicgstab krylov.cpp:57-138. */
+void orc_bicgstab(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o,
+                  cplx *x, orc_report *rep) {
+    double t0 = now_s();
+    int64_t n = A->n;
+    orc_op op = {A, dinv};
+    memset(x, 0, (size_t)n * sizeof(cplx));
+    cplx *r = cvec(n), *sh = cvec(n), *p = cvec(n), *v = cvec(n), *s = cvec(n),
+         *t = cvec(n), *tmp = cvec(n);
+    prec_apply(&op, b, r);
+    double bnorm = orc_norm2(n, r);
+    if (bnorm == 0.0) { rep->converged = 1; goto done_notrue; }
+    double brk = 1e-30 * bnorm * bnorm;
+    memcpy(sh, r, (size_t)n * sizeof(cplx));
+    cplx rho = 1.0, alpha = 1.0, omega = 1.0;
+    for (int64_t it = 1; it <= o->max_iter; ++it) {
+        cplx rho_new = orc_dot(n, sh, r);
+        if (cabs(rho_new) < brk) { rep->breakdown = ORC_BRK_RHO; rep->iterations = it - 1; break; }
+        if (it == 1) {
+            memcpy(p, r, (size_t)n * sizeof(cplx));
+        } else {
+            cplx beta = (rho_new / rho) * (alpha / omega);
+            orc_axpy(n, -omega, v, p);
+            orc_xpay(n, beta, p, r);
+        }
+        rho = rho_new;
+        op_apply(&op, p, v, tmp);
+        cplx gamma = orc_dot(n, sh, v);
+        if (cabs(gamma) < brk) { rep->breakdown = ORC_BRK_SHADOW_V; rep->iterations = it - 1; break; }
+        alpha = rho / gamma;
+        axpy_copy(n, -alpha, v, r, s);
+        orc_axpy(n, alpha, p, x);
+        double relres = orc_norm2(n, s) / bnorm;
+        if (relres <= o->tol) {
+            rep->converged = 1; rep->iterations = it; rep->final_relres = relres;
+            hist_push(rep, o, relres);
+            break;
+        }
+        op_apply(&op, s, t, tmp);
+        cplx tt = orc_dot(n, t, t);
+        if (cabs(tt) < brk) { rep->breakdown = ORC_BRK_OMEGA; rep->iterations = it; break; }
+        omega = orc_dot(n, t, s) / tt;
+        orc_axpy(n, omega, s, x);
+        axpy_copy(n, -omega, t, s, r);
+        relres = orc_norm2(n, r) / bnorm;
+        rep->final_relres = relres;
+        rep->iterations = it;
+        hist_push(rep, o, relres);
+        if (relres <= o->tol) { rep->converged = 1; break; }
+    }
+    rep->true_relres = orc_true_relres(A, b, x);
+done_notrue:
+    rep->wall_time_s = now_s() - t0;
+    free(r); free(sh); free(p); free(v); free(s); free(t); free(tmp);
+}
+
+/* bicgstab_l krylov.cpp:140-286 (Sleijpen-Fokkema BiCGSTAB(l), MGS MR step). */
+void orc_bicgstab_l(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o,
+                    cplx *x, orc_report *rep) {
+    double t0 = now_s();
+    int64_t n = A->n;
+    int64_t l = o->l;
+    orc_op op = {A, dinv};
+    memset(x, 0, (size_t)n * sizeof(cplx));
+    cplx *tmp = cvec(n), *sh = cvec(n);
+    cplx **r = malloc((size_t)(l + 1) * sizeof(cplx *));
+    cplx **u = malloc((size_t)(l + 1) * sizeof(cplx *));
+    for (int64_t i = 0; i <= l; ++i) { r[i] = cvec(n); u[i] = cvec(n); }
+    cplx *gam = cvec(l), *gam_p = cvec(l), *gam_pp = cvec(l), *sigma = cvec(l);
+    cplx *tau = cvec(l * l);
+    prec_apply(&op, b, r[0]);
+    double bnorm = orc_norm2(n, r[0]);
+    if (bnorm == 0.0) { rep->converged = 1; goto done_notrue; }
+    double brk = 1e-30 * bnorm * bnorm;
+    memcpy(sh, r[0], (size_t)n * sizeof(cplx));
+    cplx rho_old = 1.0, alpha = 0.0, omega = 1.0;
+    for (int64_t cycle = 1; cycle <= o->max_iter; ++cycle) {
+        rho_old = -omega * rho_old;
+        int broke = 0;
+        for (int64_t j = 0; j < l; ++j) {
+            cplx rho = orc_dot(n, sh, r[j]);
+            if (cabs(rho_old) < brk) { rep->breakdown = ORC_BRK_RHO; broke = 1; break; }
+            cplx beta = alpha * rho / rho_old;
+            rho_old = rho;
+            for (int64_t i = 0; i <= j; ++i) orc_xpay(n, -beta, u[i], r[i]);
+            op_apply(&op, u[j], u[j + 1], tmp);
+            cplx g = orc_dot(n, sh, u[j + 1]);
+            if (cabs(g) < brk) { rep->breakdown = ORC_BRK_SHADOW_U; broke = 1; break; }
+            alpha = rho_old / g;
+            for (int64_t i = 0; i <= j; ++i) orc_axpy(n, -alpha, u[i + 1], r[i]);
+            op_apply(&op, r[j], r[j + 1], tmp);
+            orc_axpy(n, alpha, u[0], x);
+            if (orc_norm2(n, r[0]) <= o->tol * bnorm) { broke = 1; break; }
+        }
+        if (broke) {
+            double relres = orc_norm2(n, r[0]) / bnorm;
+            rep->final_relres = relres;
+            if (relres <= o->tol) {
+                rep->converged = 1; rep->breakdown = ORC_BRK_NONE; rep->iterations = cycle;
+                hist_push(rep, o, relres);
+            } else {
+                rep->iterations = cycle - 1;
+            }
+            break;
+        }
+        for (int64_t j = 0; j < l; ++j) {
+            for (int64_t i = 0; i < j; ++i) {
+                tau[i * l + j] = orc_dot(n, r[i + 1], r[j + 1]) / sigma[i];
+                orc_axpy(n, -tau[i * l + j], r[i + 1], r[j + 1]);
+            }
+            sigma[j] = orc_dot(n, r[j + 1], r[j + 1]);
+            if (cabs(sigma[j]) < brk) { rep->breakdown = ORC_BRK_MR; broke = 1; break; }
+            gam_p[j] = orc_dot(n, r[j + 1], r[0]) / sigma[j];
+        }
+        if (broke) {
+            double relres = orc_norm2(n, r[0]) / bnorm;
+            rep->final_relres = relres;
+            rep->iterations = cycle;
+            if (relres <= o->tol) {
+                rep->converged = 1; rep->breakdown = ORC_BRK_NONE;
+                hist_push(rep, o, relres);
+            }
+            break;
+        }
+        gam[l - 1] = gam_p[l - 1];
+        omega = gam[l - 1];
+        for (int64_t jj = l - 1; jj-- > 0;) {
+            gam[jj] = gam_p[jj];
+            for (int64_t i = jj + 1; i < l; ++i) gam[jj] -= tau[jj * l + i] * gam[i];
+        }
+        for (int64_t j = 0; j + 1 < l; ++j) {
+            gam_pp[j] = gam[j + 1];
+            for (int64_t i = j + 1; i + 1 < l; ++i) gam_pp[j] += tau[j * l + i] * gam[i + 1];
+        }
+        orc_axpy(n, gam[0], r[0], x);
+        orc_axpy(n, -gam_p[l - 1], r[l], r[0]);
+        orc_axpy(n, -gam[l - 1], u[l], u[0]);
+        for (int64_t j = 1; j < l; ++j) {
+            orc_axpy(n, -gam[j - 1], u[j], u[0]);
+            orc_axpy(n, gam_pp[j - 1], r[j], x);
+            orc_axpy(n, -gam_p[j - 1], r[j], r[0]);
+        }
+        double relres = orc_norm2(n, r[0]) / bnorm;
+        rep->final_relres = relres;
+        rep->iterations = cycle;
+        hist_push(rep, o, relres);
+        if (relres <= o->tol) { rep->converged = 1; break; }
+    }
+    rep->true_relres = orc_true_relres(A, b, x);
+done_notrue:
+    rep->wall_time_s = now_s() - t0;
+    for (int64_t i = 0; i <= l; ++i) { free(r[i]); free(u[i]); }
+    free(r); free(u); free(tmp); free(sh);
+    free(gam); free(gam_p); free(gam_pp); free(sigma); free(tau);
+}
+
+/* tfqmr krylov.cpp:288-375. */
+void orc_tfqmr(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o,
+               cplx *x, orc_report *rep) {
+    double t0 = now_s();
+    int64_t n = A->n;
+    orc_op op = {A, dinv};
+    memset(x, 0, (size_t)n * sizeof(cplx));
+    cplx *r = cvec(n), *sh = cvec(n), *w = cvec(n), *u = cvec(n), *au = cvec(n),
+         *v = cvec(n), *d = cvec(n), *un = cvec(n), *aun = cvec(n), *tmp = cvec(n);
+    prec_apply(&op, b, r);
+    double bnorm = orc_norm2(n, r);
+    if (bnorm == 0.0) { rep->converged = 1; goto done_notrue; }
+    double brk = 1e-30 * bnorm * bnorm;
+    memcpy(sh, r, (size_t)n * sizeof(cplx));
+    memcpy(w, r, (size_t)n * sizeof(cplx));
+    memcpy(u, r, (size_t)n * sizeof(cplx));
+    op_apply(&op, u, au, tmp);
+    memcpy(v, au, (size_t)n * sizeof(cplx));
+    double tau = bnorm, theta = 0.0;
+    cplx eta = 0.0, rho = orc_dot(n, sh, r), alpha = 0.0;
+    for (int64_t hs = 0; hs < 2 * o->max_iter; ++hs) {
+        int even = (hs % 2 == 0);
+        if (even) {
+            cplx sigma = orc_dot(n, sh, v);
+            if (cabs(sigma) < brk) { rep->breakdown = ORC_BRK_SIGMA; break; }
+            alpha = rho / sigma;
+        }
+        orc_axpy(n, -alpha, au, w);
+        orc_xpay(n, theta * theta * eta / alpha, d, u);
+        theta = orc_norm2(n, w) / tau;
+        double c = 1.0 / sqrt(1.0 + theta * theta);
+        tau = tau * theta * c;
+        eta = c * c * alpha;
+        orc_axpy(n, eta, d, x);
+        double relres = tau * sqrt((double)(hs + 2)) / bnorm;
+        rep->final_relres = relres;
+        rep->iterations = hs / 2 + 1;
+        if (!even) hist_push(rep, o, relres);
+        if (relres <= o->tol) { rep->converged = 1; break; }
+        if (even) {
+            orc_axpy(n, -alpha, v, u);
+            op_apply(&op, u, au, tmp);
+        } else {
+            cplx rho_new = orc_dot(n, sh, w);
+            if (cabs(rho) < brk) { rep->breakdown = ORC_BRK_RHO; break; }
+            cplx beta = rho_new / rho;
+            rho = rho_new;
+            memcpy(un, w, (size_t)n * sizeof(cplx));
+            orc_axpy(n, beta, u, un);
+            op_apply(&op, un, aun, tmp);
+            orc_xpay(n, beta, v, au);
+            orc_xpay(n, beta, v, aun);
+            cplx *t1 = u; u = un; un = t1;
+            cplx *t2 = au; au = aun; aun = t2;
+        }
+    }
+    rep->true_relres = orc_true_relres(A, b, x);
+done_notrue:
+    rep->wall_time_s = now_s() - t0;
+    free(r); free(sh); free(w); free(u); free(au); free(v); free(d); free(un); free(aun); free(tmp);
+}
+
+/* GMRES(m), left-preconditioned, x0 = 0 -- BEYOND REFERENCE (no anchor in
+ * krylov.cpp; conventions follow krylov.hpp:46-49: convergence on the
+ * preconditioned relative residual |g_{j+1}| / ||M^{-1} b||, true relres
+ * recomputed after the loop, breakdown threshold 1e-30 ||M^{-1}b||^2).
+ * Arnoldi with classical Gram-Schmidt plus one reorthogonalisation (CGS2),
+ * Givens rotations with real cosine (moduli as sqrt(re^2+im^2), never
+ * hypot, so host and device round identically), back substitution at every
+ * restart.
+ * iterations counts Arnoldi steps.  The device solver follows exactly this
+ * order of operations. */
+void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o,
+               cplx *x, orc_report *rep) {
+    double t0 = now_s();
+    int64_t n = A->n, m = o->m < 1 ? 1 : o->m;
+    orc_op op = {A, dinv};
+    memset(x, 0, (size_t)n * sizeof(cplx));
+    cplx *r = cvec(n), *w = cvec(n), *tmp = cvec(n);
+    cplx *V = cvec((m + 1) * n);
+    cplx *H = cvec((m + 1) * m), *g = cvec(m + 1), *sn = cvec(m), *h1 = cvec(m + 1),
+         *h2 = cvec(m + 1), *y = cvec(m);
+    double *cs = calloc((size_t)m, sizeof(double));
+    prec_apply(&op, b, r);
+    double bnorm = orc_norm2(n, r);
+    if (bnorm == 0.0) { rep->converged = 1; goto done_notrue; }
+    double brk = 1e-30 * bnorm * bnorm;
+    int64_t total = 0;
+    double beta = bnorm;
+    for (;;) {
+        double relres0 = beta / bnorm;
+        if (total > 0) {
+            rep->final_relres = relres0;
+            if (relres0 <= o->tol) { rep->converged = 1; break; }
+        }
+        for (int64_t i = 0; i < n; ++i) V[i] = r[i] / beta;   /* complex / real */
+        for (int64_t i = 0; i <= m; ++i) g[i] = 0.0;
+        g[0] = beta;
+        int64_t k = 0;      /* columns built in this cycle */
+        int stop = 0;
+        for (int64_t j = 0; j < m; ++j) {
+            total++;
+            op_apply(&op, V + j * n, w, tmp);
+            for (int64_t i = 0; i <= j; ++i) h1[i] = orc_dot(n, V + i * n, w);
+            for (int64_t i = 0; i <= j; ++i) orc_axpy(n, -h1[i], V + i * n, w);
+            for (int64_t i = 0; i <= j; ++i) h2[i] = orc_dot(n, V + i * n, w);
+            for (int64_t i = 0; i <= j; ++i) orc_axpy(n, -h2[i], V + i * n, w);
+            double hn = orc_norm2(n, w);
+            for (int64_t i = 0; i <= j; ++i) H[i * m + j] = h1[i] + h2[i];
+            /* apply the previous rotations to column j */
+            for (int64_t i = 0; i < j; ++i) {
+                cplx a = H[i * m + j], c2 = H[(i + 1) * m + j];
+                H[i * m + j] = cs[i] * a + sn[i] * c2;
+                H[(i + 1) * m + j] = -conj(sn[i]) * a + cs[i] * c2;
+            }
+            cplx a = H[j * m + j];
+            double aa = sqrt(creal(a) * creal(a) + cimag(a) * cimag(a));
+            double nu = sqrt(aa * aa + hn * hn);
+            if (aa == 0.0) { cs[j] = 0.0; sn[j] = 1.0; H[j * m + j] = hn; }
+            else {
+                cs[j] = aa / nu;
+                sn[j] = (a / aa) * (hn / nu);
+                H[j * m + j] = (a / aa) * nu;
+            }
+            g[j + 1] = -conj(sn[j]) * g[j];
+            g[j] = cs[j] * g[j];
+            double gabs = sqrt(creal(g[j + 1]) * creal(g[j + 1]) + cimag(g[j + 1]) * cimag(g[j + 1]));
+            double relres = gabs / bnorm;
+            rep->final_relres = relres;
+            rep->iterations = total;
+            hist_push(rep, o, relres);
+            k = j + 1;
+            if (relres <= o->tol) { rep->converged = 1; stop = 1; break; }
+            if (hn * hn < brk) { rep->breakdown = ORC_BRK_ARNOLDI; stop = 1; break; }
+            if (total >= o->max_iter) { stop = 1; break; }
+            for (int64_t i = 0; i < n; ++i) V[(j + 1) * n + i] = w[i] / hn;
+        }
+        /* back substitution H(0:k,0:k) y = g(0:k), then x += V y */
+        for (int64_t i = k; i-- > 0;) {
+            cplx s = g[i];
+            for (int64_t q = i + 1; q < k; ++q) s -= H[i * m + q] * y[q];
+            y[i] = s / H[i * m + i];
+        }
+        for (int64_t q = 0; q < k; ++q) orc_axpy(n, y[q], V + q * n, x);
+        if (rep->breakdown == ORC_BRK_ARNOLDI && rep->final_relres <= o->tol) {
+            rep->converged = 1; rep->breakdown = ORC_BRK_NONE;
+        }
+        if (stop) break;
+        /* restart residual r = M^{-1}(b - A x) */
+        orc_spmv(A, x, tmp);
+        for (int64_t i = 0; i < n; ++i) tmp[i] = b[i] - tmp[i];
+        prec_apply(&op, tmp, r);
+        beta = orc_norm2(n, r);
+        if (beta == 0.0) { rep->converged = 1; rep->final_relres = 0.0; break; }
+    }
+    rep->true_relres = orc_true_relres(A, b, x);
+done_notrue:
+    rep->wall_time_s = now_s() - t0;
+    free(r); free(w); free(tmp); free(V); free(H); free(g); free(sn); free(h1); free(h2);
+    free(y); free(cs);
+}
+
+/* solve krylov.cpp:395-403 dispatch; solver ids shared with the C-ABI:
+ * 0 bicgstab, 1 bicgstab_l, 2 tfqmr, 3 gmres (beyond reference). */
+int orc_solve(int solver, int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v,
+              const cplx *dinv, const cplx *b, const orc_opts *o, cplx *x, orc_report *rep) {
+    orc_csr A = {n, rp, ci, v};
+    rep->converged = 0; rep->breakdown = 0; rep->iterations = 0;
+    rep->final_relres = 0; rep->true_relres = 0; rep->wall_time_s = 0; rep->history_len = 0;
+    switch (solver) {
+        case 0: orc_bicgstab(&A, dinv, b, o, x, rep); return 0;
+        case 1: if (o->l < 1) return -2; orc_bicgstab_l(&A, dinv, b, o, x, rep); return 0;
+        case 2: orc_tfqmr(&A, dinv, b, o, x, rep); return 0;
+        case 3: orc_gmres(&A, dinv, b, o, x, rep); return 0;
+    }
+    return -1;
+}
+
+int64_t orc_jacobi_arrays(int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v,
+                          cplx *inv_diag) {
+    orc_csr A = {n, rp, ci, v};
+    return orc_jacobi(&A, inv_diag);
+}
+
+void orc_spmv_arrays(int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v,
+                     const cplx *x, cplx *y) {
+    orc_csr A = {n, rp, ci, v};
+    orc_spmv(&A, x, y);
+}
+
+double orc_true_relres_arrays(int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v,
+                              const cplx *b, const cplx *x) {
+    orc_csr A = {n, rp, ci, v};
+    return orc_true_relres(&A, b, x);
+}
+
+/* ---------------- helmholtz (proj/core/src/helmholtz.cpp) ---------------- */
+
+typedef struct {
+    double width, height, h;
+    int64_t nx, ny, roof_begin, roof_end;
+    double adm_re, adm_im;
+} orc_grid;
+
+/* interior_count helmholtz.cpp:14-22 and build_grid helmholtz.cpp:25-57.
+ * Returns 0, or -1 bad dims, -2 bad roof fractions, -3 too coarse, -4 empty roof. */
+int orc_build_grid(double width, double height, double h, double rs, double re,
+                   double adm_re, double adm_im, orc_grid *g) {
+    if (width <= 0 || height <= 0 || h <= 0) return -1;
+    if (!(0.0 <= rs && rs < re && re <= 1.0)) return -2;
+    double cw = round(width / h), ch = round(height / h);
+    if (cw < 4.0 || ch < 4.0) return -3;
+    g->width = width; g->height = height; g->h = h;
+    g->nx = (int64_t)cw - 1;
+    g->ny = (int64_t)ch - 1;
+    g->adm_re = adm_re; g->adm_im = adm_im;
+    double x0 = rs * width, x1 = re * width;
+    int64_t b = g->nx, e = 0;
+    for (int64_t ix = 0; ix < g->nx; ++ix) {
+        double x = (double)(ix + 1) * h;
+        if (x >= x0 - 1e-9 && x <= x1 + 1e-9) {
+            if (ix < b) b = ix;
+            if (ix + 1 > e) e = ix + 1;
+        }
+    }
+    if (b >= e) return -4;
+    g->roof_begin = b; g->roof_end = e;
+    return 0;
+}
+
+/* assemble helmholtz.cpp:59-115 written straight into CSR: per row the
+ * triplets are left, right, below, above, diagonal; none repeat, so the
+ * stable (row, col) sort of csr_from_triplets yields ascending columns
+ * below < left < diag < right < above.  rp/ci/v sized n+1 / 5n / 5n. */
+int64_t orc_assemble(const orc_grid *g, double omega, double c, const cplx *dirichlet,
+                     int64_t *rp, int64_t *ci, cplx *v, cplx *b) {
+    int64_t nx = g->nx, ny = g->ny, n = nx * ny;
+    double k2 = c * c / (g->h * g->h);
+    cplx ww = 1.0;
+    cplx adm = CMPLX(g->adm_re, g->adm_im);
+    if (adm != 0.0) ww = CMPLX(1.0, 0.0) / (CMPLX(1.0, 0.0) + CMPLX(0.0, omega * g->h) * adm);
+    int64_t nnz = 0;
+    rp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) b[i] = 0.0;
+    for (int64_t iy = 0; iy < ny; ++iy) {
+        for (int64_t ix = 0; ix < nx; ++ix) {
+            int64_t row = iy * nx + ix;
+            cplx diag = CMPLX(4.0 * k2 - omega * omega, 0.0);
+            if (!(ix > 0)) diag -= k2 * ww;
+            if (!(ix + 1 < nx)) diag -= k2 * ww;
+            if (!(iy > 0)) diag -= k2 * ww;
+            if (!(iy + 1 < ny)) {
+                if (ix >= g->roof_begin && ix < g->roof_end)
+                    b[row] += k2 * dirichlet[ix - g->roof_begin];
+                else
+                    diag -= k2 * ww;
+            }
+            if (iy > 0) { ci[nnz] = row - nx; v[nnz++] = CMPLX(-k2, 0.0); }
+            if (ix > 0) { ci[nnz] = row - 1; v[nnz++] = CMPLX(-k2, 0.0); }
+            ci[nnz] = row; v[nnz++] = diag;
+            if (ix + 1 < nx) { ci[nnz] = row + 1; v[nnz++] = CMPLX(-k2, 0.0); }
+            if (iy + 1 < ny) { ci[nnz] = row + nx; v[nnz++] = CMPLX(-k2, 0.0); }
+            rp[row + 1] = nnz;
+        }
+    }
+    return nnz;
+}
+
+/* ---------------- schwarz (proj/core/src/schwarz.cpp) ---------------- */
+
+/* partition schwarz.cpp:93-109.  col_begin holds n_sub+1 entries. */
+int orc_partition(int64_t nx, int64_t n_sub, int64_t *col_begin) {
+    if (n_sub < 1) return -1;
+    if (n_sub > 1 && nx / 3 < n_sub) return -2;
+    int64_t base = nx / n_sub, rem = nx % n_sub;
+    col_begin[0] = 0;
+    for (int64_t s = 0; s < n_sub; ++s) col_begin[s + 1] = col_begin[s] + base + (s < rem ? 1 : 0);
+    return 0;
+}
+
+typedef struct {
+    int64_t c0, c1, n;
+    int64_t *rp, *ci;
+    cplx *v, *dinv;
+    cplx wl, wr;  /* rhs weights k2 / (1/h + s/2) */
+} orc_local;
+
+/* build_local schwarz.cpp:29-89. Returns 0 or -1 on an unexpected coupling. */
+static int build_local(const orc_grid *g, const orc_csr *A, double c, int64_t c0, int64_t c1,
+                       int hl, int hr, cplx s_left, cplx s_right, orc_local *ls) {
+    double h = g->h;
+    double k2 = c * c / (h * h);
+    int64_t w = c1 - c0, nl = w * g->ny;
+    cplx s_lc = s_right, s_rc = s_left;
+    cplx den_l = CMPLX(1.0 / h, 0.0) + 0.5 * s_lc;
+    cplx den_r = CMPLX(1.0 / h, 0.0) + 0.5 * s_rc;
+    ls->c0 = c0; ls->c1 = c1; ls->n = nl;
+    ls->wl = 0.0; ls->wr = 0.0;
+    if (hl) ls->wl = CMPLX(k2, 0.0) / den_l;
+    if (hr) ls->wr = CMPLX(k2, 0.0) / den_r;
+    int64_t cap = 6 * nl + 1, nt = 0;
+    int64_t *tr = malloc((size_t)cap * sizeof(int64_t)), *tc = malloc((size_t)cap * sizeof(int64_t));
+    cplx *tv = malloc((size_t)cap * sizeof(cplx));
+    for (int64_t iy = 0; iy < g->ny; ++iy) {
+        for (int64_t gx = c0; gx < c1; ++gx) {
+            int64_t grow = iy * g->nx + gx, lrow = iy * w + (gx - c0);
+            cplx extra = 0.0;
+            for (int64_t k = A->rp[grow]; k < A->rp[grow + 1]; ++k) {
+                int64_t gc = A->ci[k], cx = gc % g->nx;
+                if (cx >= c0 && cx < c1) {
+                    int64_t cy = gc / g->nx;
+                    tr[nt] = lrow; tc[nt] = cy * w + (cx - c0); tv[nt] = A->v[k]; nt++;
+                } else if (cx == c0 - 1 && hl) {
+                    extra += A->v[k] * ((CMPLX(1.0 / h, 0.0) - 0.5 * s_lc) / den_l);
+                } else if (cx == c1 && hr) {
+                    extra += A->v[k] * ((CMPLX(1.0 / h, 0.0) - 0.5 * s_rc) / den_r);
+                } else {
+                    free(tr); free(tc); free(tv);
+                    return -1;
+                }
+            }
+            if (extra != 0.0) { tr[nt] = lrow; tc[nt] = lrow; tv[nt] = extra; nt++; }
+        }
+    }
+    ls->rp = malloc((size_t)(nl + 1) * sizeof(int64_t));
+    ls->ci = malloc((size_t)(nt ? nt : 1) * sizeof(int64_t));
+    ls->v = malloc((size_t)(nt ? nt : 1) * sizeof(cplx));
+    ls->dinv = malloc((size_t)(nl ? nl : 1) * sizeof(cplx));
+    orc_csr_from_triplets(nt, tr, tc, tv, nl, nl, ls->rp, ls->ci, ls->v);
+    free(tr); free(tc); free(tv);
+    orc_csr L = {nl, ls->rp, ls->ci, ls->v};
+    if (orc_jacobi(&L, ls->dinv) >= 0) return -2;
+    return 0;
+}
+
+typedef struct {
+    int64_t outer_iterations;
+    int32_t converged;
+    int32_t inner_breakdown;
+    double *jump_history;
+    int64_t jump_cap;
+    int64_t jump_len;
+    int64_t last_inner_iterations_total;
+} orc_ddm_report;
+
+/* schwarz_solve schwarz.cpp:111-238 (additive two-sided optimized Schwarz). */
+int orc_schwarz_solve(const orc_grid *g, double c, int64_t n, const int64_t *rp,
+                      const int64_t *ci, const cplx *v, const cplx *b, int64_t n_sub,
+                      const int64_t *col_begin, cplx s_left, cplx s_right,
+                      const orc_opts *inner, double ddm_tol, int64_t max_outer,
+                      int inner_solver, cplx *x_out, orc_ddm_report *rep,
+                      orc_report *sub_reports) {
+    orc_csr A = {n, rp, ci, v};
+    rep->outer_iterations = 0; rep->converged = 0; rep->inner_breakdown = 0;
+    rep->jump_len = 0; rep->last_inner_iterations_total = 0;
+    if (n_sub == 1) {
+        cplx *dinv = cvec(n);
+        if (orc_jacobi(&A, dinv) >= 0) { free(dinv); return -2; }
+        orc_report sr;
+        memset(&sr, 0, sizeof sr);
+        orc_solve(inner_solver, n, rp, ci, v, dinv, b, inner, x_out, &sr);
+        rep->outer_iterations = 1;
+        rep->converged = sr.converged;
+        rep->last_inner_iterations_total = sr.iterations;
+        if (sub_reports) sub_reports[0] = sr;
+        free(dinv);
+        return 0;
+    }
+    double h = g->h;
+    int64_t ny = g->ny, nx = g->nx, ncut = n_sub - 1;
+    orc_local *ls = calloc((size_t)n_sub, sizeof(orc_local));
+    for (int64_t s = 0; s < n_sub; ++s) {
+        int e = build_local(g, &A, c, col_begin[s], col_begin[s + 1], s > 0, s + 1 < n_sub,
+                            s_left, s_right, &ls[s]);
+        if (e) return e;
+    }
+    cplx *gl = cvec(ncut * ny), *gr = cvec(ncut * ny);
+    cplx a_l = CMPLX(1.0 / h, 0.0) + 0.5 * s_left;
+    cplx b_l = CMPLX(-1.0 / h, 0.0) + 0.5 * s_left;
+    cplx a_r = CMPLX(1.0 / h, 0.0) + 0.5 * s_right;
+    cplx b_r = CMPLX(-1.0 / h, 0.0) + 0.5 * s_right;
+    cplx s_sum = s_left + s_right;
+    cplx *x = cvec(n), *xn = cvec(n);
+    cplx **uloc = calloc((size_t)n_sub, sizeof(cplx *));
+    double res0 = -1.0;
+    for (int64_t outer = 1; outer <= max_outer; ++outer) {
+        memset(xn, 0, (size_t)n * sizeof(cplx));
+        int inner_ok = 1;
+        int64_t inner_total = 0;
+        for (int64_t s = 0; s < n_sub; ++s) {
+            orc_local *L = &ls[s];
+            int64_t w = L->c1 - L->c0;
+            cplx *rhs = cvec(L->n);
+            for (int64_t iy = 0; iy < ny; ++iy)
+                for (int64_t gx = L->c0; gx < L->c1; ++gx) rhs[iy * w + gx - L->c0] = b[iy * nx + gx];
+            if (s > 0)
+                for (int64_t iy = 0; iy < ny; ++iy) rhs[iy * w] += L->wl * gr[(s - 1) * ny + iy];
+            if (s + 1 < n_sub)
+                for (int64_t iy = 0; iy < ny; ++iy) rhs[iy * w + w - 1] += L->wr * gl[s * ny + iy];
+            free(uloc[s]);
+            uloc[s] = cvec(L->n);
+            orc_report sr;
+            memset(&sr, 0, sizeof sr);
+            orc_solve(inner_solver, L->n, L->rp, L->ci, L->v, L->dinv, rhs, inner, uloc[s], &sr);
+            if (sub_reports) sub_reports[s] = sr;
+            inner_total += sr.iterations;
+            if (sr.breakdown) inner_ok = 0;
+            for (int64_t iy = 0; iy < ny; ++iy)
+                for (int64_t gx = L->c0; gx < L->c1; ++gx) xn[iy * nx + gx] = uloc[s][iy * w + gx - L->c0];
+            free(rhs);
+        }
+        for (int64_t q = 0; q < ncut; ++q) {
+            int64_t cut = col_begin[q + 1];
+            orc_local *Ll = &ls[q], *Lr = &ls[q + 1];
+            int64_t wl = Ll->c1 - Ll->c0, wr = Lr->c1 - Lr->c0;
+            for (int64_t iy = 0; iy < ny; ++iy) {
+                cplx el = uloc[q][iy * wl + (cut - 1 - Ll->c0)];
+                cplx er = uloc[q + 1][iy * wr + (cut - Lr->c0)];
+                cplx gho_l = (gl[q * ny + iy] - b_l * el) / a_l;
+                cplx gho_r = (gr[q * ny + iy] - b_r * er) / a_r;
+                cplx grn = -gl[q * ny + iy] + s_sum * 0.5 * (gho_l + el);
+                cplx gln = -gr[q * ny + iy] + s_sum * 0.5 * (gho_r + er);
+                gr[q * ny + iy] = grn;
+                gl[q * ny + iy] = gln;
+            }
+        }
+        double jump2 = 0.0;
+        for (int64_t q = 0; q < ncut; ++q) {
+            int64_t cut = col_begin[q + 1];
+            for (int64_t iy = 0; iy < ny; ++iy) {
+                cplx d1 = xn[iy * nx + cut - 1] - x[iy * nx + cut - 1];
+                jump2 += creal(d1) * creal(d1) + cimag(d1) * cimag(d1);
+                cplx d2 = xn[iy * nx + cut] - x[iy * nx + cut];
+                jump2 += creal(d2) * creal(d2) + cimag(d2) * cimag(d2);
+            }
+        }
+        double jump = sqrt(jump2);
+        if (rep->jump_history && rep->jump_len < rep->jump_cap) rep->jump_history[rep->jump_len] = jump;
+        rep->jump_len++;
+        rep->outer_iterations = outer;
+        rep->last_inner_iterations_total = inner_total;
+        cplx *t = x; x = xn; xn = t;
+        if (!inner_ok) { rep->converged = 0; rep->inner_breakdown = 1; break; }
+        if (res0 < 0.0) res0 = jump;
+        if (jump == 0.0 || jump <= ddm_tol * res0) { rep->converged = 1; break; }
+    }
+    memcpy(x_out, x, (size_t)n * sizeof(cplx));
+    for (int64_t s = 0; s < n_sub; ++s) {
+        free(ls[s].rp); free(ls[s].ci); free(ls[s].v); free(ls[s].dinv); free(uloc[s]);
+    }
+    free(ls); free(uloc); free(gl); free(gr); free(x); free(xn);
+    return 0;
+}
+
+/* Complex helpers exported so the device scalar code (cdiv emulating
+ * __divdc3) can be checked against libgcc on the host. */
+void orc_cdiv(double ar, double ai, double br, double bi, double *out) {
+    cplx q = CMPLX(ar, ai) / CMPLX(br, bi);
+    out[0] = creal(q); out[1] = cimag(q);
+}
