@@ -1,0 +1,171 @@
+/*
+ * cavac_b200.h -- C ABI of the B200-native complex-FP64 Krylov / Schwarz
+ * Helmholtz solver (libcavac_b200.so).
+ *
+ * Plain pointers and sizes only.  Complex arrays are interleaved (re, im)
+ * doubles -- the layout of std::complex<double> / CVector, so a reference
+ * caller passes values.data() / b.data() straight through.  Index arrays are
+ * uint64 like the reference's std::size_t (numkit.hpp:34-35); they are
+ * narrowed to int32 on upload with an overflow check.
+ *
+ * Every entry point returns CVK_OK (0) or a negative CVK_E* code; the message
+ * is available from cvk_last_error() (thread-local).  Non-convergence and
+ * Krylov breakdowns are NOT errors: they are reported in cvk_report, as the
+ * reference reports them in SolveReport (krylov.hpp:25-33).
+ *
+ * Reference interfaces each entry point replaces (paths relative to the
+ * reference tree proj/core/):
+ *   cvk_csr_upload        CsrMatrix (include/cavac/numkit.hpp:31-40)
+ *   cvk_precond_jacobi    jacobi (src/krylov.cpp:31-55)
+ *   cvk_precond_identity  identity_preconditioner (src/krylov.cpp:27-29)
+ *   cvk_solve             solve / bicgstab / bicgstab_l / tfqmr
+ *                         (include/cavac/krylov.hpp:50-69, src/krylov.cpp:57-403)
+ *   cvk_spmv              spmv (src/numkit.cpp:88-111)
+ *   cvk_dot, cvk_norm2    dot_hermitian, norm2 (src/numkit.cpp:113-125)
+ *   cvk_axpy, cvk_xpay    axpy_inplace, xpay_inplace (src/numkit.cpp:135-159)
+ *   cvk_true_relres       true_relative_residual (src/krylov.cpp:17-23)
+ *   cvk_set_exec_mode     set_exec_mode (src/numkit.cpp:29-30)
+ *   cvk_schwarz_solve     schwarz_solve (include/cavac/schwarz.hpp:54-58,
+ *                         src/schwarz.cpp:111-238)
+ *   cvk_assemble_cavity   build_grid + assemble (src/helmholtz.cpp:25-115),
+ *                         evaluated on the device for frequency sweeps
+ */
+#ifndef CAVAC_B200_H
+#define CAVAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVK_ABI_VERSION 1
+
+/* status codes */
+#define CVK_OK 0
+#define CVK_EINVAL -1      /* std::invalid_argument in the reference */
+#define CVK_ECUDA -2       /* CUDA runtime / launch failure */
+#define CVK_ENOMEM -3      /* device allocation failed */
+#define CVK_EOVERFLOW -4   /* index does not fit the device's int32 layout */
+#define CVK_EZERODIAG -5   /* jacobi: zero diagonal at row i (invalid_argument) */
+#define CVK_ESOLVER -6     /* unknown solver id (invalid_argument) */
+#define CVK_ELOGIC -7      /* std::logic_error in the reference */
+#define CVK_ETIMEOUT -8    /* device grid barrier timed out (never expected) */
+
+/* solver ids: the reference's SolverId order (krylov.hpp:63) + GMRES */
+#define CVK_BICGSTAB 0
+#define CVK_BICGSTAB_L 1
+#define CVK_TFQMR 2
+#define CVK_GMRES 3 /* beyond reference: restarted GMRES(m) */
+
+/* arithmetic modes */
+#define CVK_MODE_FAST 0 /* tree reductions, group-per-row SpMV (the product) */
+#define CVK_MODE_REF 1  /* reference order: row-sequential SpMV and sequential
+                           dots; bitwise identical to the reference CPU code */
+
+/* breakdown codes (SolveReport.breakdown strings, krylov.cpp) */
+#define CVK_BRK_NONE 0
+#define CVK_BRK_RHO 1        /* "rho breakdown" */
+#define CVK_BRK_SHADOW_V 2   /* "stagnation in <shadow, v>" */
+#define CVK_BRK_OMEGA 3      /* "omega breakdown" */
+#define CVK_BRK_SHADOW_U 4   /* "stagnation in <shadow, u>" */
+#define CVK_BRK_MR 5         /* "degenerate least-squares in MR step" */
+#define CVK_BRK_SIGMA 6      /* "sigma breakdown" */
+#define CVK_BRK_ARNOLDI 7    /* "arnoldi breakdown" (GMRES) */
+
+typedef struct cvk_ctx cvk_ctx;
+typedef struct cvk_csr cvk_csr;
+typedef struct cvk_prec cvk_prec;
+
+/* SolverOptions (krylov.hpp:13-18) + GMRES restart length m + arithmetic mode */
+typedef struct {
+    double tol;            /* default 1e-9 */
+    int64_t max_iter;      /* default 10000 */
+    int64_t l;             /* BiCGSTAB(l) degree, default 8 */
+    int64_t m;             /* GMRES restart, default 30 (beyond reference) */
+    int32_t record_history;
+    int32_t mode;          /* CVK_MODE_FAST / CVK_MODE_REF */
+} cvk_opts;
+
+/* SolveReport (krylov.hpp:25-33).  history is caller-owned (may be NULL);
+ * history_len is the number of entries the solver produced (it may exceed
+ * history_cap, in which case only the first history_cap were stored). */
+typedef struct {
+    int32_t converged;
+    int32_t breakdown;     /* CVK_BRK_* */
+    int64_t iterations;
+    double final_relres;   /* preconditioned, as recurred by the solver */
+    double true_relres;    /* ||b - Ax|| / ||b|| recomputed on the device */
+    double wall_time_s;    /* host wall time of the call */
+    double *history;
+    int64_t history_cap;
+    int64_t history_len;
+    double device_time_s;  /* CUDA-event time of the solve kernel(s) */
+    int64_t kernel_launches;
+} cvk_report;
+
+/* ---- version / errors ---- */
+int cvk_abi_version(void);
+const char *cvk_last_error(void);
+const char *cvk_breakdown_name(int code);
+const char *cvk_solver_name(int solver);
+int cvk_solver_from_name(const char *name); /* >= 0 id, or CVK_ESOLVER */
+
+/* ---- context: one device, one stream ---- */
+int cvk_ctx_create(int device, cvk_ctx **out);
+int cvk_ctx_destroy(cvk_ctx *ctx);
+/* the stream all work of this context is issued on (a cudaStream_t) */
+void *cvk_ctx_stream(cvk_ctx *ctx);
+/* ExecMode (numkit.hpp:14-21): 0 Sequential -> CVK_MODE_REF, 1 Parallel ->
+ * CVK_MODE_FAST.  Used when cvk_opts.mode < 0 and by the kernel calls. */
+int cvk_set_exec_mode(cvk_ctx *ctx, int parallel);
+int cvk_get_exec_mode(cvk_ctx *ctx);
+
+/* ---- matrix ---- */
+int cvk_csr_upload(cvk_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz,
+                   const uint64_t *row_offsets, const uint64_t *col_indices,
+                   const double *values, cvk_csr **out);
+/* replace the values on the same sparsity pattern (frequency sweeps) */
+int cvk_csr_set_values(cvk_csr *A, const double *values);
+int cvk_csr_free(cvk_csr *A);
+int64_t cvk_csr_nrows(const cvk_csr *A);
+int64_t cvk_csr_nnz(const cvk_csr *A);
+
+/* ---- preconditioners ---- */
+/* inv_diag (host, n complex) may be NULL: the inverse diagonal is then
+ * computed on the device with the reference's __divdc3 rounding. */
+int cvk_precond_jacobi(cvk_csr *A, const double *inv_diag, cvk_prec **out);
+int cvk_precond_identity(cvk_ctx *ctx, int64_t n, cvk_prec **out);
+int cvk_precond_free(cvk_prec *M);
+/* copy the device inverse diagonal back (n complex) */
+int cvk_precond_get_diag(const cvk_prec *M, double *inv_diag);
+
+/* ---- solve ---- */
+/* host b / x (x is overwritten; x0 = 0 as in the reference) */
+int cvk_solve(cvk_ctx *ctx, int solver, const cvk_csr *A, const cvk_prec *M,
+              const cvk_opts *opts, const double *b, double *x, cvk_report *rep);
+/* device-resident b / x (pointers into device memory of ctx's device) */
+int cvk_solve_device(cvk_ctx *ctx, int solver, const cvk_csr *A, const cvk_prec *M,
+                     const cvk_opts *opts, const double *b_dev, double *x_dev,
+                     cvk_report *rep);
+
+/* ---- kernels (parity tests; mode = CVK_MODE_*) ---- */
+int cvk_spmv(const cvk_csr *A, const double *x, double *y, int mode);
+int cvk_spmv_device(const cvk_csr *A, const double *x_dev, double *y_dev, int mode);
+int cvk_dot(cvk_ctx *ctx, int64_t n, const double *x, const double *y, double *out, int mode);
+int cvk_norm2(cvk_ctx *ctx, int64_t n, const double *x, double *out, int mode);
+int cvk_axpy(cvk_ctx *ctx, int64_t n, const double *alpha, const double *x, double *y);
+int cvk_xpay(cvk_ctx *ctx, int64_t n, const double *alpha, double *x, const double *y);
+int cvk_true_relres(const cvk_csr *A, const double *b, const double *x, double *out, int mode);
+
+/* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
+ * device buffers, returns the average kernel time in seconds ---- */
+int cvk_spmv_bench(const cvk_csr *A, const double *x_dev, double *y_dev, int mode,
+                   int reps, double *avg_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CAVAC_B200_H */

@@ -160,6 +160,11 @@ cplx orc_dot(int64_t n, const cplx *x, const cplx *y) {
     return acc;
 }
 
+void orc_dot_out(int64_t n, const cplx *x, const cplx *y, double *out) {
+    cplx d = orc_dot(n, x, y);
+    out[0] = creal(d); out[1] = cimag(d);
+}
+
 /* norm2 numkit.cpp:121-125: sqrt(sum re^2 + im^2), sequential. */
 double orc_norm2(int64_t n, const cplx *x) {
     double acc = 0.0;
@@ -739,11 +744,12 @@ typedef struct {
 /* schwarz_solve schwarz.cpp:111-238 (additive two-sided optimized Schwarz). */
 int orc_schwarz_solve(const orc_grid *g, double c, int64_t n, const int64_t *rp,
                       const int64_t *ci, const cplx *v, const cplx *b, int64_t n_sub,
-                      const int64_t *col_begin, cplx s_left, cplx s_right,
-                      const orc_opts *inner, double ddm_tol, int64_t max_outer,
+                      const int64_t *col_begin, double sl_re, double sl_im, double sr_re,
+                      double sr_im, const orc_opts *inner, double ddm_tol, int64_t max_outer,
                       int inner_solver, cplx *x_out, orc_ddm_report *rep,
                       orc_report *sub_reports) {
     orc_csr A = {n, rp, ci, v};
+    const cplx s_left = CMPLX(sl_re, sl_im), s_right = CMPLX(sr_re, sr_im);
     rep->outer_iterations = 0; rep->converged = 0; rep->inner_breakdown = 0;
     rep->jump_len = 0; rep->last_inner_iterations_total = 0;
     if (n_sub == 1) {

@@ -116,8 +116,7 @@ def lib():
         L.orc_spmv_arrays.argtypes = [C.c_int64, P, P, P, P, P]
         L.orc_true_relres_arrays.argtypes = [C.c_int64, P, P, P, P, P]
         L.orc_true_relres_arrays.restype = C.c_double
-        L.orc_dot.argtypes = [C.c_int64, P, P]
-        L.orc_dot.restype = C.c_double * 2
+        L.orc_dot_out.argtypes = [C.c_int64, P, P, P]
         L.orc_norm2.argtypes = [C.c_int64, P]
         L.orc_norm2.restype = C.c_double
         L.orc_csr_from_triplets.argtypes = [C.c_int64, P, P, P, C.c_int64, C.c_int64, P, P, P]
@@ -130,7 +129,7 @@ def lib():
         L.orc_partition.restype = C.c_int
         L.orc_schwarz_solve.argtypes = [
             C.POINTER(_Grid), C.c_double, C.c_int64, P, P, P, P, C.c_int64, P,
-            C.c_double * 2, C.c_double * 2, C.POINTER(_Opts), C.c_double, C.c_int64, C.c_int,
+            C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(_Opts), C.c_double, C.c_int64, C.c_int,
             P, C.POINTER(_DdmReport), P]
         L.orc_schwarz_solve.restype = C.c_int
         L.orc_cdiv.argtypes = [C.c_double] * 4 + [P]
@@ -205,8 +204,9 @@ def spmv(rp, ci, v, x):
 
 def dot(x, y):
     x, y = _c128(x), _c128(y)
-    r = lib().orc_dot(len(x), _p(x), _p(y))
-    return complex(r[0], r[1])
+    out = np.zeros(2)
+    lib().orc_dot_out(len(x), _p(x), _p(y), _p(out))
+    return complex(out[0], out[1])
 
 
 def norm2(x):
@@ -296,11 +296,10 @@ def schwarz_solve(grid: Grid, c, rp, ci, v, b, n_sub, s_left, s_right, tol=1e-9,
     rep.jump_history = hist.ctypes.data_as(C.POINTER(C.c_double))
     rep.jump_cap = len(hist)
     o = _opts(tol, max_iter, l, m, False)
-    sl = (C.c_double * 2)(complex(s_left).real, complex(s_left).imag)
-    sr = (C.c_double * 2)(complex(s_right).real, complex(s_right).imag)
     subs = (_Report * n_sub)()
     rc = lib().orc_schwarz_solve(C.byref(grid._g), c, n, _p(rp), _p(ci), _p(v), _p(b), n_sub,
-                                 _p(cb), sl, sr, C.byref(o), ddm_tol, max_outer,
+                                 _p(cb), complex(s_left).real, complex(s_left).imag,
+                                 complex(s_right).real, complex(s_right).imag, C.byref(o), ddm_tol, max_outer,
                                  SOLVERS[inner_solver], _p(x), C.byref(rep), C.cast(subs, C.c_void_p))
     if rc != 0:
         raise RuntimeError(f"schwarz_solve failed rc={rc}")

@@ -1,0 +1,593 @@
+// cvk_api.cu -- the C ABI declared in include/cavac_b200.h.
+//
+// Host control only: validation with the reference's error conventions
+// (krylov.cpp / numkit.cpp invalid_argument cases become CVK_EINVAL with the
+// same message text), device memory management, and one cooperative launch
+// per solve.  There is no CPU compute path: every numeric result comes from a
+// kernel; if the device or the kernel image is unavailable the call fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cavac_b200.h"
+#include "cvk_engine.cuh"
+#include "cvk_kernels.h"
+
+using cvk::DevReport;
+
+struct cvk_ctx {
+    int device = 0;
+    int nsm = 0;
+    cudaStream_t stream = nullptr;
+    int exec_parallel = 1;
+    // reusable workspace
+    void* work = nullptr;
+    size_t work_bytes = 0;
+    double2* part = nullptr;
+    size_t part_bytes = 0;
+    unsigned long long* bar = nullptr;  // [2]
+    DevReport* rep = nullptr;
+    double* hist = nullptr;
+    size_t hist_cap = 0;
+    double2* bx = nullptr;  // staging for host b / x
+    size_t bx_n = 0;
+    int* bad = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+struct cvk_csr {
+    cvk_ctx* ctx = nullptr;
+    int64_t n = 0, nnz = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double2* av = nullptr;
+    int group = 1;  // SpMV lanes per row for FAST mode
+};
+
+struct cvk_prec {
+    cvk_ctx* ctx = nullptr;
+    int64_t n = 0;
+    double2* dinv = nullptr;  // nullptr: identity
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                     \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess)                                                       \
+            return fail(e_ == cudaErrorMemoryAllocation ? CVK_ENOMEM : CVK_ECUDA,    \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));         \
+    } while (0)
+
+const char* kSolverNames[] = {"bicgstab", "bicgstab_l", "tfqmr", "gmres"};
+
+int pick_group(double avg_nnz) {
+    if (const char* env = std::getenv("CVK_SPMV_GROUP")) {
+        const int v = std::atoi(env);
+        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;
+    }
+    if (avg_nnz <= 2.5) return 1;
+    if (avg_nnz <= 6.0) return 4;
+    if (avg_nnz <= 12.0) return 8;
+    return 16;
+}
+
+int ensure(cvk_ctx* c, void** p, size_t* have, size_t need) {
+    if (*have >= need && *p) return CVK_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    CK(cudaMalloc(p, need));
+    *have = need;
+    (void)c;
+    return CVK_OK;
+}
+
+int resolve_mode(const cvk_ctx* c, int mode) {
+    if (mode == CVK_MODE_FAST || mode == CVK_MODE_REF) return mode;
+    return c->exec_parallel ? CVK_MODE_FAST : CVK_MODE_REF;
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+int cvk_abi_version(void) { return CVK_ABI_VERSION; }
+const char* cvk_last_error(void) { return g_err.c_str(); }
+
+const char* cvk_breakdown_name(int code) {
+    switch (code) {
+        case CVK_BRK_NONE: return "";
+        case CVK_BRK_RHO: return "rho breakdown";
+        case CVK_BRK_SHADOW_V: return "stagnation in <shadow, v>";
+        case CVK_BRK_OMEGA: return "omega breakdown";
+        case CVK_BRK_SHADOW_U: return "stagnation in <shadow, u>";
+        case CVK_BRK_MR: return "degenerate least-squares in MR step";
+        case CVK_BRK_SIGMA: return "sigma breakdown";
+        case CVK_BRK_ARNOLDI: return "arnoldi breakdown";
+    }
+    return "unknown breakdown";
+}
+
+const char* cvk_solver_name(int solver) {
+    if (solver < 0 || solver > 3) return "?";
+    return kSolverNames[solver];
+}
+
+int cvk_solver_from_name(const char* name) {
+    if (name)
+        for (int i = 0; i < 4; ++i)
+            if (std::strcmp(name, kSolverNames[i]) == 0) return i;
+    return fail(CVK_ESOLVER, std::string("unknown solver \"") + (name ? name : "") +
+                                 "\" (allowed: bicgstab, bicgstab_l, tfqmr, gmres)");
+}
+
+int cvk_ctx_create(int device, cvk_ctx** out) {
+    if (!out) return fail(CVK_EINVAL, "cvk_ctx_create: null out");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CVK_EINVAL, "cvk_ctx_create: no such device");
+    CK(cudaSetDevice(device));
+    cvk_ctx* c = new cvk_ctx();
+    c->device = device;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        delete c;
+        return fail(CVK_ECUDA, "cvk_ctx_create: device is not sm_100-class (built for sm_100a only)");
+    }
+    c->nsm = prop.multiProcessorCount;
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) {
+        delete c;
+        return fail(CVK_ECUDA, "cvk_ctx_create: device lacks cooperative launch");
+    }
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&c->bar, 2 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->rep, sizeof(DevReport)));
+    CK(cudaMalloc(&c->bad, sizeof(int)));
+    CK(cudaEventCreate(&c->e0));
+    CK(cudaEventCreate(&c->e1));
+    *out = c;
+    return CVK_OK;
+}
+
+int cvk_ctx_destroy(cvk_ctx* c) {
+    if (!c) return CVK_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->work);
+    cudaFree(c->part);
+    cudaFree(c->bar);
+    cudaFree(c->rep);
+    cudaFree(c->hist);
+    cudaFree(c->bx);
+    cudaFree(c->bad);
+    cudaEventDestroy(c->e0);
+    cudaEventDestroy(c->e1);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return CVK_OK;
+}
+
+void* cvk_ctx_stream(cvk_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int cvk_set_exec_mode(cvk_ctx* c, int parallel) {
+    if (!c) return fail(CVK_EINVAL, "null ctx");
+    c->exec_parallel = parallel ? 1 : 0;
+    return CVK_OK;
+}
+int cvk_get_exec_mode(cvk_ctx* c) { return c ? c->exec_parallel : 0; }
+
+int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const uint64_t* row_offsets,
+                   const uint64_t* col_indices, const double* values, cvk_csr** out) {
+    if (!c || !out) return fail(CVK_EINVAL, "cvk_csr_upload: null argument");
+    if (nrows < 0 || ncols < 0 || nnz < 0) return fail(CVK_EINVAL, "cvk_csr_upload: negative size");
+    if (nrows != ncols) return fail(CVK_EINVAL, "cvk_csr_upload: matrix must be square");
+    if (nrows >= INT32_MAX || nnz >= INT32_MAX)
+        return fail(CVK_EOVERFLOW, "cvk_csr_upload: size exceeds the int32 device index range");
+    if (!row_offsets || (nnz > 0 && (!col_indices || !values)))
+        return fail(CVK_EINVAL, "cvk_csr_upload: null array");
+    std::vector<int> rp((size_t)nrows + 1), ci((size_t)nnz);
+    if (row_offsets[0] != 0) return fail(CVK_EINVAL, "cvk_csr_upload: row_offsets[0] != 0");
+    for (int64_t i = 0; i <= nrows; ++i) {
+        if (row_offsets[i] > (uint64_t)nnz || (i > 0 && row_offsets[i] < row_offsets[i - 1]))
+            return fail(CVK_EINVAL, "cvk_csr_upload: row_offsets not monotone within [0, nnz]");
+        rp[(size_t)i] = (int)row_offsets[i];
+    }
+    if (row_offsets[nrows] != (uint64_t)nnz) return fail(CVK_EINVAL, "cvk_csr_upload: row_offsets[n] != nnz");
+    for (int64_t k = 0; k < nnz; ++k) {
+        if (col_indices[k] >= (uint64_t)ncols)
+            return fail(CVK_EINVAL, "cvk_csr_upload: column index out of range at " + std::to_string(k));
+        ci[(size_t)k] = (int)col_indices[k];
+    }
+    CK(cudaSetDevice(c->device));
+    cvk_csr* A = new cvk_csr();
+    A->ctx = c;
+    A->n = nrows;
+    A->nnz = nnz;
+    A->group = pick_group(nrows ? (double)nnz / (double)nrows : 1.0);
+    CK(cudaMalloc(&A->rp, sizeof(int) * (rp.size())));
+    CK(cudaMalloc(&A->ci, sizeof(int) * std::max<size_t>(1, ci.size())));
+    CK(cudaMalloc(&A->av, sizeof(double2) * std::max<int64_t>(1, nnz)));
+    CK(cudaMemcpyAsync(A->rp, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice, c->stream));
+    if (nnz) {
+        CK(cudaMemcpyAsync(A->ci, ci.data(), sizeof(int) * ci.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(A->av, values, sizeof(double2) * nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    *out = A;
+    return CVK_OK;
+}
+
+int cvk_csr_set_values(cvk_csr* A, const double* values) {
+    if (!A || (!values && A->nnz)) return fail(CVK_EINVAL, "cvk_csr_set_values: null argument");
+    CK(cudaSetDevice(A->ctx->device));
+    if (A->nnz)
+        CK(cudaMemcpyAsync(A->av, values, sizeof(double2) * A->nnz, cudaMemcpyHostToDevice, A->ctx->stream));
+    CK(cudaStreamSynchronize(A->ctx->stream));
+    return CVK_OK;
+}
+
+int cvk_csr_free(cvk_csr* A) {
+    if (!A) return CVK_OK;
+    cudaSetDevice(A->ctx->device);
+    cudaStreamSynchronize(A->ctx->stream);
+    cudaFree(A->rp);
+    cudaFree(A->ci);
+    cudaFree(A->av);
+    delete A;
+    return CVK_OK;
+}
+
+int64_t cvk_csr_nrows(const cvk_csr* A) { return A ? A->n : -1; }
+int64_t cvk_csr_nnz(const cvk_csr* A) { return A ? A->nnz : -1; }
+
+int cvk_precond_jacobi(cvk_csr* A, const double* inv_diag, cvk_prec** out) {
+    if (!A || !out) return fail(CVK_EINVAL, "cvk_precond_jacobi: null argument");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    cvk_prec* M = new cvk_prec();
+    M->ctx = c;
+    M->n = A->n;
+    CK(cudaMalloc(&M->dinv, sizeof(double2) * std::max<int64_t>(1, A->n)));
+    if (inv_diag) {
+        CK(cudaMemcpyAsync(M->dinv, inv_diag, sizeof(double2) * A->n, cudaMemcpyHostToDevice, c->stream));
+    } else {
+        const int big = INT32_MAX;
+        CK(cudaMemcpyAsync(c->bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CK(cvk::launch_inv_diag((int)A->n, A->rp, A->ci, A->av, M->dinv, c->bad, c->stream));
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (bad != INT32_MAX) {
+            cudaFree(M->dinv);
+            delete M;
+            return fail(CVK_EZERODIAG, "jacobi: zero diagonal at row " + std::to_string(bad));
+        }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    *out = M;
+    return CVK_OK;
+}
+
+int cvk_precond_identity(cvk_ctx* c, int64_t n, cvk_prec** out) {
+    if (!c || !out || n < 0) return fail(CVK_EINVAL, "cvk_precond_identity: bad argument");
+    cvk_prec* M = new cvk_prec();
+    M->ctx = c;
+    M->n = n;
+    *out = M;
+    return CVK_OK;
+}
+
+int cvk_precond_free(cvk_prec* M) {
+    if (!M) return CVK_OK;
+    if (M->dinv) {
+        cudaSetDevice(M->ctx->device);
+        cudaFree(M->dinv);
+    }
+    delete M;
+    return CVK_OK;
+}
+
+int cvk_precond_get_diag(const cvk_prec* M, double* inv_diag) {
+    if (!M || !inv_diag) return fail(CVK_EINVAL, "cvk_precond_get_diag: null argument");
+    if (!M->dinv) return fail(CVK_EINVAL, "cvk_precond_get_diag: identity preconditioner");
+    CK(cudaSetDevice(M->ctx->device));
+    CK(cudaMemcpy(inv_diag, M->dinv, sizeof(double2) * M->n, cudaMemcpyDeviceToHost));
+    return CVK_OK;
+}
+
+static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                      const double2* b_dev, double2* x_dev, cvk_report* rep) {
+    if (solver < 0 || solver > 3)
+        return fail(CVK_ESOLVER, "unknown solver id " + std::to_string(solver) +
+                                     " (allowed: bicgstab, bicgstab_l, tfqmr, gmres)");
+    const char* nm = kSolverNames[solver];
+    if (!A || !M || !o || !rep) return fail(CVK_EINVAL, std::string(nm) + ": null argument");
+    if (M->n != A->n) return fail(CVK_EINVAL, std::string(nm) + ": dimension mismatch");
+    if (solver == CVK_BICGSTAB_L && o->l < 1) return fail(CVK_EINVAL, "bicgstab_l: l must be >= 1");
+    if (solver == CVK_BICGSTAB_L && o->l > cvk::kMaxL)
+        return fail(CVK_EINVAL, "bicgstab_l: l exceeds the device limit of 16");
+    if (solver == CVK_GMRES && (o->m < 1 || o->m > cvk::kMaxSlots))
+        return fail(CVK_EINVAL, "gmres: m must be in [1, 64]");
+    if (o->max_iter < 0) return fail(CVK_EINVAL, std::string(nm) + ": negative max_iter");
+    const int n = (int)A->n;
+    const int mode = resolve_mode(c, o->mode);
+    const bool ref = mode == CVK_MODE_REF;
+    const int S = ref ? 1 : A->group;
+    const void* kern = cvk::solver_kernel(solver, S, ref);
+    if (!kern) return fail(CVK_ELOGIC, "no kernel for this configuration");
+    const size_t smem = cvk::solver_smem(solver, (int)o->m);
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cvk::kThreads, smem));
+    if (per_sm < 1) return fail(CVK_ECUDA, "solver kernel does not fit on an SM");
+    const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
+    long long G = std::min<long long>((long long)per_sm * c->nsm, chunks);
+    if (const char* env = std::getenv("CVK_MAX_CTAS")) G = std::min<long long>(G, std::max(1, std::atoi(env)));
+    const int nwork = cvk::solver_nwork(solver, (int)o->l, (int)o->m);
+    CK(cudaSetDevice(c->device));
+    int e;
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)nwork * std::max(1, n))) != CVK_OK)
+        return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
+        return e;
+    const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
+    if (hcap > 0 && (size_t)hcap > c->hist_cap) {
+        cudaFree(c->hist);
+        c->hist = nullptr;
+        c->hist_cap = 0;
+        CK(cudaMalloc(&c->hist, sizeof(double) * hcap));
+        c->hist_cap = (size_t)hcap;
+    }
+    CK(cudaMemsetAsync(c->bar, 0, 2 * sizeof(unsigned long long), c->stream));
+    cvk::KArgs a;
+    a.A = cvk::Csr{n, A->rp, A->ci, A->av};
+    a.dinv = M->dinv;
+    a.b = b_dev;
+    a.x = x_dev;
+    a.work = (double2*)c->work;
+    a.part = c->part;
+    a.bar = c->bar;
+    a.rep = c->rep;
+    a.hist = c->hist;
+    a.hist_cap = hcap;
+    a.tol = o->tol;
+    a.max_iter = o->max_iter;
+    a.l = (int)o->l;
+    a.m = (int)o->m;
+    a.record = o->record_history ? 1 : 0;
+    a.G = (int)G;
+    void* args[] = {&a};
+    CK(cudaEventRecord(c->e0, c->stream));
+    CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kThreads), args, smem, c->stream));
+    CK(cudaEventRecord(c->e1, c->stream));
+    DevReport dr;
+    CK(cudaMemcpyAsync(&dr, c->rep, sizeof(dr), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    if (dr.error) return fail(CVK_ETIMEOUT, std::string(nm) + ": device grid barrier aborted");
+    rep->converged = dr.converged;
+    rep->breakdown = dr.breakdown;
+    rep->iterations = dr.iterations;
+    rep->final_relres = dr.final_relres;
+    rep->true_relres = dr.true_relres;
+    rep->history_len = o->record_history ? dr.history_len : 0;
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = 1;
+    if (o->record_history && rep->history && rep->history_cap > 0) {
+        const long long k = std::min<long long>(std::min<long long>(rep->history_len, rep->history_cap), hcap);
+        if (k > 0) CK(cudaMemcpy(rep->history, c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    return CVK_OK;
+}
+
+int cvk_solve_device(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                     const double* b_dev, double* x_dev, cvk_report* rep) {
+    if (!c) return fail(CVK_EINVAL, "null ctx");
+    const double t0 = now_s();
+    const int e = solve_impl(c, solver, A, M, o, (const double2*)b_dev, (double2*)x_dev, rep);
+    if (e == CVK_OK) rep->wall_time_s = now_s() - t0;
+    return e;
+}
+
+int cvk_solve(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+              const double* b, double* x, cvk_report* rep) {
+    if (!c || !A || !b || !x) return fail(CVK_EINVAL, "cvk_solve: null argument");
+    const double t0 = now_s();
+    CK(cudaSetDevice(c->device));
+    const size_t n = (size_t)A->n;
+    size_t have = c->bx_n * 2 * sizeof(double2);
+    int e;
+    if ((e = ensure(c, (void**)&c->bx, &have, 2 * sizeof(double2) * std::max<size_t>(1, n))) != CVK_OK) return e;
+    c->bx_n = have / (2 * sizeof(double2));
+    double2* bd = c->bx;
+    double2* xd = c->bx + c->bx_n;
+    CK(cudaMemcpyAsync(bd, b, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    e = solve_impl(c, solver, A, M, o, bd, xd, rep);
+    if (e != CVK_OK) return e;
+    CK(cudaMemcpyAsync(x, xd, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    rep->wall_time_s = now_s() - t0;
+    return CVK_OK;
+}
+
+// ----------------------------------------------------------------- kernels
+
+static int stage(cvk_ctx* c, size_t n2) {
+    size_t have = c->bx_n * 2 * sizeof(double2);
+    int e = ensure(c, (void**)&c->bx, &have, std::max<size_t>(2 * sizeof(double2), n2 * sizeof(double2)));
+    if (e == CVK_OK) c->bx_n = have / (2 * sizeof(double2));
+    return e;
+}
+
+int cvk_spmv_device(const cvk_csr* A, const double* x_dev, double* y_dev, int mode) {
+    if (!A) return fail(CVK_EINVAL, "spmv: null matrix");
+    cvk_ctx* c = A->ctx;
+    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    CK(cudaSetDevice(c->device));
+    CK(cvk::launch_spmv(ref ? 1 : A->group, ref, (int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
+                        (double2*)y_dev, c->stream));
+    return CVK_OK;
+}
+
+int cvk_spmv(const cvk_csr* A, const double* x, double* y, int mode) {
+    if (!A || !x || !y) return fail(CVK_EINVAL, "spmv: null argument");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    const size_t n = (size_t)A->n;
+    int e;
+    if ((e = stage(c, 2 * n)) != CVK_OK) return e;
+    double2* xd = c->bx;
+    double2* yd = c->bx + n;
+    CK(cudaMemcpyAsync(xd, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    if ((e = cvk_spmv_device(A, (const double*)xd, (double*)yd, mode)) != CVK_OK) return e;
+    CK(cudaMemcpyAsync(y, yd, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return CVK_OK;
+}
+
+int cvk_spmv_bench(const cvk_csr* A, const double* x_dev, double* y_dev, int mode, int reps, double* avg_s) {
+    if (!A || !avg_s || reps < 1) return fail(CVK_EINVAL, "spmv_bench: bad argument");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    int e;
+    if ((e = cvk_spmv_device(A, x_dev, y_dev, mode)) != CVK_OK) return e;  // warm-up
+    CK(cudaEventRecord(c->e0, c->stream));
+    for (int r = 0; r < reps; ++r)
+        if ((e = cvk_spmv_device(A, x_dev, y_dev, mode)) != CVK_OK) return e;
+    CK(cudaEventRecord(c->e1, c->stream));
+    CK(cudaEventSynchronize(c->e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    *avg_s = (double)ms * 1e-3 / reps;
+    return CVK_OK;
+}
+
+static int dot_impl(cvk_ctx* c, int64_t n, const double* x, const double* y, double* out, int mode) {
+    if (!c || !x || !out || n < 0) return fail(CVK_EINVAL, "dot: bad argument");
+    CK(cudaSetDevice(c->device));
+    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    const size_t nn = (size_t)n;
+    int e;
+    if ((e = stage(c, 2 * nn + 2)) != CVK_OK) return e;
+    double2* xd = c->bx;
+    double2* yd = y ? c->bx + nn : nullptr;
+    double2* od = c->bx + 2 * nn;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    if (nn) CK(cudaMemcpyAsync(xd, x, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+    if (y && nn) CK(cudaMemcpyAsync(yd, y, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+    CK(cvk::launch_dot(ref, (int)n, xd, yd, c->part, od, c->stream));
+    CK(cudaMemcpyAsync(out, od, sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return CVK_OK;
+}
+
+int cvk_dot(cvk_ctx* c, int64_t n, const double* x, const double* y, double* out, int mode) {
+    if (!y) return fail(CVK_EINVAL, "dot_hermitian: null argument");
+    return dot_impl(c, n, x, y, out, mode);
+}
+
+int cvk_norm2(cvk_ctx* c, int64_t n, const double* x, double* out, int mode) {
+    double tmp[2];
+    const int e = dot_impl(c, n, x, nullptr, tmp, mode);
+    if (e == CVK_OK) *out = std::sqrt(tmp[0]);
+    return e;
+}
+
+static int axpy_like(cvk_ctx* c, int64_t n, const double* alpha, const double* x, double* y, bool xpay) {
+    if (!c || !alpha || !x || !y || n < 0) return fail(CVK_EINVAL, "axpy: bad argument");
+    CK(cudaSetDevice(c->device));
+    const size_t nn = (size_t)n;
+    int e;
+    if ((e = stage(c, 2 * nn)) != CVK_OK) return e;
+    double2* xd = c->bx;
+    double2* yd = c->bx + nn;
+    const double2 al = make_double2(alpha[0], alpha[1]);
+    if (nn) {
+        CK(cudaMemcpyAsync(xd, x, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(yd, y, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+    }
+    if (xpay) {
+        // x = alpha x + y: result lands in xd, copied back into the caller's x (passed as y here)
+        CK(cvk::launch_xpay((int)n, al, xd, yd, c->stream));
+        if (nn) CK(cudaMemcpyAsync(y, xd, sizeof(double2) * nn, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        CK(cvk::launch_axpy((int)n, al, xd, yd, c->stream));
+        if (nn) CK(cudaMemcpyAsync(y, yd, sizeof(double2) * nn, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return CVK_OK;
+}
+
+int cvk_axpy(cvk_ctx* c, int64_t n, const double* alpha, const double* x, double* y) {
+    return axpy_like(c, n, alpha, x, y, false);
+}
+
+int cvk_xpay(cvk_ctx* c, int64_t n, const double* alpha, double* x, const double* y) {
+    // axpy_like(xpay) reads "x" from its x argument and "y" from its y argument
+    // and writes the result into its y argument: route x there.
+    if (!c || !alpha || !x || !y || n < 0) return fail(CVK_EINVAL, "xpay: bad argument");
+    CK(cudaSetDevice(c->device));
+    const size_t nn = (size_t)n;
+    int e;
+    if ((e = stage(c, 2 * nn)) != CVK_OK) return e;
+    double2* xd = c->bx;
+    double2* yd = c->bx + nn;
+    if (nn) {
+        CK(cudaMemcpyAsync(xd, x, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(yd, y, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(cvk::launch_xpay((int)n, make_double2(alpha[0], alpha[1]), xd, yd, c->stream));
+    if (nn) CK(cudaMemcpyAsync(x, xd, sizeof(double2) * nn, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return CVK_OK;
+}
+
+int cvk_true_relres(const cvk_csr* A, const double* b, const double* x, double* out, int mode) {
+    if (!A || !b || !x || !out) return fail(CVK_EINVAL, "true_relres: null argument");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    const size_t n = (size_t)A->n;
+    int e;
+    if ((e = stage(c, 3 * n + 2)) != CVK_OK) return e;
+    double2* bd = c->bx;
+    double2* xd = c->bx + n;
+    double2* rd = c->bx + 2 * n;
+    double2* od = c->bx + 3 * n;
+    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    CK(cudaMemcpyAsync(bd, b, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(xd, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cvk::launch_residual(ref ? 1 : A->group, ref, (int)n, A->rp, A->ci, A->av, bd, xd, rd, c->stream));
+    CK(cvk::launch_dot(ref, (int)n, bd, nullptr, c->part, od, c->stream));
+    CK(cvk::launch_dot(ref, (int)n, rd, nullptr, c->part, od + 1, c->stream));
+    double2 h[2];
+    CK(cudaMemcpyAsync(h, od, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const double bn = std::sqrt(h[0].x), rn = std::sqrt(h[1].x);
+    *out = bn > 0 ? rn / bn : rn;
+    return CVK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,175 @@
+// cvk_blas.cu -- standalone sm_100a kernels behind the parity entry points
+// (cvk_spmv / cvk_dot / cvk_norm2 / cvk_axpy / cvk_xpay) and the Jacobi setup.
+//
+//   spmv            numkit.cpp:88-105   (group-per-row, streaming matrix loads)
+//   dot_hermitian   numkit.cpp:113-119  (FAST: fixed two-stage tree; REF: sequential)
+//   norm2           numkit.cpp:121-125
+//   axpy_inplace    numkit.cpp:135-146
+//   xpay_inplace    numkit.cpp:148-159
+//   jacobi          krylov.cpp:31-55    (first col==i entry, 1.0/d via __divdc3 rounding)
+#include "cvk_engine.cuh"
+#include "cvk_kernels.h"
+
+namespace cvk {
+
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restrict__ x,
+                                                   double2* __restrict__ y) {
+    const int G = gridDim.x;
+    for_rows<S>(A.n, G, [&](int row, int lane, bool valid) {
+        const double2 acc = row_sum<S>(A, row, lane, valid, [&](int c) { return __ldg(x + c); });
+        if (valid && lane == 0) __stcs(y + row, acc);
+    });
+}
+
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_residual(Csr A, const double2* __restrict__ b,
+                                                       const double2* __restrict__ x,
+                                                       double2* __restrict__ r) {
+    const int G = gridDim.x;
+    for_rows<S>(A.n, G, [&](int row, int lane, bool valid) {
+        const double2 acc = row_sum<S>(A, row, lane, valid, [&](int c) { return __ldg(x + c); });
+        if (valid && lane == 0) r[row] = cvk_sub(__ldg(b + row), acc);
+    });
+}
+
+__global__ void k_inv_diag(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double2* __restrict__ av, double2* __restrict__ out, int* bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double2 d = make_double2(0.0, 0.0);
+    bool found = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        if (ci[k] == i) { d = av[k]; found = true; break; }
+    }
+    if (!found || (d.x == 0.0 && d.y == 0.0)) {
+        atomicMin(bad, i);
+        out[i] = make_double2(0.0, 0.0);
+        return;
+    }
+    out[i] = cvk_cdiv(make_double2(1.0, 0.0), d);
+}
+
+constexpr int kDotBlocks = 592;  // 4 x 148: fixed, so the FAST sum order is fixed
+
+__global__ void __launch_bounds__(kThreads) k_dot_stage1(int n, const double2* __restrict__ x,
+                                                         const double2* __restrict__ y,
+                                                         double2* __restrict__ part) {
+    double2 acc[1] = {make_double2(0.0, 0.0)};
+    for_elems(n, gridDim.x, [&](int i) {
+        const double2 xi = __ldg(x + i);
+        if (y) acc_dot(acc[0], xi, __ldg(y + i));
+        else acc_norm(acc[0], xi);
+    });
+    cta_partial<1>(acc, part, gridDim.x);
+}
+
+__global__ void k_dot_stage2(const double2* __restrict__ part, int G, double2* out) {
+    double2 r[1];
+    fold_partials<1>(r, part, G);
+    if (threadIdx.x == 0) out[0] = r[0];
+}
+
+__global__ void k_dot_seq(int n, const double2* __restrict__ x, const double2* __restrict__ y,
+                          double2* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < n; ++i) {
+        if (y) acc_dot(acc, x[i], y[i]);
+        else acc_norm(acc, x[i]);
+    }
+    out[0] = acc;
+}
+
+__global__ void k_axpy(int n, double2 alpha, const double2* __restrict__ x, double2* __restrict__ y) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = cvk_add(y[i], cvk_mul(alpha, x[i]));
+}
+
+__global__ void k_xpay(int n, double2 alpha, double2* __restrict__ x, const double2* __restrict__ y) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = cvk_add(cvk_mul(alpha, x[i]), y[i]);
+}
+
+// ------------------------------------------------------------- launchers --
+
+static int grid_for(int n) {
+    long long g = ((long long)n + kThreads - 1) / kThreads;
+    return (int)(g < 1 ? 1 : g);
+}
+
+template <int S, bool REF>
+static cudaError_t spmv_t(int n, const int* rp, const int* ci, const double2* av, const double2* x,
+                          double2* y, cudaStream_t st) {
+    Csr A{n, rp, ci, av};
+    k_spmv<S, REF><<<grid_for(n), kThreads, 0, st>>>(A, x, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
+                        const double2* x, double2* y, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (ref) return spmv_t<1, true>(n, rp, ci, av, x, y, st);
+    switch (S) {
+        case 1: return spmv_t<1, false>(n, rp, ci, av, x, y, st);
+        case 2: return spmv_t<2, false>(n, rp, ci, av, x, y, st);
+        case 4: return spmv_t<4, false>(n, rp, ci, av, x, y, st);
+        case 8: return spmv_t<8, false>(n, rp, ci, av, x, y, st);
+        case 16: return spmv_t<16, false>(n, rp, ci, av, x, y, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int S, bool REF>
+static cudaError_t resid_t(int n, const int* rp, const int* ci, const double2* av, const double2* b,
+                           const double2* x, double2* r, cudaStream_t st) {
+    Csr A{n, rp, ci, av};
+    k_residual<S, REF><<<grid_for(n), kThreads, 0, st>>>(A, b, x, r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
+                            const double2* b, const double2* x, double2* r, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (ref) return resid_t<1, true>(n, rp, ci, av, b, x, r, st);
+    switch (S) {
+        case 1: return resid_t<1, false>(n, rp, ci, av, b, x, r, st);
+        case 2: return resid_t<2, false>(n, rp, ci, av, b, x, r, st);
+        case 4: return resid_t<4, false>(n, rp, ci, av, b, x, r, st);
+        case 8: return resid_t<8, false>(n, rp, ci, av, b, x, r, st);
+        case 16: return resid_t<16, false>(n, rp, ci, av, b, x, r, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
+                            int* bad_row, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_inv_diag<<<grid_for(n), kThreads, 0, st>>>(n, rp, ci, av, out, bad_row);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dot(bool ref, int n, const double2* x, const double2* y, double2* part,
+                       double2* out, cudaStream_t st) {
+    if (ref) {
+        k_dot_seq<<<1, 32, 0, st>>>(n, x, y, out);
+    } else {
+        k_dot_stage1<<<kDotBlocks, kThreads, 0, st>>>(n, x, y, part);
+        k_dot_stage2<<<1, kThreads, 0, st>>>(part, kDotBlocks, out);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(int n, double2 alpha, const double2* x, double2* y, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_axpy<<<grid_for(n), kThreads, 0, st>>>(n, alpha, x, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpay(int n, double2 alpha, double2* x, const double2* y, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_xpay<<<grid_for(n), kThreads, 0, st>>>(n, alpha, x, y);
+    return cudaGetLastError();
+}
+
+}  // namespace cvk

@@ -1,0 +1,283 @@
+// cvk_engine.cuh -- building blocks of the persistent Krylov kernels.
+//
+// One cooperative grid of G CTAs x 256 threads runs a whole solve.  Rows are
+// owned in chunks of 256: CTA b owns chunks b, b+G, b+2G, ...  Element loops
+// map chunk row i to thread i; SpMV loops walk the same chunk with S lanes
+// per row in S sub-rounds, so both loop kinds touch the same rows per CTA and
+// only a __syncthreads separates them.  Phases are separated by a grid
+// barrier (monotone 64-bit arrival counter, acquire spin, globaltimer abort).
+//
+// Reductions are deterministic:
+//  * FAST: each thread accumulates in grid-stride order, warps reduce by a
+//    fixed xor tree, CTAs write one partial per slot, and after the barrier
+//    EVERY CTA folds the G partials in the same fixed order -- all CTAs hold
+//    bitwise identical scalars, so the redundant scalar recurrences on every
+//    CTA agree without a broadcast phase.
+//  * REF: after the barrier thread 0 of every CTA re-reads the vectors and
+//    sums them left to right, exactly as dot_hermitian / norm2 do
+//    (numkit.cpp:113-125).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cvk_complex.h"
+
+namespace cvk {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxSlots = 64;
+constexpr int kRegions = 3;
+
+struct DevReport {
+    int32_t converged;
+    int32_t breakdown;
+    int64_t iterations;
+    double final_relres;
+    double true_relres;
+    int64_t history_len;
+    int32_t error;
+    int32_t pad;
+};
+
+struct Csr {
+    int n;
+    const int* __restrict__ rp;
+    const int* __restrict__ ci;
+    const double2* __restrict__ av;
+};
+
+// Kernel arguments (passed by value to cudaLaunchCooperativeKernel).
+struct KArgs {
+    Csr A;
+    const double2* dinv;  // nullptr -> identity preconditioner
+    const double2* b;
+    double2* x;
+    double2* work;        // nwork vectors of length n, contiguous
+    double2* part;        // kRegions x kMaxSlots x G partials
+    unsigned long long* bar;  // [0] arrival counter, [1] abort flag
+    DevReport* rep;
+    double* hist;
+    long long hist_cap;
+    double tol;
+    long long max_iter;
+    int l;
+    int m;
+    int record;
+    int G;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Grid barrier over the G co-resident CTAs of a cooperative launch.
+struct GridBar {
+    unsigned long long* bar;
+    unsigned long long target;
+    unsigned G;
+
+    __device__ GridBar(unsigned long long* b, int g) : bar(b), target(0), G((unsigned)g) {}
+
+    // returns false if the barrier was aborted (timeout anywhere in the grid)
+    __device__ bool sync() {
+        __shared__ int s_ok;
+        __syncthreads();
+        target += G;
+        if (threadIdx.x == 0) {
+            int ok = 1;
+            __threadfence();
+            atomicAdd(bar, 1ull);
+            const unsigned long long t0 = global_ns();
+            unsigned spins = 0;
+            while (ld_acquire_u64(bar) < target) {
+                if ((++spins & 1023u) == 0) {
+                    if (*((volatile unsigned long long*)(bar + 1)) != 0ull) { ok = 0; break; }
+                    if (global_ns() - t0 > 30000000000ull) {  // 30 s: never in a sane solve
+                        atomicExch(bar + 1, 1ull);
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+            __threadfence();
+            s_ok = ok;
+        }
+        __syncthreads();
+        return s_ok != 0;
+    }
+};
+
+// Streaming loads of the matrix (read once per SpMV: keep them out of L1).
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// ---------------------------------------------------------------- loops --
+
+// Element loop over the CTA's chunks: f(i) for every owned row i < n.
+template <class F>
+__device__ __forceinline__ void for_elems(int n, int G, F&& f) {
+    for (long long base = (long long)blockIdx.x * kThreads; base < n; base += (long long)G * kThreads) {
+        const long long i = base + threadIdx.x;
+        if (i < n) f((int)i);
+    }
+}
+
+// Row loop with S lanes per row over the same chunks.  f(row, lane, valid)
+// is called by every thread (valid=false past n) so group shuffles are safe.
+template <int S, class F>
+__device__ __forceinline__ void for_rows(int n, int G, F&& f) {
+    constexpr int gpb = kThreads / S;
+    const int lane = threadIdx.x & (S - 1);
+    const int grp = threadIdx.x / S;
+    for (long long base = (long long)blockIdx.x * kThreads; base < n; base += (long long)G * kThreads) {
+#pragma unroll 1
+        for (int sub = 0; sub < S; ++sub) {
+            const long long row = base + (long long)sub * gpb + grp;
+            f((int)row, lane, row < n);
+        }
+    }
+}
+
+// Row sum y = sum_k A[row,k] * x(col_k): left to right per lane; for S > 1
+// the S lane sums are combined by a fixed xor tree (all lanes get the sum).
+// With S == 1 this is exactly the reference's row loop (numkit.cpp:98-103).
+template <int S, class X>
+__device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool valid, X&& xat) {
+    double2 acc = make_double2(0.0, 0.0);
+    if (valid) {
+        const int b = __ldg(A.rp + row), e = __ldg(A.rp + row + 1);
+        for (int k = b + lane; k < e; k += S) {
+            const double2 a = ld_stream(A.av + k);
+            const int c = ld_stream(A.ci + k);
+            acc = cvk_add(acc, cvk_mul(a, xat(c)));
+        }
+    }
+    if (S > 1) {
+#pragma unroll
+        for (int o = S / 2; o > 0; o >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+    }
+    return acc;
+}
+
+// ----------------------------------------------------------- reductions --
+
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    return v;
+}
+
+// FAST: CTA partial of K slots -> part[k*G + blockIdx.x]
+template <int K>
+__device__ __forceinline__ void cta_partial(const double2 (&acc)[K], double2* part, int G) {
+    __shared__ double2 sm[K][kWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double2 v = warp_sum(acc[k]);
+        if (lane == 0) sm[k][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double2 s = sm[threadIdx.x][0];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
+        part[threadIdx.x * G + blockIdx.x] = s;
+    }
+}
+
+// FAST: after the barrier, every CTA folds the G partials in the same order.
+template <int K>
+__device__ __forceinline__ void fold_partials(double2 (&out)[K], const double2* part, int G) {
+    __shared__ double2 res[K];
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double2 s = make_double2(0.0, 0.0);
+            for (int b = lane; b < G; b += 32) s = cvk_add(s, __ldcg(part + k * G + b));
+            s = warp_sum(s);
+            if (lane == 0) res[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = res[k];
+}
+
+// REF: thread 0 of every CTA runs the sequential sums; contrib(i, acc)
+// adds element i's terms exactly as the reference loop would.
+template <int K, class C>
+__device__ __forceinline__ void seq_sums(double2 (&out)[K], int n, C&& contrib) {
+    __shared__ double2 res[K];
+    if (threadIdx.x == 0) {
+        double2 acc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+        for (int i = 0; i < n; ++i) contrib(i, acc);
+#pragma unroll
+        for (int k = 0; k < K; ++k) res[k] = acc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] = res[k];
+}
+
+// One reduction phase end: partials/sequential sums + grid barrier.
+template <bool REF, int K, class C>
+__device__ __forceinline__ bool reduce(GridBar& g, const double2 (&acc)[K], double2 (&out)[K],
+                                       double2* part, int n, C&& contrib) {
+    if (REF) {
+        if (!g.sync()) return false;
+        seq_sums<K>(out, n, contrib);
+    } else {
+        cta_partial<K>(acc, part, g.G);
+        if (!g.sync()) return false;
+        fold_partials<K>(out, part, g.G);
+    }
+    return true;
+}
+
+// Accumulation helpers used inside the phase loops (FAST) and by the REF
+// contrib functors -- the same expression in both, so the per-element terms
+// are rounded identically.
+__device__ __forceinline__ void acc_norm(double2& a, double2 v) { a.x += cvk_norm(v); }
+__device__ __forceinline__ void acc_dot(double2& a, double2 x, double2 y) { a = cvk_add(a, cvk_cmul(x, y)); }
+
+__device__ __forceinline__ double2 prec_apply(const double2* dinv, int i, double2 y) {
+    return dinv ? cvk_mul(__ldg(dinv + i), y) : y;
+}
+
+// Report / history writers (CTA 0, thread 0).
+__device__ __forceinline__ void hist_push(const KArgs& a, long long& len, double v) {
+    if (!a.record) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && len < a.hist_cap) a.hist[len] = v;
+    ++len;
+}
+
+}  // namespace cvk

@@ -1,0 +1,35 @@
+// cvk_kernels.h -- internal interface between the C ABI (cvk_api.cu) and the
+// kernel translation units.  Not installed; the public surface is
+// include/cavac_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cvk {
+
+constexpr int kMaxL = 16;  // BiCGSTAB(l): l <= kMaxL
+
+struct Csr;
+struct DevReport;
+
+// persistent solver kernels (cvk_krylov.cu)
+const void* solver_kernel(int solver, int S, bool ref);
+int solver_nwork(int solver, int l, int m);
+size_t solver_smem(int solver, int m);
+
+// standalone kernels (cvk_blas.cu); all enqueue on `st`
+cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
+                        const double2* x, double2* y, cudaStream_t st);
+cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
+                            int* bad_row, cudaStream_t st);
+// out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 1024 double2
+cudaError_t launch_dot(bool ref, int n, const double2* x, const double2* y, double2* part,
+                       double2* out, cudaStream_t st);
+cudaError_t launch_axpy(int n, double2 alpha, const double2* x, double2* y, cudaStream_t st);
+cudaError_t launch_xpay(int n, double2 alpha, double2* x, const double2* y, cudaStream_t st);
+cudaError_t launch_residual(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
+                            const double2* b, const double2* x, double2* r, cudaStream_t st);
+
+}  // namespace cvk

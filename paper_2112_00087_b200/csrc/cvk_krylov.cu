@@ -1,0 +1,960 @@
+// cvk_krylov.cu -- persistent, cooperative Krylov solvers for complex-FP64
+// CSR systems on sm_100a.  One launch = one complete solve: every scalar
+// recurrence runs on the device (redundantly and bitwise identically in every
+// CTA), so there is no host round trip per iteration.
+//
+// Reference algorithms (paths relative to the reference's proj/core/):
+//   bicgstab    src/krylov.cpp:57-138
+//   bicgstab_l  src/krylov.cpp:140-286
+//   tfqmr       src/krylov.cpp:288-375
+//   gmres       beyond reference (oracle/cavac_oracle.c orc_gmres)
+//   true_relative_residual src/krylov.cpp:17-23
+//
+// Fusion: each phase between two grid barriers fuses the reference's vector
+// updates with the SpMV + Jacobi apply that consumes them; vectors that the
+// SpMV gathers at neighbour columns are produced on the fly from their inputs
+// (e.g. p = r + beta (p - omega v) inside the SpMV of p), ping-ponged so the
+// owner's write never races a neighbour's read.  Per element the arithmetic
+// is exactly the reference's sequence of roundings, so in REF mode (S = 1,
+// sequential sums) the iterates are bitwise those of the reference.
+#include "cvk_engine.cuh"
+#include "cvk_kernels.h"
+
+namespace cvk {
+
+namespace {
+
+__device__ __forceinline__ void write_report(const KArgs& a, int conv, int brk, long long it,
+                                             double final_relres, double true_relres,
+                                             long long hist_len, int err) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.rep->converged = conv;
+        a.rep->breakdown = brk;
+        a.rep->iterations = it;
+        a.rep->final_relres = final_relres;
+        a.rep->true_relres = true_relres;
+        a.rep->history_len = hist_len;
+        a.rep->error = err;
+    }
+}
+
+// ||b - A x|| / ||b|| (krylov.cpp:17-23); scratch receives b - Ax.
+template <int S, bool REF>
+__device__ bool true_relres(GridBar& g, const KArgs& a, double2* scratch, double2* part,
+                            double& out) {
+    const int n = a.A.n;
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    const double2* x = a.x;
+    const double2* b = a.b;
+    for_rows<S>(n, a.G, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S>(a.A, row, lane, valid, [&](int c) { return x[c]; });
+        if (valid && lane == 0) {
+            const double2 bi = __ldg(b + row);
+            const double2 d = cvk_sub(bi, y);
+            scratch[row] = d;
+            if (!REF) { acc_norm(acc[0], bi); acc_norm(acc[1], d); }
+        }
+    });
+    double2 tot[2];
+    if (!reduce<REF, 2>(g, acc, tot, part, n, [&](int i, double2* q) {
+            acc_norm(q[0], b[i]);
+            acc_norm(q[1], scratch[i]);
+        }))
+        return false;
+    const double bn = sqrt(tot[0].x);
+    const double rn = sqrt(tot[1].x);
+    out = bn > 0 ? rn / bn : rn;
+    return true;
+}
+
+}  // namespace
+
+// ================================================================ BiCGSTAB
+// work: r, shadow, s, t, p[2], v[2]
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_bicgstab(KArgs a) {
+    GridBar g(a.bar, a.G);
+    const int n = a.A.n, G = a.G;
+    const double2* __restrict__ dinv = a.dinv;
+    const double2* __restrict__ b = a.b;
+    double2* x = a.x;
+    double2* r = a.work;
+    double2* sh = a.work + (size_t)n;
+    double2* s = a.work + 2 * (size_t)n;
+    double2* t = a.work + 3 * (size_t)n;
+    double2* pv[2] = {a.work + 4 * (size_t)n, a.work + 5 * (size_t)n};
+    double2* vv[2] = {a.work + 6 * (size_t)n, a.work + 7 * (size_t)n};
+    double2* part[kRegions];
+    for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
+    long long hl = 0;
+
+    // r = M^{-1} b, shadow = r, x = 0; ||r||^2 and <shadow, r>
+    double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for_elems(n, G, [&](int i) {
+        const double2 ri = prec_apply(dinv, i, __ldg(b + i));
+        r[i] = ri;
+        sh[i] = ri;
+        x[i] = make_double2(0.0, 0.0);
+        if (!REF) { acc_norm(acc0[0], ri); acc_dot(acc0[1], ri, ri); }
+    });
+    double2 t0[2];
+    if (!reduce<REF, 2>(g, acc0, t0, part[0], n, [&](int i, double2* q) {
+            acc_norm(q[0], r[i]);
+            acc_dot(q[1], sh[i], r[i]);
+        })) {
+        write_report(a, 0, 0, 0, 0, 0, 0, 1);
+        return;
+    }
+    const double bnorm = sqrt(t0[0].x);
+    if (bnorm == 0.0) {  // krylov.cpp:70-74: converged, true_relres left at 0
+        write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0);
+        return;
+    }
+    const double brk = 1e-30 * bnorm * bnorm;
+    const double tol = a.tol;
+
+    double2 rho_new = t0[1];
+    double2 rho = make_double2(1, 0), alpha = make_double2(1, 0), omega = make_double2(1, 0);
+    double2 beta = make_double2(0, 0);
+    int conv = 0, brkc = 0, cur = 0;
+    long long iters = 0;
+    double final_relres = 0.0;
+    bool ok = true;
+
+    for (long long it = 1; it <= a.max_iter; ++it) {
+        if (cvk_abs(rho_new) < brk) { brkc = 1; iters = it - 1; break; }
+        const bool first = (it == 1);
+        if (!first) beta = cvk_mul(cvk_cdiv(rho_new, rho), cvk_cdiv(alpha, omega));
+        rho = rho_new;
+        const double2* pc = pv[cur];
+        const double2* vc = vv[cur];
+        double2* pn = pv[cur ^ 1];
+        double2* vn = vv[cur ^ 1];
+        const double2 nom = cvk_neg(omega);
+        // p = r + beta (p - omega v)  [axpy_inplace(-omega, v, p); xpay_inplace(beta, p, r)]
+        auto pnew = [&](int c) -> double2 {
+            const double2 rc = r[c];
+            if (first) return rc;
+            const double2 tmp = cvk_add(pc[c], cvk_mul(nom, vc[c]));
+            return cvk_add(cvk_mul(beta, tmp), rc);
+        };
+        // phase A: v = M^{-1} A p; gamma = <shadow, v>
+        double2 accA[1] = {make_double2(0, 0)};
+        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, lane, valid, pnew);
+            if (valid && lane == 0) {
+                const double2 vi = prec_apply(dinv, row, y);
+                pn[row] = pnew(row);
+                vn[row] = vi;
+                if (!REF) acc_dot(accA[0], sh[row], vi);
+            }
+        });
+        double2 gam[1];
+        ok = reduce<REF, 1>(g, accA, gam, part[1], n,
+                            [&](int i, double2* q) { acc_dot(q[0], sh[i], vn[i]); });
+        if (!ok) break;
+        if (cvk_abs(gam[0]) < brk) { brkc = 2; iters = it - 1; break; }
+        alpha = cvk_cdiv(rho, gam[0]);
+        const double2 nal = cvk_neg(alpha);
+        // s = r - alpha v (axpy copy), x += alpha p; t = M^{-1} A s
+        auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+        double2 accB[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, lane, valid, sval);
+            if (valid && lane == 0) {
+                const double2 ti = prec_apply(dinv, row, y);
+                const double2 si = sval(row);
+                s[row] = si;
+                t[row] = ti;
+                x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
+                if (!REF) { acc_norm(accB[0], si); acc_dot(accB[1], ti, ti); acc_dot(accB[2], ti, si); }
+            }
+        });
+        double2 tB[3];
+        ok = reduce<REF, 3>(g, accB, tB, part[2], n, [&](int i, double2* q) {
+            const double2 si = s[i], ti = t[i];
+            acc_norm(q[0], si);
+            acc_dot(q[1], ti, ti);
+            acc_dot(q[2], ti, si);
+        });
+        if (!ok) break;
+        double relres = sqrt(tB[0].x) / bnorm;
+        if (relres <= tol) {
+            conv = 1; iters = it; final_relres = relres;
+            hist_push(a, hl, relres);
+            break;
+        }
+        if (cvk_abs(tB[1]) < brk) { brkc = 3; iters = it; break; }
+        omega = cvk_cdiv(tB[2], tB[1]);
+        const double2 nom2 = cvk_neg(omega);
+        // x += omega s; r = s - omega t; ||r||^2, <shadow, r>
+        double2 accC[2] = {make_double2(0, 0), make_double2(0, 0)};
+        for_elems(n, G, [&](int i) {
+            const double2 si = s[i];
+            x[i] = cvk_add(x[i], cvk_mul(omega, si));
+            const double2 ri = cvk_add(si, cvk_mul(nom2, t[i]));
+            r[i] = ri;
+            if (!REF) { acc_norm(accC[0], ri); acc_dot(accC[1], sh[i], ri); }
+        });
+        double2 tC[2];
+        ok = reduce<REF, 2>(g, accC, tC, part[0], n, [&](int i, double2* q) {
+            acc_norm(q[0], r[i]);
+            acc_dot(q[1], sh[i], r[i]);
+        });
+        if (!ok) break;
+        relres = sqrt(tC[0].x) / bnorm;
+        final_relres = relres;
+        iters = it;
+        hist_push(a, hl, relres);
+        if (relres <= tol) { conv = 1; break; }
+        rho_new = tC[1];
+        cur ^= 1;
+    }
+    double trr = 0.0;
+    if (ok) ok = true_relres<S, REF>(g, a, s, part[1], trr);
+    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// =================================================================== tfQMR
+// work: r, shadow, w, u[2], au, v, d
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_tfqmr(KArgs a) {
+    GridBar g(a.bar, a.G);
+    const int n = a.A.n, G = a.G;
+    const double2* __restrict__ dinv = a.dinv;
+    const double2* __restrict__ b = a.b;
+    double2* x = a.x;
+    double2* r = a.work;
+    double2* sh = a.work + (size_t)n;
+    double2* w = a.work + 2 * (size_t)n;
+    double2* uu[2] = {a.work + 3 * (size_t)n, a.work + 4 * (size_t)n};
+    double2* au = a.work + 5 * (size_t)n;
+    double2* v = a.work + 6 * (size_t)n;
+    double2* d = a.work + 7 * (size_t)n;
+    double2* part[kRegions];
+    for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
+    long long hl = 0;
+    const double tol = a.tol;
+
+    double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for_elems(n, G, [&](int i) {
+        const double2 ri = prec_apply(dinv, i, __ldg(b + i));
+        r[i] = ri; sh[i] = ri; w[i] = ri; uu[0][i] = ri;
+        d[i] = make_double2(0, 0);
+        x[i] = make_double2(0, 0);
+        if (!REF) { acc_norm(acc0[0], ri); acc_dot(acc0[1], ri, ri); }
+    });
+    double2 t0[2];
+    if (!reduce<REF, 2>(g, acc0, t0, part[0], n, [&](int i, double2* q) {
+            acc_norm(q[0], r[i]);
+            acc_dot(q[1], sh[i], r[i]);
+        })) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+    const double bnorm = sqrt(t0[0].x);
+    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    const double brk = 1e-30 * bnorm * bnorm;
+    double2 rho = t0[1];
+    int cur = 0;
+    bool ok = true;
+
+    // au = M^{-1} A u; v = au; sigma = <shadow, v>
+    {
+        const double2* u0 = uu[0];
+        double2 acc[1] = {make_double2(0, 0)};
+        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, lane, valid, [&](int c) { return u0[c]; });
+            if (valid && lane == 0) {
+                const double2 ai = prec_apply(dinv, row, y);
+                au[row] = ai; v[row] = ai;
+                if (!REF) acc_dot(acc[0], sh[row], ai);
+            }
+        });
+        double2 tt[1];
+        ok = reduce<REF, 1>(g, acc, tt, part[1], n, [&](int i, double2* q) { acc_dot(q[0], sh[i], v[i]); });
+        if (!ok) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+        rho = t0[1];
+        // sigma carried into the loop
+        acc0[0] = tt[0];
+    }
+    double2 sigma = acc0[0];
+    double tau = bnorm, theta = 0.0;
+    double2 eta = make_double2(0, 0), alpha = make_double2(0, 0);
+    int conv = 0, brkc = 0;
+    long long iters = 0;
+    double final_relres = 0.0;
+    bool pending_x = false;  // x += eta d still owed
+    int region = 2;
+
+    for (long long hs = 0; hs < 2 * a.max_iter; hs += 2) {
+        // ---------------- even half-step
+        if (cvk_abs(sigma) < brk) { brkc = 6; break; }
+        alpha = cvk_cdiv(rho, sigma);
+        const double2 nal = cvk_neg(alpha);
+        {
+            const double2 coef = cvk_cdiv(cvk_scale(theta * theta, eta), alpha);
+            const double2* uc = uu[cur];
+            double2 acc[1] = {make_double2(0, 0)};
+            for_elems(n, G, [&](int i) {
+                const double2 wi = cvk_add(w[i], cvk_mul(nal, au[i]));
+                w[i] = wi;
+                d[i] = cvk_add(cvk_mul(coef, d[i]), uc[i]);
+                if (!REF) acc_norm(acc[0], wi);
+            });
+            double2 tt[1];
+            ok = reduce<REF, 1>(g, acc, tt, part[region], n, [&](int i, double2* q) { acc_norm(q[0], w[i]); });
+            region = (region + 1) % kRegions;
+            if (!ok) break;
+            theta = sqrt(tt[0].x) / tau;
+            const double c = 1.0 / sqrt(1.0 + theta * theta);
+            tau = tau * theta * c;
+            eta = cvk_scale(c * c, alpha);
+            pending_x = true;
+            const double relres = tau * sqrt((double)(hs + 2)) / bnorm;
+            final_relres = relres;
+            iters = hs / 2 + 1;
+            if (relres <= tol) { conv = 1; break; }
+        }
+        // ---------------- even tail + odd head:
+        // u' = u - alpha v; au = M^{-1} A u'; x += eta d; w -= alpha au; d = coef d + u'
+        const double2 eta_e = eta;
+        const double2 coef_o = cvk_cdiv(cvk_scale(theta * theta, eta), alpha);
+        {
+            const double2* uc = uu[cur];
+            double2* un = uu[cur ^ 1];
+            auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, v[c])); };
+            double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+            for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                const double2 y = row_sum<S>(a.A, row, lane, valid, uval);
+                if (valid && lane == 0) {
+                    const double2 ui = uval(row);
+                    const double2 ai = prec_apply(dinv, row, y);
+                    un[row] = ui;
+                    au[row] = ai;
+                    const double2 di = d[row];
+                    x[row] = cvk_add(x[row], cvk_mul(eta_e, di));
+                    const double2 wi = cvk_add(w[row], cvk_mul(nal, ai));
+                    w[row] = wi;
+                    d[row] = cvk_add(cvk_mul(coef_o, di), ui);
+                    if (!REF) { acc_norm(acc[0], wi); acc_dot(acc[1], sh[row], wi); }
+                }
+            });
+            double2 tt[2];
+            ok = reduce<REF, 2>(g, acc, tt, part[region], n, [&](int i, double2* q) {
+                acc_norm(q[0], w[i]);
+                acc_dot(q[1], sh[i], w[i]);
+            });
+            region = (region + 1) % kRegions;
+            if (!ok) break;
+            cur ^= 1;
+            // odd half-step scalars
+            theta = sqrt(tt[0].x) / tau;
+            const double c = 1.0 / sqrt(1.0 + theta * theta);
+            tau = tau * theta * c;
+            eta = cvk_scale(c * c, alpha);
+            pending_x = true;
+            const double relres = tau * sqrt((double)(hs + 1 + 2)) / bnorm;
+            final_relres = relres;
+            iters = (hs + 1) / 2 + 1;
+            hist_push(a, hl, relres);
+            if (relres <= tol) { conv = 1; break; }
+            const double2 rho_new = tt[1];
+            if (cvk_abs(rho) < brk) { brkc = 1; break; }
+            const double2 beta = cvk_cdiv(rho_new, rho);
+            rho = rho_new;
+            // u_next = w + beta u; au_next = M^{-1} A u_next; v = beta(beta v + au) + au_next;
+            // x += eta d; sigma = <shadow, v>
+            const double2 eta_o = eta;
+            const double2* uc2 = uu[cur];
+            double2* un2 = uu[cur ^ 1];
+            auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc2[c])); };
+            double2 accO[1] = {make_double2(0, 0)};
+            for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                const double2 y = row_sum<S>(a.A, row, lane, valid, unext);
+                if (valid && lane == 0) {
+                    const double2 un_i = unext(row);
+                    const double2 an = prec_apply(dinv, row, y);
+                    un2[row] = un_i;
+                    double2 vi = cvk_add(cvk_mul(beta, v[row]), au[row]);
+                    vi = cvk_add(cvk_mul(beta, vi), an);
+                    v[row] = vi;
+                    au[row] = an;
+                    x[row] = cvk_add(x[row], cvk_mul(eta_o, d[row]));
+                    if (!REF) acc_dot(accO[0], sh[row], vi);
+                }
+            });
+            double2 to[1];
+            ok = reduce<REF, 1>(g, accO, to, part[region], n, [&](int i, double2* q) { acc_dot(q[0], sh[i], v[i]); });
+            region = (region + 1) % kRegions;
+            if (!ok) break;
+            pending_x = false;
+            cur ^= 1;
+            sigma = to[0];
+        }
+    }
+    if (ok && pending_x) {  // the owed x += eta d (krylov.cpp:335)
+        const double2 e = eta;
+        for_elems(n, G, [&](int i) { x[i] = cvk_add(x[i], cvk_mul(e, d[i])); });
+        ok = g.sync();
+    }
+    double trr = 0.0;
+    if (ok) ok = true_relres<S, REF>(g, a, r, part[region], trr);
+    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// ============================================================ BiCGSTAB(l)
+// work: shadow, x-scratch?, then r[0..l], u[0..l], spareR, spareU  (2l+5 vectors)
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_bicgstab_l(KArgs a) {
+    GridBar g(a.bar, a.G);
+    const int n = a.A.n, G = a.G, L = a.l;
+    const double2* __restrict__ dinv = a.dinv;
+    const double2* __restrict__ b = a.b;
+    double2* x = a.x;
+    double2* sh = a.work;
+    double2* scratch = a.work + (size_t)n;
+    double2* vbase = a.work + 2 * (size_t)n;
+    // logical -> physical vector slots: r_i = vbase[ri[i]], u_i = vbase[ui[i]]
+    __shared__ int ri[kMaxL + 2], ui[kMaxL + 2];
+    __shared__ double2 tau_s[kMaxL * kMaxL], sig_s[kMaxL], gam_s[kMaxL], gp_s[kMaxL], gpp_s[kMaxL];
+    if (threadIdx.x <= L) { ri[threadIdx.x] = threadIdx.x; ui[threadIdx.x] = L + 1 + threadIdx.x; }
+    if (threadIdx.x == 0) { ri[L + 1] = 2 * L + 2; ui[L + 1] = 2 * L + 3; }
+    __syncthreads();
+    auto R = [&](int i) -> double2* { return vbase + (size_t)ri[i] * n; };
+    auto U = [&](int i) -> double2* { return vbase + (size_t)ui[i] * n; };
+    double2* part[kRegions];
+    for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
+    int region = 0;
+    auto next_part = [&]() { double2* p = part[region]; region = (region + 1) % kRegions; return p; };
+    long long hl = 0;
+    const double tol = a.tol;
+
+    double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
+    {
+        double2* r0 = R(0);
+        for_elems(n, G, [&](int i) {
+            const double2 v0 = prec_apply(dinv, i, __ldg(b + i));
+            r0[i] = v0; sh[i] = v0;
+            x[i] = make_double2(0, 0);
+            for (int j = 1; j <= L; ++j) R(j)[i] = make_double2(0, 0);
+            for (int j = 0; j <= L; ++j) U(j)[i] = make_double2(0, 0);
+            if (!REF) { acc_norm(acc0[0], v0); acc_dot(acc0[1], v0, v0); }
+        });
+    }
+    double2 t0[2];
+    {
+        double2* r0 = R(0);
+        if (!reduce<REF, 2>(g, acc0, t0, next_part(), n, [&](int i, double2* q) {
+                acc_norm(q[0], r0[i]);
+                acc_dot(q[1], sh[i], r0[i]);
+            })) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+    }
+    const double bnorm = sqrt(t0[0].x);
+    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    const double brk = 1e-30 * bnorm * bnorm;
+    double2 rho_old = make_double2(1, 0), alpha = make_double2(0, 0), omega = make_double2(1, 0);
+    double2 rho_next = t0[1];  // <shadow, r_j> for the coming BiCG step
+    int conv = 0, brkc = 0;
+    long long iters = 0;
+    double final_relres = 0.0;
+    bool ok = true;
+
+    for (long long cycle = 1; cycle <= a.max_iter; ++cycle) {
+        rho_old = cvk_mul(cvk_neg(omega), rho_old);
+        bool broke = false;
+        double r0norm = 0.0;
+        for (int j = 0; j < L; ++j) {
+            const double2 rho = rho_next;
+            if (cvk_abs(rho_old) < brk) { brkc = 1; broke = true; break; }
+            const double2 beta = cvk_cdiv(cvk_mul(alpha, rho), rho_old);
+            rho_old = rho;
+            const double2 nbeta = cvk_neg(beta);
+            // u_i = r_i - beta u_i (i <= j); u_{j+1} = M^{-1} A u_j; g = <shadow, u_{j+1}>
+            {
+                const double2* uj_old = U(j);
+                const double2* rj = R(j);
+                double2* uj_new = vbase + (size_t)ui[L + 1] * n;  // spare
+                double2* uj1 = U(j + 1);
+                auto ujv = [&](int c) -> double2 { return cvk_add(cvk_mul(nbeta, uj_old[c]), rj[c]); };
+                double2 acc[1] = {make_double2(0, 0)};
+                for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                    const double2 y = row_sum<S>(a.A, row, lane, valid, ujv);
+                    if (valid && lane == 0) {
+                        const double2 yi = prec_apply(dinv, row, y);
+                        uj_new[row] = ujv(row);
+                        uj1[row] = yi;
+                        if (!REF) acc_dot(acc[0], sh[row], yi);
+                    }
+                });
+                // the other u_i (i < j) in element mapping
+                __syncthreads();
+                for_elems(n, G, [&](int i) {
+                    for (int q = 0; q < j; ++q) {
+                        double2* uq = U(q);
+                        uq[i] = cvk_add(cvk_mul(nbeta, uq[i]), R(q)[i]);
+                    }
+                });
+                double2 tg[1];
+                ok = reduce<REF, 1>(g, acc, tg, next_part(), n, [&](int i, double2* q) { acc_dot(q[0], sh[i], uj1[i]); });
+                if (!ok) break;
+                // swap u_j with the spare slot (uniform in every CTA)
+                if (threadIdx.x == 0) { const int tmp = ui[j]; ui[j] = ui[L + 1]; ui[L + 1] = tmp; }
+                __syncthreads();
+                if (cvk_abs(tg[0]) < brk) { brkc = 4; broke = true; break; }
+                alpha = cvk_cdiv(rho_old, tg[0]);
+            }
+            // r_i -= alpha u_{i+1} (i <= j); r_{j+1} = M^{-1} A r_j; x += alpha u_0
+            {
+                const double2 nal = cvk_neg(alpha);
+                const double2* rj_old = R(j);
+                const double2* uj1 = U(j + 1);
+                double2* rj_new = vbase + (size_t)ri[L + 1] * n;
+                double2* rj1 = R(j + 1);
+                auto rjv = [&](int c) -> double2 { return cvk_add(rj_old[c], cvk_mul(nal, uj1[c])); };
+                double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+                for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                    const double2 y = row_sum<S>(a.A, row, lane, valid, rjv);
+                    if (valid && lane == 0) {
+                        const double2 yi = prec_apply(dinv, row, y);
+                        rj_new[row] = rjv(row);
+                        rj1[row] = yi;
+                    }
+                });
+                __syncthreads();
+                const double2* u0 = U(0);
+                for_elems(n, G, [&](int i) {
+                    for (int q = 0; q < j; ++q) {
+                        double2* rq = R(q);
+                        rq[i] = cvk_add(rq[i], cvk_mul(nal, U(q + 1)[i]));
+                    }
+                    x[i] = cvk_add(x[i], cvk_mul(alpha, u0[i]));
+                    if (!REF) {
+                        const double2 r0i = (j == 0) ? rj_new[i] : R(0)[i];
+                        acc_norm(acc[0], r0i);
+                        acc_dot(acc[1], sh[i], rj1[i]);
+                    }
+                });
+                double2 tr[2];
+                ok = reduce<REF, 2>(g, acc, tr, next_part(), n, [&](int i, double2* q) {
+                    acc_norm(q[0], (j == 0) ? rj_new[i] : R(0)[i]);
+                    acc_dot(q[1], sh[i], rj1[i]);
+                });
+                if (!ok) break;
+                if (threadIdx.x == 0) { const int tmp = ri[j]; ri[j] = ri[L + 1]; ri[L + 1] = tmp; }
+                __syncthreads();
+                r0norm = sqrt(tr[0].x);
+                rho_next = tr[1];
+                if (r0norm <= tol * bnorm) { broke = true; break; }
+            }
+        }
+        if (!ok) break;
+        if (broke) {
+            // krylov.cpp:208-222 (needs ||r_0|| of the current r_0)
+            double2 tn[1];
+            double2 accn[1] = {make_double2(0, 0)};
+            double2* r0 = R(0);
+            for_elems(n, G, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
+            ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
+            if (!ok) break;
+            const double relres = sqrt(tn[0].x) / bnorm;
+            final_relres = relres;
+            if (relres <= tol) {
+                conv = 1; brkc = 0; iters = cycle;
+                hist_push(a, hl, relres);
+            } else {
+                iters = cycle - 1;
+            }
+            break;
+        }
+        // ---- minimal residual part: MGS on r_1..r_L (krylov.cpp:224-238)
+        bool mrbroke = false;
+        for (int j = 0; j < L && !mrbroke; ++j) {
+            double2* rj1 = R(j + 1);
+            for (int i = 0; i <= j; ++i) {
+                // apply the pending update r_{j+1} -= tau_{i-1,j} r_i, then
+                // the next dot: <r_{i+1}, r_{j+1}> (i < j) or sigma_j, <r_{j+1}, r_0> (i == j)
+                const bool has_upd = (i > 0);
+                const double2 ntau = has_upd ? cvk_neg(tau_s[(i - 1) * L + j]) : make_double2(0, 0);
+                const double2* rprev = has_upd ? R(i) : nullptr;
+                const double2* ri1 = R(i + 1);
+                const double2* r0 = R(0);
+                const bool last = (i == j);
+                double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+                for_elems(n, G, [&](int e) {
+                    double2 v = rj1[e];
+                    if (has_upd) { v = cvk_add(v, cvk_mul(ntau, rprev[e])); rj1[e] = v; }
+                    if (!REF) {
+                        if (!last) acc_dot(acc[0], ri1[e], v);
+                        else { acc_dot(acc[0], v, v); acc_dot(acc[1], v, r0[e]); }
+                    }
+                });
+                double2 tt[2];
+                ok = reduce<REF, 2>(g, acc, tt, next_part(), n, [&](int e, double2* q) {
+                    if (!last) acc_dot(q[0], ri1[e], rj1[e]);
+                    else { acc_dot(q[0], rj1[e], rj1[e]); acc_dot(q[1], rj1[e], r0[e]); }
+                });
+                if (!ok) break;
+                if (!last) {
+                    if (threadIdx.x == 0) tau_s[i * L + j] = cvk_cdiv(tt[0], sig_s[i]);
+                    __syncthreads();
+                } else {
+                    if (cvk_abs(tt[0]) < brk) { brkc = 5; mrbroke = true; break; }
+                    if (threadIdx.x == 0) { sig_s[j] = tt[0]; gp_s[j] = cvk_cdiv(tt[1], tt[0]); }
+                    __syncthreads();
+                }
+            }
+            if (!ok) break;
+        }
+        if (!ok) break;
+        if (mrbroke) {
+            double2 tn[1];
+            double2 accn[1] = {make_double2(0, 0)};
+            double2* r0 = R(0);
+            for_elems(n, G, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
+            ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
+            if (!ok) break;
+            const double relres = sqrt(tn[0].x) / bnorm;
+            final_relres = relres;
+            iters = cycle;
+            if (relres <= tol) { conv = 1; brkc = 0; hist_push(a, hl, relres); }
+            break;
+        }
+        // gamma, gamma', gamma'' (krylov.cpp:251-262) -- thread 0, then shared
+        if (threadIdx.x == 0) {
+            gam_s[L - 1] = gp_s[L - 1];
+            for (int jj = L - 1; jj-- > 0;) {
+                double2 gj = gp_s[jj];
+                for (int i = jj + 1; i < L; ++i) gj = cvk_sub(gj, cvk_mul(tau_s[jj * L + i], gam_s[i]));
+                gam_s[jj] = gj;
+            }
+            for (int j = 0; j + 1 < L; ++j) {
+                double2 gj = gam_s[j + 1];
+                for (int i = j + 1; i + 1 < L; ++i) gj = cvk_add(gj, cvk_mul(tau_s[j * L + i], gam_s[i + 1]));
+                gpp_s[j] = gj;
+            }
+        }
+        __syncthreads();
+        omega = gam_s[L - 1];
+        // updates (krylov.cpp:264-271), per element in the reference's order
+        double2 accU[2] = {make_double2(0, 0), make_double2(0, 0)};
+        {
+            double2* r0 = R(0);
+            double2* u0 = U(0);
+            for_elems(n, G, [&](int i) {
+                double2 xi = x[i], r0i = r0[i], u0i = u0[i];
+                xi = cvk_add(xi, cvk_mul(gam_s[0], r0i));
+                r0i = cvk_add(r0i, cvk_mul(cvk_neg(gp_s[L - 1]), R(L)[i]));
+                u0i = cvk_add(u0i, cvk_mul(cvk_neg(gam_s[L - 1]), U(L)[i]));
+                for (int j = 1; j < L; ++j) {
+                    const double2 rj = R(j)[i];
+                    u0i = cvk_add(u0i, cvk_mul(cvk_neg(gam_s[j - 1]), U(j)[i]));
+                    xi = cvk_add(xi, cvk_mul(gpp_s[j - 1], rj));
+                    r0i = cvk_add(r0i, cvk_mul(cvk_neg(gp_s[j - 1]), rj));
+                }
+                x[i] = xi; r0[i] = r0i; u0[i] = u0i;
+                if (!REF) { acc_norm(accU[0], r0i); acc_dot(accU[1], sh[i], r0i); }
+            });
+            double2 tu[2];
+            ok = reduce<REF, 2>(g, accU, tu, next_part(), n, [&](int i, double2* q) {
+                acc_norm(q[0], r0[i]);
+                acc_dot(q[1], sh[i], r0[i]);
+            });
+            if (!ok) break;
+            const double relres = sqrt(tu[0].x) / bnorm;
+            final_relres = relres;
+            iters = cycle;
+            hist_push(a, hl, relres);
+            rho_next = tu[1];
+            if (relres <= tol) { conv = 1; break; }
+        }
+    }
+    double trr = 0.0;
+    if (ok) ok = true_relres<S, REF>(g, a, scratch, next_part(), trr);
+    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// ================================================================ GMRES(m)
+// Beyond reference: left-preconditioned restarted GMRES with CGS2 Arnoldi
+// and complex Givens rotations, order of operations = orc_gmres.
+// work: r, W[2], V[0..m]   (m + 4 vectors)
+// dynamic shared: H[(m+1) m], sn[m], g[m+1], y[m], h1[m+1], h2[m+1] (double2), cs[m] (double)
+template <int S, bool REF>
+__global__ void __launch_bounds__(kThreads) k_gmres(KArgs a) {
+    GridBar g(a.bar, a.G);
+    const int n = a.A.n, G = a.G, M = a.m;
+    const double2* __restrict__ dinv = a.dinv;
+    const double2* __restrict__ b = a.b;
+    double2* x = a.x;
+    double2* r = a.work;
+    double2* Wb[2] = {a.work + (size_t)n, a.work + 2 * (size_t)n};
+    double2* V = a.work + 3 * (size_t)n;
+    extern __shared__ double2 dsm[];
+    double2* H = dsm;
+    double2* sn = H + (size_t)(M + 1) * M;
+    double2* gv = sn + M;
+    double2* yv = gv + M + 1;
+    double2* h1 = yv + M;
+    double2* h2 = h1 + M + 1;
+    double* cs = (double*)(h2 + M + 1);
+    __shared__ double2 wsum[kWarps];
+    __shared__ double2 hsm[kMaxSlots][kWarps];
+    double2* part[kRegions];
+    for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
+    int region = 0;
+    auto next_part = [&]() { double2* p = part[region]; region = (region + 1) % kRegions; return p; };
+    long long hl = 0;
+    const double tol = a.tol;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // FAST: cnt dots <V_k, w> for k < cnt over the CTA's rows -> partials
+    auto multi_dot = [&](const double2* wv, int cnt, double2* pr) {
+        for (int k = 0; k < cnt; ++k) {
+            const double2* vk = V + (size_t)k * n;
+            double2 s = make_double2(0, 0);
+            for_elems(n, G, [&](int i) { acc_dot(s, vk[i], wv[i]); });
+            s = warp_sum(s);
+            if (lane == 0) hsm[k][warp] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            double2 s = hsm[threadIdx.x][0];
+            for (int w2 = 1; w2 < kWarps; ++w2) s = cvk_add(s, hsm[threadIdx.x][w2]);
+            pr[threadIdx.x * G + blockIdx.x] = s;
+        }
+    };
+    auto fold_multi = [&](const double2* pr, int cnt, double2* out) {
+        if (threadIdx.x < 32) {
+            for (int k = 0; k < cnt; ++k) {
+                double2 s = make_double2(0, 0);
+                for (int bb = lane; bb < G; bb += 32) s = cvk_add(s, __ldcg(pr + k * G + bb));
+                s = warp_sum(s);
+                if (lane == 0) out[k] = s;
+            }
+        }
+        __syncthreads();
+    };
+    auto seq_multi = [&](const double2* wv, int cnt, double2* out) {
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < cnt; ++k) {
+                const double2* vk = V + (size_t)k * n;
+                double2 s = make_double2(0, 0);
+                for (int i = 0; i < n; ++i) acc_dot(s, vk[i], wv[i]);
+                out[k] = s;
+            }
+        }
+        __syncthreads();
+    };
+
+    // r = M^{-1} b, x = 0, ||r||
+    double2 acc0[1] = {make_double2(0, 0)};
+    for_elems(n, G, [&](int i) {
+        const double2 ri = prec_apply(dinv, i, __ldg(b + i));
+        r[i] = ri;
+        x[i] = make_double2(0, 0);
+        if (!REF) acc_norm(acc0[0], ri);
+    });
+    double2 t0[1];
+    if (!reduce<REF, 1>(g, acc0, t0, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r[i]); })) {
+        write_report(a, 0, 0, 0, 0, 0, 0, 1);
+        return;
+    }
+    const double bnorm = sqrt(t0[0].x);
+    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    const double brk = 1e-30 * bnorm * bnorm;
+    double beta = bnorm;
+    long long total = 0;
+    int conv = 0, brkc = 0;
+    double final_relres = 0.0;
+    bool ok = true;
+    int wcur = 0;
+
+    for (;;) {
+        if (total > 0) {
+            final_relres = beta / bnorm;
+            if (final_relres <= tol) { conv = 1; break; }
+        }
+        if (threadIdx.x == 0) {
+            for (int i = 0; i <= M; ++i) gv[i] = make_double2(0, 0);
+            gv[0] = make_double2(beta, 0.0);
+        }
+        __syncthreads();
+        const double2* src = r;
+        double scale = beta;
+        int k = 0;
+        bool stop = false;
+        for (int j = 0; j < M; ++j) {
+            ++total;
+            // ---- S: V_j = src / scale; w = M^{-1} A V_j; h1 = V^H w
+            double2* Vj = V + (size_t)j * n;
+            double2* w = Wb[wcur];
+            {
+                const double2* sp = src;
+                const double sc = scale;
+                auto vat = [&](int c) -> double2 { return cvk_divr(sp[c], sc); };
+                for_rows<S>(n, G, [&](int row, int ln, bool valid) {
+                    const double2 y = row_sum<S>(a.A, row, ln, valid, vat);
+                    if (valid && ln == 0) {
+                        Vj[row] = vat(row);
+                        w[row] = prec_apply(dinv, row, y);
+                    }
+                });
+                __syncthreads();
+                double2* pr = next_part();
+                if (REF) {
+                    ok = g.sync();
+                    if (!ok) break;
+                    seq_multi(w, j + 1, h1);
+                } else {
+                    multi_dot(w, j + 1, pr);
+                    ok = g.sync();
+                    if (!ok) break;
+                    fold_multi(pr, j + 1, h1);
+                }
+            }
+            // ---- R1: w -= V h1; h2 = V^H w
+            {
+                for_elems(n, G, [&](int i) {
+                    double2 wi = w[i];
+                    for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h1[q]), V[(size_t)q * n + i]));
+                    w[i] = wi;
+                });
+                double2* pr = next_part();
+                if (REF) {
+                    ok = g.sync();
+                    if (!ok) break;
+                    seq_multi(w, j + 1, h2);
+                } else {
+                    multi_dot(w, j + 1, pr);
+                    ok = g.sync();
+                    if (!ok) break;
+                    fold_multi(pr, j + 1, h2);
+                }
+            }
+            // ---- R2: w -= V h2; ||w||
+            double hn;
+            {
+                double2 acc[1] = {make_double2(0, 0)};
+                for_elems(n, G, [&](int i) {
+                    double2 wi = w[i];
+                    for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h2[q]), V[(size_t)q * n + i]));
+                    w[i] = wi;
+                    if (!REF) acc_norm(acc[0], wi);
+                });
+                double2 tn[1];
+                ok = reduce<REF, 1>(g, acc, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], w[i]); });
+                if (!ok) break;
+                hn = sqrt(tn[0].x);
+            }
+            // ---- Hessenberg column, rotations, residual estimate (thread 0)
+            if (threadIdx.x == 0) {
+                for (int i = 0; i <= j; ++i) H[i * M + j] = cvk_add(h1[i], h2[i]);
+                for (int i = 0; i < j; ++i) {
+                    const double2 a0 = H[i * M + j], c2 = H[(i + 1) * M + j];
+                    H[i * M + j] = cvk_add(cvk_scale(cs[i], a0), cvk_mul(sn[i], c2));
+                    H[(i + 1) * M + j] = cvk_add(cvk_mul(cvk_neg(cvk_conj(sn[i])), a0), cvk_scale(cs[i], c2));
+                }
+                const double2 aj = H[j * M + j];
+                const double aa = sqrt(aj.x * aj.x + aj.y * aj.y);
+                const double nu = sqrt(aa * aa + hn * hn);
+                if (aa == 0.0) {
+                    cs[j] = 0.0; sn[j] = make_double2(1.0, 0.0); H[j * M + j] = make_double2(hn, 0.0);
+                } else {
+                    cs[j] = aa / nu;
+                    sn[j] = cvk_scale(hn / nu, cvk_divr(aj, aa));
+                    H[j * M + j] = cvk_scale(nu, cvk_divr(aj, aa));
+                }
+                gv[j + 1] = cvk_mul(cvk_neg(cvk_conj(sn[j])), gv[j]);
+                gv[j] = cvk_scale(cs[j], gv[j]);
+            }
+            __syncthreads();
+            const double2 gj1 = gv[j + 1];
+            const double relres = sqrt(gj1.x * gj1.x + gj1.y * gj1.y) / bnorm;
+            final_relres = relres;
+            hist_push(a, hl, relres);
+            k = j + 1;
+            if (relres <= tol) { conv = 1; stop = true; break; }
+            if (hn * hn < brk) { brkc = 7; stop = true; break; }
+            if (total >= a.max_iter) { stop = true; break; }
+            src = w;
+            scale = hn;
+            wcur ^= 1;
+        }
+        if (!ok) break;
+        // back substitution (thread 0), then x += V y
+        if (threadIdx.x == 0) {
+            for (int i = k; i-- > 0;) {
+                double2 s = gv[i];
+                for (int q = i + 1; q < k; ++q) s = cvk_sub(s, cvk_mul(H[i * M + q], yv[q]));
+                yv[i] = cvk_cdiv(s, H[i * M + i]);
+            }
+        }
+        __syncthreads();
+        for_elems(n, G, [&](int i) {
+            double2 xi = x[i];
+            for (int q = 0; q < k; ++q) xi = cvk_add(xi, cvk_mul(yv[q], V[(size_t)q * n + i]));
+            x[i] = xi;
+        });
+        if (brkc == 7 && final_relres <= tol) { conv = 1; brkc = 0; }
+        ok = g.sync();
+        if (!ok || stop) break;
+        // restart residual r = M^{-1}(b - A x)
+        double2 acc[1] = {make_double2(0, 0)};
+        for_rows<S>(n, G, [&](int row, int ln, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, ln, valid, [&](int c) { return x[c]; });
+            if (valid && ln == 0) {
+                const double2 ri = prec_apply(dinv, row, cvk_sub(__ldg(b + row), y));
+                r[row] = ri;
+                if (!REF) acc_norm(acc[0], ri);
+            }
+        });
+        double2 tn[1];
+        ok = reduce<REF, 1>(g, acc, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r[i]); });
+        if (!ok) break;
+        beta = sqrt(tn[0].x);
+        if (beta == 0.0) { conv = 1; final_relres = 0.0; break; }
+    }
+    (void)wsum;
+    double trr = 0.0;
+    if (ok) ok = true_relres<S, REF>(g, a, Wb[0], next_part(), trr);
+    write_report(a, conv, brkc, total, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// ----------------------------------------------------------- dispatch --
+
+template <int S, bool REF>
+static const void* pick(int solver) {
+    switch (solver) {
+        case 0: return (const void*)k_bicgstab<S, REF>;
+        case 1: return (const void*)k_bicgstab_l<S, REF>;
+        case 2: return (const void*)k_tfqmr<S, REF>;
+        case 3: return (const void*)k_gmres<S, REF>;
+    }
+    return nullptr;
+}
+
+const void* solver_kernel(int solver, int S, bool ref) {
+    if (ref) return pick<1, true>(solver);
+    switch (S) {
+        case 1: return pick<1, false>(solver);
+        case 2: return pick<2, false>(solver);
+        case 4: return pick<4, false>(solver);
+        case 8: return pick<8, false>(solver);
+        case 16: return pick<16, false>(solver);
+    }
+    return nullptr;
+}
+
+int solver_nwork(int solver, int l, int m) {
+    switch (solver) {
+        case 0: return 8;
+        case 1: return 2 * l + 6;
+        case 2: return 8;
+        case 3: return m + 4;
+    }
+    return 0;
+}
+
+size_t solver_smem(int solver, int m) {
+    if (solver != 3) return 0;
+    return sizeof(double2) * ((size_t)(m + 1) * m + m + (m + 1) + m + 2 * (m + 1)) + sizeof(double) * m;
+}
+
+}  // namespace cvk

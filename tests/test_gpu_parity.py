@@ -1,0 +1,247 @@
+"""Device parity: the CUDA path (through the C ABI) against the oracle.
+
+REF mode (ExecMode.Sequential) must be BITWISE identical to the reference's
+CPU arithmetic; FAST mode (the product default) within the tolerances the
+reference's own tests use (test_numkit.cpp: 1e-13 relative for kernels) and,
+for solves, the SURVEY.md 8(c) contract: same convergence, solution rel-L2
+<= 1e-10 against the reference solved at tol 1e-12, iteration bands.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SOLVERS = ("bicgstab", "bicgstab_l", "tfqmr", "gmres")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.complex128).view(np.uint64)
+
+
+def mat(P, rp, ci, v):
+    n = len(rp) - 1
+    return P.CsrMatrix(n, n, rp, ci, v)
+
+
+def rand_csr(O, n, nnz, rng):
+    rows = rng.integers(0, n, nnz)
+    cols = rng.integers(0, n, nnz)
+    vals = rng.uniform(-1, 1, nnz) + 1j * rng.uniform(-1, 1, nnz)
+    # keep a nonzero diagonal so jacobi is defined
+    rows = np.concatenate([rows, np.arange(n)])
+    cols = np.concatenate([cols, np.arange(n)])
+    vals = np.concatenate([vals, 4.0 + rng.uniform(-1, 1, n) + 1j])
+    return O.csr_from_triplets(rows, cols, vals, n, n)
+
+
+def cavity(O, h, f=13.0, adm=0j, roof=None):
+    g = O.build_grid(2.4, 1.2, h, 0.4, 0.65, adm)
+    d = np.full(g.roof_size, 1.0 + 0j) if roof is None else roof(g.roof_size)
+    return O.assemble(g, 2 * math.pi * f, 340.0, d)
+
+
+def test_spmv_ref_bitwise_and_fast_close(cvk, oracle, golden):
+    P = cvk
+    rng = np.random.default_rng(42)
+    cases = [(golden["rp"], golden["ci"], golden["v"])]
+    for n in (5, 20, 257, 1000, 4099):
+        cases.append(rand_csr(oracle, n, 8 * n, rng))
+    for rp, ci, v in cases:
+        n = len(rp) - 1
+        x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        want = oracle.spmv(rp, ci, v, x)
+        A = mat(P, rp, ci, v)
+        got_ref = P.spmv(A, x, mode=P.ExecMode.Sequential)
+        assert np.array_equal(bits(got_ref), bits(want))
+        got = P.spmv(A, x, mode=P.ExecMode.Parallel)
+        assert np.all(np.abs(got - want) <= 1e-13 * (1.0 + np.abs(want)))
+
+
+@pytest.mark.parametrize("group", [1, 2, 4, 8, 16])
+def test_spmv_every_group_width(cvk, oracle, monkeypatch, group):
+    monkeypatch.setenv("CVK_SPMV_GROUP", str(group))
+    P = cvk
+    rng = np.random.default_rng(group)
+    rp, ci, v = rand_csr(oracle, 3001, 3001 * 14, rng)
+    x = rng.uniform(-1, 1, 3001) + 1j * rng.uniform(-1, 1, 3001)
+    A = mat(P, rp, ci, v)  # group is chosen at upload
+    got = P.spmv(A, x)
+    want = oracle.spmv(rp, ci, v, x)
+    assert np.all(np.abs(got - want) <= 1e-13 * (1.0 + np.abs(want)))
+
+
+def test_dot_norm_axpy(cvk, oracle):
+    P = cvk
+    rng = np.random.default_rng(20240817)
+    for n in (0, 1, 11, 1000, 100003):
+        x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        y = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        want = oracle.dot(x, y)
+        assert P.dot_hermitian(x, y, mode=P.ExecMode.Sequential) == want
+        got = P.dot_hermitian(x, y, mode=P.ExecMode.Parallel)
+        assert abs(got - want) <= 1e-13 * max(1.0, np.abs(x).dot(np.abs(y)))
+        assert P.norm2(x, mode=P.ExecMode.Sequential) == oracle.norm2(x)
+        assert abs(P.norm2(x) - oracle.norm2(x)) <= 1e-14 * max(1.0, oracle.norm2(x))
+        alpha = complex(rng.uniform(-1, 1), rng.uniform(-1, 1))
+        y2 = y.copy()
+        P.axpy_inplace(alpha, x, y2)
+        a, b = alpha.real, alpha.imag
+        ax = (a * x.real - b * x.imag) + 1j * (a * x.imag + b * x.real)
+        assert np.array_equal(bits(y2), bits((y.real + ax.real) + 1j * (y.imag + ax.imag)))
+    assert P.dot_hermitian([1 + 1j, 2], [1 + 1j, 2]) == 6.0
+
+
+def test_jacobi_device_bitwise(cvk, oracle, golden):
+    P = cvk
+    A = mat(P, golden["rp"], golden["ci"], golden["v"])
+    M = P.jacobi(A)
+    want = oracle.jacobi(golden["rp"], golden["ci"], golden["v"])
+    assert np.array_equal(bits(M.inv_diag), bits(want))
+    sing = P.csr_from_triplets([0, 1], [0, 0], [1.0, 1.0], 2, 2)
+    with pytest.raises(P.InvalidArgument, match="row 1"):
+        P.jacobi(sing)
+
+
+def test_golden_ref_mode_reproduces_reference(cvk, oracle, golden):
+    """The reference's recorded run, bit for bit, on the device."""
+    P = cvk
+    A = mat(P, golden["rp"], golden["ci"], golden["v"])
+    r = P.bicgstab(A, golden["b"], P.jacobi(A), P.SolverOptions(), mode=P.ExecMode.Sequential)
+    assert r.report.converged and r.report.iterations == 246
+    assert "%.17g" % r.report.final_relres == "8.9265369265007959e-10"
+    assert "%.17g" % r.report.true_relres == "8.5608367217167752e-10"
+    assert oracle.format_vector_csv(r.x) == golden["solution_csv"]
+
+
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_ref_mode_bitwise_all_solvers(cvk, oracle, golden, solver):
+    P = cvk
+    A = mat(P, golden["rp"], golden["ci"], golden["v"])
+    opts = P.SolverOptions(record_history=True, max_iter=400 if solver == "gmres" else 10000)
+    r = P.solve(P.solver_from_name(solver), A, golden["b"], P.jacobi(A), opts, mode=P.ExecMode.Sequential)
+    xo, ro = oracle.solve(solver, golden["rp"], golden["ci"], golden["v"], golden["b"],
+                          record_history=True, max_iter=opts.max_iter)
+    assert (r.report.iterations, r.report.converged) == (ro.iterations, ro.converged)
+    assert r.report.residual_history == ro.residual_history
+    assert np.array_equal(bits(r.x), bits(xo))
+    assert r.report.final_relres == ro.final_relres and r.report.true_relres == ro.true_relres
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "bicgstab_l", "tfqmr"])
+def test_fast_mode_matches_reference_solution(cvk, oracle, golden, solver):
+    """Contract of SURVEY.md 8(c): converged, relres <= tol, solution rel-L2
+    <= 1e-10 vs the reference at tol 1e-12, iterations in band."""
+    P = cvk
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    x_tight, _ = oracle.solve(solver, rp, ci, v, b, tol=1e-12)
+    r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-12))
+    assert r.report.converged and r.report.final_relres <= 1e-12
+    assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
+    _, ro = oracle.solve(solver, rp, ci, v, b, tol=1e-9)
+    r9 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    band = 0.15 if solver == "bicgstab" else 0.05
+    assert r9.report.converged
+    assert abs(r9.report.iterations - ro.iterations) <= max(2, band * ro.iterations)
+
+
+def test_gmres_fast_solution(cvk, oracle):
+    """GMRES (beyond reference): pinned through the unique solution."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.1, f=13.0)
+    A = mat(P, rp, ci, v)
+    x_tight, _ = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-13)
+    r = P.gmres(A, b, P.jacobi(A), P.SolverOptions(tol=1e-12, m=60, max_iter=20000))
+    assert r.report.converged
+    assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
+
+
+def test_ref_mode_bitwise_larger_and_damped(cvk, oracle):
+    P = cvk
+    for h, f, adm in ((0.016643, 13.0, 0j), (0.033289, 100.0, 0.01 + 0j)):
+        rp, ci, v, b = cavity(oracle, h, f, adm)
+        A = mat(P, rp, ci, v)
+        M = P.jacobi(A)
+        for s in ("bicgstab", "tfqmr", "bicgstab_l"):
+            r = P.solve(P.solver_from_name(s), A, b, M, P.SolverOptions(), mode=P.ExecMode.Sequential)
+            xo, ro = oracle.solve(s, rp, ci, v, b)
+            assert r.report.iterations == ro.iterations
+            assert np.array_equal(bits(r.x), bits(xo))
+
+
+def test_kats(cvk):
+    """test_krylov.cpp:80-121, 235-242 and the zero-rhs convention."""
+    P = cvk
+    rng = np.random.default_rng(777001)
+    I = P.csr_identity(10)
+    b = rng.uniform(-1, 1, 10) + 1j * rng.uniform(-1, 1, 10)
+    for s in SOLVERS:
+        r = P.solve(P.solver_from_name(s), I, b, P.identity_preconditioner())
+        assert r.report.converged and r.report.iterations <= 1
+        assert np.abs(r.x - b).max() <= 1e-12
+    n = 12
+    D = P.csr_from_triplets(np.arange(n), np.arange(n), [complex(1 + i, 0.5 * i) for i in range(n)], n, n)
+    b = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    for s in SOLVERS:
+        for mode in (P.ExecMode.Sequential, P.ExecMode.Parallel):
+            r = P.solve(P.solver_from_name(s), D, b, P.jacobi(D), mode=mode)
+            assert r.report.converged and r.report.iterations == 1 and r.report.true_relres <= 1e-12
+    A2 = P.csr_from_triplets([0, 1], [0, 1], [1 + 1j, 2 - 1j], 2, 2)
+    r = P.bicgstab(A2, [1 + 1j, 2 - 1j], P.jacobi(A2))
+    assert r.report.iterations == 1 and np.abs(r.x - 1).max() <= 1e-12
+    z = P.bicgstab(A2, [0j, 0j], P.jacobi(A2))
+    assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
+
+
+def test_errors_and_exhaustion(cvk, oracle):
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.05)
+    A = mat(P, rp, ci, v)
+    r = P.bicgstab(A, b, P.jacobi(A), P.SolverOptions(max_iter=3))
+    assert not r.report.converged and r.report.iterations <= 3
+    with pytest.raises(P.InvalidArgument, match="l must be >= 1"):
+        P.bicgstab_l(A, b, P.jacobi(A), P.SolverOptions(l=0))
+    with pytest.raises(P.InvalidArgument, match="dimension mismatch"):
+        P.bicgstab(A, b[:-1], P.jacobi(A))
+    with pytest.raises(P.InvalidArgument, match="allowed"):
+        P.solver_from_name("gmres2")
+
+
+def test_fast_mode_deterministic(cvk, oracle):
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.025)
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    a = P.bicgstab(A, b, M)
+    c = P.bicgstab(A, b, M)
+    assert a.report.iterations == c.report.iterations
+    assert np.array_equal(bits(a.x), bits(c.x))
+
+
+def test_tfqmr_quasi_residual_nonincreasing(cvk, oracle):
+    """test_krylov.cpp:195-209 on the device."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.1)
+    A = mat(P, rp, ci, v)
+    r = P.tfqmr(A, b, P.jacobi(A), P.SolverOptions(record_history=True))
+    h = r.report.residual_history
+    assert r.report.converged and len(h) >= 2
+    tau = [h[i] / math.sqrt(2.0 * i + 3.0) for i in range(len(h))]
+    assert all(tau[i] <= tau[i - 1] * (1 + 1e-12) for i in range(1, len(tau)))
+
+
+def test_ladder_iterations_grow(cvk, oracle):
+    """acceptance.cpp:241-257 on the device (FAST mode)."""
+    P = cvk
+    for s in ("bicgstab", "bicgstab_l", "tfqmr"):
+        prev = 0
+        for h in (0.133425, 0.066604, 0.033289, 0.016643):
+            rp, ci, v, b = cavity(oracle, h)
+            A = mat(P, rp, ci, v)
+            r = P.solve(P.solver_from_name(s), A, b, P.jacobi(A))
+            assert r.report.converged and r.report.true_relres <= 1e-8
+            assert r.report.iterations >= prev
+            prev = r.report.iterations
