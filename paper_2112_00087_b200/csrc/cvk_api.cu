@@ -17,6 +17,7 @@
 #include "../../include/cavac_b200.h"
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
+#include "cvk_phased.h"
 
 using cvk::DevReport;
 
@@ -38,6 +39,12 @@ struct cvk_ctx {
     size_t bx_n = 0;
     int* bad = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // phase-kernel path
+    cvk::PState* st = nullptr;
+    int* h_done = nullptr;  // pinned [2]
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<unsigned char> gkey;
 };
 
 struct cvk_csr {
@@ -166,6 +173,10 @@ int cvk_ctx_create(int device, cvk_ctx** out) {
     CK(cudaMalloc(&c->bad, sizeof(int)));
     CK(cudaEventCreate(&c->e0));
     CK(cudaEventCreate(&c->e1));
+    CK(cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev[1], cudaEventDisableTiming));
+    CK(cudaMalloc(&c->st, sizeof(cvk::PState)));
+    CK(cudaHostAlloc(&c->h_done, 2 * sizeof(int), cudaHostAllocDefault));
     *out = c;
     return CVK_OK;
 }
@@ -183,6 +194,11 @@ int cvk_ctx_destroy(cvk_ctx* c) {
     cudaFree(c->bad);
     cudaEventDestroy(c->e0);
     cudaEventDestroy(c->e1);
+    cudaEventDestroy(c->ev[0]);
+    cudaEventDestroy(c->ev[1]);
+    cudaFree(c->st);
+    cudaFreeHost(c->h_done);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     cudaStreamDestroy(c->stream);
     delete c;
     return CVK_OK;
@@ -316,6 +332,134 @@ int cvk_precond_get_diag(const cvk_prec* M, double* inv_diag) {
     return CVK_OK;
 }
 
+// Phase-kernel FAST path for large systems (cvk_phased.cu): BiCGSTAB and
+// tfQMR.  Init kernel(s) -> graph replays of kIterPerGraph iterations with a
+// lazily polled device `done` flag -> (tfQMR x fix-up) -> true residual.
+static constexpr int kIterPerGraph = 8;
+
+static long long phased_min_n() {
+    if (const char* env = std::getenv("CVK_PHASED_MIN_N")) return std::atoll(env);
+    return 131072;
+}
+
+static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                        const double2* b_dev, double2* x_dev, cvk_report* rep) {
+    const int n = (int)A->n;
+    const int S = A->group;
+    const cvk::PhasedKernels K = cvk::phased_kernels(S);
+    const void* heavy = solver == CVK_BICGSTAB ? K.bi_a : K.tf_e;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy, cvk::kThreads, 0));
+    if (per_sm < 1) per_sm = 1;
+    const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
+    long long G = std::min<long long>((long long)per_sm * c->nsm, chunks);
+    if (const char* env = std::getenv("CVK_MAX_CTAS")) G = std::min<long long>(G, std::max(1, std::atoi(env)));
+    int e;
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 8 * (size_t)std::max(1, n))) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
+        return e;
+    const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
+    if (hcap > 0 && (size_t)hcap > c->hist_cap) {
+        cudaFree(c->hist);
+        c->hist = nullptr;
+        c->hist_cap = 0;
+        CK(cudaMalloc(&c->hist, sizeof(double) * hcap));
+        c->hist_cap = (size_t)hcap;
+    }
+    cvk::PState hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.tol = o->tol;
+    hs.max_iter = o->max_iter;
+    hs.record = o->record_history ? 1 : 0;
+    hs.hist_cap = hcap;
+    if (o->max_iter < 1) hs.max_iter = 0;
+    std::vector<unsigned char> blob(cvk::phased_args_size());
+    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep);
+    void* args[] = {blob.data()};
+    double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
+    void* targs[] = {blob.data(), &scratch};
+    const dim3 grid((unsigned)G), block(cvk::kThreads);
+    // graph of kIterPerGraph iterations, cached while the arguments are unchanged
+    std::vector<unsigned char> key(blob);
+    key.push_back((unsigned char)solver);
+    key.push_back((unsigned char)S);
+    const unsigned char* gp = (const unsigned char*)&G;
+    key.insert(key.end(), gp, gp + sizeof(G));
+    if (!c->gexec || c->gkey != key) {
+        if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int it = 0; it < kIterPerGraph; ++it) {
+            if (solver == CVK_BICGSTAB) {
+                cudaLaunchKernel(K.bi_a, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.bi_b, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.bi_c, grid, block, args, 0, c->stream);
+            } else {
+                cudaLaunchKernel(K.tf_w, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.tf_e, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.tf_o, grid, block, args, 0, c->stream);
+            }
+        }
+        CK(cudaStreamEndCapture(c->stream, &graph));
+        CK(cudaGraphInstantiate(&c->gexec, graph, 0));
+        cudaGraphDestroy(graph);
+        c->gkey = key;
+    }
+    CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->e0, c->stream));
+    long long launches = 0;
+    if (solver == CVK_BICGSTAB) {
+        CK(cudaLaunchKernel(K.bi_init, grid, block, args, 0, c->stream));
+        launches += 1;
+    } else {
+        CK(cudaLaunchKernel(K.tf_init, grid, block, args, 0, c->stream));
+        CK(cudaLaunchKernel(K.tf_init2, grid, block, args, 0, c->stream));
+        launches += 2;
+    }
+    long long graphs = 0;
+    const long long max_graphs = o->max_iter / kIterPerGraph + 3;
+    for (;;) {
+        if (graphs >= max_graphs) break;
+        CK(cudaGraphLaunch(c->gexec, c->stream));
+        const int slot = (int)(graphs & 1);
+        CK(cudaMemcpyAsync(&c->h_done[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(c->ev[slot], c->stream));
+        ++graphs;
+        launches += 3 * kIterPerGraph;
+        if (graphs >= 2) {
+            const int old = (int)((graphs - 2) & 1);
+            CK(cudaEventSynchronize(c->ev[old]));
+            if (c->h_done[old]) break;
+        }
+    }
+    if (solver == CVK_TFQMR) {
+        CK(cudaLaunchKernel(K.tf_fix, grid, block, args, 0, c->stream));
+        launches += 1;
+    }
+    CK(cudaLaunchKernel(K.true_res, grid, block, targs, 0, c->stream));
+    launches += 1;
+    CK(cudaEventRecord(c->e1, c->stream));
+    cvk::DevReport dr;
+    CK(cudaMemcpyAsync(&dr, c->rep, sizeof(dr), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    rep->converged = dr.converged;
+    rep->breakdown = dr.breakdown;
+    rep->iterations = dr.iterations;
+    rep->final_relres = dr.final_relres;
+    rep->true_relres = dr.true_relres;
+    rep->history_len = o->record_history ? dr.history_len : 0;
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = launches;
+    if (o->record_history && rep->history && rep->history_cap > 0) {
+        const long long k = std::min<long long>(std::min<long long>(rep->history_len, rep->history_cap), hcap);
+        if (k > 0) CK(cudaMemcpy(rep->history, c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    return CVK_OK;
+}
+
 static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                       const double2* b_dev, double2* x_dev, cvk_report* rep) {
     if (solver < 0 || solver > 3)
@@ -333,6 +477,9 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     const int n = (int)A->n;
     const int mode = resolve_mode(c, o->mode);
     const bool ref = mode == CVK_MODE_REF;
+    CK(cudaSetDevice(c->device));
+    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n())
+        return solve_phased(c, solver, A, M, o, b_dev, x_dev, rep);
     const int S = ref ? 1 : A->group;
     const void* kern = cvk::solver_kernel(solver, S, ref);
     if (!kern) return fail(CVK_ELOGIC, "no kernel for this configuration");

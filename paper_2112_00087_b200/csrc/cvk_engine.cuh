@@ -29,6 +29,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSlots = 64;
 constexpr int kRegions = 3;
+constexpr int kMinCtas = 3;  // persistent solvers: <= 80 registers, 3 CTAs (24 warps) per SM
 
 struct DevReport {
     int32_t converged;
@@ -160,15 +161,36 @@ __device__ __forceinline__ void for_rows(int n, int G, F&& f) {
 // Row sum y = sum_k A[row,k] * x(col_k): left to right per lane; for S > 1
 // the S lane sums are combined by a fixed xor tree (all lanes get the sum).
 // With S == 1 this is exactly the reference's row loop (numkit.cpp:98-103).
-template <int S, class X>
+//
+// With BATCH > 1 loads are batched: each lane first issues up to U = BATCH/S
+// (value, column) loads,
+// then all U gathers, then accumulates -- the col -> x[col] dependency chain
+// is paid once per batch instead of once per entry (memory-level
+// parallelism; the accumulation order per lane is unchanged).
+template <int S, class X, int BATCH = 1>
 __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool valid, X&& xat) {
+    constexpr int U = (BATCH / S) > 0 ? (BATCH / S) : 1;
     double2 acc = make_double2(0.0, 0.0);
     if (valid) {
         const int b = __ldg(A.rp + row), e = __ldg(A.rp + row + 1);
-        for (int k = b + lane; k < e; k += S) {
-            const double2 a = ld_stream(A.av + k);
-            const int c = ld_stream(A.ci + k);
-            acc = cvk_add(acc, cvk_mul(a, xat(c)));
+        for (int k = b + lane; k < e; k += U * S) {
+            double2 a[U];
+            int c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = k + u * S;
+                if (kk < e) {
+                    a[u] = ld_stream(A.av + kk);
+                    c[u] = ld_stream(A.ci + kk);
+                }
+            }
+            double2 xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k + u * S < e) xv[u] = xat(c[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k + u * S < e) acc = cvk_add(acc, cvk_mul(a[u], xv[u]));
         }
     }
     if (S > 1) {
@@ -253,8 +275,11 @@ template <bool REF, int K, class C>
 __device__ __forceinline__ bool reduce(GridBar& g, const double2 (&acc)[K], double2 (&out)[K],
                                        double2* part, int n, C&& contrib) {
     if (REF) {
+        // thread 0 of every CTA re-reads whole vectors after the barrier; the
+        // second barrier keeps fast CTAs from rewriting them meanwhile
         if (!g.sync()) return false;
         seq_sums<K>(out, n, contrib);
+        if (!g.sync()) return false;
     } else {
         cta_partial<K>(acc, part, g.G);
         if (!g.sync()) return false;

@@ -72,7 +72,7 @@ __device__ bool true_relres(GridBar& g, const KArgs& a, double2* scratch, double
 // ================================================================ BiCGSTAB
 // work: r, shadow, s, t, p[2], v[2]
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads) k_bicgstab(KArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
     GridBar g(a.bar, a.G);
     const int n = a.A.n, G = a.G;
     const double2* __restrict__ dinv = a.dinv;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(KArgs a) {
 // =================================================================== tfQMR
 // work: r, shadow, w, u[2], au, v, d
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads) k_tfqmr(KArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
     GridBar g(a.bar, a.G);
     const int n = a.A.n, G = a.G;
     const double2* __restrict__ dinv = a.dinv;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) k_tfqmr(KArgs a) {
 // ============================================================ BiCGSTAB(l)
 // work: shadow, x-scratch?, then r[0..l], u[0..l], spareR, spareU  (2l+5 vectors)
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads) k_bicgstab_l(KArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
     GridBar g(a.bar, a.G);
     const int n = a.A.n, G = a.G, L = a.l;
     const double2* __restrict__ dinv = a.dinv;
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab_l(KArgs a) {
 // work: r, W[2], V[0..m]   (m + 4 vectors)
 // dynamic shared: H[(m+1) m], sn[m], g[m+1], y[m], h1[m+1], h2[m+1] (double2), cs[m] (double)
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads) k_gmres(KArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
     GridBar g(a.bar, a.G);
     const int n = a.A.n, G = a.G, M = a.m;
     const double2* __restrict__ dinv = a.dinv;
@@ -802,6 +802,8 @@ __global__ void __launch_bounds__(kThreads) k_gmres(KArgs a) {
                     ok = g.sync();
                     if (!ok) break;
                     seq_multi(w, j + 1, h1);
+                    ok = g.sync();
+                    if (!ok) break;
                 } else {
                     multi_dot(w, j + 1, pr);
                     ok = g.sync();
@@ -821,6 +823,8 @@ __global__ void __launch_bounds__(kThreads) k_gmres(KArgs a) {
                     ok = g.sync();
                     if (!ok) break;
                     seq_multi(w, j + 1, h2);
+                    ok = g.sync();
+                    if (!ok) break;
                 } else {
                     multi_dot(w, j + 1, pr);
                     ok = g.sync();

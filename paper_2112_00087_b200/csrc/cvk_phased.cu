@@ -1,0 +1,548 @@
+// cvk_phased.cu -- FAST-mode Krylov solvers for large systems as a chain of
+// small phase kernels, replayed from a CUDA graph.
+//
+// Why not the persistent kernel here: a single cooperative kernel carries
+// the register allocation of its most complex phase, which caps it at 3
+// CTAs/SM and leaves the SpMV phases latency-bound at ~1/3 of HBM peak
+// (profiles/r01_persistent_bicgstab.txt).  Each phase kernel below only pays
+// for its own work (batched gathers, full occupancy).
+//
+// Scalars never visit the host.  Each phase kernel ends with a deterministic
+// "last CTA folds" reduction: every CTA writes its partials, the CTA that
+// arrives last at a per-phase counter folds them in a fixed order, runs the
+// solver's scalar recurrence (breakdown tests, alpha/beta/omega, convergence,
+// iteration count, history) and writes the next state; the following kernel
+// reads it.  Once `done` is set every later kernel returns immediately, so
+// the host can queue whole graphs of iterations and poll the flag lazily.
+//
+// Algorithms and per-element roundings are those of the persistent kernels
+// (cvk_krylov.cu): bicgstab krylov.cpp:57-138, tfqmr krylov.cpp:288-375.
+#include <cuda_runtime.h>
+
+#include "cvk_engine.cuh"
+#include "cvk_kernels.h"
+#include "cvk_phased.h"
+
+namespace cvk {
+
+namespace {
+
+constexpr int kBatch = 4;  // (value, column) loads in flight per row lane (U = kBatch / S)
+
+struct PArgs {
+    Csr A;
+    const double2* dinv;
+    const double2* b;
+    double2* x;
+    double2* work;
+    double2* part;  // kMaxSlots x G per phase counter slot
+    PState* st;
+    double* hist;
+    DevReport* rep;
+};
+
+__device__ __forceinline__ double2* partv(const PArgs& a, int k) {
+    return a.part + (size_t)k * kMaxSlots * gridDim.x;
+}
+
+// Write this CTA's K partials; returns true in the CTA that arrived last,
+// with the fixed-order totals in tot (all threads of that CTA).
+template <int K>
+__device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* counter,
+                             double2 (&tot)[K]) {
+    __shared__ double2 sm[K][kWarps];
+    __shared__ int s_last;
+    const int G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double2 v = warp_sum(acc[k]);
+        if (lane == 0) sm[k][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double2 s = sm[threadIdx.x][0];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
+        part[threadIdx.x * G + blockIdx.x] = s;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == (unsigned)G - 1u);
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int b = threadIdx.x; b < G; b += kThreads) s = cvk_add(s, __ldcg(part + k * G + b));
+        s = warp_sum(s);
+        __syncthreads();
+        if (lane == 0) sm[k][warp] = s;
+        __syncthreads();
+        double2 t = sm[k][0];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) t = cvk_add(t, sm[k][w]);
+        tot[k] = t;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
+__device__ __forceinline__ void st_hist(const PArgs& a, PState* st, double v) {
+    if (!st->record) return;
+    if (st->hist_len < st->hist_cap) a.hist[st->hist_len] = v;
+    st->hist_len++;
+}
+
+// ------------------------------------------------------------ BiCGSTAB --
+// work: r, shadow, s, t, p[2], v[2]
+struct BiVecs {
+    double2 *r, *sh, *s, *t, *p0, *p1, *v0, *v1;
+    __device__ BiVecs(double2* w, size_t n)
+        : r(w), sh(w + n), s(w + 2 * n), t(w + 3 * n), p0(w + 4 * n), p1(w + 5 * n),
+          v0(w + 6 * n), v1(w + 7 * n) {}
+};
+
+// top of iteration st->it (krylov.cpp:81-96), run by the last CTA
+__device__ void bi_top(PState* st) {
+    if (st->it > st->max_iter) { st->done = 1; return; }
+    if (cvk_abs(st->rho_new) < st->brk) {
+        st->done = 1; st->brk_code = 1; st->iters = st->it - 1;
+        return;
+    }
+    if (!st->first) st->beta = cvk_mul(cvk_cdiv(st->rho_new, st->rho), cvk_cdiv(st->alpha, st->omega));
+    st->rho = st->rho_new;
+}
+
+__global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for_elems(n, gridDim.x, [&](int i) {
+        const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
+        V.r[i] = ri;
+        V.sh[i] = ri;
+        a.x[i] = make_double2(0.0, 0.0);
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], ri, ri);
+    });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 0), &a.st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    PState* st = a.st;
+    st->bnorm = sqrt(tot[0].x);
+    if (st->bnorm == 0.0) {  // krylov.cpp:70-74
+        st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1;
+        return;
+    }
+    st->brk = 1e-30 * st->bnorm * st->bnorm;
+    st->rho_new = tot[1];
+    st->rho = st->alpha = st->omega = make_double2(1.0, 0.0);
+    st->it = 1;
+    st->first = 1;
+    st->cur = 0;
+    bi_top(st);
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = st->cur;
+    const bool first = st->first != 0;
+    const double2 beta = st->beta, nom = cvk_neg(st->omega);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pc = cur ? V.p1 : V.p0;
+    const double2* __restrict__ vc = cur ? V.v1 : V.v0;
+    double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    const double2* __restrict__ sh = V.sh;
+    auto pnew = [&](int c) -> double2 {
+        const double2 rc = r[c];
+        if (first) return rc;
+        return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+    };
+    double2 acc[1] = {make_double2(0, 0)};
+    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S, decltype(pnew)&, kBatch>(a.A, row, lane, valid, pnew);
+        if (valid && lane == 0) {
+            const double2 vi = prec_apply(a.dinv, row, y);
+            pn[row] = pnew(row);
+            vn[row] = vi;
+            acc_dot(acc[0], sh[row], vi);
+        }
+    });
+    double2 tot[1];
+    if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    if (cvk_abs(tot[0]) < st->brk) {
+        st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
+        return;
+    }
+    st->alpha = cvk_cdiv(st->rho, tot[0]);
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = st->cur;
+    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    const double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    double2* __restrict__ s = V.s;
+    double2* __restrict__ t = V.t;
+    double2* __restrict__ x = a.x;
+    auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+    double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S, decltype(sval)&, kBatch>(a.A, row, lane, valid, sval);
+        if (valid && lane == 0) {
+            const double2 ti = prec_apply(a.dinv, row, y);
+            const double2 si = sval(row);
+            s[row] = si;
+            t[row] = ti;
+            x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
+            acc_norm(acc[0], si);
+            acc_dot(acc[1], ti, ti);
+            acc_dot(acc[2], ti, si);
+        }
+    });
+    double2 tot[3];
+    if (!partial_last<3>(acc, partv(a, 2), &st->counter[2], tot)) return;
+    if (threadIdx.x != 0) return;
+    const double relres = sqrt(tot[0].x) / st->bnorm;
+    if (relres <= st->tol) {
+        st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
+        st_hist(a, st, relres);
+        return;
+    }
+    if (cvk_abs(tot[1]) < st->brk) {
+        st->done = 1; st->brk_code = 3; st->iters = st->it;
+        return;
+    }
+    st->omega = cvk_cdiv(tot[2], tot[1]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const double2 omega = st->omega, nom = cvk_neg(st->omega);
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    const double2* __restrict__ s = V.s;
+    const double2* __restrict__ t = V.t;
+    const double2* __restrict__ sh = V.sh;
+    double2* __restrict__ r = V.r;
+    double2* __restrict__ x = a.x;
+    for_elems(n, gridDim.x, [&](int i) {
+        const double2 si = s[i];
+        x[i] = cvk_add(x[i], cvk_mul(omega, si));
+        const double2 ri = cvk_add(si, cvk_mul(nom, t[i]));
+        r[i] = ri;
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], sh[i], ri);
+    });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    const double relres = sqrt(tot[0].x) / st->bnorm;
+    st->final_relres = relres;
+    st->iters = st->it;
+    st_hist(a, st, relres);
+    if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
+    st->rho_new = tot[1];
+    st->cur ^= 1;
+    st->first = 0;
+    st->it++;
+    bi_top(st);
+}
+
+// --------------------------------------------------------------- tfQMR --
+// work: r, shadow, w, u[2], au, v, d
+struct TfVecs {
+    double2 *r, *sh, *w, *u0, *u1, *au, *v, *d;
+    __device__ TfVecs(double2* wk, size_t n)
+        : r(wk), sh(wk + n), w(wk + 2 * n), u0(wk + 3 * n), u1(wk + 4 * n), au(wk + 5 * n),
+          v(wk + 6 * n), d(wk + 7 * n) {}
+};
+
+// even half-step head (krylov.cpp:319-326), run by the last CTA after sigma
+__device__ void tf_even_head(PState* st, double2 sigma) {
+    if (st->it > st->max_iter) { st->done = 1; return; }
+    if (cvk_abs(sigma) < st->brk) { st->done = 1; st->brk_code = 6; return; }
+    st->alpha = cvk_cdiv(st->rho, sigma);
+}
+
+__global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for_elems(n, gridDim.x, [&](int i) {
+        const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
+        V.r[i] = ri; V.sh[i] = ri; V.w[i] = ri; V.u0[i] = ri;
+        V.d[i] = make_double2(0, 0);
+        a.x[i] = make_double2(0, 0);
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], ri, ri);
+    });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 0), &a.st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    PState* st = a.st;
+    st->bnorm = sqrt(tot[0].x);
+    if (st->bnorm == 0.0) { st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1; return; }
+    st->brk = 1e-30 * st->bnorm * st->bnorm;
+    st->rho = tot[1];
+    st->tau = st->bnorm;
+    st->theta = 0.0;
+    st->eta = make_double2(0, 0);
+    st->alpha = make_double2(0, 0);
+    st->it = 1;  // even half-step index = 2 (it - 1)
+    st->cur = 0;
+}
+
+// au = M^{-1} A u0, v = au, sigma = <shadow, v>
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2* __restrict__ u0 = V.u0;
+    auto uat = [&](int c) -> double2 { return u0[c]; };
+    double2 acc[1] = {make_double2(0, 0)};
+    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S, decltype(uat)&, kBatch>(a.A, row, lane, valid, uat);
+        if (valid && lane == 0) {
+            const double2 ai = prec_apply(a.dinv, row, y);
+            V.au[row] = ai;
+            V.v[row] = ai;
+            acc_dot(acc[0], V.sh[row], ai);
+        }
+    });
+    double2 tot[1];
+    if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    tf_even_head(st, tot[0]);
+}
+
+// even half-step body: w -= alpha au; d = coef d + u; ||w||
+__global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 nal = cvk_neg(st->alpha);
+    const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
+    const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
+    double2 acc[1] = {make_double2(0, 0)};
+    for_elems(n, gridDim.x, [&](int i) {
+        const double2 wi = cvk_add(V.w[i], cvk_mul(nal, V.au[i]));
+        V.w[i] = wi;
+        V.d[i] = cvk_add(cvk_mul(coef, V.d[i]), uc[i]);
+        acc_norm(acc[0], wi);
+    });
+    double2 tot[1];
+    if (!partial_last<1>(acc, partv(a, 2), &st->counter[2], tot)) return;
+    if (threadIdx.x != 0) return;
+    st->theta = sqrt(tot[0].x) / st->tau;
+    const double c = 1.0 / sqrt(1.0 + st->theta * st->theta);
+    st->tau = st->tau * st->theta * c;
+    st->eta = cvk_scale(c * c, st->alpha);
+    st->pending_x = 1;
+    const long long hs = 2 * (st->it - 1);
+    const double relres = st->tau * sqrt((double)(hs + 2)) / st->bnorm;
+    st->final_relres = relres;
+    st->iters = hs / 2 + 1;
+    if (relres <= st->tol) { st->done = 1; st->conv = 1; }
+}
+
+// even tail + odd head: u' = u - alpha v; au = M^{-1} A u'; x += eta d;
+// w -= alpha au; d = coef d + u'; ||w||, <shadow, w>
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 nal = cvk_neg(st->alpha);
+    const double2 eta_e = st->eta;
+    const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
+    const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
+    double2* __restrict__ un = st->cur ? V.u0 : V.u1;
+    const double2* __restrict__ vv = V.v;
+    auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S, decltype(uval)&, kBatch>(a.A, row, lane, valid, uval);
+        if (valid && lane == 0) {
+            const double2 ui = uval(row);
+            const double2 ai = prec_apply(a.dinv, row, y);
+            un[row] = ui;
+            V.au[row] = ai;
+            const double2 di = V.d[row];
+            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_e, di));
+            const double2 wi = cvk_add(V.w[row], cvk_mul(nal, ai));
+            V.w[row] = wi;
+            V.d[row] = cvk_add(cvk_mul(coef, di), ui);
+            acc_norm(acc[0], wi);
+            acc_dot(acc[1], V.sh[row], wi);
+        }
+    });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    st->cur ^= 1;
+    st->theta = sqrt(tot[0].x) / st->tau;
+    const double c = 1.0 / sqrt(1.0 + st->theta * st->theta);
+    st->tau = st->tau * st->theta * c;
+    st->eta = cvk_scale(c * c, st->alpha);
+    st->pending_x = 1;
+    const long long hs = 2 * (st->it - 1) + 1;
+    const double relres = st->tau * sqrt((double)(hs + 2)) / st->bnorm;
+    st->final_relres = relres;
+    st->iters = hs / 2 + 1;
+    st_hist(a, st, relres);
+    if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
+    if (cvk_abs(st->rho) < st->brk) { st->done = 1; st->brk_code = 1; return; }
+    st->beta = cvk_cdiv(tot[1], st->rho);
+    st->rho = tot[1];
+}
+
+// odd tail: u_next = w + beta u; au_next = M^{-1} A u_next;
+// v = beta (beta v + au) + au_next; x += eta d; sigma = <shadow, v>
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 beta = st->beta, eta_o = st->eta;
+    const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
+    double2* __restrict__ un = st->cur ? V.u0 : V.u1;
+    const double2* __restrict__ w = V.w;
+    auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
+    double2 acc[1] = {make_double2(0, 0)};
+    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+        const double2 y = row_sum<S, decltype(unext)&, kBatch>(a.A, row, lane, valid, unext);
+        if (valid && lane == 0) {
+            const double2 un_i = unext(row);
+            const double2 an = prec_apply(a.dinv, row, y);
+            un[row] = un_i;
+            double2 vi = cvk_add(cvk_mul(beta, V.v[row]), V.au[row]);
+            vi = cvk_add(cvk_mul(beta, vi), an);
+            V.v[row] = vi;
+            V.au[row] = an;
+            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_o, V.d[row]));
+            acc_dot(acc[0], V.sh[row], vi);
+        }
+    });
+    double2 tot[1];
+    if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    st->pending_x = 0;
+    st->cur ^= 1;
+    st->it++;
+    tf_even_head(st, tot[0]);
+}
+
+// owed x += eta d after a tfQMR exit (krylov.cpp:335)
+__global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
+    PState* st = a.st;
+    if (!st->pending_x) return;
+    TfVecs V(a.work, (size_t)a.A.n);
+    const double2 e = st->eta;
+    for_elems(a.A.n, gridDim.x, [&](int i) { a.x[i] = cvk_add(a.x[i], cvk_mul(e, V.d[i])); });
+}
+
+// ------------------------------------------------- true residual + report
+template <int S>
+__global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
+    PState* st = a.st;
+    const int n = a.A.n;
+    const double2* __restrict__ x = a.x;
+    auto xat = [&](int c) -> double2 { return x[c]; };
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    if (!st->skip_true) {
+        for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S, decltype(xat)&, kBatch>(a.A, row, lane, valid, xat);
+            if (valid && lane == 0) {
+                const double2 bi = __ldg(a.b + row);
+                const double2 d = cvk_sub(bi, y);
+                scratch[row] = d;
+                acc_norm(acc[0], bi);
+                acc_norm(acc[1], d);
+            }
+        });
+    }
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 2), &st->counter[3], tot)) return;
+    if (threadIdx.x != 0) return;
+    double trr = 0.0;
+    if (!st->skip_true) {
+        const double bn = sqrt(tot[0].x), rn = sqrt(tot[1].x);
+        trr = bn > 0 ? rn / bn : rn;
+    }
+    a.rep->converged = st->conv;
+    a.rep->breakdown = st->brk_code;
+    a.rep->iterations = st->iters;
+    a.rep->final_relres = st->final_relres;
+    a.rep->true_relres = trr;
+    a.rep->history_len = st->hist_len;
+    a.rep->error = 0;
+}
+
+template <int S>
+PhasedKernels kernels_for() {
+    PhasedKernels k;
+    k.bi_init = (const void*)k_bi_init;
+    k.bi_a = (const void*)k_bi_a<S>;
+    k.bi_b = (const void*)k_bi_b<S>;
+    k.bi_c = (const void*)k_bi_c;
+    k.tf_init = (const void*)k_tf_init;
+    k.tf_init2 = (const void*)k_tf_init2<S>;
+    k.tf_w = (const void*)k_tf_w;
+    k.tf_e = (const void*)k_tf_e<S>;
+    k.tf_o = (const void*)k_tf_o<S>;
+    k.tf_fix = (const void*)k_tf_fix;
+    k.true_res = (const void*)k_true<S>;
+    return k;
+}
+
+}  // namespace
+
+PhasedKernels phased_kernels(int S) {
+    switch (S) {
+        case 1: return kernels_for<1>();
+        case 2: return kernels_for<2>();
+        case 4: return kernels_for<4>();
+        case 8: return kernels_for<8>();
+        default: return kernels_for<16>();
+    }
+}
+
+size_t phased_args_size() { return sizeof(PArgs); }
+
+void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep) {
+    PArgs* p = (PArgs*)out;
+    p->A = A;
+    p->dinv = dinv;
+    p->b = b;
+    p->x = x;
+    p->work = work;
+    p->part = part;
+    p->st = st;
+    p->hist = hist;
+    p->rep = rep;
+}
+
+}  // namespace cvk

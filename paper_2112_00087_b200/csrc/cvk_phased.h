@@ -1,0 +1,35 @@
+// cvk_phased.h -- device state and kernel table of the phase-kernel solvers
+// (cvk_phased.cu), shared with the host launcher in cvk_api.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cvk {
+
+struct Csr;
+struct DevReport;
+
+// Solver state carried between phase kernels (device memory).  Written only
+// by the last-arriving CTA of each phase kernel; read by the next kernel.
+struct PState {
+    double2 rho, rho_new, alpha, omega, beta, eta;
+    double bnorm, brk, tol, final_relres, tau, theta;
+    long long it, iters, max_iter, hist_len, hist_cap;
+    int done, conv, brk_code, first, pending_x, cur, record, skip_true;
+    unsigned counter[4];
+};
+
+struct PhasedKernels {
+    const void *bi_init, *bi_a, *bi_b, *bi_c;
+    const void *tf_init, *tf_init2, *tf_w, *tf_e, *tf_o, *tf_fix;
+    const void* true_res;  // (PArgs, double2* scratch)
+};
+
+PhasedKernels phased_kernels(int S);
+size_t phased_args_size();
+void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep);
+
+}  // namespace cvk
