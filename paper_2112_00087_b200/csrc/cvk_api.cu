@@ -53,7 +53,8 @@ struct cvk_csr {
     int* rp = nullptr;
     int* ci = nullptr;
     double2* av = nullptr;
-    int group = 1;  // SpMV lanes per row for FAST mode
+    int group = 1;  // SpMV lanes per row for FAST mode (persistent kernels)
+    int tile = 1;   // spmv_tiled product tile: max entries of a 256-row chunk (capped)
 };
 
 struct cvk_prec {
@@ -241,6 +242,14 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     A->n = nrows;
     A->nnz = nnz;
     A->group = pick_group(nrows ? (double)nnz / (double)nrows : 1.0);
+    {
+        int mx = 1;
+        for (int64_t b = 0; b < nrows; b += cvk::kThreads) {
+            const int64_t e = std::min<int64_t>(b + cvk::kThreads, nrows);
+            mx = std::max(mx, rp[(size_t)e] - rp[(size_t)b]);
+        }
+        A->tile = std::min(mx, cvk::kMaxTile);
+    }
     CK(cudaMalloc(&A->rp, sizeof(int) * (rp.size())));
     CK(cudaMalloc(&A->ci, sizeof(int) * std::max<size_t>(1, ci.size())));
     CK(cudaMalloc(&A->av, sizeof(double2) * std::max<int64_t>(1, nnz)));
@@ -346,10 +355,13 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
                         const double2* b_dev, double2* x_dev, cvk_report* rep) {
     const int n = (int)A->n;
     const int S = A->group;
-    const cvk::PhasedKernels K = cvk::phased_kernels(S);
-    const void* heavy = solver == CVK_BICGSTAB ? K.bi_a : K.tf_e;
+    const cvk::PhasedKernels K = cvk::phased_kernels();
+    const size_t smem = sizeof(double2) * (size_t)A->tile;
+    for (const void* kf : {K.bi_a, K.bi_b, K.tf_init2, K.tf_e, K.tf_o, K.true_res})
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    const void* heavy = solver == CVK_BICGSTAB ? K.bi_b : K.tf_e;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy, cvk::kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy, cvk::kThreads, smem));
     if (per_sm < 1) per_sm = 1;
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>((long long)per_sm * c->nsm, chunks);
@@ -375,7 +387,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if (o->max_iter < 1) hs.max_iter = 0;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep);
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->tile);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
@@ -392,13 +404,13 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < kIterPerGraph; ++it) {
             if (solver == CVK_BICGSTAB) {
-                cudaLaunchKernel(K.bi_a, grid, block, args, 0, c->stream);
-                cudaLaunchKernel(K.bi_b, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.bi_a, grid, block, args, smem, c->stream);
+                cudaLaunchKernel(K.bi_b, grid, block, args, smem, c->stream);
                 cudaLaunchKernel(K.bi_c, grid, block, args, 0, c->stream);
             } else {
                 cudaLaunchKernel(K.tf_w, grid, block, args, 0, c->stream);
-                cudaLaunchKernel(K.tf_e, grid, block, args, 0, c->stream);
-                cudaLaunchKernel(K.tf_o, grid, block, args, 0, c->stream);
+                cudaLaunchKernel(K.tf_e, grid, block, args, smem, c->stream);
+                cudaLaunchKernel(K.tf_o, grid, block, args, smem, c->stream);
             }
         }
         CK(cudaStreamEndCapture(c->stream, &graph));
@@ -414,7 +426,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         launches += 1;
     } else {
         CK(cudaLaunchKernel(K.tf_init, grid, block, args, 0, c->stream));
-        CK(cudaLaunchKernel(K.tf_init2, grid, block, args, 0, c->stream));
+        CK(cudaLaunchKernel(K.tf_init2, grid, block, args, smem, c->stream));
         launches += 2;
     }
     long long graphs = 0;
@@ -437,7 +449,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaLaunchKernel(K.tf_fix, grid, block, args, 0, c->stream));
         launches += 1;
     }
-    CK(cudaLaunchKernel(K.true_res, grid, block, targs, 0, c->stream));
+    CK(cudaLaunchKernel(K.true_res, grid, block, targs, smem, c->stream));
     launches += 1;
     CK(cudaEventRecord(c->e1, c->stream));
     cvk::DevReport dr;
@@ -594,7 +606,7 @@ int cvk_spmv_device(const cvk_csr* A, const double* x_dev, double* y_dev, int mo
     const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
     CK(cvk::launch_spmv(ref ? 1 : A->group, ref, (int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
-                        (double2*)y_dev, c->stream));
+                        (double2*)y_dev, A->tile, c->stream));
     return CVK_OK;
 }
 

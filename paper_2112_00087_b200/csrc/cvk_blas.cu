@@ -7,6 +7,8 @@
 //   axpy_inplace    numkit.cpp:135-146
 //   xpay_inplace    numkit.cpp:148-159
 //   jacobi          krylov.cpp:31-55    (first col==i entry, 1.0/d via __divdc3 rounding)
+#include <cstdlib>
+
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 
@@ -21,6 +23,13 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restr
         const double2 acc = row_sum<S, decltype(xat)&, (REF ? 1 : 8)>(A, row, lane, valid, xat);
         if (valid && lane == 0) __stcs(y + row, acc);
     });
+}
+
+// FAST SpMV: nnz-tiled chunks (one CTA per 256-row chunk)
+__global__ void __launch_bounds__(kThreads) k_spmv_tiled(Csr A, const double2* __restrict__ x,
+                                                         double2* __restrict__ y, int tile) {
+    auto xat = [&](int c) { return __ldg(x + c); };
+    spmv_tiled<4>(A, gridDim.x, tile, xat, [&](int row, double2 acc) { __stcs(y + row, acc); });
 }
 
 template <int S, bool REF>
@@ -108,9 +117,17 @@ static cudaError_t spmv_t(int n, const int* rp, const int* ci, const double2* av
 }
 
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
-                        const double2* x, double2* y, cudaStream_t st) {
+                        const double2* x, double2* y, int tile, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     if (ref) return spmv_t<1, true>(n, rp, ci, av, x, y, st);
+    if (tile > 0 && !std::getenv("CVK_SPMV_ROWS")) {
+        const size_t smem = sizeof(double2) * (size_t)tile;
+        cudaError_t e = cudaFuncSetAttribute(k_spmv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        Csr A{n, rp, ci, av};
+        k_spmv_tiled<<<grid_for(n), kThreads, smem, st>>>(A, x, y, tile);
+        return cudaGetLastError();
+    }
     switch (S) {
         case 1: return spmv_t<1, false>(n, rp, ci, av, x, y, st);
         case 2: return spmv_t<2, false>(n, rp, ci, av, x, y, st);

@@ -27,7 +27,7 @@ namespace cvk {
 
 namespace {
 
-constexpr int kBatch = 4;  // (value, column) loads in flight per row lane (U = kBatch / S)
+constexpr int kBatch = 4;  // (value, column) loads in flight per thread per round
 
 struct PArgs {
     Csr A;
@@ -39,6 +39,7 @@ struct PArgs {
     PState* st;
     double* hist;
     DevReport* rep;
+    int tile;  // shared-memory product tile (entries) of spmv_tiled
 };
 
 __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
@@ -145,7 +146,6 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     bi_top(st);
 }
 
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
     PState* st = a.st;
     if (st->done) return;
@@ -166,14 +166,11 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
         return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
     };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-        const double2 y = row_sum<S, decltype(pnew)&, kBatch>(a.A, row, lane, valid, pnew);
-        if (valid && lane == 0) {
-            const double2 vi = prec_apply(a.dinv, row, y);
-            pn[row] = pnew(row);
-            vn[row] = vi;
-            acc_dot(acc[0], sh[row], vi);
-        }
+    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, pnew, [&](int row, double2 y) {
+        const double2 vi = prec_apply(a.dinv, row, y);
+        pn[row] = pnew(row);
+        vn[row] = vi;
+        acc_dot(acc[0], sh[row], vi);
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -185,7 +182,6 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
     st->alpha = cvk_cdiv(st->rho, tot[0]);
 }
 
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     PState* st = a.st;
     if (st->done) return;
@@ -201,18 +197,15 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     double2* __restrict__ x = a.x;
     auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
     double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-        const double2 y = row_sum<S, decltype(sval)&, kBatch>(a.A, row, lane, valid, sval);
-        if (valid && lane == 0) {
-            const double2 ti = prec_apply(a.dinv, row, y);
-            const double2 si = sval(row);
-            s[row] = si;
-            t[row] = ti;
-            x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
-            acc_norm(acc[0], si);
-            acc_dot(acc[1], ti, ti);
-            acc_dot(acc[2], ti, si);
-        }
+    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, sval, [&](int row, double2 y) {
+        const double2 ti = prec_apply(a.dinv, row, y);
+        const double2 si = sval(row);
+        s[row] = si;
+        t[row] = ti;
+        x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
+        acc_norm(acc[0], si);
+        acc_dot(acc[1], ti, ti);
+        acc_dot(acc[2], ti, si);
     });
     double2 tot[3];
     if (!partial_last<3>(acc, partv(a, 2), &st->counter[2], tot)) return;
@@ -310,7 +303,6 @@ __global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
 }
 
 // au = M^{-1} A u0, v = au, sigma = <shadow, v>
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     PState* st = a.st;
     if (st->done) return;
@@ -319,14 +311,11 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     const double2* __restrict__ u0 = V.u0;
     auto uat = [&](int c) -> double2 { return u0[c]; };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-        const double2 y = row_sum<S, decltype(uat)&, kBatch>(a.A, row, lane, valid, uat);
-        if (valid && lane == 0) {
-            const double2 ai = prec_apply(a.dinv, row, y);
-            V.au[row] = ai;
-            V.v[row] = ai;
-            acc_dot(acc[0], V.sh[row], ai);
-        }
+    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, uat, [&](int row, double2 y) {
+        const double2 ai = prec_apply(a.dinv, row, y);
+        V.au[row] = ai;
+        V.v[row] = ai;
+        acc_dot(acc[0], V.sh[row], ai);
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -367,7 +356,6 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
 
 // even tail + odd head: u' = u - alpha v; au = M^{-1} A u'; x += eta d;
 // w -= alpha au; d = coef d + u'; ||w||, <shadow, w>
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     PState* st = a.st;
     if (st->done) return;
@@ -381,21 +369,18 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     const double2* __restrict__ vv = V.v;
     auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-        const double2 y = row_sum<S, decltype(uval)&, kBatch>(a.A, row, lane, valid, uval);
-        if (valid && lane == 0) {
-            const double2 ui = uval(row);
-            const double2 ai = prec_apply(a.dinv, row, y);
-            un[row] = ui;
-            V.au[row] = ai;
-            const double2 di = V.d[row];
-            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_e, di));
-            const double2 wi = cvk_add(V.w[row], cvk_mul(nal, ai));
-            V.w[row] = wi;
-            V.d[row] = cvk_add(cvk_mul(coef, di), ui);
-            acc_norm(acc[0], wi);
-            acc_dot(acc[1], V.sh[row], wi);
-        }
+    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, uval, [&](int row, double2 y) {
+        const double2 ui = uval(row);
+        const double2 ai = prec_apply(a.dinv, row, y);
+        un[row] = ui;
+        V.au[row] = ai;
+        const double2 di = V.d[row];
+        a.x[row] = cvk_add(a.x[row], cvk_mul(eta_e, di));
+        const double2 wi = cvk_add(V.w[row], cvk_mul(nal, ai));
+        V.w[row] = wi;
+        V.d[row] = cvk_add(cvk_mul(coef, di), ui);
+        acc_norm(acc[0], wi);
+        acc_dot(acc[1], V.sh[row], wi);
     });
     double2 tot[2];
     if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
@@ -419,7 +404,6 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
 
 // odd tail: u_next = w + beta u; au_next = M^{-1} A u_next;
 // v = beta (beta v + au) + au_next; x += eta d; sigma = <shadow, v>
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     PState* st = a.st;
     if (st->done) return;
@@ -431,19 +415,16 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     const double2* __restrict__ w = V.w;
     auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-        const double2 y = row_sum<S, decltype(unext)&, kBatch>(a.A, row, lane, valid, unext);
-        if (valid && lane == 0) {
-            const double2 un_i = unext(row);
-            const double2 an = prec_apply(a.dinv, row, y);
-            un[row] = un_i;
-            double2 vi = cvk_add(cvk_mul(beta, V.v[row]), V.au[row]);
-            vi = cvk_add(cvk_mul(beta, vi), an);
-            V.v[row] = vi;
-            V.au[row] = an;
-            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_o, V.d[row]));
-            acc_dot(acc[0], V.sh[row], vi);
-        }
+    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, unext, [&](int row, double2 y) {
+        const double2 un_i = unext(row);
+        const double2 an = prec_apply(a.dinv, row, y);
+        un[row] = un_i;
+        double2 vi = cvk_add(cvk_mul(beta, V.v[row]), V.au[row]);
+        vi = cvk_add(cvk_mul(beta, vi), an);
+        V.v[row] = vi;
+        V.au[row] = an;
+        a.x[row] = cvk_add(a.x[row], cvk_mul(eta_o, V.d[row]));
+        acc_dot(acc[0], V.sh[row], vi);
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -464,7 +445,6 @@ __global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
 }
 
 // ------------------------------------------------- true residual + report
-template <int S>
 __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     PState* st = a.st;
     const int n = a.A.n;
@@ -472,15 +452,12 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     auto xat = [&](int c) -> double2 { return x[c]; };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
     if (!st->skip_true) {
-        for_rows<S>(n, gridDim.x, [&](int row, int lane, bool valid) {
-            const double2 y = row_sum<S, decltype(xat)&, kBatch>(a.A, row, lane, valid, xat);
-            if (valid && lane == 0) {
-                const double2 bi = __ldg(a.b + row);
-                const double2 d = cvk_sub(bi, y);
-                scratch[row] = d;
-                acc_norm(acc[0], bi);
-                acc_norm(acc[1], d);
-            }
+        spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, xat, [&](int row, double2 y) {
+            const double2 bi = __ldg(a.b + row);
+            const double2 d = cvk_sub(bi, y);
+            scratch[row] = d;
+            acc_norm(acc[0], bi);
+            acc_norm(acc[1], d);
         });
     }
     double2 tot[2];
@@ -500,40 +477,33 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     a.rep->error = 0;
 }
 
-template <int S>
-PhasedKernels kernels_for() {
+PhasedKernels kernels_all() {
     PhasedKernels k;
     k.bi_init = (const void*)k_bi_init;
-    k.bi_a = (const void*)k_bi_a<S>;
-    k.bi_b = (const void*)k_bi_b<S>;
+    k.bi_a = (const void*)k_bi_a;
+    k.bi_b = (const void*)k_bi_b;
     k.bi_c = (const void*)k_bi_c;
     k.tf_init = (const void*)k_tf_init;
-    k.tf_init2 = (const void*)k_tf_init2<S>;
+    k.tf_init2 = (const void*)k_tf_init2;
     k.tf_w = (const void*)k_tf_w;
-    k.tf_e = (const void*)k_tf_e<S>;
-    k.tf_o = (const void*)k_tf_o<S>;
+    k.tf_e = (const void*)k_tf_e;
+    k.tf_o = (const void*)k_tf_o;
     k.tf_fix = (const void*)k_tf_fix;
-    k.true_res = (const void*)k_true<S>;
+    k.true_res = (const void*)k_true;
     return k;
 }
 
 }  // namespace
 
-PhasedKernels phased_kernels(int S) {
-    switch (S) {
-        case 1: return kernels_for<1>();
-        case 2: return kernels_for<2>();
-        case 4: return kernels_for<4>();
-        case 8: return kernels_for<8>();
-        default: return kernels_for<16>();
-    }
-}
+PhasedKernels phased_kernels() { return kernels_all(); }
 
 size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep) {
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
+                      int tile) {
     PArgs* p = (PArgs*)out;
+    p->tile = tile;
     p->A = A;
     p->dinv = dinv;
     p->b = b;

@@ -27,9 +27,10 @@ struct PhasedKernels {
     const void* true_res;  // (PArgs, double2* scratch)
 };
 
-PhasedKernels phased_kernels(int S);
+PhasedKernels phased_kernels();
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep);
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
+                      int tile);
 
 }  // namespace cvk

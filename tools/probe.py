@@ -21,11 +21,16 @@ g = H.build_grid(2.4, 1.2, h, 0.4, 0.65, 0.01)
 t = time.time()
 prob = H.assemble(g, 2 * math.pi * 100.0, 340.0, np.ones(g.roof_size(), np.complex128))
 print(f"n={g.size()} nnz={prob.A.nnz()} assemble {time.time()-t:.2f}s", flush=True)
-for S in (1, 2, 4, 8):
+A = P.CsrMatrix(prob.A.nrows, prob.A.ncols, prob.A.row_offsets, prob.A.col_indices, prob.A.values)
+tt, gbs = spmv_gbs(A)
+print(f"spmv tiled: {tt*1e6:.1f} us  {gbs:.0f} GB/s", flush=True)
+os.environ["CVK_SPMV_ROWS"] = "1"
+for S in (1, 2, 4):
     os.environ["CVK_SPMV_GROUP"] = str(S)
     A = P.CsrMatrix(prob.A.nrows, prob.A.ncols, prob.A.row_offsets, prob.A.col_indices, prob.A.values)
     tt, gbs = spmv_gbs(A)
-    print(f"spmv S={S}: {tt*1e6:.1f} us  {gbs:.0f} GB/s", flush=True)
+    print(f"spmv rows S={S}: {tt*1e6:.1f} us  {gbs:.0f} GB/s", flush=True)
+del os.environ["CVK_SPMV_ROWS"]
 for S in (int(s) for s in os.environ.get("PROBE_SOLVE_S", "4").split(",")):
     os.environ["CVK_SPMV_GROUP"] = str(S)
     A = P.CsrMatrix(prob.A.nrows, prob.A.ncols, prob.A.row_offsets, prob.A.col_indices, prob.A.values)
