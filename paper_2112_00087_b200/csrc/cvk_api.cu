@@ -53,8 +53,7 @@ struct cvk_csr {
     int* rp = nullptr;
     int* ci = nullptr;
     double2* av = nullptr;
-    int group = 1;  // SpMV lanes per row for FAST mode (persistent kernels)
-    int tile = 1;   // spmv_tiled product tile: max entries of a 256-row chunk (capped)
+    int group = 1;  // SpMV lanes per row for FAST mode
 };
 
 struct cvk_prec {
@@ -87,10 +86,11 @@ int pick_group(double avg_nnz) {
         const int v = std::atoi(env);
         if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;
     }
-    if (avg_nnz <= 2.5) return 1;
-    if (avg_nnz <= 6.0) return 4;
-    if (avg_nnz <= 12.0) return 8;
-    return 16;
+    // thread per row with all of a row's loads issued up front wins up to
+    // ~16 entries per row (profiles/r01_spmv_lab.txt); lanes per row beyond
+    if (avg_nnz <= 16.0) return 1;
+    if (avg_nnz <= 48.0) return 4;
+    return 8;
 }
 
 int ensure(cvk_ctx* c, void** p, size_t* have, size_t need) {
@@ -242,14 +242,7 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     A->n = nrows;
     A->nnz = nnz;
     A->group = pick_group(nrows ? (double)nnz / (double)nrows : 1.0);
-    {
-        int mx = 1;
-        for (int64_t b = 0; b < nrows; b += cvk::kThreads) {
-            const int64_t e = std::min<int64_t>(b + cvk::kThreads, nrows);
-            mx = std::max(mx, rp[(size_t)e] - rp[(size_t)b]);
-        }
-        A->tile = std::min(mx, cvk::kMaxTile);
-    }
+
     CK(cudaMalloc(&A->rp, sizeof(int) * (rp.size())));
     CK(cudaMalloc(&A->ci, sizeof(int) * std::max<size_t>(1, ci.size())));
     CK(cudaMalloc(&A->av, sizeof(double2) * std::max<int64_t>(1, nnz)));
@@ -356,9 +349,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const int n = (int)A->n;
     const int S = A->group;
     const cvk::PhasedKernels K = cvk::phased_kernels();
-    const size_t smem = sizeof(double2) * (size_t)A->tile;
-    for (const void* kf : {K.bi_a, K.bi_b, K.tf_init2, K.tf_e, K.tf_o, K.true_res})
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    const size_t smem = 0;
     const void* heavy = solver == CVK_BICGSTAB ? K.bi_b : K.tf_e;
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy, cvk::kThreads, smem));
@@ -387,7 +378,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if (o->max_iter < 1) hs.max_iter = 0;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->tile);
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
@@ -606,7 +597,7 @@ int cvk_spmv_device(const cvk_csr* A, const double* x_dev, double* y_dev, int mo
     const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
     CK(cvk::launch_spmv(ref ? 1 : A->group, ref, (int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
-                        (double2*)y_dev, A->tile, c->stream));
+                        (double2*)y_dev, 0, c->stream));
     return CVK_OK;
 }
 

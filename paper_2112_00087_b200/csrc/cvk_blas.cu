@@ -25,13 +25,6 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restr
     });
 }
 
-// FAST SpMV: nnz-tiled chunks (one CTA per 256-row chunk)
-__global__ void __launch_bounds__(kThreads) k_spmv_tiled(Csr A, const double2* __restrict__ x,
-                                                         double2* __restrict__ y, int tile) {
-    auto xat = [&](int c) { return __ldg(x + c); };
-    spmv_tiled<4>(A, gridDim.x, tile, xat, [&](int row, double2 acc) { __stcs(y + row, acc); });
-}
-
 template <int S, bool REF>
 __global__ void __launch_bounds__(kThreads) k_residual(Csr A, const double2* __restrict__ b,
                                                        const double2* __restrict__ x,
@@ -120,14 +113,7 @@ cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, co
                         const double2* x, double2* y, int tile, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     if (ref) return spmv_t<1, true>(n, rp, ci, av, x, y, st);
-    if (tile > 0 && !std::getenv("CVK_SPMV_ROWS")) {
-        const size_t smem = sizeof(double2) * (size_t)tile;
-        cudaError_t e = cudaFuncSetAttribute(k_spmv_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        Csr A{n, rp, ci, av};
-        k_spmv_tiled<<<grid_for(n), kThreads, smem, st>>>(A, x, y, tile);
-        return cudaGetLastError();
-    }
+    (void)tile;
     switch (S) {
         case 1: return spmv_t<1, false>(n, rp, ci, av, x, y, st);
         case 2: return spmv_t<2, false>(n, rp, ci, av, x, y, st);

@@ -118,18 +118,12 @@ struct GridBar {
     }
 };
 
-// Streaming loads of the matrix (read once per SpMV: keep them out of L1).
-__device__ __forceinline__ double2 ld_stream(const double2* p) {
-    double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                 : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ int ld_stream(const int* p) {
-    int v;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
+// Matrix loads: read-only path, L1-allocating.  Adjacent rows share 32-byte
+// sectors of the value/column arrays, so L1::no_allocate refetches them from
+// L2 and measured 1.9 vs 5.4 TB/s on the 10M-DOF cavity (tools/spmv_lab.cu,
+// profiles/r01_spmv_lab.txt).
+__device__ __forceinline__ double2 ld_mat(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ int ld_mat(const int* p) { return __ldg(p); }
 
 // ---------------------------------------------------------------- loops --
 
@@ -180,8 +174,8 @@ __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool
             for (int u = 0; u < U; ++u) {
                 const int kk = k + u * S;
                 if (kk < e) {
-                    a[u] = ld_stream(A.av + kk);
-                    c[u] = ld_stream(A.ci + kk);
+                    a[u] = ld_mat(A.av + kk);
+                    c[u] = ld_mat(A.ci + kk);
                 }
             }
             double2 xv[U];
@@ -201,79 +195,6 @@ __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool
         }
     }
     return acc;
-}
-
-// nnz-tiled SpMV over the CTA's 256-row chunks (the phase kernels' SpMV).
-// Per chunk: row pointers -> shared; every thread loads the chunk's
-// (value, column) entries coalesced and independently of row boundaries,
-// gathers x(col) and stores the product in shared memory; then thread t sums
-// row base+t left to right from shared memory and runs epi(row, y).  The
-// row sum is therefore rounded exactly like the reference's row loop
-// (numkit.cpp:98-103) while the loads have no row-pointer dependency.  The
-// next chunk's row pointers are prefetched while the current one computes.
-// Chunks with more than `tile` entries fall back to thread-per-row.
-// epi is called for every row of the chunk by the thread that owns it in
-// for_elems, so elementwise and SpMV phases agree on row ownership.
-// Requires dynamic shared memory of tile * sizeof(double2).
-template <int U, class X, class E>
-__device__ __forceinline__ void spmv_tiled(const Csr& A, int G, int tile, X&& xat, E&& epi) {
-    extern __shared__ double2 prod[];
-    __shared__ int srp[kThreads + 1];
-    const int n = A.n;
-    const int t = threadIdx.x;
-    long long base = (long long)blockIdx.x * kThreads;
-    int rp_a = 0, rp_b = 0;
-    if (base < n) {
-        rp_a = __ldg(A.rp + (((base + t) < (long long)n) ? (base + t) : (long long)n));
-        if (t == 0) rp_b = __ldg(A.rp + (((base + kThreads) < (long long)n) ? (base + kThreads) : (long long)n));
-    }
-    for (; base < n; base += (long long)G * kThreads) {
-        srp[t] = rp_a;
-        if (t == 0) srp[kThreads] = rp_b;
-        __syncthreads();
-        const long long nb = base + (long long)G * kThreads;
-        if (nb < n) {  // prefetch the next chunk's row pointers
-            rp_a = __ldg(A.rp + (((nb + t) < (long long)n) ? (nb + t) : (long long)n));
-            if (t == 0) rp_b = __ldg(A.rp + (((nb + kThreads) < (long long)n) ? (nb + kThreads) : (long long)n));
-        }
-        const int k0 = srp[0];
-        const int cnt = srp[kThreads] - k0;
-        const long long row = base + t;
-        if (cnt <= tile) {
-            for (int k = t; k < cnt; k += U * kThreads) {
-                double2 a[U];
-                int c[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int kk = k + u * kThreads;
-                    if (kk < cnt) {
-                        a[u] = ld_stream(A.av + k0 + kk);
-                        c[u] = ld_stream(A.ci + k0 + kk);
-                    }
-                }
-                double2 xv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (k + u * kThreads < cnt) xv[u] = xat(c[u]);
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (k + u * kThreads < cnt) prod[k + u * kThreads] = cvk_mul(a[u], xv[u]);
-            }
-            __syncthreads();
-            if (row < n) {
-                double2 acc = make_double2(0.0, 0.0);
-                const int e = srp[t + 1] - k0;
-                for (int k = srp[t] - k0; k < e; ++k) acc = cvk_add(acc, prod[k]);
-                epi((int)row, acc);
-            }
-        } else if (row < n) {
-            double2 acc = make_double2(0.0, 0.0);
-            for (int k = srp[t]; k < srp[t + 1]; ++k)
-                acc = cvk_add(acc, cvk_mul(ld_stream(A.av + k), xat(ld_stream(A.ci + k))));
-            epi((int)row, acc);
-        }
-        __syncthreads();
-    }
 }
 
 // ----------------------------------------------------------- reductions --

@@ -10,7 +10,6 @@
 namespace cvk {
 
 constexpr int kMaxL = 16;     // BiCGSTAB(l): l <= kMaxL
-constexpr int kMaxTile = 6144; // spmv_tiled: <= 96 KB of shared products per CTA
 
 struct Csr;
 struct DevReport;
@@ -21,7 +20,6 @@ int solver_nwork(int solver, int l, int m);
 size_t solver_smem(int solver, int m);
 
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
-// FAST: nnz-tiled (tile = max chunk entries, <= kMaxTile); REF: thread per row
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);
 cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,

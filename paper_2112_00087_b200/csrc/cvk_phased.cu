@@ -27,7 +27,7 @@ namespace cvk {
 
 namespace {
 
-constexpr int kBatch = 4;  // (value, column) loads in flight per thread per round
+constexpr int kBatch = 8;  // (value, column) loads issued up front per row (thread per row)
 
 struct PArgs {
     Csr A;
@@ -39,7 +39,6 @@ struct PArgs {
     PState* st;
     double* hist;
     DevReport* rep;
-    int tile;  // shared-memory product tile (entries) of spmv_tiled
 };
 
 __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
@@ -166,11 +165,14 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
         return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
     };
     double2 acc[1] = {make_double2(0, 0)};
-    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, pnew, [&](int row, double2 y) {
-        const double2 vi = prec_apply(a.dinv, row, y);
-        pn[row] = pnew(row);
-        vn[row] = vi;
-        acc_dot(acc[0], sh[row], vi);
+    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(pnew)&, kBatch>(a.A, row, 0, valid, pnew);
+        if (valid) {
+            const double2 vi = prec_apply(a.dinv, row, y);
+            pn[row] = pnew(row);
+            vn[row] = vi;
+            acc_dot(acc[0], sh[row], vi);
+        }
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -197,15 +199,18 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     double2* __restrict__ x = a.x;
     auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
     double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, sval, [&](int row, double2 y) {
-        const double2 ti = prec_apply(a.dinv, row, y);
-        const double2 si = sval(row);
-        s[row] = si;
-        t[row] = ti;
-        x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
-        acc_norm(acc[0], si);
-        acc_dot(acc[1], ti, ti);
-        acc_dot(acc[2], ti, si);
+    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(sval)&, kBatch>(a.A, row, 0, valid, sval);
+        if (valid) {
+            const double2 ti = prec_apply(a.dinv, row, y);
+            const double2 si = sval(row);
+            s[row] = si;
+            t[row] = ti;
+            x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
+            acc_norm(acc[0], si);
+            acc_dot(acc[1], ti, ti);
+            acc_dot(acc[2], ti, si);
+        }
     });
     double2 tot[3];
     if (!partial_last<3>(acc, partv(a, 2), &st->counter[2], tot)) return;
@@ -311,11 +316,14 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     const double2* __restrict__ u0 = V.u0;
     auto uat = [&](int c) -> double2 { return u0[c]; };
     double2 acc[1] = {make_double2(0, 0)};
-    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, uat, [&](int row, double2 y) {
-        const double2 ai = prec_apply(a.dinv, row, y);
-        V.au[row] = ai;
-        V.v[row] = ai;
-        acc_dot(acc[0], V.sh[row], ai);
+    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(uat)&, kBatch>(a.A, row, 0, valid, uat);
+        if (valid) {
+            const double2 ai = prec_apply(a.dinv, row, y);
+            V.au[row] = ai;
+            V.v[row] = ai;
+            acc_dot(acc[0], V.sh[row], ai);
+        }
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -369,18 +377,21 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     const double2* __restrict__ vv = V.v;
     auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, uval, [&](int row, double2 y) {
-        const double2 ui = uval(row);
-        const double2 ai = prec_apply(a.dinv, row, y);
-        un[row] = ui;
-        V.au[row] = ai;
-        const double2 di = V.d[row];
-        a.x[row] = cvk_add(a.x[row], cvk_mul(eta_e, di));
-        const double2 wi = cvk_add(V.w[row], cvk_mul(nal, ai));
-        V.w[row] = wi;
-        V.d[row] = cvk_add(cvk_mul(coef, di), ui);
-        acc_norm(acc[0], wi);
-        acc_dot(acc[1], V.sh[row], wi);
+    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(uval)&, kBatch>(a.A, row, 0, valid, uval);
+        if (valid) {
+            const double2 ui = uval(row);
+            const double2 ai = prec_apply(a.dinv, row, y);
+            un[row] = ui;
+            V.au[row] = ai;
+            const double2 di = V.d[row];
+            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_e, di));
+            const double2 wi = cvk_add(V.w[row], cvk_mul(nal, ai));
+            V.w[row] = wi;
+            V.d[row] = cvk_add(cvk_mul(coef, di), ui);
+            acc_norm(acc[0], wi);
+            acc_dot(acc[1], V.sh[row], wi);
+        }
     });
     double2 tot[2];
     if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
@@ -415,16 +426,19 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     const double2* __restrict__ w = V.w;
     auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
     double2 acc[1] = {make_double2(0, 0)};
-    spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, unext, [&](int row, double2 y) {
-        const double2 un_i = unext(row);
-        const double2 an = prec_apply(a.dinv, row, y);
-        un[row] = un_i;
-        double2 vi = cvk_add(cvk_mul(beta, V.v[row]), V.au[row]);
-        vi = cvk_add(cvk_mul(beta, vi), an);
-        V.v[row] = vi;
-        V.au[row] = an;
-        a.x[row] = cvk_add(a.x[row], cvk_mul(eta_o, V.d[row]));
-        acc_dot(acc[0], V.sh[row], vi);
+    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(unext)&, kBatch>(a.A, row, 0, valid, unext);
+        if (valid) {
+            const double2 un_i = unext(row);
+            const double2 an = prec_apply(a.dinv, row, y);
+            un[row] = un_i;
+            double2 vi = cvk_add(cvk_mul(beta, V.v[row]), V.au[row]);
+            vi = cvk_add(cvk_mul(beta, vi), an);
+            V.v[row] = vi;
+            V.au[row] = an;
+            a.x[row] = cvk_add(a.x[row], cvk_mul(eta_o, V.d[row]));
+            acc_dot(acc[0], V.sh[row], vi);
+        }
     });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
@@ -452,12 +466,15 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     auto xat = [&](int c) -> double2 { return x[c]; };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
     if (!st->skip_true) {
-        spmv_tiled<kBatch>(a.A, gridDim.x, a.tile, xat, [&](int row, double2 y) {
-            const double2 bi = __ldg(a.b + row);
-            const double2 d = cvk_sub(bi, y);
-            scratch[row] = d;
-            acc_norm(acc[0], bi);
-            acc_norm(acc[1], d);
+        for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+            const double2 y = row_sum<1, decltype(xat)&, kBatch>(a.A, row, 0, valid, xat);
+            if (valid) {
+                const double2 bi = __ldg(a.b + row);
+                const double2 d = cvk_sub(bi, y);
+                scratch[row] = d;
+                acc_norm(acc[0], bi);
+                acc_norm(acc[1], d);
+            }
         });
     }
     double2 tot[2];
@@ -500,10 +517,8 @@ PhasedKernels phased_kernels() { return kernels_all(); }
 size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int tile) {
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep) {
     PArgs* p = (PArgs*)out;
-    p->tile = tile;
     p->A = A;
     p->dinv = dinv;
     p->b = b;

@@ -30,7 +30,6 @@ struct PhasedKernels {
 PhasedKernels phased_kernels();
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int tile);
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep);
 
 }  // namespace cvk
