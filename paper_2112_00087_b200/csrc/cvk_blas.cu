@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restr
     const int G = gridDim.x;
     for_rows<S>(A.n, G, [&](int row, int lane, bool valid) {
         auto xat = [&](int c) { return __ldg(x + c); };
-        const double2 acc = row_sum<S, decltype(xat)&, (REF ? 1 : 8)>(A, row, lane, valid, xat);
+        const double2 acc = row_sum<S, decltype(xat)&, (REF ? 1 : 5)>(A, row, lane, valid, xat);
         if (valid && lane == 0) __stcs(y + row, acc);
     });
 }

@@ -156,11 +156,10 @@ __device__ __forceinline__ void for_rows(int n, int G, F&& f) {
 // the S lane sums are combined by a fixed xor tree (all lanes get the sum).
 // With S == 1 this is exactly the reference's row loop (numkit.cpp:98-103).
 //
-// With BATCH > 1 loads are batched: each lane first issues up to U = BATCH/S
-// (value, column) loads,
-// then all U gathers, then accumulates -- the col -> x[col] dependency chain
-// is paid once per batch instead of once per entry (memory-level
-// parallelism; the accumulation order per lane is unchanged).
+// With BATCH > 1 each lane first issues up to U = BATCH/S (value, column)
+// loads, then the U gathers -- the row_ptr -> col -> x[col] chain is paid
+// once per batch instead of once per entry, at a register cost small enough
+// to keep full occupancy (the accumulation order per lane is unchanged).
 template <int S, class X, int BATCH = 1>
 __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool valid, X&& xat) {
     constexpr int U = (BATCH / S) > 0 ? (BATCH / S) : 1;
@@ -178,13 +177,9 @@ __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool
                     c[u] = ld_mat(A.ci + kk);
                 }
             }
-            double2 xv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (k + u * S < e) xv[u] = xat(c[u]);
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (k + u * S < e) acc = cvk_add(acc, cvk_mul(a[u], xv[u]));
+                if (k + u * S < e) acc = cvk_add(acc, cvk_mul(a[u], xat(c[u])));
         }
     }
     if (S > 1) {

@@ -27,7 +27,7 @@ namespace cvk {
 
 namespace {
 
-constexpr int kBatch = 8;  // (value, column) loads issued up front per row (thread per row)
+constexpr int kBatch = 5;  // (value, column) loads issued up front per row (thread per row)
 
 struct PArgs {
     Csr A;
