@@ -355,7 +355,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy, cvk::kThreads, smem));
     if (per_sm < 1) per_sm = 1;
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
-    long long G = std::min<long long>((long long)per_sm * c->nsm, chunks);
+    // one 256-row chunk per CTA up to kChunkCtasCap CTAs (hardware scheduling
+    // keeps the memory pipes full), grid-stride beyond that
+    long long cap = 32LL * per_sm * c->nsm;
+    if (const char* env = std::getenv("CVK_PHASED_GRID")) cap = std::max(1LL, std::atoll(env)) * per_sm * c->nsm;
+    long long G = std::min<long long>(cap, chunks);
     if (const char* env = std::getenv("CVK_MAX_CTAS")) G = std::min<long long>(G, std::max(1, std::atoi(env)));
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 8 * (size_t)std::max(1, n))) != CVK_OK) return e;

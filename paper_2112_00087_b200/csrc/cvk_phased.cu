@@ -41,8 +41,10 @@ struct PArgs {
     DevReport* rep;
 };
 
+constexpr int kPhSlots = 4;  // reduction slots per phase (max K used is 3)
+
 __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
-    return a.part + (size_t)k * kMaxSlots * gridDim.x;
+    return a.part + (size_t)k * kPhSlots * gridDim.x;
 }
 
 // Write this CTA's K partials; returns true in the CTA that arrived last,
