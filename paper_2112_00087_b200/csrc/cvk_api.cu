@@ -344,6 +344,21 @@ static long long phased_min_n() {
     return 131072;
 }
 
+// cudaLaunchKernel with the programmatic-stream-serialization attribute (PDL)
+static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("CVK_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, f, args);
+}
+
 static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                         const double2* b_dev, double2* x_dev, cvk_report* rep) {
     const int n = (int)A->n;
@@ -399,13 +414,13 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < kIterPerGraph; ++it) {
             if (solver == CVK_BICGSTAB) {
-                cudaLaunchKernel(K.bi_a, grid, block, args, smem, c->stream);
-                cudaLaunchKernel(K.bi_b, grid, block, args, smem, c->stream);
-                cudaLaunchKernel(K.bi_c, grid, block, args, 0, c->stream);
+                launch_pdl(K.bi_a, grid, block, args, smem, c->stream);
+                launch_pdl(K.bi_b, grid, block, args, smem, c->stream);
+                launch_pdl(K.bi_c, grid, block, args, 0, c->stream);
             } else {
-                cudaLaunchKernel(K.tf_w, grid, block, args, 0, c->stream);
-                cudaLaunchKernel(K.tf_e, grid, block, args, smem, c->stream);
-                cudaLaunchKernel(K.tf_o, grid, block, args, smem, c->stream);
+                launch_pdl(K.tf_w, grid, block, args, 0, c->stream);
+                launch_pdl(K.tf_e, grid, block, args, smem, c->stream);
+                launch_pdl(K.tf_o, grid, block, args, smem, c->stream);
             }
         }
         CK(cudaStreamEndCapture(c->stream, &graph));
@@ -417,11 +432,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     CK(cudaEventRecord(c->e0, c->stream));
     long long launches = 0;
     if (solver == CVK_BICGSTAB) {
-        CK(cudaLaunchKernel(K.bi_init, grid, block, args, 0, c->stream));
+        CK(launch_pdl(K.bi_init, grid, block, args, 0, c->stream));
         launches += 1;
     } else {
-        CK(cudaLaunchKernel(K.tf_init, grid, block, args, 0, c->stream));
-        CK(cudaLaunchKernel(K.tf_init2, grid, block, args, smem, c->stream));
+        CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
+        CK(launch_pdl(K.tf_init2, grid, block, args, smem, c->stream));
         launches += 2;
     }
     long long graphs = 0;
@@ -441,10 +456,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         }
     }
     if (solver == CVK_TFQMR) {
-        CK(cudaLaunchKernel(K.tf_fix, grid, block, args, 0, c->stream));
+        CK(launch_pdl(K.tf_fix, grid, block, args, 0, c->stream));
         launches += 1;
     }
-    CK(cudaLaunchKernel(K.true_res, grid, block, targs, smem, c->stream));
+    CK(launch_pdl(K.true_res, grid, block, targs, smem, c->stream));
     launches += 1;
     CK(cudaEventRecord(c->e1, c->stream));
     cvk::DevReport dr;

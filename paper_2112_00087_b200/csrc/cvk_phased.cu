@@ -91,6 +91,14 @@ __device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* c
     return true;
 }
 
+// Programmatic dependent launch: the successor kernel is launched while this
+// one drains; it blocks here until this grid has completed and its memory is
+// visible, so launch latency and CTA rasterisation overlap the tail.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void st_hist(const PArgs& a, PState* st, double v) {
     if (!st->record) return;
     if (st->hist_len < st->hist_cap) a.hist[st->hist_len] = v;
@@ -117,7 +125,8 @@ __device__ void bi_top(PState* st) {
     st->rho = st->rho_new;
 }
 
-__global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 5) k_bi_init(PArgs a) {
+    pdl_enter();
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
@@ -147,7 +156,8 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     bi_top(st);
 }
 
-__global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_bi_a(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -186,7 +196,8 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
     st->alpha = cvk_cdiv(st->rho, tot[0]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_bi_b(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -230,7 +241,8 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     st->omega = cvk_cdiv(tot[2], tot[1]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) k_bi_c(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -281,7 +293,8 @@ __device__ void tf_even_head(PState* st, double2 sigma) {
     st->alpha = cvk_cdiv(st->rho, sigma);
 }
 
-__global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 5) k_tf_init(PArgs a) {
+    pdl_enter();
     const int n = a.A.n;
     TfVecs V(a.work, (size_t)n);
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
@@ -310,7 +323,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
 }
 
 // au = M^{-1} A u0, v = au, sigma = <shadow, v>
-__global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_tf_init2(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -334,7 +348,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
 }
 
 // even half-step body: w -= alpha au; d = coef d + u; ||w||
-__global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) k_tf_w(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -366,7 +381,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
 
 // even tail + odd head: u' = u - alpha v; au = M^{-1} A u'; x += eta d;
 // w -= alpha au; d = coef d + u'; ||w||, <shadow, w>
-__global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_tf_e(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -417,7 +433,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
 
 // odd tail: u_next = w + beta u; au_next = M^{-1} A u_next;
 // v = beta (beta v + au) + au_next; x += eta d; sigma = <shadow, v>
-__global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_tf_o(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (st->done) return;
     const int n = a.A.n;
@@ -452,7 +469,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
 }
 
 // owed x += eta d after a tfQMR exit (krylov.cpp:335)
-__global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
+__global__ void __launch_bounds__(kThreads, 6) k_tf_fix(PArgs a) {
+    pdl_enter();
     PState* st = a.st;
     if (!st->pending_x) return;
     TfVecs V(a.work, (size_t)a.A.n);
@@ -461,7 +479,8 @@ __global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
 }
 
 // ------------------------------------------------- true residual + report
-__global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
+__global__ void __launch_bounds__(kThreads, 4) k_true(PArgs a, double2* scratch) {
+    pdl_enter();
     PState* st = a.st;
     const int n = a.A.n;
     const double2* __restrict__ x = a.x;

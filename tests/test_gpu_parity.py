@@ -247,3 +247,47 @@ def test_ladder_iterations_grow(cvk, oracle):
             assert r.report.converged and r.report.true_relres <= 1e-8
             assert r.report.iterations >= prev
             prev = r.report.iterations
+
+
+@pytest.fixture(params=["persistent", "phased"])
+def fast_path(request, monkeypatch):
+    """Run a FAST-mode test on both device paths: the persistent cooperative
+    kernel (small systems) and the phase-kernel graph path (large systems)."""
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0" if request.param == "phased" else "1000000000")
+    return request.param
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "tfqmr"])
+def test_fast_paths_agree_with_reference(cvk, oracle, golden, fast_path, solver):
+    P = cvk
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    x_tight, _ = oracle.solve(solver, rp, ci, v, b, tol=1e-12)
+    r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-12, record_history=True))
+    assert r.report.converged and r.report.final_relres <= 1e-12
+    assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
+    assert len(r.report.residual_history) >= r.report.iterations - 1
+    assert abs(r.report.true_relres - oracle.true_relres(rp, ci, v, b, r.x)) <= 1e-3 * r.report.true_relres + 1e-15
+    _, ro = oracle.solve(solver, rp, ci, v, b, tol=1e-9)
+    r9 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    assert r9.report.converged
+    assert abs(r9.report.iterations - ro.iterations) <= max(2, 0.15 * ro.iterations)
+    # exhaustion, zero rhs, determinism
+    e = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(max_iter=3))
+    assert not e.report.converged and e.report.iterations <= 3
+    z = P.solve(P.solver_from_name(solver), A, np.zeros_like(b), M)
+    assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
+    r2 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    assert np.array_equal(bits(r2.x), bits(r9.x))
+
+
+def test_fast_paths_diagonal_kat(cvk, fast_path):
+    P = cvk
+    n = 12
+    rng = np.random.default_rng(1)
+    D = P.csr_from_triplets(np.arange(n), np.arange(n), [complex(1 + i, 0.5 * i) for i in range(n)], n, n)
+    b = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    for s in ("bicgstab", "tfqmr"):
+        r = P.solve(P.solver_from_name(s), D, b, P.jacobi(D))
+        assert r.report.converged and r.report.iterations == 1 and r.report.true_relres <= 1e-12
