@@ -53,6 +53,8 @@ struct cvk_csr {
     int* rp = nullptr;
     int* ci = nullptr;
     double2* av = nullptr;
+    void* blob = nullptr;  // av | ci | rp in one allocation
+    size_t blob_bytes = 0;
     int group = 1;  // SpMV lanes per row for FAST mode
 };
 
@@ -243,9 +245,16 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     A->nnz = nnz;
     A->group = pick_group(nrows ? (double)nnz / (double)nrows : 1.0);
 
-    CK(cudaMalloc(&A->rp, sizeof(int) * (rp.size())));
-    CK(cudaMalloc(&A->ci, sizeof(int) * std::max<size_t>(1, ci.size())));
-    CK(cudaMalloc(&A->av, sizeof(double2) * std::max<int64_t>(1, nnz)));
+    // one allocation [values | columns | row offsets] so a single L2
+    // access-policy window can pin the whole matrix (solve-time persistence)
+    const size_t vb = sizeof(double2) * (size_t)std::max<int64_t>(1, nnz);
+    const size_t cb = (sizeof(int) * (size_t)std::max<int64_t>(1, nnz) + 255) & ~(size_t)255;
+    const size_t rb = sizeof(int) * rp.size();
+    CK(cudaMalloc(&A->blob, vb + cb + rb));
+    A->blob_bytes = vb + cb + rb;
+    A->av = (double2*)A->blob;
+    A->ci = (int*)((char*)A->blob + vb);
+    A->rp = (int*)((char*)A->blob + vb + cb);
     CK(cudaMemcpyAsync(A->rp, rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice, c->stream));
     if (nnz) {
         CK(cudaMemcpyAsync(A->ci, ci.data(), sizeof(int) * ci.size(), cudaMemcpyHostToDevice, c->stream));
@@ -269,9 +278,7 @@ int cvk_csr_free(cvk_csr* A) {
     if (!A) return CVK_OK;
     cudaSetDevice(A->ctx->device);
     cudaStreamSynchronize(A->ctx->stream);
-    cudaFree(A->rp);
-    cudaFree(A->ci);
-    cudaFree(A->av);
+    cudaFree(A->blob);
     delete A;
     return CVK_OK;
 }
@@ -344,6 +351,35 @@ static long long phased_min_n() {
     return 131072;
 }
 
+// Pin the matrix in L2 for the duration of a solve: every Krylov iteration
+// re-reads A twice, and on B200 up to the persisting-L2 limit of it can stay
+// resident across iterations while the vectors stream (CVK_L2_PERSIST=0
+// disables).  Returns true if a window was set.
+static bool l2_pin(cvk_ctx* c, const cvk_csr* A) {
+    if (const char* env = std::getenv("CVK_L2_PERSIST"))
+        if (std::atoi(env) == 0) return false;
+    int maxwin = 0, maxpers = 0;
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+    if (maxwin <= 0 || maxpers <= 0) return false;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxpers) != cudaSuccess) return false;
+    const size_t win = std::min<size_t>(A->blob_bytes, (size_t)maxwin);
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = A->blob;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxpers / (double)win);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    return cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+}
+
+static void l2_unpin(cvk_ctx* c) {
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+}
+
 // cudaLaunchKernel with the programmatic-stream-serialization attribute (PDL)
 static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
@@ -360,7 +396,7 @@ static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args,
 }
 
 static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
-                        const double2* b_dev, double2* x_dev, cvk_report* rep) {
+                        const double2* b_dev, double2* x_dev, cvk_report* rep, bool pinned) {
     const int n = (int)A->n;
     const int S = A->group;
     const cvk::PhasedKernels K = cvk::phased_kernels();
@@ -406,6 +442,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     std::vector<unsigned char> key(blob);
     key.push_back((unsigned char)solver);
     key.push_back((unsigned char)S);
+    key.push_back((unsigned char)(pinned ? 1 : 0));  // captured nodes carry the L2 window
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
     if (!c->gexec || c->gkey != key) {
@@ -500,8 +537,12 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     const int mode = resolve_mode(c, o->mode);
     const bool ref = mode == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
-    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n())
-        return solve_phased(c, solver, A, M, o, b_dev, x_dev, rep);
+    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n()) {
+        const bool pinned = l2_pin(c, A);
+        const int rc = solve_phased(c, solver, A, M, o, b_dev, x_dev, rep, pinned);
+        if (pinned) l2_unpin(c);
+        return rc;
+    }
     const int S = ref ? 1 : A->group;
     const void* kern = cvk::solver_kernel(solver, S, ref);
     if (!kern) return fail(CVK_ELOGIC, "no kernel for this configuration");
