@@ -351,13 +351,13 @@ static long long phased_min_n() {
     return 131072;
 }
 
-// Pin the matrix in L2 for the duration of a solve: every Krylov iteration
-// re-reads A twice, and on B200 up to the persisting-L2 limit of it can stay
-// resident across iterations while the vectors stream (CVK_L2_PERSIST=0
-// disables).  Returns true if a window was set.
+// Optional (CVK_L2_PERSIST=1): pin the matrix in L2 for the duration of a
+// solve.  Measured on the 1M-DOF cavity it is SLOWER (201 vs 177 us per
+// BiCGSTAB iteration): the persisting carve-out starves the eight streamed
+// work vectors, so it is off by default.  Returns true if a window was set.
 static bool l2_pin(cvk_ctx* c, const cvk_csr* A) {
-    if (const char* env = std::getenv("CVK_L2_PERSIST"))
-        if (std::atoi(env) == 0) return false;
+    const char* env = std::getenv("CVK_L2_PERSIST");
+    if (!env || std::atoi(env) == 0) return false;
     int maxwin = 0, maxpers = 0;
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
     cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c->device);

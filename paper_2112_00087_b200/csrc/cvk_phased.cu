@@ -125,7 +125,7 @@ __device__ void bi_top(PState* st) {
     st->rho = st->rho_new;
 }
 
-__global__ void __launch_bounds__(kThreads, 5) k_bi_init(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_bi_init(PArgs a) {
     bi_top(st);
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_bi_a(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_bi_a(PArgs a) {
     st->alpha = cvk_cdiv(st->rho, tot[0]);
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_bi_b(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_bi_b(PArgs a) {
     st->omega = cvk_cdiv(tot[2], tot[1]);
 }
 
-__global__ void __launch_bounds__(kThreads, 6) k_bi_c(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -293,7 +293,7 @@ __device__ void tf_even_head(PState* st, double2 sigma) {
     st->alpha = cvk_cdiv(st->rho, sigma);
 }
 
-__global__ void __launch_bounds__(kThreads, 5) k_tf_init(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     TfVecs V(a.work, (size_t)n);
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_tf_init(PArgs a) {
 }
 
 // au = M^{-1} A u0, v = au, sigma = <shadow, v>
-__global__ void __launch_bounds__(kThreads, 4) k_tf_init2(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tf_init2(PArgs a) {
 }
 
 // even half-step body: w -= alpha au; d = coef d + u; ||w||
-__global__ void __launch_bounds__(kThreads, 6) k_tf_w(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_tf_w(PArgs a) {
 
 // even tail + odd head: u' = u - alpha v; au = M^{-1} A u'; x += eta d;
 // w -= alpha au; d = coef d + u'; ||w||, <shadow, w>
-__global__ void __launch_bounds__(kThreads, 4) k_tf_e(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tf_e(PArgs a) {
 
 // odd tail: u_next = w + beta u; au_next = M^{-1} A u_next;
 // v = beta (beta v + au) + au_next; x += eta d; sigma = <shadow, v>
-__global__ void __launch_bounds__(kThreads, 4) k_tf_o(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tf_o(PArgs a) {
 }
 
 // owed x += eta d after a tfQMR exit (krylov.cpp:335)
-__global__ void __launch_bounds__(kThreads, 6) k_tf_fix(PArgs a) {
+__global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (!st->pending_x) return;
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_tf_fix(PArgs a) {
 }
 
 // ------------------------------------------------- true residual + report
-__global__ void __launch_bounds__(kThreads, 4) k_true(PArgs a, double2* scratch) {
+__global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     pdl_enter();
     PState* st = a.st;
     const int n = a.A.n;
