@@ -159,6 +159,46 @@ int cvk_axpy(cvk_ctx *ctx, int64_t n, const double *alpha, const double *x, doub
 int cvk_xpay(cvk_ctx *ctx, int64_t n, const double *alpha, double *x, const double *y);
 int cvk_true_relres(const cvk_csr *A, const double *b, const double *x, double *out, int mode);
 
+/* ---- Schwarz domain decomposition (schwarz.hpp:16-58) ---- */
+
+/* CavityGrid (helmholtz.hpp:18-39): interior nodes, node = iy * nx + ix */
+typedef struct {
+    double width, height, h;
+    int64_t nx, ny, roof_begin, roof_end;
+    double admittance_re, admittance_im;
+} cvk_grid;
+
+/* DdmReport (schwarz.hpp:35-40) */
+typedef struct {
+    int64_t outer_iterations;
+    int32_t converged;
+    int32_t inner_breakdown;
+    double *jump_history;        /* caller-owned, may be NULL */
+    int64_t jump_cap;
+    int64_t jump_len;
+    cvk_report *sub_reports;     /* last sweep's per-subdomain reports (caller-owned) */
+    int64_t n_sub_reports;
+    int64_t total_inner_iterations; /* last sweep, summed over subdomains */
+    double device_time_s;
+    double wall_time_s;
+    int64_t kernel_launches;
+} cvk_ddm_report;
+
+/* partition (schwarz.cpp:93-109): col_begin receives n_sub + 1 entries */
+int cvk_partition(int64_t nx, int64_t n_sub, int64_t *col_begin);
+
+/* schwarz_solve (schwarz.cpp:111-238) on one device: host system (the
+ * reference's HelmholtzProblem A, b on `grid`), strips col_begin[n_sub+1],
+ * Robin coefficients s_left / s_right (complex, 2 doubles each); the inner
+ * solves of all strips run batched in one cooperative launch per sweep.
+ * inner->mode selects REF (bitwise reference) or FAST arithmetic. */
+int cvk_schwarz_solve(cvk_ctx *ctx, const cvk_grid *grid, double c, int64_t n, int64_t nnz,
+                      const uint64_t *row_offsets, const uint64_t *col_indices,
+                      const double *values, const double *b, int64_t n_sub,
+                      const int64_t *col_begin, const double *s_left, const double *s_right,
+                      const cvk_opts *inner, double ddm_tol, int64_t max_outer, int inner_solver,
+                      double *x, cvk_ddm_report *rep);
+
 /* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
  * device buffers, returns the average kernel time in seconds ---- */
 int cvk_spmv_bench(const cvk_csr *A, const double *x_dev, double *y_dev, int mode,

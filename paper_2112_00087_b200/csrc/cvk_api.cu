@@ -117,6 +117,8 @@ double now_s() {
 
 }  // namespace
 
+int cvk_fail(int code, const std::string& msg) { return fail(code, msg); }
+
 extern "C" {
 
 int cvk_abi_version(void) { return CVK_ABI_VERSION; }
@@ -587,6 +589,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     a.m = (int)o->m;
     a.record = o->record_history ? 1 : 0;
     a.G = (int)G;
+    a.cta_base = 0;
     void* args[] = {&a};
     CK(cudaEventRecord(c->e0, c->stream));
     CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kThreads), args, smem, c->stream));
@@ -801,3 +804,41 @@ int cvk_true_relres(const cvk_csr* A, const double* b, const double* x, double* 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------- DDM support (cvk_ddm.cu)
+
+extern "C" void* cvk_ddm_stream(cvk_ctx* c) { return c->stream; }
+
+extern "C" int cvk_ddm_ctas(cvk_ctx* c, int solver, int mode, size_t smem, int* total) {
+    const void* k = cvk::solver_kernel(solver, 1, mode == CVK_MODE_REF, true);
+    if (!k) return fail(CVK_ELOGIC, "no batched kernel");
+    CK(cudaSetDevice(c->device));
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, cvk::kThreads, smem));
+    *total = per_sm * c->nsm;
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_launch_batched(cvk_ctx* c, int solver, int mode, const void* segs, int nseg,
+                                      int total_ctas, size_t smem, float* ms) {
+    const void* k = cvk::solver_kernel(solver, 1, mode == CVK_MODE_REF, true);
+    void* args[] = {(void*)&segs, &nseg};
+    CK(cudaLaunchCooperativeKernel(k, dim3((unsigned)total_ctas), dim3(cvk::kThreads), args, smem, c->stream));
+    (void)ms;
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_single(cvk_ctx* c, int64_t n, int64_t nnz, const uint64_t* rp, const uint64_t* ci,
+                              const double* v, const double* b, const cvk_opts* inner, int solver, double* x,
+                              cvk_report* rep) {
+    cvk_csr* A = nullptr;
+    int e = cvk_csr_upload(c, n, n, nnz, rp, ci, v, &A);
+    if (e != CVK_OK) return e;
+    cvk_prec* M = nullptr;
+    e = cvk_precond_jacobi(A, nullptr, &M);
+    if (e == CVK_OK) e = cvk_solve(c, solver, A, M, inner, b, x, rep);
+    cvk_precond_free(M);
+    cvk_csr_free(A);
+    return e;
+}

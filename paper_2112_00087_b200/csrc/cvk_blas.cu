@@ -18,7 +18,7 @@ template <int S, bool REF>
 __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restrict__ x,
                                                    double2* __restrict__ y) {
     const int G = gridDim.x;
-    for_rows<S>(A.n, G, [&](int row, int lane, bool valid) {
+    for_rows<S>(A.n, G, blockIdx.x, [&](int row, int lane, bool valid) {
         auto xat = [&](int c) { return __ldg(x + c); };
         const double2 acc = row_sum<S, decltype(xat)&, (REF ? 1 : 5)>(A, row, lane, valid, xat);
         if (valid && lane == 0) __stcs(y + row, acc);
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(Csr A, const double2* __r
                                                        const double2* __restrict__ x,
                                                        double2* __restrict__ r) {
     const int G = gridDim.x;
-    for_rows<S>(A.n, G, [&](int row, int lane, bool valid) {
+    for_rows<S>(A.n, G, blockIdx.x, [&](int row, int lane, bool valid) {
         const double2 acc = row_sum<S>(A, row, lane, valid, [&](int c) { return __ldg(x + c); });
         if (valid && lane == 0) r[row] = cvk_sub(__ldg(b + row), acc);
     });
@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(kThreads) k_dot_stage1(int n, const double2* _
                                                          const double2* __restrict__ y,
                                                          double2* __restrict__ part) {
     double2 acc[1] = {make_double2(0.0, 0.0)};
-    for_elems(n, gridDim.x, [&](int i) {
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 xi = __ldg(x + i);
         if (y) acc_dot(acc[0], xi, __ldg(y + i));
         else acc_norm(acc[0], xi);
     });
-    cta_partial<1>(acc, part, gridDim.x);
+    cta_partial<1>(acc, part, gridDim.x, blockIdx.x);
 }
 
 __global__ void k_dot_stage2(const double2* __restrict__ part, int G, double2* out) {

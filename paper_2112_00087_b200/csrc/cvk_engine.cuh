@@ -67,6 +67,7 @@ struct KArgs {
     int m;
     int record;
     int G;
+    int cta_base;  // first CTA of this solve in a batched launch
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -87,7 +88,10 @@ struct GridBar {
     unsigned long long target;
     unsigned G;
 
-    __device__ GridBar(unsigned long long* b, int g) : bar(b), target(0), G((unsigned)g) {}
+    int cta;  // CTA index within this grid (or within a batched segment)
+
+    __device__ GridBar(unsigned long long* b, int g, int cta_ = -1)
+        : bar(b), target(0), G((unsigned)g), cta(cta_ < 0 ? (int)blockIdx.x : cta_) {}
 
     // returns false if the barrier was aborted (timeout anywhere in the grid)
     __device__ bool sync() {
@@ -129,8 +133,8 @@ __device__ __forceinline__ int ld_mat(const int* p) { return __ldg(p); }
 
 // Element loop over the CTA's chunks: f(i) for every owned row i < n.
 template <class F>
-__device__ __forceinline__ void for_elems(int n, int G, F&& f) {
-    for (long long base = (long long)blockIdx.x * kThreads; base < n; base += (long long)G * kThreads) {
+__device__ __forceinline__ void for_elems(int n, int G, int cta, F&& f) {
+    for (long long base = (long long)cta * kThreads; base < n; base += (long long)G * kThreads) {
         const long long i = base + threadIdx.x;
         if (i < n) f((int)i);
     }
@@ -139,11 +143,11 @@ __device__ __forceinline__ void for_elems(int n, int G, F&& f) {
 // Row loop with S lanes per row over the same chunks.  f(row, lane, valid)
 // is called by every thread (valid=false past n) so group shuffles are safe.
 template <int S, class F>
-__device__ __forceinline__ void for_rows(int n, int G, F&& f) {
+__device__ __forceinline__ void for_rows(int n, int G, int cta, F&& f) {
     constexpr int gpb = kThreads / S;
     const int lane = threadIdx.x & (S - 1);
     const int grp = threadIdx.x / S;
-    for (long long base = (long long)blockIdx.x * kThreads; base < n; base += (long long)G * kThreads) {
+    for (long long base = (long long)cta * kThreads; base < n; base += (long long)G * kThreads) {
 #pragma unroll 1
         for (int sub = 0; sub < S; ++sub) {
             const long long row = base + (long long)sub * gpb + grp;
@@ -203,9 +207,9 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
     return v;
 }
 
-// FAST: CTA partial of K slots -> part[k*G + blockIdx.x]
+// FAST: CTA partial of K slots -> part[k*G + cta]
 template <int K>
-__device__ __forceinline__ void cta_partial(const double2 (&acc)[K], double2* part, int G) {
+__device__ __forceinline__ void cta_partial(const double2 (&acc)[K], double2* part, int G, int cta) {
     __shared__ double2 sm[K][kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -218,7 +222,7 @@ __device__ __forceinline__ void cta_partial(const double2 (&acc)[K], double2* pa
         double2 s = sm[threadIdx.x][0];
 #pragma unroll
         for (int w = 1; w < kWarps; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
-        part[threadIdx.x * G + blockIdx.x] = s;
+        part[threadIdx.x * G + cta] = s;
     }
 }
 
@@ -270,7 +274,7 @@ __device__ __forceinline__ bool reduce(GridBar& g, const double2 (&acc)[K], doub
         seq_sums<K>(out, n, contrib);
         if (!g.sync()) return false;
     } else {
-        cta_partial<K>(acc, part, g.G);
+        cta_partial<K>(acc, part, g.G, g.cta);
         if (!g.sync()) return false;
         fold_partials<K>(out, part, g.G);
     }
@@ -288,9 +292,9 @@ __device__ __forceinline__ double2 prec_apply(const double2* dinv, int i, double
 }
 
 // Report / history writers (CTA 0, thread 0).
-__device__ __forceinline__ void hist_push(const KArgs& a, long long& len, double v) {
+__device__ __forceinline__ void hist_push(const KArgs& a, int cta, long long& len, double v) {
     if (!a.record) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && len < a.hist_cap) a.hist[len] = v;
+    if (cta == 0 && threadIdx.x == 0 && len < a.hist_cap) a.hist[len] = v;
     ++len;
 }
 

@@ -7,6 +7,11 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <string>
+
+// shared error channel of the C ABI (cvk_last_error); returns code
+int cvk_fail(int code, const std::string& msg);
+
 namespace cvk {
 
 constexpr int kMaxL = 16;     // BiCGSTAB(l): l <= kMaxL
@@ -15,7 +20,8 @@ struct Csr;
 struct DevReport;
 
 // persistent solver kernels (cvk_krylov.cu)
-const void* solver_kernel(int solver, int S, bool ref);
+// batched: k_solve_batched(const KArgs* segs, int nseg) instead of k_solve(KArgs)
+const void* solver_kernel(int solver, int S, bool ref, bool batched = false);
 int solver_nwork(int solver, int l, int m);
 size_t solver_smem(int solver, int m);
 

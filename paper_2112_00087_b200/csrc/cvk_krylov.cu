@@ -24,10 +24,10 @@ namespace cvk {
 
 namespace {
 
-__device__ __forceinline__ void write_report(const KArgs& a, int conv, int brk, long long it,
+__device__ __forceinline__ void write_report(const KArgs& a, int cta, int conv, int brk, long long it,
                                              double final_relres, double true_relres,
                                              long long hist_len, int err) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (cta == 0 && threadIdx.x == 0) {
         a.rep->converged = conv;
         a.rep->breakdown = brk;
         a.rep->iterations = it;
@@ -46,7 +46,7 @@ __device__ bool true_relres(GridBar& g, const KArgs& a, double2* scratch, double
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
     const double2* x = a.x;
     const double2* b = a.b;
-    for_rows<S>(n, a.G, [&](int row, int lane, bool valid) {
+    for_rows<S>(n, a.G, g.cta, [&](int row, int lane, bool valid) {
         const double2 y = row_sum<S>(a.A, row, lane, valid, [&](int c) { return x[c]; });
         if (valid && lane == 0) {
             const double2 bi = __ldg(b + row);
@@ -72,8 +72,7 @@ __device__ bool true_relres(GridBar& g, const KArgs& a, double2* scratch, double
 // ================================================================ BiCGSTAB
 // work: r, shadow, s, t, p[2], v[2]
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
-    GridBar g(a.bar, a.G);
+__device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
     const int n = a.A.n, G = a.G;
     const double2* __restrict__ dinv = a.dinv;
     const double2* __restrict__ b = a.b;
@@ -90,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
 
     // r = M^{-1} b, shadow = r, x = 0; ||r||^2 and <shadow, r>
     double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_elems(n, G, [&](int i) {
+    for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri;
         sh[i] = ri;
@@ -102,12 +101,12 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
             acc_norm(q[0], r[i]);
             acc_dot(q[1], sh[i], r[i]);
         })) {
-        write_report(a, 0, 0, 0, 0, 0, 0, 1);
+        write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1);
         return;
     }
     const double bnorm = sqrt(t0[0].x);
     if (bnorm == 0.0) {  // krylov.cpp:70-74: converged, true_relres left at 0
-        write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0);
+        write_report(a, g.cta, 1, 0, 0, 0.0, 0.0, 0, 0);
         return;
     }
     const double brk = 1e-30 * bnorm * bnorm;
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
         };
         // phase A: v = M^{-1} A p; gamma = <shadow, v>
         double2 accA[1] = {make_double2(0, 0)};
-        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+        for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, pnew);
             if (valid && lane == 0) {
                 const double2 vi = prec_apply(dinv, row, y);
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
         // s = r - alpha v (axpy copy), x += alpha p; t = M^{-1} A s
         auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
         double2 accB[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+        for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, sval);
             if (valid && lane == 0) {
                 const double2 ti = prec_apply(dinv, row, y);
@@ -181,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
         double relres = sqrt(tB[0].x) / bnorm;
         if (relres <= tol) {
             conv = 1; iters = it; final_relres = relres;
-            hist_push(a, hl, relres);
+            hist_push(a, g.cta, hl, relres);
             break;
         }
         if (cvk_abs(tB[1]) < brk) { brkc = 3; iters = it; break; }
@@ -189,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
         const double2 nom2 = cvk_neg(omega);
         // x += omega s; r = s - omega t; ||r||^2, <shadow, r>
         double2 accC[2] = {make_double2(0, 0), make_double2(0, 0)};
-        for_elems(n, G, [&](int i) {
+        for_elems(n, G, g.cta, [&](int i) {
             const double2 si = s[i];
             x[i] = cvk_add(x[i], cvk_mul(omega, si));
             const double2 ri = cvk_add(si, cvk_mul(nom2, t[i]));
@@ -205,21 +204,20 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab(KArgs a) {
         relres = sqrt(tC[0].x) / bnorm;
         final_relres = relres;
         iters = it;
-        hist_push(a, hl, relres);
+        hist_push(a, g.cta, hl, relres);
         if (relres <= tol) { conv = 1; break; }
         rho_new = tC[1];
         cur ^= 1;
     }
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, s, part[1], trr);
-    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+    write_report(a, g.cta, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
 }
 
 // =================================================================== tfQMR
 // work: r, shadow, w, u[2], au, v, d
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
-    GridBar g(a.bar, a.G);
+__device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
     const int n = a.A.n, G = a.G;
     const double2* __restrict__ dinv = a.dinv;
     const double2* __restrict__ b = a.b;
@@ -237,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
     const double tol = a.tol;
 
     double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_elems(n, G, [&](int i) {
+    for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri; sh[i] = ri; w[i] = ri; uu[0][i] = ri;
         d[i] = make_double2(0, 0);
@@ -248,9 +246,9 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
     if (!reduce<REF, 2>(g, acc0, t0, part[0], n, [&](int i, double2* q) {
             acc_norm(q[0], r[i]);
             acc_dot(q[1], sh[i], r[i]);
-        })) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+        })) { write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1); return; }
     const double bnorm = sqrt(t0[0].x);
-    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    if (bnorm == 0.0) { write_report(a, g.cta, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
     const double brk = 1e-30 * bnorm * bnorm;
     double2 rho = t0[1];
     int cur = 0;
@@ -260,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
     {
         const double2* u0 = uu[0];
         double2 acc[1] = {make_double2(0, 0)};
-        for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+        for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, [&](int c) { return u0[c]; });
             if (valid && lane == 0) {
                 const double2 ai = prec_apply(dinv, row, y);
@@ -270,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
         });
         double2 tt[1];
         ok = reduce<REF, 1>(g, acc, tt, part[1], n, [&](int i, double2* q) { acc_dot(q[0], sh[i], v[i]); });
-        if (!ok) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+        if (!ok) { write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1); return; }
         rho = t0[1];
         // sigma carried into the loop
         acc0[0] = tt[0];
@@ -293,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
             const double2 coef = cvk_cdiv(cvk_scale(theta * theta, eta), alpha);
             const double2* uc = uu[cur];
             double2 acc[1] = {make_double2(0, 0)};
-            for_elems(n, G, [&](int i) {
+            for_elems(n, G, g.cta, [&](int i) {
                 const double2 wi = cvk_add(w[i], cvk_mul(nal, au[i]));
                 w[i] = wi;
                 d[i] = cvk_add(cvk_mul(coef, d[i]), uc[i]);
@@ -322,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
             double2* un = uu[cur ^ 1];
             auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, v[c])); };
             double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-            for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+            for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                 const double2 y = row_sum<S>(a.A, row, lane, valid, uval);
                 if (valid && lane == 0) {
                     const double2 ui = uval(row);
@@ -354,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
             const double relres = tau * sqrt((double)(hs + 1 + 2)) / bnorm;
             final_relres = relres;
             iters = (hs + 1) / 2 + 1;
-            hist_push(a, hl, relres);
+            hist_push(a, g.cta, hl, relres);
             if (relres <= tol) { conv = 1; break; }
             const double2 rho_new = tt[1];
             if (cvk_abs(rho) < brk) { brkc = 1; break; }
@@ -367,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
             double2* un2 = uu[cur ^ 1];
             auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc2[c])); };
             double2 accO[1] = {make_double2(0, 0)};
-            for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+            for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                 const double2 y = row_sum<S>(a.A, row, lane, valid, unext);
                 if (valid && lane == 0) {
                     const double2 un_i = unext(row);
@@ -392,19 +390,18 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_tfqmr(KArgs a) {
     }
     if (ok && pending_x) {  // the owed x += eta d (krylov.cpp:335)
         const double2 e = eta;
-        for_elems(n, G, [&](int i) { x[i] = cvk_add(x[i], cvk_mul(e, d[i])); });
+        for_elems(n, G, g.cta, [&](int i) { x[i] = cvk_add(x[i], cvk_mul(e, d[i])); });
         ok = g.sync();
     }
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, r, part[region], trr);
-    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+    write_report(a, g.cta, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
 }
 
 // ============================================================ BiCGSTAB(l)
 // work: shadow, x-scratch?, then r[0..l], u[0..l], spareR, spareU  (2l+5 vectors)
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
-    GridBar g(a.bar, a.G);
+__device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
     const int n = a.A.n, G = a.G, L = a.l;
     const double2* __restrict__ dinv = a.dinv;
     const double2* __restrict__ b = a.b;
@@ -430,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
     double2 acc0[2] = {make_double2(0, 0), make_double2(0, 0)};
     {
         double2* r0 = R(0);
-        for_elems(n, G, [&](int i) {
+        for_elems(n, G, g.cta, [&](int i) {
             const double2 v0 = prec_apply(dinv, i, __ldg(b + i));
             r0[i] = v0; sh[i] = v0;
             x[i] = make_double2(0, 0);
@@ -445,10 +442,10 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
         if (!reduce<REF, 2>(g, acc0, t0, next_part(), n, [&](int i, double2* q) {
                 acc_norm(q[0], r0[i]);
                 acc_dot(q[1], sh[i], r0[i]);
-            })) { write_report(a, 0, 0, 0, 0, 0, 0, 1); return; }
+            })) { write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1); return; }
     }
     const double bnorm = sqrt(t0[0].x);
-    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    if (bnorm == 0.0) { write_report(a, g.cta, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
     const double brk = 1e-30 * bnorm * bnorm;
     double2 rho_old = make_double2(1, 0), alpha = make_double2(0, 0), omega = make_double2(1, 0);
     double2 rho_next = t0[1];  // <shadow, r_j> for the coming BiCG step
@@ -475,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
                 double2* uj1 = U(j + 1);
                 auto ujv = [&](int c) -> double2 { return cvk_add(cvk_mul(nbeta, uj_old[c]), rj[c]); };
                 double2 acc[1] = {make_double2(0, 0)};
-                for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                     const double2 y = row_sum<S>(a.A, row, lane, valid, ujv);
                     if (valid && lane == 0) {
                         const double2 yi = prec_apply(dinv, row, y);
@@ -486,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
                 });
                 // the other u_i (i < j) in element mapping
                 __syncthreads();
-                for_elems(n, G, [&](int i) {
+                for_elems(n, G, g.cta, [&](int i) {
                     for (int q = 0; q < j; ++q) {
                         double2* uq = U(q);
                         uq[i] = cvk_add(cvk_mul(nbeta, uq[i]), R(q)[i]);
@@ -510,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
                 double2* rj1 = R(j + 1);
                 auto rjv = [&](int c) -> double2 { return cvk_add(rj_old[c], cvk_mul(nal, uj1[c])); };
                 double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-                for_rows<S>(n, G, [&](int row, int lane, bool valid) {
+                for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                     const double2 y = row_sum<S>(a.A, row, lane, valid, rjv);
                     if (valid && lane == 0) {
                         const double2 yi = prec_apply(dinv, row, y);
@@ -520,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
                 });
                 __syncthreads();
                 const double2* u0 = U(0);
-                for_elems(n, G, [&](int i) {
+                for_elems(n, G, g.cta, [&](int i) {
                     for (int q = 0; q < j; ++q) {
                         double2* rq = R(q);
                         rq[i] = cvk_add(rq[i], cvk_mul(nal, U(q + 1)[i]));
@@ -551,14 +548,14 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
             double2 tn[1];
             double2 accn[1] = {make_double2(0, 0)};
             double2* r0 = R(0);
-            for_elems(n, G, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
+            for_elems(n, G, g.cta, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
             ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
             if (!ok) break;
             const double relres = sqrt(tn[0].x) / bnorm;
             final_relres = relres;
             if (relres <= tol) {
                 conv = 1; brkc = 0; iters = cycle;
-                hist_push(a, hl, relres);
+                hist_push(a, g.cta, hl, relres);
             } else {
                 iters = cycle - 1;
             }
@@ -578,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
                 const double2* r0 = R(0);
                 const bool last = (i == j);
                 double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-                for_elems(n, G, [&](int e) {
+                for_elems(n, G, g.cta, [&](int e) {
                     double2 v = rj1[e];
                     if (has_upd) { v = cvk_add(v, cvk_mul(ntau, rprev[e])); rj1[e] = v; }
                     if (!REF) {
@@ -608,13 +605,13 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
             double2 tn[1];
             double2 accn[1] = {make_double2(0, 0)};
             double2* r0 = R(0);
-            for_elems(n, G, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
+            for_elems(n, G, g.cta, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
             ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
             if (!ok) break;
             const double relres = sqrt(tn[0].x) / bnorm;
             final_relres = relres;
             iters = cycle;
-            if (relres <= tol) { conv = 1; brkc = 0; hist_push(a, hl, relres); }
+            if (relres <= tol) { conv = 1; brkc = 0; hist_push(a, g.cta, hl, relres); }
             break;
         }
         // gamma, gamma', gamma'' (krylov.cpp:251-262) -- thread 0, then shared
@@ -638,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
         {
             double2* r0 = R(0);
             double2* u0 = U(0);
-            for_elems(n, G, [&](int i) {
+            for_elems(n, G, g.cta, [&](int i) {
                 double2 xi = x[i], r0i = r0[i], u0i = u0[i];
                 xi = cvk_add(xi, cvk_mul(gam_s[0], r0i));
                 r0i = cvk_add(r0i, cvk_mul(cvk_neg(gp_s[L - 1]), R(L)[i]));
@@ -661,14 +658,14 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
             const double relres = sqrt(tu[0].x) / bnorm;
             final_relres = relres;
             iters = cycle;
-            hist_push(a, hl, relres);
+            hist_push(a, g.cta, hl, relres);
             rho_next = tu[1];
             if (relres <= tol) { conv = 1; break; }
         }
     }
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, scratch, next_part(), trr);
-    write_report(a, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+    write_report(a, g.cta, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
 }
 
 // ================================================================ GMRES(m)
@@ -677,8 +674,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_bicgstab_l(KArgs a) {
 // work: r, W[2], V[0..m]   (m + 4 vectors)
 // dynamic shared: H[(m+1) m], sn[m], g[m+1], y[m], h1[m+1], h2[m+1] (double2), cs[m] (double)
 template <int S, bool REF>
-__global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
-    GridBar g(a.bar, a.G);
+__device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     const int n = a.A.n, G = a.G, M = a.m;
     const double2* __restrict__ dinv = a.dinv;
     const double2* __restrict__ b = a.b;
@@ -709,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
         for (int k = 0; k < cnt; ++k) {
             const double2* vk = V + (size_t)k * n;
             double2 s = make_double2(0, 0);
-            for_elems(n, G, [&](int i) { acc_dot(s, vk[i], wv[i]); });
+            for_elems(n, G, g.cta, [&](int i) { acc_dot(s, vk[i], wv[i]); });
             s = warp_sum(s);
             if (lane == 0) hsm[k][warp] = s;
         }
@@ -717,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
         if (threadIdx.x < cnt) {
             double2 s = hsm[threadIdx.x][0];
             for (int w2 = 1; w2 < kWarps; ++w2) s = cvk_add(s, hsm[threadIdx.x][w2]);
-            pr[threadIdx.x * G + blockIdx.x] = s;
+            pr[threadIdx.x * G + g.cta] = s;
         }
     };
     auto fold_multi = [&](const double2* pr, int cnt, double2* out) {
@@ -745,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
 
     // r = M^{-1} b, x = 0, ||r||
     double2 acc0[1] = {make_double2(0, 0)};
-    for_elems(n, G, [&](int i) {
+    for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri;
         x[i] = make_double2(0, 0);
@@ -753,11 +749,11 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
     });
     double2 t0[1];
     if (!reduce<REF, 1>(g, acc0, t0, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r[i]); })) {
-        write_report(a, 0, 0, 0, 0, 0, 0, 1);
+        write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1);
         return;
     }
     const double bnorm = sqrt(t0[0].x);
-    if (bnorm == 0.0) { write_report(a, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
+    if (bnorm == 0.0) { write_report(a, g.cta, 1, 0, 0, 0.0, 0.0, 0, 0); return; }
     const double brk = 1e-30 * bnorm * bnorm;
     double beta = bnorm;
     long long total = 0;
@@ -789,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
                 const double2* sp = src;
                 const double sc = scale;
                 auto vat = [&](int c) -> double2 { return cvk_divr(sp[c], sc); };
-                for_rows<S>(n, G, [&](int row, int ln, bool valid) {
+                for_rows<S>(n, G, g.cta, [&](int row, int ln, bool valid) {
                     const double2 y = row_sum<S>(a.A, row, ln, valid, vat);
                     if (valid && ln == 0) {
                         Vj[row] = vat(row);
@@ -813,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
             }
             // ---- R1: w -= V h1; h2 = V^H w
             {
-                for_elems(n, G, [&](int i) {
+                for_elems(n, G, g.cta, [&](int i) {
                     double2 wi = w[i];
                     for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h1[q]), V[(size_t)q * n + i]));
                     w[i] = wi;
@@ -836,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
             double hn;
             {
                 double2 acc[1] = {make_double2(0, 0)};
-                for_elems(n, G, [&](int i) {
+                for_elems(n, G, g.cta, [&](int i) {
                     double2 wi = w[i];
                     for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h2[q]), V[(size_t)q * n + i]));
                     w[i] = wi;
@@ -872,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
             const double2 gj1 = gv[j + 1];
             const double relres = sqrt(gj1.x * gj1.x + gj1.y * gj1.y) / bnorm;
             final_relres = relres;
-            hist_push(a, hl, relres);
+            hist_push(a, g.cta, hl, relres);
             k = j + 1;
             if (relres <= tol) { conv = 1; stop = true; break; }
             if (hn * hn < brk) { brkc = 7; stop = true; break; }
@@ -891,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
             }
         }
         __syncthreads();
-        for_elems(n, G, [&](int i) {
+        for_elems(n, G, g.cta, [&](int i) {
             double2 xi = x[i];
             for (int q = 0; q < k; ++q) xi = cvk_add(xi, cvk_mul(yv[q], V[(size_t)q * n + i]));
             x[i] = xi;
@@ -901,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
         if (!ok || stop) break;
         // restart residual r = M^{-1}(b - A x)
         double2 acc[1] = {make_double2(0, 0)};
-        for_rows<S>(n, G, [&](int row, int ln, bool valid) {
+        for_rows<S>(n, G, g.cta, [&](int row, int ln, bool valid) {
             const double2 y = row_sum<S>(a.A, row, ln, valid, [&](int c) { return x[c]; });
             if (valid && ln == 0) {
                 const double2 ri = prec_apply(dinv, row, cvk_sub(__ldg(b + row), y));
@@ -918,30 +914,64 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_gmres(KArgs a) {
     (void)wsum;
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, Wb[0], next_part(), trr);
-    write_report(a, conv, brkc, total, final_relres, trr, hl, ok ? 0 : 1);
+    write_report(a, g.cta, conv, brkc, total, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// ------------------------------------------------------------ kernels --
+
+template <int S, bool REF, int SOLVER>
+__device__ __forceinline__ void run_body(const KArgs& a, GridBar& g) {
+    if (SOLVER == 0) bicgstab_body<S, REF>(a, g);
+    else if (SOLVER == 1) bicgstab_l_body<S, REF>(a, g);
+    else if (SOLVER == 2) tfqmr_body<S, REF>(a, g);
+    else gmres_body<S, REF>(a, g);
+}
+
+// one solve per cooperative launch
+template <int S, bool REF, int SOLVER>
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_solve(KArgs a) {
+    GridBar g(a.bar, a.G);
+    run_body<S, REF, SOLVER>(a, g);
+}
+
+// K10: independent solves (Schwarz subdomains) batched into one cooperative
+// launch.  Segment s owns CTAs [segs[s].cta_base, + segs[s].G) with its own
+// barrier counter, partials, report and vectors; segments finish at their
+// own iteration counts.
+template <int S, bool REF, int SOLVER>
+__global__ void __launch_bounds__(kThreads, kMinCtas) k_solve_batched(const KArgs* segs, int nseg) {
+    __shared__ KArgs sa;
+    if (threadIdx.x == 0) {
+        int s = 0;
+        while (s + 1 < nseg && (int)blockIdx.x >= segs[s + 1].cta_base) ++s;
+        sa = segs[s];
+    }
+    __syncthreads();
+    GridBar g(sa.bar, sa.G, (int)blockIdx.x - sa.cta_base);
+    run_body<S, REF, SOLVER>(sa, g);
 }
 
 // ----------------------------------------------------------- dispatch --
 
 template <int S, bool REF>
-static const void* pick(int solver) {
+static const void* pick(int solver, bool batched) {
     switch (solver) {
-        case 0: return (const void*)k_bicgstab<S, REF>;
-        case 1: return (const void*)k_bicgstab_l<S, REF>;
-        case 2: return (const void*)k_tfqmr<S, REF>;
-        case 3: return (const void*)k_gmres<S, REF>;
+        case 0: return batched ? (const void*)k_solve_batched<S, REF, 0> : (const void*)k_solve<S, REF, 0>;
+        case 1: return batched ? (const void*)k_solve_batched<S, REF, 1> : (const void*)k_solve<S, REF, 1>;
+        case 2: return batched ? (const void*)k_solve_batched<S, REF, 2> : (const void*)k_solve<S, REF, 2>;
+        case 3: return batched ? (const void*)k_solve_batched<S, REF, 3> : (const void*)k_solve<S, REF, 3>;
     }
     return nullptr;
 }
 
-const void* solver_kernel(int solver, int S, bool ref) {
-    if (ref) return pick<1, true>(solver);
+const void* solver_kernel(int solver, int S, bool ref, bool batched) {
+    if (ref) return pick<1, true>(solver, batched);
     switch (S) {
-        case 1: return pick<1, false>(solver);
-        case 2: return pick<2, false>(solver);
-        case 4: return pick<4, false>(solver);
-        case 8: return pick<8, false>(solver);
-        case 16: return pick<16, false>(solver);
+        case 1: return pick<1, false>(solver, batched);
+        case 2: return pick<2, false>(solver, batched);
+        case 4: return pick<4, false>(solver, batched);
+        case 8: return pick<8, false>(solver, batched);
+        case 16: return pick<16, false>(solver, batched);
     }
     return nullptr;
 }

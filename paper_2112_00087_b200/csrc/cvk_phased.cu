@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_elems(n, gridDim.x, [&](int i) {
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri;
         V.sh[i] = ri;
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
         return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
     };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(pnew)&, kBatch>(a.A, row, 0, valid, pnew);
         if (valid) {
             const double2 vi = prec_apply(a.dinv, row, y);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     double2* __restrict__ x = a.x;
     auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
     double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(sval)&, kBatch>(a.A, row, 0, valid, sval);
         if (valid) {
             const double2 ti = prec_apply(a.dinv, row, y);
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     const double2* __restrict__ sh = V.sh;
     double2* __restrict__ r = V.r;
     double2* __restrict__ x = a.x;
-    for_elems(n, gridDim.x, [&](int i) {
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 si = s[i];
         x[i] = cvk_add(x[i], cvk_mul(omega, si));
         const double2 ri = cvk_add(si, cvk_mul(nom, t[i]));
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
     const int n = a.A.n;
     TfVecs V(a.work, (size_t)n);
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_elems(n, gridDim.x, [&](int i) {
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri; V.sh[i] = ri; V.w[i] = ri; V.u0[i] = ri;
         V.d[i] = make_double2(0, 0);
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     const double2* __restrict__ u0 = V.u0;
     auto uat = [&](int c) -> double2 { return u0[c]; };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uat)&, kBatch>(a.A, row, 0, valid, uat);
         if (valid) {
             const double2 ai = prec_apply(a.dinv, row, y);
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
     const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
     const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
     double2 acc[1] = {make_double2(0, 0)};
-    for_elems(n, gridDim.x, [&](int i) {
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 wi = cvk_add(V.w[i], cvk_mul(nal, V.au[i]));
         V.w[i] = wi;
         V.d[i] = cvk_add(cvk_mul(coef, V.d[i]), uc[i]);
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     const double2* __restrict__ vv = V.v;
     auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
-    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uval)&, kBatch>(a.A, row, 0, valid, uval);
         if (valid) {
             const double2 ui = uval(row);
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     const double2* __restrict__ w = V.w;
     auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
     double2 acc[1] = {make_double2(0, 0)};
-    for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(unext)&, kBatch>(a.A, row, 0, valid, unext);
         if (valid) {
             const double2 un_i = unext(row);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
     if (!st->pending_x) return;
     TfVecs V(a.work, (size_t)a.A.n);
     const double2 e = st->eta;
-    for_elems(a.A.n, gridDim.x, [&](int i) { a.x[i] = cvk_add(a.x[i], cvk_mul(e, V.d[i])); });
+    for_elems(a.A.n, gridDim.x, blockIdx.x, [&](int i) { a.x[i] = cvk_add(a.x[i], cvk_mul(e, V.d[i])); });
 }
 
 // ------------------------------------------------- true residual + report
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     auto xat = [&](int c) -> double2 { return x[c]; };
     double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
     if (!st->skip_true) {
-        for_rows<1>(n, gridDim.x, [&](int row, int, bool valid) {
+        for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
             const double2 y = row_sum<1, decltype(xat)&, kBatch>(a.A, row, 0, valid, xat);
             if (valid) {
                 const double2 bi = __ldg(a.b + row);
