@@ -394,7 +394,7 @@ extern "C" int cvk_schwarz_solve(cvk_ctx* ctx, const cvk_grid* grid, double c, i
         float ms = 0.f;
         e = cvk_ddm_launch_batched(ctx, inner_solver, mode, d_segs, (int)n_sub, cta_base, smem, &ms);
         if (e != CVK_OK) return e;
-        k_ddm_exchange<<<1, 1024, xsmem, st>>>(geo, d_u, d_gl, d_gr, d_prev, d2(a_l), d2(b_l), d2(a_r), d2(b_r),
+        k_ddm_exchange<<<1, 256, xsmem, st>>>(geo, d_u, d_gl, d_gr, d_prev, d2(a_l), d2(b_l), d2(a_r), d2(b_r),
                                               d2(s_sum), d_jump);
         DK(cudaGetLastError());
         DK(cudaEventRecord(e1, st));
