@@ -312,7 +312,9 @@ def main():
                  "frac": spmv_bytes / spmv_s.value / 1e9 / peak, "bytes": spmv_bytes},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "BiCGSTAB iteration phase kernels (k_bi_a/k_bi_b/k_bi_c)",
+                     "kernel": "BiCGSTAB iteration: TMA-streamed SpMV phases k_bi_a_s + k_bi_b_s, "
+                               "elementwise phase k_bi_c (3 launches per iteration, CUDA-graph replay)",
+                     "traffic_unit": "DRAM bytes per iteration (ncu, sum of the 3 launches)",
                      "bytes_per_iteration": iter_bytes, "peak_kind": peak_kind},
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 16 * nnz + 16 * n,
                 "d2h_bytes_per_step": 16 * n},

@@ -18,6 +18,7 @@
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 #include "cvk_phased.h"
+#include "cvk_stream.cuh"
 
 using cvk::DevReport;
 
@@ -56,6 +57,7 @@ struct cvk_csr {
     void* blob = nullptr;  // av | ci | rp in one allocation
     size_t blob_bytes = 0;
     int group = 1;  // SpMV lanes per row for FAST mode
+    int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
 };
 
 struct cvk_prec {
@@ -251,7 +253,8 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     // access-policy window can pin the whole matrix (solve-time persistence)
     const size_t vb = sizeof(double2) * (size_t)std::max<int64_t>(1, nnz);
     const size_t cb = (sizeof(int) * (size_t)std::max<int64_t>(1, nnz) + 255) & ~(size_t)255;
-    const size_t rb = sizeof(int) * rp.size();
+    // 16 bytes of padding: the streamed kernels copy row offsets in 16-byte units
+    const size_t rb = sizeof(int) * rp.size() + 16;
     CK(cudaMalloc(&A->blob, vb + cb + rb));
     A->blob_bytes = vb + cb + rb;
     A->av = (double2*)A->blob;
@@ -263,6 +266,13 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
         CK(cudaMemcpyAsync(A->av, values, sizeof(double2) * nnz, cudaMemcpyHostToDevice, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
+    {
+        long long mk = 0;
+        for (int64_t r0 = 0; r0 < nrows; r0 += cvk::kStreamRows)
+            mk = std::max<long long>(mk, (long long)rp[(size_t)std::min<int64_t>(r0 + cvk::kStreamRows, nrows)] -
+                                             (long long)rp[(size_t)r0]);
+        A->capk = (int)((mk + 3) & ~3LL);
+    }
     *out = A;
     return CVK_OK;
 }
@@ -433,9 +443,31 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     hs.record = o->record_history ? 1 : 0;
     hs.hist_cap = hcap;
     if (o->max_iter < 1) hs.max_iter = 0;
+    // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    auto stages_for = [&](int nvec) {
+        cvk::StreamLayout L{A->capk, nvec, 1};
+        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8;
+        return (int)std::min<long long>(cvk::kStreamMaxStages, std::max<long long>(0, avail / (long long)L.stage_bytes()));
+    };
+    const int st5 = stages_for(5), st7 = stages_for(7), st8 = stages_for(8);
+    const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&
+                          (solver == CVK_BICGSTAB ? st5 >= 2 : std::min(st7, st8) >= 2);
+    auto smem_for = [&](int nvec, int stg) { return cvk::StreamLayout{A->capk, nvec, stg}.smem_bytes(); };
+    const void* sk[4] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s};
+    if (streamed)
+        for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096));
+    // elementwise phases: grid-stride, 4 elements per thread per trip
+    long long Ge = std::min<long long>(4LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
+    if (const char* env = std::getenv("CVK_ELEM_CTAS")) Ge = std::max(1, std::atoi(env));
+    if (!streamed) Ge = G;
+    const long long Gmax = std::max<long long>(std::max<long long>(G, Ge), c->nsm);
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
+        return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep);
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, st5, st7, st8);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
@@ -447,21 +479,36 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     key.push_back((unsigned char)(pinned ? 1 : 0));  // captured nodes carry the L2 window
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
+    key.push_back((unsigned char)(streamed ? 1 : 0));
+    const unsigned char* gep = (const unsigned char*)&Ge;
+    key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
         if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const dim3 sgrid((unsigned)c->nsm), sblock(cvk::kStreamThreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
             if (solver == CVK_BICGSTAB) {
-                launch_pdl(K.bi_a, grid, block, args, smem, c->stream);
-                launch_pdl(K.bi_b, grid, block, args, smem, c->stream);
-                launch_pdl(K.bi_c, grid, block, args, 0, c->stream);
+                if (streamed) {
+                    launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(5, st5), c->stream);
+                    launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(5, st5), c->stream);
+                } else {
+                    launch_pdl(K.bi_a, grid, block, args, smem, c->stream);
+                    launch_pdl(K.bi_b, grid, block, args, smem, c->stream);
+                }
+                launch_pdl(K.bi_c, egrid, block, args, 0, c->stream);
             } else {
-                launch_pdl(K.tf_w, grid, block, args, 0, c->stream);
-                launch_pdl(K.tf_e, grid, block, args, smem, c->stream);
-                launch_pdl(K.tf_o, grid, block, args, smem, c->stream);
+                launch_pdl(K.tf_w, egrid, block, args, 0, c->stream);
+                if (streamed) {
+                    launch_pdl(K.tf_e_s, sgrid, sblock, args, smem_for(7, st7), c->stream);
+                    launch_pdl(K.tf_o_s, sgrid, sblock, args, smem_for(8, st8), c->stream);
+                } else {
+                    launch_pdl(K.tf_e, grid, block, args, smem, c->stream);
+                    launch_pdl(K.tf_o, grid, block, args, smem, c->stream);
+                }
             }
         }
+        CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
         CK(cudaGraphInstantiate(&c->gexec, graph, 0));
         cudaGraphDestroy(graph);
@@ -659,6 +706,15 @@ int cvk_spmv_device(const cvk_csr* A, const double* x_dev, double* y_dev, int mo
     cvk_ctx* c = A->ctx;
     const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
+    if (!ref && A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && !std::getenv("CVK_NO_STREAM")) {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        const cudaError_t e = cvk::launch_spmv_stream((int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
+                                                      (double2*)y_dev, A->capk, c->nsm, optin, c->stream);
+        if (e == cudaSuccess) return CVK_OK;
+        if (e != cudaErrorInvalidConfiguration) CK(e);
+        (void)cudaGetLastError();
+    }
     CK(cvk::launch_spmv(ref ? 1 : A->group, ref, (int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
                         (double2*)y_dev, 0, c->stream));
     return CVK_OK;

@@ -7,10 +7,12 @@
 //   axpy_inplace    numkit.cpp:135-146
 //   xpay_inplace    numkit.cpp:148-159
 //   jacobi          krylov.cpp:31-55    (first col==i entry, 1.0/d via __divdc3 rounding)
+#include <algorithm>
 #include <cstdlib>
 
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
+#include "cvk_stream.cuh"
 
 namespace cvk {
 
@@ -23,6 +25,32 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restr
         const double2 acc = row_sum<S, decltype(xat)&, (REF ? 1 : 5)>(A, row, lane, valid, xat);
         if (valid && lane == 0) __stcs(y + row, acc);
     });
+}
+
+// FAST standalone SpMV on the TMA ring (cvk_stream.cuh): x staged per chunk,
+// out-of-chunk columns gathered through L1/L2; per-row order as k_spmv.
+__global__ void __launch_bounds__(kStreamThreads, 1) k_spmv_s(Csr A, StreamLayout L, const double2* __restrict__ x,
+                                                              double2* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const double2* vecs[1] = {x};
+    stream_rows(A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        const double2 acc = chunk_row_sum<5>(ch, t, [&](int l) { return ch.v(0, l); },
+                                             [&](int c) { return __ldg(x + c); });
+        __stcs(y + ch.r0 + t, acc);
+    });
+}
+
+cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
+                               double2* y, int capk, int nsm, int optin, cudaStream_t st) {
+    StreamLayout L{capk, 1, 1};
+    const long long avail = (long long)optin - 4096 - 2 * kStreamMaxStages * 8;
+    L.stages = (int)std::min<long long>(kStreamMaxStages, avail / (long long)L.stage_bytes());
+    if (L.stages < 2) return cudaErrorInvalidConfiguration;
+    const size_t smem = L.smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_spmv_s<<<nsm, kStreamThreads, smem, st>>>(Csr{n, rp, ci, av}, L, x, y);
+    return cudaGetLastError();
 }
 
 template <int S, bool REF>

@@ -28,6 +28,9 @@ size_t solver_smem(int solver, int m);
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);
+// FAST SpMV on the TMA ring; cudaErrorInvalidConfiguration if a chunk does not fit
+cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
+                               double2* y, int capk, int nsm, int optin, cudaStream_t st);
 cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
                             int* bad_row, cudaStream_t st);
 // out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 1024 double2

@@ -22,6 +22,7 @@
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 #include "cvk_phased.h"
+#include "cvk_stream.cuh"
 
 namespace cvk {
 
@@ -39,6 +40,8 @@ struct PArgs {
     PState* st;
     double* hist;
     DevReport* rep;
+    int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
+    int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
 };
 
 constexpr int kPhSlots = 4;  // reduction slots per phase (max K used is 3)
@@ -49,10 +52,11 @@ __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
 
 // Write this CTA's K partials; returns true in the CTA that arrived last,
 // with the fixed-order totals in tot (all threads of that CTA).
-template <int K>
+template <int K, int NT = kThreads>
 __device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* counter,
                              double2 (&tot)[K]) {
-    __shared__ double2 sm[K][kWarps];
+    constexpr int NW = NT / 32;
+    __shared__ double2 sm[K][NW];
     __shared__ int s_last;
     const int G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -65,7 +69,7 @@ __device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* c
     if (threadIdx.x < K) {
         double2 s = sm[threadIdx.x][0];
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
+        for (int w = 1; w < NW; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
         part[threadIdx.x * G + blockIdx.x] = s;
         __threadfence();
     }
@@ -77,18 +81,43 @@ __device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* c
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         double2 s = make_double2(0.0, 0.0);
-        for (int b = threadIdx.x; b < G; b += kThreads) s = cvk_add(s, __ldcg(part + k * G + b));
+        for (int b = threadIdx.x; b < G; b += NT) s = cvk_add(s, __ldcg(part + k * G + b));
         s = warp_sum(s);
         __syncthreads();
         if (lane == 0) sm[k][warp] = s;
         __syncthreads();
         double2 t = sm[k][0];
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) t = cvk_add(t, sm[k][w]);
+        for (int w = 1; w < NW; ++w) t = cvk_add(t, sm[k][w]);
         tot[k] = t;
     }
     if (threadIdx.x == 0) *counter = 0u;
     return true;
+}
+
+// Grid-stride element loop with U elements per thread per trip; all loads of
+// a trip are issued before its first store (the elementwise phases are
+// latency-bound with one 16-byte load per vector in flight; tools/bicg_lab.cu
+// phase C: 3.5 vs 2.0 TB/s at 1M DOF).  Launched on a grid of
+// kElemCtasPerSm CTAs per SM.
+constexpr int kElemBatch = 4;
+template <int U, class LD, class STF>
+__device__ __forceinline__ void for_elems_batched(int n, LD&& ld, STF&& stf) {
+    using T = decltype(ld(0));
+    const long long stride = (long long)gridDim.x * kThreads;
+    for (long long base = (long long)blockIdx.x * kThreads + threadIdx.x; base < n; base += stride * U) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * stride;
+            if (i < n) v[u] = ld((int)i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * stride;
+            if (i < n) stf((int)i, v[u]);
+        }
+    }
 }
 
 // Programmatic dependent launch: the successor kernel is launched while this
@@ -254,14 +283,16 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     const double2* __restrict__ sh = V.sh;
     double2* __restrict__ r = V.r;
     double2* __restrict__ x = a.x;
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        const double2 si = s[i];
-        x[i] = cvk_add(x[i], cvk_mul(omega, si));
-        const double2 ri = cvk_add(si, cvk_mul(nom, t[i]));
-        r[i] = ri;
-        acc_norm(acc[0], ri);
-        acc_dot(acc[1], sh[i], ri);
-    });
+    struct L4 { double2 s, t, sh, x; };
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L4{s[i], t[i], sh[i], x[i]}; },
+        [&](int i, const L4& v) {
+            x[i] = cvk_add(v.x, cvk_mul(omega, v.s));
+            const double2 ri = cvk_add(v.s, cvk_mul(nom, v.t));
+            r[i] = ri;
+            acc_norm(acc[0], ri);
+            acc_dot(acc[1], v.sh, ri);
+        });
     double2 tot[2];
     if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
     if (threadIdx.x != 0) return;
@@ -358,12 +389,15 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
     const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
     const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
     double2 acc[1] = {make_double2(0, 0)};
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        const double2 wi = cvk_add(V.w[i], cvk_mul(nal, V.au[i]));
-        V.w[i] = wi;
-        V.d[i] = cvk_add(cvk_mul(coef, V.d[i]), uc[i]);
-        acc_norm(acc[0], wi);
-    });
+    struct L4 { double2 w, au, d, u; };
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L4{V.w[i], V.au[i], V.d[i], uc[i]}; },
+        [&](int i, const L4& v) {
+            const double2 wi = cvk_add(v.w, cvk_mul(nal, v.au));
+            V.w[i] = wi;
+            V.d[i] = cvk_add(cvk_mul(coef, v.d), v.u);
+            acc_norm(acc[0], wi);
+        });
     double2 tot[1];
     if (!partial_last<1>(acc, partv(a, 2), &st->counter[2], tot)) return;
     if (threadIdx.x != 0) return;
@@ -478,6 +512,202 @@ __global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
     for_elems(a.A.n, gridDim.x, blockIdx.x, [&](int i) { a.x[i] = cvk_add(a.x[i], cvk_mul(e, V.d[i])); });
 }
 
+// ----------------------------------------------- streamed (TMA) variants --
+// The SpMV phases of BiCGSTAB and tfQMR on the producer/consumer ring of
+// cvk_stream.cuh: same per-element arithmetic and per-row accumulation order
+// as the thread-per-row kernels above, one CTA per SM.
+
+__device__ __forceinline__ double2 prec_staged(const PArgs& a, const Chunk& ch, int j, int t, double2 y) {
+    return a.dinv ? cvk_mul(ch.v(j, t), y) : y;
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = st->cur;
+    const bool first = st->first != 0;
+    const double2 beta = st->beta, nom = cvk_neg(st->omega);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pc = cur ? V.p1 : V.p0;
+    const double2* __restrict__ vc = cur ? V.v1 : V.v0;
+    double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
+    const StreamLayout L{a.capk, 5, a.st5};
+    double2 acc[1] = {make_double2(0, 0)};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {
+            const double2 rc = ch.v(0, l);
+            if (first) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
+        };
+        auto xg = [&](int c) -> double2 {
+            const double2 rc = r[c];
+            if (first) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+        };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 vi = prec_staged(a, ch, 4, t, y);
+        const int row = ch.r0 + t;
+        pn[row] = xs(t);
+        vn[row] = vi;
+        acc_dot(acc[0], ch.v(3, t), vi);
+    });
+    double2 tot[1];
+    if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    if (cvk_abs(tot[0]) < st->brk) {
+        st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
+        return;
+    }
+    st->alpha = cvk_cdiv(st->rho, tot[0]);
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = st->cur;
+    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    const double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    double2* __restrict__ s = V.s;
+    double2* __restrict__ t_ = V.t;
+    double2* __restrict__ x = a.x;
+    const double2* vecs[5] = {r, vn, a.dinv, pn, x};
+    const StreamLayout L{a.capk, 5, a.st5};
+    double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
+        auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 ti = prec_staged(a, ch, 2, t, y);
+        const double2 si = xs(t);
+        const int row = ch.r0 + t;
+        s[row] = si;
+        t_[row] = ti;
+        x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
+        acc_norm(acc[0], si);
+        acc_dot(acc[1], ti, ti);
+        acc_dot(acc[2], ti, si);
+    });
+    double2 tot[3];
+    if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot)) return;
+    if (threadIdx.x != 0) return;
+    const double relres = sqrt(tot[0].x) / st->bnorm;
+    if (relres <= st->tol) {
+        st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
+        st_hist(a, st, relres);
+        return;
+    }
+    if (cvk_abs(tot[1]) < st->brk) {
+        st->done = 1; st->brk_code = 3; st->iters = st->it;
+        return;
+    }
+    st->omega = cvk_cdiv(tot[2], tot[1]);
+}
+
+// even tail + odd head of tfQMR (k_tf_e) on the ring
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 nal = cvk_neg(st->alpha);
+    const double2 eta_e = st->eta;
+    const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
+    const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
+    double2* __restrict__ un = st->cur ? V.u0 : V.u1;
+    const double2* __restrict__ vv = V.v;
+    const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
+    const StreamLayout L{a.capk, 7, a.st7};
+    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
+        auto xg = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const int row = ch.r0 + t;
+        const double2 ui = xs(t);
+        const double2 ai = prec_staged(a, ch, 2, t, y);
+        un[row] = ui;
+        V.au[row] = ai;
+        const double2 di = ch.v(3, t);
+        a.x[row] = cvk_add(ch.v(4, t), cvk_mul(eta_e, di));
+        const double2 wi = cvk_add(ch.v(5, t), cvk_mul(nal, ai));
+        V.w[row] = wi;
+        V.d[row] = cvk_add(cvk_mul(coef, di), ui);
+        acc_norm(acc[0], wi);
+        acc_dot(acc[1], ch.v(6, t), wi);
+    });
+    double2 tot[2];
+    if (!partial_last<2, kStreamThreads>(acc, partv(a, 0), &st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    st->cur ^= 1;
+    st->theta = sqrt(tot[0].x) / st->tau;
+    const double c = 1.0 / sqrt(1.0 + st->theta * st->theta);
+    st->tau = st->tau * st->theta * c;
+    st->eta = cvk_scale(c * c, st->alpha);
+    st->pending_x = 1;
+    const long long hs = 2 * (st->it - 1) + 1;
+    const double relres = st->tau * sqrt((double)(hs + 2)) / st->bnorm;
+    st->final_relres = relres;
+    st->iters = hs / 2 + 1;
+    st_hist(a, st, relres);
+    if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
+    if (cvk_abs(st->rho) < st->brk) { st->done = 1; st->brk_code = 1; return; }
+    st->beta = cvk_cdiv(tot[1], st->rho);
+    st->rho = tot[1];
+}
+
+// odd tail of tfQMR (k_tf_o) on the ring
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 beta = st->beta, eta_o = st->eta;
+    const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
+    double2* __restrict__ un = st->cur ? V.u0 : V.u1;
+    const double2* __restrict__ w = V.w;
+    const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
+    const StreamLayout L{a.capk, 8, a.st8};
+    double2 acc[1] = {make_double2(0, 0)};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
+        auto xg = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const int row = ch.r0 + t;
+        const double2 un_i = xs(t);
+        const double2 an = prec_staged(a, ch, 2, t, y);
+        un[row] = un_i;
+        double2 vi = cvk_add(cvk_mul(beta, ch.v(3, t)), ch.v(4, t));
+        vi = cvk_add(cvk_mul(beta, vi), an);
+        V.v[row] = vi;
+        V.au[row] = an;
+        a.x[row] = cvk_add(ch.v(5, t), cvk_mul(eta_o, ch.v(6, t)));
+        acc_dot(acc[0], ch.v(7, t), vi);
+    });
+    double2 tot[1];
+    if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    st->pending_x = 0;
+    st->cur ^= 1;
+    st->it++;
+    tf_even_head(st, tot[0]);
+}
+
 // ------------------------------------------------- true residual + report
 __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     pdl_enter();
@@ -528,6 +758,10 @@ PhasedKernels kernels_all() {
     k.tf_o = (const void*)k_tf_o;
     k.tf_fix = (const void*)k_tf_fix;
     k.true_res = (const void*)k_true;
+    k.bi_a_s = (const void*)k_bi_a_s;
+    k.bi_b_s = (const void*)k_bi_b_s;
+    k.tf_e_s = (const void*)k_tf_e_s;
+    k.tf_o_s = (const void*)k_tf_o_s;
     return k;
 }
 
@@ -538,8 +772,13 @@ PhasedKernels phased_kernels() { return kernels_all(); }
 size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep) {
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
+                      int capk, int st5, int st7, int st8) {
     PArgs* p = (PArgs*)out;
+    p->capk = capk;
+    p->st5 = st5;
+    p->st7 = st7;
+    p->st8 = st8;
     p->A = A;
     p->dinv = dinv;
     p->b = b;

@@ -25,11 +25,14 @@ struct PhasedKernels {
     const void *bi_init, *bi_a, *bi_b, *bi_c;
     const void *tf_init, *tf_init2, *tf_w, *tf_e, *tf_o, *tf_fix;
     const void* true_res;  // (PArgs, double2* scratch)
+    // streamed SpMV phases (cvk_stream.cuh): kStreamThreads threads, dynamic smem
+    const void *bi_a_s, *bi_b_s, *tf_e_s, *tf_o_s;
 };
 
 PhasedKernels phased_kernels();
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
-                      double2* work, double2* part, PState* st, double* hist, DevReport* rep);
+                      double2* work, double2* part, PState* st, double* hist, DevReport* rep,
+                      int capk, int st5, int st7, int st8);
 
 }  // namespace cvk

@@ -1,0 +1,210 @@
+// cvk_stream.cuh -- TMA-fed row streaming for the phase kernels.
+//
+// A phase kernel that contains an SpMV walks the matrix in chunks of R
+// consecutive rows.  One producer warp streams, per chunk, the row offsets,
+// the column/value slab and the chunk's row-local vectors into a ring of
+// shared-memory stages with 1-D bulk copies (cp.async.bulk, completion on an
+// mbarrier with an expected byte count); NCG consumer groups of R threads
+// (thread per row) compute from shared memory and release the stage on a
+// second mbarrier.  Bytes in flight per SM are (stages - 1) x stage size,
+// independent of registers and occupancy -- the r01 thread-per-row kernels
+// were latency-bound at 36-47% warp occupancy (profiles/r02_phase_kernels.txt),
+// and tools/bicg_lab.cu measured this shape at 4.2 vs 3.0 TB/s (1M DOF) and
+// 5.9 vs 3.7 TB/s (4M DOF) for the BiCGSTAB p-update + SpMV phase.
+//
+// Gathers x[col]: columns inside the chunk read the staged vectors from
+// shared memory; the rest (the +-nx band neighbours of the cavity grid) go to
+// global memory through L1/L2.  Accumulation order per row is left to right,
+// as in row_sum (cvk_engine.cuh).
+//
+// Grid: one CTA per SM, chunks assigned grid-stride (chunk = cta + i*G).  The
+// producer prefetches the k-ranges of its next 32 chunks with one load per
+// lane, so the pointer chase rp -> (ci, av) never stalls the ring.
+//
+// Alignment: bulk copies need 16-byte aligned addresses and sizes.  Vectors
+// are double2 (16 B); row offsets are copied from the chunk start (R is a
+// multiple of 4) rounded up to 4 entries, so the row-offset array carries 16
+// bytes of padding; columns are copied from floor4(k0) to ceil4(k1), so the
+// column array is followed by >= 16 bytes of allocated memory (cvk_api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cvk_engine.cuh"
+
+namespace cvk {
+
+constexpr int kStreamRows = 256;  // R: rows per chunk = threads per consumer group
+constexpr int kStreamGroups = 2;  // NCG consumer groups
+constexpr int kStreamThreads = kStreamRows * kStreamGroups + 32;
+constexpr int kStreamMaxStages = 8;
+constexpr int kStreamMaxVecs = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @P1 bra.uni DONE%=;\n"
+        " bra.uni WAIT%=;\n"
+        "DONE%=:\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Shared-memory layout of one stage (host and device agree on it).
+struct StreamLayout {
+    int capk;    // nnz capacity of a chunk (multiple of 4)
+    int nvec;    // staged row-local vectors
+    int stages;  // ring depth
+    __host__ __device__ size_t rp_bytes() const { return (size_t)(kStreamRows + 4) * 4; }
+    __host__ __device__ size_t ci_bytes() const { return (size_t)(capk + 8) * 4; }
+    __host__ __device__ size_t av_bytes() const { return (size_t)capk * 16; }
+    __host__ __device__ size_t vec_bytes() const { return (size_t)kStreamRows * 16; }
+    __host__ __device__ size_t stage_bytes() const {
+        return rp_bytes() + ci_bytes() + av_bytes() + (size_t)nvec * vec_bytes();
+    }
+    __host__ __device__ size_t smem_bytes() const { return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8; }
+};
+
+// What a consumer thread sees of its chunk.
+struct Chunk {
+    const int* rp;      // global row offsets of rows r0 .. r0+rows
+    const int* ci;      // columns, index k - k0 + cio
+    const double2* av;  // values, index k - k0
+    const double2* vec; // staged vectors, vec[j * R + l]
+    int k0, cio, r0, rows;
+    __device__ __forceinline__ double2 v(int j, int l) const { return vec[j * kStreamRows + l]; }
+    __device__ __forceinline__ bool local(int c, int& l) const {
+        l = c - r0;
+        return (unsigned)l < (unsigned)rows;
+    }
+};
+
+// Row sum for row t of the chunk: y = sum_k A[k] * x(col_k), left to right,
+// with x read through xs(l) for in-chunk columns and xg(c) otherwise.  The
+// (value, column) pairs of a batch come from shared memory; the global
+// gathers of a batch are all issued before the first product.
+template <int BATCH, class XS, class XG>
+__device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs, XG&& xg) {
+    const int b = ch.rp[t] - ch.k0, e = ch.rp[t + 1] - ch.k0;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = b; k < e; k += BATCH) {
+        double2 a[BATCH], xv[BATCH];
+        int c[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u)
+            if (k + u < e) {
+                a[u] = ch.av[k + u];
+                c[u] = ch.ci[k + u + ch.cio];
+            }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u)
+            if (k + u < e) {
+                int l;
+                xv[u] = ch.local(c[u], l) ? xs(l) : xg(c[u]);
+            }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u)
+            if (k + u < e) acc = cvk_add(acc, cvk_mul(a[u], xv[u]));
+    }
+    return acc;
+}
+
+// The producer/consumer ring.  `vecs` lists the row-local vectors to stage
+// (nullptr entries are skipped but keep their slot).  body(t, chunk) runs for
+// every row t < rows of every chunk in consumer threads.  Must be called by
+// all kStreamThreads threads of the CTA; returns when the CTA's chunks are done.
+template <class Body>
+__device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L, const double2* const* vecs,
+                                            unsigned char* smem, Body&& body) {
+    uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
+    uint64_t* empty = full + kStreamMaxStages;
+    const int n = A.n;
+    const int nchunks = (n + kStreamRows - 1) / kStreamRows;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x;
+    const int ST = L.stages;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kStreamRows);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid >= kStreamGroups * kStreamRows) {
+        const int lane = tid & 31;
+        int it = 0;
+        for (int c0 = blockIdx.x; c0 < nchunks; c0 += 32 * G) {
+            const int cj = c0 + lane * G;
+            int k0j = 0, k1j = 0;
+            if (cj < nchunks) {
+                k0j = __ldg(A.rp + cj * kStreamRows);
+                k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
+            }
+            for (int j = 0; j < 32; ++j, ++it) {
+                const int chunk = c0 + j * G;
+                if (chunk >= nchunks) break;
+                const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
+                if (lane == 0) {
+                    const int s = it % ST;
+                    mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
+                    unsigned char* sp = smem + (size_t)s * L.stage_bytes();
+                    const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
+                    const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
+                    const uint32_t b_rp = (uint32_t)(((rows + 1 + 3) & ~3) * 4);
+                    const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
+                    const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
+                    const uint32_t b_v = (uint32_t)(rows * 16);
+                    uint32_t tx = b_rp + b_ci + b_av;
+                    for (int j2 = 0; j2 < L.nvec; ++j2)
+                        if (vecs[j2]) tx += b_v;
+                    mbar_expect_tx(full + s, tx);
+                    bulk_g2s(sp, A.rp + r0, b_rp, full + s);
+                    unsigned char* q = sp + L.rp_bytes();
+                    if (b_ci) bulk_g2s(q, A.ci + a0, b_ci, full + s);
+                    q += L.ci_bytes();
+                    if (b_av) bulk_g2s(q, A.av + k0, b_av, full + s);
+                    q += L.av_bytes();
+                    for (int j2 = 0; j2 < L.nvec; ++j2, q += L.vec_bytes())
+                        if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, full + s);
+                }
+            }
+        }
+    } else {
+        const int g = tid / kStreamRows, t = tid % kStreamRows;
+        for (int chunk = blockIdx.x + g * G, it = g; chunk < nchunks; chunk += kStreamGroups * G, it += kStreamGroups) {
+            const int s = it % ST;
+            mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
+            const unsigned char* sp = smem + (size_t)s * L.stage_bytes();
+            Chunk ch;
+            ch.rp = (const int*)sp;
+            ch.ci = (const int*)(sp + L.rp_bytes());
+            ch.av = (const double2*)(sp + L.rp_bytes() + L.ci_bytes());
+            ch.vec = (const double2*)(sp + L.rp_bytes() + L.ci_bytes() + L.av_bytes());
+            ch.r0 = chunk * kStreamRows;
+            ch.rows = min(kStreamRows, n - ch.r0);
+            ch.k0 = ch.rp[0];
+            ch.cio = ch.k0 & 3;
+            if (t < ch.rows) body(t, ch);
+            mbar_arrive(empty + s);
+        }
+    }
+}
+
+}  // namespace cvk

@@ -291,3 +291,46 @@ def test_fast_paths_diagonal_kat(cvk, fast_path):
     for s in ("bicgstab", "tfqmr"):
         r = P.solve(P.solver_from_name(s), D, b, P.jacobi(D))
         assert r.report.converged and r.report.iterations == 1 and r.report.true_relres <= 1e-12
+
+
+def irregular_csr(O, n, rng, max_row=40):
+    """Rows of 1..max_row entries (many longer than one 5-entry batch, some
+    chunks far denser than others), columns anywhere -- inside and outside
+    each 256-row chunk -- plus a dominant diagonal."""
+    lens = rng.integers(0, max_row, n)
+    lens[rng.integers(0, n, n // 20)] = 0  # diagonal-only rows
+    rows = np.repeat(np.arange(n), lens)
+    cols = rng.integers(0, n, len(rows))
+    near = rng.random(len(rows)) < 0.5
+    cols[near] = np.clip(rows[near] + rng.integers(-300, 300, near.sum()), 0, n - 1)
+    vals = 0.12 * (rng.uniform(-1, 1, len(rows)) + 1j * rng.uniform(-1, 1, len(rows)))
+    rows = np.concatenate([rows, np.arange(n)])
+    cols = np.concatenate([cols, np.arange(n)])
+    vals = np.concatenate([vals, 3.0 + rng.uniform(0, 1, n) + 0.5j])
+    return O.csr_from_triplets(rows, cols, vals, n, n)
+
+
+@pytest.mark.parametrize("stream", ["streamed", "thread-per-row"])
+def test_phased_irregular_rows(cvk, oracle, monkeypatch, stream):
+    """The phase-kernel path (TMA-streamed SpMV phases and the fallback) on a
+    ragged matrix: chunk edges, rows longer than a batch, empty off-diagonal
+    rows, a partial last chunk, Jacobi and identity preconditioners."""
+    P = cvk
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    if stream != "streamed":
+        monkeypatch.setenv("CVK_NO_STREAM", "1")
+    rng = np.random.default_rng(7)
+    n = 256 * 11 + 77
+    rp, ci, v = irregular_csr(oracle, n, rng)
+    b = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    A = mat(P, rp, ci, v)
+    for s in ("bicgstab", "tfqmr"):
+        for prec in ("jacobi", "identity"):
+            M = P.jacobi(A) if prec == "jacobi" else P.identity_preconditioner()
+            x_ref, _ = oracle.solve(s, rp, ci, v, b, dinv=None if prec == "jacobi" else "identity",
+                                    tol=1e-13)
+            r = P.solve(P.solver_from_name(s), A, b, M, P.SolverOptions(tol=1e-12))
+            assert r.report.converged, (s, prec, r.report)
+            err = np.linalg.norm(r.x - x_ref) / np.linalg.norm(x_ref)
+            assert err <= 1e-10, (s, prec, err)
+            assert r.report.true_relres <= 1e-10
