@@ -579,7 +579,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     if (solver == CVK_BICGSTAB_L && o->l < 1) return fail(CVK_EINVAL, "bicgstab_l: l must be >= 1");
     if (solver == CVK_BICGSTAB_L && o->l > cvk::kMaxL)
         return fail(CVK_EINVAL, "bicgstab_l: l exceeds the device limit of 16");
-    if (solver == CVK_GMRES && (o->m < 1 || o->m > cvk::kMaxSlots))
+    if (solver == CVK_GMRES && (o->m < 1 || o->m > cvk::kMaxDots))
         return fail(CVK_EINVAL, "gmres: m must be in [1, 64]");
     if (o->max_iter < 0) return fail(CVK_EINVAL, std::string(nm) + ": negative max_iter");
     const int n = (int)A->n;

@@ -27,7 +27,8 @@ namespace cvk {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxSlots = 64;
+constexpr int kMaxDots = 64;                // GMRES(m): m <= kMaxDots
+constexpr int kMaxSlots = 2 * kMaxDots + 4;  // partial slots per region (hi and lo per reduction)
 constexpr int kRegions = 3;
 constexpr int kMinCtas = 3;  // persistent solvers: <= 80 registers, 3 CTAs (24 warps) per SM
 
@@ -197,6 +198,72 @@ __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool
 }
 
 // ----------------------------------------------------------- reductions --
+//
+// FAST reductions accumulate in double-double (each component carries
+// hi + lo, updated with Knuth's TwoSum), combine CTA and grid partials the
+// same way, and return the renormalised hi.  The per-element terms are the
+// reference's roundings (std::norm, conj(x) * y); their sum is then all but
+// exact, so the reduced scalars -- and with them iterates and iteration
+// counts -- do not depend on the grid size, the row-to-CTA mapping or which
+// FAST path (persistent, phase-kernel, streamed) ran.  REF mode keeps the
+// reference's plain sequential double sums (seq_sums).
+
+struct CAcc {
+    double2 hi = make_double2(0.0, 0.0);
+    double2 lo = make_double2(0.0, 0.0);
+};
+
+// (hi, lo) += x, renormalised (|lo| <= ulp(hi) / 2)
+__device__ __forceinline__ void dd_add1(double& hi, double& lo, double x) {
+    const double s = hi + x;
+    const double bb = s - hi;
+    double e = (hi - (s - bb)) + (x - bb);
+    e += lo;
+    hi = s + e;
+    lo = e - (hi - s);
+}
+
+// (hi, lo) += (bh, bl)
+__device__ __forceinline__ void dd_add2(double& hi, double& lo, double bh, double bl) {
+    const double s = hi + bh;
+    const double bb = s - hi;
+    double e = (hi - (s - bb)) + (bh - bb);
+    e += lo + bl;
+    hi = s + e;
+    lo = e - (hi - s);
+}
+
+__device__ __forceinline__ void cacc_add(CAcc& a, const CAcc& b) {
+    dd_add2(a.hi.x, a.lo.x, b.hi.x, b.lo.x);
+    dd_add2(a.hi.y, a.lo.y, b.hi.y, b.lo.y);
+}
+
+__device__ __forceinline__ CAcc warp_sum(CAcc v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        CAcc w;
+        w.hi.x = __shfl_xor_sync(0xffffffffu, v.hi.x, o);
+        w.hi.y = __shfl_xor_sync(0xffffffffu, v.hi.y, o);
+        w.lo.x = __shfl_xor_sync(0xffffffffu, v.lo.x, o);
+        w.lo.y = __shfl_xor_sync(0xffffffffu, v.lo.y, o);
+        // order the operands so both lanes of a pair compute the same sum
+        if (threadIdx.x & o) { CAcc t = v; v = w; w = t; }
+        cacc_add(v, w);
+    }
+    return v;
+}
+
+// partial layout: slot 2k holds the hi parts of reduction k, slot 2k+1 the lo parts
+__device__ __forceinline__ void cacc_store(double2* part, int k, int G, int cta, const CAcc& v) {
+    part[(size_t)(2 * k) * G + cta] = v.hi;
+    part[(size_t)(2 * k + 1) * G + cta] = v.lo;
+}
+__device__ __forceinline__ CAcc cacc_load(const double2* part, int k, int G, int b) {
+    CAcc v;
+    v.hi = __ldcg(part + (size_t)(2 * k) * G + b);
+    v.lo = __ldcg(part + (size_t)(2 * k + 1) * G + b);
+    return v;
+}
 
 __device__ __forceinline__ double2 warp_sum(double2 v) {
 #pragma unroll
@@ -207,23 +274,32 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
     return v;
 }
 
-// FAST: CTA partial of K slots -> part[k*G + cta]
-template <int K>
-__device__ __forceinline__ void cta_partial(const double2 (&acc)[K], double2* part, int G, int cta) {
-    __shared__ double2 sm[K][kWarps];
+// FAST: CTA partial of K reductions -> part slots 2k (hi), 2k+1 (lo)
+template <int K, int NT = kThreads>
+__device__ __forceinline__ void cta_partial(const CAcc (&acc)[K], double2* part, int G, int cta) {
+    constexpr int NW = NT / 32;
+    __shared__ CAcc sm[K][NW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const double2 v = warp_sum(acc[k]);
+        const CAcc v = warp_sum(acc[k]);
         if (lane == 0) sm[k][warp] = v;
     }
     __syncthreads();
     if (threadIdx.x < K) {
-        double2 s = sm[threadIdx.x][0];
+        CAcc s = sm[threadIdx.x][0];
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
-        part[threadIdx.x * G + cta] = s;
+        for (int w = 1; w < NW; ++w) cacc_add(s, sm[threadIdx.x][w]);
+        cacc_store(part, threadIdx.x, G, cta, s);
     }
+}
+
+// FAST: fold the G partials of reduction k (one warp; all lanes get the sum)
+__device__ __forceinline__ double2 fold_one(const double2* part, int k, int G, int lane) {
+    CAcc s;
+    for (int b = lane; b < G; b += 32) cacc_add(s, cacc_load(part, k, G, b));
+    s = warp_sum(s);
+    return s.hi;
 }
 
 // FAST: after the barrier, every CTA folds the G partials in the same order.
@@ -234,9 +310,7 @@ __device__ __forceinline__ void fold_partials(double2 (&out)[K], const double2* 
         const int lane = threadIdx.x;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            double2 s = make_double2(0.0, 0.0);
-            for (int b = lane; b < G; b += 32) s = cvk_add(s, __ldcg(part + k * G + b));
-            s = warp_sum(s);
+            const double2 s = fold_one(part, k, G, lane);
             if (lane == 0) res[k] = s;
         }
     }
@@ -265,7 +339,7 @@ __device__ __forceinline__ void seq_sums(double2 (&out)[K], int n, C&& contrib) 
 
 // One reduction phase end: partials/sequential sums + grid barrier.
 template <bool REF, int K, class C>
-__device__ __forceinline__ bool reduce(GridBar& g, const double2 (&acc)[K], double2 (&out)[K],
+__device__ __forceinline__ bool reduce(GridBar& g, const CAcc (&acc)[K], double2 (&out)[K],
                                        double2* part, int n, C&& contrib) {
     if (REF) {
         // thread 0 of every CTA re-reads whole vectors after the barrier; the
@@ -286,6 +360,12 @@ __device__ __forceinline__ bool reduce(GridBar& g, const double2 (&acc)[K], doub
 // are rounded identically.
 __device__ __forceinline__ void acc_norm(double2& a, double2 v) { a.x += cvk_norm(v); }
 __device__ __forceinline__ void acc_dot(double2& a, double2 x, double2 y) { a = cvk_add(a, cvk_cmul(x, y)); }
+__device__ __forceinline__ void acc_norm(CAcc& a, double2 v) { dd_add1(a.hi.x, a.lo.x, cvk_norm(v)); }
+__device__ __forceinline__ void acc_dot(CAcc& a, double2 x, double2 y) {
+    const double2 t = cvk_cmul(x, y);
+    dd_add1(a.hi.x, a.lo.x, t.x);
+    dd_add1(a.hi.y, a.lo.y, t.y);
+}
 
 __device__ __forceinline__ double2 prec_apply(const double2* dinv, int i, double2 y) {
     return dinv ? cvk_mul(__ldg(dinv + i), y) : y;

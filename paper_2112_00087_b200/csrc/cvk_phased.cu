@@ -44,7 +44,7 @@ struct PArgs {
     int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
 };
 
-constexpr int kPhSlots = 4;  // reduction slots per phase (max K used is 3)
+constexpr int kPhSlots = 8;  // partial slots per phase: hi + lo for up to 4 reductions
 
 __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
     return a.part + (size_t)k * kPhSlots * gridDim.x;
@@ -53,24 +53,24 @@ __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
 // Write this CTA's K partials; returns true in the CTA that arrived last,
 // with the fixed-order totals in tot (all threads of that CTA).
 template <int K, int NT = kThreads>
-__device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* counter,
+__device__ bool partial_last(const CAcc (&acc)[K], double2* part, unsigned* counter,
                              double2 (&tot)[K]) {
     constexpr int NW = NT / 32;
-    __shared__ double2 sm[K][NW];
+    __shared__ CAcc sm[K][NW];
     __shared__ int s_last;
     const int G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const double2 v = warp_sum(acc[k]);
+        const CAcc v = warp_sum(acc[k]);
         if (lane == 0) sm[k][warp] = v;
     }
     __syncthreads();
     if (threadIdx.x < K) {
-        double2 s = sm[threadIdx.x][0];
+        CAcc s = sm[threadIdx.x][0];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) s = cvk_add(s, sm[threadIdx.x][w]);
-        part[threadIdx.x * G + blockIdx.x] = s;
+        for (int w = 1; w < NW; ++w) cacc_add(s, sm[threadIdx.x][w]);
+        cacc_store(part, threadIdx.x, G, blockIdx.x, s);
         __threadfence();
     }
     __syncthreads();
@@ -80,16 +80,16 @@ __device__ bool partial_last(const double2 (&acc)[K], double2* part, unsigned* c
     __threadfence();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        double2 s = make_double2(0.0, 0.0);
-        for (int b = threadIdx.x; b < G; b += NT) s = cvk_add(s, __ldcg(part + k * G + b));
+        CAcc s;
+        for (int b = threadIdx.x; b < G; b += NT) cacc_add(s, cacc_load(part, k, G, b));
         s = warp_sum(s);
         __syncthreads();
         if (lane == 0) sm[k][warp] = s;
         __syncthreads();
-        double2 t = sm[k][0];
+        CAcc t = sm[k][0];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) t = cvk_add(t, sm[k][w]);
-        tot[k] = t;
+        for (int w = 1; w < NW; ++w) cacc_add(t, sm[k][w]);
+        tot[k] = t.hi;
     }
     if (threadIdx.x == 0) *counter = 0u;
     return true;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
         if (first) return rc;
         return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
     };
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(pnew)&, kBatch>(a.A, row, 0, valid, pnew);
         if (valid) {
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     double2* __restrict__ t = V.t;
     double2* __restrict__ x = a.x;
     auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
-    double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[3];
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(sval)&, kBatch>(a.A, row, 0, valid, sval);
         if (valid) {
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     const double2 omega = st->omega, nom = cvk_neg(st->omega);
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     const double2* __restrict__ s = V.s;
     const double2* __restrict__ t = V.t;
     const double2* __restrict__ sh = V.sh;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     TfVecs V(a.work, (size_t)n);
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri; V.sh[i] = ri; V.w[i] = ri; V.u0[i] = ri;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     TfVecs V(a.work, (size_t)n);
     const double2* __restrict__ u0 = V.u0;
     auto uat = [&](int c) -> double2 { return u0[c]; };
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uat)&, kBatch>(a.A, row, 0, valid, uat);
         if (valid) {
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
     const double2 nal = cvk_neg(st->alpha);
     const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
     const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     struct L4 { double2 w, au, d, u; };
     for_elems_batched<kElemBatch>(
         n, [&](int i) { return L4{V.w[i], V.au[i], V.d[i], uc[i]}; },
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uval)&, kBatch>(a.A, row, 0, valid, uval);
         if (valid) {
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(unext)&, kBatch>(a.A, row, 0, valid, unext);
         if (valid) {
@@ -521,7 +521,7 @@ __device__ __forceinline__ double2 prec_staged(const PArgs& a, const Chunk& ch, 
     return a.dinv ? cvk_mul(ch.v(j, t), y) : y;
 }
 
-__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
+__global__ void __maxnreg__(112) k_bi_a_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
     const StreamLayout L{a.capk, 5, a.st5};
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {
             const double2 rc = ch.v(0, l);
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     st->alpha = cvk_cdiv(st->rho, tot[0]);
 }
 
-__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
+__global__ void __maxnreg__(112) k_bi_b_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
     const StreamLayout L{a.capk, 5, a.st5};
-    double2 acc[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[3];
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
 }
 
 // even tail + odd head of tfQMR (k_tf_e) on the ring
-__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
+__global__ void __maxnreg__(112) k_tf_e_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
     const StreamLayout L{a.capk, 7, a.st7};
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
 }
 
 // odd tail of tfQMR (k_tf_o) on the ring
-__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
+__global__ void __maxnreg__(112) k_tf_o_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
     const StreamLayout L{a.capk, 8, a.st8};
-    double2 acc[1] = {make_double2(0, 0)};
+    CAcc acc[1];
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     const int n = a.A.n;
     const double2* __restrict__ x = a.x;
     auto xat = [&](int c) -> double2 { return x[c]; };
-    double2 acc[2] = {make_double2(0, 0), make_double2(0, 0)};
+    CAcc acc[2];
     if (!st->skip_true) {
         for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
             const double2 y = row_sum<1, decltype(xat)&, kBatch>(a.A, row, 0, valid, xat);

@@ -334,3 +334,30 @@ def test_phased_irregular_rows(cvk, oracle, monkeypatch, stream):
             err = np.linalg.norm(r.x - x_ref) / np.linalg.norm(x_ref)
             assert err <= 1e-10, (s, prec, err)
             assert r.report.true_relres <= 1e-10
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "tfqmr"])
+def test_fast_paths_bitwise_identical(cvk, golden, monkeypatch, solver):
+    """FAST reductions are double-double (cvk_engine.cuh): the reduced scalars
+    do not depend on grid size or row-to-CTA mapping, so the persistent
+    kernel, the thread-per-row phase kernels and the TMA-streamed phase
+    kernels -- three different decompositions -- produce the same bits."""
+    P = cvk
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    out = {}
+    for path, env in (("persistent", {"CVK_PHASED_MIN_N": "1000000000"}),
+                      ("phased", {"CVK_PHASED_MIN_N": "0", "CVK_NO_STREAM": "1"}),
+                      ("streamed", {"CVK_PHASED_MIN_N": "0"}),
+                      ("persistent-small-grid", {"CVK_PHASED_MIN_N": "1000000000", "CVK_MAX_CTAS": "3"})):
+        for k in ("CVK_PHASED_MIN_N", "CVK_NO_STREAM", "CVK_MAX_CTAS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-10))
+        out[path] = (r.report.iterations, bits(r.x))
+    it0, x0 = out["persistent"]
+    for path, (it, x) in out.items():
+        assert it == it0, (path, it, it0)
+        assert np.array_equal(x, x0), path
