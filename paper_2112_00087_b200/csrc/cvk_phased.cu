@@ -521,7 +521,7 @@ __device__ __forceinline__ double2 prec_staged(const PArgs& a, const Chunk& ch, 
     return a.dinv ? cvk_mul(ch.v(j, t), y) : y;
 }
 
-__global__ void __maxnreg__(112) k_bi_a_s(PArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -567,7 +567,7 @@ __global__ void __maxnreg__(112) k_bi_a_s(PArgs a) {
     st->alpha = cvk_cdiv(st->rho, tot[0]);
 }
 
-__global__ void __maxnreg__(112) k_bi_b_s(PArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -616,7 +616,7 @@ __global__ void __maxnreg__(112) k_bi_b_s(PArgs a) {
 }
 
 // even tail + odd head of tfQMR (k_tf_e) on the ring
-__global__ void __maxnreg__(112) k_tf_e_s(PArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;
@@ -670,7 +670,7 @@ __global__ void __maxnreg__(112) k_tf_e_s(PArgs a) {
 }
 
 // odd tail of tfQMR (k_tf_o) on the ring
-__global__ void __maxnreg__(112) k_tf_o_s(PArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
     PState* st = a.st;

@@ -35,7 +35,11 @@
 
 namespace cvk {
 
-constexpr int kStreamRows = 256;  // R: rows per chunk = threads per consumer group
+// R = 240 rows per chunk: 2 x 240 consumers + 1 producer warp = 16 warps, so
+// the register file allows 128 registers per thread (17 warps would be
+// allocated as 20 and cap the kernels at 96 registers, with spills).
+// R must be a multiple of 4 (16-byte aligned row-offset copies).
+constexpr int kStreamRows = 240;  // R: rows per chunk = threads per consumer group
 constexpr int kStreamGroups = 2;  // NCG consumer groups
 constexpr int kStreamThreads = kStreamRows * kStreamGroups + 32;
 constexpr int kStreamMaxStages = 8;
