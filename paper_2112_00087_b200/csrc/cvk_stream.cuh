@@ -35,11 +35,13 @@
 
 namespace cvk {
 
-// R = 240 rows per chunk: 2 x 240 consumers + 1 producer warp = 16 warps, so
-// the register file allows 128 registers per thread (17 warps would be
-// allocated as 20 and cap the kernels at 96 registers, with spills).
-// R must be a multiple of 4 (16-byte aligned row-offset copies).
-constexpr int kStreamRows = 240;  // R: rows per chunk = threads per consumer group
+// R = 224 rows per chunk: 2 x 7 consumer warps + 1 producer warp = 15 warps
+// (allocated as 16), so the register file allows 128 registers per thread;
+// 256-row groups (17 warps, allocated as 20) cap the kernels at 96 registers
+// with spills, and 240-row groups split a warp between the two groups (that
+// warp then serves both rings: 168 vs 114 us per BiCGSTAB iteration, 1M DOF).
+// R must be a multiple of 4 (16-byte aligned row-offset copies) and of 32.
+constexpr int kStreamRows = 224;  // R: rows per chunk = threads per consumer group
 constexpr int kStreamGroups = 2;  // NCG consumer groups
 constexpr int kStreamThreads = kStreamRows * kStreamGroups + 32;
 constexpr int kStreamMaxStages = 8;
