@@ -12,7 +12,8 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "libcavac_b200.so")
+# CVK_LIB_PATH: measurement builds of the same sources (tools/variant_build.sh)
+LIB_PATH = os.environ.get("CVK_LIB_PATH") or os.path.join(PKG, "libcavac_b200.so")
 HEADER = os.path.join(ROOT, "include", "cavac_b200.h")
 
 CVK_OK = 0

@@ -449,7 +449,9 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     auto stages_for = [&](int nvec) {
         cvk::StreamLayout L{A->capk, nvec, 1};
         const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8;
-        return (int)std::min<long long>(cvk::kStreamMaxStages, std::max<long long>(0, avail / (long long)L.stage_bytes()));
+        long long cap = cvk::kStreamMaxStages;
+        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
+        return (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));
     };
     const int st5 = stages_for(5), st7 = stages_for(7), st8 = stages_for(8);
     const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&

@@ -86,7 +86,7 @@ constexpr int kDotBlocks = 592;  // 4 x 148: fixed, so the FAST sum order is fix
 __global__ void __launch_bounds__(kThreads) k_dot_stage1(int n, const double2* __restrict__ x,
                                                          const double2* __restrict__ y,
                                                          double2* __restrict__ part) {
-    CAcc acc[1];
+    CAcc acc[1] = {};
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 xi = __ldg(x + i);
         if (y) acc_dot(acc[0], xi, __ldg(y + i));

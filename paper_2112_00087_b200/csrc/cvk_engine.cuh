@@ -208,12 +208,14 @@ __device__ __forceinline__ double2 row_sum(const Csr& A, int row, int lane, bool
 // FAST path (persistent, phase-kernel, streamed) ran.  REF mode keeps the
 // reference's plain sequential double sums (seq_sums).
 
-struct CAcc {
-    double2 hi = make_double2(0.0, 0.0);
-    double2 lo = make_double2(0.0, 0.0);
+struct CAcc {  // aggregate: declare as `CAcc a = {};` (zero); no initialisers so __shared__ arrays are legal
+    double2 hi, lo;
 };
 
 // (hi, lo) += x, renormalised (|lo| <= ulp(hi) / 2)
+#ifdef CVK_REDUCE_PLAIN  // measurement variant only (tools/): plain double sums
+__device__ __forceinline__ void dd_add1(double& hi, double&, double x) { hi += x; }
+#else
 __device__ __forceinline__ void dd_add1(double& hi, double& lo, double x) {
     const double s = hi + x;
     const double bb = s - hi;
@@ -222,6 +224,7 @@ __device__ __forceinline__ void dd_add1(double& hi, double& lo, double x) {
     hi = s + e;
     lo = e - (hi - s);
 }
+#endif
 
 // (hi, lo) += (bh, bl)
 __device__ __forceinline__ void dd_add2(double& hi, double& lo, double bh, double bl) {
@@ -296,7 +299,7 @@ __device__ __forceinline__ void cta_partial(const CAcc (&acc)[K], double2* part,
 
 // FAST: fold the G partials of reduction k (one warp; all lanes get the sum)
 __device__ __forceinline__ double2 fold_one(const double2* part, int k, int G, int lane) {
-    CAcc s;
+    CAcc s = {};
     for (int b = lane; b < G; b += 32) cacc_add(s, cacc_load(part, k, G, b));
     s = warp_sum(s);
     return s.hi;

@@ -43,7 +43,7 @@ template <int S, bool REF>
 __device__ bool true_relres(GridBar& g, const KArgs& a, double2* scratch, double2* part,
                             double& out) {
     const int n = a.A.n;
-    CAcc acc[2];
+    CAcc acc[2] = {};
     const double2* x = a.x;
     const double2* b = a.b;
     for_rows<S>(n, a.G, g.cta, [&](int row, int lane, bool valid) {
@@ -88,7 +88,7 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
     long long hl = 0;
 
     // r = M^{-1} b, shadow = r, x = 0; ||r||^2 and <shadow, r>
-    CAcc acc0[2];
+    CAcc acc0[2] = {};
     for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri;
@@ -138,7 +138,7 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
             return cvk_add(cvk_mul(beta, tmp), rc);
         };
         // phase A: v = M^{-1} A p; gamma = <shadow, v>
-        CAcc accA[1];
+        CAcc accA[1] = {};
         for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, pnew);
             if (valid && lane == 0) {
@@ -157,7 +157,7 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
         const double2 nal = cvk_neg(alpha);
         // s = r - alpha v (axpy copy), x += alpha p; t = M^{-1} A s
         auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
-        CAcc accB[3];
+        CAcc accB[3] = {};
         for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, sval);
             if (valid && lane == 0) {
@@ -187,7 +187,7 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
         omega = cvk_cdiv(tB[2], tB[1]);
         const double2 nom2 = cvk_neg(omega);
         // x += omega s; r = s - omega t; ||r||^2, <shadow, r>
-        CAcc accC[2];
+        CAcc accC[2] = {};
         for_elems(n, G, g.cta, [&](int i) {
             const double2 si = s[i];
             x[i] = cvk_add(x[i], cvk_mul(omega, si));
@@ -234,7 +234,7 @@ __device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
     long long hl = 0;
     const double tol = a.tol;
 
-    CAcc acc0[2];
+    CAcc acc0[2] = {};
     for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri; sh[i] = ri; w[i] = ri; uu[0][i] = ri;
@@ -258,7 +258,7 @@ __device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
     // au = M^{-1} A u; v = au; sigma = <shadow, v>
     {
         const double2* u0 = uu[0];
-        CAcc acc[1];
+        CAcc acc[1] = {};
         for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
             const double2 y = row_sum<S>(a.A, row, lane, valid, [&](int c) { return u0[c]; });
             if (valid && lane == 0) {
@@ -291,7 +291,7 @@ __device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
         {
             const double2 coef = cvk_cdiv(cvk_scale(theta * theta, eta), alpha);
             const double2* uc = uu[cur];
-            CAcc acc[1];
+            CAcc acc[1] = {};
             for_elems(n, G, g.cta, [&](int i) {
                 const double2 wi = cvk_add(w[i], cvk_mul(nal, au[i]));
                 w[i] = wi;
@@ -320,7 +320,7 @@ __device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
             const double2* uc = uu[cur];
             double2* un = uu[cur ^ 1];
             auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, v[c])); };
-            CAcc acc[2];
+            CAcc acc[2] = {};
             for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                 const double2 y = row_sum<S>(a.A, row, lane, valid, uval);
                 if (valid && lane == 0) {
@@ -365,7 +365,7 @@ __device__ __forceinline__ void tfqmr_body(const KArgs& a, GridBar& g) {
             const double2* uc2 = uu[cur];
             double2* un2 = uu[cur ^ 1];
             auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc2[c])); };
-            CAcc accO[1];
+            CAcc accO[1] = {};
             for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                 const double2 y = row_sum<S>(a.A, row, lane, valid, unext);
                 if (valid && lane == 0) {
@@ -425,7 +425,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
     long long hl = 0;
     const double tol = a.tol;
 
-    CAcc acc0[2];
+    CAcc acc0[2] = {};
     {
         double2* r0 = R(0);
         for_elems(n, G, g.cta, [&](int i) {
@@ -472,7 +472,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
                 double2* uj_new = vbase + (size_t)ui[L + 1] * n;  // spare
                 double2* uj1 = U(j + 1);
                 auto ujv = [&](int c) -> double2 { return cvk_add(cvk_mul(nbeta, uj_old[c]), rj[c]); };
-                CAcc acc[1];
+                CAcc acc[1] = {};
                 for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                     const double2 y = row_sum<S>(a.A, row, lane, valid, ujv);
                     if (valid && lane == 0) {
@@ -507,7 +507,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
                 double2* rj_new = vbase + (size_t)ri[L + 1] * n;
                 double2* rj1 = R(j + 1);
                 auto rjv = [&](int c) -> double2 { return cvk_add(rj_old[c], cvk_mul(nal, uj1[c])); };
-                CAcc acc[2];
+                CAcc acc[2] = {};
                 for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
                     const double2 y = row_sum<S>(a.A, row, lane, valid, rjv);
                     if (valid && lane == 0) {
@@ -547,7 +547,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
         if (broke) {
             // krylov.cpp:208-222 (needs ||r_0|| of the current r_0)
             double2 tn[1];
-            CAcc accn[1];
+            CAcc accn[1] = {};
             double2* r0 = R(0);
             for_elems(n, G, g.cta, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
             ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
@@ -575,7 +575,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
                 const double2* ri1 = R(i + 1);
                 const double2* r0 = R(0);
                 const bool last = (i == j);
-                CAcc acc[2];
+                CAcc acc[2] = {};
                 for_elems(n, G, g.cta, [&](int e) {
                     double2 v = rj1[e];
                     if (has_upd) { v = cvk_add(v, cvk_mul(ntau, rprev[e])); rj1[e] = v; }
@@ -604,7 +604,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
         if (!ok) break;
         if (mrbroke) {
             double2 tn[1];
-            CAcc accn[1];
+            CAcc accn[1] = {};
             double2* r0 = R(0);
             for_elems(n, G, g.cta, [&](int i) { if (!REF) acc_norm(accn[0], r0[i]); });
             ok = reduce<REF, 1>(g, accn, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], r0[i]); });
@@ -632,7 +632,7 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
         __syncthreads();
         omega = gam_s[L - 1];
         // updates (krylov.cpp:264-271), per element in the reference's order
-        CAcc accU[2];
+        CAcc accU[2] = {};
         {
             double2* r0 = R(0);
             double2* u0 = U(0);
@@ -705,7 +705,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     auto multi_dot = [&](const double2* wv, int cnt, double2* pr) {
         for (int k = 0; k < cnt; ++k) {
             const double2* vk = V + (size_t)k * n;
-            CAcc s;
+            CAcc s = {};
             for_elems(n, G, g.cta, [&](int i) { acc_dot(s, vk[i], wv[i]); });
             s = warp_sum(s);
             if (lane == 0) hsm[k][warp] = s;
@@ -739,7 +739,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     };
 
     // r = M^{-1} b, x = 0, ||r||
-    CAcc acc0[1];
+    CAcc acc0[1] = {};
     for_elems(n, G, g.cta, [&](int i) {
         const double2 ri = prec_apply(dinv, i, __ldg(b + i));
         r[i] = ri;
@@ -830,7 +830,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
             // ---- R2: w -= V h2; ||w||
             double hn;
             {
-                CAcc acc[1];
+                CAcc acc[1] = {};
                 for_elems(n, G, g.cta, [&](int i) {
                     double2 wi = w[i];
                     for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h2[q]), V[(size_t)q * n + i]));
@@ -895,7 +895,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
         ok = g.sync();
         if (!ok || stop) break;
         // restart residual r = M^{-1}(b - A x)
-        CAcc acc[1];
+        CAcc acc[1] = {};
         for_rows<S>(n, G, g.cta, [&](int row, int ln, bool valid) {
             const double2 y = row_sum<S>(a.A, row, ln, valid, [&](int c) { return x[c]; });
             if (valid && ln == 0) {

@@ -80,7 +80,7 @@ __device__ bool partial_last(const CAcc (&acc)[K], double2* part, unsigned* coun
     __threadfence();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        CAcc s;
+        CAcc s = {};
         for (int b = threadIdx.x; b < G; b += NT) cacc_add(s, cacc_load(part, k, G, b));
         s = warp_sum(s);
         __syncthreads();
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
-    CAcc acc[2];
+    CAcc acc[2] = {};
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_a(PArgs a) {
         if (first) return rc;
         return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
     };
-    CAcc acc[1];
+    CAcc acc[1] = {};
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(pnew)&, kBatch>(a.A, row, 0, valid, pnew);
         if (valid) {
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_b(PArgs a) {
     double2* __restrict__ t = V.t;
     double2* __restrict__ x = a.x;
     auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
-    CAcc acc[3];
+    CAcc acc[3] = {};
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(sval)&, kBatch>(a.A, row, 0, valid, sval);
         if (valid) {
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     const double2 omega = st->omega, nom = cvk_neg(st->omega);
-    CAcc acc[2];
+    CAcc acc[2] = {};
     const double2* __restrict__ s = V.s;
     const double2* __restrict__ t = V.t;
     const double2* __restrict__ sh = V.sh;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init(PArgs a) {
     pdl_enter();
     const int n = a.A.n;
     TfVecs V(a.work, (size_t)n);
-    CAcc acc[2];
+    CAcc acc[2] = {};
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
         V.r[i] = ri; V.sh[i] = ri; V.w[i] = ri; V.u0[i] = ri;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_init2(PArgs a) {
     TfVecs V(a.work, (size_t)n);
     const double2* __restrict__ u0 = V.u0;
     auto uat = [&](int c) -> double2 { return u0[c]; };
-    CAcc acc[1];
+    CAcc acc[1] = {};
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uat)&, kBatch>(a.A, row, 0, valid, uat);
         if (valid) {
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_w(PArgs a) {
     const double2 nal = cvk_neg(st->alpha);
     const double2 coef = cvk_cdiv(cvk_scale(st->theta * st->theta, st->eta), st->alpha);
     const double2* __restrict__ uc = st->cur ? V.u1 : V.u0;
-    CAcc acc[1];
+    CAcc acc[1] = {};
     struct L4 { double2 w, au, d, u; };
     for_elems_batched<kElemBatch>(
         n, [&](int i) { return L4{V.w[i], V.au[i], V.d[i], uc[i]}; },
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_e(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     auto uval = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
-    CAcc acc[2];
+    CAcc acc[2] = {};
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(uval)&, kBatch>(a.A, row, 0, valid, uval);
         if (valid) {
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kThreads) k_tf_o(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     auto unext = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
-    CAcc acc[1];
+    CAcc acc[1] = {};
     for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
         const double2 y = row_sum<1, decltype(unext)&, kBatch>(a.A, row, 0, valid, unext);
         if (valid) {
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
     const StreamLayout L{a.capk, 5, a.st5};
-    CAcc acc[1];
+    CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {
             const double2 rc = ch.v(0, l);
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
     const StreamLayout L{a.capk, 5, a.st5};
-    CAcc acc[3];
+    CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
     const StreamLayout L{a.capk, 7, a.st7};
-    CAcc acc[2];
+    CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
     const StreamLayout L{a.capk, 8, a.st8};
-    CAcc acc[1];
+    CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
         auto xg = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     const int n = a.A.n;
     const double2* __restrict__ x = a.x;
     auto xat = [&](int c) -> double2 { return x[c]; };
-    CAcc acc[2];
+    CAcc acc[2] = {};
     if (!st->skip_true) {
         for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
             const double2 y = row_sum<1, decltype(xat)&, kBatch>(a.A, row, 0, valid, xat);

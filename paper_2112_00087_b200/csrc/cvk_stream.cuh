@@ -41,8 +41,14 @@ namespace cvk {
 // with spills, and 240-row groups split a warp between the two groups (that
 // warp then serves both rings: 168 vs 114 us per BiCGSTAB iteration, 1M DOF).
 // R must be a multiple of 4 (16-byte aligned row-offset copies) and of 32.
-constexpr int kStreamRows = 224;  // R: rows per chunk = threads per consumer group
-constexpr int kStreamGroups = 2;  // NCG consumer groups
+#ifndef CVK_STREAM_ROWS
+#define CVK_STREAM_ROWS 224
+#endif
+#ifndef CVK_STREAM_GROUPS
+#define CVK_STREAM_GROUPS 2
+#endif
+constexpr int kStreamRows = CVK_STREAM_ROWS;      // R: rows per chunk = threads per consumer group
+constexpr int kStreamGroups = CVK_STREAM_GROUPS;  // NCG consumer groups
 constexpr int kStreamThreads = kStreamRows * kStreamGroups + 32;
 constexpr int kStreamMaxStages = 8;
 constexpr int kStreamMaxVecs = 8;

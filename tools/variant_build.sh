@@ -1,0 +1,18 @@
+#!/bin/bash
+# Build a measurement variant of libcavac_b200.so with extra nvcc defines:
+#   tools/variant_build.sh <name> -DFOO ...   ->  _variants/<name>/libcavac_b200.so
+# Select it at run time with CVK_LIB_PATH=_variants/<name>/libcavac_b200.so
+set -e
+cd "$(dirname "$0")/.."
+name=$1; shift
+out=_variants/$name
+mkdir -p $out
+objs=()
+for f in cvk_api cvk_blas cvk_krylov cvk_phased cvk_ddm; do
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
+    -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude "$@" -c paper_2112_00087_b200/csrc/$f.cu -o $out/$f.o &
+  objs+=($out/$f.o)
+done
+wait
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libcavac_b200.so "${objs[@]}" -lcudart
+echo $out/libcavac_b200.so
