@@ -124,6 +124,9 @@ int cvk_fail(int code, const std::string& msg) { return fail(code, msg); }
 extern "C" {
 
 int cvk_abi_version(void) { return CVK_ABI_VERSION; }
+
+// measurement builds only (CVK_TRACE): not part of include/cavac_b200.h
+int cvk_trace_read(void* out, size_t bytes) { return cvk::phased_trace_read(out, bytes); }
 const char* cvk_last_error(void) { return g_err.c_str(); }
 
 const char* cvk_breakdown_name(int code) {

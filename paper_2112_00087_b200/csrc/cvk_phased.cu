@@ -44,53 +44,116 @@ struct PArgs {
     int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
 };
 
+// ------------------------------------------------------------ tracing --
+// CVK_TRACE builds (tools/variant_build.sh trace -DCVK_TRACE) record per-CTA
+// globaltimer stamps of the phase kernels: [kernel][iteration % 16][cta][4]
+// = entry (after the PDL wait), main loop done (CTA-wide), partial published,
+// fold done (last CTA only).  Read with cvk_trace_read().
+#ifdef CVK_TRACE
+constexpr int kTrK = 4, kTrIt = 16, kTrCta = 1024;
+__device__ unsigned long long g_trace[kTrK * kTrIt * kTrCta * 4];
+__device__ __forceinline__ unsigned long long tr_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TR(kid, it, slot) \
+    do { if (threadIdx.x == 0 && blockIdx.x < kTrCta) \
+        g_trace[((((kid) * kTrIt + ((it) % kTrIt)) * kTrCta) + blockIdx.x) * 4 + (slot)] = tr_now(); } while (0)
+#else
+#define TR(kid, it, slot) do { } while (0)
+#endif
+
 constexpr int kPhSlots = 8;  // partial slots per phase: hi + lo for up to 4 reductions
 
 __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
     return a.part + (size_t)k * kPhSlots * gridDim.x;
 }
 
-// Write this CTA's K partials; returns true in the CTA that arrived last,
-// with the fixed-order totals in tot (all threads of that CTA).
+// K-wide double-double butterfly over a warp: every lane ends with the same
+// K sums (operands ordered by lane, so the pairs agree bit for bit).  The
+// step loop is kept rolled: this epilogue runs once per CTA from a cold
+// instruction cache, and the unrolled form (K x 5 steps x 4 shuffles + dd
+// adds, plus unrolled cross-warp chains) cost 5 us per reduction in the
+// last CTA's fold (tools/trace_phase.py).
+template <int K>
+__device__ __forceinline__ void warp_sum_k(CAcc (&v)[K]) {
+#pragma unroll 1
+    for (int o = 16; o > 0; o >>= 1) {
+        const bool up = (threadIdx.x & o) != 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            CAcc w;
+            w.hi.x = __shfl_xor_sync(0xffffffffu, v[k].hi.x, o);
+            w.hi.y = __shfl_xor_sync(0xffffffffu, v[k].hi.y, o);
+            w.lo.x = __shfl_xor_sync(0xffffffffu, v[k].lo.x, o);
+            w.lo.y = __shfl_xor_sync(0xffffffffu, v[k].lo.y, o);
+            CAcc a = up ? w : v[k];
+            const CAcc b = up ? v[k] : w;
+            cacc_add(a, b);
+            v[k] = a;
+        }
+    }
+}
+
+// CTA sum of K accumulators: warp butterflies, then warp 0 combines the
+// per-warp sums with a second butterfly.  Result valid in warp 0.
+template <int K, int NT>
+__device__ __forceinline__ void cta_sum_k(CAcc (&v)[K], CAcc (*sm)[32]) {
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    warp_sum_k<K>(v);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (lane < NW) v[k] = sm[k][lane];
+            else v[k] = CAcc{};
+        }
+        warp_sum_k<K>(v);
+    }
+}
+
+// Publish this CTA's K partials; returns true in the CTA that arrived last,
+// with the grid totals in tot (valid in thread 0 -- callers continue with
+// thread 0 only).
 template <int K, int NT = kThreads>
 __device__ bool partial_last(const CAcc (&acc)[K], double2* part, unsigned* counter,
-                             double2 (&tot)[K]) {
-    constexpr int NW = NT / 32;
-    __shared__ CAcc sm[K][NW];
+                             double2 (&tot)[K], int kid = -1, long long it = 0) {
+    __shared__ CAcc sm[K][32];
     __shared__ int s_last;
     const int G = gridDim.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    CAcc v[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const CAcc v = warp_sum(acc[k]);
-        if (lane == 0) sm[k][warp] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < K) {
-        CAcc s = sm[threadIdx.x][0];
+    for (int k = 0; k < K; ++k) v[k] = acc[k];
+    cta_sum_k<K, NT>(v, sm);
+    if (kid >= 0) TR(kid, it, 1);
+    if (threadIdx.x == 0) {
 #pragma unroll
-        for (int w = 1; w < NW; ++w) cacc_add(s, sm[threadIdx.x][w]);
-        cacc_store(part, threadIdx.x, G, blockIdx.x, s);
+        for (int k = 0; k < K; ++k) cacc_store(part, k, G, blockIdx.x, v[k]);
         __threadfence();
+        s_last = (atomicAdd(counter, 1u) == (unsigned)G - 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == (unsigned)G - 1u);
-    __syncthreads();
+    if (kid >= 0) TR(kid, it, 2);
     if (!s_last) return false;
     __threadfence();
+    CAcc s[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        CAcc s = {};
-        for (int b = threadIdx.x; b < G; b += NT) cacc_add(s, cacc_load(part, k, G, b));
-        s = warp_sum(s);
-        __syncthreads();
-        if (lane == 0) sm[k][warp] = s;
-        __syncthreads();
-        CAcc t = sm[k][0];
+    for (int k = 0; k < K; ++k) s[k] = CAcc{};
+#pragma unroll 1
+    for (int b = threadIdx.x; b < G; b += NT) {
 #pragma unroll
-        for (int w = 1; w < NW; ++w) cacc_add(t, sm[k][w]);
-        tot[k] = t.hi;
+        for (int k = 0; k < K; ++k) cacc_add(s[k], cacc_load(part, k, G, b));
     }
+    cta_sum_k<K, NT>(s, sm);
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = s[k].hi;
+    if (kid >= 0) TR(kid, it, 3);
     if (threadIdx.x == 0) *counter = 0u;
     return true;
 }
@@ -274,6 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
+    TR(0, st->it, 0);
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     const double2 omega = st->omega, nom = cvk_neg(st->omega);
@@ -294,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
             acc_dot(acc[1], v.sh, ri);
         });
     double2 tot[2];
-    if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot)) return;
+    if (!partial_last<2>(acc, partv(a, 0), &st->counter[0], tot, 0, st->it)) return;
     if (threadIdx.x != 0) return;
     const double relres = sqrt(tot[0].x) / st->bnorm;
     st->final_relres = relres;
@@ -526,6 +590,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
+    TR(1, st->it, 0);
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     const int cur = st->cur;
@@ -558,7 +623,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         acc_dot(acc[0], ch.v(3, t), vi);
     });
     double2 tot[1];
-    if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
     if (threadIdx.x != 0) return;
     if (cvk_abs(tot[0]) < st->brk) {
         st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
@@ -572,6 +637,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
+    TR(2, st->it, 0);
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     const int cur = st->cur;
@@ -600,7 +666,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
         acc_dot(acc[2], ti, si);
     });
     double2 tot[3];
-    if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot)) return;
+    if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
     const double relres = sqrt(tot[0].x) / st->bnorm;
     if (relres <= st->tol) {
@@ -768,6 +834,16 @@ PhasedKernels kernels_all() {
 }  // namespace
 
 PhasedKernels phased_kernels() { return kernels_all(); }
+
+int phased_trace_read(void* out, size_t bytes) {
+#ifdef CVK_TRACE
+    const size_t n = sizeof(g_trace) < bytes ? sizeof(g_trace) : bytes;
+    return cudaMemcpyFromSymbol(out, g_trace, n) == cudaSuccess ? (int)n : -1;
+#else
+    (void)out; (void)bytes;
+    return 0;
+#endif
+}
 
 size_t phased_args_size() { return sizeof(PArgs); }
 

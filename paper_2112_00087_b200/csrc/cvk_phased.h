@@ -30,6 +30,8 @@ struct PhasedKernels {
 };
 
 PhasedKernels phased_kernels();
+// CVK_TRACE builds: copy the phase-kernel timestamp buffer (bytes copied, 0 otherwise)
+int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
