@@ -452,7 +452,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     auto stages_for = [&](int nvec) {
         cvk::StreamLayout L{A->capk, nvec, 1};
         const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8;
-        long long cap = cvk::kStreamMaxStages;
+        long long cap = 4;  // 4-stage ring (measured: 4 >= 5, 3, 2 on the 1M-DOF cavity)
         if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
         return (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));
     };
@@ -464,7 +464,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096));
     // elementwise phases: grid-stride, 4 elements per thread per trip
-    long long Ge = std::min<long long>(4LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
+    long long Ge = std::min<long long>(2LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
     if (const char* env = std::getenv("CVK_ELEM_CTAS")) Ge = std::max(1, std::atoi(env));
     if (!streamed) Ge = G;
     const long long Gmax = std::max<long long>(std::max<long long>(G, Ge), c->nsm);
@@ -472,7 +472,8 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, st5, st7, st8);
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, st5, st7, st8,
+                          std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};

@@ -42,6 +42,7 @@ struct PArgs {
     DevReport* rep;
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
     int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
+    int contig;         // streamed chunk assignment (StreamLayout::contig)
 };
 
 // ------------------------------------------------------------ tracing --
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ pn = cur ? V.p0 : V.p1;
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
-    const StreamLayout L{a.capk, 5, a.st5};
+    const StreamLayout L{a.capk, 5, a.st5, a.contig};
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ t_ = V.t;
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
-    const StreamLayout L{a.capk, 5, a.st5};
+    const StreamLayout L{a.capk, 5, a.st5, a.contig};
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
-    const StreamLayout L{a.capk, 7, a.st7};
+    const StreamLayout L{a.capk, 7, a.st7, a.contig};
     CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -748,7 +749,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
-    const StreamLayout L{a.capk, 8, a.st8};
+    const StreamLayout L{a.capk, 8, a.st8, a.contig};
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
@@ -849,8 +850,9 @@ size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8) {
+                      int capk, int st5, int st7, int st8, int contig) {
     PArgs* p = (PArgs*)out;
+    p->contig = contig;
     p->capk = capk;
     p->st5 = st5;
     p->st7 = st7;

@@ -35,6 +35,6 @@ int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8);
+                      int capk, int st5, int st7, int st8, int contig);
 
 }  // namespace cvk

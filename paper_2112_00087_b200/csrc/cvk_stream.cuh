@@ -83,6 +83,7 @@ struct StreamLayout {
     int capk;    // nnz capacity of a chunk (multiple of 4)
     int nvec;    // staged row-local vectors
     int stages;  // ring depth
+    int contig = 0;  // 1: each CTA takes a contiguous block of chunks; 0: grid-stride
     __host__ __device__ size_t rp_bytes() const { return (size_t)(kStreamRows + 4) * 4; }
     __host__ __device__ size_t ci_bytes() const { return (size_t)(capk + 8) * 4; }
     __host__ __device__ size_t av_bytes() const { return (size_t)capk * 16; }
@@ -159,19 +160,25 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // this CTA's chunks: chunk_of(i), i < cnt
+    const int cpc = (nchunks + G - 1) / G;
+    const int first = L.contig ? blockIdx.x * cpc : blockIdx.x;
+    const int cnt = L.contig ? max(0, min(nchunks, first + cpc) - first)
+                             : (blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / G + 1 : 0);
+    const int step = L.contig ? 1 : G;
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
-        int it = 0;
-        for (int c0 = blockIdx.x; c0 < nchunks; c0 += 32 * G) {
-            const int cj = c0 + lane * G;
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int cj = first + (i0 + lane) * step;
             int k0j = 0, k1j = 0;
-            if (cj < nchunks) {
+            if (i0 + lane < cnt) {
                 k0j = __ldg(A.rp + cj * kStreamRows);
                 k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
             }
-            for (int j = 0; j < 32; ++j, ++it) {
-                const int chunk = c0 + j * G;
-                if (chunk >= nchunks) break;
+            for (int j = 0; j < 32; ++j) {
+                const int it = i0 + j;
+                if (it >= cnt) break;
+                const int chunk = first + it * step;
                 const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
                 if (lane == 0) {
                     const int s = it % ST;
@@ -200,7 +207,8 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
         }
     } else {
         const int g = tid / kStreamRows, t = tid % kStreamRows;
-        for (int chunk = blockIdx.x + g * G, it = g; chunk < nchunks; chunk += kStreamGroups * G, it += kStreamGroups) {
+        for (int it = g; it < cnt; it += kStreamGroups) {
+            const int chunk = first + it * step;
             const int s = it % ST;
             mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
             const unsigned char* sp = smem + (size_t)s * L.stage_bytes();
