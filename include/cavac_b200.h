@@ -27,8 +27,11 @@
  *   cvk_set_exec_mode     set_exec_mode (src/numkit.cpp:29-30)
  *   cvk_schwarz_solve     schwarz_solve (include/cavac/schwarz.hpp:54-58,
  *                         src/schwarz.cpp:111-238)
- *   cvk_assemble_cavity   build_grid + assemble (src/helmholtz.cpp:25-115),
- *                         evaluated on the device for frequency sweeps
+ *   cvk_csr_assemble_cavity  assemble (src/helmholtz.cpp:59-115) values at a
+ *                         new omega, evaluated on the device for frequency
+ *                         sweeps (driver pattern: bench_solvers,
+ *                         src/pipeline.cpp:227-293)
+ *   cvk_precond_jacobi_refresh  jacobi (src/krylov.cpp:31-55) on new values
  */
 #ifndef CAVAC_B200_H
 #define CAVAC_B200_H
@@ -128,6 +131,8 @@ int cvk_csr_upload(cvk_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz,
                    const double *values, cvk_csr **out);
 /* replace the values on the same sparsity pattern (frequency sweeps) */
 int cvk_csr_set_values(cvk_csr *A, const double *values);
+/* copy the device values back (nnz complex) */
+int cvk_csr_get_values(const cvk_csr *A, double *values);
 int cvk_csr_free(cvk_csr *A);
 int64_t cvk_csr_nrows(const cvk_csr *A);
 int64_t cvk_csr_nnz(const cvk_csr *A);
@@ -198,6 +203,20 @@ int cvk_schwarz_solve(cvk_ctx *ctx, const cvk_grid *grid, double c, int64_t n, i
                       const int64_t *col_begin, const double *s_left, const double *s_right,
                       const cvk_opts *inner, double ddm_tol, int64_t max_outer, int inner_solver,
                       double *x, cvk_ddm_report *rep);
+
+/* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */
+
+/* Overwrite A's values with the cavity operator at `omega` (assemble,
+ * helmholtz.cpp:59-115): off-diagonals -c^2/h^2, diagonal 4c^2/h^2 - omega^2
+ * minus (c^2/h^2) w per missing wall neighbour, w = 1/(1 + i omega h beta)
+ * (beta = grid admittance; w = 1 for rigid walls), bitwise the reference's
+ * values.  A must carry the cavity's 5-point pattern (as uploaded from an
+ * assemble() of the same grid); otherwise CVK_EINVAL names the first
+ * mismatching row.  The rhs does not depend on omega. */
+int cvk_csr_assemble_cavity(cvk_csr *A, const cvk_grid *grid, double omega, double c);
+/* recompute M's inverse diagonal from A's current values (jacobi,
+ * krylov.cpp:31-55; CVK_EZERODIAG names the row as the reference does) */
+int cvk_precond_jacobi_refresh(cvk_prec *M, const cvk_csr *A);
 
 /* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
  * device buffers, returns the average kernel time in seconds ---- */

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <complex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -289,6 +290,14 @@ int cvk_csr_set_values(cvk_csr* A, const double* values) {
     return CVK_OK;
 }
 
+int cvk_csr_get_values(const cvk_csr* A, double* values) {
+    if (!A || (!values && A->nnz)) return fail(CVK_EINVAL, "cvk_csr_get_values: null argument");
+    CK(cudaSetDevice(A->ctx->device));
+    CK(cudaStreamSynchronize(A->ctx->stream));
+    if (A->nnz) CK(cudaMemcpy(values, A->av, sizeof(double2) * A->nnz, cudaMemcpyDeviceToHost));
+    return CVK_OK;
+}
+
 int cvk_csr_free(cvk_csr* A) {
     if (!A) return CVK_OK;
     cudaSetDevice(A->ctx->device);
@@ -326,6 +335,48 @@ int cvk_precond_jacobi(cvk_csr* A, const double* inv_diag, cvk_prec** out) {
     }
     CK(cudaStreamSynchronize(c->stream));
     *out = M;
+    return CVK_OK;
+}
+
+int cvk_precond_jacobi_refresh(cvk_prec* M, const cvk_csr* A) {
+    if (!M || !A) return fail(CVK_EINVAL, "cvk_precond_jacobi_refresh: null argument");
+    if (!M->dinv) return fail(CVK_EINVAL, "cvk_precond_jacobi_refresh: identity preconditioner");
+    if (M->n != A->n || M->ctx != A->ctx) return fail(CVK_EINVAL, "cvk_precond_jacobi_refresh: dimension mismatch");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    const int big = INT32_MAX;
+    CK(cudaMemcpyAsync(c->bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cvk::launch_inv_diag((int)A->n, A->rp, A->ci, A->av, M->dinv, c->bad, c->stream));
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (bad != INT32_MAX) return fail(CVK_EZERODIAG, "jacobi: zero diagonal at row " + std::to_string(bad));
+    return CVK_OK;
+}
+
+int cvk_csr_assemble_cavity(cvk_csr* A, const cvk_grid* g, double omega, double c_sound) {
+    if (!A || !g) return fail(CVK_EINVAL, "cvk_csr_assemble_cavity: null argument");
+    if (g->nx < 1 || g->ny < 1 || g->nx * g->ny != A->n)
+        return fail(CVK_EINVAL, "cvk_csr_assemble_cavity: grid does not match the matrix size");
+    cvk_ctx* c = A->ctx;
+    // host scalars with std::complex, exactly as helmholtz.cpp:65-73
+    using Cx = std::complex<double>;
+    const double k2 = c_sound * c_sound / (g->h * g->h);
+    const Cx adm(g->admittance_re, g->admittance_im);
+    Cx ww(1.0);
+    if (adm != Cx(0.0)) ww = 1.0 / (Cx(1.0) + Cx(0.0, omega * g->h) * adm);
+    const Cx kw = k2 * ww;
+    CK(cudaSetDevice(c->device));
+    const int big = INT32_MAX;
+    CK(cudaMemcpyAsync(c->bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cvk::launch_cavity_values((int)g->nx, (int)g->ny, (int)g->roof_begin, (int)g->roof_end, k2, omega * omega,
+                                 kw.real(), kw.imag(), A->rp, A->ci, A->av, c->bad, c->nsm, c->stream));
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (bad != INT32_MAX)
+        return fail(CVK_EINVAL, "cvk_csr_assemble_cavity: matrix pattern is not the cavity's 5-point pattern at row " +
+                                    std::to_string(bad));
     return CVK_OK;
 }
 

@@ -31,6 +31,11 @@ cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, co
 // FAST SpMV on the TMA ring; cudaErrorInvalidConfiguration if a chunk does not fit
 cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
                                double2* y, int capk, int nsm, int optin, cudaStream_t st);
+// cavity operator values at omega on the cavity's 5-point pattern (cvk_assemble.cu);
+// *bad receives the first row whose pattern does not match (INT32_MAX if none)
+cudaError_t launch_cavity_values(int nx, int ny, int roof_begin, int roof_end, double k2, double om2,
+                                 double kw_re, double kw_im, const int* rp, const int* ci, double2* av,
+                                 int* bad, int nsm, cudaStream_t st);
 cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
                             int* bad_row, cudaStream_t st);
 // out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 1024 double2
