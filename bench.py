@@ -46,6 +46,10 @@ FREQ_HZ = 100.0
 ADMITTANCE = 0.01
 TOL = 1e-8
 MAX_ITER = 20000
+# the reference's own iteration count on this system (tools/ref_converge.py:
+# oracle/_ref, ExecMode::Parallel, run to convergence: 6952 iterations, 688 s
+# on 8 threads); the CPU baseline is its measured s/iteration x this count
+REF_ITERS = 6952
 
 
 def workload_config(n, nnz):
@@ -161,7 +165,7 @@ def cpu_reference(prob, steps, warmup, iters_full, sample_iters):
         "sample": f"{sample_iters} BiCGSTAB iterations of the same {A.nrows}-DOF system "
                   f"(reference ExecMode::Parallel, OpenMP {threads} threads; dots single-threaded by "
                   f"the reference's design), median of {max(1, steps)}, extrapolated x {iters_full} "
-                  f"iterations (the device solve's count)",
+                  f"iterations (the reference's own count on this system, tools/ref_converge.py)",
     }
 
 
@@ -182,7 +186,7 @@ def main():
         if rank != 0:
             return 0
         prob = build_system()
-        iters_full = int(os.environ.get("CVK_REF_ITERS_FULL", "5557"))
+        iters_full = int(os.environ.get("CVK_REF_ITERS_FULL", str(REF_ITERS)))
         cb = cpu_reference(prob, args.steps, args.warmup, iters_full, args.cpu_sample_iters)
         line = {
             "metric": METRIC, "value": cb["value"], "unit": "s", "n_gpus": args.gpus,
@@ -297,7 +301,7 @@ def main():
             traffic = json.load(open(tp)).get("bicgstab_iteration_dram_bytes")
         except Exception:
             traffic = None
-    cb = cpu_reference(prob, 1, 0, iters, args.cpu_sample_iters)
+    cb = cpu_reference(prob, 1, 0, REF_ITERS, args.cpu_sample_iters)
     line = {
         "metric": METRIC,
         "value": t_solve, "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -305,7 +309,7 @@ def main():
         "vs_baseline": None, "dtype": "c128 (f64 complex)",
         "data": "synthetic (reference build_grid/assemble, roof Dirichlet 1+0i)",
         "config": dict(workload_config(n, nnz), parallelism=f"replicas x{args.gpus}"),
-        "iterations": iters, "converged": bool(reps[-1].converged),
+        "iterations": iters, "reference_iterations": REF_ITERS, "converged": bool(reps[-1].converged),
         "final_relres": reps[-1].final_relres, "true_relres": reps[-1].true_relres,
         "seconds_per_iteration": t_solve / max(iters, 1),
         "spmv": {"gbs": spmv_bytes / spmv_s.value / 1e9, "seconds": spmv_s.value,
