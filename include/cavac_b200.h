@@ -204,6 +204,52 @@ int cvk_schwarz_solve(cvk_ctx *ctx, const cvk_grid *grid, double c, int64_t n, i
                       const cvk_opts *inner, double ddm_tol, int64_t max_outer, int inner_solver,
                       double *x, cvk_ddm_report *rep);
 
+/* ---- multi-GPU Schwarz: one rank's strips (schwarz.cpp:111-238 split
+ * across devices; the caller moves the interface data between ranks) ----
+ *
+ * A rank owns global strips [s_begin, s_end) of the n_sub-strip partition
+ * col_begin.  Interface slot j = 0..ns (ns = s_end - s_begin) is the cut
+ * between global strips s_begin+j-1 and s_begin+j; slot 0 / slot ns are the
+ * rank's external cuts (present iff s_begin > 0 / s_end < n_sub).  One call
+ * of cvk_ddm_rank_sweep is one outer sweep of the reference for these
+ * strips: local rhs with the current interface data, every local inner solve
+ * (one batched launch), the Robin trace update on internal cuts, and for the
+ * external cuts the local side's new data, returned for the neighbour:
+ *   g_out_left  (ny complex): the new g_l of slot 0 (left neighbour's right
+ *               edge data), computed from this rank's left edge column;
+ *   g_out_right (ny complex): the new g_r of slot ns.
+ * The data received from the neighbours is passed to the next sweep as
+ * g_in_left (new g_r of slot 0) / g_in_right (new g_l of slot ns); NULL
+ * keeps the current values (zero initially).  jump_terms receives
+ * 2*(ns+1)*ny doubles [slot][row][side]: |x_new - x_old|^2 of the cut's left
+ * column (side 0) and right column (side 1) where that column is local,
+ * 0 otherwise -- the caller sums them over all ranks in the reference's
+ * order (per cut, per row, left then right, schwarz.cpp:211-220), so the
+ * multi-rank interface norm is bitwise the single-process one. */
+typedef struct cvk_ddm_rank cvk_ddm_rank;
+typedef struct {
+    int32_t inner_breakdown;        /* any local inner solve broke down */
+    int32_t pad;
+    int64_t total_inner_iterations; /* summed over the rank's strips */
+    double device_time_s;
+    int64_t kernel_launches;
+} cvk_ddm_sweep_info;
+
+int cvk_ddm_rank_create(cvk_ctx *ctx, const cvk_grid *grid, double c, int64_t n, int64_t nnz,
+                        const uint64_t *row_offsets, const uint64_t *col_indices, const double *values,
+                        const double *b, int64_t n_sub, const int64_t *col_begin, int64_t s_begin,
+                        int64_t s_end, const double *s_left, const double *s_right, const cvk_opts *inner,
+                        int inner_solver, cvk_ddm_rank **out);
+int cvk_ddm_rank_sweep(cvk_ddm_rank *rank, const double *g_in_left, const double *g_in_right,
+                       double *g_out_left, double *g_out_right, double *jump_terms,
+                       cvk_ddm_sweep_info *info);
+/* the last sweep's per-strip inner reports (cap entries) */
+int cvk_ddm_rank_reports(const cvk_ddm_rank *rank, cvk_report *reps, int64_t cap);
+/* the rank's columns col_begin[s_begin] .. col_begin[s_end]-1 of x, row-major
+ * (ny rows x width complex) */
+int cvk_ddm_rank_solution(cvk_ddm_rank *rank, double *x_cols);
+int cvk_ddm_rank_destroy(cvk_ddm_rank *rank);
+
 /* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */
 
 /* Overwrite A's values with the cavity operator at `omega` (assemble,

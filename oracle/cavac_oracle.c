@@ -731,6 +731,29 @@ static int build_local(const orc_grid *g, const orc_csr *A, double c, int64_t c0
     return 0;
 }
 
+/* build_local exported for the multi-rank host-logic tests: the local CSR
+ * (out arrays sized >= 6 * (c1 - c0) * ny + 1), its Jacobi inverse diagonal
+ * and the rhs weights w[0] = k2/(1/h + s_right/2) (left cut), w[1] (right
+ * cut).  Returns nnz, or < 0 on error. */
+int64_t orc_local_system(const orc_grid *g, double c, int64_t n, const int64_t *rp, const int64_t *ci,
+                         const cplx *v, int64_t c0, int64_t c1, int hl, int hr, double sl_re, double sl_im,
+                         double sr_re, double sr_im, int64_t *out_rp, int64_t *out_ci, cplx *out_v,
+                         cplx *out_dinv, cplx *w) {
+    orc_csr A = {n, rp, ci, v};
+    orc_local L;
+    int e = build_local(g, &A, c, c0, c1, hl, hr, CMPLX(sl_re, sl_im), CMPLX(sr_re, sr_im), &L);
+    if (e) return e;
+    int64_t nnz = L.rp[L.n];
+    memcpy(out_rp, L.rp, (size_t)(L.n + 1) * sizeof(int64_t));
+    memcpy(out_ci, L.ci, (size_t)nnz * sizeof(int64_t));
+    memcpy(out_v, L.v, (size_t)nnz * sizeof(cplx));
+    memcpy(out_dinv, L.dinv, (size_t)L.n * sizeof(cplx));
+    w[0] = L.wl;
+    w[1] = L.wr;
+    free(L.rp); free(L.ci); free(L.v); free(L.dinv);
+    return nnz;
+}
+
 typedef struct {
     int64_t outer_iterations;
     int32_t converged;

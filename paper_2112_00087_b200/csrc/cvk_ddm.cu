@@ -17,6 +17,7 @@
 #include <chrono>
 #include <complex>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -94,70 +95,90 @@ int build_strip(int64_t nx, int64_t ny, double h, double c, const uint64_t* rp, 
     return CVK_OK;
 }
 
+// A rank's strips: global strips s0 .. s0+ns-1, local index j.  Interface
+// "slots" j = 0..ns: slot j is the cut between global strips s0+j-1 and
+// s0+j (it exists iff 0 < s0+j < n_sub); slots 1..ns-1 are internal to the
+// rank, slot 0 / slot ns are the rank's external left / right cuts whose
+// other side lives on a neighbouring rank.
 struct DdmGeom {
-    int n_sub, ny, nx;
-    const int* c0;       // [n_sub]
-    const int* width;    // [n_sub]
-    const int* loff;     // [n_sub] offset of strip s in the concatenated local vectors
+    int ns, ny, nx;
+    int has_left, has_right;  // external cuts present (s0 > 0, s0 + ns < n_sub)
+    const int* c0;            // [ns] first global column of local strip j
+    const int* width;         // [ns]
+    const int* loff;          // [ns + 1] offset of strip j in the concatenated local vectors
 };
 
-// local rhs (schwarz.cpp:160-175)
+__device__ __forceinline__ bool slot_exists(const DdmGeom& g, int j) {
+    return (j > 0 && j < g.ns) || (j == 0 && g.has_left) || (j == g.ns && g.has_right);
+}
+
+// local rhs (schwarz.cpp:160-175): b on the strip, + w_L g_r at the left
+// edge (slot j), + w_R g_l at the right edge (slot j + 1)
 __global__ void k_ddm_rhs(DdmGeom g, const double2* __restrict__ b, const double2* __restrict__ gl,
                           const double2* __restrict__ gr, const double2* __restrict__ wlr,
                           double2* __restrict__ rhs, int ntot) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ntot) return;
     int s = 0;
-    while (s + 1 < g.n_sub && i >= g.loff[s + 1]) ++s;
+    while (s + 1 < g.ns && i >= g.loff[s + 1]) ++s;
     const int li = i - g.loff[s], w = g.width[s];
     const int iy = li / w, lx = li - iy * w;
     double2 r = b[(size_t)iy * g.nx + g.c0[s] + lx];
-    if (s > 0 && lx == 0) r = cvk_add(r, cvk_mul(wlr[2 * s], gr[(size_t)(s - 1) * g.ny + iy]));
-    if (s + 1 < g.n_sub && lx == w - 1) r = cvk_add(r, cvk_mul(wlr[2 * s + 1], gl[(size_t)s * g.ny + iy]));
+    if (lx == 0 && slot_exists(g, s)) r = cvk_add(r, cvk_mul(wlr[2 * s], gr[(size_t)s * g.ny + iy]));
+    if (lx == w - 1 && slot_exists(g, s + 1)) r = cvk_add(r, cvk_mul(wlr[2 * s + 1], gl[(size_t)(s + 1) * g.ny + iy]));
     rhs[i] = r;
 }
 
-// trace exchange (schwarz.cpp:187-208) on every (cut, row); then the jump
-// (schwarz.cpp:211-220) summed by one thread in the reference's order.
+// trace exchange (schwarz.cpp:187-208) on every (slot, row) with the old
+// g's, and the interface-jump terms |x_new - x_old|^2 of the edge columns
+// (schwarz.cpp:211-220; summed on the host in the reference's order).  For
+// an external slot only the local side is updated: its new g is written to
+// out_left (slot 0: the left neighbour's g_l) / out_right (slot ns: the right
+// neighbour's g_r) for the caller to send.
 __global__ void k_ddm_exchange(DdmGeom g, const double2* __restrict__ u, double2* gl, double2* gr,
                                double2* prev, double2 a_l, double2 b_l, double2 a_r, double2 b_r,
-                               double2 s_sum, double* jump2_out) {
-    const int ncut = g.n_sub - 1;
-    const int tot = ncut * g.ny;
-    extern __shared__ double2 dj[];  // per (cut,row): d_left, d_right
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int q = e / g.ny, iy = e - q * g.ny;
-        const int wl = g.width[q], wr = g.width[q + 1];
-        const double2 el = u[g.loff[q] + (size_t)iy * wl + (wl - 1)];
-        const double2 er = u[g.loff[q + 1] + (size_t)iy * wr];
+                               double2 s_sum, double* terms, double2* out_left, double2* out_right) {
+    const int tot = (g.ns + 1) * g.ny;
+    const double2 half = cvk_scale(0.5, s_sum);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+        const int j = e / g.ny, iy = e - j * g.ny;
+        terms[2 * e] = 0.0;
+        terms[2 * e + 1] = 0.0;
+        if (!slot_exists(g, j)) continue;
         const double2 glv = gl[e], grv = gr[e];
-        const double2 gho_l = cvk_cdiv(cvk_sub(glv, cvk_mul(b_l, el)), a_l);
-        const double2 gho_r = cvk_cdiv(cvk_sub(grv, cvk_mul(b_r, er)), a_r);
-        const double2 half = cvk_scale(0.5, s_sum);
-        gr[e] = cvk_add(cvk_neg(glv), cvk_mul(half, cvk_add(gho_l, el)));
-        gl[e] = cvk_add(cvk_neg(grv), cvk_mul(half, cvk_add(gho_r, er)));
-        dj[2 * e] = cvk_sub(el, prev[2 * e]);
-        dj[2 * e + 1] = cvk_sub(er, prev[2 * e + 1]);
-        prev[2 * e] = el;
-        prev[2 * e + 1] = er;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double j2 = 0.0;
-        for (int e = 0; e < 2 * tot; ++e) j2 += cvk_norm(dj[e]);
-        *jump2_out = j2;
+        if (j >= 1) {  // left side local: strip j-1, its last column (cut - 1)
+            const int wl = g.width[j - 1];
+            const double2 el = u[g.loff[j - 1] + (size_t)iy * wl + (wl - 1)];
+            const double2 gho_l = cvk_cdiv(cvk_sub(glv, cvk_mul(b_l, el)), a_l);
+            const double2 grn = cvk_add(cvk_neg(glv), cvk_mul(half, cvk_add(gho_l, el)));
+            if (j == g.ns) out_right[iy] = grn;
+            else gr[e] = grn;
+            terms[2 * e] = cvk_norm(cvk_sub(el, prev[2 * e]));
+            prev[2 * e] = el;
+        }
+        if (j < g.ns) {  // right side local: strip j, its first column (cut)
+            const int wr = g.width[j];
+            const double2 er = u[g.loff[j] + (size_t)iy * wr];
+            const double2 gho_r = cvk_cdiv(cvk_sub(grv, cvk_mul(b_r, er)), a_r);
+            const double2 gln = cvk_add(cvk_neg(grv), cvk_mul(half, cvk_add(gho_r, er)));
+            if (j == 0) out_left[iy] = gln;
+            else gl[e] = gln;
+            terms[2 * e + 1] = cvk_norm(cvk_sub(er, prev[2 * e + 1]));
+            prev[2 * e + 1] = er;
+        }
     }
 }
 
-// x[global] = u_loc (schwarz.cpp:180-183, last sweep)
-__global__ void k_ddm_scatter(DdmGeom g, const double2* __restrict__ u, double2* __restrict__ x, int ntot) {
+// the rank's columns, row-major over (iy, column) (schwarz.cpp:180-183)
+__global__ void k_ddm_scatter(DdmGeom g, const double2* __restrict__ u, double2* __restrict__ x, int col0,
+                              int ncols, int ntot) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ntot) return;
     int s = 0;
-    while (s + 1 < g.n_sub && i >= g.loff[s + 1]) ++s;
+    while (s + 1 < g.ns && i >= g.loff[s + 1]) ++s;
     const int li = i - g.loff[s], w = g.width[s];
     const int iy = li / w, lx = li - iy * w;
-    x[(size_t)iy * g.nx + g.c0[s] + lx] = u[i];
+    x[(size_t)iy * ncols + (g.c0[s] - col0) + lx] = u[i];
 }
 
 }  // namespace
@@ -212,13 +233,285 @@ extern "C" int cvk_ddm_launch_batched(cvk_ctx* ctx, int solver, int mode, const 
 extern "C" int cvk_ddm_ctas(cvk_ctx* ctx, int solver, int mode, size_t smem, int* total);
 extern "C" void* cvk_ddm_stream(cvk_ctx* ctx);
 
+// ---------------------------------------------------------------- rank plan
+// The strips [s0, s1) of an n_sub-strip partition on one device: local
+// systems + Jacobi built once, then one call per outer sweep.  A single rank
+// owning every strip is the single-device schwarz_solve; one rank per GPU
+// (strips split across ranks, external slots exchanged by the caller) is the
+// multi-GPU DDM (paper_2112_00087_b200/ddm_dist.py).
+struct cvk_ddm_rank {
+    cvk_ctx* ctx = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf mem;
+    int64_t n_sub = 0, s0 = 0, s1 = 0, ns = 0, nx = 0, ny = 0, col0 = 0, col1 = 0, ntot = 0;
+    int solver = 0, mode = 0, total_ctas = 0;
+    size_t smem = 0;
+    cvk::DdmGeom geo{};
+    double2 *d_b = nullptr, *d_rhs = nullptr, *d_u = nullptr, *d_gl = nullptr, *d_gr = nullptr,
+            *d_prev = nullptr, *d_wlr = nullptr, *d_out = nullptr, *d_x = nullptr;
+    double* d_terms = nullptr;
+    unsigned long long* d_bars = nullptr;
+    cvk::DevReport* d_reps = nullptr;
+    cvk::KArgs* d_segs = nullptr;
+    double2 a_l{}, b_l{}, a_r{}, b_r{}, s_sum{};
+    std::vector<cvk::DevReport> hr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~cvk_ddm_rank() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c, int64_t n, int64_t nnz,
+                                   const uint64_t* row_offsets, const uint64_t* col_indices,
+                                   const double* values, const double* b, int64_t n_sub,
+                                   const int64_t* col_begin, int64_t s_begin, int64_t s_end,
+                                   const double* s_left, const double* s_right, const cvk_opts* inner,
+                                   int inner_solver, cvk_ddm_rank** out) {
+    using namespace cvk;
+    if (!ctx || !grid || !row_offsets || !b || !col_begin || !s_left || !s_right || !inner || !out)
+        return dfail(CVK_EINVAL, "schwarz_solve: null argument");
+    if (grid->nx * grid->ny != n) return dfail(CVK_EINVAL, "schwarz_solve: grid does not match the system");
+    if (inner_solver < 0 || inner_solver > 3) return dfail(CVK_ESOLVER, "schwarz_solve: unknown inner solver");
+    if (n_sub < 2 || n_sub > 4096) return dfail(CVK_EINVAL, "schwarz_solve: n_sub out of range");
+    if (s_begin < 0 || s_end > n_sub || s_begin >= s_end) return dfail(CVK_EINVAL, "ddm rank: bad strip range");
+    (void)nnz;
+    auto R = std::make_unique<cvk_ddm_rank>();
+    R->ctx = ctx;
+    R->n_sub = n_sub;
+    R->s0 = s_begin;
+    R->s1 = s_end;
+    R->ns = s_end - s_begin;
+    R->nx = grid->nx;
+    R->ny = grid->ny;
+    R->col0 = col_begin[s_begin];
+    R->col1 = col_begin[s_end];
+    R->solver = inner_solver;
+    const int64_t ns = R->ns, ny = R->ny, nx = R->nx;
+    const double h = grid->h;
+    const Cx sl(s_left[0], s_left[1]), sr(s_right[0], s_right[1]);
+    std::vector<Strip> strips((size_t)ns);
+    const Cx* vals = reinterpret_cast<const Cx*>(values);
+    for (int64_t j = 0; j < ns; ++j) {
+        const int64_t s = s_begin + j;
+        const int e = build_strip(nx, ny, h, c, row_offsets, col_indices, vals, col_begin[s], col_begin[s + 1],
+                                  s > 0, s + 1 < n_sub, sl, sr, strips[(size_t)j]);
+        if (e != CVK_OK) return dfail(e, "build_local: unexpected cross coupling");
+    }
+    cudaStream_t st = (cudaStream_t)cvk_ddm_stream(ctx);
+    R->st = st;
+    DevBuf& mem = R->mem;
+    std::vector<int> h_c0(ns), h_w(ns), h_off(ns + 1);
+    int64_t ntot = 0;
+    for (int64_t j = 0; j < ns; ++j) {
+        h_c0[j] = (int)strips[j].c0;
+        h_w[j] = (int)(strips[j].c1 - strips[j].c0);
+        h_off[j] = (int)ntot;
+        ntot += strips[j].n;
+    }
+    h_off[ns] = (int)ntot;
+    R->ntot = ntot;
+    int *d_c0, *d_w, *d_off;
+    DK(mem.alloc(&d_c0, ns));
+    DK(mem.alloc(&d_w, ns));
+    DK(mem.alloc(&d_off, ns + 1));
+    DK(cudaMemcpyAsync(d_c0, h_c0.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, st));
+    DK(cudaMemcpyAsync(d_w, h_w.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, st));
+    DK(cudaMemcpyAsync(d_off, h_off.data(), sizeof(int) * (ns + 1), cudaMemcpyHostToDevice, st));
+    R->geo = DdmGeom{(int)ns, (int)ny, (int)nx, s_begin > 0 ? 1 : 0, s_end < n_sub ? 1 : 0, d_c0, d_w, d_off};
+    const int64_t nslot = (ns + 1) * ny;
+    DK(mem.alloc(&R->d_b, n));
+    DK(mem.alloc(&R->d_rhs, ntot));
+    DK(mem.alloc(&R->d_u, ntot));
+    DK(mem.alloc(&R->d_gl, nslot));
+    DK(mem.alloc(&R->d_gr, nslot));
+    DK(mem.alloc(&R->d_prev, 2 * nslot));
+    DK(mem.alloc(&R->d_terms, 2 * nslot));
+    DK(mem.alloc(&R->d_out, 2 * ny));
+    DK(mem.alloc(&R->d_wlr, 2 * ns));
+    DK(mem.alloc(&R->d_x, ntot));
+    DK(cudaMemcpyAsync(R->d_b, b, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    DK(cudaMemsetAsync(R->d_gl, 0, sizeof(double2) * nslot, st));
+    DK(cudaMemsetAsync(R->d_gr, 0, sizeof(double2) * nslot, st));
+    DK(cudaMemsetAsync(R->d_prev, 0, sizeof(double2) * 2 * nslot, st));
+    DK(cudaMemsetAsync(R->d_out, 0, sizeof(double2) * 2 * ny, st));
+    std::vector<double2> h_wlr(2 * ns);
+    for (int64_t j = 0; j < ns; ++j) {
+        h_wlr[2 * j] = make_double2(strips[j].wl.real(), strips[j].wl.imag());
+        h_wlr[2 * j + 1] = make_double2(strips[j].wr.real(), strips[j].wr.imag());
+    }
+    DK(cudaMemcpyAsync(R->d_wlr, h_wlr.data(), sizeof(double2) * 2 * ns, cudaMemcpyHostToDevice, st));
+
+    // local CSRs + Jacobi, one batched-solve segment per strip
+    R->mode = inner->mode == CVK_MODE_REF ? CVK_MODE_REF : CVK_MODE_FAST;
+    R->smem = solver_smem(inner_solver, (int)inner->m);
+    int e = cvk_ddm_ctas(ctx, inner_solver, R->mode, R->smem, &R->total_ctas);
+    if (e != CVK_OK) return e;
+    const int nwork = solver_nwork(inner_solver, (int)inner->l, (int)inner->m);
+    std::vector<KArgs> segs((size_t)ns);
+    int* d_bad;
+    DK(mem.alloc(&d_bad, 1));
+    std::vector<int> gs(ns, 1);
+    {
+        int64_t chunks_tot = 0;
+        std::vector<int64_t> ch(ns);
+        for (int64_t j = 0; j < ns; ++j) {
+            ch[j] = std::max<int64_t>(1, (strips[j].n + kThreads - 1) / kThreads);
+            chunks_tot += ch[j];
+        }
+        const int budget = std::max<int>(R->total_ctas, (int)ns);
+        for (int64_t j = 0; j < ns; ++j)
+            gs[j] = (int)std::max<int64_t>(1, std::min<int64_t>(ch[j], (int64_t)budget * ch[j] / chunks_tot));
+    }
+    int cta_base = 0;
+    DK(mem.alloc(&R->d_bars, 2 * ns));
+    DK(mem.alloc(&R->d_reps, ns));
+    for (int64_t j = 0; j < ns; ++j) {
+        const Strip& S = strips[j];
+        int *rp, *ci;
+        double2 *av, *dinv, *work, *part;
+        DK(mem.alloc(&rp, S.rp.size()));
+        DK(mem.alloc(&ci, S.ci.size()));
+        DK(mem.alloc(&av, S.v.size()));
+        DK(mem.alloc(&dinv, S.n));
+        DK(mem.alloc(&work, (size_t)nwork * S.n));
+        DK(mem.alloc(&part, (size_t)kRegions * kMaxSlots * gs[j]));
+        DK(cudaMemcpyAsync(rp, S.rp.data(), sizeof(int) * S.rp.size(), cudaMemcpyHostToDevice, st));
+        DK(cudaMemcpyAsync(ci, S.ci.data(), sizeof(int) * S.ci.size(), cudaMemcpyHostToDevice, st));
+        DK(cudaMemcpyAsync(av, S.v.data(), sizeof(double2) * S.v.size(), cudaMemcpyHostToDevice, st));
+        const int big = 0x7fffffff;
+        DK(cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+        DK(launch_inv_diag((int)S.n, rp, ci, av, dinv, d_bad, st));
+        int bad = 0;
+        DK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        DK(cudaStreamSynchronize(st));
+        if (bad != big) return dfail(CVK_EZERODIAG, "jacobi: zero diagonal at row " + std::to_string(bad));
+        KArgs& a = segs[j];
+        std::memset(&a, 0, sizeof(a));
+        a.A = Csr{(int)S.n, rp, ci, av};
+        a.dinv = dinv;
+        a.b = R->d_rhs + h_off[j];
+        a.x = R->d_u + h_off[j];
+        a.work = work;
+        a.part = part;
+        a.bar = R->d_bars + 2 * j;
+        a.rep = R->d_reps + j;
+        a.hist = nullptr;
+        a.hist_cap = 0;
+        a.tol = inner->tol;
+        a.max_iter = inner->max_iter;
+        a.l = (int)inner->l;
+        a.m = (int)inner->m;
+        a.record = 0;
+        a.G = gs[j];
+        a.cta_base = cta_base;
+        cta_base += gs[j];
+    }
+    R->total_ctas = cta_base;
+    DK(mem.alloc(&R->d_segs, ns));
+    DK(cudaMemcpyAsync(R->d_segs, segs.data(), sizeof(KArgs) * ns, cudaMemcpyHostToDevice, st));
+    auto d2 = [](Cx z) { return make_double2(z.real(), z.imag()); };
+    R->a_l = d2(Cx(1.0 / h) + 0.5 * sl);
+    R->b_l = d2(Cx(-1.0 / h) + 0.5 * sl);
+    R->a_r = d2(Cx(1.0 / h) + 0.5 * sr);
+    R->b_r = d2(Cx(-1.0 / h) + 0.5 * sr);
+    R->s_sum = d2(sl + sr);
+    R->hr.resize((size_t)ns);
+    DK(cudaEventCreate(&R->e0));
+    DK(cudaEventCreate(&R->e1));
+    DK(cudaStreamSynchronize(st));
+    *out = R.release();
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_sweep(cvk_ddm_rank* R, const double* g_in_left, const double* g_in_right,
+                                  double* g_out_left, double* g_out_right, double* jump_terms,
+                                  cvk_ddm_sweep_info* info) {
+    using namespace cvk;
+    if (!R || !jump_terms || !info) return dfail(CVK_EINVAL, "ddm rank sweep: null argument");
+    cudaStream_t st = R->st;
+    const int64_t ny = R->ny, ns = R->ns;
+    // incoming external data (the neighbours' previous-sweep updates)
+    if (R->geo.has_left && g_in_left)
+        DK(cudaMemcpyAsync(R->d_gr, g_in_left, sizeof(double2) * ny, cudaMemcpyHostToDevice, st));
+    if (R->geo.has_right && g_in_right)
+        DK(cudaMemcpyAsync(R->d_gl + ns * ny, g_in_right, sizeof(double2) * ny, cudaMemcpyHostToDevice, st));
+    const int threads = 256;
+    DK(cudaEventRecord(R->e0, st));
+    k_ddm_rhs<<<(unsigned)((R->ntot + threads - 1) / threads), threads, 0, st>>>(R->geo, R->d_b, R->d_gl, R->d_gr,
+                                                                                R->d_wlr, R->d_rhs, (int)R->ntot);
+    DK(cudaGetLastError());
+    DK(cudaMemsetAsync(R->d_bars, 0, sizeof(unsigned long long) * 2 * ns, st));
+    float ms = 0.f;
+    const int e = cvk_ddm_launch_batched(R->ctx, R->solver, R->mode, R->d_segs, (int)ns, R->total_ctas, R->smem, &ms);
+    if (e != CVK_OK) return e;
+    const int64_t nslot = (ns + 1) * ny;
+    const unsigned xb = (unsigned)std::min<int64_t>(64, (nslot + threads - 1) / threads);
+    k_ddm_exchange<<<std::max(1u, xb), threads, 0, st>>>(R->geo, R->d_u, R->d_gl, R->d_gr, R->d_prev, R->a_l, R->b_l,
+                                                         R->a_r, R->b_r, R->s_sum, R->d_terms, R->d_out,
+                                                         R->d_out + ny);
+    DK(cudaGetLastError());
+    DK(cudaEventRecord(R->e1, st));
+    DK(cudaMemcpyAsync(jump_terms, R->d_terms, sizeof(double) * 2 * nslot, cudaMemcpyDeviceToHost, st));
+    if (g_out_left) DK(cudaMemcpyAsync(g_out_left, R->d_out, sizeof(double2) * ny, cudaMemcpyDeviceToHost, st));
+    if (g_out_right) DK(cudaMemcpyAsync(g_out_right, R->d_out + ny, sizeof(double2) * ny, cudaMemcpyDeviceToHost, st));
+    DK(cudaMemcpyAsync(R->hr.data(), R->d_reps, sizeof(DevReport) * ns, cudaMemcpyDeviceToHost, st));
+    DK(cudaStreamSynchronize(st));
+    float sweep_ms = 0.f;
+    cudaEventElapsedTime(&sweep_ms, R->e0, R->e1);
+    info->inner_breakdown = 0;
+    info->total_inner_iterations = 0;
+    for (int64_t j = 0; j < ns; ++j) {
+        if (R->hr[j].error) return dfail(CVK_ETIMEOUT, "schwarz_solve: inner solve grid barrier aborted");
+        if (R->hr[j].breakdown) info->inner_breakdown = 1;
+        info->total_inner_iterations += R->hr[j].iterations;
+    }
+    info->device_time_s = sweep_ms * 1e-3;
+    info->kernel_launches = 3;
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_reports(const cvk_ddm_rank* R, cvk_report* reps, int64_t cap) {
+    if (!R || (!reps && cap > 0)) return dfail(CVK_EINVAL, "ddm rank reports: null argument");
+    for (int64_t j = 0; j < R->ns && j < cap; ++j) {
+        cvk_report& r = reps[j];
+        r.converged = R->hr[j].converged;
+        r.breakdown = R->hr[j].breakdown;
+        r.iterations = R->hr[j].iterations;
+        r.final_relres = R->hr[j].final_relres;
+        r.true_relres = R->hr[j].true_relres;
+        r.history_len = 0;
+    }
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_solution(cvk_ddm_rank* R, double* x_cols) {
+    using namespace cvk;
+    if (!R || !x_cols) return dfail(CVK_EINVAL, "ddm rank solution: null argument");
+    const int threads = 256;
+    k_ddm_scatter<<<(unsigned)((R->ntot + threads - 1) / threads), threads, 0, R->st>>>(
+        R->geo, R->d_u, R->d_x, (int)R->col0, (int)(R->col1 - R->col0), (int)R->ntot);
+    DK(cudaGetLastError());
+    DK(cudaMemcpyAsync(x_cols, R->d_x, sizeof(double2) * R->ntot, cudaMemcpyDeviceToHost, R->st));
+    DK(cudaStreamSynchronize(R->st));
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_destroy(cvk_ddm_rank* R) {
+    if (R) {
+        cudaStreamSynchronize(R->st);
+        delete R;
+    }
+    return CVK_OK;
+}
+
+// schwarz_solve (schwarz.cpp:111-238) on one device = one rank owning every strip
 extern "C" int cvk_schwarz_solve(cvk_ctx* ctx, const cvk_grid* grid, double c, int64_t n, int64_t nnz,
                                  const uint64_t* row_offsets, const uint64_t* col_indices,
                                  const double* values, const double* b, int64_t n_sub,
                                  const int64_t* col_begin, const double* s_left, const double* s_right,
                                  const cvk_opts* inner, double ddm_tol, int64_t max_outer,
                                  int inner_solver, double* x, cvk_ddm_report* rep) {
-    using namespace cvk;
     const double t_wall0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
     if (!ctx || !grid || !row_offsets || !b || !col_begin || !s_left || !s_right || !inner || !x || !rep)
         return dfail(CVK_EINVAL, "schwarz_solve: null argument");
@@ -245,180 +538,36 @@ extern "C" int cvk_schwarz_solve(cvk_ctx* ctx, const cvk_grid* grid, double c, i
         return CVK_OK;
     }
     if (n_sub < 1 || n_sub > 256) return dfail(CVK_EINVAL, "schwarz_solve: n_sub out of range");
-    const int64_t nx = grid->nx, ny = grid->ny;
-    const double h = grid->h;
-    const Cx sl(s_left[0], s_left[1]), sr(s_right[0], s_right[1]);
-    std::vector<Strip> strips((size_t)n_sub);
-    const Cx* vals = reinterpret_cast<const Cx*>(values);
-    for (int64_t s = 0; s < n_sub; ++s) {
-        const int e = build_strip(nx, ny, h, c, row_offsets, col_indices, vals, col_begin[s], col_begin[s + 1],
-                                  s > 0, s + 1 < n_sub, sl, sr, strips[(size_t)s]);
-        if (e != CVK_OK) return dfail(e, "build_local: unexpected cross coupling");
-    }
-    // ---------------- device state
-    cudaStream_t st = (cudaStream_t)cvk_ddm_stream(ctx);
-    DevBuf mem;
-    std::vector<int> h_c0(n_sub), h_w(n_sub), h_off(n_sub + 1);
-    int64_t ntot = 0;
-    for (int64_t s = 0; s < n_sub; ++s) {
-        h_c0[s] = (int)strips[s].c0;
-        h_w[s] = (int)(strips[s].c1 - strips[s].c0);
-        h_off[s] = (int)ntot;
-        ntot += strips[s].n;
-    }
-    h_off[n_sub] = (int)ntot;
-    int *d_c0, *d_w, *d_off;
-    DK(mem.alloc(&d_c0, n_sub));
-    DK(mem.alloc(&d_w, n_sub));
-    DK(mem.alloc(&d_off, n_sub + 1));
-    DK(cudaMemcpyAsync(d_c0, h_c0.data(), sizeof(int) * n_sub, cudaMemcpyHostToDevice, st));
-    DK(cudaMemcpyAsync(d_w, h_w.data(), sizeof(int) * n_sub, cudaMemcpyHostToDevice, st));
-    DK(cudaMemcpyAsync(d_off, h_off.data(), sizeof(int) * (n_sub + 1), cudaMemcpyHostToDevice, st));
-    DdmGeom geo{(int)n_sub, (int)ny, (int)nx, d_c0, d_w, d_off};
-    double2 *d_b, *d_rhs, *d_u, *d_gl, *d_gr, *d_prev, *d_wlr, *d_x;
-    double* d_jump;
-    DK(mem.alloc(&d_b, n));
-    DK(mem.alloc(&d_rhs, ntot));
-    DK(mem.alloc(&d_u, ntot));
-    DK(mem.alloc(&d_gl, (n_sub - 1) * ny));
-    DK(mem.alloc(&d_gr, (n_sub - 1) * ny));
-    DK(mem.alloc(&d_prev, 2 * (n_sub - 1) * ny));
-    DK(mem.alloc(&d_wlr, 2 * n_sub));
-    DK(mem.alloc(&d_x, n));
-    DK(mem.alloc(&d_jump, 1));
-    DK(cudaMemcpyAsync(d_b, b, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
-    DK(cudaMemsetAsync(d_gl, 0, sizeof(double2) * (n_sub - 1) * ny, st));
-    DK(cudaMemsetAsync(d_gr, 0, sizeof(double2) * (n_sub - 1) * ny, st));
-    DK(cudaMemsetAsync(d_prev, 0, sizeof(double2) * 2 * (n_sub - 1) * ny, st));
-    std::vector<double2> h_wlr(2 * n_sub);
-    for (int64_t s = 0; s < n_sub; ++s) {
-        h_wlr[2 * s] = make_double2(strips[s].wl.real(), strips[s].wl.imag());
-        h_wlr[2 * s + 1] = make_double2(strips[s].wr.real(), strips[s].wr.imag());
-    }
-    DK(cudaMemcpyAsync(d_wlr, h_wlr.data(), sizeof(double2) * 2 * n_sub, cudaMemcpyHostToDevice, st));
-
-    // local CSRs + Jacobi
-    const int mode = inner->mode == CVK_MODE_REF ? CVK_MODE_REF : CVK_MODE_FAST;
-    const size_t smem = solver_smem(inner_solver, (int)inner->m);
-    int total_ctas = 0;
-    int e = cvk_ddm_ctas(ctx, inner_solver, mode, smem, &total_ctas);
+    cvk_ddm_rank* R = nullptr;
+    int e = cvk_ddm_rank_create(ctx, grid, c, n, nnz, row_offsets, col_indices, values, b, n_sub, col_begin, 0, n_sub,
+                                s_left, s_right, inner, inner_solver, &R);
     if (e != CVK_OK) return e;
-    const int nwork = solver_nwork(inner_solver, (int)inner->l, (int)inner->m);
-    std::vector<KArgs> segs((size_t)n_sub);
-    int* d_bad;
-    DK(mem.alloc(&d_bad, 1));
-    // CTAs per strip proportional to its chunks, at least 1
-    std::vector<int> gs(n_sub, 1);
-    {
-        int64_t chunks_tot = 0;
-        std::vector<int64_t> ch(n_sub);
-        for (int64_t s = 0; s < n_sub; ++s) {
-            ch[s] = std::max<int64_t>(1, (strips[s].n + kThreads - 1) / kThreads);
-            chunks_tot += ch[s];
-        }
-        int budget = std::max<int>(total_ctas, (int)n_sub);
-        for (int64_t s = 0; s < n_sub; ++s)
-            gs[s] = (int)std::max<int64_t>(1, std::min<int64_t>(ch[s], (int64_t)budget * ch[s] / chunks_tot));
-    }
-    int cta_base = 0;
-    unsigned long long* d_bars;
-    DevReport* d_reps;
-    DK(mem.alloc(&d_bars, 2 * n_sub));
-    DK(mem.alloc(&d_reps, n_sub));
-    for (int64_t s = 0; s < n_sub; ++s) {
-        const Strip& S = strips[s];
-        int *rp, *ci;
-        double2 *av, *dinv, *work, *part;
-        DK(mem.alloc(&rp, S.rp.size()));
-        DK(mem.alloc(&ci, S.ci.size()));
-        DK(mem.alloc(&av, S.v.size()));
-        DK(mem.alloc(&dinv, S.n));
-        DK(mem.alloc(&work, (size_t)nwork * S.n));
-        DK(mem.alloc(&part, (size_t)kRegions * kMaxSlots * gs[s]));
-        DK(cudaMemcpyAsync(rp, S.rp.data(), sizeof(int) * S.rp.size(), cudaMemcpyHostToDevice, st));
-        DK(cudaMemcpyAsync(ci, S.ci.data(), sizeof(int) * S.ci.size(), cudaMemcpyHostToDevice, st));
-        DK(cudaMemcpyAsync(av, S.v.data(), sizeof(double2) * S.v.size(), cudaMemcpyHostToDevice, st));
-        const int big = 0x7fffffff;
-        DK(cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-        DK(launch_inv_diag((int)S.n, rp, ci, av, dinv, d_bad, st));
-        int bad = 0;
-        DK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-        DK(cudaStreamSynchronize(st));
-        if (bad != big) return dfail(CVK_EZERODIAG, "jacobi: zero diagonal at row " + std::to_string(bad));
-        KArgs& a = segs[s];
-        std::memset(&a, 0, sizeof(a));
-        a.A = Csr{(int)S.n, rp, ci, av};
-        a.dinv = dinv;
-        a.b = d_rhs + h_off[s];
-        a.x = d_u + h_off[s];
-        a.work = work;
-        a.part = part;
-        a.bar = d_bars + 2 * s;
-        a.rep = d_reps + s;
-        a.hist = nullptr;
-        a.hist_cap = 0;
-        a.tol = inner->tol;
-        a.max_iter = inner->max_iter;
-        a.l = (int)inner->l;
-        a.m = (int)inner->m;
-        a.record = 0;
-        a.G = gs[s];
-        a.cta_base = cta_base;
-        cta_base += gs[s];
-    }
-    KArgs* d_segs;
-    DK(mem.alloc(&d_segs, n_sub));
-    DK(cudaMemcpyAsync(d_segs, segs.data(), sizeof(KArgs) * n_sub, cudaMemcpyHostToDevice, st));
-
-    const Cx a_l = Cx(1.0 / h) + 0.5 * sl, b_l = Cx(-1.0 / h) + 0.5 * sl;
-    const Cx a_r = Cx(1.0 / h) + 0.5 * sr, b_r = Cx(-1.0 / h) + 0.5 * sr;
-    const Cx s_sum = sl + sr;
-    auto d2 = [](Cx z) { return make_double2(z.real(), z.imag()); };
-    const int ncut = (int)n_sub - 1;
-    const int threads = 256;
-    const size_t xsmem = sizeof(double2) * 2 * (size_t)ncut * ny;
-    if (xsmem > 200 * 1024) return dfail(CVK_EINVAL, "schwarz_solve: interface too large for the exchange kernel");
-    if (xsmem > 48 * 1024) DK(cudaFuncSetAttribute(k_ddm_exchange, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
-    double res0 = -1.0;
-    float dev_ms = 0.f;
+    std::unique_ptr<cvk_ddm_rank, int (*)(cvk_ddm_rank*)> guard(R, cvk_ddm_rank_destroy);
+    const int64_t ny = grid->ny, ncut = n_sub - 1;
+    std::vector<double> terms((size_t)(2 * (n_sub + 1) * ny));
+    double res0 = -1.0, dev_s = 0.0;
     int64_t launches = 0;
-    std::vector<DevReport> hr((size_t)n_sub);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
     for (int64_t outer = 1; outer <= max_outer; ++outer) {
-        DK(cudaEventRecord(e0, st));
-        k_ddm_rhs<<<(unsigned)((ntot + threads - 1) / threads), threads, 0, st>>>(geo, d_b, d_gl, d_gr, d_wlr, d_rhs, (int)ntot);
-        DK(cudaGetLastError());
-        DK(cudaMemsetAsync(d_bars, 0, sizeof(unsigned long long) * 2 * n_sub, st));
-        float ms = 0.f;
-        e = cvk_ddm_launch_batched(ctx, inner_solver, mode, d_segs, (int)n_sub, cta_base, smem, &ms);
+        cvk_ddm_sweep_info info;
+        std::memset(&info, 0, sizeof info);
+        e = cvk_ddm_rank_sweep(R, nullptr, nullptr, nullptr, nullptr, terms.data(), &info);
         if (e != CVK_OK) return e;
-        k_ddm_exchange<<<1, 256, xsmem, st>>>(geo, d_u, d_gl, d_gr, d_prev, d2(a_l), d2(b_l), d2(a_r), d2(b_r),
-                                              d2(s_sum), d_jump);
-        DK(cudaGetLastError());
-        DK(cudaEventRecord(e1, st));
-        launches += 3;
+        dev_s += info.device_time_s;
+        launches += info.kernel_launches;
+        // jump^2 in the reference's order: per cut, per row, left column then right
         double jump2 = 0.0;
-        DK(cudaMemcpyAsync(&jump2, d_jump, sizeof(double), cudaMemcpyDeviceToHost, st));
-        DK(cudaMemcpyAsync(hr.data(), d_reps, sizeof(DevReport) * n_sub, cudaMemcpyDeviceToHost, st));
-        DK(cudaStreamSynchronize(st));
-        float sweep_ms = 0.f;
-        cudaEventElapsedTime(&sweep_ms, e0, e1);
-        dev_ms += sweep_ms;
-        bool inner_ok = true;
-        int64_t inner_total = 0;
-        for (int64_t s = 0; s < n_sub; ++s) {
-            if (hr[s].error) return dfail(CVK_ETIMEOUT, "schwarz_solve: inner solve grid barrier aborted");
-            if (hr[s].breakdown) inner_ok = false;
-            inner_total += hr[s].iterations;
-        }
+        for (int64_t q = 0; q < ncut; ++q)
+            for (int64_t iy = 0; iy < ny; ++iy) {
+                const size_t e2 = (size_t)(2 * ((q + 1) * ny + iy));
+                jump2 += terms[e2];
+                jump2 += terms[e2 + 1];
+            }
         const double jump = std::sqrt(jump2);
         if (rep->jump_history && rep->jump_len < rep->jump_cap) rep->jump_history[rep->jump_len] = jump;
         rep->jump_len++;
         rep->outer_iterations = outer;
-        rep->total_inner_iterations = inner_total;
-        if (!inner_ok) {
+        rep->total_inner_iterations = info.total_inner_iterations;
+        if (info.inner_breakdown) {
             rep->converged = 0;
             rep->inner_breakdown = 1;
             break;
@@ -429,24 +578,10 @@ extern "C" int cvk_schwarz_solve(cvk_ctx* ctx, const cvk_grid* grid, double c, i
             break;
         }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (rep->sub_reports) {
-        for (int64_t s = 0; s < n_sub && s < rep->n_sub_reports; ++s) {
-            cvk_report& r = rep->sub_reports[s];
-            r.converged = hr[s].converged;
-            r.breakdown = hr[s].breakdown;
-            r.iterations = hr[s].iterations;
-            r.final_relres = hr[s].final_relres;
-            r.true_relres = hr[s].true_relres;
-            r.history_len = 0;
-        }
-    }
-    k_ddm_scatter<<<(unsigned)((ntot + threads - 1) / threads), threads, 0, st>>>(geo, d_u, d_x, (int)ntot);
-    DK(cudaGetLastError());
-    DK(cudaMemcpyAsync(x, d_x, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
-    DK(cudaStreamSynchronize(st));
-    rep->device_time_s = dev_ms * 1e-3;
+    if (rep->sub_reports) cvk_ddm_rank_reports(R, rep->sub_reports, rep->n_sub_reports);
+    e = cvk_ddm_rank_solution(R, x);  // all strips: the rank's columns are the whole grid
+    if (e != CVK_OK) return e;
+    rep->device_time_s = dev_s;
     rep->kernel_launches = launches + 1;
     rep->wall_time_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t_wall0;
