@@ -59,6 +59,7 @@ struct cvk_csr {
     size_t blob_bytes = 0;
     int group = 1;  // SpMV lanes per row for FAST mode
     int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
+    int* cmax = nullptr;  // [nchunks] largest column of each streamed chunk (L2 prefetch)
 };
 
 struct cvk_prec {
@@ -276,6 +277,17 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
             mk = std::max<long long>(mk, (long long)rp[(size_t)std::min<int64_t>(r0 + cvk::kStreamRows, nrows)] -
                                              (long long)rp[(size_t)r0]);
         A->capk = (int)((mk + 3) & ~3LL);
+        const int64_t nch = (nrows + cvk::kStreamRows - 1) / cvk::kStreamRows;
+        std::vector<int> cm((size_t)std::max<int64_t>(1, nch), -1);
+        for (int64_t q = 0; q < nch; ++q) {
+            const int64_t r1 = std::min<int64_t>((q + 1) * cvk::kStreamRows, nrows);
+            for (int64_t k = rp[(size_t)(q * cvk::kStreamRows)]; k < rp[(size_t)r1]; ++k)
+                cm[(size_t)q] = std::max(cm[(size_t)q], ci[(size_t)k]);
+        }
+        if (cudaMalloc(&A->cmax, sizeof(int) * cm.size()) == cudaSuccess)
+            cudaMemcpy(A->cmax, cm.data(), sizeof(int) * cm.size(), cudaMemcpyHostToDevice);
+        else
+            A->cmax = nullptr;
     }
     *out = A;
     return CVK_OK;
@@ -303,6 +315,7 @@ int cvk_csr_free(cvk_csr* A) {
     cudaSetDevice(A->ctx->device);
     cudaStreamSynchronize(A->ctx->stream);
     cudaFree(A->blob);
+    if (A->cmax) cudaFree(A->cmax);
     delete A;
     return CVK_OK;
 }
@@ -522,9 +535,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
         return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
-    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev,
+    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
                           (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, st5, st7, st8,
-                          std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0);
+                          std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0,
+                          std::getenv("CVK_STREAM_DYN") ? std::atoi(std::getenv("CVK_STREAM_DYN")) : 0,
+                          std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};

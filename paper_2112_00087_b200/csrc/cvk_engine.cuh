@@ -48,6 +48,7 @@ struct Csr {
     const int* __restrict__ rp;
     const int* __restrict__ ci;
     const double2* __restrict__ av;
+    const int* cmax = nullptr;  // per streamed chunk: largest column index (L2 prefetch window), optional
 };
 
 // Kernel arguments (passed by value to cudaLaunchCooperativeKernel).

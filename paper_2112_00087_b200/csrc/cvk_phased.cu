@@ -43,6 +43,8 @@ struct PArgs {
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
     int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
     int contig;         // streamed chunk assignment (StreamLayout::contig)
+    int dyn;            // 1: dynamic chunk assignment (stream_rows, PState::chunk_ctr)
+    int pf_rows;        // StreamLayout::pf_rows (L2 prefetch of the forward gather band)
 };
 
 // ------------------------------------------------------------ tracing --
@@ -58,11 +60,14 @@ __device__ __forceinline__ unsigned long long tr_now() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+__device__ unsigned long long g_sprof[kTrK * kTrCta * 4];
+#define SPROF(kid) (g_sprof + ((size_t)(kid) * kTrCta + (blockIdx.x < kTrCta ? blockIdx.x : 0)) * 4)
 #define TR(kid, it, slot) \
     do { if (threadIdx.x == 0 && blockIdx.x < kTrCta) \
         g_trace[((((kid) * kTrIt + ((it) % kTrIt)) * kTrCta) + blockIdx.x) * 4 + (slot)] = tr_now(); } while (0)
 #else
 #define TR(kid, it, slot) do { } while (0)
+#define SPROF(kid) ((unsigned long long*)nullptr)
 #endif
 
 constexpr int kPhSlots = 8;  // partial slots per phase: hi + lo for up to 4 reductions
@@ -603,7 +608,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ pn = cur ? V.p0 : V.p1;
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
-    const StreamLayout L{a.capk, 5, a.st5, a.contig};
+    StreamLayout L{a.capk, 5, a.st5, a.contig};
+    L.ngather = 3;
+    L.pf_rows = a.pf_rows;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {
@@ -622,10 +629,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         pn[row] = xs(t);
         vn[row] = vi;
         acc_dot(acc[0], ch.v(3, t), vi);
-    });
+    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1));
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
     if (threadIdx.x != 0) return;
+    st->chunk_ctr[0] = 0u;
     if (cvk_abs(tot[0]) < st->brk) {
         st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
         return;
@@ -650,7 +658,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ t_ = V.t;
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
-    const StreamLayout L{a.capk, 5, a.st5, a.contig};
+    StreamLayout L{a.capk, 5, a.st5, a.contig};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -665,10 +675,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
         acc_norm(acc[0], si);
         acc_dot(acc[1], ti, ti);
         acc_dot(acc[2], ti, si);
-    });
+    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2));
     double2 tot[3];
     if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
+    st->chunk_ctr[1] = 0u;
     const double relres = sqrt(tot[0].x) / st->bnorm;
     if (relres <= st->tol) {
         st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
@@ -697,7 +708,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
-    const StreamLayout L{a.capk, 7, a.st7, a.contig};
+    StreamLayout L{a.capk, 7, a.st7, a.contig};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
     CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -715,10 +728,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
         V.d[row] = cvk_add(cvk_mul(coef, di), ui);
         acc_norm(acc[0], wi);
         acc_dot(acc[1], ch.v(6, t), wi);
-    });
+    }, a.dyn ? &st->chunk_ctr[2] : nullptr, SPROF(3));
     double2 tot[2];
     if (!partial_last<2, kStreamThreads>(acc, partv(a, 0), &st->counter[0], tot)) return;
     if (threadIdx.x != 0) return;
+    st->chunk_ctr[2] = 0u;
     st->cur ^= 1;
     st->theta = sqrt(tot[0].x) / st->tau;
     const double c = 1.0 / sqrt(1.0 + st->theta * st->theta);
@@ -749,7 +763,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
-    const StreamLayout L{a.capk, 8, a.st8, a.contig};
+    StreamLayout L{a.capk, 8, a.st8, a.contig};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
@@ -765,10 +781,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
         V.au[row] = an;
         a.x[row] = cvk_add(ch.v(5, t), cvk_mul(eta_o, ch.v(6, t)));
         acc_dot(acc[0], ch.v(7, t), vi);
-    });
+    }, a.dyn ? &st->chunk_ctr[3] : nullptr, SPROF(3));
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
     if (threadIdx.x != 0) return;
+    st->chunk_ctr[3] = 0u;
     st->pending_x = 0;
     st->cur ^= 1;
     st->it++;
@@ -838,8 +855,14 @@ PhasedKernels phased_kernels() { return kernels_all(); }
 
 int phased_trace_read(void* out, size_t bytes) {
 #ifdef CVK_TRACE
-    const size_t n = sizeof(g_trace) < bytes ? sizeof(g_trace) : bytes;
-    return cudaMemcpyFromSymbol(out, g_trace, n) == cudaSuccess ? (int)n : -1;
+    // [g_trace | g_sprof]
+    size_t n = sizeof(g_trace) < bytes ? sizeof(g_trace) : bytes;
+    if (cudaMemcpyFromSymbol(out, g_trace, n) != cudaSuccess) return -1;
+    if (bytes >= sizeof(g_trace) + sizeof(g_sprof)) {
+        if (cudaMemcpyFromSymbol((char*)out + sizeof(g_trace), g_sprof, sizeof(g_sprof)) != cudaSuccess) return -1;
+        n += sizeof(g_sprof);
+    }
+    return (int)n;
 #else
     (void)out; (void)bytes;
     return 0;
@@ -850,9 +873,11 @@ size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8, int contig) {
+                      int capk, int st5, int st7, int st8, int contig, int dyn, int pf_rows) {
     PArgs* p = (PArgs*)out;
+    p->pf_rows = pf_rows;
     p->contig = contig;
+    p->dyn = dyn;
     p->capk = capk;
     p->st5 = st5;
     p->st7 = st7;

@@ -19,6 +19,7 @@ struct PState {
     long long it, iters, max_iter, hist_len, hist_cap;
     int done, conv, brk_code, first, pending_x, cur, record, skip_true;
     unsigned counter[4];
+    unsigned chunk_ctr[4];  // dynamic chunk counters of the streamed kernels (reset by their last CTA)
 };
 
 struct PhasedKernels {
@@ -35,6 +36,6 @@ int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8, int contig);
+                      int capk, int st5, int st7, int st8, int contig, int dyn, int pf_rows);
 
 }  // namespace cvk

@@ -73,6 +73,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         " bra.uni WAIT%=;\n"
         "DONE%=:\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
@@ -84,6 +87,8 @@ struct StreamLayout {
     int nvec;    // staged row-local vectors
     int stages;  // ring depth
     int contig = 0;  // 1: each CTA takes a contiguous block of chunks; 0: grid-stride
+    int ngather = 0;  // vecs[0..ngather) are also gathered at neighbour columns
+    int pf_rows = 0;  // L2-prefetch window (rows) below the chunk's largest column, 0 = off
     __host__ __device__ size_t rp_bytes() const { return (size_t)(kStreamRows + 4) * 4; }
     __host__ __device__ size_t ci_bytes() const { return (size_t)(capk + 8) * 4; }
     __host__ __device__ size_t av_bytes() const { return (size_t)capk * 16; }
@@ -91,7 +96,10 @@ struct StreamLayout {
     __host__ __device__ size_t stage_bytes() const {
         return rp_bytes() + ci_bytes() + av_bytes() + (size_t)nvec * vec_bytes();
     }
-    __host__ __device__ size_t smem_bytes() const { return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8; }
+    // stages, then full / empty barriers, then the per-stage chunk header
+    __host__ __device__ size_t smem_bytes() const {
+        return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8 + kStreamMaxStages * 4;
+    }
 };
 
 // What a consumer thread sees of its chunk.
@@ -142,11 +150,62 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
 // (nullptr entries are skipped but keep their slot).  body(t, chunk) runs for
 // every row t < rows of every chunk in consumer threads.  Must be called by
 // all kStreamThreads threads of the CTA; returns when the CTA's chunks are done.
+//
+// Chunk assignment: with dyn == nullptr, static (grid-stride, or contiguous
+// blocks with L.contig).  With dyn pointing at a zeroed global counter,
+// dynamic: the producer takes kDynBatch chunks at a time with one atomicAdd,
+// so slower SMs simply stream fewer chunks (the static grid-stride split left
+// the p90 CTA of the BiCGSTAB s/t phase 25% behind the median,
+// profiles/r01_phase_timeline.txt).  The chunk index travels to the consumers
+// in a per-stage header; -1 ends a consumer group.  FAST reductions are
+// double-double, so the run-to-run varying chunk-to-CTA map does not change
+// any result bit.  The caller resets *dyn after the kernel (last CTA).
+constexpr int kDynBatch = 2;
+
+__device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L, const double2* const* vecs,
+                                             unsigned char* sp, uint64_t* bar, int chunk, int k0, int k1,
+                                             int cmax) {
+    const int n = A.n;
+    const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
+    const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
+    const uint32_t b_rp = (uint32_t)(((rows + 1 + 3) & ~3) * 4);
+    const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
+    const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
+    const uint32_t b_v = (uint32_t)(rows * 16);
+    uint32_t tx = b_rp + b_ci + b_av;
+    for (int j2 = 0; j2 < L.nvec; ++j2)
+        if (vecs[j2]) tx += b_v;
+    mbar_expect_tx(bar, tx);
+    bulk_g2s(sp, A.rp + r0, b_rp, bar);
+    unsigned char* q = sp + L.rp_bytes();
+    if (b_ci) bulk_g2s(q, A.ci + a0, b_ci, bar);
+    q += L.ci_bytes();
+    if (b_av) bulk_g2s(q, A.av + k0, b_av, bar);
+    q += L.av_bytes();
+    for (int j2 = 0; j2 < L.nvec; ++j2, q += L.vec_bytes())
+        if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, bar);
+    // forward band of the gathered vectors (e.g. the +nx neighbours of the
+    // cavity grid): not yet streamed by any CTA, so the consumers' gathers
+    // would miss to DRAM -- pull it into L2 now
+    if (L.pf_rows > 0 && cmax >= r0 + rows) {
+        const int lo = max(r0 + rows, cmax - L.pf_rows + 1), hi = min(cmax, n - 1);
+        if (hi >= lo)
+            for (int j2 = 0; j2 < L.ngather; ++j2)
+                if (vecs[j2]) bulk_prefetch_l2(vecs[j2] + lo, (uint32_t)((hi - lo + 1) * 16));
+    }
+}
+
+// prof (measurement builds): [0] producer cycles waiting for free stages,
+// [1] consumer (thread 0) cycles waiting for full stages, [2] consumer cycles
+// in the row body, [3] chunks consumed by thread 0's group
 template <class Body>
 __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L, const double2* const* vecs,
-                                            unsigned char* smem, Body&& body) {
+                                            unsigned char* smem, Body&& body, unsigned* dyn = nullptr,
+                                            unsigned long long* prof = nullptr) {
+    unsigned long long pw = 0, cw = 0, cb = 0, cn = 0;
     uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
     uint64_t* empty = full + kStreamMaxStages;
+    int* hdr = (int*)(empty + kStreamMaxStages);
     const int n = A.n;
     const int nchunks = (n + kStreamRows - 1) / kStreamRows;
     const int G = gridDim.x;
@@ -160,7 +219,7 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // this CTA's chunks: chunk_of(i), i < cnt
+    // static split: this CTA's chunks first + i * step, i < cnt
     const int cpc = (nchunks + G - 1) / G;
     const int first = L.contig ? blockIdx.x * cpc : blockIdx.x;
     const int cnt = L.contig ? max(0, min(nchunks, first + cpc) - first)
@@ -168,49 +227,74 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     const int step = L.contig ? 1 : G;
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
-        for (int i0 = 0; i0 < cnt; i0 += 32) {
-            const int cj = first + (i0 + lane) * step;
-            int k0j = 0, k1j = 0;
-            if (i0 + lane < cnt) {
-                k0j = __ldg(A.rp + cj * kStreamRows);
-                k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
+        int it = 0;
+        auto put = [&](int chunk, int k0, int k1, int cm) {  // lane 0
+            const int s = it % ST;
+            const long long t0 = prof ? clock64() : 0;
+            mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
+            if (prof) pw += clock64() - t0;
+            hdr[s] = chunk;
+            stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, chunk, k0, k1, cm);
+            ++it;
+        };
+        const bool pf = L.pf_rows > 0 && A.cmax != nullptr;
+        if (dyn) {
+            int base = 0;
+            if (lane == 0) base = (int)atomicAdd(dyn, (unsigned)kDynBatch);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            while (base < nchunks) {
+                int k0j = 0, k1j = 0, cmj = -1;
+                if (lane < kDynBatch && base + lane < nchunks) {
+                    const int cj = base + lane;
+                    k0j = __ldg(A.rp + cj * kStreamRows);
+                    k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
+                    if (pf) cmj = __ldg(A.cmax + cj);
+                }
+                int nb = 0;
+                if (lane == 0) nb = (int)atomicAdd(dyn, (unsigned)kDynBatch);  // next batch, in flight
+#pragma unroll
+                for (int j = 0; j < kDynBatch; ++j) {
+                    const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
+                    const int cm = __shfl_sync(0xffffffffu, cmj, j);
+                    if (lane == 0 && base + j < nchunks) put(base + j, k0, k1, cm);
+                }
+                base = __shfl_sync(0xffffffffu, nb, 0);
             }
-            for (int j = 0; j < 32; ++j) {
-                const int it = i0 + j;
-                if (it >= cnt) break;
-                const int chunk = first + it * step;
-                const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
-                if (lane == 0) {
+            if (lane == 0) {
+                for (int g = 0; g < kStreamGroups; ++g) {  // one end marker per consumer group
                     const int s = it % ST;
                     mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
-                    unsigned char* sp = smem + (size_t)s * L.stage_bytes();
-                    const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
-                    const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
-                    const uint32_t b_rp = (uint32_t)(((rows + 1 + 3) & ~3) * 4);
-                    const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
-                    const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
-                    const uint32_t b_v = (uint32_t)(rows * 16);
-                    uint32_t tx = b_rp + b_ci + b_av;
-                    for (int j2 = 0; j2 < L.nvec; ++j2)
-                        if (vecs[j2]) tx += b_v;
-                    mbar_expect_tx(full + s, tx);
-                    bulk_g2s(sp, A.rp + r0, b_rp, full + s);
-                    unsigned char* q = sp + L.rp_bytes();
-                    if (b_ci) bulk_g2s(q, A.ci + a0, b_ci, full + s);
-                    q += L.ci_bytes();
-                    if (b_av) bulk_g2s(q, A.av + k0, b_av, full + s);
-                    q += L.av_bytes();
-                    for (int j2 = 0; j2 < L.nvec; ++j2, q += L.vec_bytes())
-                        if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, full + s);
+                    hdr[s] = -1;
+                    mbar_arrive(full + s);
+                    ++it;
+                }
+            }
+        } else {
+            for (int i0 = 0; i0 < cnt; i0 += 32) {
+                const int cj = first + (i0 + lane) * step;
+                int k0j = 0, k1j = 0, cmj = -1;
+                if (i0 + lane < cnt) {
+                    k0j = __ldg(A.rp + cj * kStreamRows);
+                    k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
+                    if (pf) cmj = __ldg(A.cmax + cj);
+                }
+                for (int j = 0; j < 32; ++j) {
+                    if (i0 + j >= cnt) break;
+                    const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
+                    const int cm = __shfl_sync(0xffffffffu, cmj, j);
+                    if (lane == 0) put(first + (i0 + j) * step, k0, k1, cm);
                 }
             }
         }
     } else {
         const int g = tid / kStreamRows, t = tid % kStreamRows;
-        for (int it = g; it < cnt; it += kStreamGroups) {
-            const int chunk = first + it * step;
+        for (int it = g; dyn || it < cnt; it += kStreamGroups) {
             const int s = it % ST;
+            const long long t0 = prof ? clock64() : 0;
             mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
+            const long long t1 = prof ? clock64() : 0;
+            const int chunk = hdr[s];
+            if (chunk < 0) break;
             const unsigned char* sp = smem + (size_t)s * L.stage_bytes();
             Chunk ch;
             ch.rp = (const int*)sp;
@@ -223,7 +307,17 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             ch.cio = ch.k0 & 3;
             if (t < ch.rows) body(t, ch);
             mbar_arrive(empty + s);
+            if (prof) {
+                const long long t2 = clock64();
+                cw += t1 - t0;
+                cb += t2 - t1;
+                ++cn;
+            }
         }
+    }
+    if (prof) {
+        if (tid == kStreamGroups * kStreamRows) prof[0] = pw;
+        if (tid == 0) { prof[1] = cw; prof[2] = cb; prof[3] = cn; }
     }
 }
 

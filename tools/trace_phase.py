@@ -25,10 +25,11 @@ P.bicgstab(A, prob.b, M, P.SolverOptions(tol=1e-30, max_iter=maxit))
 r = P.bicgstab(A, prob.b, M, P.SolverOptions(tol=1e-30, max_iter=maxit))
 L = _lib.load()
 L.cvk_trace_read.restype = C.c_int
-buf = np.zeros(KT * IT * CTA * 4, np.uint64)
+buf = np.zeros(KT * IT * CTA * 4 + KT * CTA * 4, np.uint64)
 got = L.cvk_trace_read(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes))
 assert got > 0, "not a CVK_TRACE build"
-t = buf.reshape(KT, IT, CTA, 4).astype(np.float64)
+t = buf[:KT * IT * CTA * 4].reshape(KT, IT, CTA, 4).astype(np.float64)
+sp = buf[KT * IT * CTA * 4:].reshape(KT, CTA, 4).astype(np.float64)
 names = {1: "k_bi_a_s", 2: "k_bi_b_s", 0: "k_bi_c"}
 order = [1, 2, 0]
 rows = []
@@ -67,3 +68,10 @@ for k in order:
     slow = ids[np.argsort(-d)[:8]]
     print(f"{names[k]:9} loop us: p10 {np.percentile(d, 10):.2f} p50 {np.median(d):.2f} "
           f"p90 {np.percentile(d, 90):.2f} max {d.max():.2f}; slowest CTAs {list(slow)}")
+
+# streamed-kernel pipeline balance (last launch of each kernel, clock cycles per CTA)
+for k in (1, 2):
+    blk = sp[k, :148]
+    print(f"{names[k]:9} producer waits for free stage {np.median(blk[:, 0]) / 1965:.2f} us, consumer waits for "
+          f"full stage {np.median(blk[:, 1]) / 1965:.2f} us, consumer body {np.median(blk[:, 2]) / 1965:.2f} us, "
+          f"chunks/group {np.median(blk[:, 3]):.0f} (medians over CTAs)")
