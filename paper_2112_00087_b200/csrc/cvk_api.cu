@@ -60,6 +60,7 @@ struct cvk_csr {
     int group = 1;  // SpMV lanes per row for FAST mode
     int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
     int* cmax = nullptr;  // [nchunks] largest column of each streamed chunk (L2 prefetch)
+    int4* bands = nullptr;  // [nchunks] halo bands {b0, w0, b1, w1} of each streamed chunk
 };
 
 struct cvk_prec {
@@ -288,6 +289,38 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
             cudaMemcpy(A->cmax, cm.data(), sizeof(int) * cm.size(), cudaMemcpyHostToDevice);
         else
             A->cmax = nullptr;
+        // Halo bands: the out-of-chunk columns of each chunk, clustered; the two
+        // most-referenced clusters that fit in kStreamRows rows are staged with
+        // the chunk (cvk_stream.cuh).  For the cavity grid these are the +-nx
+        // neighbour rows; anything else stays a global gather.
+        std::vector<int4> bd((size_t)std::max<int64_t>(1, nch), make_int4(0, 0, 0, 0));
+        bool any = false;
+        std::vector<int> cols;
+        for (int64_t q = 0; q < nch; ++q) {
+            const int64_t r0 = q * cvk::kStreamRows, r1 = std::min<int64_t>(r0 + cvk::kStreamRows, nrows);
+            cols.clear();
+            for (int64_t k = rp[(size_t)r0]; k < rp[(size_t)r1]; ++k)
+                if (ci[(size_t)k] < r0 || ci[(size_t)k] >= r1) cols.push_back(ci[(size_t)k]);
+            if (cols.empty()) continue;
+            std::sort(cols.begin(), cols.end());
+            // clusters: maximal runs whose span fits a band
+            struct Cl { int lo, hi, cnt; };
+            std::vector<Cl> cl;
+            for (int v : cols) {
+                if (!cl.empty() && v - cl.back().lo < cvk::kStreamRows) { cl.back().hi = v; cl.back().cnt++; }
+                else cl.push_back({v, v, 1});
+            }
+            std::sort(cl.begin(), cl.end(), [](const Cl& a, const Cl& b) { return a.cnt > b.cnt; });
+            int4 b = make_int4(0, 0, 0, 0);
+            if (cl.size() >= 1 && cl[0].cnt >= 8) { b.x = cl[0].lo; b.y = cl[0].hi - cl[0].lo + 1; }
+            if (cl.size() >= 2 && cl[1].cnt >= 8) { b.z = cl[1].lo; b.w = cl[1].hi - cl[1].lo + 1; }
+            if (b.y || b.w) any = true;
+            bd[(size_t)q] = b;
+        }
+        if (any && cudaMalloc(&A->bands, sizeof(int4) * bd.size()) == cudaSuccess)
+            cudaMemcpy(A->bands, bd.data(), sizeof(int4) * bd.size(), cudaMemcpyHostToDevice);
+        else
+            A->bands = nullptr;
     }
     *out = A;
     return CVK_OK;
@@ -316,6 +349,7 @@ int cvk_csr_free(cvk_csr* A) {
     cudaStreamSynchronize(A->ctx->stream);
     cudaFree(A->blob);
     if (A->cmax) cudaFree(A->cmax);
+    if (A->bands) cudaFree(A->bands);
     delete A;
     return CVK_OK;
 }
@@ -513,17 +547,27 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    auto stages_for = [&](int nvec) {
-        cvk::StreamLayout L{A->capk, nvec, 1};
-        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8;
-        long long cap = 4;  // 4-stage ring (measured: 4 >= 5, 3, 2 on the 1M-DOF cavity)
-        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
-        return (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));
+    // per kernel: staged vectors, gathered vectors (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s)
+    const int kvec[4] = {5, 5, 7, 8}, kgat[4] = {3, 2, 2, 2};
+    // halo-band staging: measured no faster on the 1M cavity (consumer latency is
+    // not dominated by the out-of-chunk gathers), so opt-in (CVK_BANDS=1)
+    const int nband = (A->bands && std::getenv("CVK_BANDS") && std::atoi(std::getenv("CVK_BANDS"))) ? 1 : 0;
+    auto layout_for = [&](int k, int stg) {
+        cvk::StreamLayout L{A->capk, kvec[k], stg};
+        L.ngather = kgat[k];
+        L.nband = nband;
+        return L;
     };
-    const int st5 = stages_for(5), st7 = stages_for(7), st8 = stages_for(8);
+    int stg[4];
+    for (int k = 0; k < 4; ++k) {
+        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+        long long cap = nband ? 3 : 4;  // measured best ring depths
+        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
+        stg[k] = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)layout_for(k, 1).stage_bytes()));
+    }
     const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&
-                          (solver == CVK_BICGSTAB ? st5 >= 2 : std::min(st7, st8) >= 2);
-    auto smem_for = [&](int nvec, int stg) { return cvk::StreamLayout{A->capk, nvec, stg}.smem_bytes(); };
+                          (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2 : std::min(stg[2], stg[3]) >= 2);
+    auto smem_for = [&](int k) { return layout_for(k, stg[k]).smem_bytes(); };
     const void* sk[4] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096));
@@ -535,11 +579,12 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
         return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
-    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, st5, st7, st8,
+    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, A->bands}, M->dinv, b_dev, x_dev,
+                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, stg,
                           std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0,
                           std::getenv("CVK_STREAM_DYN") ? std::atoi(std::getenv("CVK_STREAM_DYN")) : 0,
-                          std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows);
+                          std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : (nband ? 0 : 2 * cvk::kStreamRows),
+                          nband);
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
@@ -562,8 +607,8 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         for (int it = 0; it < kIterPerGraph; ++it) {
             if (solver == CVK_BICGSTAB) {
                 if (streamed) {
-                    launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(5, st5), c->stream);
-                    launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(5, st5), c->stream);
+                    launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(0), c->stream);
+                    launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(1), c->stream);
                 } else {
                     launch_pdl(K.bi_a, grid, block, args, smem, c->stream);
                     launch_pdl(K.bi_b, grid, block, args, smem, c->stream);
@@ -572,8 +617,8 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
             } else {
                 launch_pdl(K.tf_w, egrid, block, args, 0, c->stream);
                 if (streamed) {
-                    launch_pdl(K.tf_e_s, sgrid, sblock, args, smem_for(7, st7), c->stream);
-                    launch_pdl(K.tf_o_s, sgrid, sblock, args, smem_for(8, st8), c->stream);
+                    launch_pdl(K.tf_e_s, sgrid, sblock, args, smem_for(2), c->stream);
+                    launch_pdl(K.tf_o_s, sgrid, sblock, args, smem_for(3), c->stream);
                 } else {
                     launch_pdl(K.tf_e, grid, block, args, smem, c->stream);
                     launch_pdl(K.tf_o, grid, block, args, smem, c->stream);

@@ -49,6 +49,7 @@ struct Csr {
     const int* __restrict__ ci;
     const double2* __restrict__ av;
     const int* cmax = nullptr;  // per streamed chunk: largest column index (L2 prefetch window), optional
+    const int4* bands = nullptr;  // per streamed chunk: halo bands {b0, w0, b1, w1} (cvk_stream.cuh), optional
 };
 
 // Kernel arguments (passed by value to cudaLaunchCooperativeKernel).

@@ -41,10 +41,11 @@ struct PArgs {
     double* hist;
     DevReport* rep;
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
-    int st5, st7, st8;  // ring depths for 5 / 7 / 8 staged vectors
+    int nst[4];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s
     int contig;         // streamed chunk assignment (StreamLayout::contig)
     int dyn;            // 1: dynamic chunk assignment (stream_rows, PState::chunk_ctr)
     int pf_rows;        // StreamLayout::pf_rows (L2 prefetch of the forward gather band)
+    int nband;          // StreamLayout::nband (stage the halo bands of the gathered vectors)
 };
 
 // ------------------------------------------------------------ tracing --
@@ -608,9 +609,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ pn = cur ? V.p0 : V.p1;
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
-    StreamLayout L{a.capk, 5, a.st5, a.contig};
+    StreamLayout L{a.capk, 5, a.nst[0], a.contig};
     L.ngather = 3;
     L.pf_rows = a.pf_rows;
+    L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {
@@ -658,9 +660,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ t_ = V.t;
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
-    StreamLayout L{a.capk, 5, a.st5, a.contig};
+    StreamLayout L{a.capk, 5, a.nst[1], a.contig};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
+    L.nband = a.nband;
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -708,9 +711,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
-    StreamLayout L{a.capk, 7, a.st7, a.contig};
+    StreamLayout L{a.capk, 7, a.nst[2], a.contig};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
+    L.nband = a.nband;
     CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
@@ -763,9 +767,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
-    StreamLayout L{a.capk, 8, a.st8, a.contig};
+    StreamLayout L{a.capk, 8, a.nst[3], a.contig};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
+    L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
@@ -873,15 +878,14 @@ size_t phased_args_size() { return sizeof(PArgs); }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8, int contig, int dyn, int pf_rows) {
+                      int capk, const int* nst, int contig, int dyn, int pf_rows, int nband) {
     PArgs* p = (PArgs*)out;
+    p->nband = nband;
     p->pf_rows = pf_rows;
     p->contig = contig;
     p->dyn = dyn;
     p->capk = capk;
-    p->st5 = st5;
-    p->st7 = st7;
-    p->st8 = st8;
+    for (int i = 0; i < 4; ++i) p->nst[i] = nst[i];
     p->A = A;
     p->dinv = dinv;
     p->b = b;

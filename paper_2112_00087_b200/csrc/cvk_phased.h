@@ -36,6 +36,6 @@ int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, int st5, int st7, int st8, int contig, int dyn, int pf_rows);
+                      int capk, const int* nst, int contig, int dyn, int pf_rows, int nband);
 
 }  // namespace cvk

@@ -89,16 +89,19 @@ struct StreamLayout {
     int contig = 0;  // 1: each CTA takes a contiguous block of chunks; 0: grid-stride
     int ngather = 0;  // vecs[0..ngather) are also gathered at neighbour columns
     int pf_rows = 0;  // L2-prefetch window (rows) below the chunk's largest column, 0 = off
+    int nband = 0;    // 1: stage the chunk's halo bands of the gathered vectors (A.bands)
     __host__ __device__ size_t rp_bytes() const { return (size_t)(kStreamRows + 4) * 4; }
     __host__ __device__ size_t ci_bytes() const { return (size_t)(capk + 8) * 4; }
     __host__ __device__ size_t av_bytes() const { return (size_t)capk * 16; }
     __host__ __device__ size_t vec_bytes() const { return (size_t)kStreamRows * 16; }
+    // gathered vectors get 3 R slots when banded: [chunk rows | band 0 | band 1]
+    __host__ __device__ int gslots() const { return nband ? 3 : 1; }
     __host__ __device__ size_t stage_bytes() const {
-        return rp_bytes() + ci_bytes() + av_bytes() + (size_t)nvec * vec_bytes();
+        return rp_bytes() + ci_bytes() + av_bytes() + (size_t)(nvec + (gslots() - 1) * ngather) * vec_bytes();
     }
-    // stages, then full / empty barriers, then the per-stage chunk header
+    // stages, then full / empty barriers, then the per-stage header (8 ints)
     __host__ __device__ size_t smem_bytes() const {
-        return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8 + kStreamMaxStages * 4;
+        return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8 + kStreamMaxStages * 32;
     }
 };
 
@@ -107,17 +110,28 @@ struct Chunk {
     const int* rp;      // global row offsets of rows r0 .. r0+rows
     const int* ci;      // columns, index k - k0 + cio
     const double2* av;  // values, index k - k0
-    const double2* vec; // staged vectors, vec[j * R + l]
+    const double2* vec; // staged vectors (voff)
     int k0, cio, r0, rows;
-    __device__ __forceinline__ double2 v(int j, int l) const { return vec[j * kStreamRows + l]; }
-    __device__ __forceinline__ bool local(int c, int& l) const {
-        l = c - r0;
-        return (unsigned)l < (unsigned)rows;
+    int ng, gs;         // gathered vectors, their slot count (1, or 3 when banded)
+    int b0, w0, b1, w1; // halo bands [b, b + w) (w = 0: none)
+    __device__ __forceinline__ int voff(int j) const {
+        return (j < ng ? j * gs : ng * gs + (j - ng)) * kStreamRows;
+    }
+    __device__ __forceinline__ double2 v(int j, int l) const { return vec[voff(j) + l]; }
+    // slot of column c in a gathered vector's staged data, or -1 (global)
+    __device__ __forceinline__ int stage_index(int c) const {
+        const int l = c - r0;
+        if ((unsigned)l < (unsigned)rows) return l;
+        const int l0 = c - b0, l1 = c - b1;
+        if ((unsigned)l0 < (unsigned)w0) return kStreamRows + l0;
+        if ((unsigned)l1 < (unsigned)w1) return 2 * kStreamRows + l1;
+        return -1;
     }
 };
 
 // Row sum for row t of the chunk: y = sum_k A[k] * x(col_k), left to right,
-// with x read through xs(l) for in-chunk columns and xg(c) otherwise.  The
+// with x read through xs(l) for columns staged in shared memory (the chunk's
+// rows and its halo bands; l = Chunk::stage_index) and xg(c) otherwise.  The
 // (value, column) pairs of a batch come from shared memory; the global
 // gathers of a batch are all issued before the first product.
 template <int BATCH, class XS, class XG>
@@ -136,8 +150,8 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
 #pragma unroll
         for (int u = 0; u < BATCH; ++u)
             if (k + u < e) {
-                int l;
-                xv[u] = ch.local(c[u], l) ? xs(l) : xg(c[u]);
+                const int l = ch.stage_index(c[u]);
+                xv[u] = l >= 0 ? xs(l) : xg(c[u]);
             }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u)
@@ -164,7 +178,7 @@ constexpr int kDynBatch = 2;
 
 __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L, const double2* const* vecs,
                                              unsigned char* sp, uint64_t* bar, int chunk, int k0, int k1,
-                                             int cmax) {
+                                             int cmax, int4 band) {
     const int n = A.n;
     const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
     const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
@@ -172,9 +186,11 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
     const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
     const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
     const uint32_t b_v = (uint32_t)(rows * 16);
+    const bool banded = L.nband != 0;
+    const uint32_t b_h0 = banded ? (uint32_t)(band.y * 16) : 0u, b_h1 = banded ? (uint32_t)(band.w * 16) : 0u;
     uint32_t tx = b_rp + b_ci + b_av;
     for (int j2 = 0; j2 < L.nvec; ++j2)
-        if (vecs[j2]) tx += b_v;
+        if (vecs[j2]) tx += b_v + (j2 < L.ngather ? b_h0 + b_h1 : 0u);
     mbar_expect_tx(bar, tx);
     bulk_g2s(sp, A.rp + r0, b_rp, bar);
     unsigned char* q = sp + L.rp_bytes();
@@ -182,8 +198,16 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
     q += L.ci_bytes();
     if (b_av) bulk_g2s(q, A.av + k0, b_av, bar);
     q += L.av_bytes();
-    for (int j2 = 0; j2 < L.nvec; ++j2, q += L.vec_bytes())
-        if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, bar);
+    for (int j2 = 0; j2 < L.nvec; ++j2) {
+        if (vecs[j2]) {
+            bulk_g2s(q, vecs[j2] + r0, b_v, bar);
+            if (j2 < L.ngather && banded) {
+                if (b_h0) bulk_g2s(q + L.vec_bytes(), vecs[j2] + band.x, b_h0, bar);
+                if (b_h1) bulk_g2s(q + 2 * L.vec_bytes(), vecs[j2] + band.z, b_h1, bar);
+            }
+        }
+        q += (j2 < L.ngather ? L.gslots() : 1) * L.vec_bytes();
+    }
     // forward band of the gathered vectors (e.g. the +nx neighbours of the
     // cavity grid): not yet streamed by any CTA, so the consumers' gathers
     // would miss to DRAM -- pull it into L2 now
@@ -228,13 +252,18 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
         int it = 0;
-        auto put = [&](int chunk, int k0, int k1, int cm) {  // lane 0
+        const bool banded = L.nband != 0 && A.bands != nullptr;
+        auto put = [&](int chunk, int k0, int k1, int cm, int4 band) {  // lane 0
             const int s = it % ST;
             const long long t0 = prof ? clock64() : 0;
             mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
             if (prof) pw += clock64() - t0;
-            hdr[s] = chunk;
-            stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, chunk, k0, k1, cm);
+            hdr[8 * s] = chunk;
+            hdr[8 * s + 1] = band.x;
+            hdr[8 * s + 2] = band.y;
+            hdr[8 * s + 3] = band.z;
+            hdr[8 * s + 4] = band.w;
+            stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, chunk, k0, k1, cm, band);
             ++it;
         };
         const bool pf = L.pf_rows > 0 && A.cmax != nullptr;
@@ -244,11 +273,13 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             base = __shfl_sync(0xffffffffu, base, 0);
             while (base < nchunks) {
                 int k0j = 0, k1j = 0, cmj = -1;
+                int4 bj = make_int4(0, 0, 0, 0);
                 if (lane < kDynBatch && base + lane < nchunks) {
                     const int cj = base + lane;
                     k0j = __ldg(A.rp + cj * kStreamRows);
                     k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
                     if (pf) cmj = __ldg(A.cmax + cj);
+                    if (banded) bj = __ldg(A.bands + cj);
                 }
                 int nb = 0;
                 if (lane == 0) nb = (int)atomicAdd(dyn, (unsigned)kDynBatch);  // next batch, in flight
@@ -256,7 +287,9 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
                 for (int j = 0; j < kDynBatch; ++j) {
                     const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
                     const int cm = __shfl_sync(0xffffffffu, cmj, j);
-                    if (lane == 0 && base + j < nchunks) put(base + j, k0, k1, cm);
+                    const int4 bd = make_int4(__shfl_sync(0xffffffffu, bj.x, j), __shfl_sync(0xffffffffu, bj.y, j),
+                                              __shfl_sync(0xffffffffu, bj.z, j), __shfl_sync(0xffffffffu, bj.w, j));
+                    if (lane == 0 && base + j < nchunks) put(base + j, k0, k1, cm, bd);
                 }
                 base = __shfl_sync(0xffffffffu, nb, 0);
             }
@@ -264,7 +297,7 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
                 for (int g = 0; g < kStreamGroups; ++g) {  // one end marker per consumer group
                     const int s = it % ST;
                     mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
-                    hdr[s] = -1;
+                    hdr[8 * s] = -1;
                     mbar_arrive(full + s);
                     ++it;
                 }
@@ -273,16 +306,20 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             for (int i0 = 0; i0 < cnt; i0 += 32) {
                 const int cj = first + (i0 + lane) * step;
                 int k0j = 0, k1j = 0, cmj = -1;
+                int4 bj = make_int4(0, 0, 0, 0);
                 if (i0 + lane < cnt) {
                     k0j = __ldg(A.rp + cj * kStreamRows);
                     k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
                     if (pf) cmj = __ldg(A.cmax + cj);
+                    if (banded) bj = __ldg(A.bands + cj);
                 }
                 for (int j = 0; j < 32; ++j) {
                     if (i0 + j >= cnt) break;
                     const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
                     const int cm = __shfl_sync(0xffffffffu, cmj, j);
-                    if (lane == 0) put(first + (i0 + j) * step, k0, k1, cm);
+                    const int4 bd = make_int4(__shfl_sync(0xffffffffu, bj.x, j), __shfl_sync(0xffffffffu, bj.y, j),
+                                              __shfl_sync(0xffffffffu, bj.z, j), __shfl_sync(0xffffffffu, bj.w, j));
+                    if (lane == 0) put(first + (i0 + j) * step, k0, k1, cm, bd);
                 }
             }
         }
@@ -293,7 +330,7 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             const long long t0 = prof ? clock64() : 0;
             mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
             const long long t1 = prof ? clock64() : 0;
-            const int chunk = hdr[s];
+            const int chunk = hdr[8 * s];
             if (chunk < 0) break;
             const unsigned char* sp = smem + (size_t)s * L.stage_bytes();
             Chunk ch;
@@ -301,6 +338,12 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             ch.ci = (const int*)(sp + L.rp_bytes());
             ch.av = (const double2*)(sp + L.rp_bytes() + L.ci_bytes());
             ch.vec = (const double2*)(sp + L.rp_bytes() + L.ci_bytes() + L.av_bytes());
+            ch.ng = L.ngather;
+            ch.gs = L.gslots();
+            ch.b0 = hdr[8 * s + 1];
+            ch.w0 = L.nband ? hdr[8 * s + 2] : 0;
+            ch.b1 = hdr[8 * s + 3];
+            ch.w1 = L.nband ? hdr[8 * s + 4] : 0;
             ch.r0 = chunk * kStreamRows;
             ch.rows = min(kStreamRows, n - ch.r0);
             ch.k0 = ch.rp[0];
