@@ -685,6 +685,72 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     return CVK_OK;
 }
 
+// Persistent TMA-streamed BiCGSTAB (cvk_streamk.cu): one cooperative launch per
+// solve, one CTA per SM.  Returns CVK_OK, an error, or 1 if the matrix does
+// not fit the ring (caller falls back to the phase kernels).
+static int solve_streamk(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o, const double2* b_dev,
+                         double2* x_dev, cvk_report* rep) {
+    const int n = (int)A->n;
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    cvk::StreamLayout L{A->capk, 5, 1};
+    L.ngather = 3;
+    {
+        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+        long long cap = 4;
+        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
+        L.stages = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));
+    }
+    if (L.stages < 2 || A->nnz == 0) return 1;
+    const void* kern = cvk::streamk_bicgstab_kernel();
+    const size_t smem = L.smem_bytes();
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cvk::kStreamThreads, smem));
+    if (per_sm < 1) return 1;
+    const int G = c->nsm;
+    int e;
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 8 * (size_t)std::max(1, n))) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
+        return e;
+    const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
+    if (hcap > 0 && (size_t)hcap > c->hist_cap) {
+        cudaFree(c->hist);
+        c->hist = nullptr;
+        c->hist_cap = 0;
+        CK(cudaMalloc(&c->hist, sizeof(double) * hcap));
+        c->hist_cap = (size_t)hcap;
+    }
+    CK(cudaMemsetAsync(c->bar, 0, 2 * sizeof(unsigned long long), c->stream));
+    std::vector<unsigned char> blob(cvk::streamk_args_size());
+    cvk::streamk_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, A->bands}, M->dinv, b_dev, x_dev,
+                           (double2*)c->work, c->part, c->bar, c->rep, c->hist, hcap, o->tol,
+                           o->max_iter < 1 ? 0 : o->max_iter, o->record_history ? 1 : 0, L);
+    void* args[] = {blob.data()};
+    CK(cudaEventRecord(c->e0, c->stream));
+    CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kStreamThreads), args, smem, c->stream));
+    CK(cudaEventRecord(c->e1, c->stream));
+    DevReport dr;
+    CK(cudaMemcpyAsync(&dr, c->rep, sizeof(dr), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    if (dr.error) return fail(CVK_ETIMEOUT, "bicgstab: device grid barrier aborted");
+    rep->converged = dr.converged;
+    rep->breakdown = dr.breakdown;
+    rep->iterations = dr.iterations;
+    rep->final_relres = dr.final_relres;
+    rep->true_relres = dr.true_relres;
+    rep->history_len = o->record_history ? dr.history_len : 0;
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = 1;
+    if (o->record_history && rep->history && rep->history_cap > 0) {
+        const long long k = std::min<long long>(std::min<long long>(rep->history_len, rep->history_cap), hcap);
+        if (k > 0) CK(cudaMemcpy(rep->history, c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    return CVK_OK;
+}
+
 static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                       const double2* b_dev, double2* x_dev, cvk_report* rep) {
     if (solver < 0 || solver > 3)
@@ -703,6 +769,11 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     const int mode = resolve_mode(c, o->mode);
     const bool ref = mode == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
+    if (!ref && solver == CVK_BICGSTAB && (long long)n >= phased_min_n() &&
+        !(std::getenv("CVK_STREAMK") && std::atoi(std::getenv("CVK_STREAMK")) == 0) && !std::getenv("CVK_NO_STREAM")) {
+        const int rc = solve_streamk(c, A, M, o, b_dev, x_dev, rep);
+        if (rc != 1) return rc;
+    }
     if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n()) {
         const bool pinned = l2_pin(c, A);
         const int rc = solve_phased(c, solver, A, M, o, b_dev, x_dev, rep, pinned);

@@ -279,6 +279,54 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
     return v;
 }
 
+// K-wide double-double butterfly over a warp: every lane ends with the same
+// K sums (operands ordered by lane, so the pairs agree bit for bit).  The
+// step loop is kept rolled: this epilogue runs once per CTA from a cold
+// instruction cache, and the unrolled form (K x 5 steps x 4 shuffles + dd
+// adds, plus unrolled cross-warp chains) cost 5 us per reduction in the
+// last CTA's fold (tools/trace_phase.py).
+template <int K>
+__device__ __forceinline__ void warp_sum_k(CAcc (&v)[K]) {
+#pragma unroll 1
+    for (int o = 16; o > 0; o >>= 1) {
+        const bool up = (threadIdx.x & o) != 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            CAcc w;
+            w.hi.x = __shfl_xor_sync(0xffffffffu, v[k].hi.x, o);
+            w.hi.y = __shfl_xor_sync(0xffffffffu, v[k].hi.y, o);
+            w.lo.x = __shfl_xor_sync(0xffffffffu, v[k].lo.x, o);
+            w.lo.y = __shfl_xor_sync(0xffffffffu, v[k].lo.y, o);
+            CAcc a = up ? w : v[k];
+            const CAcc b = up ? v[k] : w;
+            cacc_add(a, b);
+            v[k] = a;
+        }
+    }
+}
+
+// CTA sum of K accumulators: warp butterflies, then warp 0 combines the
+// per-warp sums with a second butterfly.  Result valid in warp 0.
+template <int K, int NT>
+__device__ __forceinline__ void cta_sum_k(CAcc (&v)[K], CAcc (*sm)[32]) {
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    warp_sum_k<K>(v);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (lane < NW) v[k] = sm[k][lane];
+            else v[k] = CAcc{};
+        }
+        warp_sum_k<K>(v);
+    }
+}
+
 // FAST: CTA partial of K reductions -> part slots 2k (hi), 2k+1 (lo)
 template <int K, int NT = kThreads>
 __device__ __forceinline__ void cta_partial(const CAcc (&acc)[K], double2* part, int G, int cta) {

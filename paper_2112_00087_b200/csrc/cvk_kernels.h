@@ -25,6 +25,15 @@ const void* solver_kernel(int solver, int S, bool ref, bool batched = false);
 int solver_nwork(int solver, int l, int m);
 size_t solver_smem(int solver, int m);
 
+// persistent TMA-streamed BiCGSTAB (cvk_streamk.cu): cooperative, one CTA per
+// SM, kStreamThreads threads, dynamic smem = L.smem_bytes()
+struct StreamLayout;
+const void* streamk_bicgstab_kernel();
+size_t streamk_args_size();
+void streamk_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
+                       double2* part, unsigned long long* bar, DevReport* rep, double* hist, long long hist_cap,
+                       double tol, long long max_iter, int record, const StreamLayout& L);
+
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);

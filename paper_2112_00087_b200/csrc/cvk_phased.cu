@@ -77,54 +77,6 @@ __device__ __forceinline__ double2* partv(const PArgs& a, int k) {
     return a.part + (size_t)k * kPhSlots * gridDim.x;
 }
 
-// K-wide double-double butterfly over a warp: every lane ends with the same
-// K sums (operands ordered by lane, so the pairs agree bit for bit).  The
-// step loop is kept rolled: this epilogue runs once per CTA from a cold
-// instruction cache, and the unrolled form (K x 5 steps x 4 shuffles + dd
-// adds, plus unrolled cross-warp chains) cost 5 us per reduction in the
-// last CTA's fold (tools/trace_phase.py).
-template <int K>
-__device__ __forceinline__ void warp_sum_k(CAcc (&v)[K]) {
-#pragma unroll 1
-    for (int o = 16; o > 0; o >>= 1) {
-        const bool up = (threadIdx.x & o) != 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            CAcc w;
-            w.hi.x = __shfl_xor_sync(0xffffffffu, v[k].hi.x, o);
-            w.hi.y = __shfl_xor_sync(0xffffffffu, v[k].hi.y, o);
-            w.lo.x = __shfl_xor_sync(0xffffffffu, v[k].lo.x, o);
-            w.lo.y = __shfl_xor_sync(0xffffffffu, v[k].lo.y, o);
-            CAcc a = up ? w : v[k];
-            const CAcc b = up ? v[k] : w;
-            cacc_add(a, b);
-            v[k] = a;
-        }
-    }
-}
-
-// CTA sum of K accumulators: warp butterflies, then warp 0 combines the
-// per-warp sums with a second butterfly.  Result valid in warp 0.
-template <int K, int NT>
-__device__ __forceinline__ void cta_sum_k(CAcc (&v)[K], CAcc (*sm)[32]) {
-    constexpr int NW = NT / 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    warp_sum_k<K>(v);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) sm[k][warp] = v[k];
-    }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (lane < NW) v[k] = sm[k][lane];
-            else v[k] = CAcc{};
-        }
-        warp_sum_k<K>(v);
-    }
-}
-
 // Publish this CTA's K partials; returns true in the CTA that arrived last,
 // with the grid totals in tot (valid in thread 0 -- callers continue with
 // thread 0 only).
@@ -615,9 +567,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        // slot 0 of the chunk rows holds p_new (pre); band slots hold raw r, p, v
         auto xs = [&](int l) -> double2 {
             const double2 rc = ch.v(0, l);
-            if (first) return rc;
+            if (first || l < kStreamRows) return rc;
             return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
         };
         auto xg = [&](int c) -> double2 {
@@ -631,7 +584,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         pn[row] = xs(t);
         vn[row] = vi;
         acc_dot(acc[0], ch.v(3, t), vi);
-    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1));
+    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1), [&](int t, const Chunk& ch) {
+        if (!first)
+            ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
+    });
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
     if (threadIdx.x != 0) return;
@@ -666,7 +622,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     L.nband = a.nband;
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds s (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+        };
         auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
         const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
         const double2 ti = prec_staged(a, ch, 2, t, y);
@@ -678,7 +636,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
         acc_norm(acc[0], si);
         acc_dot(acc[1], ti, ti);
         acc_dot(acc[2], ti, si);
-    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2));
+    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
+    });
     double2 tot[3];
     if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
@@ -717,7 +677,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     L.nband = a.nband;
     CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l))); };
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds u - alpha v (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+        };
         auto xg = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
         const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
         const int row = ch.r0 + t;
@@ -732,7 +694,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
         V.d[row] = cvk_add(cvk_mul(coef, di), ui);
         acc_norm(acc[0], wi);
         acc_dot(acc[1], ch.v(6, t), wi);
-    }, a.dyn ? &st->chunk_ctr[2] : nullptr, SPROF(3));
+    }, a.dyn ? &st->chunk_ctr[2] : nullptr, SPROF(3), [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
+    });
     double2 tot[2];
     if (!partial_last<2, kStreamThreads>(acc, partv(a, 0), &st->counter[0], tot)) return;
     if (threadIdx.x != 0) return;
@@ -773,7 +737,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        auto xs = [&](int l) -> double2 { return cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l))); };
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds w + beta u (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l)));
+        };
         auto xg = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
         const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
         const int row = ch.r0 + t;
@@ -786,7 +752,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
         V.au[row] = an;
         a.x[row] = cvk_add(ch.v(5, t), cvk_mul(eta_o, ch.v(6, t)));
         acc_dot(acc[0], ch.v(7, t), vi);
-    }, a.dyn ? &st->chunk_ctr[3] : nullptr, SPROF(3));
+    }, a.dyn ? &st->chunk_ctr[3] : nullptr, SPROF(3), [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(beta, ch.v(1, t))));
+    });
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
     if (threadIdx.x != 0) return;

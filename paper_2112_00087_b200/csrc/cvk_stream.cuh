@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "cvk_engine.cuh"
 
 namespace cvk {
@@ -118,6 +120,7 @@ struct Chunk {
         return (j < ng ? j * gs : ng * gs + (j - ng)) * kStreamRows;
     }
     __device__ __forceinline__ double2 v(int j, int l) const { return vec[voff(j) + l]; }
+    __device__ __forceinline__ void set(int j, int l, double2 x) const { const_cast<double2*>(vec)[voff(j) + l] = x; }
     // slot of column c in a gathered vector's staged data, or -1 (global)
     __device__ __forceinline__ int stage_index(int c) const {
         const int l = c - r0;
@@ -222,10 +225,46 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
 // prof (measurement builds): [0] producer cycles waiting for free stages,
 // [1] consumer (thread 0) cycles waiting for full stages, [2] consumer cycles
 // in the row body, [3] chunks consumed by thread 0's group
-template <class Body>
+struct NoPre {
+    __device__ __forceinline__ void operator()(int, const Chunk&) const {}
+};
+
+// pre(t, chunk), when given, runs for every row of the chunk before any
+// body() of that chunk (the consumer group syncs on a named barrier in
+// between): a phase computes each row's gathered combination once -- e.g.
+// p = r + beta (p - omega v) -- into the staged slot of vector 0, so the
+// in-chunk gathers read one value instead of recomputing it per entry.
+// Persistent use (one ring across many phases of one kernel): call
+// stream_init once, then stream_rows with init = false and base = the ring
+// position where this phase starts (phases so far x chunks per CTA); static
+// chunk assignment only.
+__device__ __forceinline__ void stream_init(unsigned char* smem, const StreamLayout& L) {
+    uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
+    uint64_t* empty = full + kStreamMaxStages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < L.stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kStreamRows);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// chunks per CTA under the static split
+__device__ __forceinline__ int stream_chunks_per_cta(int n, const StreamLayout& L) {
+    const int nchunks = (n + kStreamRows - 1) / kStreamRows, G = gridDim.x;
+    const int cpc = (nchunks + G - 1) / G;
+    if (L.contig) return max(0, min(nchunks, (int)blockIdx.x * cpc + cpc) - (int)blockIdx.x * cpc);
+    return (int)blockIdx.x < nchunks ? (nchunks - 1 - (int)blockIdx.x) / G + 1 : 0;
+}
+
+template <class Body, class Pre = NoPre>
 __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L, const double2* const* vecs,
                                             unsigned char* smem, Body&& body, unsigned* dyn = nullptr,
-                                            unsigned long long* prof = nullptr) {
+                                            unsigned long long* prof = nullptr, Pre&& pre = Pre(), int base = 0,
+                                            bool init = true) {
+    constexpr bool kPre = !std::is_same<typename std::decay<Pre>::type, NoPre>::value;
     unsigned long long pw = 0, cw = 0, cb = 0, cn = 0;
     uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
     uint64_t* empty = full + kStreamMaxStages;
@@ -235,14 +274,7 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     const int G = gridDim.x;
     const int tid = threadIdx.x;
     const int ST = L.stages;
-    if (tid == 0) {
-        for (int s = 0; s < ST; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, kStreamRows);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
+    if (init) stream_init(smem, L);
     // static split: this CTA's chunks first + i * step, i < cnt
     const int cpc = (nchunks + G - 1) / G;
     const int first = L.contig ? blockIdx.x * cpc : blockIdx.x;
@@ -251,7 +283,7 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     const int step = L.contig ? 1 : G;
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
-        int it = 0;
+        int it = base;
         const bool banded = L.nband != 0 && A.bands != nullptr;
         auto put = [&](int chunk, int k0, int k1, int cm, int4 band) {  // lane 0
             const int s = it % ST;
@@ -325,7 +357,8 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
         }
     } else {
         const int g = tid / kStreamRows, t = tid % kStreamRows;
-        for (int it = g; dyn || it < cnt; it += kStreamGroups) {
+        for (int i = g; dyn || i < cnt; i += kStreamGroups) {
+            const int it = base + i;
             const int s = it % ST;
             const long long t0 = prof ? clock64() : 0;
             mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
@@ -348,6 +381,10 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             ch.rows = min(kStreamRows, n - ch.r0);
             ch.k0 = ch.rp[0];
             ch.cio = ch.k0 & 3;
+            if (kPre) {
+                if (t < ch.rows) pre(t, ch);
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kStreamRows) : "memory");
+            }
             if (t < ch.rows) body(t, ch);
             mbar_arrive(empty + s);
             if (prof) {
