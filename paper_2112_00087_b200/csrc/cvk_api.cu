@@ -130,6 +130,7 @@ int cvk_abi_version(void) { return CVK_ABI_VERSION; }
 
 // measurement builds only (CVK_TRACE): not part of include/cavac_b200.h
 int cvk_trace_read(void* out, size_t bytes) { return cvk::phased_trace_read(out, bytes); }
+int cvk_streamk_trace_read(unsigned long long* out16) { return cvk::streamk_trace_read(out16); }
 const char* cvk_last_error(void) { return g_err.c_str(); }
 
 const char* cvk_breakdown_name(int code) {
@@ -769,8 +770,13 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     const int mode = resolve_mode(c, o->mode);
     const bool ref = mode == CVK_MODE_REF;
     CK(cudaSetDevice(c->device));
+    // persistent streamed BiCGSTAB: opt-in (CVK_STREAMK=1).  Measured 218-293 vs
+    // 134-143 us per iteration for the phase kernels at 1M DOF: with ~200 KB
+    // of shared memory resident for the whole solve the L1 left for global
+    // loads is too small for the element phase's memory-level parallelism
+    // (40 vs 14 us), and the merged phases spill (tools/trace_streamk.py).
     if (!ref && solver == CVK_BICGSTAB && (long long)n >= phased_min_n() &&
-        !(std::getenv("CVK_STREAMK") && std::atoi(std::getenv("CVK_STREAMK")) == 0) && !std::getenv("CVK_NO_STREAM")) {
+        std::getenv("CVK_STREAMK") && std::atoi(std::getenv("CVK_STREAMK")) == 1 && !std::getenv("CVK_NO_STREAM")) {
         const int rc = solve_streamk(c, A, M, o, b_dev, x_dev, rep);
         if (rc != 1) return rc;
     }

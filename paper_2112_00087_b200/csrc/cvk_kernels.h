@@ -29,6 +29,7 @@ size_t solver_smem(int solver, int m);
 // SM, kStreamThreads threads, dynamic smem = L.smem_bytes()
 struct StreamLayout;
 const void* streamk_bicgstab_kernel();
+int streamk_trace_read(unsigned long long* out16);  // CVK_TRACE builds
 size_t streamk_args_size();
 void streamk_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
                        double2* part, unsigned long long* bar, DevReport* rep, double* hist, long long hist_cap,

@@ -29,6 +29,21 @@ namespace {
 
 constexpr int NT = kStreamThreads;
 
+#ifdef CVK_TRACE
+// CTA 0 / CTA 1 timestamps of the last iteration's phase boundaries (globaltimer ns)
+__device__ unsigned long long g_sk_trace[2][8];
+#define SKT(slot)                                                                   \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < 2) {                                   \
+            unsigned long long t_;                                                  \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+            g_sk_trace[blockIdx.x][slot] = t_;                                      \
+        }                                                                           \
+    } while (0)
+#else
+#define SKT(slot) do { } while (0)
+#endif
+
 struct SKArgs {
     Csr A;
     const double2* dinv;  // nullptr: identity
@@ -113,6 +128,109 @@ __device__ __forceinline__ void hist(const SKArgs& a, SState& S, double v) {
     ++S.hl;
 }
 
+// Each phase is its own (non-inlined) function so that its register
+// allocation does not have to coexist with the other phases' live ranges:
+// inlined into one kernel, the three bodies spilled ~1 KB per thread and the
+// phases ran 1.5-3x slower than as separate kernels.
+struct Acc2 { CAcc v[2]; };
+struct Acc3 { CAcc v[3]; };
+
+__device__ __noinline__ CAcc phase_a(Csr A, const double2* dinv, StreamLayout L, unsigned char* smem, int base,
+                                     int first, double2 beta, double2 nom, const double2* r, const double2* pc,
+                                     const double2* vc, double2* pn, double2* vn, const double2* sh) {
+    const double2* vecs[5] = {r, pc, vc, sh, dinv};
+    CAcc acc = {};
+    stream_rows(
+        A, L, vecs, smem,
+        [&](int t, const Chunk& ch) {
+            auto xs = [&](int l) -> double2 {
+                const double2 rc = ch.v(0, l);
+                if (first || l < kStreamRows) return rc;
+                return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
+            };
+            auto xg = [&](int c) -> double2 {
+                const double2 rc = r[c];
+                if (first) return rc;
+                return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+            };
+            const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
+            const double2 vi = dinv ? cvk_mul(ch.v(4, t), y) : y;
+            const int row = ch.r0 + t;
+            pn[row] = xs(t);
+            vn[row] = vi;
+            acc_dot(acc, ch.v(3, t), vi);
+        },
+        nullptr, nullptr,
+        [&](int t, const Chunk& ch) {
+            if (!first)
+                ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
+        },
+        base, false);
+    return acc;
+}
+
+__device__ __noinline__ Acc3 phase_b(Csr A, const double2* dinv, StreamLayout L, unsigned char* smem, int base,
+                                     double2 alpha, const double2* r, const double2* vn, const double2* pn,
+                                     double2* x, double2* sv, double2* tv) {
+    const double2 nal = cvk_neg(alpha);
+    const double2* vecs[5] = {r, vn, dinv, pn, x};
+    Acc3 acc = {};
+    stream_rows(
+        A, L, vecs, smem,
+        [&](int t, const Chunk& ch) {
+            auto xs = [&](int l) -> double2 {
+                return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+            };
+            auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+            const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
+            const double2 ti = dinv ? cvk_mul(ch.v(2, t), y) : y;
+            const double2 si = xs(t);
+            const int row = ch.r0 + t;
+            sv[row] = si;
+            tv[row] = ti;
+            x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
+            acc_norm(acc.v[0], si);
+            acc_dot(acc.v[1], ti, ti);
+            acc_dot(acc.v[2], ti, si);
+        },
+        nullptr, nullptr,
+        [&](int t, const Chunk& ch) { ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t)))); },
+        base, false);
+    return acc;
+}
+
+__device__ __noinline__ Acc2 phase_c(int n, double2 omega, const double2* sv, const double2* tv, const double2* sh,
+                                     double2* x, double2* r) {
+    const double2 nomg = cvk_neg(omega);
+    Acc2 acc = {};
+    struct L4 { double2 s, t, sh, x; };
+    elems<4>(n, [&](int i) { return L4{sv[i], tv[i], sh[i], x[i]}; },
+             [&](int i, const L4& v) {
+                 x[i] = cvk_add(v.x, cvk_mul(omega, v.s));
+                 const double2 ri = cvk_add(v.s, cvk_mul(nomg, v.t));
+                 r[i] = ri;
+                 acc_norm(acc.v[0], ri);
+                 acc_dot(acc.v[1], v.sh, ri);
+             });
+    return acc;
+}
+
+__device__ __noinline__ Acc2 phase_true(Csr A, StreamLayout L, unsigned char* smem, int base, const double2* x,
+                                        const double2* b) {
+    const double2* vecs[5] = {x, b, nullptr, nullptr, nullptr};  // L.nvec = 5: unused slots skipped
+    Acc2 acc = {};
+    stream_rows(
+        A, L, vecs, smem,
+        [&](int t, const Chunk& ch) {
+            const double2 y = chunk_row_sum<5>(ch, t, [&](int l) { return ch.v(0, l); }, [&](int c) { return x[c]; });
+            const double2 bi = ch.v(1, t);
+            acc_norm(acc.v[0], bi);
+            acc_norm(acc.v[1], cvk_sub(bi, y));
+        },
+        nullptr, nullptr, NoPre(), base, false);
+    return acc;
+}
+
 __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ CAcc sm[3][32];
@@ -124,15 +242,16 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
     double2* sh = a.work + nn;
     double2* sv = a.work + 2 * nn;
     double2* tv = a.work + 3 * nn;
-    double2* P[2] = {a.work + 4 * nn, a.work + 5 * nn};
-    double2* V[2] = {a.work + 6 * nn, a.work + 7 * nn};
+    // p[c] = work + (4 + c) n, v[c] = work + (6 + c) n (no runtime-indexed local arrays: they live on the stack)
     const double2* dinv = a.dinv;
     double2* x = a.x;
     GridBar g(a.bar, gridDim.x);
-    double2* part[kRegions];
-    for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * gridDim.x;
     int region = 0;
-    auto next_part = [&]() { double2* p = part[region]; region = (region + 1) % kRegions; return p; };
+    auto next_part = [&]() {
+        double2* p = a.part + (size_t)region * kMaxSlots * gridDim.x;
+        region = region + 1 == kRegions ? 0 : region + 1;
+        return p;
+    };
     const StreamLayout L = a.L;
     stream_init(smem, L);
     const int cnt = stream_chunks_per_cta(n, L);
@@ -187,44 +306,20 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
         const int cur = S.cur;
         const bool first = S.first != 0;
         const double2 beta = S.beta, nom = cvk_neg(S.omega);
-        const double2* __restrict__ pc = P[cur];
-        const double2* __restrict__ vc = V[cur];
-        double2* __restrict__ pn = P[cur ^ 1];
-        double2* __restrict__ vn = V[cur ^ 1];
+        const double2* __restrict__ pc = a.work + (size_t)(4 + cur) * nn;
+        const double2* __restrict__ vc = a.work + (size_t)(6 + cur) * nn;
+        double2* __restrict__ pn = a.work + (size_t)(5 - cur) * nn;
+        double2* __restrict__ vn = a.work + (size_t)(7 - cur) * nn;
 
         // ---- A: p_new on the fly, v = M^-1 A p, <shadow, v>
+        SKT(0);
         {
-            const double2* vecs[5] = {r, pc, vc, sh, dinv};
-            CAcc acc[1] = {};
-            stream_rows(
-                a.A, L, vecs, smem,
-                [&](int t, const Chunk& ch) {
-                    auto xs = [&](int l) -> double2 {
-                        const double2 rc = ch.v(0, l);
-                        if (first || l < kStreamRows) return rc;
-                        return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
-                    };
-                    auto xg = [&](int c) -> double2 {
-                        const double2 rc = r[c];
-                        if (first) return rc;
-                        return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
-                    };
-                    const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
-                    const double2 vi = dinv ? cvk_mul(ch.v(4, t), y) : y;
-                    const int row = ch.r0 + t;
-                    pn[row] = xs(t);
-                    vn[row] = vi;
-                    acc_dot(acc[0], ch.v(3, t), vi);
-                },
-                nullptr, nullptr,
-                [&](int t, const Chunk& ch) {
-                    if (!first)
-                        ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
-                },
-                base, false);
+            CAcc acc[1] = {phase_a(a.A, dinv, L, smem, base, first ? 1 : 0, beta, nom, r, pc, vc, pn, vn, sh)};
             base += cnt;
+            SKT(1);
             double2 tot[1];
             if (!(ok = grid_reduce<1>(acc, tot, next_part(), g, sm, res))) break;
+            SKT(2);
             if (threadIdx.x == 0) {
                 if (cvk_abs(tot[0]) < S.brk) {
                     S.done = 1; S.brk_code = 2; S.iters = S.it - 1;
@@ -237,33 +332,13 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
         }
         // ---- B: s = r - alpha v on the fly, t = M^-1 A s, x += alpha p
         {
-            const double2 alpha = S.alpha, nal = cvk_neg(S.alpha);
-            const double2* vecs[5] = {r, vn, dinv, pn, x};
-            CAcc acc[3] = {};
-            stream_rows(
-                a.A, L, vecs, smem,
-                [&](int t, const Chunk& ch) {
-                    auto xs = [&](int l) -> double2 {
-                        return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
-                    };
-                    auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
-                    const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
-                    const double2 ti = dinv ? cvk_mul(ch.v(2, t), y) : y;
-                    const double2 si = xs(t);
-                    const int row = ch.r0 + t;
-                    sv[row] = si;
-                    tv[row] = ti;
-                    x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
-                    acc_norm(acc[0], si);
-                    acc_dot(acc[1], ti, ti);
-                    acc_dot(acc[2], ti, si);
-                },
-                nullptr, nullptr,
-                [&](int t, const Chunk& ch) { ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t)))); },
-                base, false);
+            const Acc3 b3 = phase_b(a.A, dinv, L, smem, base, S.alpha, r, vn, pn, x, sv, tv);
+            CAcc acc[3] = {b3.v[0], b3.v[1], b3.v[2]};
             base += cnt;
+            SKT(3);
             double2 tot[3];
             if (!(ok = grid_reduce<3>(acc, tot, next_part(), g, sm, res))) break;
+            SKT(4);
             if (threadIdx.x == 0) {
                 const double relres = sqrt(tot[0].x) / S.bnorm;
                 if (relres <= a.tol) {  // krylov.cpp:107-114 half-step exit
@@ -280,19 +355,12 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
         }
         // ---- C: x += omega s, r = s - omega t, ||r||, <shadow, r>
         {
-            const double2 omega = S.omega, nomg = cvk_neg(S.omega);
-            CAcc acc[2] = {};
-            struct L4 { double2 s, t, sh, x; };
-            elems<4>(n, [&](int i) { return L4{sv[i], tv[i], sh[i], x[i]}; },
-                     [&](int i, const L4& v) {
-                         x[i] = cvk_add(v.x, cvk_mul(omega, v.s));
-                         const double2 ri = cvk_add(v.s, cvk_mul(nomg, v.t));
-                         r[i] = ri;
-                         acc_norm(acc[0], ri);
-                         acc_dot(acc[1], v.sh, ri);
-                     });
+            const Acc2 c2 = phase_c(n, S.omega, sv, tv, sh, x, r);
+            CAcc acc[2] = {c2.v[0], c2.v[1]};
+            SKT(5);
             double2 tot[2];
             if (!(ok = grid_reduce<2>(acc, tot, next_part(), g, sm, res))) break;
+            SKT(6);
             if (threadIdx.x == 0) {
                 const double relres = sqrt(tot[0].x) / S.bnorm;
                 S.final_relres = relres;
@@ -314,18 +382,8 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
     // ---- true residual ||b - A x|| / ||b|| (krylov.cpp:17-23), skipped for b = 0
     double trr = 0.0;
     if (ok && !zero_rhs) {
-        const double2* vecs[2] = {x, a.b};
-        CAcc acc[2] = {};
-        stream_rows(
-            a.A, L, vecs, smem,
-            [&](int t, const Chunk& ch) {
-                const double2 y = chunk_row_sum<5>(ch, t, [&](int l) { return ch.v(0, l); },
-                                                   [&](int c) { return x[c]; });
-                const double2 bi = ch.v(1, t);
-                acc_norm(acc[0], bi);
-                acc_norm(acc[1], cvk_sub(bi, y));
-            },
-            nullptr, nullptr, NoPre(), base, false);
+        const Acc2 t2 = phase_true(a.A, L, smem, base, x, a.b);
+        CAcc acc[2] = {t2.v[0], t2.v[1]};
         base += cnt;
         double2 tot[2];
         ok = grid_reduce<2>(acc, tot, next_part(), g, sm, res);
@@ -348,6 +406,15 @@ __global__ void __launch_bounds__(NT, 1) k_bicgstab_stream(SKArgs a) {
 }  // namespace
 
 const void* streamk_bicgstab_kernel() { return (const void*)k_bicgstab_stream; }
+
+int streamk_trace_read(unsigned long long* out16) {
+#ifdef CVK_TRACE
+    return cudaMemcpyFromSymbol(out16, g_sk_trace, sizeof(g_sk_trace)) == cudaSuccess ? 16 : -1;
+#else
+    (void)out16;
+    return 0;
+#endif
+}
 
 size_t streamk_args_size() { return sizeof(SKArgs); }
 
