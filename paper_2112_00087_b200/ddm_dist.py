@@ -253,3 +253,24 @@ def schwarz_solve_distributed(problem: HelmholtzProblem, part: Partition, tp: Tr
     for c0, blk in blocks:
         x[:, c0:c0 + blk.shape[1]] = blk
     return DdmResult(x.ravel(), rep)
+
+
+def tune_parameters_distributed(problem: HelmholtzProblem, part: Partition, candidates, inner: SolverOptions,
+                                budget: int, mode: Optional[ExecMode] = None, group=None, entry_fn=None):
+    """tune_parameters (schwarz.cpp:240-280) with the candidates spread over the
+    ranks of a torch.distributed group (candidate i on rank i % world, each a
+    complete single-device schwarz_solve -- the sweep is embarrassingly
+    parallel).  The table is gathered back into
+    candidate order, so the minimiser, the tie-break and the all-diverged
+    error are the reference's on every rank."""
+    from .schwarz import InvalidArgument, select_best, tune_entry
+    if not candidates:
+        raise InvalidArgument("tune_parameters: empty candidate grid")
+    comm = _Comm(group)
+    fn = entry_fn or tune_entry
+    mine = {i: fn(problem, part, tp, inner, budget, mode) for i, tp in enumerate(candidates)
+            if i % comm.world == comm.rank}
+    table = {}
+    for part_table in comm.allgather_obj(mine):
+        table.update(part_table)
+    return select_best([table[i] for i in range(len(candidates))])

@@ -144,28 +144,38 @@ class TuneResult:
     table: List[TuneEntry]
 
 
-def tune_parameters(problem: HelmholtzProblem, part: Partition, candidates: List[TransmissionParams],
-                    inner: SolverOptions, budget: int, mode: Optional[ExecMode] = None) -> TuneResult:
-    """schwarz.cpp:240-280: minimiser by outer iterations, ties by total inner
-    iterations of the last sweep; RuntimeError when every candidate diverges."""
-    if not candidates:
-        raise InvalidArgument("tune_parameters: empty candidate grid")
-    table, best, key = [], None, None
-    for tp in candidates:
-        r = schwarz_solve(problem, part, tp, inner, 1e-6, budget, mode=mode)
-        e = TuneEntry(tp, r.report.outer_iterations, r.report.total_inner_iterations, r.report.converged)
-        table.append(e)
+def tune_entry(problem: HelmholtzProblem, part: Partition, tp: TransmissionParams, inner: SolverOptions,
+               budget: int, mode: Optional[ExecMode] = None) -> TuneEntry:
+    """One candidate of tune_parameters: schwarz_solve at ddm_tol 1e-6 within the budget."""
+    r = schwarz_solve(problem, part, tp, inner, 1e-6, budget, mode=mode)
+    return TuneEntry(tp, r.report.outer_iterations, r.report.total_inner_iterations, r.report.converged)
+
+
+def select_best(table: List[TuneEntry]) -> TuneResult:
+    """schwarz.cpp:258-279 over a complete table in candidate order."""
+    best, key = None, None
+    for e in table:
         if not e.converged:
             continue
         k = (e.outer_iterations, e.total_inner_iterations)
         if key is None or k < key:
-            key, best = k, tp
+            key, best = k, e.params
     if best is None:
         msg = "tune_parameters: all candidates diverged;" + "".join(
             f" ({e.params.s_left.real:f}+{e.params.s_left.imag:f}i / {e.params.s_right.real:f}+"
             f"{e.params.s_right.imag:f}i: {e.outer_iterations})" for e in table)
         raise RuntimeError(msg)
     return TuneResult(best, table)
+
+
+def tune_parameters(problem: HelmholtzProblem, part: Partition, candidates: List[TransmissionParams],
+                    inner: SolverOptions, budget: int, mode: Optional[ExecMode] = None) -> TuneResult:
+    """schwarz.cpp:240-280: minimiser by outer iterations, ties by total inner
+    iterations of the last sweep; RuntimeError when every candidate diverges.
+    (ddm_dist.tune_parameters_distributed spreads the candidates over GPUs.)"""
+    if not candidates:
+        raise InvalidArgument("tune_parameters: empty candidate grid")
+    return select_best([tune_entry(problem, part, tp, inner, budget, mode) for tp in candidates])
 
 
 def default_candidate_grid(k: float) -> List[TransmissionParams]:

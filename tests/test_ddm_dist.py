@@ -111,3 +111,63 @@ def test_strip_ranges():
     assert strip_ranges(7, 3) == [(0, 3), (3, 5), (5, 7)]
     with pytest.raises(ValueError):
         strip_ranges(2, 3)
+
+
+def _tune_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2112_00087_b200 import SolverOptions
+        from paper_2112_00087_b200.ddm_dist import tune_parameters_distributed
+        from paper_2112_00087_b200.schwarz import default_candidate_grid
+        O, g, prob, Partition = _case()
+        cb = [int(v) for v in O.partition(g.nx, 3)]
+        part = Partition(3, cb, cb[1:-1])
+        cands = default_candidate_grid(prob.omega / prob.c)[:12]
+        r = tune_parameters_distributed(prob, part, cands, SolverOptions(tol=1e-10), 150,
+                                        entry_fn=_oracle_entry)
+        q.put((rank, r.best, [(e.outer_iterations, e.total_inner_iterations, e.converged) for e in r.table]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _oracle_entry(problem, part, tp, inner, budget, mode=None):
+    """tune_entry with the oracle's schwarz_solve (test infrastructure)."""
+    from oracle import oracle as O
+    from paper_2112_00087_b200.schwarz import TuneEntry
+    g = problem.grid
+    og = O.build_grid(2.4, 1.2, g.h, 0.4, 0.65, g.wall_admittance)
+    A = problem.A
+    x, rep = O.schwarz_solve(og, problem.c, A.row_offsets, A.col_indices, A.values, problem.b, part.n_sub,
+                             tp.s_left, tp.s_right, tol=inner.tol, ddm_tol=1e-6, max_outer=budget)
+    return TuneEntry(tp, rep["outer_iterations"], sum(rep["sub_iterations"]), rep["converged"])
+
+
+def test_distributed_tuning_matches_serial():
+    """Candidates spread over 3 gloo ranks: the gathered table and the
+    minimiser equal the serial tune loop (schwarz.cpp:240-280)."""
+    import multiprocessing as mp
+    from paper_2112_00087_b200 import SolverOptions
+    from paper_2112_00087_b200.schwarz import default_candidate_grid, select_best
+    O, g, prob, Partition = _case()
+    O.build()
+    cb = [int(v) for v in O.partition(g.nx, 3)]
+    part = Partition(3, cb, cb[1:-1])
+    cands = default_candidate_grid(prob.omega / prob.c)[:12]
+    serial = select_best([_oracle_entry(prob, part, tp, SolverOptions(tol=1e-10), 150) for tp in cands])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tune_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [(e.outer_iterations, e.total_inner_iterations, e.converged) for e in serial.table]
+    for rank, best, table in outs:
+        assert table == want
+        assert best == serial.best
