@@ -264,6 +264,15 @@ int cvk_csr_assemble_cavity(cvk_csr *A, const cvk_grid *grid, double omega, doub
  * krylov.cpp:31-55; CVK_EZERODIAG names the row as the reference does) */
 int cvk_precond_jacobi_refresh(cvk_prec *M, const cvk_csr *A);
 
+/* FEM operator (beyond the reference's FD cavity; synthetic P1 cavity in
+ * paper_2112_00087_b200/fem3d.py): real K, M, C on A's pattern, resident on
+ * A's device; cvk_fem_set_omega writes A = K - omega^2 M + i omega C
+ * (re = K - (omega*omega) M, im = omega C). */
+typedef struct cvk_fem cvk_fem;
+int cvk_fem_create(cvk_csr *A, const double *K, const double *M, const double *C, cvk_fem **out);
+int cvk_fem_set_omega(cvk_fem *op, double omega);
+int cvk_fem_free(cvk_fem *op);
+
 /* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
  * device buffers, returns the average kernel time in seconds ---- */
 int cvk_spmv_bench(const cvk_csr *A, const double *x_dev, double *y_dev, int mode,

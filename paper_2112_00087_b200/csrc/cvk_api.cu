@@ -428,6 +428,47 @@ int cvk_csr_assemble_cavity(cvk_csr* A, const cvk_grid* g, double omega, double 
     return CVK_OK;
 }
 
+struct cvk_fem {
+    cvk_csr* A = nullptr;
+    double* kmc = nullptr;  // K | M | C, nnz each
+};
+
+int cvk_fem_create(cvk_csr* A, const double* K, const double* M, const double* Cd, cvk_fem** out) {
+    if (!A || !K || !M || !Cd || !out) return fail(CVK_EINVAL, "cvk_fem_create: null argument");
+    CK(cudaSetDevice(A->ctx->device));
+    cvk_fem* F = new cvk_fem();
+    F->A = A;
+    const size_t nz = (size_t)std::max<int64_t>(1, A->nnz);
+    if (cudaMalloc(&F->kmc, 3 * sizeof(double) * nz) != cudaSuccess) {
+        delete F;
+        return fail(CVK_ENOMEM, "cvk_fem_create: device allocation failed");
+    }
+    CK(cudaMemcpyAsync(F->kmc, K, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, A->ctx->stream));
+    CK(cudaMemcpyAsync(F->kmc + nz, M, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, A->ctx->stream));
+    CK(cudaMemcpyAsync(F->kmc + 2 * nz, Cd, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, A->ctx->stream));
+    CK(cudaStreamSynchronize(A->ctx->stream));
+    *out = F;
+    return CVK_OK;
+}
+
+int cvk_fem_set_omega(cvk_fem* F, double omega) {
+    if (!F) return fail(CVK_EINVAL, "cvk_fem_set_omega: null argument");
+    cvk_csr* A = F->A;
+    CK(cudaSetDevice(A->ctx->device));
+    const size_t nz = (size_t)std::max<int64_t>(1, A->nnz);
+    CK(cvk::launch_fem_values(A->nnz, F->kmc, F->kmc + nz, F->kmc + 2 * nz, omega, A->av, A->ctx->nsm, A->ctx->stream));
+    CK(cudaStreamSynchronize(A->ctx->stream));
+    return CVK_OK;
+}
+
+int cvk_fem_free(cvk_fem* F) {
+    if (!F) return CVK_OK;
+    cudaSetDevice(F->A->ctx->device);
+    cudaFree(F->kmc);
+    delete F;
+    return CVK_OK;
+}
+
 int cvk_precond_identity(cvk_ctx* c, int64_t n, cvk_prec** out) {
     if (!c || !out || n < 0) return fail(CVK_EINVAL, "cvk_precond_identity: bad argument");
     cvk_prec* M = new cvk_prec();

@@ -60,7 +60,23 @@ __global__ void __launch_bounds__(kThreads) k_cavity_values(int nx, int ny, int 
     }
 }
 
+// FEM operator A(omega) = K - omega^2 M + i omega C on a fixed pattern
+// (paper_2112_00087_b200/fem3d.py): re = K - (omega omega) M, im = omega C
+__global__ void __launch_bounds__(kThreads) k_fem_values(long long nnz, const double* __restrict__ K,
+                                                         const double* __restrict__ M, const double* __restrict__ Cd,
+                                                         double om2, double omega, double2* __restrict__ av) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
+        av[k] = make_double2(K[k] - om2 * M[k], omega * Cd[k]);
+}
+
 }  // namespace
+
+cudaError_t launch_fem_values(long long nnz, const double* K, const double* M, const double* Cd, double omega,
+                              double2* av, int nsm, cudaStream_t st) {
+    const long long blocks = std::min<long long>((nnz + kThreads - 1) / kThreads, 8LL * nsm);
+    k_fem_values<<<(unsigned)std::max<long long>(1, blocks), kThreads, 0, st>>>(nnz, K, M, Cd, omega * omega, omega, av);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_cavity_values(int nx, int ny, int roof_begin, int roof_end, double k2, double om2,
                                  double kw_re, double kw_im, const int* rp, const int* ci, double2* av,

@@ -46,6 +46,9 @@ cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double
 cudaError_t launch_cavity_values(int nx, int ny, int roof_begin, int roof_end, double k2, double om2,
                                  double kw_re, double kw_im, const int* rp, const int* ci, double2* av,
                                  int* bad, int nsm, cudaStream_t st);
+// FEM operator values K - omega^2 M + i omega C (cvk_assemble.cu)
+cudaError_t launch_fem_values(long long nnz, const double* K, const double* M, const double* Cd, double omega,
+                              double2* av, int nsm, cudaStream_t st);
 cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
                             int* bad_row, cudaStream_t st);
 // out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 1024 double2
