@@ -347,10 +347,19 @@ __device__ __forceinline__ void cta_partial(const CAcc (&acc)[K], double2* part,
     }
 }
 
-// FAST: fold the G partials of reduction k (one warp; all lanes get the sum)
+// FAST: fold the G partials of reduction k (one warp; all lanes get the sum).
+// Loads are issued 4 at a time before their adds: a load-add chain over
+// G/32 partials serialises G/32 L2 round trips (~4 us per reduction at
+// G = 444; the persistent solvers at 50k DOF spent most of an iteration here).
 __device__ __forceinline__ double2 fold_one(const double2* part, int k, int G, int lane) {
     CAcc s = {};
-    for (int b = lane; b < G; b += 32) cacc_add(s, cacc_load(part, k, G, b));
+    for (int b0 = lane; b0 < G; b0 += 128) {
+        CAcc v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = b0 + 32 * u < G ? cacc_load(part, k, G, b0 + 32 * u) : CAcc{};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cacc_add(s, v[u]);
+    }
     s = warp_sum(s);
     return s.hi;
 }
@@ -359,13 +368,10 @@ __device__ __forceinline__ double2 fold_one(const double2* part, int k, int G, i
 template <int K>
 __device__ __forceinline__ void fold_partials(double2 (&out)[K], const double2* part, int G) {
     __shared__ double2 res[K];
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const double2 s = fold_one(part, k, G, lane);
-            if (lane == 0) res[k] = s;
-        }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = warp; k < K; k += (int)(blockDim.x >> 5)) {  // one warp per reduction
+        const double2 s = fold_one(part, k, G, lane);
+        if (lane == 0) res[k] = s;
     }
     __syncthreads();
 #pragma unroll

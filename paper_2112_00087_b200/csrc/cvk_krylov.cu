@@ -718,11 +718,9 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
         }
     };
     auto fold_multi = [&](const double2* pr, int cnt, double2* out) {
-        if (threadIdx.x < 32) {
-            for (int k = 0; k < cnt; ++k) {
-                const double2 s = fold_one(pr, k, G, lane);
-                if (lane == 0) out[k] = s;
-            }
+        for (int k = warp; k < cnt; k += kWarps) {  // one warp per dot product
+            const double2 s = fold_one(pr, k, G, lane);
+            if (lane == 0) out[k] = s;
         }
         __syncthreads();
     };
