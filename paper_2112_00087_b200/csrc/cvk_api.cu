@@ -589,8 +589,9 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    // per kernel: staged vectors, gathered vectors (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s)
-    const int kvec[4] = {5, 5, 7, 8}, kgat[4] = {3, 2, 2, 2};
+    // per kernel: staged vectors, gathered vectors
+    // (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_bm_a_s, k_bm_b_s)
+    const int kvec[6] = {5, 5, 7, 8, 7, 6}, kgat[6] = {3, 2, 2, 2, 4, 2};
     // halo-band staging: measured no faster on the 1M cavity (consumer latency is
     // not dominated by the out-of-chunk gathers), so opt-in (CVK_BANDS=1)
     const int nband = (A->bands && std::getenv("CVK_BANDS") && std::atoi(std::getenv("CVK_BANDS"))) ? 1 : 0;
@@ -600,19 +601,25 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         L.nband = nband;
         return L;
     };
-    int stg[4];
-    for (int k = 0; k < 4; ++k) {
-        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+    int stg[6];
+    for (int k = 0; k < 6; ++k) {
+        const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
         long long cap = nband ? 3 : 4;  // measured best ring depths
         if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
         stg[k] = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)layout_for(k, 1).stage_bytes()));
     }
     const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&
                           (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2 : std::min(stg[2], stg[3]) >= 2);
+    // BiCGSTAB in two streamed kernels per iteration (k_bm_*): opt-in
+    // (CVK_BICG_MERGED=1).  Measured 152 vs 142 us per iteration at 1M DOF:
+    // one launch fewer and 16 n fewer bytes, but the merged SpMV phase (7
+    // staged, 4 gathered vectors) is consumer-bound.
+    const bool merged = streamed && solver == CVK_BICGSTAB && std::min(stg[4], stg[5]) >= 2 &&
+                        std::getenv("CVK_BICG_MERGED") && std::atoi(std::getenv("CVK_BICG_MERGED")) == 1;
     auto smem_for = [&](int k) { return layout_for(k, stg[k]).smem_bytes(); };
-    const void* sk[4] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s};
+    const void* sk[6] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.bm_a_s, K.bm_b_s};
     if (streamed)
-        for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096));
+        for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // elementwise phases: grid-stride, 4 elements per thread per trip
     long long Ge = std::min<long long>(2LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
     if (const char* env = std::getenv("CVK_ELEM_CTAS")) Ge = std::max(1, std::atoi(env));
@@ -639,6 +646,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
     key.push_back((unsigned char)(streamed ? 1 : 0));
+    key.push_back((unsigned char)(merged ? 1 : 0));
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
@@ -647,7 +655,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const dim3 sgrid((unsigned)c->nsm), sblock(cvk::kStreamThreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
-            if (solver == CVK_BICGSTAB) {
+            if (merged) {
+                launch_pdl(K.bm_a_s, sgrid, sblock, args, smem_for(4), c->stream);
+                launch_pdl(K.bm_b_s, sgrid, sblock, args, smem_for(5), c->stream);
+            } else if (solver == CVK_BICGSTAB) {
                 if (streamed) {
                     launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(0), c->stream);
                     launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(1), c->stream);
@@ -677,7 +688,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     CK(cudaEventRecord(c->e0, c->stream));
     long long launches = 0;
     if (solver == CVK_BICGSTAB) {
-        CK(launch_pdl(K.bi_init, grid, block, args, 0, c->stream));
+        CK(launch_pdl(merged ? K.bm_init : K.bi_init, grid, block, args, 0, c->stream));
         launches += 1;
     } else {
         CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
@@ -693,7 +704,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaMemcpyAsync(&c->h_done[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += 3 * kIterPerGraph;
+        launches += (merged ? 2 : 3) * kIterPerGraph;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));
@@ -738,7 +749,7 @@ static int solve_streamk(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const 
     cvk::StreamLayout L{A->capk, 5, 1};
     L.ngather = 3;
     {
-        const long long avail = (long long)optin - 4096 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+        const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
         long long cap = 4;
         if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
         L.stages = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));

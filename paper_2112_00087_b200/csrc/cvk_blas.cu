@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_spmv_s(Csr A, StreamLayou
 cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
                                double2* y, int capk, int nsm, int optin, cudaStream_t st) {
     StreamLayout L{capk, 1, 1};
-    const long long avail = (long long)optin - 4096 - 2 * kStreamMaxStages * 8;
+    const long long avail = (long long)optin - 8192 - 2 * kStreamMaxStages * 8;
     L.stages = (int)std::min<long long>(kStreamMaxStages, avail / (long long)L.stage_bytes());
     if (L.stages < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = L.smem_bytes();

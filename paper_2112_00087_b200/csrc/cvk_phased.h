@@ -28,6 +28,8 @@ struct PhasedKernels {
     const void* true_res;  // (PArgs, double2* scratch)
     // streamed SpMV phases (cvk_stream.cuh): kStreamThreads threads, dynamic smem
     const void *bi_a_s, *bi_b_s, *tf_e_s, *tf_o_s;
+    // BiCGSTAB in two streamed kernels per iteration (x/r update merged into A)
+    const void *bm_init, *bm_a_s, *bm_b_s;
 };
 
 PhasedKernels phased_kernels();

@@ -364,3 +364,27 @@ def test_fast_paths_bitwise_identical(cvk, golden, monkeypatch, solver):
     for path, (it, x) in out.items():
         assert it == it0, (path, it, it0)
         assert np.array_equal(x, x0), path
+
+
+def test_merged_bicgstab_matches_reference(cvk, oracle, golden, monkeypatch):
+    """The opt-in two-kernel BiCGSTAB (rho_new from <shadow,s> - omega <shadow,t>,
+    x/r update merged into the next SpMV phase): same solution as the
+    reference at tol 1e-12, iteration count in the BiCGSTAB band."""
+    P = cvk
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    monkeypatch.setenv("CVK_BICG_MERGED", "1")
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    x_tight, _ = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-12)
+    r = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-12, record_history=True))
+    assert r.report.converged and r.report.final_relres <= 1e-12
+    assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
+    assert len(r.report.residual_history) >= r.report.iterations - 1
+    _, ro = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-9)
+    r9 = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-9))
+    assert r9.report.converged and abs(r9.report.iterations - ro.iterations) <= max(2, 0.15 * ro.iterations)
+    e = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(max_iter=3))
+    assert not e.report.converged and e.report.iterations == 3
+    z = P.solve(P.SolverId.BiCGStab, A, np.zeros_like(b), M)
+    assert z.report.converged and z.report.iterations == 0
