@@ -28,7 +28,10 @@ namespace cvk {
 
 namespace {
 
-constexpr int kBatch = 5;  // (value, column) loads issued up front per row (thread per row)
+#ifndef CVK_BATCH
+#define CVK_BATCH 5
+#endif
+constexpr int kBatch = CVK_BATCH;  // (value, column) loads issued up front per row (thread per row)
 
 struct PArgs {
     Csr A;
