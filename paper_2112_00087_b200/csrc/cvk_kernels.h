@@ -35,6 +35,18 @@ void streamk_pack_args(void* out, const Csr& A, const double2* dinv, const doubl
                        double2* part, unsigned long long* bar, DevReport* rep, double* hist, long long hist_cap,
                        double tol, long long max_iter, int record, const StreamLayout& L);
 
+// phase-kernel GMRES(m) (cvk_gmres.cu), kThreads threads per CTA
+struct GmresKernels {
+    const void *init, *x, *spmv, *dots, *upd1, *upd2, *true_res;
+};
+GmresKernels gmres_kernels();
+size_t gmres_state_size();
+size_t gmres_args_size();
+void gmres_init_state(void* host_state, double tol, long long max_iter, int m, int record, long long hist_cap);
+int gmres_state_done_offset();
+void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
+                     double2* part, void* st, double* hist, DevReport* rep);
+
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);

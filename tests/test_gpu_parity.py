@@ -388,3 +388,28 @@ def test_merged_bicgstab_matches_reference(cvk, oracle, golden, monkeypatch):
     assert not e.report.converged and e.report.iterations == 3
     z = P.solve(P.SolverId.BiCGStab, A, np.zeros_like(b), M)
     assert z.report.converged and z.report.iterations == 0
+
+
+@pytest.mark.parametrize("m", [30, 7])
+def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, golden, monkeypatch, m):
+    """GMRES(m) as phase kernels (cvk_gmres.cu) = the persistent kernel, bit
+    for bit (same operation order, double-double dots), across restarts; and
+    pinned to the reference solution at tight tolerance."""
+    P = cvk
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    out = {}
+    for path, min_n in (("persistent", "1000000000"), ("phased", "0")):
+        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+        r = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(tol=1e-11, m=m, max_iter=5000, record_history=True))
+        out[path] = r
+    a_, b_ = out["persistent"], out["phased"]
+    assert a_.report.converged and b_.report.converged
+    assert a_.report.iterations == b_.report.iterations
+    assert np.array_equal(bits(a_.x), bits(b_.x))
+    assert a_.report.residual_history == b_.report.residual_history
+    x_tight, _ = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-13)
+    assert np.linalg.norm(b_.x - x_tight) / np.linalg.norm(x_tight) <= 1e-9
+    e = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(m=m, max_iter=5))
+    assert not e.report.converged and e.report.iterations == 5
