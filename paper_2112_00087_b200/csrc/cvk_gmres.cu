@@ -136,7 +136,16 @@ __global__ void __launch_bounds__(kThreads) k_g_x(GArgs a) {
         __syncthreads();
         for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
             double2 xi = a.x[i];
-            for (int q = 0; q < k; ++q) xi = cvk_add(xi, cvk_mul(y[q], Vq(a, q)[i]));
+            const int cnt = k;
+            for (int q0 = 0; q0 < cnt; q0 += 4) {
+                    double2 vq4[4];
+#pragma unroll
+                    for (int u4 = 0; u4 < 4; ++u4)
+                        if (q0 + u4 < cnt) vq4[u4] = Vq(a, q0 + u4)[i];
+#pragma unroll
+                    for (int u4 = 0; u4 < 4; ++u4)
+                        if (q0 + u4 < cnt) xi = cvk_add(xi, cvk_mul(y[q0 + u4], vq4[u4]));
+                }
             a.x[i] = xi;
         });
     } else if (mode != G_WAIT) {
@@ -223,37 +232,51 @@ __global__ void __launch_bounds__(kThreads) k_g_dots(GArgs a) {
     if (UPDATE)
         for (int q = threadIdx.x; q < cnt; q += blockDim.x) hs[q] = st->h1[q];
     __syncthreads();
-    CAcc s[kMaxDots / kWarps];
-#pragma unroll
-    for (int u = 0; u < kMaxDots / kWarps; ++u) s[u] = CAcc{};
     const int nblk = (n + kGB - 1) / kGB;
-    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-        const int r0 = blk * kGB;
-        if (UPDATE) {
-            const int i = r0 + threadIdx.x;
-            if (i < n) {
-                double2 wi = w[i];
-                for (int q = 0; q < cnt; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q]), Vq(a, q)[i]));
-                w[i] = wi;
-            }
-            __syncthreads();
-        }
-#pragma unroll
-        for (int u = 0; u < kMaxDots / kWarps; ++u) {
-            const int q = warp + kWarps * u;
-            if (q < cnt) {
-                const double2* vq = Vq(a, q);
-                for (int i = r0 + lane; i < min(r0 + kGB, n); i += 32) acc_dot(s[u], vq[i], w[i]);
-            }
-        }
-        if (UPDATE) __syncthreads();
-    }
     double2* pr = a.part;
+    auto update_block = [&](int blk) {  // w -= V h1 on one block (thread per row, 4 basis loads in flight)
+        const int i = blk * kGB + threadIdx.x;
+        if (i < n) {
+            double2 wi = w[i];
+            for (int q0 = 0; q0 < cnt; q0 += 4) {
+                double2 vq4[4];
 #pragma unroll
-    for (int u = 0; u < kMaxDots / kWarps; ++u) {
-        const int q = warp + kWarps * u;
-        if (q < cnt) {
-            const CAcc t = warp_sum(s[u]);
+                for (int u4 = 0; u4 < 4; ++u4)
+                    if (q0 + u4 < cnt) vq4[u4] = Vq(a, q0 + u4)[i];
+#pragma unroll
+                for (int u4 = 0; u4 < 4; ++u4)
+                    if (q0 + u4 < cnt) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q0 + u4]), vq4[u4]));
+            }
+            w[i] = wi;
+        }
+    };
+    auto dot_block = [&](CAcc& sq, const double2* vq, int blk) {  // one basis vector, one block
+        const int r0 = blk * kGB;
+#pragma unroll
+        for (int e0 = 0; e0 < kGB / 32; e0 += 4) {
+            double2 vv[4], wv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = r0 + lane + 32 * (e0 + e);
+                if (i < n) { vv[e] = vq[i]; wv[e] = w[i]; }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (r0 + lane + 32 * (e0 + e) < n) acc_dot(sq, vv[e], wv[e]);
+        }
+    };
+    {
+        // update every block of this CTA first, then the dots with one
+        // accumulator live at a time (measured faster than block-interleaved
+        // update+dots, whose 122 registers halve the occupancy)
+        if (UPDATE) {
+            for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) update_block(blk);
+            __syncthreads();  // the dots below read only this CTA's rows
+        }
+        for (int q = warp; q < cnt; q += kWarps) {
+            CAcc sq = {};
+            for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) dot_block(sq, Vq(a, q), blk);
+            const CAcc t = warp_sum(sq);
             if (lane == 0) {
                 cacc_store(pr, q, gridDim.x, blockIdx.x, t);
                 __threadfence();
@@ -282,7 +305,15 @@ __global__ void __launch_bounds__(kThreads) k_g_upd2(GArgs a) {
     CAcc acc = {};
     for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
         double2 wi = w[i];
-        for (int q = 0; q < cnt; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q]), Vq(a, q)[i]));
+        for (int q0 = 0; q0 < cnt; q0 += 4) {
+            double2 vq4[4];
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4)
+                if (q0 + u4 < cnt) vq4[u4] = Vq(a, q0 + u4)[i];
+#pragma unroll
+            for (int u4 = 0; u4 < 4; ++u4)
+                if (q0 + u4 < cnt) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q0 + u4]), vq4[u4]));
+        }
         w[i] = wi;
         acc_norm(acc, wi);
     });

@@ -391,12 +391,13 @@ def test_merged_bicgstab_matches_reference(cvk, oracle, golden, monkeypatch):
 
 
 @pytest.mark.parametrize("m", [30, 7])
-def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, golden, monkeypatch, m):
+def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, monkeypatch, m):
     """GMRES(m) as phase kernels (cvk_gmres.cu) = the persistent kernel, bit
     for bit (same operation order, double-double dots), across restarts; and
     pinned to the reference solution at tight tolerance."""
     P = cvk
-    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    # a damped cavity GMRES(m) converges on (the golden 74 Hz system stalls GMRES(30))
+    rp, ci, v, b = cavity(oracle, 0.05, f=13.0, adm=0.02)
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     out = {}
