@@ -51,6 +51,10 @@ struct cvk_ctx {
     void* gst = nullptr;  // cvk::GState
     cudaGraphExec_t gm_exec = nullptr;
     std::vector<unsigned char> gm_key;
+    // phase-kernel BiCGSTAB(l)
+    void* bst = nullptr;  // cvk::BLState
+    cudaGraphExec_t bl_exec = nullptr;
+    std::vector<unsigned char> bl_key;
 };
 
 struct cvk_csr {
@@ -219,6 +223,8 @@ int cvk_ctx_destroy(cvk_ctx* c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
     cudaFree(c->gst);
+    if (c->bl_exec) cudaGraphExecDestroy(c->bl_exec);
+    cudaFree(c->bst);
     cudaStreamDestroy(c->stream);
     delete c;
     return CVK_OK;
@@ -907,6 +913,98 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     return CVK_OK;
 }
 
+// Phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): N identical step launches per graph.
+static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                              const double2* b_dev, double2* x_dev, cvk_report* rep) {
+    const int n = (int)A->n;
+    const int L = (int)o->l;
+    const cvk::BiclKernels K = cvk::bicgl_kernels();
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.step, cvk::kThreads, 0));
+    const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
+    long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, chunks);
+    if (const char* env = std::getenv("CVK_BICGL_CTAS")) G = std::max(1, std::atoi(env));
+    int e;
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(2 * L + 6) * std::max(1, n))) != CVK_OK)
+        return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
+        return e;
+    if (!c->bst) CK(cudaMalloc(&c->bst, cvk::bicgl_state_size()));
+    const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
+    if (hcap > 0 && (size_t)hcap > c->hist_cap) {
+        cudaFree(c->hist);
+        c->hist = nullptr;
+        c->hist_cap = 0;
+        CK(cudaMalloc(&c->hist, sizeof(double) * hcap));
+        c->hist_cap = (size_t)hcap;
+    }
+    std::vector<unsigned char> hs(cvk::bicgl_state_size(), 0);
+    cvk::bicgl_init_state(hs.data(), o->tol, o->max_iter < 1 ? 0 : o->max_iter, L, o->record_history ? 1 : 0, hcap);
+    std::vector<unsigned char> blob(cvk::bicgl_args_size());
+    cvk::bicgl_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev, (double2*)c->work,
+                         c->part, c->bst, c->hist, c->rep);
+    void* args[] = {blob.data()};
+    const dim3 grid((unsigned)G), block(cvk::kThreads);
+    constexpr int kStepsPerGraph = 32;
+    std::vector<unsigned char> key(blob);
+    const unsigned char* gp = (const unsigned char*)&G;
+    key.insert(key.end(), gp, gp + sizeof(G));
+    if (!c->bl_exec || c->bl_key != key) {
+        if (c->bl_exec) { cudaGraphExecDestroy(c->bl_exec); c->bl_exec = nullptr; }
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int it = 0; it < kStepsPerGraph; ++it) launch_pdl(K.step, grid, block, args, 0, c->stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamEndCapture(c->stream, &graph));
+        CK(cudaGraphInstantiate(&c->bl_exec, graph, 0));
+        cudaGraphDestroy(graph);
+        c->bl_key = key;
+    }
+    CK(cudaMemcpyAsync(c->bst, hs.data(), hs.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->e0, c->stream));
+    CK(launch_pdl(K.init, grid, block, args, 0, c->stream));
+    long long launches = 1;
+    const int* done_ptr = (const int*)((const char*)c->bst + cvk::bicgl_state_done_offset());
+    const long long per_cycle = 2LL * L + (long long)L * (L + 1) / 2 + 2;
+    const long long max_graphs = (std::max<long long>(1, o->max_iter) * per_cycle) / kStepsPerGraph + 3;
+    long long graphs = 0;
+    for (;;) {
+        if (graphs >= max_graphs) break;
+        CK(cudaGraphLaunch(c->bl_exec, c->stream));
+        const int slot = (int)(graphs & 1);
+        CK(cudaMemcpyAsync(&c->h_done[slot], done_ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(c->ev[slot], c->stream));
+        ++graphs;
+        launches += kStepsPerGraph;
+        if (graphs >= 2) {
+            const int old = (int)((graphs - 2) & 1);
+            CK(cudaEventSynchronize(c->ev[old]));
+            if (c->h_done[old]) break;
+        }
+    }
+    CK(launch_pdl(K.true_res, grid, block, args, 0, c->stream));
+    launches += 1;
+    CK(cudaEventRecord(c->e1, c->stream));
+    DevReport dr;
+    CK(cudaMemcpyAsync(&dr, c->rep, sizeof(dr), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    rep->converged = dr.converged;
+    rep->breakdown = dr.breakdown;
+    rep->iterations = dr.iterations;
+    rep->final_relres = dr.final_relres;
+    rep->true_relres = dr.true_relres;
+    rep->history_len = o->record_history ? dr.history_len : 0;
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = launches;
+    if (o->record_history && rep->history && rep->history_cap > 0) {
+        const long long k = std::min<long long>(std::min<long long>(rep->history_len, rep->history_cap), hcap);
+        if (k > 0) CK(cudaMemcpy(rep->history, c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    return CVK_OK;
+}
+
 static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                       const double2* b_dev, double2* x_dev, cvk_report* rep) {
     if (solver < 0 || solver > 3)
@@ -938,6 +1036,8 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     // GMRES phase kernels from 32k rows (50k DOF: 58 vs 63 us per step; BiCGSTAB keeps the persistent kernel there)
     if (!ref && solver == CVK_GMRES && (long long)n >= std::min(phased_min_n(), 32768LL) && !std::getenv("CVK_GMRES_PERSISTENT"))
         return solve_gmres_phased(c, A, M, o, b_dev, x_dev, rep);
+    if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= phased_min_n() && !std::getenv("CVK_BICGL_PERSISTENT"))
+        return solve_bicgl_phased(c, A, M, o, b_dev, x_dev, rep);
     if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n()) {
         const bool pinned = l2_pin(c, A);
         const int rc = solve_phased(c, solver, A, M, o, b_dev, x_dev, rep, pinned);

@@ -47,6 +47,18 @@ int gmres_state_done_offset();
 void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
                      double2* part, void* st, double* hist, DevReport* rep);
 
+// phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): one uniform step kernel
+struct BiclKernels {
+    const void *init, *step, *true_res;
+};
+BiclKernels bicgl_kernels();
+size_t bicgl_state_size();
+size_t bicgl_args_size();
+int bicgl_state_done_offset();
+void bicgl_init_state(void* host_state, double tol, long long max_iter, int l, int record, long long hist_cap);
+void bicgl_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
+                     double2* part, void* st, double* hist, DevReport* rep);
+
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);

@@ -414,3 +414,30 @@ def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, monkeypatch, m):
     assert np.linalg.norm(b_.x - x_tight) / np.linalg.norm(x_tight) <= 1e-9
     e = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(m=m, max_iter=5))
     assert not e.report.converged and e.report.iterations == 5
+
+
+@pytest.mark.parametrize("l", [8, 2, 1])
+def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypatch, l):
+    """BiCGSTAB(l) as the uniform phase-step kernel (cvk_bicgl.cu) = the
+    persistent kernel bit for bit (double-double reductions), and the
+    reference's iteration count within the +-5% band of SURVEY.md 8(c)."""
+    P = cvk
+    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    out = {}
+    for path, min_n in (("persistent", "1000000000"), ("phased", "0")):
+        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+        out[path] = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(tol=1e-10, l=l, record_history=True))
+    a_, b_ = out["persistent"], out["phased"]
+    assert a_.report.converged and b_.report.converged
+    assert a_.report.iterations == b_.report.iterations
+    assert np.array_equal(bits(a_.x), bits(b_.x))
+    assert a_.report.residual_history == b_.report.residual_history
+    _, ro = oracle.solve("bicgstab_l", rp, ci, v, b, tol=1e-10, l=l)
+    assert abs(b_.report.iterations - ro.iterations) <= max(2, 0.05 * ro.iterations)
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    e = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(l=l, max_iter=2))
+    assert not e.report.converged and e.report.iterations == 2
+    z = P.solve(P.SolverId.BiCGStabL, A, np.zeros_like(b), M, P.SolverOptions(l=l))
+    assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
