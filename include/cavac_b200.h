@@ -273,6 +273,60 @@ int cvk_fem_create(cvk_csr *A, const double *K, const double *M, const double *C
 int cvk_fem_set_omega(cvk_fem *op, double omega);
 int cvk_fem_free(cvk_fem *op);
 
+/* ---- row-block global Krylov (SURVEY.md 8(e) mode 1; beyond the reference,
+ * whose solve() runs on one address space, krylov.hpp:68-69) ----
+ *
+ * One rank's contiguous block of rows of the global system.  Local columns
+ * are [0, n_own) for own rows and n_own + h for halo entry h (a row of
+ * another rank).  Every reduction phase of BiCGSTAB (krylov.cpp:57-138) is
+ *   cvk_rowblock_local(ph)  -- the phase's rows; the rank's double-double
+ *                              partial sums and the boundary values other
+ *                              ranks read go to the rank's exchange slot;
+ *   all-gather              -- of every rank's slot into `recv` (caller:
+ *                              NCCL over NVLink, gloo, or
+ *                              cvk_rowblock_exchange_local for blocks that
+ *                              share one device);
+ *   cvk_rowblock_post(ph)   -- fold the ranks' partials in rank order, run
+ *                              the scalar recurrence, unpack the halo.
+ * The reductions are double-double, so iterates are bitwise those of a
+ * single-device FAST solve for any number of blocks. */
+#define CVK_RB_INIT 0 /* r = M^-1 b, shadow, x = 0; ||r||, <r,r>; r halo */
+#define CVK_RB_A 1    /* p, v = M^-1 A p, <shadow, v>; p, v halo */
+#define CVK_RB_B 2    /* s, t = M^-1 A s, x += alpha p; ||s||, <t,t>, <t,s> */
+#define CVK_RB_C 3    /* x += omega s, r = s - omega t; ||r||, <shadow, r>; r halo */
+#define CVK_RB_X 4    /* x halo (before the true residual) */
+#define CVK_RB_T 5    /* ||b||, ||b - A x|| -> report */
+typedef struct cvk_rowblock cvk_rowblock;
+typedef struct {
+    int64_t n_own, n_halo, nnz;
+    const int64_t *row_offsets; /* n_own + 1, from 0 */
+    const int64_t *col_local;   /* nnz, each in [0, n_own + n_halo) */
+    const double *values;       /* 2 nnz, interleaved complex */
+    const double *inv_diag;     /* 2 n_own (jacobi of the global matrix), NULL = identity */
+    const double *b;            /* 2 n_own */
+    int64_t n_send;             /* own rows other ranks read */
+    const int64_t *send_rows;   /* n_send local rows, in exchange order */
+    int64_t n_ranks, max_send;  /* max_send = largest n_send over all ranks */
+    const int64_t *halo_src;    /* n_halo: src_rank * max_send + position in src's send list */
+    int64_t history_cap;
+} cvk_rowblock_desc;
+int cvk_rowblock_create(cvk_ctx *ctx, const cvk_rowblock_desc *desc, int solver, const cvk_opts *opts,
+                        cvk_rowblock **out);
+/* device exchange buffers: send = this rank's slot (slot_doubles), recv =
+ * n_ranks slots, slot q at recv + q * slot_doubles */
+int cvk_rowblock_exchange(cvk_rowblock *rb, double **send_dev, double **recv_dev, int64_t *slot_doubles);
+int cvk_rowblock_local(cvk_rowblock *rb, int phase);
+int cvk_rowblock_post(cvk_rowblock *rb, int phase);
+/* all-gather for n blocks on one device (stream-ordered device copies) */
+int cvk_rowblock_exchange_local(cvk_rowblock *const *rbs, int n);
+/* whole solve for n blocks on one device: the phase loop with lazy polling */
+int cvk_rowblock_solve_local(cvk_rowblock *const *rbs, int n);
+/* synchronises; *done = the solver's stop flag */
+int cvk_rowblock_done(cvk_rowblock *rb, int *done);
+/* after CVK_RB_X and CVK_RB_T: own rows of x (2 n_own doubles) and the report */
+int cvk_rowblock_result(cvk_rowblock *rb, double *x_own, cvk_report *rep);
+int cvk_rowblock_destroy(cvk_rowblock *rb);
+
 /* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
  * device buffers, returns the average kernel time in seconds ---- */
 int cvk_spmv_bench(const cvk_csr *A, const double *x_dev, double *y_dev, int mode,

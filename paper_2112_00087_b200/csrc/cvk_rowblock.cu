@@ -1,0 +1,713 @@
+// cvk_rowblock.cu -- row-block global BiCGSTAB: one rank's contiguous block
+// of rows of the global system (SURVEY.md 8(e) mode 1).
+//
+// The reference solves on one address space (krylov.cpp:57-138).  Here the
+// rows are split over ranks (one per GPU, or several blocks on one device);
+// each reduction phase of the fused BiCGSTAB schedule (cvk_phased.cu k_bi_*)
+// becomes
+//
+//   k_rb_<phase>  the phase over the rank's own rows; its last CTA folds the
+//                 CTA partials into the rank's double-double totals and
+//                 writes them to the rank's exchange slot
+//   k_rb_pack     boundary values other ranks gather (r after C, p and v
+//                 after A, x before the true residual) into the same slot
+//   all-gather    of every rank's slot (NCCL / gloo / device copies)
+//   k_rb_post     every rank folds the ranks' totals in rank order and runs
+//                 the reference's scalar logic (identical on all ranks), and
+//                 unpacks its halo from the gathered slots
+//
+// so there is exactly one collective per reduction, carrying both the
+// reduction and the halo.  The halo needs no extra exchange step because p
+// is formed inside the SpMV gathers from r, p_old and v, whose halo values
+// arrive with the preceding phases.
+//
+// Per-row SpMV order, per-element roundings and the double-double reductions
+// are those of the single-device FAST kernels, so iterates are bitwise a
+// single-device solve for any number of blocks
+// (tests/test_gpu_rowblock.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cavac_b200.h"
+#include "cvk_engine.cuh"
+#include "cvk_kernels.h"
+#include "cvk_phased.h"
+
+namespace cvk {
+namespace {
+
+constexpr int kHdr = 16;   // exchange slot header: up to 4 complex dd totals (hi.x hi.y lo.x lo.y)
+constexpr int kRbBatch = 5;
+
+struct RBArgs {
+    Csr A;               // n = own rows; columns < n_own + n_halo
+    long long nv;        // vector stride
+    const double2* dinv;
+    const double2* b;
+    double2* work;       // x r sh s t p0 p1 v0 v1, stride nv
+    double2* part;       // CTA partials (cacc_store layout, 3 reductions)
+    PState* st;
+    double* hist;
+    DevReport* rep;
+    double* send;        // this rank's exchange slot
+    const double* recv;  // nranks slots
+    int nranks, slot;    // slot: doubles per rank
+    const int* send_rows;
+    int n_send, max_send;
+    const int* halo_src;
+    int n_halo;
+};
+
+enum { VX = 0, VR, VSH, VS, VT, VP0, VP1, VV0, VV1, kRbVecs };
+
+__device__ __forceinline__ double2* vec(const RBArgs& a, int k) { return a.work + (size_t)k * a.nv; }
+
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// CTA partials -> the rank's double-double totals in send[0 .. 4K) (last CTA)
+template <int K>
+__device__ void rank_total(const CAcc (&acc)[K], const RBArgs& a, unsigned* counter) {
+    __shared__ CAcc sm[K][32];
+    __shared__ int s_last;
+    const int G = gridDim.x;
+    CAcc v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = acc[k];
+    cta_sum_k<K, kThreads>(v, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) cacc_store(a.part, k, G, blockIdx.x, v[k]);
+        __threadfence();
+        s_last = (atomicAdd(counter, 1u) == (unsigned)G - 1u);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    CAcc s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k] = CAcc{};
+#pragma unroll 1
+    for (int q = threadIdx.x; q < G; q += kThreads) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) cacc_add(s[k], cacc_load(a.part, k, G, q));
+    }
+    cta_sum_k<K, kThreads>(s, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            a.send[4 * k + 0] = s[k].hi.x;
+            a.send[4 * k + 1] = s[k].hi.y;
+            a.send[4 * k + 2] = s[k].lo.x;
+            a.send[4 * k + 3] = s[k].lo.y;
+        }
+        *counter = 0u;
+    }
+}
+
+// the ranks' totals of reduction k, folded in rank order
+__device__ double2 fold_ranks(const RBArgs& a, int k) {
+    CAcc s = {};
+    for (int q = 0; q < a.nranks; ++q) {
+        const double* p = a.recv + (size_t)q * a.slot + 4 * k;
+        CAcc t;
+        t.hi = make_double2(p[0], p[1]);
+        t.lo = make_double2(p[2], p[3]);
+        cacc_add(s, t);
+    }
+    return s.hi;
+}
+
+__device__ __forceinline__ void rb_hist(const RBArgs& a, PState* st, double v) {
+    if (!st->record) return;
+    if (st->hist_len < st->hist_cap) a.hist[st->hist_len] = v;
+    st->hist_len++;
+}
+
+// top of iteration st->it (krylov.cpp:81-96)
+__device__ void rb_top(PState* st) {
+    if (st->it > st->max_iter) { st->done = 1; return; }
+    if (cvk_abs(st->rho_new) < st->brk) {
+        st->done = 1; st->brk_code = 1; st->iters = st->it - 1;
+        return;
+    }
+    if (!st->first) st->beta = cvk_mul(cvk_cdiv(st->rho_new, st->rho), cvk_cdiv(st->alpha, st->omega));
+    st->rho = st->rho_new;
+}
+
+// ------------------------------------------------------------ local phases
+
+__global__ void __launch_bounds__(kThreads) k_rb_init(RBArgs a) {
+    pdl_wait();
+    const int n = a.A.n;
+    double2* r = vec(a, VR);
+    double2* sh = vec(a, VSH);
+    double2* x = vec(a, VX);
+    CAcc acc[2] = {};
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
+        r[i] = ri;
+        sh[i] = ri;
+        x[i] = make_double2(0.0, 0.0);
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], ri, ri);
+    });
+    rank_total<2>(acc, a, &a.st->counter[0]);
+}
+
+// p = r + beta (p - omega v) formed in the gathers; v = M^-1 A p; <shadow, v>
+__global__ void __launch_bounds__(kThreads) k_rb_a(RBArgs a) {
+    pdl_wait();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n, cur = st->cur;
+    const bool first = st->first != 0;
+    const double2 beta = st->beta, nom = cvk_neg(st->omega);
+    const double2* __restrict__ r = vec(a, VR);
+    const double2* __restrict__ pc = vec(a, cur ? VP1 : VP0);
+    const double2* __restrict__ vc = vec(a, cur ? VV1 : VV0);
+    double2* __restrict__ pn = vec(a, cur ? VP0 : VP1);
+    double2* __restrict__ vn = vec(a, cur ? VV0 : VV1);
+    const double2* __restrict__ sh = vec(a, VSH);
+    auto pnew = [&](int c) -> double2 {
+        const double2 rc = r[c];
+        if (first) return rc;
+        return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+    };
+    CAcc acc[1] = {};
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(pnew)&, kRbBatch>(a.A, row, 0, valid, pnew);
+        if (valid) {
+            const double2 vi = prec_apply(a.dinv, row, y);
+            pn[row] = pnew(row);
+            vn[row] = vi;
+            acc_dot(acc[0], sh[row], vi);
+        }
+    });
+    rank_total<1>(acc, a, &st->counter[1]);
+}
+
+// s = r - alpha v formed in the gathers; t = M^-1 A s; x += alpha p
+__global__ void __launch_bounds__(kThreads) k_rb_b(RBArgs a) {
+    pdl_wait();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n, cur = st->cur;
+    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
+    const double2* __restrict__ r = vec(a, VR);
+    const double2* __restrict__ pn = vec(a, cur ? VP0 : VP1);
+    const double2* __restrict__ vn = vec(a, cur ? VV0 : VV1);
+    double2* __restrict__ s = vec(a, VS);
+    double2* __restrict__ t = vec(a, VT);
+    double2* __restrict__ x = vec(a, VX);
+    auto sval = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+    CAcc acc[3] = {};
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(sval)&, kRbBatch>(a.A, row, 0, valid, sval);
+        if (valid) {
+            const double2 ti = prec_apply(a.dinv, row, y);
+            const double2 si = sval(row);
+            s[row] = si;
+            t[row] = ti;
+            x[row] = cvk_add(x[row], cvk_mul(alpha, pn[row]));
+            acc_norm(acc[0], si);
+            acc_dot(acc[1], ti, ti);
+            acc_dot(acc[2], ti, si);
+        }
+    });
+    rank_total<3>(acc, a, &st->counter[2]);
+}
+
+// x += omega s; r = s - omega t; ||r||, <shadow, r>
+__global__ void __launch_bounds__(kThreads) k_rb_c(RBArgs a) {
+    pdl_wait();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    const double2 omega = st->omega, nom = cvk_neg(st->omega);
+    const double2* __restrict__ s = vec(a, VS);
+    const double2* __restrict__ t = vec(a, VT);
+    const double2* __restrict__ sh = vec(a, VSH);
+    double2* __restrict__ r = vec(a, VR);
+    double2* __restrict__ x = vec(a, VX);
+    CAcc acc[2] = {};
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 si = s[i], ti = t[i];
+        x[i] = cvk_add(x[i], cvk_mul(omega, si));
+        const double2 ri = cvk_add(si, cvk_mul(nom, ti));
+        r[i] = ri;
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], sh[i], ri);
+    });
+    rank_total<2>(acc, a, &st->counter[0]);
+}
+
+// ||b||^2, ||b - A x||^2 over own rows (x halo from CVK_RB_X); krylov.cpp:17-23
+__global__ void __launch_bounds__(kThreads) k_rb_t(RBArgs a) {
+    pdl_wait();
+    PState* st = a.st;
+    const int n = a.A.n;
+    const double2* __restrict__ x = vec(a, VX);
+    auto xat = [&](int c) -> double2 { return x[c]; };
+    CAcc acc[2] = {};
+    if (!st->skip_true) {
+        for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
+            const double2 y = row_sum<1, decltype(xat)&, kRbBatch>(a.A, row, 0, valid, xat);
+            if (valid) {
+                const double2 bi = __ldg(a.b + row);
+                acc_norm(acc[0], bi);
+                acc_norm(acc[1], cvk_sub(bi, y));
+            }
+        });
+    }
+    rank_total<2>(acc, a, &st->counter[3]);
+}
+
+// ------------------------------------------------------------- exchange --
+
+// values of phase ph's halo vectors (nv_ph of them) for exchange position k
+__device__ __forceinline__ int phase_vecs(int ph, int cur, int (&v)[2]) {
+    switch (ph) {
+        case CVK_RB_INIT: case CVK_RB_C: v[0] = VR; return 1;
+        case CVK_RB_A: v[0] = cur ? VP0 : VP1; v[1] = cur ? VV0 : VV1; return 2;
+        case CVK_RB_X: v[0] = VX; return 1;
+        default: return 0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_rb_pack(RBArgs a, int ph) {
+    pdl_wait();
+    const PState* st = a.st;
+    if (ph != CVK_RB_X && st->done) return;
+    int vv[2];
+    const int nvp = phase_vecs(ph, st->cur, vv);
+    double2* out = (double2*)(a.send + kHdr);
+    const long long total = (long long)a.n_send * nvp;
+    for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < total; i += (long long)gridDim.x * kThreads) {
+        const int k = (int)(i / nvp), j = (int)(i - (long long)k * nvp);
+        out[i] = vec(a, vv[j])[__ldg(a.send_rows + k)];
+    }
+}
+
+// fold + scalar recurrence (CTA 0, thread 0) and halo unpack (all CTAs)
+__global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
+    pdl_wait();
+    PState* st = a.st;
+    if (ph != CVK_RB_X && ph != CVK_RB_T && st->done) return;
+    int vv[2];
+    const int nvp = phase_vecs(ph, st->cur, vv);
+    const long long total = (long long)a.n_halo * nvp;
+    for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < total; i += (long long)gridDim.x * kThreads) {
+        const int h = (int)(i / nvp), j = (int)(i - (long long)h * nvp);
+        const int src = __ldg(a.halo_src + h);
+        const int q = src / a.max_send, k = src - q * a.max_send;
+        const double2* in = (const double2*)(a.recv + (size_t)q * a.slot + kHdr);
+        vec(a, vv[j])[a.A.n + h] = in[(size_t)k * nvp + j];
+    }
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    switch (ph) {
+        case CVK_RB_INIT: {  // krylov.cpp:62-79
+            const double2 nr = fold_ranks(a, 0), rr = fold_ranks(a, 1);
+            st->bnorm = sqrt(nr.x);
+            if (st->bnorm == 0.0) {
+                st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1;
+                return;
+            }
+            st->brk = 1e-30 * st->bnorm * st->bnorm;
+            st->rho_new = rr;
+            st->rho = st->alpha = st->omega = make_double2(1.0, 0.0);
+            st->it = 1;
+            st->first = 1;
+            st->cur = 0;
+            rb_top(st);
+            return;
+        }
+        case CVK_RB_A: {  // krylov.cpp:97-103
+            const double2 sv = fold_ranks(a, 0);
+            if (cvk_abs(sv) < st->brk) {
+                st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
+                return;
+            }
+            st->alpha = cvk_cdiv(st->rho, sv);
+            return;
+        }
+        case CVK_RB_B: {  // krylov.cpp:104-122
+            const double2 ss = fold_ranks(a, 0), tt = fold_ranks(a, 1), ts = fold_ranks(a, 2);
+            const double relres = sqrt(ss.x) / st->bnorm;
+            if (relres <= st->tol) {
+                st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
+                rb_hist(a, st, relres);
+                return;
+            }
+            if (cvk_abs(tt) < st->brk) {
+                st->done = 1; st->brk_code = 3; st->iters = st->it;
+                return;
+            }
+            st->omega = cvk_cdiv(ts, tt);
+            return;
+        }
+        case CVK_RB_C: {  // krylov.cpp:123-133
+            const double2 rn = fold_ranks(a, 0), shr = fold_ranks(a, 1);
+            const double relres = sqrt(rn.x) / st->bnorm;
+            st->final_relres = relres;
+            st->iters = st->it;
+            rb_hist(a, st, relres);
+            if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
+            st->rho_new = shr;
+            st->cur ^= 1;
+            st->first = 0;
+            st->it++;
+            rb_top(st);
+            return;
+        }
+        case CVK_RB_T: {  // krylov.cpp:17-23, 135
+            double trr = 0.0;
+            if (!st->skip_true) {
+                const double bn = sqrt(fold_ranks(a, 0).x), rn = sqrt(fold_ranks(a, 1).x);
+                trr = bn > 0 ? rn / bn : rn;
+            }
+            a.rep->converged = st->conv;
+            a.rep->breakdown = st->brk_code;
+            a.rep->iterations = st->iters;
+            a.rep->final_relres = st->final_relres;
+            a.rep->true_relres = trr;
+            a.rep->history_len = st->hist_len;
+            a.rep->error = 0;
+            return;
+        }
+        default: return;
+    }
+}
+
+}  // namespace
+}  // namespace cvk
+
+// ---------------------------------------------------------------- host ---
+
+using cvk::PState;
+
+struct cvk_rowblock {
+    cvk_ctx* ctx = nullptr;
+    cudaStream_t s = nullptr;
+    int nsm = 0;
+    int64_t n_own = 0, n_halo = 0, nnz = 0, nv = 0;
+    int G = 1, Gx = 1;  // row/elem phases; pack/post
+    std::vector<void*> bufs;
+    double* send = nullptr;
+    double* recv = nullptr;
+    int64_t slot = 0;
+    cvk::RBArgs args{};
+    int64_t hist_cap = 0;
+    long long launches = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    double t_wall0 = 0.0;
+    int solver = CVK_BICGSTAB;
+    ~cvk_rowblock() {
+        for (void* p : bufs) cudaFree(p);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+    template <class T>
+    cudaError_t alloc(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, std::max<size_t>(1, count) * sizeof(T));
+        if (e == cudaSuccess) {
+            bufs.push_back(q);
+            *p = (T*)q;
+        }
+        return e;
+    }
+};
+
+namespace {
+
+int rbfail(int code, const std::string& m) { return cvk_fail(code, m); }
+#define RK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return rbfail(e_ == cudaErrorMemoryAllocation ? CVK_ENOMEM : CVK_ECUDA,               \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+    } while (0)
+
+double wall_now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+cudaError_t rb_launch(const void* f, int grid, cudaStream_t s, void** args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(cvk::kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, f, args);
+}
+
+}  // namespace
+
+extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int solver, const cvk_opts* o,
+                                   cvk_rowblock** out) {
+    if (!ctx || !d || !o || !out) return rbfail(CVK_EINVAL, "cvk_rowblock_create: null argument");
+    *out = nullptr;
+    if (solver != CVK_BICGSTAB)
+        return rbfail(CVK_ESOLVER, "cvk_rowblock_create: the row-block path runs bicgstab");
+    if (o->mode == CVK_MODE_REF)
+        return rbfail(CVK_EINVAL, "cvk_rowblock_create: REF mode is single-device (sequential sums)");
+    if (d->n_own < 0 || d->n_halo < 0 || d->nnz < 0 || d->n_ranks < 1 || d->n_send < 0 || d->max_send < d->n_send)
+        return rbfail(CVK_EINVAL, "cvk_rowblock_create: bad sizes");
+    if (d->n_own + d->n_halo >= (1LL << 31) || d->nnz >= (1LL << 31) || d->n_ranks * std::max<int64_t>(1, d->max_send) >= (1LL << 31))
+        return rbfail(CVK_EOVERFLOW, "cvk_rowblock_create: block does not fit int32 indices");
+    const int64_t ncol = d->n_own + d->n_halo;
+    if (d->n_own > 0 && (!d->row_offsets || !d->b)) return rbfail(CVK_EINVAL, "cvk_rowblock_create: null rows / rhs");
+    if (d->n_own > 0 && (d->row_offsets[0] != 0 || d->row_offsets[d->n_own] != d->nnz))
+        return rbfail(CVK_EINVAL, "cvk_rowblock_create: row_offsets must run 0 .. nnz");
+    std::vector<int> rp((size_t)d->n_own + 1, 0), ci((size_t)d->nnz), sr((size_t)d->n_send), hs((size_t)d->n_halo);
+    for (int64_t i = 0; i < d->n_own; ++i) {
+        if (d->row_offsets[i + 1] < d->row_offsets[i]) return rbfail(CVK_EINVAL, "cvk_rowblock_create: row_offsets decrease");
+        rp[(size_t)i + 1] = (int)d->row_offsets[i + 1];
+    }
+    for (int64_t k = 0; k < d->nnz; ++k) {
+        if (d->col_local[k] < 0 || d->col_local[k] >= ncol)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_create: column " + std::to_string(d->col_local[k]) + " outside the block");
+        ci[(size_t)k] = (int)d->col_local[k];
+    }
+    for (int64_t k = 0; k < d->n_send; ++k) {
+        if (d->send_rows[k] < 0 || d->send_rows[k] >= d->n_own) return rbfail(CVK_EINVAL, "cvk_rowblock_create: send row outside the block");
+        sr[(size_t)k] = (int)d->send_rows[k];
+    }
+    for (int64_t h = 0; h < d->n_halo; ++h) {
+        if (d->halo_src[h] < 0 || d->halo_src[h] >= d->n_ranks * d->max_send)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_create: halo source outside the exchange");
+        hs[(size_t)h] = (int)d->halo_src[h];
+    }
+
+    cvk_rowblock* R = new cvk_rowblock();
+    auto bail = [&](int e) { delete R; return e; };
+    R->ctx = ctx;
+    R->s = (cudaStream_t)cvk_ctx_stream(ctx);
+    R->solver = solver;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&R->nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return bail(rbfail(CVK_ECUDA, "cvk_rowblock_create: no device"));
+    R->n_own = d->n_own;
+    R->n_halo = d->n_halo;
+    R->nnz = d->nnz;
+    R->nv = (ncol + 31) / 32 * 32;
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)cvk::k_rb_b, cvk::kThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const long long chunks = std::max<long long>(1, (d->n_own + cvk::kThreads - 1) / cvk::kThreads);
+    R->G = (int)std::min<long long>(chunks, 32LL * per_sm * R->nsm);
+    const long long xchunks = std::max<long long>(1, (std::max(d->n_send, d->n_halo) * 2 + cvk::kThreads - 1) / cvk::kThreads);
+    R->Gx = (int)std::min<long long>(xchunks, R->nsm);
+    R->slot = cvk::kHdr + 4 * std::max<int64_t>(1, d->max_send);
+    R->hist_cap = o->record_history ? std::max<int64_t>(d->history_cap, 0) : 0;
+
+    int *d_rp, *d_ci, *d_sr, *d_hs;
+    double2 *d_av, *d_dinv = nullptr, *d_b, *d_work, *d_part;
+    PState* d_st;
+    double* d_hist;
+    cvk::DevReport* d_rep;
+    cudaError_t e = cudaSuccess;
+    if ((e = R->alloc(&d_rp, rp.size())) != cudaSuccess || (e = R->alloc(&d_ci, ci.size())) != cudaSuccess ||
+        (e = R->alloc(&d_sr, sr.size())) != cudaSuccess || (e = R->alloc(&d_hs, hs.size())) != cudaSuccess ||
+        (e = R->alloc(&d_av, (size_t)d->nnz)) != cudaSuccess || (e = R->alloc(&d_b, (size_t)d->n_own)) != cudaSuccess ||
+        (e = R->alloc(&d_work, (size_t)cvk::kRbVecs * R->nv)) != cudaSuccess ||
+        (e = R->alloc(&d_part, (size_t)6 * R->G)) != cudaSuccess || (e = R->alloc(&d_st, 1)) != cudaSuccess ||
+        (e = R->alloc(&d_hist, (size_t)std::max<int64_t>(1, R->hist_cap))) != cudaSuccess ||
+        (e = R->alloc(&d_rep, 1)) != cudaSuccess || (e = R->alloc(&R->send, (size_t)R->slot)) != cudaSuccess ||
+        (e = R->alloc(&R->recv, (size_t)R->slot * d->n_ranks)) != cudaSuccess ||
+        (d->inv_diag && (e = R->alloc(&d_dinv, (size_t)d->n_own)) != cudaSuccess))
+        return bail(rbfail(e == cudaErrorMemoryAllocation ? CVK_ENOMEM : CVK_ECUDA,
+                           std::string("cvk_rowblock_create: ") + cudaGetErrorString(e)));
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, R->s) : cudaSuccess;
+    };
+    if ((e = h2d(d_rp, rp.data(), rp.size() * 4)) != cudaSuccess || (e = h2d(d_ci, ci.data(), ci.size() * 4)) != cudaSuccess ||
+        (e = h2d(d_sr, sr.data(), sr.size() * 4)) != cudaSuccess || (e = h2d(d_hs, hs.data(), hs.size() * 4)) != cudaSuccess ||
+        (e = h2d(d_av, d->values, (size_t)d->nnz * 16)) != cudaSuccess ||
+        (e = h2d(d_b, d->b, (size_t)d->n_own * 16)) != cudaSuccess ||
+        (d_dinv && (e = h2d(d_dinv, d->inv_diag, (size_t)d->n_own * 16)) != cudaSuccess) ||
+        (e = cudaMemsetAsync(d_work, 0, sizeof(double2) * cvk::kRbVecs * R->nv, R->s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(R->send, 0, sizeof(double) * R->slot, R->s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(R->recv, 0, sizeof(double) * R->slot * d->n_ranks, R->s)) != cudaSuccess)
+        return bail(rbfail(CVK_ECUDA, std::string("cvk_rowblock_create: upload: ") + cudaGetErrorString(e)));
+    PState hs0;
+    std::memset(&hs0, 0, sizeof(hs0));
+    hs0.tol = o->tol;
+    hs0.max_iter = o->max_iter < 1 ? 0 : o->max_iter;
+    hs0.record = R->hist_cap > 0 ? 1 : 0;
+    hs0.hist_cap = R->hist_cap;
+    if ((e = cudaMemcpyAsync(d_st, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, R->s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(R->s)) != cudaSuccess || (e = cudaEventCreate(&R->e0)) != cudaSuccess ||
+        (e = cudaEventCreate(&R->e1)) != cudaSuccess)
+        return bail(rbfail(CVK_ECUDA, std::string("cvk_rowblock_create: ") + cudaGetErrorString(e)));
+
+    cvk::RBArgs& a = R->args;
+    a.A.n = (int)d->n_own;
+    a.A.rp = d_rp;
+    a.A.ci = d_ci;
+    a.A.av = d_av;
+    a.nv = R->nv;
+    a.dinv = d_dinv;
+    a.b = d_b;
+    a.work = d_work;
+    a.part = d_part;
+    a.st = d_st;
+    a.hist = d_hist;
+    a.rep = d_rep;
+    a.send = R->send;
+    a.recv = R->recv;
+    a.nranks = (int)d->n_ranks;
+    a.slot = (int)R->slot;
+    a.send_rows = d_sr;
+    a.n_send = (int)d->n_send;
+    a.max_send = (int)std::max<int64_t>(1, d->max_send);
+    a.halo_src = d_hs;
+    a.n_halo = (int)d->n_halo;
+    *out = R;
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_exchange(cvk_rowblock* R, double** send, double** recv, int64_t* slot) {
+    if (!R) return rbfail(CVK_EINVAL, "cvk_rowblock_exchange: null block");
+    if (send) *send = R->send;
+    if (recv) *recv = R->recv;
+    if (slot) *slot = R->slot;
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_local(cvk_rowblock* R, int ph) {
+    if (!R) return rbfail(CVK_EINVAL, "cvk_rowblock_local: null block");
+    void* args[2] = {&R->args, &ph};
+    const void* f = nullptr;
+    switch (ph) {
+        case CVK_RB_INIT:
+            R->t_wall0 = wall_now();
+            R->launches = 0;
+            RK(cudaEventRecord(R->e0, R->s));
+            f = (const void*)cvk::k_rb_init;
+            break;
+        case CVK_RB_A: f = (const void*)cvk::k_rb_a; break;
+        case CVK_RB_B: f = (const void*)cvk::k_rb_b; break;
+        case CVK_RB_C: f = (const void*)cvk::k_rb_c; break;
+        case CVK_RB_X: break;
+        case CVK_RB_T: f = (const void*)cvk::k_rb_t; break;
+        default: return rbfail(CVK_EINVAL, "cvk_rowblock_local: unknown phase " + std::to_string(ph));
+    }
+    if (f) {
+        RK(rb_launch(f, R->G, R->s, args));
+        R->launches++;
+    }
+    if (ph == CVK_RB_INIT || ph == CVK_RB_A || ph == CVK_RB_C || ph == CVK_RB_X) {
+        if (R->args.n_send > 0) {
+            RK(rb_launch((const void*)cvk::k_rb_pack, R->Gx, R->s, args));
+            R->launches++;
+        }
+    }
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_post(cvk_rowblock* R, int ph) {
+    if (!R) return rbfail(CVK_EINVAL, "cvk_rowblock_post: null block");
+    if (ph < CVK_RB_INIT || ph > CVK_RB_T) return rbfail(CVK_EINVAL, "cvk_rowblock_post: unknown phase " + std::to_string(ph));
+    void* args[2] = {&R->args, &ph};
+    RK(rb_launch((const void*)cvk::k_rb_post, R->Gx, R->s, args));
+    R->launches++;
+    if (ph == CVK_RB_T) RK(cudaEventRecord(R->e1, R->s));
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_exchange_local(cvk_rowblock* const* rbs, int n) {
+    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_exchange_local: no blocks");
+    for (int q = 0; q < n; ++q)
+        if (!rbs[q] || rbs[q]->args.nranks != n || rbs[q]->slot != rbs[0]->slot || rbs[q]->s != rbs[0]->s)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_exchange_local: blocks disagree on ranks / slot / stream");
+    const size_t bytes = sizeof(double) * rbs[0]->slot;
+    for (int dst = 0; dst < n; ++dst)
+        for (int q = 0; q < n; ++q)
+            RK(cudaMemcpyAsync(rbs[dst]->recv + (size_t)q * rbs[0]->slot, rbs[q]->send, bytes, cudaMemcpyDeviceToDevice,
+                               rbs[0]->s));
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_done(cvk_rowblock* R, int* done) {
+    if (!R || !done) return rbfail(CVK_EINVAL, "cvk_rowblock_done: null argument");
+    int v = 0;
+    RK(cudaMemcpyAsync(&v, &R->args.st->done, sizeof(int), cudaMemcpyDeviceToHost, R->s));
+    RK(cudaStreamSynchronize(R->s));
+    *done = v;
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
+    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: no blocks");
+    auto phase = [&](int ph) -> int {
+        int e;
+        for (int q = 0; q < n; ++q)
+            if ((e = cvk_rowblock_local(rbs[q], ph)) != CVK_OK) return e;
+        if ((e = cvk_rowblock_exchange_local(rbs, n)) != CVK_OK) return e;
+        for (int q = 0; q < n; ++q)
+            if ((e = cvk_rowblock_post(rbs[q], ph)) != CVK_OK) return e;
+        return CVK_OK;
+    };
+    int e;
+    if ((e = phase(CVK_RB_INIT)) != CVK_OK) return e;
+    for (;;) {
+        int done = 0;
+        if ((e = cvk_rowblock_done(rbs[0], &done)) != CVK_OK) return e;
+        if (done) break;
+        for (int k = 0; k < 8; ++k)
+            for (int ph : {CVK_RB_A, CVK_RB_B, CVK_RB_C})
+                if ((e = phase(ph)) != CVK_OK) return e;
+    }
+    if ((e = phase(CVK_RB_X)) != CVK_OK) return e;
+    return phase(CVK_RB_T);
+}
+
+extern "C" int cvk_rowblock_result(cvk_rowblock* R, double* x_own, cvk_report* rep) {
+    if (!R) return rbfail(CVK_EINVAL, "cvk_rowblock_result: null block");
+    cvk::DevReport dr;
+    RK(cudaMemcpyAsync(&dr, R->args.rep, sizeof(dr), cudaMemcpyDeviceToHost, R->s));
+    if (x_own && R->n_own > 0)
+        RK(cudaMemcpyAsync(x_own, R->args.work, sizeof(double2) * R->n_own, cudaMemcpyDeviceToHost, R->s));
+    RK(cudaStreamSynchronize(R->s));
+    if (rep) {
+        rep->converged = dr.converged;
+        rep->breakdown = dr.breakdown;
+        rep->iterations = dr.iterations;
+        rep->final_relres = dr.final_relres;
+        rep->true_relres = dr.true_relres;
+        rep->history_len = dr.history_len;
+        if (rep->history && rep->history_cap > 0 && R->hist_cap > 0) {
+            const int64_t k = std::min<int64_t>(std::min<int64_t>(rep->history_cap, dr.history_len), R->hist_cap);
+            if (k > 0) RK(cudaMemcpy(rep->history, R->args.hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+        }
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, R->e0, R->e1) == cudaSuccess) rep->device_time_s = ms * 1e-3;
+        else cudaGetLastError();
+        rep->wall_time_s = wall_now() - R->t_wall0;
+        rep->kernel_launches = R->launches;
+    }
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_destroy(cvk_rowblock* R) {
+    if (R) {
+        cudaStreamSynchronize(R->s);
+        delete R;
+    }
+    return CVK_OK;
+}

@@ -1,0 +1,347 @@
+"""Row-block global Krylov: the global BiCGSTAB solve with the rows split over
+ranks (SURVEY.md 8(e) mode 1).  Beyond the reference, whose solve()
+(krylov.hpp:68-69, krylov.cpp:57-138) runs in one address space; the
+iterates are bitwise those of a single-device FAST solve for any number of
+blocks.
+
+Each rank owns a contiguous block of rows [r0, r1) (nnz-balanced by
+default).  Its local columns are its own rows first, then a halo: the
+sorted rows of other ranks that its rows reference.  Per reduction phase of
+BiCGSTAB there is one all-gather of a small exchange slot per rank carrying
+the rank's double-double partial sums and the boundary values other ranks
+read (r after the x/r update, p and v after the first SpMV phase); every
+rank then folds the partials in rank order and runs the same scalar
+recurrence (csrc/cvk_rowblock.cu).
+
+Three ways to run the blocks:
+  * solve_row_blocks     -- n blocks on one device, the all-gather done by
+                            stream-ordered device copies (one C call);
+  * solve_distributed    -- one block per rank of a torch.distributed group;
+                            NCCL all-gathers on the library's stream (no host
+                            round trip per phase), gloo staged through host;
+  * RowBlockEngine       -- the per-rank engine both use; tests plug a numpy
+                            engine into solve_distributed to run the N>1
+                            host logic on CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _lib
+from .cavac import (CsrMatrix, Device, InvalidArgument, Preconditioner, SolveReport, SolveResult, SolverId,
+                    SolverOptions, _BRK, _cvec)
+
+P = C.c_void_p
+PH_INIT, PH_A, PH_B, PH_C, PH_X, PH_T = range(6)
+ITER_PHASES = (PH_A, PH_B, PH_C)
+ITERS_PER_POLL = 8  # iterations queued between reads of the device stop flag
+
+
+class CvkRowblockDesc(C.Structure):
+    _fields_ = [("n_own", C.c_int64), ("n_halo", C.c_int64), ("nnz", C.c_int64),
+                ("row_offsets", P), ("col_local", P), ("values", P), ("inv_diag", P), ("b", P),
+                ("n_send", C.c_int64), ("send_rows", P), ("n_ranks", C.c_int64), ("max_send", C.c_int64),
+                ("halo_src", P), ("history_cap", C.c_int64)]
+
+
+def _bind(L):
+    if getattr(L, "_rb_bound", False):
+        return
+    i32, i64 = C.c_int, C.c_int64
+    L.cvk_rowblock_create.argtypes = [P, C.POINTER(CvkRowblockDesc), i32, C.POINTER(_lib.CvkOpts), C.POINTER(P)]
+    L.cvk_rowblock_exchange.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(i64)]
+    L.cvk_rowblock_local.argtypes = [P, i32]
+    L.cvk_rowblock_post.argtypes = [P, i32]
+    L.cvk_rowblock_exchange_local.argtypes = [C.POINTER(P), i32]
+    L.cvk_rowblock_solve_local.argtypes = [C.POINTER(P), i32]
+    L.cvk_rowblock_done.argtypes = [P, C.POINTER(i32)]
+    L.cvk_rowblock_result.argtypes = [P, P, C.POINTER(_lib.CvkReport)]
+    L.cvk_rowblock_destroy.argtypes = [P]
+    for f in ("create", "exchange", "local", "post", "exchange_local", "solve_local", "done", "result", "destroy"):
+        getattr(L, "cvk_rowblock_" + f).restype = i32
+    L._rb_bound = True
+
+
+# ------------------------------------------------------------------ plan --
+
+@dataclass
+class RowBlockPlan:
+    """One rank's block of the global system."""
+    rank: int
+    n_ranks: int
+    r0: int
+    r1: int
+    row_offsets: np.ndarray   # int64 [n_own + 1], from 0
+    col_local: np.ndarray     # int64 [nnz]: own rows 0..n_own-1, halo n_own + h
+    values: np.ndarray        # complex128 [nnz]
+    halo_cols: np.ndarray     # int64 [n_halo]: global rows of the halo entries (sorted)
+    send_rows: np.ndarray     # int64 [n_send]: local rows other ranks read (sorted)
+    max_send: int
+    halo_src: np.ndarray      # int64 [n_halo]: owner * max_send + position in the owner's send list
+
+    @property
+    def n_own(self) -> int:
+        return self.r1 - self.r0
+
+
+def row_bounds(A: CsrMatrix, n_ranks: int, balance: str = "nnz") -> np.ndarray:
+    """Contiguous row blocks: equal rows, or (default) equal nonzeros."""
+    n = A.nrows
+    if n_ranks < 1:
+        raise InvalidArgument("row blocks: need at least one rank")
+    if balance == "rows":
+        return np.array([(q * n) // n_ranks for q in range(n_ranks + 1)], np.int64)
+    if balance != "nnz":
+        raise InvalidArgument(f'row blocks: unknown balance "{balance}" (allowed: nnz, rows)')
+    rp = np.asarray(A.row_offsets, np.int64)
+    targets = (np.arange(n_ranks + 1, dtype=np.float64) * rp[-1]) / n_ranks
+    b = np.searchsorted(rp, targets, side="left").astype(np.int64)
+    b[0], b[-1] = 0, n
+    return np.maximum.accumulate(np.minimum(b, n))
+
+
+def plan_row_blocks(A: CsrMatrix, n_ranks: int, bounds: Optional[np.ndarray] = None) -> List[RowBlockPlan]:
+    """Every rank's block, halo and exchange lists (all ranks compute the
+    same plan from the global pattern)."""
+    if A.nrows != A.ncols:
+        raise InvalidArgument("row blocks: matrix must be square")
+    bounds = row_bounds(A, n_ranks) if bounds is None else np.asarray(bounds, np.int64)
+    if len(bounds) != n_ranks + 1 or bounds[0] != 0 or bounds[-1] != A.nrows or np.any(np.diff(bounds) < 0):
+        raise InvalidArgument("row blocks: bounds must run 0 .. n, non-decreasing")
+    rp = np.asarray(A.row_offsets, np.int64)
+    ci = np.asarray(A.col_indices, np.int64)
+    vals = np.asarray(A.values, np.complex128)
+    halos, cols = [], []
+    for q in range(n_ranks):
+        r0, r1 = int(bounds[q]), int(bounds[q + 1])
+        c = ci[rp[r0]:rp[r1]]
+        ext = (c < r0) | (c >= r1)
+        halo = np.unique(c[ext])
+        loc = c - r0
+        loc[ext] = (r1 - r0) + np.searchsorted(halo, c[ext])
+        halos.append(halo)
+        cols.append(loc)
+    owner_of = lambda g: np.searchsorted(bounds, g, side="right") - 1  # noqa: E731
+    needed = [[] for _ in range(n_ranks)]
+    for q in range(n_ranks):
+        own = owner_of(halos[q])
+        for o in np.unique(own):
+            needed[int(o)].append(halos[q][own == o])
+    sends = [np.unique(np.concatenate(v)) - bounds[o] if v else np.zeros(0, np.int64)
+             for o, v in enumerate(needed)]
+    max_send = max([len(s) for s in sends] + [0])
+    plans = []
+    for q in range(n_ranks):
+        r0, r1 = int(bounds[q]), int(bounds[q + 1])
+        own = owner_of(halos[q])
+        src = np.zeros(len(halos[q]), np.int64)
+        for o in np.unique(own):
+            m = own == o
+            src[m] = int(o) * max_send + np.searchsorted(sends[int(o)], halos[q][m] - bounds[o])
+        plans.append(RowBlockPlan(q, n_ranks, r0, r1, rp[r0:r1 + 1] - rp[r0], cols[q], vals[rp[r0]:rp[r1]],
+                                  halos[q], sends[q].astype(np.int64), max_send, src))
+    return plans
+
+
+# --------------------------------------------------------------- engines --
+
+class RowBlockEngine:
+    """One block on one device (cvk_rowblock_*, csrc/cvk_rowblock.cu)."""
+
+    def __init__(self, plan: RowBlockPlan, b_own: np.ndarray, inv_diag_own: Optional[np.ndarray],
+                 opts: SolverOptions, dev: Optional[Device] = None):
+        L = _lib.load()
+        _bind(L)
+        self.L, self.plan = L, plan
+        self.dev = dev or Device.default()
+        self._keep = [np.ascontiguousarray(a) for a in
+                      (plan.row_offsets, plan.col_local, plan.values, plan.send_rows, plan.halo_src)]
+        self._b = _cvec(b_own)
+        self._d = None if inv_diag_own is None else _cvec(inv_diag_own)
+        self.hist_cap = 2 * opts.max_iter + 8 if opts.record_history else 0
+        p = lambda a: None if a is None else a.ctypes.data_as(P)  # noqa: E731
+        rp, ci, av, sr, hs = self._keep
+        d = CvkRowblockDesc(plan.n_own, len(plan.halo_cols), len(ci), p(rp), p(ci), p(av), p(self._d), p(self._b),
+                            len(sr), p(sr), plan.n_ranks, plan.max_send, p(hs), self.hist_cap)
+        o = _lib.CvkOpts(float(opts.tol), int(opts.max_iter), int(opts.l), int(opts.m),
+                         1 if opts.record_history else 0, _lib.MODE_FAST)
+        h = P()
+        code = L.cvk_rowblock_create(self.dev.handle, C.byref(d), int(SolverId.BiCGStab), C.byref(o), C.byref(h))
+        if code in (-1, -6):
+            raise InvalidArgument(_lib.last_error())
+        _lib.check(code)
+        self.h = h
+        s, r, n = P(), P(), C.c_int64()
+        _lib.check(L.cvk_rowblock_exchange(h, C.byref(s), C.byref(r), C.byref(n)))
+        self.send_ptr, self.recv_ptr, self.slot = s.value, r.value, n.value
+        self.stream = L.cvk_ctx_stream(self.dev.handle)
+
+    def local(self, ph: int) -> None:
+        _lib.check(self.L.cvk_rowblock_local(self.h, ph))
+
+    def post(self, ph: int) -> None:
+        _lib.check(self.L.cvk_rowblock_post(self.h, ph))
+
+    def done(self) -> bool:
+        v = C.c_int()
+        _lib.check(self.L.cvk_rowblock_done(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def result(self):
+        x = np.zeros(self.plan.n_own, np.complex128)
+        rep = _lib.CvkReport()
+        hist = None
+        if self.hist_cap:
+            hist = np.zeros(self.hist_cap, np.float64)
+            rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+            rep.history_cap = len(hist)
+        _lib.check(self.L.cvk_rowblock_result(self.h, x.ctypes.data_as(P), C.byref(rep)))
+        return x, _report(rep, hist)
+
+    # exchange buffers as torch tensors over the library's device memory
+    def tensors(self):
+        import torch
+
+        class _Cai:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3}
+        dev = torch.device("cuda", self.dev.index)
+        send = torch.as_tensor(_Cai(self.send_ptr, self.slot), device=dev)
+        recv = torch.as_tensor(_Cai(self.recv_ptr, self.slot * self.plan.n_ranks), device=dev)
+        return send, recv
+
+    def close(self):
+        if self.h:
+            self.L.cvk_rowblock_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _report(r, hist) -> SolveReport:
+    h = [] if hist is None else list(hist[: min(r.history_len, len(hist))])
+    return SolveReport(bool(r.converged), int(r.iterations), r.final_relres, r.true_relres, r.wall_time_s, h,
+                       _BRK.get(r.breakdown, "unknown breakdown"), r.device_time_s, int(r.kernel_launches))
+
+
+def _check_system(A: CsrMatrix, b, M: Preconditioner):
+    b = _cvec(b)
+    if A.nrows != A.ncols or A.nrows != len(b):
+        raise InvalidArgument("bicgstab: dimension mismatch")
+    d = None
+    if M is not None and M.kind != "identity":
+        d = _cvec(M.inv_diag)
+        if len(d) != A.nrows:
+            raise InvalidArgument("preconditioner: dimension mismatch")
+    return b, d
+
+
+def solve_row_blocks(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, n_blocks: int = 2,
+                     bounds: Optional[np.ndarray] = None, dev: Optional[Device] = None) -> SolveResult:
+    """BiCGSTAB over n_blocks row blocks on one device: every block runs the
+    multi-rank kernels, the all-gather is a device copy (same stream)."""
+    opts = opts or SolverOptions()
+    b, d = _check_system(A, b, M)
+    plans = plan_row_blocks(A, n_blocks, bounds)
+    engines = [RowBlockEngine(pl, b[pl.r0:pl.r1], None if d is None else d[pl.r0:pl.r1], opts, dev) for pl in plans]
+    try:
+        L = engines[0].L
+        arr = (P * n_blocks)(*[e.h for e in engines])
+        _lib.check(L.cvk_rowblock_solve_local(arr, n_blocks))
+        xs, reps = zip(*[e.result() for e in engines])
+    finally:
+        for e in engines:
+            e.close()
+    rep = reps[0]
+    rep.kernel_launches = sum(r.kernel_launches for r in reps)
+    return SolveResult(np.concatenate(xs) if xs else np.zeros(0, np.complex128), rep)
+
+
+# ---------------------------------------------------------- distributed --
+
+class _Exchange:
+    """The per-phase all-gather of the ranks' exchange slots."""
+
+    def __init__(self, engine, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.engine = engine
+        self.backend = dist.get_backend(group)
+        if isinstance(engine, RowBlockEngine):
+            self.send, self.recv = engine.tensors()
+            self.stream = torch.cuda.ExternalStream(engine.stream, device=self.send.device)
+        else:  # host engine: numpy buffers shared with CPU tensors
+            self.send, self.recv = torch.from_numpy(engine.send), torch.from_numpy(engine.recv)
+            self.stream = None
+
+    def __call__(self) -> None:
+        torch, dist = self.torch, self.dist
+        if self.stream is not None and self.backend == "nccl":
+            # NCCL orders itself after the library's stream and the stream after it
+            with torch.cuda.stream(self.stream):
+                dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            return
+        if self.stream is not None:  # gloo with device buffers: stage through host
+            with torch.cuda.stream(self.stream):
+                host = self.send.cpu()
+            parts = [torch.empty_like(host) for _ in range(dist.get_world_size(self.group))]
+            dist.all_gather(parts, host, group=self.group)
+            with torch.cuda.stream(self.stream):
+                self.recv.copy_(torch.cat(parts))
+            return
+        parts = [torch.empty_like(self.send) for _ in range(dist.get_world_size(self.group))]
+        dist.all_gather(parts, self.send, group=self.group)
+        self.recv.copy_(torch.cat(parts))
+
+
+EngineFactory = Callable[[RowBlockPlan, np.ndarray, Optional[np.ndarray], SolverOptions], object]
+
+
+def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, group=None,
+                      bounds: Optional[np.ndarray] = None, engine_factory: Optional[EngineFactory] = None,
+                      gather_solution: bool = True) -> SolveResult:
+    """BiCGSTAB (krylov.cpp:57-138) with one row block per rank of a
+    torch.distributed group (initialised by the caller; NCCL for device
+    engines, gloo staged through host).  Every rank returns the same report;
+    x is the full solution (gather_solution) or the rank's own rows."""
+    import torch.distributed as dist
+    opts = opts or SolverOptions()
+    b, d = _check_system(A, b, M)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    plan = plan_row_blocks(A, world, bounds)[rank]
+    factory = engine_factory or (lambda pl, bo, do, o: RowBlockEngine(pl, bo, do, o))
+    eng = factory(plan, b[plan.r0:plan.r1], None if d is None else d[plan.r0:plan.r1], opts)
+    try:
+        xchg = _Exchange(eng, group)
+
+        def phase(ph):
+            eng.local(ph)
+            xchg()
+            eng.post(ph)
+
+        phase(PH_INIT)
+        while not eng.done():
+            for _ in range(ITERS_PER_POLL):
+                for ph in ITER_PHASES:
+                    phase(ph)
+        phase(PH_X)
+        phase(PH_T)
+        x_own, rep = eng.result()
+    finally:
+        if hasattr(eng, "close"):
+            eng.close()
+    if not gather_solution:
+        return SolveResult(x_own, rep)
+    parts = [None] * world
+    dist.all_gather_object(parts, x_own, group=group)
+    return SolveResult(np.concatenate(parts), rep)

@@ -1,0 +1,128 @@
+"""Row-block global BiCGSTAB on the device (csrc/cvk_rowblock.cu, SURVEY.md
+8(e) mode 1): n row blocks on one device, and two processes sharing the
+device over gloo, must reproduce the single-device FAST solve bit for bit
+(solution, iteration count, residual history) -- the reductions are
+double-double and every per-row / per-element rounding is the same."""
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.complex128).view(np.uint64)
+
+
+def cavity(h, f=60.0, adm=0.01 + 0j):
+    from paper_2112_00087_b200 import helmholtz as H
+    g = H.build_grid(2.4, 1.2, h, 0.4, 0.65, adm)
+    d = np.array([1.0 + 0.05 * i + 0.2j for i in range(g.roof_size())])
+    p = H.assemble(g, 2 * np.pi * f, 340.0, d)
+    return p.A, np.asarray(p.b, np.complex128)
+
+
+def _same(a, b):
+    assert a.report.converged == b.report.converged
+    assert a.report.iterations == b.report.iterations
+    assert a.report.breakdown == b.report.breakdown
+    assert np.array_equal(bits(a.x), bits(b.x))
+    assert a.report.residual_history == b.report.residual_history
+    assert a.report.final_relres == b.report.final_relres
+
+
+@pytest.mark.parametrize("h", [0.05, 0.0075, 0.004])
+@pytest.mark.parametrize("n_blocks", [1, 2, 3, 5])
+def test_row_blocks_bitwise_single_device(cvk, h, n_blocks):
+    """50k- and 180k-DOF cavities (the latter on the streamed phase kernels
+    single-device) and the golden-size system."""
+    from paper_2112_00087_b200.rowblock import solve_row_blocks
+    P = cvk
+    A, b = cavity(h)
+    M = P.jacobi(A)
+    o = P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, M, o)
+    got = solve_row_blocks(A, b, M, o, n_blocks=n_blocks)
+    assert ref.report.converged
+    _same(got, ref)
+    assert got.report.true_relres == pytest.approx(ref.report.true_relres, rel=1e-12)
+    assert got.report.kernel_launches > 0 and got.report.device_time > 0
+
+
+def test_row_blocks_edge_cases(cvk):
+    from paper_2112_00087_b200.rowblock import solve_row_blocks
+    P = cvk
+    A, b = cavity(0.05)
+    M = P.jacobi(A)
+    # identity preconditioner, rows-balanced bounds with an empty block
+    I = P.identity_preconditioner()
+    o = P.SolverOptions(tol=1e-8, record_history=True)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, I, o)
+    bounds = np.array([0, 0, 400, A.nrows], np.int64)
+    _same(solve_row_blocks(A, b, I, o, n_blocks=3, bounds=bounds), ref)
+    # zero rhs: converged in 0 iterations, true relres left at 0
+    z = solve_row_blocks(A, np.zeros_like(b), M, P.SolverOptions(), n_blocks=2)
+    assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
+    assert not np.any(z.x)
+    # max_iter exhausted: not converged, iterations = max_iter
+    e = solve_row_blocks(A, b, M, P.SolverOptions(max_iter=3), n_blocks=2)
+    r = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(max_iter=3))
+    assert not e.report.converged and e.report.iterations == 3
+    assert np.array_equal(bits(e.x), bits(r.x))
+    with pytest.raises(P.InvalidArgument):
+        solve_row_blocks(A, b[:-1], M, n_blocks=2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q, h):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2112_00087_b200 as P
+        from paper_2112_00087_b200.rowblock import solve_distributed
+        A, b = cavity(h)
+        M = P.jacobi(A)
+        r = solve_distributed(A, b, M, P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000))
+        q.put((rank, r.x, r.report.iterations, list(r.report.residual_history), r.report.converged))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_two_processes_one_device(cvk):
+    """The multi-process path (RowBlockEngine + torch.distributed exchange,
+    gloo staged through host) with both ranks on device 0."""
+    import multiprocessing as mp
+    P = cvk
+    h = 0.0075
+    A, b = cavity(h)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True,
+                                                                           max_iter=20000))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, h)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, x, it, hist, conv in outs:
+        assert conv and it == ref.report.iterations
+        assert hist == ref.report.residual_history
+        assert np.array_equal(bits(x), bits(ref.x)), rank
+    assert math.isfinite(ref.report.true_relres)

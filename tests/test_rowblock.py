@@ -1,0 +1,150 @@
+"""Row-block global BiCGSTAB host logic (rowblock.py, SURVEY.md 8(e) mode 1)
+on CPU: the block plan / halo / exchange lists, and solve_distributed on 2
+and 3 gloo ranks with the numpy engine (tests/rowblock_numpy_engine.py),
+which must reproduce the one-block run bit for bit -- solution, iteration
+count and residual history -- and the oracle's solution."""
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _system(h=0.1, f=60.0, adm=0.01 + 0j):
+    from paper_2112_00087_b200 import helmholtz as H
+    g = H.build_grid(2.4, 1.2, h, 0.4, 0.65, adm)
+    d = np.array([1.0 + 0.05 * i + 0.2j for i in range(g.roof_size())])
+    p = H.assemble(g, 2 * np.pi * f, 340.0, d)
+    return p.A, np.asarray(p.b, np.complex128)
+
+
+def _inv_diag(A):
+    from paper_2112_00087_b200.helmholtz import cdiv
+    rp, ci, v = A.row_offsets, A.col_indices, A.values
+    out = np.zeros(A.nrows, np.complex128)
+    for i in range(A.nrows):
+        k = rp[i] + int(np.nonzero(ci[rp[i]:rp[i + 1]] == i)[0][0])
+        out[i] = cdiv(1 + 0j, complex(v[k]))
+    return out
+
+
+def _random_csr(n, seed, per_row=6):
+    from paper_2112_00087_b200.cavac import CsrMatrix
+    rng = np.random.default_rng(seed)
+    rp, ci = [0], []
+    for i in range(n):
+        cols = np.unique(np.concatenate([[i], rng.integers(0, n, per_row)]))
+        ci.extend(cols)
+        rp.append(len(ci))
+    v = rng.standard_normal(len(ci)) + 1j * rng.standard_normal(len(ci))
+    return CsrMatrix(n, n, np.array(rp, np.uint64), np.array(ci, np.uint64), v)
+
+
+@pytest.mark.parametrize("n_ranks,balance", [(1, "nnz"), (2, "nnz"), (3, "rows"), (5, "nnz")])
+def test_plan_halo_reproduces_global_spmv(n_ranks, balance):
+    """Each block's local SpMV over [own | halo] equals the global SpMV rows:
+    the halo of every block is filled from the owners' send lists exactly as
+    the exchange slot layout maps it (halo_src = owner * max_send + k)."""
+    from paper_2112_00087_b200.rowblock import plan_row_blocks, row_bounds
+    A = _random_csr(97, 5)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(A.nrows) + 1j * rng.standard_normal(A.nrows)
+    rp, ci, v = (np.asarray(a) for a in (A.row_offsets, A.col_indices, A.values))
+    ref = np.array([np.sum(v[rp[i]:rp[i + 1]] * x[ci[rp[i]:rp[i + 1]].astype(np.int64)]) for i in range(A.nrows)])
+    bounds = row_bounds(A, n_ranks, balance)
+    plans = plan_row_blocks(A, n_ranks, bounds)
+    ms = plans[0].max_send
+    slots = np.zeros((n_ranks, max(1, ms)), np.complex128)
+    for pl in plans:
+        assert pl.max_send == ms and len(pl.send_rows) <= ms
+        assert np.all(np.diff(pl.send_rows) > 0)
+        slots[pl.rank, :len(pl.send_rows)] = x[pl.r0 + pl.send_rows]
+    y = np.zeros(A.nrows, np.complex128)
+    for pl in plans:
+        q, k = np.divmod(pl.halo_src, max(1, ms))
+        xl = np.concatenate([x[pl.r0:pl.r1], slots[q, k]])
+        assert np.array_equal(xl[pl.n_own:], x[pl.halo_cols])
+        for i in range(pl.n_own):
+            a, b = pl.row_offsets[i], pl.row_offsets[i + 1]
+            y[pl.r0 + i] = np.sum(pl.values[a:b] * xl[pl.col_local[a:b]])
+    assert np.array_equal(y, ref)
+    assert sum(pl.n_own for pl in plans) == A.nrows
+    if balance == "nnz" and n_ranks > 1:
+        nnz = [pl.row_offsets[-1] for pl in plans]
+        assert max(nnz) - min(nnz) <= 2 * 7
+
+
+def test_plan_rejects_bad_bounds():
+    from paper_2112_00087_b200.cavac import InvalidArgument
+    from paper_2112_00087_b200.rowblock import plan_row_blocks, row_bounds
+    A = _random_csr(20, 2)
+    with pytest.raises(InvalidArgument):
+        plan_row_blocks(A, 2, np.array([0, 15, 10]))
+    with pytest.raises(InvalidArgument):
+        row_bounds(A, 0)
+    with pytest.raises(InvalidArgument):
+        row_bounds(A, 2, "cols")
+
+
+def _worker(rank, world, port, q, kw):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from rowblock_numpy_engine import NumpyRowBlockEngine
+        from paper_2112_00087_b200.cavac import Preconditioner, SolverOptions
+        from paper_2112_00087_b200.rowblock import solve_distributed
+        A, b = _system(**kw)
+        M = Preconditioner("jacobi", _inv_diag(A))
+        r = solve_distributed(A, b, M, SolverOptions(tol=1e-10, record_history=True),
+                              engine_factory=NumpyRowBlockEngine)
+        q.put((rank, r.x, r.report.iterations, list(r.report.residual_history), r.report.converged,
+               r.report.true_relres))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_rowblock_matches_one_block(world, oracle):
+    import multiprocessing as mp
+    from rowblock_numpy_engine import run_serial
+    from paper_2112_00087_b200.cavac import SolverOptions
+    kw = dict(h=0.1, f=60.0)
+    A, b = _system(**kw)
+    x1, rep1 = run_serial(A, b, _inv_diag(A), SolverOptions(tol=1e-10, record_history=True))
+    assert rep1.converged
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kw)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, x, it, hist, conv, trr in outs:
+        assert conv and it == rep1.iterations, (rank, it, rep1.iterations)
+        assert np.array_equal(np.asarray(hist).view(np.uint64), np.asarray(rep1.residual_history).view(np.uint64))
+        assert np.array_equal(x.view(np.uint64), x1.view(np.uint64)), rank
+        assert trr == rep1.true_relres
+    # the reference algorithm (sequential sums) on the same system: same solution
+    rp, ci, v = A.row_offsets.astype(np.int64), A.col_indices.astype(np.int64), np.asarray(A.values)
+    xo, ro = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-10)
+    assert abs(ro.iterations - rep1.iterations) <= max(2, 0.15 * ro.iterations)
+    assert np.linalg.norm(x1 - xo) <= 1e-7 * np.linalg.norm(xo)
+    assert math.isfinite(rep1.true_relres) and rep1.true_relres < 1e-8
