@@ -37,6 +37,7 @@
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 #include "cvk_phased.h"
+#include "cvk_stream.cuh"
 
 namespace cvk {
 namespace {
@@ -61,6 +62,9 @@ struct RBArgs {
     int n_send, max_send;
     const int* halo_src;
     int n_halo;
+    int capk;            // streamed SpMV phases: chunk nnz capacity, ring depths, L2 prefetch window
+    int nst[2];
+    int pf_rows;
 };
 
 enum { VX = 0, VR, VSH, VS, VT, VP0, VP1, VV0, VV1, kRbVecs };
@@ -73,7 +77,7 @@ __device__ __forceinline__ void pdl_wait() {
 }
 
 // CTA partials -> the rank's double-double totals in send[0 .. 4K) (last CTA)
-template <int K>
+template <int K, int NT = kThreads>
 __device__ void rank_total(const CAcc (&acc)[K], const RBArgs& a, unsigned* counter) {
     __shared__ CAcc sm[K][32];
     __shared__ int s_last;
@@ -81,7 +85,7 @@ __device__ void rank_total(const CAcc (&acc)[K], const RBArgs& a, unsigned* coun
     CAcc v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = acc[k];
-    cta_sum_k<K, kThreads>(v, sm);
+    cta_sum_k<K, NT>(v, sm);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) cacc_store(a.part, k, G, blockIdx.x, v[k]);
@@ -95,11 +99,11 @@ __device__ void rank_total(const CAcc (&acc)[K], const RBArgs& a, unsigned* coun
 #pragma unroll
     for (int k = 0; k < K; ++k) s[k] = CAcc{};
 #pragma unroll 1
-    for (int q = threadIdx.x; q < G; q += kThreads) {
+    for (int q = threadIdx.x; q < G; q += NT) {
 #pragma unroll
         for (int k = 0; k < K; ++k) cacc_add(s[k], cacc_load(a.part, k, G, q));
     }
-    cta_sum_k<K, kThreads>(s, sm);
+    cta_sum_k<K, NT>(s, sm);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -225,8 +229,93 @@ __global__ void __launch_bounds__(kThreads) k_rb_b(RBArgs a) {
     rank_total<3>(acc, a, &st->counter[2]);
 }
 
-// x += omega s; r = s - omega t; ||r||, <shadow, r>
-__global__ void __launch_bounds__(kThreads) k_rb_c(RBArgs a) {
+// ---- streamed (TMA ring) SpMV phases: cvk_phased.cu k_bi_a_s / k_bi_b_s
+// with the rank's totals instead of the scalar logic
+
+__global__ void __launch_bounds__(kStreamThreads, 1) k_rb_a_s(RBArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_wait();
+    PState* st = a.st;
+    if (st->done) return;
+    const int cur = st->cur;
+    const bool first = st->first != 0;
+    const double2 beta = st->beta, nom = cvk_neg(st->omega);
+    const double2* __restrict__ r = vec(a, VR);
+    const double2* __restrict__ pc = vec(a, cur ? VP1 : VP0);
+    const double2* __restrict__ vc = vec(a, cur ? VV1 : VV0);
+    double2* __restrict__ pn = vec(a, cur ? VP0 : VP1);
+    double2* __restrict__ vn = vec(a, cur ? VV0 : VV1);
+    const double2* vecs[5] = {r, pc, vc, vec(a, VSH), a.dinv};
+    StreamLayout L{a.capk, 5, a.nst[0], 0};
+    L.ngather = 3;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[1] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds p_new (pre)
+            const double2 rc = ch.v(0, l);
+            if (first || l < kStreamRows) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
+        };
+        auto xg = [&](int c) -> double2 {
+            const double2 rc = r[c];
+            if (first) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+        };
+        const double2 y = chunk_row_sum<kRbBatch>(ch, t, xs, xg);
+        const double2 vi = a.dinv ? cvk_mul(ch.v(4, t), y) : y;
+        const int row = ch.r0 + t;
+        pn[row] = xs(t);
+        vn[row] = vi;
+        acc_dot(acc[0], ch.v(3, t), vi);
+    }, nullptr, nullptr, [&](int t, const Chunk& ch) {
+        if (!first)
+            ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
+    });
+    rank_total<1, kStreamThreads>(acc, a, &st->counter[1]);
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 1) k_rb_b_s(RBArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_wait();
+    PState* st = a.st;
+    if (st->done) return;
+    const int cur = st->cur;
+    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
+    const double2* __restrict__ r = vec(a, VR);
+    const double2* __restrict__ pn = vec(a, cur ? VP0 : VP1);
+    const double2* __restrict__ vn = vec(a, cur ? VV0 : VV1);
+    double2* __restrict__ s = vec(a, VS);
+    double2* __restrict__ t_ = vec(a, VT);
+    double2* __restrict__ x = vec(a, VX);
+    const double2* vecs[5] = {r, vn, a.dinv, pn, x};
+    StreamLayout L{a.capk, 5, a.nst[1], 0};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[3] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds s (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+        };
+        auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+        const double2 y = chunk_row_sum<kRbBatch>(ch, t, xs, xg);
+        const double2 ti = a.dinv ? cvk_mul(ch.v(2, t), y) : y;
+        const double2 si = xs(t);
+        const int row = ch.r0 + t;
+        s[row] = si;
+        t_[row] = ti;
+        x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
+        acc_norm(acc[0], si);
+        acc_dot(acc[1], ti, ti);
+        acc_dot(acc[2], ti, si);
+    }, nullptr, nullptr, [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
+    });
+    rank_total<3, kStreamThreads>(acc, a, &st->counter[2]);
+}
+
+// x += omega s; r = s - omega t; ||r||, <shadow, r> -- small grid, 4 elements
+// per thread per trip with all loads first (cvk_phased.cu k_bi_c)
+__global__ void __launch_bounds__(kThreads) k_rb_c4(RBArgs a) {
     pdl_wait();
     PState* st = a.st;
     if (st->done) return;
@@ -238,14 +327,27 @@ __global__ void __launch_bounds__(kThreads) k_rb_c(RBArgs a) {
     double2* __restrict__ r = vec(a, VR);
     double2* __restrict__ x = vec(a, VX);
     CAcc acc[2] = {};
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        const double2 si = s[i], ti = t[i];
-        x[i] = cvk_add(x[i], cvk_mul(omega, si));
-        const double2 ri = cvk_add(si, cvk_mul(nom, ti));
-        r[i] = ri;
-        acc_norm(acc[0], ri);
-        acc_dot(acc[1], sh[i], ri);
-    });
+    constexpr int U = 4;
+    const long long stride = (long long)gridDim.x * kThreads;
+    for (long long base = (long long)blockIdx.x * kThreads + threadIdx.x; base < n; base += stride * U) {
+        double2 vs[U], vt[U], vh[U], vx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * stride;
+            if (i < n) { vs[u] = s[i]; vt[u] = t[i]; vh[u] = sh[i]; vx[u] = x[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * stride;
+            if (i < n) {
+                x[i] = cvk_add(vx[u], cvk_mul(omega, vs[u]));
+                const double2 ri = cvk_add(vs[u], cvk_mul(nom, vt[u]));
+                r[i] = ri;
+                acc_norm(acc[0], ri);
+                acc_dot(acc[1], vh[u], ri);
+            }
+        }
+    }
     rank_total<2>(acc, a, &st->counter[0]);
 }
 
@@ -398,7 +500,9 @@ struct cvk_rowblock {
     cudaStream_t s = nullptr;
     int nsm = 0;
     int64_t n_own = 0, n_halo = 0, nnz = 0, nv = 0;
-    int G = 1, Gx = 1;  // row/elem phases; pack/post
+    int G = 1, Gx = 1, Ge = 1;  // thread-per-row phases; pack/post; elementwise phase
+    bool streamed = false;
+    size_t smem_a = 0, smem_b = 0;
     std::vector<void*> bufs;
     double* send = nullptr;
     double* recv = nullptr;
@@ -409,6 +513,7 @@ struct cvk_rowblock {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     double t_wall0 = 0.0;
     int solver = CVK_BICGSTAB;
+    long long max_iter = 0;
     ~cvk_rowblock() {
         for (void* p : bufs) cudaFree(p);
         if (e0) cudaEventDestroy(e0);
@@ -441,11 +546,12 @@ double wall_now() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-cudaError_t rb_launch(const void* f, int grid, cudaStream_t s, void** args) {
+cudaError_t rb_launch(const void* f, int grid, cudaStream_t s, void** args, int threads = cvk::kThreads,
+                      size_t smem = 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(cvk::kThreads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -513,19 +619,58 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
     const long long xchunks = std::max<long long>(1, (std::max(d->n_send, d->n_halo) * 2 + cvk::kThreads - 1) / cvk::kThreads);
     R->Gx = (int)std::min<long long>(xchunks, R->nsm);
     R->slot = cvk::kHdr + 4 * std::max<int64_t>(1, d->max_send);
+    R->Ge = (int)std::min<long long>(2LL * R->nsm, std::max<long long>(1, (d->n_own + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
+    // streamed SpMV phases (TMA ring, cvk_stream.cuh) as in the single-device
+    // phase kernels: chunk capacity, each chunk's largest own column (L2
+    // prefetch of the forward band), ring depth from the shared-memory budget
+    const int64_t nch = (d->n_own + cvk::kStreamRows - 1) / cvk::kStreamRows;
+    long long mk = 0;
+    std::vector<int> cm((size_t)std::max<int64_t>(1, nch), -1);
+    for (int64_t q = 0; q < nch; ++q) {
+        const int64_t a0 = q * cvk::kStreamRows, a1 = std::min<int64_t>(a0 + cvk::kStreamRows, d->n_own);
+        mk = std::max<long long>(mk, (long long)(rp[(size_t)a1] - rp[(size_t)a0]));
+        for (int k = rp[(size_t)a0]; k < rp[(size_t)a1]; ++k)
+            if (ci[(size_t)k] < d->n_own) cm[(size_t)q] = std::max(cm[(size_t)q], ci[(size_t)k]);
+    }
+    const int capk = (int)((mk + 3) & ~3LL);
+    int optin = 0, nst[2] = {0, 0};
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int kv[2] = {5, 5}, kg[2] = {3, 2};
+    for (int k = 0; k < 2; ++k) {
+        cvk::StreamLayout L1{capk, kv[k], 1};
+        L1.ngather = kg[k];
+        const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+        nst[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)L1.stage_bytes()));
+    }
+    long long smin = 65536;
+    if (const char* env = std::getenv("CVK_RB_STREAM_MIN")) smin = std::atoll(env);
+    R->streamed = d->nnz > 0 && d->n_own >= smin && std::min(nst[0], nst[1]) >= 2 && !std::getenv("CVK_NO_STREAM");
+    if (R->streamed) {
+        for (int k = 0; k < 2; ++k) {
+            cvk::StreamLayout L{capk, kv[k], nst[k]};
+            L.ngather = kg[k];
+            (k ? R->smem_b : R->smem_a) = L.smem_bytes();
+        }
+        if (cudaFuncSetAttribute((const void*)cvk::k_rb_a_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192) != cudaSuccess ||
+            cudaFuncSetAttribute((const void*)cvk::k_rb_b_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192) != cudaSuccess)
+            return bail(rbfail(CVK_ECUDA, "cvk_rowblock_create: shared-memory opt-in failed"));
+    }
+    const int Gpart = std::max(std::max(R->G, R->Ge), R->nsm);
     R->hist_cap = o->record_history ? std::max<int64_t>(d->history_cap, 0) : 0;
+    R->max_iter = std::max<long long>(0, o->max_iter);
 
-    int *d_rp, *d_ci, *d_sr, *d_hs;
+    int *d_rp, *d_ci, *d_sr, *d_hs, *d_cmax;
     double2 *d_av, *d_dinv = nullptr, *d_b, *d_work, *d_part;
     PState* d_st;
     double* d_hist;
     cvk::DevReport* d_rep;
     cudaError_t e = cudaSuccess;
-    if ((e = R->alloc(&d_rp, rp.size())) != cudaSuccess || (e = R->alloc(&d_ci, ci.size())) != cudaSuccess ||
+    if ((e = R->alloc(&d_rp, rp.size() + 4)) != cudaSuccess || (e = R->alloc(&d_ci, ci.size() + 8)) != cudaSuccess ||
+        (e = R->alloc(&d_cmax, cm.size())) != cudaSuccess ||
         (e = R->alloc(&d_sr, sr.size())) != cudaSuccess || (e = R->alloc(&d_hs, hs.size())) != cudaSuccess ||
         (e = R->alloc(&d_av, (size_t)d->nnz)) != cudaSuccess || (e = R->alloc(&d_b, (size_t)d->n_own)) != cudaSuccess ||
         (e = R->alloc(&d_work, (size_t)cvk::kRbVecs * R->nv)) != cudaSuccess ||
-        (e = R->alloc(&d_part, (size_t)6 * R->G)) != cudaSuccess || (e = R->alloc(&d_st, 1)) != cudaSuccess ||
+        (e = R->alloc(&d_part, (size_t)6 * Gpart)) != cudaSuccess || (e = R->alloc(&d_st, 1)) != cudaSuccess ||
         (e = R->alloc(&d_hist, (size_t)std::max<int64_t>(1, R->hist_cap))) != cudaSuccess ||
         (e = R->alloc(&d_rep, 1)) != cudaSuccess || (e = R->alloc(&R->send, (size_t)R->slot)) != cudaSuccess ||
         (e = R->alloc(&R->recv, (size_t)R->slot * d->n_ranks)) != cudaSuccess ||
@@ -536,7 +681,7 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, R->s) : cudaSuccess;
     };
     if ((e = h2d(d_rp, rp.data(), rp.size() * 4)) != cudaSuccess || (e = h2d(d_ci, ci.data(), ci.size() * 4)) != cudaSuccess ||
-        (e = h2d(d_sr, sr.data(), sr.size() * 4)) != cudaSuccess || (e = h2d(d_hs, hs.data(), hs.size() * 4)) != cudaSuccess ||
+        (e = h2d(d_sr, sr.data(), sr.size() * 4)) != cudaSuccess || (e = h2d(d_cmax, cm.data(), cm.size() * 4)) != cudaSuccess || (e = h2d(d_hs, hs.data(), hs.size() * 4)) != cudaSuccess ||
         (e = h2d(d_av, d->values, (size_t)d->nnz * 16)) != cudaSuccess ||
         (e = h2d(d_b, d->b, (size_t)d->n_own * 16)) != cudaSuccess ||
         (d_dinv && (e = h2d(d_dinv, d->inv_diag, (size_t)d->n_own * 16)) != cudaSuccess) ||
@@ -560,6 +705,11 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
     a.A.rp = d_rp;
     a.A.ci = d_ci;
     a.A.av = d_av;
+    a.A.cmax = d_cmax;
+    a.capk = capk;
+    a.nst[0] = nst[0];
+    a.nst[1] = nst[1];
+    a.pf_rows = std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows;
     a.nv = R->nv;
     a.dinv = d_dinv;
     a.b = d_b;
@@ -600,9 +750,20 @@ extern "C" int cvk_rowblock_local(cvk_rowblock* R, int ph) {
             RK(cudaEventRecord(R->e0, R->s));
             f = (const void*)cvk::k_rb_init;
             break;
-        case CVK_RB_A: f = (const void*)cvk::k_rb_a; break;
-        case CVK_RB_B: f = (const void*)cvk::k_rb_b; break;
-        case CVK_RB_C: f = (const void*)cvk::k_rb_c; break;
+        case CVK_RB_A:
+        case CVK_RB_B:
+            if (R->streamed) {
+                RK(rb_launch(ph == CVK_RB_A ? (const void*)cvk::k_rb_a_s : (const void*)cvk::k_rb_b_s, R->nsm, R->s,
+                             args, cvk::kStreamThreads, ph == CVK_RB_A ? R->smem_a : R->smem_b));
+                R->launches++;
+            } else {
+                f = ph == CVK_RB_A ? (const void*)cvk::k_rb_a : (const void*)cvk::k_rb_b;
+            }
+            break;
+        case CVK_RB_C:
+            RK(rb_launch((const void*)cvk::k_rb_c4, R->Ge, R->s, args));
+            R->launches++;
+            break;
         case CVK_RB_X: break;
         case CVK_RB_T: f = (const void*)cvk::k_rb_t; break;
         default: return rbfail(CVK_EINVAL, "cvk_rowblock_local: unknown phase " + std::to_string(ph));
@@ -654,25 +815,96 @@ extern "C" int cvk_rowblock_done(cvk_rowblock* R, int* done) {
 
 extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
     if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: no blocks");
+    for (int q = 0; q < n; ++q)
+        if (!rbs[q] || rbs[q]->args.nranks != n || rbs[q]->slot != rbs[0]->slot || rbs[q]->s != rbs[0]->s)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: blocks disagree on ranks / slot / stream");
+    // the blocks share one stream, so they can share one gathered buffer:
+    // block q writes its slot q in place and every block reads them all --
+    // the all-gather costs nothing
+    double* shared = nullptr;
+    RK(cudaMalloc(&shared, sizeof(double) * rbs[0]->slot * n));
+    for (int q = 0; q < n; ++q) {
+        rbs[q]->args.send = shared + (size_t)q * rbs[0]->slot;
+        rbs[q]->args.recv = shared;
+    }
+    struct Restore {
+        cvk_rowblock* const* rbs;
+        int n;
+        double* shared;
+        ~Restore() {
+            cudaStreamSynchronize(rbs[0]->s);
+            for (int q = 0; q < n; ++q) {
+                rbs[q]->args.send = rbs[q]->send;
+                rbs[q]->args.recv = rbs[q]->recv;
+            }
+            cudaFree(shared);
+        }
+    } restore{rbs, n, shared};
     auto phase = [&](int ph) -> int {
         int e;
         for (int q = 0; q < n; ++q)
             if ((e = cvk_rowblock_local(rbs[q], ph)) != CVK_OK) return e;
-        if ((e = cvk_rowblock_exchange_local(rbs, n)) != CVK_OK) return e;
         for (int q = 0; q < n; ++q)
             if ((e = cvk_rowblock_post(rbs[q], ph)) != CVK_OK) return e;
         return CVK_OK;
     };
     int e;
     if ((e = phase(CVK_RB_INIT)) != CVK_OK) return e;
-    for (;;) {
-        int done = 0;
-        if ((e = cvk_rowblock_done(rbs[0], &done)) != CVK_OK) return e;
-        if (done) break;
-        for (int k = 0; k < 8; ++k)
-            for (int ph : {CVK_RB_A, CVK_RB_B, CVK_RB_C})
-                if ((e = phase(ph)) != CVK_OK) return e;
+    // kIters iterations of every block captured once and replayed, with the
+    // stop flag read back lazily (one graph in flight behind the poll), as
+    // the single-device phase kernels do
+    constexpr int kIters = 8;
+    cudaStream_t s = rbs[0]->s;
+    std::vector<long long> before(n);
+    for (int q = 0; q < n; ++q) before[q] = rbs[q]->launches;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    RK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kIters && e == CVK_OK; ++k)
+        for (int ph : {CVK_RB_A, CVK_RB_B, CVK_RB_C})
+            if (e == CVK_OK) e = phase(ph);
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (e != CVK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return e;
     }
+    RK(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&gx, graph, 0);
+    cudaGraphDestroy(graph);
+    RK(ie);
+    std::vector<long long> per_graph(n);
+    for (int q = 0; q < n; ++q) per_graph[q] = rbs[q]->launches - before[q], rbs[q]->launches = before[q];
+    int* h_done = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+        if (gx) cudaGraphExecDestroy(gx);
+        if (h_done) cudaFreeHost(h_done);
+        for (cudaEvent_t x : ev)
+            if (x) cudaEventDestroy(x);
+    };
+    if (cudaMallocHost(&h_done, 2 * sizeof(int)) != cudaSuccess || cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+        cleanup();
+        return rbfail(CVK_ECUDA, "cvk_rowblock_solve_local: host flag / events");
+    }
+    const long long max_graphs = rbs[0]->max_iter / kIters + 3;
+    long long graphs = 0;
+    cudaError_t le = cudaSuccess;
+    while (graphs < max_graphs && le == cudaSuccess) {
+        const int sl = (int)(graphs & 1);
+        if ((le = cudaGraphLaunch(gx, s)) != cudaSuccess) break;
+        if ((le = cudaMemcpyAsync(&h_done[sl], &rbs[0]->args.st->done, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) break;
+        if ((le = cudaEventRecord(ev[sl], s)) != cudaSuccess) break;
+        ++graphs;
+        for (int q = 0; q < n; ++q) rbs[q]->launches += per_graph[q];
+        if (graphs >= 2) {
+            const int old = (int)((graphs - 2) & 1);
+            if ((le = cudaEventSynchronize(ev[old])) != cudaSuccess) break;
+            if (h_done[old]) break;
+        }
+    }
+    cleanup();
+    RK(le);
     if ((e = phase(CVK_RB_X)) != CVK_OK) return e;
     return phase(CVK_RB_T);
 }

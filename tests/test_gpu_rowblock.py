@@ -126,3 +126,41 @@ def test_distributed_two_processes_one_device(cvk):
         assert hist == ref.report.residual_history
         assert np.array_equal(bits(x), bits(ref.x)), rank
     assert math.isfinite(ref.report.true_relres)
+
+
+def _nccl_worker(port, q, h):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_2112_00087_b200 as P
+        from paper_2112_00087_b200.rowblock import solve_distributed
+        A, b = cavity(h)
+        r = solve_distributed(A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000))
+        q.put((r.x, r.report.iterations, list(r.report.residual_history)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_nccl_plumbing_one_rank(cvk):
+    """NCCL all-gather on the library's stream over the exchange buffers
+    (torch tensors wrapping the library's device memory): one rank, so the
+    plumbing is exercised on the one GPU this suite has."""
+    import multiprocessing as mp
+    P = cvk
+    h = 0.004
+    A, b = cavity(h)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True,
+                                                                           max_iter=20000))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, h))
+    p.start()
+    x, it, hist = q.get(timeout=900)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert it == ref.report.iterations and hist == ref.report.residual_history
+    assert np.array_equal(bits(x), bits(ref.x))
