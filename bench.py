@@ -176,6 +176,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample-iters", type=int, default=40)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "rowblock"],
+                    help="N > 1: independent replicas (default), or one global solve over N row blocks "
+                         "(rowblock.py, strong scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -202,10 +205,18 @@ def main():
 
     import torch
     dist = None
-    if world > 1:
+    if world > 1 or args.mode == "rowblock":
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    if args.mode == "rowblock":
+        return run_rowblock(args, dist, world, rank, local)
 
     import paper_2112_00087_b200 as P
     from paper_2112_00087_b200 import _lib
@@ -330,6 +341,85 @@ def main():
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+    return 0
+
+
+def run_rowblock(args, dist, world, rank, local):
+    """One global BiCGSTAB over `world` row blocks, one per GPU (rowblock.py,
+    csrc/cvk_rowblock.cu): strong scaling of the same system.  value = device
+    time of the solve (CUDA events on each rank's stream), max over ranks;
+    e2e adds the per-step H2D of the rank's matrix block and rhs (a fresh
+    block) and the D2H of its rows of x."""
+    import torch
+    import paper_2112_00087_b200 as P
+    from paper_2112_00087_b200.cavac import Device
+    from paper_2112_00087_b200.rowblock import RowBlockEngine, plan_row_blocks
+
+    Device._default = Device(local)
+    prob = build_system()
+    A = prob.A
+    n, nnz = A.nrows, A.nnz()
+    d = P.jacobi(A).inv_diag
+    plan = plan_row_blocks(A, world)[rank]
+    b = np.asarray(prob.b, np.complex128)
+    opts = P.SolverOptions(tol=TOL, max_iter=MAX_ITER)
+    eng = RowBlockEngine(plan, b[plan.r0:plan.r1], d[plan.r0:plan.r1], opts)
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.solve_nccl()
+        eng.result()
+    reps = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            eng.solve_nccl()
+            reps.append(eng.result()[1])
+        barrier()
+    t_solve = statistics.mean(r.device_time for r in reps)
+    launches = sum(r.kernel_launches for r in reps)
+    e2e = []
+    for _ in range(args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        e = RowBlockEngine(plan, b[plan.r0:plan.r1], d[plan.r0:plan.r1], opts)
+        e.solve_nccl()
+        x_own, rep = e.result()
+        e.close()
+        barrier()
+        e2e.append(time.perf_counter() - t0)
+    t = torch.tensor([t_solve, statistics.mean(e2e)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_solve, t_e2e = float(t[0]), float(t[1])
+    it = reps[-1].iterations
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    peak, peak_kind = peaks()
+    iter_bytes = 40 * nnz + 344 * n
+    achieved = iter_bytes * it / t_solve / 1e9
+    line = {
+        "metric": METRIC, "value": t_solve, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_solve * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128 (f64 complex)",
+        "data": "synthetic (reference build_grid/assemble, roof Dirichlet 1+0i)",
+        "config": dict(workload_config(n, nnz), parallelism=f"row blocks x{world} (one global BiCGSTAB)"),
+        "iterations": it, "converged": bool(reps[-1].converged), "final_relres": reps[-1].final_relres,
+        "true_relres": reps[-1].true_relres, "seconds_per_iteration": t_solve / max(it, 1),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                     "frac": achieved / (peak * world), "traffic": None,
+                     "kernel": "row-block BiCGSTAB iteration (k_rb_a_s, k_rb_b_s, k_rb_c4, pack/post, "
+                               "3 ncclAllGather per iteration)", "bytes_per_iteration": iter_bytes,
+                     "peak_kind": peak_kind + f" x {world} GPUs"},
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 20 * nnz + 48 * n,
+                "d2h_bytes_per_step": 16 * n},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 

@@ -32,6 +32,9 @@
  *                         sweeps (driver pattern: bench_solvers,
  *                         src/pipeline.cpp:227-293)
  *   cvk_precond_jacobi_refresh  jacobi (src/krylov.cpp:31-55) on new values
+ *   cvk_rowblock_*        bicgstab (src/krylov.cpp:57-138) with the rows split
+ *                         over ranks / GPUs (no reference counterpart: its
+ *                         solve runs in one address space, krylov.hpp:68-69)
  */
 #ifndef CAVAC_B200_H
 #define CAVAC_B200_H
@@ -321,6 +324,14 @@ int cvk_rowblock_post(cvk_rowblock *rb, int phase);
 int cvk_rowblock_exchange_local(cvk_rowblock *const *rbs, int n);
 /* whole solve for n blocks on one device: the phase loop with lazy polling */
 int cvk_rowblock_solve_local(cvk_rowblock *const *rbs, int n);
+/* whole solve for one block per process over NCCL (the same phase loop,
+ * ncclAllGather on the context's stream, captured in CUDA graphs).  Rank 0
+ * makes the id (NCCL_UNIQUE_ID_BYTES = 128 bytes) and the caller broadcasts
+ * it; every rank attaches with its plan rank.  libnccl.so.2 is resolved at
+ * run time. */
+int cvk_nccl_unique_id(char *id);
+int cvk_rowblock_attach_nccl(cvk_rowblock *rb, const char *id, int rank);
+int cvk_rowblock_solve_nccl(cvk_rowblock *rb);
 /* synchronises; *done = the solver's stop flag */
 int cvk_rowblock_done(cvk_rowblock *rb, int *done);
 /* after CVK_RB_X and CVK_RB_T: own rows of x (2 n_own doubles) and the report */

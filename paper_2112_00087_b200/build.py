@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
             list(ex.map(_run, jobs))
     if force or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"])
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"])
     # C++ host API (namespace cavac) over the C ABI
     cpp_srcs = [os.path.join(CPP, f) for f in sorted(os.listdir(CPP))] if os.path.isdir(CPP) else []
     cpp_srcs = [f for f in cpp_srcs if f.endswith(".cpp")]

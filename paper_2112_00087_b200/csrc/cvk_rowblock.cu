@@ -26,6 +26,8 @@
 // single-device solve for any number of blocks
 // (tests/test_gpu_rowblock.py).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -495,6 +497,35 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
 
 using cvk::PState;
 
+// NCCL resolved at run time from the process's libnccl.so.2 (the one
+// torch.distributed already loaded, or the system's): the library has no
+// link-time NCCL dependency and single-device users never load it.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+static const NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+        a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+        a.all_gather = (decltype(a.all_gather))dlsym(h, "ncclAllGather");
+        a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+        a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_gather && a.comm_destroy && a.error_string;
+        return a;
+    }();
+    return api;
+}
+
 struct cvk_rowblock {
     cvk_ctx* ctx = nullptr;
     cudaStream_t s = nullptr;
@@ -514,7 +545,11 @@ struct cvk_rowblock {
     double t_wall0 = 0.0;
     int solver = CVK_BICGSTAB;
     long long max_iter = 0;
+    ncclComm_t comm = nullptr;
+    int rank = -1;
+    PState st0{};  // initial solver state, restored by every CVK_RB_INIT (blocks are reusable)
     ~cvk_rowblock() {
+        if (comm) nccl_api().comm_destroy(comm);
         for (void* p : bufs) cudaFree(p);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -695,6 +730,7 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
     hs0.max_iter = o->max_iter < 1 ? 0 : o->max_iter;
     hs0.record = R->hist_cap > 0 ? 1 : 0;
     hs0.hist_cap = R->hist_cap;
+    R->st0 = hs0;
     if ((e = cudaMemcpyAsync(d_st, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, R->s)) != cudaSuccess ||
         (e = cudaStreamSynchronize(R->s)) != cudaSuccess || (e = cudaEventCreate(&R->e0)) != cudaSuccess ||
         (e = cudaEventCreate(&R->e1)) != cudaSuccess)
@@ -747,6 +783,7 @@ extern "C" int cvk_rowblock_local(cvk_rowblock* R, int ph) {
         case CVK_RB_INIT:
             R->t_wall0 = wall_now();
             R->launches = 0;
+            RK(cudaMemcpyAsync(R->args.st, &R->st0, sizeof(PState), cudaMemcpyHostToDevice, R->s));
             RK(cudaEventRecord(R->e0, R->s));
             f = (const void*)cvk::k_rb_init;
             break;
@@ -813,46 +850,24 @@ extern "C" int cvk_rowblock_done(cvk_rowblock* R, int* done) {
     return CVK_OK;
 }
 
-extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
-    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: no blocks");
-    for (int q = 0; q < n; ++q)
-        if (!rbs[q] || rbs[q]->args.nranks != n || rbs[q]->slot != rbs[0]->slot || rbs[q]->s != rbs[0]->s)
-            return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: blocks disagree on ranks / slot / stream");
-    // the blocks share one stream, so they can share one gathered buffer:
-    // block q writes its slot q in place and every block reads them all --
-    // the all-gather costs nothing
-    double* shared = nullptr;
-    RK(cudaMalloc(&shared, sizeof(double) * rbs[0]->slot * n));
-    for (int q = 0; q < n; ++q) {
-        rbs[q]->args.send = shared + (size_t)q * rbs[0]->slot;
-        rbs[q]->args.recv = shared;
-    }
-    struct Restore {
-        cvk_rowblock* const* rbs;
-        int n;
-        double* shared;
-        ~Restore() {
-            cudaStreamSynchronize(rbs[0]->s);
-            for (int q = 0; q < n; ++q) {
-                rbs[q]->args.send = rbs[q]->send;
-                rbs[q]->args.recv = rbs[q]->recv;
-            }
-            cudaFree(shared);
-        }
-    } restore{rbs, n, shared};
+namespace {
+// The solve's phase loop for blocks on one stream: INIT, then kIters
+// iterations (A, B, C per block, xchg between local and post) captured once
+// and replayed with the stop flag read back lazily (one graph in flight
+// behind the poll, as the single-device phase kernels do), then X and T.
+template <class Xchg>
+int run_phases(cvk_rowblock* const* rbs, int n, Xchg&& xchg) {
     auto phase = [&](int ph) -> int {
         int e;
         for (int q = 0; q < n; ++q)
             if ((e = cvk_rowblock_local(rbs[q], ph)) != CVK_OK) return e;
+        if ((e = xchg()) != CVK_OK) return e;
         for (int q = 0; q < n; ++q)
             if ((e = cvk_rowblock_post(rbs[q], ph)) != CVK_OK) return e;
         return CVK_OK;
     };
     int e;
     if ((e = phase(CVK_RB_INIT)) != CVK_OK) return e;
-    // kIters iterations of every block captured once and replayed, with the
-    // stop flag read back lazily (one graph in flight behind the poll), as
-    // the single-device phase kernels do
     constexpr int kIters = 8;
     cudaStream_t s = rbs[0]->s;
     std::vector<long long> before(n);
@@ -885,7 +900,7 @@ extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
     if (cudaMallocHost(&h_done, 2 * sizeof(int)) != cudaSuccess || cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
         cleanup();
-        return rbfail(CVK_ECUDA, "cvk_rowblock_solve_local: host flag / events");
+        return rbfail(CVK_ECUDA, "rowblock solve: host flag / events");
     }
     const long long max_graphs = rbs[0]->max_iter / kIters + 3;
     long long graphs = 0;
@@ -907,6 +922,80 @@ extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
     RK(le);
     if ((e = phase(CVK_RB_X)) != CVK_OK) return e;
     return phase(CVK_RB_T);
+}
+
+}  // namespace
+
+extern "C" int cvk_rowblock_solve_local(cvk_rowblock* const* rbs, int n) {
+    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: no blocks");
+    for (int q = 0; q < n; ++q)
+        if (!rbs[q] || rbs[q]->args.nranks != n || rbs[q]->slot != rbs[0]->slot || rbs[q]->s != rbs[0]->s)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_solve_local: blocks disagree on ranks / slot / stream");
+    // the blocks share one stream, so they can share one gathered buffer:
+    // block q writes its slot q in place and every block reads them all --
+    // the all-gather costs nothing
+    double* shared = nullptr;
+    RK(cudaMalloc(&shared, sizeof(double) * rbs[0]->slot * n));
+    for (int q = 0; q < n; ++q) {
+        rbs[q]->args.send = shared + (size_t)q * rbs[0]->slot;
+        rbs[q]->args.recv = shared;
+    }
+    struct Restore {
+        cvk_rowblock* const* rbs;
+        int n;
+        double* shared;
+        ~Restore() {
+            cudaStreamSynchronize(rbs[0]->s);
+            for (int q = 0; q < n; ++q) {
+                rbs[q]->args.send = rbs[q]->send;
+                rbs[q]->args.recv = rbs[q]->recv;
+            }
+            cudaFree(shared);
+        }
+    } restore{rbs, n, shared};
+    return run_phases(rbs, n, [] { return CVK_OK; });
+}
+
+extern "C" int cvk_nccl_unique_id(char* id) {
+    if (!id) return rbfail(CVK_EINVAL, "cvk_nccl_unique_id: null id");
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return rbfail(CVK_ECUDA, "cvk_nccl_unique_id: libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    const ncclResult_t r = api.get_unique_id(&u);
+    if (r != ncclSuccess) return rbfail(CVK_ECUDA, std::string("ncclGetUniqueId: ") + api.error_string(r));
+    std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_attach_nccl(cvk_rowblock* R, const char* id, int rank) {
+    if (!R || !id) return rbfail(CVK_EINVAL, "cvk_rowblock_attach_nccl: null argument");
+    if (rank < 0 || rank >= R->args.nranks) return rbfail(CVK_EINVAL, "cvk_rowblock_attach_nccl: rank outside the plan");
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return rbfail(CVK_ECUDA, "cvk_rowblock_attach_nccl: libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    if (R->comm) {
+        api.comm_destroy(R->comm);
+        R->comm = nullptr;
+    }
+    const ncclResult_t r = api.comm_init_rank(&R->comm, R->args.nranks, u, rank);
+    if (r != ncclSuccess) {
+        R->comm = nullptr;
+        return rbfail(CVK_ECUDA, std::string("ncclCommInitRank: ") + api.error_string(r));
+    }
+    R->rank = rank;
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_solve_nccl(cvk_rowblock* R) {
+    if (!R || !R->comm) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_nccl: no NCCL communicator attached");
+    const NcclApi& api = nccl_api();
+    cvk_rowblock* rbs[1] = {R};
+    return run_phases(rbs, 1, [&]() -> int {
+        const ncclResult_t r = api.all_gather(R->send, R->recv, (size_t)R->slot, ncclDouble, R->comm, R->s);
+        if (r != ncclSuccess) return rbfail(CVK_ECUDA, std::string("ncclAllGather: ") + api.error_string(r));
+        return CVK_OK;
+    });
 }
 
 extern "C" int cvk_rowblock_result(cvk_rowblock* R, double* x_own, cvk_report* rep) {

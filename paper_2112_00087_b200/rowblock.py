@@ -61,7 +61,12 @@ def _bind(L):
     L.cvk_rowblock_done.argtypes = [P, C.POINTER(i32)]
     L.cvk_rowblock_result.argtypes = [P, P, C.POINTER(_lib.CvkReport)]
     L.cvk_rowblock_destroy.argtypes = [P]
-    for f in ("create", "exchange", "local", "post", "exchange_local", "solve_local", "done", "result", "destroy"):
+    L.cvk_nccl_unique_id.argtypes = [C.c_char_p]
+    L.cvk_nccl_unique_id.restype = i32
+    L.cvk_rowblock_attach_nccl.argtypes = [P, C.c_char_p, i32]
+    L.cvk_rowblock_solve_nccl.argtypes = [P]
+    for f in ("create", "exchange", "local", "post", "exchange_local", "solve_local", "done", "result", "destroy",
+              "attach_nccl", "solve_nccl"):
         getattr(L, "cvk_rowblock_" + f).restype = i32
     L._rb_bound = True
 
@@ -179,6 +184,25 @@ class RowBlockEngine:
         _lib.check(L.cvk_rowblock_exchange(h, C.byref(s), C.byref(r), C.byref(n)))
         self.send_ptr, self.recv_ptr, self.slot = s.value, r.value, n.value
         self.stream = L.cvk_ctx_stream(self.dev.handle)
+
+    def solve_nccl(self, group=None) -> None:
+        """The whole phase loop in the library over its own NCCL communicator
+        (bootstrapped through the torch.distributed group): ncclAllGather on
+        the library's stream, captured in CUDA graphs with the kernels."""
+        import torch.distributed as dist
+        if getattr(self, "_nccl_attached", False):
+            _lib.check(self.L.cvk_rowblock_solve_nccl(self.h))
+            return
+        rank = dist.get_rank(group)
+        box = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            _lib.check(self.L.cvk_nccl_unique_id(buf))
+            box = [buf.raw]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        _lib.check(self.L.cvk_rowblock_attach_nccl(self.h, box[0], self.plan.rank))
+        self._nccl_attached = True
+        _lib.check(self.L.cvk_rowblock_solve_nccl(self.h))
 
     def local(self, ph: int) -> None:
         _lib.check(self.L.cvk_rowblock_local(self.h, ph))
@@ -309,11 +333,14 @@ EngineFactory = Callable[[RowBlockPlan, np.ndarray, Optional[np.ndarray], Solver
 
 def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, group=None,
                       bounds: Optional[np.ndarray] = None, engine_factory: Optional[EngineFactory] = None,
-                      gather_solution: bool = True) -> SolveResult:
+                      gather_solution: bool = True, use_library_nccl: bool = True) -> SolveResult:
     """BiCGSTAB (krylov.cpp:57-138) with one row block per rank of a
-    torch.distributed group (initialised by the caller; NCCL for device
-    engines, gloo staged through host).  Every rank returns the same report;
-    x is the full solution (gather_solution) or the rank's own rows."""
+    torch.distributed group (initialised by the caller).  With device engines
+    on an NCCL group the library runs the whole loop over its own NCCL
+    communicator (use_library_nccl; otherwise the phases are issued from here
+    with torch's NCCL all-gather on the library's stream); gloo stages the
+    exchange through host.  Every rank returns the same report; x is the full
+    solution (gather_solution) or the rank's own rows."""
     import torch.distributed as dist
     opts = opts or SolverOptions()
     b, d = _check_system(A, b, M)
@@ -322,20 +349,23 @@ def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverO
     factory = engine_factory or (lambda pl, bo, do, o: RowBlockEngine(pl, bo, do, o))
     eng = factory(plan, b[plan.r0:plan.r1], None if d is None else d[plan.r0:plan.r1], opts)
     try:
-        xchg = _Exchange(eng, group)
+        if isinstance(eng, RowBlockEngine) and dist.get_backend(group) == "nccl" and use_library_nccl:
+            eng.solve_nccl(group)
+        else:
+            xchg = _Exchange(eng, group)
 
-        def phase(ph):
-            eng.local(ph)
-            xchg()
-            eng.post(ph)
+            def phase(ph):
+                eng.local(ph)
+                xchg()
+                eng.post(ph)
 
-        phase(PH_INIT)
-        while not eng.done():
-            for _ in range(ITERS_PER_POLL):
-                for ph in ITER_PHASES:
-                    phase(ph)
-        phase(PH_X)
-        phase(PH_T)
+            phase(PH_INIT)
+            while not eng.done():
+                for _ in range(ITERS_PER_POLL):
+                    for ph in ITER_PHASES:
+                        phase(ph)
+            phase(PH_X)
+            phase(PH_T)
         x_own, rep = eng.result()
     finally:
         if hasattr(eng, "close"):

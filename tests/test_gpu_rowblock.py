@@ -128,7 +128,7 @@ def test_distributed_two_processes_one_device(cvk):
     assert math.isfinite(ref.report.true_relres)
 
 
-def _nccl_worker(port, q, h):
+def _nccl_worker(port, q, h, lib_nccl):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -139,16 +139,19 @@ def _nccl_worker(port, q, h):
         import paper_2112_00087_b200 as P
         from paper_2112_00087_b200.rowblock import solve_distributed
         A, b = cavity(h)
-        r = solve_distributed(A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000))
+        r = solve_distributed(A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000),
+                              use_library_nccl=lib_nccl)
         q.put((r.x, r.report.iterations, list(r.report.residual_history)))
     finally:
         dist.destroy_process_group()
 
 
-def test_distributed_nccl_plumbing_one_rank(cvk):
-    """NCCL all-gather on the library's stream over the exchange buffers
-    (torch tensors wrapping the library's device memory): one rank, so the
-    plumbing is exercised on the one GPU this suite has."""
+@pytest.mark.parametrize("lib_nccl", [True, False])
+def test_distributed_nccl_plumbing_one_rank(cvk, lib_nccl):
+    """NCCL on one rank, so the plumbing runs on the one GPU this suite has:
+    the library's own communicator with the graph-captured phase loop
+    (cvk_rowblock_solve_nccl), or torch's all-gather on the library's stream
+    over tensors wrapping the exchange buffers."""
     import multiprocessing as mp
     P = cvk
     h = 0.004
@@ -157,7 +160,7 @@ def test_distributed_nccl_plumbing_one_rank(cvk):
                                                                            max_iter=20000))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, h))
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, h, lib_nccl))
     p.start()
     x, it, hist = q.get(timeout=900)
     p.join(timeout=60)
