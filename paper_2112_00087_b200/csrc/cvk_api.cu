@@ -830,7 +830,9 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     if (const char* env = std::getenv("CVK_GMRES_CTAS")) G = std::max(1, std::atoi(env));
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(m + 4) * std::max(1, n))) != CVK_OK) return e;
-    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
+    // partials of the G-CTA kernels and of the one-CTA-per-SM streamed ones
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes,
+                    sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)std::max<long long>(G, c->nsm))) != CVK_OK)
         return e;
     if (!c->gst) CK(cudaMalloc(&c->gst, cvk::gmres_state_size()));
     const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
@@ -843,14 +845,34 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     }
     std::vector<unsigned char> hs(cvk::gmres_state_size(), 0);
     cvk::gmres_init_state(hs.data(), o->tol, o->max_iter < 1 ? 0 : o->max_iter, m, o->record_history ? 1 : 0, hcap);
+    // Arnoldi SpMV on the TMA ring when a chunk fits >= 2 stages (as the
+    // BiCGSTAB / tfQMR phase kernels; CVK_NO_STREAM=1 keeps thread per row)
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    cvk::StreamLayout SL{A->capk, 2, 1};
+    SL.ngather = 1;
+    const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+    int nst = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)SL.stage_bytes()));
+    if (nst < 2 || A->nnz == 0 || std::getenv("CVK_NO_STREAM")) nst = 0;
+    SL.stages = std::max(1, nst);
+    if (nst) CK(cudaFuncSetAttribute(K.spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
+    // second CGS pass from shared-memory tiles (k_g_ud_s): needs 2 stages of
+    // (m + 2) 128-row vectors
+    int ud_smem = optin - 8192 - 4096;
+    const bool ud = nst && m <= 32 && (long long)ud_smem >= 2LL * (m + 2) * 128 * 16 + 256 && !std::getenv("CVK_GMRES_NO_TILES");
+    if (ud) CK(cudaFuncSetAttribute(K.upd1_s, cudaFuncAttributeMaxDynamicSharedMemorySize, ud_smem));
+    void* uargs[2] = {nullptr, &ud_smem};
+    const int pf = std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows;
     std::vector<unsigned char> blob(cvk::gmres_args_size());
-    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av}, M->dinv, b_dev, x_dev, (double2*)c->work,
-                         c->part, c->gst, c->hist, c->rep);
+    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, nullptr}, M->dinv, b_dev, x_dev,
+                         (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf);
     void* args[] = {blob.data()};
+    uargs[0] = blob.data();
     const dim3 grid((unsigned)G), block(cvk::kThreads);
     std::vector<unsigned char> key(blob);
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
+    key.push_back((unsigned char)(ud ? 1 : 0));
     if (!c->gm_exec || c->gm_key != key) {
         if (c->gm_exec) { cudaGraphExecDestroy(c->gm_exec); c->gm_exec = nullptr; }
         cudaGraph_t graph;
@@ -858,8 +880,12 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
         for (int it = 0; it < kIterPerGraph; ++it) {
             launch_pdl(K.x, grid, block, args, 0, c->stream);
             launch_pdl(K.spmv, grid, block, args, 0, c->stream);
+            if (nst) launch_pdl(K.spmv_s, dim3((unsigned)c->nsm), dim3(cvk::kStreamThreads), args, SL.smem_bytes(), c->stream);
             launch_pdl(K.dots, grid, block, args, 0, c->stream);
-            launch_pdl(K.upd1, grid, block, args, 0, c->stream);
+            if (ud)
+                launch_pdl(K.upd1_s, dim3((unsigned)c->nsm), dim3(cvk::kGmresTileThreads), uargs, (size_t)ud_smem, c->stream);
+            else
+                launch_pdl(K.upd1, grid, block, args, 0, c->stream);
             launch_pdl(K.upd2, grid, block, args, 0, c->stream);
         }
         CK(cudaGetLastError());
@@ -883,7 +909,7 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
         CK(cudaMemcpyAsync(&c->h_done[slot], done_ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += 5 * kIterPerGraph;
+        launches += (nst ? 6 : 5) * kIterPerGraph;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));

@@ -20,6 +20,7 @@
 
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
+#include "cvk_stream.cuh"
 
 namespace cvk {
 
@@ -50,6 +51,7 @@ struct GArgs {
     GState* st;
     double* hist;
     DevReport* rep;
+    int capk, nst, pf_rows;  // streamed Arnoldi SpMV (k_g_spmv_s); nst = 0: not streamed
 };
 
 __device__ __forceinline__ void pdl_enter_g() {
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(kThreads) k_g_spmv(GArgs a) {
     if (mode != G_ARN && mode != G_RR) return;
     const int n = a.A.n;
     if (mode == G_ARN) {
+        if (a.nst > 0) return;  // the streamed kernel k_g_spmv_s runs the Arnoldi SpMV
         const int j = st->j;
         const double2* src = j == 0 ? vec(a, 0) : vec(a, 1 + (st->wcur ^ 1));
         double2* w = vec(a, 1 + st->wcur);
@@ -216,6 +219,33 @@ __global__ void __launch_bounds__(kThreads) k_g_spmv(GArgs a) {
     st->j = 0;
     st->k = 0;
     st->mode = G_WAIT;
+}
+
+// The Arnoldi SpMV on the TMA ring (cvk_stream.cuh): V_j = src / scale is
+// formed once per chunk row in the pre-hook and by the out-of-chunk gathers,
+// w = M^-1 A V_j -- the per-element roundings and per-row order of k_g_spmv.
+__global__ void __launch_bounds__(kStreamThreads, 1) k_g_spmv_s(GArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter_g();
+    GState* st = a.st;
+    if (st->done || st->mode != G_ARN) return;
+    const int j = st->j;
+    const double2* src = j == 0 ? vec(a, 0) : vec(a, 1 + (st->wcur ^ 1));
+    double2* w = vec(a, 1 + st->wcur);
+    double2* vj = Vq(a, j);
+    const double sc = st->scale;
+    const double2* vecs[2] = {src, a.dinv};
+    StreamLayout L{a.capk, 2, a.nst, 0};
+    L.ngather = 1;
+    L.pf_rows = a.pf_rows;
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return ch.v(0, l); };
+        auto xg = [&](int c) -> double2 { return cvk_divr(src[c], sc); };
+        const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
+        const int row = ch.r0 + t;
+        vj[row] = xs(t);
+        w[row] = a.dinv ? cvk_mul(ch.v(1, t), y) : y;
+    }, nullptr, nullptr, [&](int t, const Chunk& ch) { ch.set(0, t, cvk_divr(ch.v(0, t), sc)); });
 }
 
 // h = V^H w over q <= j (UPDATE: first w -= V h1 per row).  Basis vectors are
@@ -290,6 +320,110 @@ __global__ void __launch_bounds__(kThreads) k_g_dots(GArgs a) {
         if (lane == 0) out[q] = v;
     }
     if (threadIdx.x == 0) st->counter[UPDATE ? 1 : 0] = 0;
+}
+
+// Second CGS pass in ONE read of the basis: w -= V h1, then h2 = V^H w, on
+// row tiles of [w | V_0 .. V_j] streamed into shared memory by TMA (a ring of
+// as many stages as fit).  k_g_dots<true> reads V twice (its update pass,
+// then its dot pass); at 5M DOF that pass was ~30% of an Arnoldi step.
+// Per-row update order is that of k_g_dots<true>; h2 is double-double, so
+// the scalars equal it.
+constexpr int kTileRows = 128;                          // rows per tile = threads per consumer group
+constexpr int kTileGroups = 3;                          // consumer groups
+constexpr int kTileThreads = kTileRows * kTileGroups + 32;  // + producer warp
+constexpr int kTileWarps = kTileRows / 32;              // warps per group
+constexpr int kTileQ = 8;                               // basis vectors per warp: cnt <= 32 (m <= 32)
+
+__global__ void __launch_bounds__(kTileThreads, 1) k_g_ud_s(GArgs a, int smem_bytes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter_g();
+    GState* st = a.st;
+    if (st->done || st->mode != G_ARN) return;
+    const int n = a.A.n, cnt = st->j + 1;
+    double2* w = vec(a, 1 + st->wcur);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    __shared__ double2 hs[kMaxDots];
+    __shared__ CAcc red[kTileGroups][kMaxDots];
+    for (int q = tid; q < cnt; q += blockDim.x) hs[q] = st->h1[q];
+    const size_t vb = (size_t)kTileRows * 16, sb = (size_t)(cnt + 1) * vb;
+    const int ST = (int)min((size_t)kStreamMaxStages, ((size_t)smem_bytes - 2 * kStreamMaxStages * 8) / sb);
+    uint64_t* full = (uint64_t*)(smem + (size_t)ST * sb);  // sb is a multiple of 2 KB
+    uint64_t* empty = full + kStreamMaxStages;
+    if (tid == 0) {
+        for (int q = 0; q < ST; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, kTileRows);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ntiles = (n + kTileRows - 1) / kTileRows, G = gridDim.x;
+    const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    if (tid >= kTileGroups * kTileRows) {  // producer warp (lane 0 issues; the loop is warp-uniform)
+        for (int i = 0; i < mine; ++i) {
+            const int s = i % ST, r0 = (blockIdx.x + i * G) * kTileRows;
+            const uint32_t bytes = (uint32_t)(min(kTileRows, n - r0) * 16);
+            if (lane == 0) {
+                mbar_wait(empty + s, ((uint32_t)(i / ST) & 1u) ^ 1u);
+                mbar_expect_tx(full + s, bytes * (uint32_t)(cnt + 1));
+                unsigned char* sp = smem + (size_t)s * sb;
+                bulk_g2s(sp, w + r0, bytes, full + s);
+                for (int q = 0; q < cnt; ++q) bulk_g2s(sp + (size_t)(q + 1) * vb, Vq(a, q) + r0, bytes, full + s);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int g = tid / kTileRows, t = tid % kTileRows, wq = (tid % kTileRows) >> 5;
+        CAcc acc[kTileQ];
+#pragma unroll
+        for (int u = 0; u < kTileQ; ++u) acc[u] = CAcc{};
+        for (int i = g; i < mine; i += kTileGroups) {
+            const int s = i % ST, r0 = (blockIdx.x + i * G) * kTileRows, rows = min(kTileRows, n - r0);
+            mbar_wait(full + s, (uint32_t)(i / ST) & 1u);
+            double2* W = (double2*)(smem + (size_t)s * sb);
+            const double2* V = W + kTileRows;
+            if (t < rows) {
+                double2 wi = W[t];
+                for (int q = 0; q < cnt; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q]), V[(size_t)q * kTileRows + t]));
+                W[t] = wi;
+                w[r0 + t] = wi;
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kTileRows) : "memory");
+#pragma unroll
+            for (int u = 0; u < kTileQ; ++u) {
+                const int q = wq + kTileWarps * u;
+                if (q < cnt) {
+                    const double2* vq = V + (size_t)q * kTileRows;
+#pragma unroll
+                    for (int e = 0; e < kTileRows / 32; ++e) {
+                        const int row = lane + 32 * e;
+                        if (row < rows) acc_dot(acc[u], vq[row], W[row]);
+                    }
+                }
+            }
+            mbar_arrive(empty + s);
+        }
+#pragma unroll
+        for (int u = 0; u < kTileQ; ++u) {
+            const int q = wq + kTileWarps * u;
+            const CAcc tq = warp_sum(acc[u]);
+            if (q < cnt && lane == 0) red[g][q] = tq;
+        }
+    }
+    __syncthreads();
+    double2* pr = a.part;
+    if (tid < cnt) {
+        CAcc sq = red[0][tid];
+        for (int g = 1; g < kTileGroups; ++g) cacc_add(sq, red[g][tid]);
+        cacc_store(pr, tid, G, blockIdx.x, sq);
+        __threadfence();
+    }
+    if (!arrive_last(&st->counter[1])) return;
+    for (int q = warp; q < cnt; q += kTileThreads / 32) {
+        const double2 v = fold_one(pr, q, G, lane);
+        if (lane == 0) st->h2[q] = v;
+    }
+    if (tid == 0) st->counter[1] = 0;
 }
 
 // w -= V h2, ||w||; then (last CTA) the Givens step of the persistent kernel
@@ -416,6 +550,8 @@ GmresKernels gmres_kernels() {
     k.init = (const void*)k_g_init;
     k.x = (const void*)k_g_x;
     k.spmv = (const void*)k_g_spmv;
+    k.spmv_s = (const void*)k_g_spmv_s;
+    k.upd1_s = (const void*)k_g_ud_s;
     k.dots = (const void*)k_g_dots<false>;
     k.upd1 = (const void*)k_g_dots<true>;
     k.upd2 = (const void*)k_g_upd2;
@@ -439,8 +575,11 @@ void gmres_init_state(void* host_state, double tol, long long max_iter, int m, i
 int gmres_state_done_offset() { return (int)offsetof(GState, done); }
 
 void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
-                     double2* part, void* st, double* hist, DevReport* rep) {
+                     double2* part, void* st, double* hist, DevReport* rep, int capk, int nst, int pf_rows) {
     GArgs* p = (GArgs*)out;
+    p->capk = capk;
+    p->nst = nst;
+    p->pf_rows = pf_rows;
     p->A = A;
     p->dinv = dinv;
     p->b = b;

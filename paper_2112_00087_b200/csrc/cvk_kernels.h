@@ -38,14 +38,17 @@ void streamk_pack_args(void* out, const Csr& A, const double2* dinv, const doubl
 // phase-kernel GMRES(m) (cvk_gmres.cu), kThreads threads per CTA
 struct GmresKernels {
     const void *init, *x, *spmv, *dots, *upd1, *upd2, *true_res;
+    const void* spmv_s;  // streamed Arnoldi SpMV: kStreamThreads threads, dynamic smem
+    const void* upd1_s;  // (GArgs, int smem_bytes): w -= V h1 and h2 = V^H w in one TMA-fed pass
 };
+constexpr int kGmresTileThreads = 3 * 128 + 32;
 GmresKernels gmres_kernels();
 size_t gmres_state_size();
 size_t gmres_args_size();
 void gmres_init_state(void* host_state, double tol, long long max_iter, int m, int record, long long hist_cap);
 int gmres_state_done_offset();
 void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
-                     double2* part, void* st, double* hist, DevReport* rep);
+                     double2* part, void* st, double* hist, DevReport* rep, int capk, int nst, int pf_rows);
 
 // phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): one uniform step kernel
 struct BiclKernels {
