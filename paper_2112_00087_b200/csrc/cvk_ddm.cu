@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <chrono>
 #include <complex>
 #include <cstring>
@@ -256,7 +258,17 @@ struct cvk_ddm_rank {
     double2 a_l{}, b_l{}, a_r{}, b_r{}, s_sum{};
     std::vector<cvk::DevReport> hr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // FAST mode, every strip >= CVK_DDM_SEQ_MIN rows: the strips' inner
+    // solves run one after another on the single-system path (TMA-streamed
+    // phase kernels), not as CTA segments of one batched persistent launch
+    bool seq = false;
+    std::vector<cvk_csr*> seq_A;
+    std::vector<cvk_prec*> seq_M;
+    std::vector<int64_t> off;
+    cvk_opts inner_opts{};
     ~cvk_ddm_rank() {
+        for (cvk_prec* M : seq_M) cvk_precond_free(M);
+        for (cvk_csr* A : seq_A) cvk_csr_free(A);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
     }
@@ -408,6 +420,34 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
         cta_base += gs[j];
     }
     R->total_ctas = cta_base;
+    R->off.assign(h_off.begin(), h_off.end());
+    R->inner_opts = *inner;
+    R->inner_opts.record_history = 0;
+    R->inner_opts.mode = R->mode;
+    {
+        // a strip this large fills the device on its own: the batched launch
+        // gives each strip ~1/ns of the SMs on the latency-bound persistent
+        // kernel (5M DOF, 8 strips: ~490 us per inner iteration)
+        long long thr = 131072;
+        if (const char* env = std::getenv("CVK_DDM_SEQ_MIN")) thr = std::atoll(env);
+        int64_t nmin = INT64_MAX;
+        for (const Strip& S : strips) nmin = std::min<int64_t>(nmin, S.n);
+        R->seq = R->mode == CVK_MODE_FAST && nmin >= thr;
+    }
+    if (R->seq) {
+        for (int64_t j = 0; j < ns; ++j) {
+            const Strip& S = strips[j];
+            std::vector<uint64_t> rp64(S.rp.begin(), S.rp.end()), ci64(S.ci.begin(), S.ci.end());
+            cvk_csr* A = nullptr;
+            cvk_prec* M = nullptr;
+            int ee = cvk_csr_upload(ctx, S.n, S.n, (int64_t)S.ci.size(), rp64.data(), ci64.data(),
+                                    reinterpret_cast<const double*>(S.v.data()), &A);
+            if (ee != CVK_OK) return ee;
+            R->seq_A.push_back(A);
+            if ((ee = cvk_precond_jacobi(A, nullptr, &M)) != CVK_OK) return ee;
+            R->seq_M.push_back(M);
+        }
+    }
     DK(mem.alloc(&R->d_segs, ns));
     DK(cudaMemcpyAsync(R->d_segs, segs.data(), sizeof(KArgs) * ns, cudaMemcpyHostToDevice, st));
     auto d2 = [](Cx z) { return make_double2(z.real(), z.imag()); };
@@ -443,8 +483,29 @@ extern "C" int cvk_ddm_rank_sweep(cvk_ddm_rank* R, const double* g_in_left, cons
     DK(cudaGetLastError());
     DK(cudaMemsetAsync(R->d_bars, 0, sizeof(unsigned long long) * 2 * ns, st));
     float ms = 0.f;
-    const int e = cvk_ddm_launch_batched(R->ctx, R->solver, R->mode, R->d_segs, (int)ns, R->total_ctas, R->smem, &ms);
-    if (e != CVK_OK) return e;
+    long long launches = 3;
+    if (R->seq) {
+        for (int64_t j = 0; j < ns; ++j) {
+            cvk_report rep{};
+            const int e = cvk_solve_device(R->ctx, R->solver, R->seq_A[j], R->seq_M[j], &R->inner_opts,
+                                           reinterpret_cast<const double*>(R->d_rhs + R->off[j]),
+                                           reinterpret_cast<double*>(R->d_u + R->off[j]), &rep);
+            if (e != CVK_OK) return e;
+            DevReport& d = R->hr[j];
+            d.converged = rep.converged;
+            d.breakdown = rep.breakdown;
+            d.iterations = rep.iterations;
+            d.final_relres = rep.final_relres;
+            d.true_relres = rep.true_relres;
+            d.history_len = 0;
+            d.error = 0;
+            launches += rep.kernel_launches;
+        }
+        DK(cudaMemcpyAsync(R->d_reps, R->hr.data(), sizeof(DevReport) * ns, cudaMemcpyHostToDevice, st));
+    } else {
+        const int e = cvk_ddm_launch_batched(R->ctx, R->solver, R->mode, R->d_segs, (int)ns, R->total_ctas, R->smem, &ms);
+        if (e != CVK_OK) return e;
+    }
     const int64_t nslot = (ns + 1) * ny;
     const unsigned xb = (unsigned)std::min<int64_t>(64, (nslot + threads - 1) / threads);
     k_ddm_exchange<<<std::max(1u, xb), threads, 0, st>>>(R->geo, R->d_u, R->d_gl, R->d_gr, R->d_prev, R->a_l, R->b_l,
@@ -467,7 +528,7 @@ extern "C" int cvk_ddm_rank_sweep(cvk_ddm_rank* R, const double* g_in_left, cons
         info->total_inner_iterations += R->hr[j].iterations;
     }
     info->device_time_s = sweep_ms * 1e-3;
-    info->kernel_launches = 3;
+    info->kernel_launches = launches;
     return CVK_OK;
 }
 

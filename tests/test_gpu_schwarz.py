@@ -161,3 +161,28 @@ def test_tune_parameters(cvk, ddm):
     assert (chosen.outer_iterations, chosen.total_inner_iterations) == best
     with pytest.raises(cvk.InvalidArgument):
         S.tune_parameters(p, part, [], P.SolverOptions(), 10)
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "tfqmr", "gmres"])
+def test_sequential_strip_solves_bitwise_batched(cvk, ddm, monkeypatch, solver):
+    """FAST DDM with the strips' inner solves run one after another on the
+    single-system path (used when every strip has >= CVK_DDM_SEQ_MIN rows;
+    forced here) = the batched persistent launch, bit for bit: the inner
+    reductions are double-double on both paths."""
+    H, S = ddm
+    P = cvk
+    p = cavity_problem(H, 0.05)
+    k = p.omega / p.c
+    part = S.partition(p.grid, 3)
+    tp = S.TransmissionParams(complex(2.0, k), complex(2.0, k))
+    sid = P.solver_from_name(solver)
+    out = {}
+    for path, thr in (("batched", "1000000000"), ("sequential", "0")):
+        monkeypatch.setenv("CVK_DDM_SEQ_MIN", thr)
+        monkeypatch.setenv("CVK_PHASED_MIN_N", "0" if path == "sequential" else "1000000000")
+        out[path] = S.schwarz_solve(p, part, tp, P.SolverOptions(tol=1e-10, m=20), 1e-8, 40, inner_solver=sid)
+    a, b = out["batched"], out["sequential"]
+    assert a.report.outer_iterations == b.report.outer_iterations
+    assert a.report.interface_residual_history == b.report.interface_residual_history
+    assert a.report.total_inner_iterations == b.report.total_inner_iterations
+    assert np.array_equal(bits(a.x), bits(b.x))
