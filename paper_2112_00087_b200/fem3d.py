@@ -74,6 +74,10 @@ class FemCavity:
     def matrix(self, omega: float) -> CsrMatrix:
         return CsrMatrix(self.n, self.n, self.rp, self.ci, self.values(omega))
 
+    def coords(self) -> np.ndarray:
+        """Vertex coordinates (n, 3) in DOF order (for geometric partitioning)."""
+        return _vertices(self.nx, self.ny, self.nz, self.lx, self.ly, self.lz)
+
 
 def _vertices(nx, ny, nz, lx, ly, lz):
     i, j, k = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")

@@ -152,6 +152,67 @@ def plan_row_blocks(A: CsrMatrix, n_ranks: int, bounds: Optional[np.ndarray] = N
     return plans
 
 
+# ------------------------------------------------ geometric partitioning --
+
+def rcb_partition(coords, n_parts: int) -> np.ndarray:
+    """Recursive coordinate bisection (the geometric stand-in for METIS-style
+    subdomains of an FEM mesh): split the point set along its longest extent
+    at the count that gives each side its share of the parts, recursively.
+    Returns the part id of every point; part sizes differ by at most one."""
+    xyz = np.asarray(coords, np.float64)
+    if xyz.ndim != 2 or n_parts < 1:
+        raise InvalidArgument("rcb_partition: coords must be (n, d) and n_parts >= 1")
+    part = np.zeros(len(xyz), np.int64)
+
+    def split(idx, p0, k):
+        if k == 1 or len(idx) == 0:
+            part[idx] = p0
+            return
+        kl = k // 2
+        nl = (len(idx) * kl) // k
+        ext = xyz[idx].max(axis=0) - xyz[idx].min(axis=0)
+        ax = int(np.argmax(ext))
+        order = idx[np.lexsort((idx, xyz[idx, ax]))]  # ties broken by index: deterministic
+        split(order[:nl], p0, kl)
+        split(order[nl:], p0 + kl, k - kl)
+
+    split(np.arange(len(xyz), dtype=np.int64), 0, n_parts)
+    return part
+
+
+def permute_system(A: CsrMatrix, perm: np.ndarray) -> CsrMatrix:
+    """P A P^T with new row k = old row perm[k]; columns renumbered and
+    sorted per row (values carried)."""
+    perm = np.asarray(perm, np.int64)
+    n = A.nrows
+    if A.nrows != A.ncols or len(perm) != n or not np.array_equal(np.sort(perm), np.arange(n)):
+        raise InvalidArgument("permute_system: perm must be a permutation of the rows of a square matrix")
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    rp = np.asarray(A.row_offsets, np.int64)
+    ci = np.asarray(A.col_indices, np.int64)
+    v = np.asarray(A.values, np.complex128)
+    lens = np.diff(rp)[perm]
+    nrp = np.zeros(n + 1, np.int64)
+    nrp[1:] = np.cumsum(lens)
+    src = np.repeat(rp[perm], lens) + (np.arange(nrp[-1]) - np.repeat(nrp[:-1], lens))
+    rows = np.repeat(np.arange(n), lens)
+    cols = inv[ci[src]]
+    order = np.lexsort((cols, rows))
+    return CsrMatrix(n, n, nrp.astype(np.uint64), cols[order].astype(np.uint64), v[src][order])
+
+
+def rcb_order(coords, n_parts: int):
+    """Permutation that makes every RCB part a contiguous block of rows
+    (parts in id order, original order inside a part) and the block bounds."""
+    part = rcb_partition(coords, n_parts)
+    perm = np.lexsort((np.arange(len(part)), part))
+    counts = np.bincount(part, minlength=n_parts)
+    bounds = np.zeros(n_parts + 1, np.int64)
+    bounds[1:] = np.cumsum(counts)
+    return perm, bounds
+
+
 # --------------------------------------------------------------- engines --
 
 class RowBlockEngine:
@@ -269,12 +330,31 @@ def _check_system(A: CsrMatrix, b, M: Preconditioner):
     return b, d
 
 
+def _rcb_system(A, b, d, coords, n_blocks):
+    perm, bounds = rcb_order(coords, n_blocks)
+    return permute_system(A, perm), b[perm], None if d is None else d[perm], perm, bounds
+
+
+def _unpermute(res: SolveResult, perm) -> SolveResult:
+    x = np.empty_like(res.x)
+    x[perm] = res.x
+    return SolveResult(x, res.report)
+
+
 def solve_row_blocks(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, n_blocks: int = 2,
-                     bounds: Optional[np.ndarray] = None, dev: Optional[Device] = None) -> SolveResult:
+                     bounds: Optional[np.ndarray] = None, dev: Optional[Device] = None,
+                     coords=None) -> SolveResult:
     """BiCGSTAB over n_blocks row blocks on one device: every block runs the
-    multi-rank kernels, the all-gather is a device copy (same stream)."""
+    multi-rank kernels, the all-gather is a device copy (same stream).  With
+    `coords` (one point per row, e.g. FemCavity.coords()) the blocks are RCB
+    parts: the system is permuted so each part is contiguous, and x is
+    returned in the original numbering."""
     opts = opts or SolverOptions()
     b, d = _check_system(A, b, M)
+    if coords is not None:
+        Ap, bp, dp, perm, bnd = _rcb_system(A, b, d, coords, n_blocks)
+        Mp = Preconditioner("identity") if dp is None else Preconditioner("jacobi", dp)
+        return _unpermute(solve_row_blocks(Ap, bp, Mp, opts, n_blocks, bnd, dev), perm)
     plans = plan_row_blocks(A, n_blocks, bounds)
     engines = [RowBlockEngine(pl, b[pl.r0:pl.r1], None if d is None else d[pl.r0:pl.r1], opts, dev) for pl in plans]
     try:
@@ -333,18 +413,25 @@ EngineFactory = Callable[[RowBlockPlan, np.ndarray, Optional[np.ndarray], Solver
 
 def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, group=None,
                       bounds: Optional[np.ndarray] = None, engine_factory: Optional[EngineFactory] = None,
-                      gather_solution: bool = True, use_library_nccl: bool = True) -> SolveResult:
+                      gather_solution: bool = True, use_library_nccl: bool = True, coords=None) -> SolveResult:
     """BiCGSTAB (krylov.cpp:57-138) with one row block per rank of a
     torch.distributed group (initialised by the caller).  With device engines
     on an NCCL group the library runs the whole loop over its own NCCL
     communicator (use_library_nccl; otherwise the phases are issued from here
     with torch's NCCL all-gather on the library's stream); gloo stages the
     exchange through host.  Every rank returns the same report; x is the full
-    solution (gather_solution) or the rank's own rows."""
+    solution (gather_solution) or the rank's own rows.  `coords` makes the
+    ranks' blocks RCB parts (as in solve_row_blocks; x is then always the full
+    solution in the original numbering)."""
     import torch.distributed as dist
     opts = opts or SolverOptions()
     b, d = _check_system(A, b, M)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if coords is not None:
+        Ap, bp, dp, perm, bnd = _rcb_system(A, b, d, coords, world)
+        Mp = Preconditioner("identity") if dp is None else Preconditioner("jacobi", dp)
+        res = solve_distributed(Ap, bp, Mp, opts, group, bnd, engine_factory, True, use_library_nccl)
+        return _unpermute(res, perm)
     plan = plan_row_blocks(A, world, bounds)[rank]
     factory = engine_factory or (lambda pl, bo, do, o: RowBlockEngine(pl, bo, do, o))
     eng = factory(plan, b[plan.r0:plan.r1], None if d is None else d[plan.r0:plan.r1], opts)

@@ -167,3 +167,27 @@ def test_distributed_nccl_plumbing_one_rank(cvk, lib_nccl):
     assert p.exitcode == 0
     assert it == ref.report.iterations and hist == ref.report.residual_history
     assert np.array_equal(bits(x), bits(ref.x))
+
+
+def test_rcb_blocks_on_renumbered_fem_mesh(cvk):
+    """FEM-3D box with a random node numbering, 4 RCB blocks (the system is
+    permuted so each part is contiguous, x returned in the original
+    numbering): same solution as the single-device solve on the original
+    system (the permutation changes the per-row summation order, so not bit
+    for bit)."""
+    from paper_2112_00087_b200 import fem3d as F
+    from paper_2112_00087_b200.rowblock import permute_system, solve_row_blocks
+    P = cvk
+    cav = F.build_cavity(10)
+    A0 = P.CsrMatrix(cav.n, cav.n, cav.rp.astype(np.uint64), cav.ci.astype(np.uint64), cav.values(2 * np.pi * 60.0))
+    shuffle = np.random.default_rng(3).permutation(cav.n)
+    A = permute_system(A0, shuffle)
+    b = np.asarray(cav.b, np.complex128)[shuffle]
+    xyz = cav.coords()[shuffle]
+    o = P.SolverOptions(tol=1e-11, max_iter=20000)
+    ref = P.solve(P.SolverId.BiCGStab, A0, cav.b, P.jacobi(A0), o)
+    got = solve_row_blocks(A, b, P.jacobi(A), o, n_blocks=4, coords=xyz)
+    assert ref.report.converged and got.report.converged
+    assert abs(got.report.iterations - ref.report.iterations) <= max(3, 0.15 * ref.report.iterations)
+    x = got.x[np.argsort(shuffle)]
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)

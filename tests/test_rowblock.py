@@ -148,3 +148,49 @@ def test_distributed_rowblock_matches_one_block(world, oracle):
     assert abs(ro.iterations - rep1.iterations) <= max(2, 0.15 * ro.iterations)
     assert np.linalg.norm(x1 - xo) <= 1e-7 * np.linalg.norm(xo)
     assert math.isfinite(rep1.true_relres) and rep1.true_relres < 1e-8
+
+
+def test_rcb_partition_balanced_and_compact():
+    """RCB parts of the FEM box: sizes within one, and on a randomly
+    renumbered mesh the parts' halos are as small as the natural slabs'
+    (contiguous blocks of the shuffled numbering have halos near the whole
+    mesh)."""
+    from paper_2112_00087_b200 import fem3d as F
+    from paper_2112_00087_b200.cavac import CsrMatrix
+    from paper_2112_00087_b200.rowblock import permute_system, plan_row_blocks, rcb_order, rcb_partition
+    cav = F.build_cavity(6)
+    xyz = cav.coords()
+    A = CsrMatrix(cav.n, cav.n, cav.rp.astype(np.uint64), cav.ci.astype(np.uint64), cav.values(300.0))
+    for k in (1, 2, 3, 5, 8):
+        part = rcb_partition(xyz, k)
+        sizes = np.bincount(part, minlength=k)
+        assert sizes.max() - sizes.min() <= 1 and sizes.sum() == cav.n
+    rng = np.random.default_rng(0)
+    shuffle = rng.permutation(cav.n)
+    As = permute_system(A, shuffle)
+    xs = xyz[shuffle]
+    halo = lambda plans: sum(len(p.halo_cols) for p in plans)  # noqa: E731
+    natural = halo(plan_row_blocks(A, 4, np.array([(q * cav.n) // 4 for q in range(5)])))
+    naive = halo(plan_row_blocks(As, 4, np.array([(q * cav.n) // 4 for q in range(5)])))
+    perm, bounds = rcb_order(xs, 4)
+    rcb = halo(plan_row_blocks(permute_system(As, perm), 4, bounds))
+    assert naive > 2.5 * natural
+    assert rcb <= 1.5 * natural
+
+
+def test_permute_system_is_similarity():
+    from paper_2112_00087_b200.rowblock import permute_system
+    A = _random_csr(60, 3)
+    perm = np.random.default_rng(4).permutation(60)
+    Ap = permute_system(A, perm)
+    D = np.zeros((60, 60), np.complex128)
+    rp, ci, v = (np.asarray(a) for a in (A.row_offsets, A.col_indices, A.values))
+    for i in range(60):
+        D[i, ci[rp[i]:rp[i + 1]].astype(np.int64)] = v[rp[i]:rp[i + 1]]
+    Dp = np.zeros_like(D)
+    rp2, ci2, v2 = (np.asarray(a) for a in (Ap.row_offsets, Ap.col_indices, Ap.values))
+    for i in range(60):
+        c = ci2[rp2[i]:rp2[i + 1]].astype(np.int64)
+        assert np.all(np.diff(c) > 0)
+        Dp[i, c] = v2[rp2[i]:rp2[i + 1]]
+    assert np.array_equal(Dp, D[np.ix_(perm, perm)])
