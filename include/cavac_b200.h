@@ -251,6 +251,11 @@ int cvk_ddm_rank_reports(const cvk_ddm_rank *rank, cvk_report *reps, int64_t cap
 /* the rank's columns col_begin[s_begin] .. col_begin[s_end]-1 of x, row-major
  * (ny rows x width complex) */
 int cvk_ddm_rank_solution(cvk_ddm_rank *rank, double *x_cols);
+/* the interface traces g_l, g_r of every slot ((n_strips + 1) x ny complex
+ * each, slot j = the cut left of local strip j): get / overwrite the state of
+ * the outer iteration (Krylov acceleration, paper_2112_00087_b200/ddm_krylov.py) */
+int cvk_ddm_rank_get_traces(cvk_ddm_rank *rank, double *g_l, double *g_r);
+int cvk_ddm_rank_set_traces(cvk_ddm_rank *rank, const double *g_l, const double *g_r);
 int cvk_ddm_rank_destroy(cvk_ddm_rank *rank);
 
 /* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */

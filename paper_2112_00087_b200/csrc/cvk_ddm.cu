@@ -558,6 +558,26 @@ extern "C" int cvk_ddm_rank_solution(cvk_ddm_rank* R, double* x_cols) {
     return CVK_OK;
 }
 
+// interface traces g_l, g_r of every slot ((ns + 1) x ny complex each):
+// the state of the outer iteration, for Krylov acceleration on the host
+extern "C" int cvk_ddm_rank_get_traces(cvk_ddm_rank* R, double* g_l, double* g_r) {
+    if (!R || !g_l || !g_r) return dfail(CVK_EINVAL, "ddm rank traces: null argument");
+    const size_t bytes = sizeof(double2) * (size_t)(R->ns + 1) * R->ny;
+    DK(cudaMemcpyAsync(g_l, R->d_gl, bytes, cudaMemcpyDeviceToHost, R->st));
+    DK(cudaMemcpyAsync(g_r, R->d_gr, bytes, cudaMemcpyDeviceToHost, R->st));
+    DK(cudaStreamSynchronize(R->st));
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_set_traces(cvk_ddm_rank* R, const double* g_l, const double* g_r) {
+    if (!R || !g_l || !g_r) return dfail(CVK_EINVAL, "ddm rank traces: null argument");
+    const size_t bytes = sizeof(double2) * (size_t)(R->ns + 1) * R->ny;
+    DK(cudaMemcpyAsync(R->d_gl, g_l, bytes, cudaMemcpyHostToDevice, R->st));
+    DK(cudaMemcpyAsync(R->d_gr, g_r, bytes, cudaMemcpyHostToDevice, R->st));
+    DK(cudaStreamSynchronize(R->st));
+    return CVK_OK;
+}
+
 extern "C" int cvk_ddm_rank_destroy(cvk_ddm_rank* R) {
     if (R) {
         cudaStreamSynchronize(R->st);

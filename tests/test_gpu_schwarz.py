@@ -186,3 +186,26 @@ def test_sequential_strip_solves_bitwise_batched(cvk, ddm, monkeypatch, solver):
     assert a.report.interface_residual_history == b.report.interface_residual_history
     assert a.report.total_inner_iterations == b.report.total_inner_iterations
     assert np.array_equal(bits(a.x), bits(b.x))
+
+
+@pytest.mark.parametrize("ns", [2, 4, 8])
+def test_krylov_interface_iteration(cvk, ddm, ns):
+    """GMRES on the interface equation (ddm_krylov.py): the same subdomain
+    problems and trace update as the reference's fixed-point sweep, far fewer
+    sweeps, and the monodomain solution (acceptance.cpp:277-291 tolerance)."""
+    from paper_2112_00087_b200.ddm_krylov import schwarz_solve_krylov
+    H, S = ddm
+    P = cvk
+    p = cavity_problem(H, 0.05)
+    k = p.omega / p.c
+    part = S.partition(p.grid, ns)
+    tp = S.TransmissionParams(complex(2.0, k), complex(2.0, k))
+    inner = P.SolverOptions(tol=1e-12)
+    fixed = S.schwarz_solve(p, part, tp, inner, 1e-8, 600)
+    kr = schwarz_solve_krylov(p, part, tp, inner, tol=1e-9, max_sweeps=300)
+    mono = P.bicgstab(p.A, p.b, P.jacobi(p.A), P.SolverOptions(tol=1e-12))
+    assert fixed.report.converged and kr.report.converged
+    assert kr.report.sweeps < fixed.report.outer_iterations / 2, (kr.report.sweeps, fixed.report.outer_iterations)
+    err = np.linalg.norm(kr.x - mono.x) / np.linalg.norm(mono.x)
+    assert err <= 1e-6, err
+    assert kr.report.residual_history[-1] <= 1e-9
