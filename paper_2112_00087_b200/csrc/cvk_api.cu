@@ -1062,9 +1062,10 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     // GMRES phase kernels from 32k rows (50k DOF: 58 vs 63 us per step; BiCGSTAB keeps the persistent kernel there)
     if (!ref && solver == CVK_GMRES && (long long)n >= std::min(phased_min_n(), 32768LL) && !std::getenv("CVK_GMRES_PERSISTENT"))
         return solve_gmres_phased(c, A, M, o, b_dev, x_dev, rep);
-    // BiCGSTAB(l) step kernel: opt-in; at 1M DOF it matches the persistent kernel
-    // (2443 vs 2382 us per l=8 cycle on the cavity, 3148 vs 3282 on 3-D FEM)
-    if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= phased_min_n() && std::getenv("CVK_BICGL_PHASED"))
+    // BiCGSTAB(l) step kernel from 131072 rows (1M DOF, l = 8: 2293 vs 2380 us
+    // per cycle on the cavity, 3007 vs 3085 on 3-D FEM; CVK_BICGL_PERSISTENT=1
+    // keeps the persistent kernel)
+    if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= phased_min_n() && !std::getenv("CVK_BICGL_PERSISTENT"))
         return solve_bicgl_phased(c, A, M, o, b_dev, x_dev, rep);
     if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n()) {
         const bool pinned = l2_pin(c, A);

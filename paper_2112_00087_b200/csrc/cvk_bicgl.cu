@@ -90,6 +90,29 @@ __device__ bool reduce_last(const CAcc (&acc)[K], double2* part, unsigned* count
     return true;
 }
 
+// element loop over the CTA's 256-row chunks (the ownership of for_rows),
+// U chunks per trip with every load of a trip issued before its stores:
+// the MGS phases are a few vector reads each, latency-bound one element at
+// a time (35 us for 48 MB at 1M DOF)
+template <int U, class LD, class STF>
+__device__ __forceinline__ void elems_batched(int n, int G, int cta, LD&& ld, STF&& stf) {
+    using T = decltype(ld(0));
+    const long long step = (long long)G * kThreads;
+    for (long long base = (long long)cta * kThreads + threadIdx.x; base < n; base += U * step) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * step;
+            if (i < n) v[u] = ld((int)i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = base + u * step;
+            if (i < n) stf((int)i, v[u]);
+        }
+    }
+}
+
 __device__ __forceinline__ void bhist(const BLArgs& a, BLState* st, double v) {
     if (!st->record) return;
     if (st->hl < st->hist_cap) a.hist[st->hl] = v;
@@ -156,7 +179,10 @@ __global__ void __launch_bounds__(kThreads) k_bl_init(BLArgs a) {
     start_cycle(st);
 }
 
-__global__ void __launch_bounds__(kThreads) k_bl_step(BLArgs a) {
+#ifndef CVK_BL_BATCH
+#define CVK_BL_BATCH 2  // measured at 1M DOF: 1 -> 2343, 2 -> 2293, 4 -> 2382 us per l=8 cycle
+#endif
+__global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
     pdl_enter_b();
     BLState* st = a.st;
     if (st->done) return;
@@ -261,12 +287,17 @@ __global__ void __launch_bounds__(kThreads) k_bl_step(BLArgs a) {
         const double2* ri1 = R(i + 1);
         const double2* r0 = R(0);
         CAcc acc[2] = {};
-        for_elems(n, G, cta, [&](int e) {
-            double2 v = rj1[e];
-            if (has_upd) { v = cvk_add(v, cvk_mul(ntau, rprev[e])); rj1[e] = v; }
-            if (!last) acc_dot(acc[0], ri1[e], v);
-            else { acc_dot(acc[0], v, v); acc_dot(acc[1], v, r0[e]); }
-        });
+        const double2* other = last ? r0 : ri1;
+        struct L3 { double2 rj, rp, o; };
+        elems_batched<CVK_BL_BATCH>(
+            n, G, cta,
+            [&](int e) { return L3{rj1[e], has_upd ? rprev[e] : make_double2(0.0, 0.0), other[e]}; },
+            [&](int e, const L3& l) {
+                double2 v = l.rj;
+                if (has_upd) { v = cvk_add(v, cvk_mul(ntau, l.rp)); rj1[e] = v; }
+                if (!last) acc_dot(acc[0], l.o, v);
+                else { acc_dot(acc[0], v, v); acc_dot(acc[1], v, l.o); }
+            });
         double2 tot[2];
         if (!reduce_last<2>(acc, a.part, &st->counter[0], tot)) return;
         if (threadIdx.x != 0) return;

@@ -427,9 +427,11 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
     M = P.jacobi(A)
     out = {}
     monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
-    for path, opt_in in (("persistent", None), ("phased", "1")):
-        if opt_in:
-            monkeypatch.setenv("CVK_BICGL_PHASED", opt_in)
+    for path in ("persistent", "phased"):
+        if path == "persistent":
+            monkeypatch.setenv("CVK_BICGL_PERSISTENT", "1")
+        else:
+            monkeypatch.delenv("CVK_BICGL_PERSISTENT", raising=False)
         out[path] = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(tol=1e-10, l=l, record_history=True))
     a_, b_ = out["persistent"], out["phased"]
     assert a_.report.converged and b_.report.converged
