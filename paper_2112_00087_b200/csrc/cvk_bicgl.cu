@@ -215,10 +215,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
             }
         });
         __syncthreads();
+        // u_q = r_q - beta u_q for q < j: the loads of four q's are issued
+        // before their stores (distinct slots), not one load-store chain per q
         for_elems(n, G, cta, [&](int i) {
-            for (int q = 0; q < j; ++q) {
-                double2* uq = U(q);
-                uq[i] = cvk_add(cvk_mul(nbeta, uq[i]), R(q)[i]);
+            for (int q0 = 0; q0 < j; q0 += 4) {
+                double2 uv[4], rv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < j) { uv[u] = U(q0 + u)[i]; rv[u] = R(q0 + u)[i]; }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < j) U(q0 + u)[i] = cvk_add(cvk_mul(nbeta, uv[u]), rv[u]);
             }
         });
         double2 tot[1];
@@ -250,9 +257,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
         __syncthreads();
         const double2* u0 = U(0);
         for_elems(n, G, cta, [&](int i) {
-            for (int q = 0; q < j; ++q) {
-                double2* rq = R(q);
-                rq[i] = cvk_add(rq[i], cvk_mul(nal, U(q + 1)[i]));
+            for (int q0 = 0; q0 < j; q0 += 4) {
+                double2 rv[4], uv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < j) { rv[u] = R(q0 + u)[i]; uv[u] = U(q0 + u + 1)[i]; }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < j) R(q0 + u)[i] = cvk_add(rv[u], cvk_mul(nal, uv[u]));
             }
             a.x[i] = cvk_add(a.x[i], cvk_mul(alpha, u0[i]));
             const double2 r0i = (j == 0) ? rj_new[i] : R(0)[i];
