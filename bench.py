@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "rowblock"],
                     help="N > 1: independent replicas (default), or one global solve over N row blocks "
                          "(rowblock.py, strong scaling)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="--mode rowblock: NCCL all-gathers, or the library's IPC mailbox exchange")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -369,14 +371,15 @@ def run_rowblock(args, dist, world, rank, local):
         dist.barrier()
         torch.cuda.synchronize()
 
+    run = eng.solve_p2p if args.exchange == "p2p" else eng.solve_nccl
     for _ in range(args.warmup):
-        eng.solve_nccl()
+        run()
         eng.result()
     reps = []
     with ClockSampler(local) as clk:
         barrier()
         for _ in range(args.steps):
-            eng.solve_nccl()
+            run()
             reps.append(eng.result()[1])
         barrier()
     t_solve = statistics.mean(r.device_time for r in reps)
@@ -386,7 +389,7 @@ def run_rowblock(args, dist, world, rank, local):
         barrier()
         t0 = time.perf_counter()
         e = RowBlockEngine(plan, b[plan.r0:plan.r1], d[plan.r0:plan.r1], opts)
-        e.solve_nccl()
+        e.solve_p2p() if args.exchange == "p2p" else e.solve_nccl()
         x_own, rep = e.result()
         e.close()
         barrier()
@@ -406,13 +409,14 @@ def run_rowblock(args, dist, world, rank, local):
         "warmup": args.warmup, "ms_per_step": t_solve * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128 (f64 complex)",
         "data": "synthetic (reference build_grid/assemble, roof Dirichlet 1+0i)",
-        "config": dict(workload_config(n, nnz), parallelism=f"row blocks x{world} (one global BiCGSTAB)"),
+        "config": dict(workload_config(n, nnz), parallelism=f"row blocks x{world} (one global BiCGSTAB)",
+                       exchange=args.exchange),
         "iterations": it, "converged": bool(reps[-1].converged), "final_relres": reps[-1].final_relres,
         "true_relres": reps[-1].true_relres, "seconds_per_iteration": t_solve / max(it, 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
                      "frac": achieved / (peak * world), "traffic": None,
                      "kernel": "row-block BiCGSTAB iteration (k_rb_a_s, k_rb_b_s, k_rb_c4, pack/post, "
-                               "3 ncclAllGather per iteration)", "bytes_per_iteration": iter_bytes,
+                               "3 exchanges per iteration)", "bytes_per_iteration": iter_bytes,
                      "peak_kind": peak_kind + f" x {world} GPUs"},
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": 20 * nnz + 48 * n,
                 "d2h_bytes_per_step": 16 * n},

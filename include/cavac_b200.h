@@ -337,6 +337,18 @@ int cvk_rowblock_solve_local(cvk_rowblock *const *rbs, int n);
 int cvk_nccl_unique_id(char *id);
 int cvk_rowblock_attach_nccl(cvk_rowblock *rb, const char *id, int rank);
 int cvk_rowblock_solve_nccl(cvk_rowblock *rb);
+/* peer-to-peer exchange without a collective library: each rank's pack
+ * kernel writes its slot into every rank's mailbox (NVLink stores through
+ * CUDA IPC mappings) and raises its flag there; the post kernel waits on its
+ * local flags (20 s without progress -> CVK_ETIMEOUT).  The handle is a
+ * cudaIpcMemHandle_t (64 bytes); `handles` holds all ranks' in rank order.
+ * _attach_local wires n blocks of one process together (same device). */
+int cvk_rowblock_p2p_handle(cvk_rowblock *rb, void *handle);
+int cvk_rowblock_p2p_attach(cvk_rowblock *rb, const void *handles, int rank);
+int cvk_rowblock_p2p_attach_local(cvk_rowblock *const *rbs, int n);
+/* the phase loop of p2p-attached blocks sharing one stream (one block per
+ * process on a multi-GPU node, or n blocks on one device) */
+int cvk_rowblock_solve_p2p(cvk_rowblock *const *rbs, int n);
 /* synchronises; *done = the solver's stop flag */
 int cvk_rowblock_done(cvk_rowblock *rb, int *done);
 /* after CVK_RB_X and CVK_RB_T: own rows of x (2 n_own doubles) and the report */

@@ -67,6 +67,13 @@ struct RBArgs {
     int capk;            // streamed SpMV phases: chunk nnz capacity, ring depths, L2 prefetch window
     int nst[2];
     int pf_rows;
+    // peer-to-peer exchange (cvk_rowblock_p2p_*): every rank's pack kernel
+    // writes its slot straight into every rank's mailbox (NVLink stores) and
+    // raises its flag there; the post kernel waits on the local flags.
+    int p2p, rank, flag_bytes;
+    unsigned char* const* peers;  // [nranks] mailbox bases (own included)
+    unsigned char* mbox;          // own mailbox: [flags | seq | 2 x nranks slots]
+    unsigned* pack_ctr;           // CTA arrivals of the pack kernel
 };
 
 enum { VX = 0, VR, VSH, VS, VT, VP0, VP1, VV0, VV1, kRbVecs };
@@ -118,11 +125,33 @@ __device__ void rank_total(const CAcc (&acc)[K], const RBArgs& a, unsigned* coun
     }
 }
 
+// mailbox pieces (p2p mode)
+__device__ __forceinline__ unsigned long long* mb_flags(unsigned char* base) { return (unsigned long long*)base; }
+__device__ __forceinline__ unsigned long long* mb_seq(const RBArgs& a) {
+    return (unsigned long long*)(a.mbox + a.flag_bytes);
+}
+__device__ __forceinline__ double* mb_data(unsigned char* base, const RBArgs& a, int parity) {
+    return (double*)(base + a.flag_bytes + 256) + (size_t)parity * a.nranks * a.slot;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // the ranks' totals of reduction k, folded in rank order
-__device__ double2 fold_ranks(const RBArgs& a, int k) {
+__device__ double2 fold_ranks(const RBArgs& a, int k, const double* recv) {
     CAcc s = {};
     for (int q = 0; q < a.nranks; ++q) {
-        const double* p = a.recv + (size_t)q * a.slot + 4 * k;
+        const double* p = recv + (size_t)q * a.slot + 4 * k;
         CAcc t;
         t.hi = make_double2(p[0], p[1]);
         t.lo = make_double2(p[2], p[3]);
@@ -389,6 +418,40 @@ __device__ __forceinline__ int phase_vecs(int ph, int cur, int (&v)[2]) {
 __global__ void __launch_bounds__(kThreads) k_rb_pack(RBArgs a, int ph) {
     pdl_wait();
     const PState* st = a.st;
+    if (a.p2p) {
+        // every phase: the header (this rank's totals) and the boundary values
+        // go to all mailboxes; the done test is the same on every rank
+        if (ph != CVK_RB_X && ph != CVK_RB_T && st->done) return;
+        const unsigned long long seq0 = *(volatile unsigned long long*)mb_seq(a);
+        const int parity = (int)((seq0 + 1) & 1);
+        int vv[2];
+        const int nvp = phase_vecs(ph, st->cur, vv);
+        const long long items = kHdr / 2 + (long long)a.n_send * nvp;
+        for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < items; i += (long long)gridDim.x * kThreads) {
+            double2 v;
+            if (i < kHdr / 2) {
+                v = ((const double2*)a.send)[i];
+            } else {
+                const long long e = i - kHdr / 2;
+                const int k = (int)(e / nvp), j = (int)(e - (long long)k * nvp);
+                v = vec(a, vv[j])[__ldg(a.send_rows + k)];
+            }
+            for (int q = 0; q < a.nranks; ++q)
+                ((double2*)(mb_data(a.peers[q], a, parity) + (size_t)a.rank * a.slot))[i] = v;
+        }
+        __shared__ int s_last;
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(a.pack_ctr, 1u) == gridDim.x - 1u;
+        __syncthreads();
+        if (!s_last || threadIdx.x != 0) return;
+        *a.pack_ctr = 0u;
+        __threadfence_system();
+        const unsigned long long seq = seq0 + 1;
+        *mb_seq(a) = seq;
+        for (int q = 0; q < a.nranks; ++q) st_release_sys(mb_flags(a.peers[q]) + a.rank, seq);
+        return;
+    }
     if (ph != CVK_RB_X && st->done) return;
     int vv[2];
     const int nvp = phase_vecs(ph, st->cur, vv);
@@ -405,6 +468,27 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
     pdl_wait();
     PState* st = a.st;
     if (ph != CVK_RB_X && ph != CVK_RB_T && st->done) return;
+    const double* recv = a.recv;
+    if (a.p2p) {
+        // wait until every rank has pushed this phase (its flag here reaches
+        // our sequence number); 20 s without progress aborts the solve
+        const unsigned long long seq = *(volatile unsigned long long*)mb_seq(a);
+        __shared__ int s_ok;
+        if (threadIdx.x == 0) {
+            int ok = 1;
+            const unsigned long long t0 = now_ns();
+            for (int q = 0; q < a.nranks && ok; ++q)
+                while (ld_acquire_sys(mb_flags(a.mbox) + q) < seq)
+                    if (now_ns() - t0 > 20000000000ull) { ok = 0; break; }
+            s_ok = ok;
+        }
+        __syncthreads();
+        if (!s_ok) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) { a.rep->error = 1; st->done = 1; }
+            return;
+        }
+        recv = mb_data(a.mbox, a, (int)(seq & 1));
+    }
     int vv[2];
     const int nvp = phase_vecs(ph, st->cur, vv);
     const long long total = (long long)a.n_halo * nvp;
@@ -412,13 +496,13 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
         const int h = (int)(i / nvp), j = (int)(i - (long long)h * nvp);
         const int src = __ldg(a.halo_src + h);
         const int q = src / a.max_send, k = src - q * a.max_send;
-        const double2* in = (const double2*)(a.recv + (size_t)q * a.slot + kHdr);
+        const double2* in = (const double2*)(recv + (size_t)q * a.slot + kHdr);
         vec(a, vv[j])[a.A.n + h] = in[(size_t)k * nvp + j];
     }
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     switch (ph) {
         case CVK_RB_INIT: {  // krylov.cpp:62-79
-            const double2 nr = fold_ranks(a, 0), rr = fold_ranks(a, 1);
+            const double2 nr = fold_ranks(a, 0, recv), rr = fold_ranks(a, 1, recv);
             st->bnorm = sqrt(nr.x);
             if (st->bnorm == 0.0) {
                 st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1;
@@ -434,7 +518,7 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
             return;
         }
         case CVK_RB_A: {  // krylov.cpp:97-103
-            const double2 sv = fold_ranks(a, 0);
+            const double2 sv = fold_ranks(a, 0, recv);
             if (cvk_abs(sv) < st->brk) {
                 st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
                 return;
@@ -443,7 +527,7 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
             return;
         }
         case CVK_RB_B: {  // krylov.cpp:104-122
-            const double2 ss = fold_ranks(a, 0), tt = fold_ranks(a, 1), ts = fold_ranks(a, 2);
+            const double2 ss = fold_ranks(a, 0, recv), tt = fold_ranks(a, 1, recv), ts = fold_ranks(a, 2, recv);
             const double relres = sqrt(ss.x) / st->bnorm;
             if (relres <= st->tol) {
                 st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
@@ -458,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
             return;
         }
         case CVK_RB_C: {  // krylov.cpp:123-133
-            const double2 rn = fold_ranks(a, 0), shr = fold_ranks(a, 1);
+            const double2 rn = fold_ranks(a, 0, recv), shr = fold_ranks(a, 1, recv);
             const double relres = sqrt(rn.x) / st->bnorm;
             st->final_relres = relres;
             st->iters = st->it;
@@ -474,7 +558,7 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
         case CVK_RB_T: {  // krylov.cpp:17-23, 135
             double trr = 0.0;
             if (!st->skip_true) {
-                const double bn = sqrt(fold_ranks(a, 0).x), rn = sqrt(fold_ranks(a, 1).x);
+                const double bn = sqrt(fold_ranks(a, 0, recv).x), rn = sqrt(fold_ranks(a, 1, recv).x);
                 trr = bn > 0 ? rn / bn : rn;
             }
             a.rep->converged = st->conv;
@@ -482,8 +566,7 @@ __global__ void __launch_bounds__(kThreads) k_rb_post(RBArgs a, int ph) {
             a.rep->iterations = st->iters;
             a.rep->final_relres = st->final_relres;
             a.rep->true_relres = trr;
-            a.rep->history_len = st->hist_len;
-            a.rep->error = 0;
+            a.rep->history_len = st->hist_len;  // rep->error: zeroed at CVK_RB_INIT, set by an aborted wait
             return;
         }
         default: return;
@@ -548,8 +631,13 @@ struct cvk_rowblock {
     ncclComm_t comm = nullptr;
     int rank = -1;
     PState st0{};  // initial solver state, restored by every CVK_RB_INIT (blocks are reusable)
+    unsigned char* mbox = nullptr;  // p2p mailbox (cudaMalloc'd: IPC-exportable)
+    size_t mbox_bytes = 0;
+    std::vector<void*> ipc_open;    // peers' mailboxes opened through CUDA IPC
+    unsigned char** d_peers = nullptr;
     ~cvk_rowblock() {
         if (comm) nccl_api().comm_destroy(comm);
+        for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
         for (void* p : bufs) cudaFree(p);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -712,6 +800,15 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
         (d->inv_diag && (e = R->alloc(&d_dinv, (size_t)d->n_own)) != cudaSuccess))
         return bail(rbfail(e == cudaErrorMemoryAllocation ? CVK_ENOMEM : CVK_ECUDA,
                            std::string("cvk_rowblock_create: ") + cudaGetErrorString(e)));
+    // p2p mailbox: [flags: nranks u64, 256-B padded | seq u64 | 2 x nranks slots]
+    const int flag_bytes = (int)(((d->n_ranks * 8 + 255) / 256) * 256);
+    R->mbox_bytes = (size_t)flag_bytes + 256 + sizeof(double) * 2 * (size_t)R->slot * d->n_ranks;
+    unsigned* d_pack_ctr = nullptr;
+    if ((e = R->alloc(&R->mbox, R->mbox_bytes)) != cudaSuccess || (e = R->alloc(&d_pack_ctr, 1)) != cudaSuccess ||
+        (e = R->alloc(&R->d_peers, (size_t)d->n_ranks)) != cudaSuccess ||
+        (e = cudaMemsetAsync(R->mbox, 0, R->mbox_bytes, R->s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(d_pack_ctr, 0, sizeof(unsigned), R->s)) != cudaSuccess)
+        return bail(rbfail(CVK_ECUDA, std::string("cvk_rowblock_create: mailbox: ") + cudaGetErrorString(e)));
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, R->s) : cudaSuccess;
     };
@@ -763,6 +860,12 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
     a.max_send = (int)std::max<int64_t>(1, d->max_send);
     a.halo_src = d_hs;
     a.n_halo = (int)d->n_halo;
+    a.p2p = 0;
+    a.rank = 0;
+    a.flag_bytes = flag_bytes;
+    a.peers = R->d_peers;
+    a.mbox = R->mbox;
+    a.pack_ctr = d_pack_ctr;
     *out = R;
     return CVK_OK;
 }
@@ -784,6 +887,7 @@ extern "C" int cvk_rowblock_local(cvk_rowblock* R, int ph) {
             R->t_wall0 = wall_now();
             R->launches = 0;
             RK(cudaMemcpyAsync(R->args.st, &R->st0, sizeof(PState), cudaMemcpyHostToDevice, R->s));
+            RK(cudaMemsetAsync(R->args.rep, 0, sizeof(cvk::DevReport), R->s));
             RK(cudaEventRecord(R->e0, R->s));
             f = (const void*)cvk::k_rb_init;
             break;
@@ -809,7 +913,10 @@ extern "C" int cvk_rowblock_local(cvk_rowblock* R, int ph) {
         RK(rb_launch(f, R->G, R->s, args));
         R->launches++;
     }
-    if (ph == CVK_RB_INIT || ph == CVK_RB_A || ph == CVK_RB_C || ph == CVK_RB_X) {
+    if (R->args.p2p) {
+        RK(rb_launch((const void*)cvk::k_rb_pack, R->Gx, R->s, args));
+        R->launches++;
+    } else if (ph == CVK_RB_INIT || ph == CVK_RB_A || ph == CVK_RB_C || ph == CVK_RB_X) {
         if (R->args.n_send > 0) {
             RK(rb_launch((const void*)cvk::k_rb_pack, R->Gx, R->s, args));
             R->launches++;
@@ -998,6 +1105,63 @@ extern "C" int cvk_rowblock_solve_nccl(cvk_rowblock* R) {
     });
 }
 
+extern "C" int cvk_rowblock_p2p_handle(cvk_rowblock* R, void* handle) {
+    if (!R || !handle) return rbfail(CVK_EINVAL, "cvk_rowblock_p2p_handle: null argument");
+    cudaIpcMemHandle_t h;
+    RK(cudaIpcGetMemHandle(&h, R->mbox));
+    std::memcpy(handle, &h, sizeof(h));
+    return CVK_OK;
+}
+
+namespace {
+int p2p_set(cvk_rowblock* R, const std::vector<unsigned char*>& bases, int rank) {
+    RK(cudaMemcpyAsync(R->d_peers, bases.data(), sizeof(unsigned char*) * bases.size(), cudaMemcpyHostToDevice, R->s));
+    RK(cudaStreamSynchronize(R->s));
+    R->args.p2p = 1;
+    R->args.rank = rank;
+    return CVK_OK;
+}
+}  // namespace
+
+extern "C" int cvk_rowblock_p2p_attach(cvk_rowblock* R, const void* handles, int rank) {
+    if (!R || !handles) return rbfail(CVK_EINVAL, "cvk_rowblock_p2p_attach: null argument");
+    const int n = R->args.nranks;
+    if (rank < 0 || rank >= n) return rbfail(CVK_EINVAL, "cvk_rowblock_p2p_attach: rank outside the plan");
+    std::vector<unsigned char*> bases((size_t)n, nullptr);
+    for (int q = 0; q < n; ++q) {
+        if (q == rank) { bases[q] = R->mbox; continue; }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, (const unsigned char*)handles + (size_t)q * sizeof(h), sizeof(h));
+        void* p = nullptr;
+        RK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        R->ipc_open.push_back(p);
+        bases[q] = (unsigned char*)p;
+    }
+    return p2p_set(R, bases, rank);
+}
+
+extern "C" int cvk_rowblock_p2p_attach_local(cvk_rowblock* const* rbs, int n) {
+    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_p2p_attach_local: no blocks");
+    std::vector<unsigned char*> bases((size_t)n);
+    for (int q = 0; q < n; ++q) {
+        if (!rbs[q] || rbs[q]->args.nranks != n) return rbfail(CVK_EINVAL, "cvk_rowblock_p2p_attach_local: plan mismatch");
+        bases[q] = rbs[q]->mbox;
+    }
+    for (int q = 0; q < n; ++q) {
+        const int e = p2p_set(rbs[q], bases, q);
+        if (e != CVK_OK) return e;
+    }
+    return CVK_OK;
+}
+
+extern "C" int cvk_rowblock_solve_p2p(cvk_rowblock* const* rbs, int n) {
+    if (!rbs || n < 1) return rbfail(CVK_EINVAL, "cvk_rowblock_solve_p2p: no blocks");
+    for (int q = 0; q < n; ++q)
+        if (!rbs[q] || !rbs[q]->args.p2p || rbs[q]->s != rbs[0]->s)
+            return rbfail(CVK_EINVAL, "cvk_rowblock_solve_p2p: blocks must be p2p-attached and share a stream");
+    return run_phases(rbs, n, [] { return CVK_OK; });
+}
+
 extern "C" int cvk_rowblock_result(cvk_rowblock* R, double* x_own, cvk_report* rep) {
     if (!R) return rbfail(CVK_EINVAL, "cvk_rowblock_result: null block");
     cvk::DevReport dr;
@@ -1005,6 +1169,7 @@ extern "C" int cvk_rowblock_result(cvk_rowblock* R, double* x_own, cvk_report* r
     if (x_own && R->n_own > 0)
         RK(cudaMemcpyAsync(x_own, R->args.work, sizeof(double2) * R->n_own, cudaMemcpyDeviceToHost, R->s));
     RK(cudaStreamSynchronize(R->s));
+    if (dr.error) return rbfail(CVK_ETIMEOUT, "row-block solve: a peer stopped answering (p2p exchange wait aborted)");
     if (rep) {
         rep->converged = dr.converged;
         rep->breakdown = dr.breakdown;

@@ -65,8 +65,12 @@ def _bind(L):
     L.cvk_nccl_unique_id.restype = i32
     L.cvk_rowblock_attach_nccl.argtypes = [P, C.c_char_p, i32]
     L.cvk_rowblock_solve_nccl.argtypes = [P]
+    L.cvk_rowblock_p2p_handle.argtypes = [P, P]
+    L.cvk_rowblock_p2p_attach.argtypes = [P, C.c_char_p, i32]
+    L.cvk_rowblock_p2p_attach_local.argtypes = [C.POINTER(P), i32]
+    L.cvk_rowblock_solve_p2p.argtypes = [C.POINTER(P), i32]
     for f in ("create", "exchange", "local", "post", "exchange_local", "solve_local", "done", "result", "destroy",
-              "attach_nccl", "solve_nccl"):
+              "attach_nccl", "solve_nccl", "p2p_handle", "p2p_attach", "p2p_attach_local", "solve_p2p"):
         getattr(L, "cvk_rowblock_" + f).restype = i32
     L._rb_bound = True
 
@@ -265,6 +269,24 @@ class RowBlockEngine:
         self._nccl_attached = True
         _lib.check(self.L.cvk_rowblock_solve_nccl(self.h))
 
+    def solve_p2p(self, group=None) -> None:
+        """The phase loop with the library's own peer-to-peer exchange: every
+        rank's mailbox is mapped into every other rank through CUDA IPC
+        (handles all-gathered over the torch.distributed group once), the
+        pack kernels store into the peers' mailboxes and the post kernels
+        wait on local flags -- no collective library on the data path."""
+        import torch.distributed as dist
+        if not getattr(self, "_p2p_attached", False):
+            h = C.create_string_buffer(64)
+            _lib.check(self.L.cvk_rowblock_p2p_handle(self.h, h))
+            allh = [None] * dist.get_world_size(group)
+            dist.all_gather_object(allh, h.raw, group=group)
+            _lib.check(self.L.cvk_rowblock_p2p_attach(self.h, b"".join(allh), self.plan.rank))
+            self._p2p_attached = True
+            dist.barrier(group=group)
+        arr = (P * 1)(self.h)
+        _lib.check(self.L.cvk_rowblock_solve_p2p(arr, 1))
+
     def local(self, ph: int) -> None:
         _lib.check(self.L.cvk_rowblock_local(self.h, ph))
 
@@ -343,7 +365,7 @@ def _unpermute(res: SolveResult, perm) -> SolveResult:
 
 def solve_row_blocks(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, n_blocks: int = 2,
                      bounds: Optional[np.ndarray] = None, dev: Optional[Device] = None,
-                     coords=None) -> SolveResult:
+                     coords=None, p2p: bool = False) -> SolveResult:
     """BiCGSTAB over n_blocks row blocks on one device: every block runs the
     multi-rank kernels, the all-gather is a device copy (same stream).  With
     `coords` (one point per row, e.g. FemCavity.coords()) the blocks are RCB
@@ -354,13 +376,17 @@ def solve_row_blocks(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOp
     if coords is not None:
         Ap, bp, dp, perm, bnd = _rcb_system(A, b, d, coords, n_blocks)
         Mp = Preconditioner("identity") if dp is None else Preconditioner("jacobi", dp)
-        return _unpermute(solve_row_blocks(Ap, bp, Mp, opts, n_blocks, bnd, dev), perm)
+        return _unpermute(solve_row_blocks(Ap, bp, Mp, opts, n_blocks, bnd, dev, p2p=p2p), perm)
     plans = plan_row_blocks(A, n_blocks, bounds)
     engines = [RowBlockEngine(pl, b[pl.r0:pl.r1], None if d is None else d[pl.r0:pl.r1], opts, dev) for pl in plans]
     try:
         L = engines[0].L
         arr = (P * n_blocks)(*[e.h for e in engines])
-        _lib.check(L.cvk_rowblock_solve_local(arr, n_blocks))
+        if p2p:  # the mailbox exchange of the multi-GPU p2p path, blocks wired in-process
+            _lib.check(L.cvk_rowblock_p2p_attach_local(arr, n_blocks))
+            _lib.check(L.cvk_rowblock_solve_p2p(arr, n_blocks))
+        else:
+            _lib.check(L.cvk_rowblock_solve_local(arr, n_blocks))
         xs, reps = zip(*[e.result() for e in engines])
     finally:
         for e in engines:
@@ -413,13 +439,16 @@ EngineFactory = Callable[[RowBlockPlan, np.ndarray, Optional[np.ndarray], Solver
 
 def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverOptions] = None, group=None,
                       bounds: Optional[np.ndarray] = None, engine_factory: Optional[EngineFactory] = None,
-                      gather_solution: bool = True, use_library_nccl: bool = True, coords=None) -> SolveResult:
+                      gather_solution: bool = True, use_library_nccl: bool = True, coords=None,
+                      exchange: str = "collective") -> SolveResult:
     """BiCGSTAB (krylov.cpp:57-138) with one row block per rank of a
     torch.distributed group (initialised by the caller).  With device engines
     on an NCCL group the library runs the whole loop over its own NCCL
     communicator (use_library_nccl; otherwise the phases are issued from here
     with torch's NCCL all-gather on the library's stream); gloo stages the
-    exchange through host.  Every rank returns the same report; x is the full
+    exchange through host.  exchange="p2p" replaces the collective with the
+    library's mailbox exchange over CUDA IPC peer mappings (device engines;
+    one GPU per rank).  Every rank returns the same report; x is the full
     solution (gather_solution) or the rank's own rows.  `coords` makes the
     ranks' blocks RCB parts (as in solve_row_blocks; x is then always the full
     solution in the original numbering)."""
@@ -430,13 +459,16 @@ def solve_distributed(A: CsrMatrix, b, M: Preconditioner, opts: Optional[SolverO
     if coords is not None:
         Ap, bp, dp, perm, bnd = _rcb_system(A, b, d, coords, world)
         Mp = Preconditioner("identity") if dp is None else Preconditioner("jacobi", dp)
-        res = solve_distributed(Ap, bp, Mp, opts, group, bnd, engine_factory, True, use_library_nccl)
+        res = solve_distributed(Ap, bp, Mp, opts, group, bnd, engine_factory, True, use_library_nccl,
+                                exchange=exchange)
         return _unpermute(res, perm)
     plan = plan_row_blocks(A, world, bounds)[rank]
     factory = engine_factory or (lambda pl, bo, do, o: RowBlockEngine(pl, bo, do, o))
     eng = factory(plan, b[plan.r0:plan.r1], None if d is None else d[plan.r0:plan.r1], opts)
     try:
-        if isinstance(eng, RowBlockEngine) and dist.get_backend(group) == "nccl" and use_library_nccl:
+        if isinstance(eng, RowBlockEngine) and exchange == "p2p":
+            eng.solve_p2p(group)
+        elif isinstance(eng, RowBlockEngine) and dist.get_backend(group) == "nccl" and use_library_nccl:
             eng.solve_nccl(group)
         else:
             xchg = _Exchange(eng, group)

@@ -191,3 +191,55 @@ def test_rcb_blocks_on_renumbered_fem_mesh(cvk):
     assert abs(got.report.iterations - ref.report.iterations) <= max(3, 0.15 * ref.report.iterations)
     x = got.x[np.argsort(shuffle)]
     assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("n_blocks", [1, 2, 3, 5])
+def test_p2p_mailbox_exchange_bitwise(cvk, n_blocks):
+    """The peer-to-peer mailbox exchange (pack kernels store every rank's slot
+    into all mailboxes and raise flags, post kernels wait on them) with the
+    blocks wired in-process on one device: bitwise the single-device solve."""
+    from paper_2112_00087_b200.rowblock import solve_row_blocks
+    P = cvk
+    for h in (0.05, 0.004):
+        A, b = cavity(h)
+        M = P.jacobi(A)
+        o = P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000)
+        ref = P.solve(P.SolverId.BiCGStab, A, b, M, o)
+        _same(solve_row_blocks(A, b, M, o, n_blocks=n_blocks, p2p=True), ref)
+
+
+def _p2p_worker(port, q, h):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        import paper_2112_00087_b200 as P
+        from paper_2112_00087_b200.rowblock import solve_distributed
+        A, b = cavity(h)
+        o = P.SolverOptions(tol=1e-9, record_history=True, max_iter=20000)
+        r = solve_distributed(A, b, P.jacobi(A), o, exchange="p2p")
+        q.put((r.x, r.report.iterations, list(r.report.residual_history)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_p2p_plumbing_one_rank(cvk):
+    """solve_distributed(exchange="p2p"): IPC handle export, the all-gather of
+    handles over the group and attach, then the graph-captured mailbox loop;
+    one rank here (one GPU)."""
+    import multiprocessing as mp
+    P = cvk
+    h = 0.0075
+    A, b = cavity(h)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, P.jacobi(A), P.SolverOptions(tol=1e-9, record_history=True,
+                                                                           max_iter=20000))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_p2p_worker, args=(_free_port(), q, h))
+    p.start()
+    x, it, hist = q.get(timeout=900)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert it == ref.report.iterations and hist == ref.report.residual_history
+    assert np.array_equal(bits(x), bits(ref.x))
