@@ -243,3 +243,27 @@ def test_distributed_p2p_plumbing_one_rank(cvk):
     assert p.exitcode == 0
     assert it == ref.report.iterations and hist == ref.report.residual_history
     assert np.array_equal(bits(x), bits(ref.x))
+
+
+def test_p2p_edge_cases(cvk):
+    """p2p exchange with an empty block, the identity preconditioner, zero
+    rhs and an exhausted iteration budget; and RCB blocks with p2p."""
+    from paper_2112_00087_b200.rowblock import solve_row_blocks
+    P = cvk
+    A, b = cavity(0.05)
+    M = P.jacobi(A)
+    I = P.identity_preconditioner()
+    o = P.SolverOptions(tol=1e-8, record_history=True)
+    _same(solve_row_blocks(A, b, I, o, n_blocks=3, bounds=np.array([0, 0, 500, A.nrows]), p2p=True),
+          P.solve(P.SolverId.BiCGStab, A, b, I, o))
+    z = solve_row_blocks(A, np.zeros_like(b), M, P.SolverOptions(), n_blocks=2, p2p=True)
+    assert z.report.converged and z.report.iterations == 0 and not np.any(z.x)
+    e = solve_row_blocks(A, b, M, P.SolverOptions(max_iter=3), n_blocks=4, p2p=True)
+    r = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(max_iter=3))
+    assert not e.report.converged and e.report.iterations == 3
+    assert np.array_equal(bits(e.x), bits(r.x))
+    g = np.stack(np.meshgrid(np.arange(47.0), np.arange(23.0), indexing="xy"), -1).reshape(-1, 2)
+    q = solve_row_blocks(A, b, M, P.SolverOptions(tol=1e-11), n_blocks=4, coords=g, p2p=True)
+    ref = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-11))
+    assert q.report.converged
+    assert np.linalg.norm(q.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
