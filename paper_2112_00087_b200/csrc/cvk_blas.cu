@@ -14,6 +14,10 @@
 #include "cvk_kernels.h"
 #include "cvk_stream.cuh"
 
+#ifndef CVK_SPMV_BATCH
+#define CVK_SPMV_BATCH 5  // (value, column) loads in flight per row in the streamed SpMV
+#endif
+
 namespace cvk {
 
 template <int S, bool REF>
@@ -34,7 +38,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_spmv_s(Csr A, StreamLayou
     extern __shared__ __align__(128) unsigned char smem[];
     const double2* vecs[1] = {x};
     stream_rows(A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        const double2 acc = chunk_row_sum<5>(ch, t, [&](int l) { return ch.v(0, l); },
+        const double2 acc = chunk_row_sum<CVK_SPMV_BATCH>(ch, t, [&](int l) { return ch.v(0, l); },
                                              [&](int c) { return __ldg(x + c); });
         __stcs(y + ch.r0 + t, acc);
     });

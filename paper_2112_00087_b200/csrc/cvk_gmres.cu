@@ -22,6 +22,10 @@
 #include "cvk_kernels.h"
 #include "cvk_stream.cuh"
 
+#ifndef CVK_SPMV_BATCH
+#define CVK_SPMV_BATCH 5  // (value, column) loads in flight per row in the streamed SpMV
+#endif
+
 namespace cvk {
 
 namespace {
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_g_spmv_s(GArgs a) {
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 { return ch.v(0, l); };
         auto xg = [&](int c) -> double2 { return cvk_divr(src[c], sc); };
-        const double2 y = chunk_row_sum<5>(ch, t, xs, xg);
+        const double2 y = chunk_row_sum<CVK_SPMV_BATCH>(ch, t, xs, xg);
         const int row = ch.r0 + t;
         vj[row] = xs(t);
         w[row] = a.dinv ? cvk_mul(ch.v(1, t), y) : y;

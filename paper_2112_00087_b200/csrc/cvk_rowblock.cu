@@ -45,7 +45,7 @@ namespace cvk {
 namespace {
 
 constexpr int kHdr = 16;   // exchange slot header: up to 4 complex dd totals (hi.x hi.y lo.x lo.y)
-constexpr int kRbBatch = 5;
+constexpr int kRbBatch = 2;  // as cvk_phased.cu CVK_BATCH
 
 struct RBArgs {
     Csr A;               // n = own rows; columns < n_own + n_halo
