@@ -355,6 +355,22 @@ int cvk_rowblock_done(cvk_rowblock *rb, int *done);
 int cvk_rowblock_result(cvk_rowblock *rb, double *x_own, cvk_report *rep);
 int cvk_rowblock_destroy(cvk_rowblock *rb);
 
+/* ---- Matrix Market I/O at scale (host; read_matrix_market /
+ * write_matrix_market, mmio.cpp:10-63, + csr_from_triplets, numkit.cpp:41-75).
+ * The reader parses with nthreads threads (<= 0: all cores) and returns the
+ * CSR the reference builds (duplicates summed in input order, columns
+ * sorted); arrays are malloc'd, release them with cvk_mm_free.  The writer
+ * prints "%.17g" values, byte-identical to the reference's writer. ---- */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    uint64_t *row_offsets; /* nrows + 1 */
+    uint64_t *col_indices; /* nnz, 0-based */
+    double *values;        /* 2 nnz, interleaved complex */
+} cvk_mm_matrix;
+int cvk_mm_read(const char *path, int nthreads, cvk_mm_matrix *out);
+void cvk_mm_free(cvk_mm_matrix *m);
+int cvk_mm_write(const char *path, const cvk_mm_matrix *m, int nthreads);
+
 /* ---- SpMV timing helper for the bench: `reps` back-to-back launches on
  * device buffers, returns the average kernel time in seconds ---- */
 int cvk_spmv_bench(const cvk_csr *A, const double *x_dev, double *y_dev, int mode,
