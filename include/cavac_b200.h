@@ -158,6 +158,12 @@ int cvk_solve_device(cvk_ctx *ctx, int solver, const cvk_csr *A, const cvk_prec 
                      const cvk_opts *opts, const double *b_dev, double *x_dev,
                      cvk_report *rep);
 
+/* BiCGSTAB from the x0 in x_dev (beyond the reference, whose solvers start
+ * from 0): r0 = M^-1 (b - A x0); relative residuals stay measured against
+ * ||M^-1 b||.  Used for warm-started Schwarz inner solves. */
+int cvk_solve_device_warm(cvk_ctx *ctx, const cvk_csr *A, const cvk_prec *M, const cvk_opts *opts,
+                          const double *b_dev, double *x_dev, cvk_report *rep);
+
 /* ---- kernels (parity tests; mode = CVK_MODE_*) ---- */
 int cvk_spmv(const cvk_csr *A, const double *x, double *y, int mode);
 int cvk_spmv_device(const cvk_csr *A, const double *x_dev, double *y_dev, int mode);
@@ -256,6 +262,10 @@ int cvk_ddm_rank_solution(cvk_ddm_rank *rank, double *x_cols);
  * the outer iteration (Krylov acceleration, paper_2112_00087_b200/ddm_krylov.py) */
 int cvk_ddm_rank_get_traces(cvk_ddm_rank *rank, double *g_l, double *g_r);
 int cvk_ddm_rank_set_traces(cvk_ddm_rank *rank, const double *g_l, const double *g_r);
+/* warm-started inner solves (beyond the reference; BiCGSTAB inner solver):
+ * each strip's solve starts from its previous-sweep solution.  Also set for
+ * cvk_schwarz_solve by the environment variable CVK_DDM_WARM=1. */
+int cvk_ddm_rank_set_warm(cvk_ddm_rank *rank, int warm);
 int cvk_ddm_rank_destroy(cvk_ddm_rank *rank);
 
 /* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */

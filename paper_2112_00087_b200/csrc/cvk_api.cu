@@ -53,6 +53,8 @@ struct cvk_ctx {
     std::vector<unsigned char> gm_key;
     // phase-kernel BiCGSTAB(l)
     void* bst = nullptr;  // cvk::BLState
+    // the next BiCGSTAB solve starts from the x passed in (cvk_solve_device_warm)
+    int warm_next = 0;
     cudaGraphExec_t bl_exec = nullptr;
     std::vector<unsigned char> bl_key;
 };
@@ -598,6 +600,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     hs.record = o->record_history ? 1 : 0;
     hs.hist_cap = hcap;
     if (o->max_iter < 1) hs.max_iter = 0;
+    hs.warm = (solver == CVK_BICGSTAB && c->warm_next) ? 1 : 0;
     // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
@@ -626,7 +629,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // (CVK_BICG_MERGED=1).  Measured 152 vs 142 us per iteration at 1M DOF:
     // one launch fewer and 16 n fewer bytes, but the merged SpMV phase (7
     // staged, 4 gathered vectors) is consumer-bound.
-    const bool merged = streamed && solver == CVK_BICGSTAB && std::min(stg[4], stg[5]) >= 2 &&
+    const bool merged = streamed && solver == CVK_BICGSTAB && std::min(stg[4], stg[5]) >= 2 && !hs.warm &&
                         std::getenv("CVK_BICG_MERGED") && std::atoi(std::getenv("CVK_BICG_MERGED")) == 1;
     auto smem_for = [&](int k) { return layout_for(k, stg[k]).smem_bytes(); };
     const void* sk[6] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.bm_a_s, K.bm_b_s};
@@ -1054,7 +1057,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     // of shared memory resident for the whole solve the L1 left for global
     // loads is too small for the element phase's memory-level parallelism
     // (40 vs 14 us), and the merged phases spill (tools/trace_streamk.py).
-    if (!ref && solver == CVK_BICGSTAB && (long long)n >= phased_min_n() &&
+    if (!ref && solver == CVK_BICGSTAB && (long long)n >= phased_min_n() && !c->warm_next &&
         std::getenv("CVK_STREAMK") && std::atoi(std::getenv("CVK_STREAMK")) == 1 && !std::getenv("CVK_NO_STREAM")) {
         const int rc = solve_streamk(c, A, M, o, b_dev, x_dev, rep);
         if (rc != 1) return rc;
@@ -1118,6 +1121,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     a.record = o->record_history ? 1 : 0;
     a.G = (int)G;
     a.cta_base = 0;
+    a.warm = (solver == CVK_BICGSTAB && c->warm_next) ? 1 : 0;
     void* args[] = {&a};
     CK(cudaEventRecord(c->e0, c->stream));
     CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kThreads), args, smem, c->stream));
@@ -1149,6 +1153,15 @@ int cvk_solve_device(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M
     const double t0 = now_s();
     const int e = solve_impl(c, solver, A, M, o, (const double2*)b_dev, (double2*)x_dev, rep);
     if (e == CVK_OK) rep->wall_time_s = now_s() - t0;
+    return e;
+}
+
+int cvk_solve_device_warm(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o, const double* b_dev,
+                          double* x_dev, cvk_report* rep) {
+    if (!c) return fail(CVK_EINVAL, "null ctx");
+    c->warm_next = 1;
+    const int e = cvk_solve_device(c, CVK_BICGSTAB, A, M, o, b_dev, x_dev, rep);
+    c->warm_next = 0;
     return e;
 }
 

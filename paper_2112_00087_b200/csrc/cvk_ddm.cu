@@ -262,6 +262,9 @@ struct cvk_ddm_rank {
     // solves run one after another on the single-system path (TMA-streamed
     // phase kernels), not as CTA segments of one batched persistent launch
     bool seq = false;
+    // warm start (beyond the reference): each inner BiCGSTAB starts from the
+    // strip's previous-sweep solution instead of 0
+    bool warm = false;
     std::vector<cvk_csr*> seq_A;
     std::vector<cvk_prec*> seq_M;
     std::vector<int64_t> off;
@@ -335,6 +338,7 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
     DK(mem.alloc(&R->d_b, n));
     DK(mem.alloc(&R->d_rhs, ntot));
     DK(mem.alloc(&R->d_u, ntot));
+    DK(cudaMemsetAsync(R->d_u, 0, sizeof(double2) * ntot, st));  // x0 of a warm-started first sweep
     DK(mem.alloc(&R->d_gl, nslot));
     DK(mem.alloc(&R->d_gr, nslot));
     DK(mem.alloc(&R->d_prev, 2 * nslot));
@@ -421,6 +425,8 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
     }
     R->total_ctas = cta_base;
     R->off.assign(h_off.begin(), h_off.end());
+    R->warm = inner_solver == CVK_BICGSTAB && std::getenv("CVK_DDM_WARM") && std::atoi(std::getenv("CVK_DDM_WARM")) == 1;
+    for (int64_t j = 0; j < ns; ++j) segs[j].warm = R->warm ? 1 : 0;
     R->inner_opts = *inner;
     R->inner_opts.record_history = 0;
     R->inner_opts.mode = R->mode;
@@ -487,9 +493,11 @@ extern "C" int cvk_ddm_rank_sweep(cvk_ddm_rank* R, const double* g_in_left, cons
     if (R->seq) {
         for (int64_t j = 0; j < ns; ++j) {
             cvk_report rep{};
-            const int e = cvk_solve_device(R->ctx, R->solver, R->seq_A[j], R->seq_M[j], &R->inner_opts,
-                                           reinterpret_cast<const double*>(R->d_rhs + R->off[j]),
-                                           reinterpret_cast<double*>(R->d_u + R->off[j]), &rep);
+            const double* bj = reinterpret_cast<const double*>(R->d_rhs + R->off[j]);
+            double* uj = reinterpret_cast<double*>(R->d_u + R->off[j]);
+            const int e = R->warm ? cvk_solve_device_warm(R->ctx, R->seq_A[j], R->seq_M[j], &R->inner_opts, bj, uj, &rep)
+                                  : cvk_solve_device(R->ctx, R->solver, R->seq_A[j], R->seq_M[j], &R->inner_opts, bj,
+                                                     uj, &rep);
             if (e != CVK_OK) return e;
             DevReport& d = R->hr[j];
             d.converged = rep.converged;
@@ -555,6 +563,17 @@ extern "C" int cvk_ddm_rank_solution(cvk_ddm_rank* R, double* x_cols) {
     DK(cudaGetLastError());
     DK(cudaMemcpyAsync(x_cols, R->d_x, sizeof(double2) * R->ntot, cudaMemcpyDeviceToHost, R->st));
     DK(cudaStreamSynchronize(R->st));
+    return CVK_OK;
+}
+
+extern "C" int cvk_ddm_rank_set_warm(cvk_ddm_rank* R, int warm) {
+    if (!R) return dfail(CVK_EINVAL, "ddm rank warm: null rank");
+    if (warm && R->solver != CVK_BICGSTAB) return dfail(CVK_EINVAL, "ddm rank warm: BiCGSTAB inner solves only");
+    R->warm = warm != 0;
+    std::vector<cvk::KArgs> segs((size_t)R->ns);
+    DK(cudaMemcpy(segs.data(), R->d_segs, sizeof(cvk::KArgs) * R->ns, cudaMemcpyDeviceToHost));
+    for (cvk::KArgs& a : segs) a.warm = R->warm ? 1 : 0;
+    DK(cudaMemcpy(R->d_segs, segs.data(), sizeof(cvk::KArgs) * R->ns, cudaMemcpyHostToDevice));
     return CVK_OK;
 }
 

@@ -71,6 +71,7 @@ struct KArgs {
     int record;
     int G;
     int cta_base;  // first CTA of this solve in a batched launch
+    int warm;      // BiCGSTAB only: x holds x0 (r0 = M^-1 (b - A x0)); 0 = the reference's x0 = 0
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {

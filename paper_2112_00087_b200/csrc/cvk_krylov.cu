@@ -87,18 +87,34 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
     for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
     long long hl = 0;
 
-    // r = M^{-1} b, shadow = r, x = 0; ||r||^2 and <shadow, r>
+    // r = M^{-1} b, shadow = r, x = 0; ||r||^2 and <shadow, r>.  Warm start
+    // (beyond the reference, Schwarz inner solves): r = M^{-1} (b - A x0) and
+    // the same bnorm = ||M^{-1} b|| the relative residuals are measured by.
     CAcc acc0[2] = {};
-    for_elems(n, G, g.cta, [&](int i) {
-        const double2 ri = prec_apply(dinv, i, __ldg(b + i));
-        r[i] = ri;
-        sh[i] = ri;
-        x[i] = make_double2(0.0, 0.0);
-        if (!REF) { acc_norm(acc0[0], ri); acc_dot(acc0[1], ri, ri); }
-    });
+    if (a.warm) {
+        auto xat = [&](int c) -> double2 { return x[c]; };
+        for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, lane, valid, xat);
+            if (valid && lane == 0) {
+                const double2 bi = __ldg(b + row);
+                const double2 ri = prec_apply(dinv, row, cvk_sub(bi, y));
+                r[row] = ri;
+                sh[row] = ri;
+                if (!REF) { acc_norm(acc0[0], prec_apply(dinv, row, bi)); acc_dot(acc0[1], ri, ri); }
+            }
+        });
+    } else {
+        for_elems(n, G, g.cta, [&](int i) {
+            const double2 ri = prec_apply(dinv, i, __ldg(b + i));
+            r[i] = ri;
+            sh[i] = ri;
+            x[i] = make_double2(0.0, 0.0);
+            if (!REF) { acc_norm(acc0[0], ri); acc_dot(acc0[1], ri, ri); }
+        });
+    }
     double2 t0[2];
     if (!reduce<REF, 2>(g, acc0, t0, part[0], n, [&](int i, double2* q) {
-            acc_norm(q[0], r[i]);
+            acc_norm(q[0], a.warm ? prec_apply(dinv, i, __ldg(b + i)) : r[i]);
             acc_dot(q[1], sh[i], r[i]);
         })) {
         write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1);

@@ -184,14 +184,30 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(PArgs a) {
     const int n = a.A.n;
     BiVecs V(a.work, (size_t)n);
     CAcc acc[2] = {};
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
-        V.r[i] = ri;
-        V.sh[i] = ri;
-        a.x[i] = make_double2(0.0, 0.0);
-        acc_norm(acc[0], ri);
-        acc_dot(acc[1], ri, ri);
-    });
+    if (a.st->warm) {  // r = M^-1 (b - A x0), bnorm = ||M^-1 b|| (cvk_krylov.cu bicgstab_body)
+        const double2* __restrict__ x = a.x;
+        auto xat = [&](int c) -> double2 { return x[c]; };
+        for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
+            const double2 y = row_sum<1, decltype(xat)&, kBatch>(a.A, row, 0, valid, xat);
+            if (valid) {
+                const double2 bi = __ldg(a.b + row);
+                const double2 ri = prec_apply(a.dinv, row, cvk_sub(bi, y));
+                V.r[row] = ri;
+                V.sh[row] = ri;
+                acc_norm(acc[0], prec_apply(a.dinv, row, bi));
+                acc_dot(acc[1], ri, ri);
+            }
+        });
+    } else {
+        for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
+            const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
+            V.r[i] = ri;
+            V.sh[i] = ri;
+            a.x[i] = make_double2(0.0, 0.0);
+            acc_norm(acc[0], ri);
+            acc_dot(acc[1], ri, ri);
+        });
+    }
     double2 tot[2];
     if (!partial_last<2>(acc, partv(a, 0), &a.st->counter[0], tot)) return;
     if (threadIdx.x != 0) return;

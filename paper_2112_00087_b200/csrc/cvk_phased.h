@@ -18,6 +18,7 @@ struct PState {
     double bnorm, brk, tol, final_relres, tau, theta;
     long long it, iters, max_iter, hist_len, hist_cap;
     int done, conv, brk_code, first, pending_x, cur, record, skip_true;
+    int warm;  // BiCGSTAB: start from the x passed in (k_bi_init)
     unsigned counter[4];
     unsigned chunk_ctr[4];  // dynamic chunk counters of the streamed kernels (reset by their last CTA)
 };

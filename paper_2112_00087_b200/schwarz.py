@@ -97,7 +97,23 @@ def _grid(g: CavityGrid) -> CvkGrid:
 def schwarz_solve(problem: HelmholtzProblem, part: Partition, tp: TransmissionParams,
                   inner: SolverOptions, ddm_tol: float, max_outer: int,
                   inner_solver: SolverId = SolverId.BiCGStab,
-                  mode: Optional[ExecMode] = None) -> DdmResult:
+                  mode: Optional[ExecMode] = None, warm_start: bool = False) -> DdmResult:
+    """schwarz_solve (schwarz.cpp:111-238).  warm_start (beyond the reference,
+    BiCGSTAB inner solver): each strip's inner solve starts from its
+    previous-sweep solution instead of 0."""
+    if warm_start:
+        if SolverId(inner_solver) != SolverId.BiCGStab:
+            raise InvalidArgument("schwarz_solve: warm_start needs the bicgstab inner solver")
+        import os
+        old = os.environ.get("CVK_DDM_WARM")
+        os.environ["CVK_DDM_WARM"] = "1"
+        try:
+            return schwarz_solve(problem, part, tp, inner, ddm_tol, max_outer, inner_solver, mode)
+        finally:
+            if old is None:
+                os.environ.pop("CVK_DDM_WARM", None)
+            else:
+                os.environ["CVK_DDM_WARM"] = old
     L = _setup_lib()
     A = problem.A
     n = A.nrows

@@ -209,3 +209,55 @@ def test_krylov_interface_iteration(cvk, ddm, ns):
     err = np.linalg.norm(kr.x - mono.x) / np.linalg.norm(mono.x)
     assert err <= 1e-6, err
     assert kr.report.residual_history[-1] <= 1e-9
+
+
+def test_warm_started_inner_solves(cvk, ddm, monkeypatch):
+    """Warm-started inner BiCGSTAB (beyond the reference): the same DDM
+    solution as the reference's cold starts (monodomain tolerance) with fewer
+    inner iterations, bitwise the same on the batched persistent and the
+    sequential phase-kernel paths; and a warm start from x0 = 0 is bitwise a
+    cold solve on both single-system paths."""
+    H, S = ddm
+    P = cvk
+    from paper_2112_00087_b200 import _lib
+    import ctypes as C
+    p = cavity_problem(H, 0.05)
+    k = p.omega / p.c
+    part = S.partition(p.grid, 4)
+    tp = S.TransmissionParams(complex(2.0, k), complex(2.0, k))
+    inner = P.SolverOptions(tol=1e-10)
+    cold = S.schwarz_solve(p, part, tp, inner, 1e-8, 300)
+    warm = S.schwarz_solve(p, part, tp, inner, 1e-8, 300, warm_start=True)
+    mono = P.bicgstab(p.A, p.b, P.jacobi(p.A), P.SolverOptions(tol=1e-12))
+    assert cold.report.converged and warm.report.converged
+    tot = lambda r: sum(s.iterations for s in r.report.per_subdomain_solves)  # noqa: E731
+    assert tot(warm) < tot(cold), (tot(warm), tot(cold))
+    assert np.linalg.norm(warm.x - mono.x) <= 1e-6 * np.linalg.norm(mono.x)
+    monkeypatch.setenv("CVK_DDM_SEQ_MIN", "0")
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    seq = S.schwarz_solve(p, part, tp, inner, 1e-8, 300, warm_start=True)
+    assert seq.report.outer_iterations == warm.report.outer_iterations
+    assert np.array_equal(bits(seq.x), bits(warm.x))
+    # warm from zero = cold, on the persistent and the phase-kernel path
+    L = _lib.load()
+    L.cvk_solve_device_warm.argtypes = [C.c_void_p] * 6 + [C.POINTER(_lib.CvkReport)]
+    import torch
+    A = p.A
+    M = P.jacobi(A)
+    dev = P.Device.default()
+    for min_n in ("1000000000", "0"):
+        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+        r = P.solve(P.SolverId.BiCGStab, A, p.b, M, P.SolverOptions(tol=1e-10))
+        bd = torch.from_numpy(np.asarray(p.b, np.complex128).view(np.float64).copy()).cuda()
+        xd = torch.zeros_like(bd)
+        o = P.cavac._opts(P.SolverOptions(tol=1e-10), None)
+        rep = _lib.CvkReport()
+        _lib.check(L.cvk_solve_device_warm(dev.handle, A.device(dev), M.device(A, dev), C.byref(o),
+                                           C.c_void_p(bd.data_ptr()), C.c_void_p(xd.data_ptr()), C.byref(rep)))
+        assert rep.iterations == r.report.iterations
+        assert np.array_equal(bits(xd.cpu().numpy().view(np.complex128)), bits(r.x))
+        # from the converged solution: done at once
+        rep2 = _lib.CvkReport()
+        _lib.check(L.cvk_solve_device_warm(dev.handle, A.device(dev), M.device(A, dev), C.byref(o),
+                                           C.c_void_p(bd.data_ptr()), C.c_void_p(xd.data_ptr()), C.byref(rep2)))
+        assert rep2.converged and rep2.iterations <= 1
