@@ -559,6 +559,19 @@ __global__ void __launch_bounds__(kThreads) k_tf_fix(PArgs a) {
 // cvk_stream.cuh: same per-element arithmetic and per-row accumulation order
 // as the thread-per-row kernels above, one CTA per SM.
 
+// Pre-hook switch (CVK_PRE_HOOK): with it, each chunk row's gathered
+// combination is formed once into shared memory behind a group barrier;
+// without it, every in-chunk gather forms it from the staged vectors.
+#ifndef CVK_PRE_HOOK
+#define CVK_PRE_HOOK 1
+#endif
+constexpr bool kPreHook = CVK_PRE_HOOK != 0;
+template <bool ON, class F>
+__device__ __forceinline__ auto PreIf(F&& f) {
+    if constexpr (ON) return f;
+    else return NoPre();
+}
+
 __device__ __forceinline__ double2 prec_staged(const PArgs& a, const Chunk& ch, int j, int t, double2 y) {
     return a.dinv ? cvk_mul(ch.v(j, t), y) : y;
 }
@@ -589,7 +602,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         // slot 0 of the chunk rows holds p_new (pre); band slots hold raw r, p, v
         auto xs = [&](int l) -> double2 {
             const double2 rc = ch.v(0, l);
-            if (first || l < kStreamRows) return rc;
+            if (first || (kPreHook && l < kStreamRows)) return rc;
             return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
         };
         auto xg = [&](int c) -> double2 {
@@ -603,10 +616,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         pn[row] = xs(t);
         vn[row] = vi;
         acc_dot(acc[0], ch.v(3, t), vi);
-    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1), [&](int t, const Chunk& ch) {
+    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1), PreIf<kPreHook>([&](int t, const Chunk& ch) {
         if (!first)
             ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
-    });
+    }));
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
     if (threadIdx.x != 0) return;
@@ -642,7 +655,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds s (pre)
-            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+            return (kPreHook && l < kStreamRows) ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
         };
         auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
         const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
@@ -655,9 +668,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
         acc_norm(acc[0], si);
         acc_dot(acc[1], ti, ti);
         acc_dot(acc[2], ti, si);
-    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), [&](int t, const Chunk& ch) {
+    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
-    });
+    }));
     double2 tot[3];
     if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
@@ -945,9 +958,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bm_b_s(PArgs a) {
         acc_dot(acc[2], ti, si);
         acc_dot(acc[3], shi, si);
         acc_dot(acc[4], shi, ti);
-    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), [&](int t, const Chunk& ch) {
+    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
-    });
+    }));
     double2 tot[5];
     if (!partial_last<5, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
