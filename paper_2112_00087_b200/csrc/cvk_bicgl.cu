@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(kThreads) k_bl_init(BLArgs a) {
     start_cycle(st);
 }
 
+#ifndef CVK_BL_SPMV_BATCH
+#define CVK_BL_SPMV_BATCH 5  // gathers in flight per row in the u/r SpMV phases
+#endif
 #ifndef CVK_BL_BATCH
 #define CVK_BL_BATCH 2  // measured at 1M DOF: 1 -> 2343, 2 -> 2293, 4 -> 2382 us per l=8 cycle
 #endif
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
         auto ujv = [&](int c) -> double2 { return cvk_add(cvk_mul(nbeta, uj_old[c]), rj[c]); };
         CAcc acc[1] = {};
         for_rows<1>(n, G, cta, [&](int row, int, bool valid) {
-            const double2 y = row_sum<1, decltype(ujv)&, 5>(a.A, row, 0, valid, ujv);
+            const double2 y = row_sum<1, decltype(ujv)&, CVK_BL_SPMV_BATCH>(a.A, row, 0, valid, ujv);
             if (valid) {
                 const double2 yi = prec_apply(dinv, row, y);
                 uj_new[row] = ujv(row);
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
         auto rjv = [&](int c) -> double2 { return cvk_add(rj_old[c], cvk_mul(nal, uj1[c])); };
         CAcc acc[2] = {};
         for_rows<1>(n, G, cta, [&](int row, int, bool valid) {
-            const double2 y = row_sum<1, decltype(rjv)&, 5>(a.A, row, 0, valid, rjv);
+            const double2 y = row_sum<1, decltype(rjv)&, CVK_BL_SPMV_BATCH>(a.A, row, 0, valid, rjv);
             if (valid) {
                 rj_new[row] = rjv(row);
                 rj1[row] = prec_apply(dinv, row, y);
