@@ -23,6 +23,30 @@
 
 using cvk::DevReport;
 
+// the phase kernels compiled with 4 x 128-row consumer groups (cvk_phased_g4.cu)
+namespace cvk_g4 {
+int flavor_stream_rows();
+int flavor_stream_threads();
+size_t flavor_stage_bytes(int capk, int nvec, int ngather);
+size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
+void flavor_kernels(void* out);
+void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
+                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
+                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
+                      int dyn, int pf_rows, int nband);
+}  // namespace cvk_g4
+namespace cvk {
+int flavor_stream_rows();
+int flavor_stream_threads();
+size_t flavor_stage_bytes(int capk, int nvec, int ngather);
+size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
+void flavor_kernels(void* out);
+void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
+                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
+                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
+                      int dyn, int pf_rows, int nband);
+}  // namespace cvk
+
 struct cvk_ctx {
     int device = 0;
     int nsm = 0;
@@ -69,6 +93,7 @@ struct cvk_csr {
     size_t blob_bytes = 0;
     int group = 1;  // SpMV lanes per row for FAST mode
     int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
+    int capk_g4 = 0;  // the same for the 128-row chunks of the cvk_g4 flavor
     int* cmax = nullptr;  // [nchunks] largest column of each streamed chunk (L2 prefetch)
     int4* bands = nullptr;  // [nchunks] halo bands {b0, w0, b1, w1} of each streamed chunk
 };
@@ -293,6 +318,11 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
             mk = std::max<long long>(mk, (long long)rp[(size_t)std::min<int64_t>(r0 + cvk::kStreamRows, nrows)] -
                                              (long long)rp[(size_t)r0]);
         A->capk = (int)((mk + 3) & ~3LL);
+        long long mk4 = 0;
+        const int r4 = cvk_g4::flavor_stream_rows();
+        for (int64_t r0 = 0; r0 < nrows; r0 += r4)
+            mk4 = std::max<long long>(mk4, (long long)rp[(size_t)std::min<int64_t>(r0 + r4, nrows)] - (long long)rp[(size_t)r0]);
+        A->capk_g4 = (int)((mk4 + 3) & ~3LL);
         const int64_t nch = (nrows + cvk::kStreamRows - 1) / cvk::kStreamRows;
         std::vector<int> cm((size_t)std::max<int64_t>(1, nch), -1);
         for (int64_t q = 0; q < nch; ++q) {
@@ -568,7 +598,19 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
                         const double2* b_dev, double2* x_dev, cvk_report* rep, bool pinned) {
     const int n = (int)A->n;
     const int S = A->group;
-    const cvk::PhasedKernels K = cvk::phased_kernels();
+    // consumer shape of the streamed phases: 4 x 128 rows for matrices with
+    // many out-of-chunk gathers per row (FEM-3D), 2 x 224 for the 5-point
+    // cavity (cvk_phased_g4.cu); CVK_STREAM_FLAVOR=g2|g4 forces one
+    bool g4 = A->n > 0 && (double)A->nnz / (double)A->n > 8.0;
+    if (const char* env = std::getenv("CVK_STREAM_FLAVOR")) g4 = std::strcmp(env, "g4") == 0;
+    cvk::PhasedKernels K;
+    if (g4) cvk_g4::flavor_kernels(&K);
+    else cvk::flavor_kernels(&K);
+    const int sthreads = g4 ? cvk_g4::flavor_stream_threads() : cvk::flavor_stream_threads();
+    const int scapk = g4 ? A->capk_g4 : A->capk;
+    auto stage_bytes = [&](int nvec, int ngather) {
+        return g4 ? cvk_g4::flavor_stage_bytes(scapk, nvec, ngather) : cvk::flavor_stage_bytes(scapk, nvec, ngather);
+    };
     const size_t smem = 0;
     const void* heavy = solver == CVK_BICGSTAB ? K.bi_b : K.tf_e;
     int per_sm = 0;
@@ -609,19 +651,21 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const int kvec[6] = {5, 5, 7, 8, 7, 6}, kgat[6] = {3, 2, 2, 2, 4, 2};
     // halo-band staging: measured no faster on the 1M cavity (consumer latency is
     // not dominated by the out-of-chunk gathers), so opt-in (CVK_BANDS=1)
-    const int nband = (A->bands && std::getenv("CVK_BANDS") && std::atoi(std::getenv("CVK_BANDS"))) ? 1 : 0;
+    // band staging is per 224-row chunk: the 2 x 224 flavor only
+    const int nband = (!g4 && A->bands && std::getenv("CVK_BANDS") && std::atoi(std::getenv("CVK_BANDS"))) ? 1 : 0;
     auto layout_for = [&](int k, int stg) {
         cvk::StreamLayout L{A->capk, kvec[k], stg};
         L.ngather = kgat[k];
         L.nband = nband;
         return L;
     };
+    auto stage_bytes_k = [&](int k) { return g4 ? stage_bytes(kvec[k], kgat[k]) : layout_for(k, 1).stage_bytes(); };
     int stg[6];
     for (int k = 0; k < 6; ++k) {
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
         long long cap = nband ? 3 : 4;  // measured best ring depths
         if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
-        stg[k] = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)layout_for(k, 1).stage_bytes()));
+        stg[k] = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));
     }
     const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&
                           (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2 : std::min(stg[2], stg[3]) >= 2);
@@ -631,7 +675,9 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // staged, 4 gathered vectors) is consumer-bound.
     const bool merged = streamed && solver == CVK_BICGSTAB && std::min(stg[4], stg[5]) >= 2 && !hs.warm &&
                         std::getenv("CVK_BICG_MERGED") && std::atoi(std::getenv("CVK_BICG_MERGED")) == 1;
-    auto smem_for = [&](int k) { return layout_for(k, stg[k]).smem_bytes(); };
+    auto smem_for = [&](int k) {
+        return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
+    };
     const void* sk[6] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.bm_a_s, K.bm_b_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
@@ -643,12 +689,17 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
         return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
-    cvk::phased_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, A->bands}, M->dinv, b_dev, x_dev,
-                          (double2*)c->work, c->part, c->st, c->hist, c->rep, A->capk, stg,
-                          std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0,
-                          std::getenv("CVK_STREAM_DYN") ? std::atoi(std::getenv("CVK_STREAM_DYN")) : 0,
-                          std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : (nband ? 0 : 2 * cvk::kStreamRows),
-                          nband);
+    {
+        const int contig = std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0;
+        const int dyn = std::getenv("CVK_STREAM_DYN") ? std::atoi(std::getenv("CVK_STREAM_DYN")) : 0;
+        // the L2 prefetch window reads A->cmax, which is per 224-row chunk
+        const int pf = g4 ? 0
+                          : (std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF"))
+                                                          : (nband ? 0 : 2 * cvk::kStreamRows));
+        (g4 ? cvk_g4::flavor_pack_args : cvk::flavor_pack_args)(
+            blob.data(), n, A->rp, A->ci, A->av, g4 ? nullptr : A->cmax, g4 ? nullptr : A->bands, M->dinv, b_dev,
+            x_dev, (double2*)c->work, c->part, c->st, c->hist, c->rep, scapk, stg, contig, dyn, pf, nband);
+    }
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
@@ -662,13 +713,14 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     key.insert(key.end(), gp, gp + sizeof(G));
     key.push_back((unsigned char)(streamed ? 1 : 0));
     key.push_back((unsigned char)(merged ? 1 : 0));
+    key.push_back((unsigned char)(g4 ? 1 : 0));
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
         if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        const dim3 sgrid((unsigned)c->nsm), sblock(cvk::kStreamThreads), egrid((unsigned)Ge);
+        const dim3 sgrid((unsigned)c->nsm), sblock((unsigned)sthreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
             if (merged) {
                 launch_pdl(K.bm_a_s, sgrid, sblock, args, smem_for(4), c->stream);

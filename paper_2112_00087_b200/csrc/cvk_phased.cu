@@ -19,6 +19,8 @@
 // (cvk_krylov.cu): bicgstab krylov.cpp:57-138, tfqmr krylov.cpp:288-375.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 #include "cvk_phased.h"
@@ -1066,6 +1068,33 @@ int phased_trace_read(void* out, size_t bytes) {
 }
 
 size_t phased_args_size() { return sizeof(PArgs); }
+
+// The consumer shape of this translation unit's ring.  cvk_phased_g4.cu
+// compiles this file again (namespace cvk_g4) with 4 groups of 128 rows; the
+// host picks a flavor per matrix through these plain-typed entry points.
+int flavor_stream_rows() { return kStreamRows; }
+int flavor_stream_threads() { return kStreamThreads; }
+size_t flavor_stage_bytes(int capk, int nvec, int ngather) {
+    StreamLayout L{capk, nvec, 1};
+    L.ngather = ngather;
+    return L.stage_bytes();
+}
+size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages) {
+    StreamLayout L{capk, nvec, stages};
+    L.ngather = ngather;
+    return L.smem_bytes();
+}
+void flavor_kernels(void* out) {
+    const PhasedKernels k = kernels_all();
+    memcpy(out, &k, sizeof(k));
+}
+void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
+                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
+                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
+                      int dyn, int pf_rows, int nband) {
+    phased_pack_args(out, Csr{n, rp, ci, av, cmax, bands}, dinv, b, x, work, part, (PState*)st, hist,
+                     (DevReport*)rep, capk, nst, contig, dyn, pf_rows, nband);
+}
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,

@@ -447,3 +447,28 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
     assert not e.report.converged and e.report.iterations == 2
     z = P.solve(P.SolverId.BiCGStabL, A, np.zeros_like(b), M, P.SolverOptions(l=l))
     assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "tfqmr"])
+def test_stream_flavors_bitwise(cvk, oracle, monkeypatch, solver):
+    """The two consumer shapes of the streamed phase kernels (2 x 224 rows,
+    cvk_phased.cu; 4 x 128 rows, cvk_phased_g4.cu) give the same bits on a
+    cavity and an FEM-3D system -- only the row-to-thread mapping differs."""
+    from paper_2112_00087_b200 import fem3d as F
+    P = cvk
+    cav = F.build_cavity(12)
+    systems = [cavity(oracle, 0.0075, f=60.0, adm=0.01),
+               (cav.rp, cav.ci, cav.values(2 * np.pi * 80.0), np.asarray(cav.b, np.complex128))]
+    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    for rp, ci, v, b in systems:
+        A = mat(P, rp, ci, v)
+        M = P.jacobi(A)
+        out = {}
+        for fl in ("g2", "g4"):
+            monkeypatch.setenv("CVK_STREAM_FLAVOR", fl)
+            out[fl] = P.solve(P.solver_from_name(solver), A, b, M,
+                              P.SolverOptions(tol=1e-10, max_iter=5000, record_history=True))
+        a_, b_ = out["g2"], out["g4"]
+        assert a_.report.converged and a_.report.iterations == b_.report.iterations
+        assert np.array_equal(bits(a_.x), bits(b_.x))
+        assert a_.report.residual_history == b_.report.residual_history
