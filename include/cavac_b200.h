@@ -148,6 +148,21 @@ int cvk_precond_identity(cvk_ctx *ctx, int64_t n, cvk_prec **out);
 int cvk_precond_free(cvk_prec *M);
 /* copy the device inverse diagonal back (n complex) */
 int cvk_precond_get_diag(const cvk_prec *M, double *inv_diag);
+/* ILU(0) (beyond the reference: it has only jacobi / identity,
+ * src/krylov.cpp:27-55).  Exact ILU(0) factor on A's pattern (IKJ, host),
+ * applied on the device by `sweeps` (>= 0) Jacobi sweeps per triangle.
+ * Zero or missing pivot -> CVK_EZERODIAG.  Solves with an ILU(0) M support
+ * CVK_BICGSTAB only (the reference's operation order, host-driven loop of
+ * device kernels); other solvers return CVK_EINVAL. */
+int cvk_precond_ilu0(cvk_csr *A, int sweeps, cvk_prec **out);
+/* copy the factor back: L (strict lower) and U (diagonal and above) in A's
+ * value slots (nnz complex) */
+int cvk_precond_get_ilu0(const cvk_prec *M, double *factor);
+/* z_dev = M^-1 r_dev on ctx's stream (any preconditioner kind; device
+ * pointers, n complex each, must not alias) */
+int cvk_precond_apply_device(const cvk_prec *M, const double *r_dev, double *z_dev);
+/* the same with host r / z (staged through ctx's buffers) */
+int cvk_precond_apply(const cvk_prec *M, const double *r, double *z);
 
 /* ---- solve ---- */
 /* host b / x (x is overwritten; x0 = 0 as in the reference) */

@@ -880,3 +880,80 @@ void orc_cdiv(double ar, double ai, double br, double bi, double *out) {
     cplx q = CMPLX(ar, ai) / CMPLX(br, bi);
     out[0] = creal(q); out[1] = cimag(q);
 }
+
+/* ---- ILU(0) (beyond the reference: SURVEY.md 8(f) rank 4; the reference has
+ * only jacobi / identity, krylov.cpp:27-55).  Parity for this preconditioner
+ * is UNPINNED against the reference (it has none); the device factor and
+ * apply are checked against this restatement, the solves by solution-only
+ * checks.
+ *
+ * orc_ilu0_arrays: exact ILU(0) on the CSR pattern, IKJ order: for row i and
+ * each stored k < i in column order, l_ik = a_ik / u_kk (C99 complex
+ * division), then a_ij -= l_ik * u_kj for every stored j > k of row k that is
+ * also stored in row i.  fac gets L (strict lower, unit diagonal implied) and
+ * U (diagonal and above) in A's value slots.  Returns -1, or the first row
+ * whose pivot is missing or zero. */
+int64_t orc_ilu0_arrays(int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v, cplx *fac) {
+    int64_t *pos = malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int64_t *dg = malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int64_t bad = -1;
+    for (int64_t i = 0; i < n; ++i) pos[i] = -1;
+    memcpy(fac, v, (size_t)(rp[n]) * sizeof(cplx));
+    for (int64_t i = 0; i < n && bad < 0; ++i) {
+        dg[i] = -1;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            pos[ci[p]] = p;
+            if (ci[p] == i) dg[i] = p;
+        }
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int64_t k = ci[p];
+            if (k >= i) break;
+            fac[p] = fac[p] / fac[dg[k]];
+            const cplx lik = fac[p];
+            for (int64_t q = dg[k] + 1; q < rp[k + 1]; ++q) {
+                const int64_t t = pos[ci[q]];
+                if (t >= 0) fac[t] = fac[t] - lik * fac[q];
+            }
+        }
+        if (dg[i] < 0 || fac[dg[i]] == 0.0) bad = i;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) pos[ci[p]] = -1;
+    }
+    free(pos);
+    free(dg);
+    return bad;
+}
+
+/* orc_ilu0_apply_arrays: z ~= U^{-1} L^{-1} r by `sweeps` Jacobi sweeps per
+ * triangle (the device's sync-free apply):
+ *   y_0 = r,          y_k[i] = r[i] - sum_{j<i} l_ij y_{k-1}[j]
+ *   z_0 = d .* y,     z_k[i] = d[i] (y[i] - sum_{j>i} u_ij z_{k-1}[j]),  d = 1 / u_ii
+ * sums in CSR order, one rounding per complex op. */
+void orc_ilu0_apply_arrays(int64_t n, const int64_t *rp, const int64_t *ci, const cplx *fac,
+                           int64_t sweeps, const cplx *r, cplx *z) {
+    cplx *y = cvec(n), *w = cvec(n), *d = cvec(n);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+            if (ci[p] == i) d[i] = CMPLX(1.0, 0.0) / fac[p];
+    memcpy(y, r, (size_t)n * sizeof(cplx));
+    for (int64_t k = 0; k < sweeps; ++k) {
+        for (int64_t i = 0; i < n; ++i) {
+            cplx s = r[i];
+            for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < i; ++p) s = s - fac[p] * y[ci[p]];
+            w[i] = s;
+        }
+        memcpy(y, w, (size_t)n * sizeof(cplx));
+    }
+    for (int64_t i = 0; i < n; ++i) z[i] = d[i] * y[i];
+    for (int64_t k = 0; k < sweeps; ++k) {
+        for (int64_t i = 0; i < n; ++i) {
+            cplx s = y[i];
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+                if (ci[p] > i) s = s - fac[p] * z[ci[p]];
+            w[i] = d[i] * s;
+        }
+        memcpy(z, w, (size_t)n * sizeof(cplx));
+    }
+    free(y);
+    free(w);
+    free(d);
+}

@@ -133,6 +133,9 @@ def lib():
             P, C.POINTER(_DdmReport), P]
         L.orc_schwarz_solve.restype = C.c_int
         L.orc_cdiv.argtypes = [C.c_double] * 4 + [P]
+        L.orc_ilu0_arrays.argtypes = [C.c_int64, P, P, P, P]
+        L.orc_ilu0_arrays.restype = C.c_int64
+        L.orc_ilu0_apply_arrays.argtypes = [C.c_int64, P, P, P, C.c_int64, P, P]
     return _lib
 
 
@@ -193,6 +196,26 @@ def solve(solver, rp, ci, v, b, dinv=None, tol=1e-9, max_iter=10000, l=8, m=30,
     if rc != 0:
         raise ValueError(f"orc_solve failed rc={rc}")
     return x, _report(rep, hist)
+
+
+def ilu0(rp, ci, v):
+    """Exact ILU(0) factor in A's value slots (cavac_oracle.c orc_ilu0_arrays;
+    beyond the reference, which has only jacobi/identity, krylov.cpp:27-55)."""
+    rp, ci, v = _i64(rp), _i64(ci), _c128(v)
+    n = len(rp) - 1
+    f = np.zeros(len(v), np.complex128)
+    bad = lib().orc_ilu0_arrays(n, _p(rp), _p(ci), _p(v), _p(f))
+    if bad >= 0:
+        raise ValueError(f"ilu0: zero pivot at row {bad}")
+    return f
+
+
+def ilu0_apply(rp, ci, fac, sweeps, r):
+    """z ~= U^-1 L^-1 r by `sweeps` Jacobi sweeps per triangle (orc_ilu0_apply_arrays)."""
+    rp, ci, fac, r = _i64(rp), _i64(ci), _c128(fac), _c128(r)
+    z = np.zeros(len(rp) - 1, np.complex128)
+    lib().orc_ilu0_apply_arrays(len(rp) - 1, _p(rp), _p(ci), _p(fac), int(sweeps), _p(r), _p(z))
+    return z
 
 
 def spmv(rp, ci, v, x):

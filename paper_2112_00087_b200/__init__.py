@@ -7,7 +7,8 @@ CUDA behind the C ABI in include/cavac_b200.h).
 from .cavac import (  # noqa: F401
     CsrMatrix, Device, ExecMode, InvalidArgument, LogicError, Preconditioner, SolveReport,
     SolveResult, SolverId, SolverOptions, axpy, axpy_inplace, bicgstab, bicgstab_l,
-    csr_from_triplets, csr_identity, dot_hermitian, exec_mode, gmres, identity_preconditioner,
+    csr_from_triplets, csr_identity, dot_hermitian, exec_mode, gmres, identity_preconditioner, ilu0,
+    ilu0_factor,
     jacobi, norm2, scale_inplace, set_exec_mode, solve, solver_from_name, solver_name, spmv,
     tfqmr, true_relative_residual, xpay_inplace,
 )

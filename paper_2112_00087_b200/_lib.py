@@ -113,6 +113,10 @@ def load():
         "cvk_precond_identity": ([P, i64, C.POINTER(P)], i32),
         "cvk_precond_free": ([P], i32),
         "cvk_precond_get_diag": ([P, P], i32),
+        "cvk_precond_ilu0": ([P, i32, C.POINTER(P)], i32),
+        "cvk_precond_get_ilu0": ([P, P], i32),
+        "cvk_precond_apply_device": ([P, P, P], i32),
+        "cvk_precond_apply": ([P, P, P], i32),
         "cvk_solve": ([P, i32, P, P, C.POINTER(CvkOpts), P, P, C.POINTER(CvkReport)], i32),
         "cvk_solve_device": ([P, i32, P, P, C.POINTER(CvkOpts), P, P, C.POINTER(CvkReport)], i32),
         "cvk_spmv": ([P, P, P, i32], i32),

@@ -318,6 +318,12 @@ class Preconditioner:
         v = _cvec(v)
         if self.kind == "identity":
             return v.copy()
+        if self.kind == "ilu0":  # device sweeps (cvk_ilu.cu)
+            if len(v) != self._A.nrows:
+                raise InvalidArgument("preconditioner: dimension mismatch")
+            z = np.zeros_like(v)
+            check(_lib.load().cvk_precond_apply(self.device(self._A), _ptr(v), _ptr(z)))
+            return z
         # elementwise inv_diag[i] * v[i] with the reference rounding (no FMA)
         a, b = self.inv_diag.real, self.inv_diag.imag
         c, d = v.real, v.imag
@@ -332,6 +338,13 @@ class Preconditioner:
             L = _lib.load()
             if self.kind == "identity":
                 check(L.cvk_precond_identity(dev.handle, A.nrows, C.byref(hh)))
+            elif self.kind == "ilu0":
+                if A is not self._A:
+                    raise InvalidArgument("ilu0: factor belongs to another matrix")
+                code = L.cvk_precond_ilu0(A.device(dev), self.sweeps, C.byref(hh))
+                if code == -5:
+                    raise InvalidArgument(_lib.last_error())
+                check(code)
             else:
                 if len(self.inv_diag) != A.nrows:
                     raise InvalidArgument("preconditioner: dimension mismatch")
@@ -370,6 +383,31 @@ def jacobi(A: CsrMatrix) -> Preconditioner:
     M = Preconditioner("jacobi", d, A)
     M._dev[(Device.default().index, A.nrows)] = hh
     return M
+
+
+def ilu0(A: CsrMatrix, sweeps: int = 2) -> Preconditioner:
+    """ILU(0) (beyond the reference, which has jacobi / identity only,
+    krylov.cpp:27-55): exact IKJ factor on A's pattern, applied on the device
+    by `sweeps` Jacobi sweeps per triangle (cvk_ilu.cu).  Zero pivot ->
+    InvalidArgument.  solve() accepts it for BiCGStab."""
+    if A.nrows != A.ncols:
+        raise InvalidArgument("ilu0: matrix must be square")
+    if not 0 <= int(sweeps) <= 64:
+        raise InvalidArgument("ilu0: sweeps must be in [0, 64]")
+    M = Preconditioner("ilu0", None, A)
+    M.sweeps = int(sweeps)
+    M.device(A)  # factor now: a zero pivot raises here
+    return M
+
+
+def ilu0_factor(M: Preconditioner) -> np.ndarray:
+    """The factor in A's value slots: L strict lower (unit diagonal implied), U on and above."""
+    if M.kind != "ilu0":
+        raise InvalidArgument("ilu0_factor: not an ILU(0) preconditioner")
+    f = np.zeros(len(M._A.values), np.complex128)
+    if len(f):
+        check(_lib.load().cvk_precond_get_ilu0(M.device(M._A), _ptr(f)))
+    return f
 
 
 _BRK = {0: None, 1: "rho breakdown", 2: "stagnation in <shadow, v>", 3: "omega breakdown",

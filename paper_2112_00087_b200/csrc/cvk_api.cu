@@ -101,7 +101,9 @@ struct cvk_csr {
 struct cvk_prec {
     cvk_ctx* ctx = nullptr;
     int64_t n = 0;
-    double2* dinv = nullptr;  // nullptr: identity
+    double2* dinv = nullptr;  // nullptr: identity (unless ilu is set)
+    cvk::IluDev* ilu = nullptr;  // ILU(0) (cvk_precond_ilu0); dinv stays nullptr
+    std::vector<double2> ilu_fac;  // host copy of the factor in A's value slots
 };
 
 namespace {
@@ -528,15 +530,293 @@ int cvk_precond_free(cvk_prec* M) {
         cudaSetDevice(M->ctx->device);
         cudaFree(M->dinv);
     }
+    if (M->ilu) {
+        cudaSetDevice(M->ctx->device);
+        cudaFree(M->ilu->blob);
+        delete M->ilu;
+    }
     delete M;
     return CVK_OK;
 }
 
 int cvk_precond_get_diag(const cvk_prec* M, double* inv_diag) {
     if (!M || !inv_diag) return fail(CVK_EINVAL, "cvk_precond_get_diag: null argument");
-    if (!M->dinv) return fail(CVK_EINVAL, "cvk_precond_get_diag: identity preconditioner");
+    if (!M->dinv) return fail(CVK_EINVAL, M->ilu ? "cvk_precond_get_diag: ILU(0) preconditioner"
+                                                 : "cvk_precond_get_diag: identity preconditioner");
     CK(cudaSetDevice(M->ctx->device));
     CK(cudaMemcpy(inv_diag, M->dinv, sizeof(double2) * M->n, cudaMemcpyDeviceToHost));
+    return CVK_OK;
+}
+
+// ILU(0): exact factor on A's pattern on the host (IKJ; the order and
+// roundings of oracle/cavac_oracle.c orc_ilu0_arrays), split into strict L,
+// strict U and d = 1 / u_ii for the device sweeps (cvk_ilu.cu).  Beyond the
+// reference (krylov.cpp:27-55 has jacobi / identity only).
+int cvk_precond_ilu0(cvk_csr* A, int sweeps, cvk_prec** out) {
+    if (!A || !out) return fail(CVK_EINVAL, "cvk_precond_ilu0: null argument");
+    if (sweeps < 0 || sweeps > 64) return fail(CVK_EINVAL, "cvk_precond_ilu0: sweeps must be in [0, 64]");
+    cvk_ctx* c = A->ctx;
+    CK(cudaSetDevice(c->device));
+    const int64_t n = A->n, nnz = A->nnz;
+    std::vector<int> rp(n + 1), ci(std::max<int64_t>(1, nnz));
+    std::vector<double2> f(std::max<int64_t>(1, nnz));
+    CK(cudaMemcpyAsync(rp.data(), A->rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+    if (nnz) {
+        CK(cudaMemcpyAsync(ci.data(), A->ci, sizeof(int) * nnz, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(f.data(), A->av, sizeof(double2) * nnz, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> pos(std::max<int64_t>(1, n), -1), dg(std::max<int64_t>(1, n), -1);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            pos[ci[p]] = p;
+            if (ci[p] == i) dg[i] = p;
+        }
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            const int k = ci[p];
+            if (k >= i) break;
+            f[p] = cvk_cdiv(f[p], f[dg[k]]);
+            const double2 lik = f[p];
+            for (int q = (int)dg[k] + 1; q < rp[k + 1]; ++q) {
+                const int64_t t = pos[ci[q]];
+                if (t >= 0) f[t] = cvk_sub(f[t], cvk_mul(lik, f[q]));
+            }
+        }
+        for (int p = rp[i]; p < rp[i + 1]; ++p) pos[ci[p]] = -1;
+        if (dg[i] < 0 || (f[dg[i]].x == 0.0 && f[dg[i]].y == 0.0))
+            return fail(CVK_EZERODIAG, "ilu0: zero pivot at row " + std::to_string(i));
+    }
+    // split: L strict lower, U strict upper (CSR order kept), d = 1 / u_ii
+    std::vector<int> lrp(n + 1, 0), urp(n + 1, 0), lci, uci;
+    std::vector<double2> lav, uav, d(std::max<int64_t>(1, n));
+    lci.reserve(nnz / 2 + 1), uci.reserve(nnz / 2 + 1), lav.reserve(nnz / 2 + 1), uav.reserve(nnz / 2 + 1);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int p = rp[i]; p < rp[i + 1]; ++p) {
+            if (ci[p] < i) { lci.push_back(ci[p]); lav.push_back(f[p]); }
+            else if (ci[p] > i) { uci.push_back(ci[p]); uav.push_back(f[p]); }
+        }
+        lrp[i + 1] = (int)lci.size();
+        urp[i + 1] = (int)uci.size();
+        d[i] = cvk_cdiv(make_double2(1.0, 0.0), f[dg[i]]);
+    }
+    const size_t nl = lci.size(), nu = uci.size();
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t o_lav = 0, o_uav = o_lav + al(16 * nl), o_d = o_uav + al(16 * nu), o_lci = o_d + al(16 * n),
+                 o_uci = o_lci + al(4 * nl), o_lrp = o_uci + al(4 * nu), o_urp = o_lrp + al(4 * (n + 1)),
+                 total = o_urp + al(4 * (n + 1));
+    cvk::IluDev* I = new cvk::IluDev();
+    I->n = (int)n;
+    I->sweeps = sweeps;
+    if (cudaMalloc(&I->blob, total) != cudaSuccess) {
+        delete I;
+        return fail(CVK_ENOMEM, "ilu0: out of device memory");
+    }
+    char* b = (char*)I->blob;
+    I->lav = (double2*)(b + o_lav), I->uav = (double2*)(b + o_uav), I->dinv = (double2*)(b + o_d);
+    I->lci = (int*)(b + o_lci), I->uci = (int*)(b + o_uci), I->lrp = (int*)(b + o_lrp), I->urp = (int*)(b + o_urp);
+    cudaStream_t st = c->stream;
+    if (nl) CK(cudaMemcpyAsync(I->lav, lav.data(), 16 * nl, cudaMemcpyHostToDevice, st));
+    if (nu) CK(cudaMemcpyAsync(I->uav, uav.data(), 16 * nu, cudaMemcpyHostToDevice, st));
+    if (nl) CK(cudaMemcpyAsync(I->lci, lci.data(), 4 * nl, cudaMemcpyHostToDevice, st));
+    if (nu) CK(cudaMemcpyAsync(I->uci, uci.data(), 4 * nu, cudaMemcpyHostToDevice, st));
+    if (n) CK(cudaMemcpyAsync(I->dinv, d.data(), 16 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(I->lrp, lrp.data(), 4 * (n + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(I->urp, urp.data(), 4 * (n + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    cvk_prec* M = new cvk_prec();
+    M->ctx = c;
+    M->n = n;
+    M->ilu = I;
+    f.resize(nnz);
+    M->ilu_fac = std::move(f);
+    *out = M;
+    return CVK_OK;
+}
+
+int cvk_precond_get_ilu0(const cvk_prec* M, double* factor) {
+    if (!M || !factor) return fail(CVK_EINVAL, "cvk_precond_get_ilu0: null argument");
+    if (!M->ilu) return fail(CVK_EINVAL, "cvk_precond_get_ilu0: not an ILU(0) preconditioner");
+    if (!M->ilu_fac.empty()) std::memcpy(factor, M->ilu_fac.data(), sizeof(double2) * M->ilu_fac.size());
+    return CVK_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// z = M^-1 r on the device for any preconditioner kind; tmp >= 2 n complex
+int prec_apply_dev(const cvk_prec* M, const double2* r, double2* z, double2* tmp, int* nl) {
+    cvk_ctx* c = M->ctx;
+    const int n = (int)M->n;
+    if (n <= 0) return CVK_OK;
+    if (M->ilu) {
+        CK(cvk::launch_ilu0_apply(*M->ilu, r, z, tmp, nl, c->stream));
+    } else if (M->dinv) {
+        cvk::IluDev J;  // s = 0: z = d .* r
+        J.n = n;
+        J.sweeps = 0;
+        J.dinv = M->dinv;
+        CK(cvk::launch_ilu0_apply(J, r, z, tmp, nl, c->stream));
+    } else {
+        CK(cudaMemcpyAsync(z, r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return CVK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int cvk_precond_apply_device(const cvk_prec* M, const double* r_dev, double* z_dev) {
+    if (!M || (M->n && (!r_dev || !z_dev))) return fail(CVK_EINVAL, "cvk_precond_apply_device: null argument");
+    if (r_dev == z_dev && M->n) return fail(CVK_EINVAL, "cvk_precond_apply_device: r and z alias");
+    cvk_ctx* c = M->ctx;
+    CK(cudaSetDevice(c->device));
+    int e;
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 2 * std::max<size_t>(1, M->n))) != CVK_OK)
+        return e;
+    return prec_apply_dev(M, (const double2*)r_dev, (double2*)z_dev, (double2*)c->work, nullptr);
+}
+
+static int stage(cvk_ctx* c, size_t n2);
+
+int cvk_precond_apply(const cvk_prec* M, const double* r, double* z) {
+    if (!M || (M->n && (!r || !z))) return fail(CVK_EINVAL, "cvk_precond_apply: null argument");
+    cvk_ctx* c = M->ctx;
+    CK(cudaSetDevice(c->device));
+    const size_t n = (size_t)M->n;
+    if (!n) return CVK_OK;
+    int e;
+    if ((e = stage(c, 2 * n)) != CVK_OK) return e;
+    double2* rd = c->bx;
+    double2* zd = c->bx + n;
+    CK(cudaMemcpyAsync(rd, r, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    if ((e = cvk_precond_apply_device(M, (const double*)rd, (double*)zd)) != CVK_OK) return e;
+    CK(cudaMemcpyAsync(z, zd, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return CVK_OK;
+}
+
+// BiCGSTAB with a general preconditioner (ILU(0)): the reference's operation
+// order (krylov.cpp:57-138 = oracle orc_bicgstab) as a host loop of device
+// kernels -- SpMV, preconditioner sweeps, axpys and double-double dots --
+// with one scalar read-back per dependent reduction (4 per iteration; the
+// final ||r|| rides with the next rho).  FAST or REF dots per the mode.
+static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                                  const double2* b, double2* x, cvk_report* rep) {
+    const int n = (int)A->n;
+    const bool ref = resolve_mode(c, o->mode) == CVK_MODE_REF;
+    cudaStream_t st = c->stream;
+    int e;
+    const size_t nv = (size_t)std::max(1, n);
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (9 * nv + 8))) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    double2* w = (double2*)c->work;
+    double2 *r = w, *sh = w + nv, *p = w + 2 * nv, *v = w + 3 * nv, *s = w + 4 * nv, *t = w + 5 * nv,
+            *tmp = w + 6 * nv, *ptmp = w + 7 * nv, *od = w + 9 * nv;
+    long long launches = 0;
+    int nl = 0;
+    auto dot = [&](const double2* xx, const double2* yy, int slot) -> cudaError_t {
+        launches += ref ? 1 : 2;
+        return cvk::launch_dot(ref, n, xx, yy, c->part, od + slot, st);
+    };
+    auto fetch = [&](double2* h, int k) -> cudaError_t {
+        cudaError_t ce = cudaMemcpyAsync(h, od, sizeof(double2) * k, cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        return ce;
+    };
+    auto op = [&](const double2* in, double2* outv) -> int {  // outv = M^-1 (A in)
+        int rc = cvk_spmv_device(A, (const double*)in, (double*)tmp, ref ? CVK_MODE_REF : CVK_MODE_FAST);
+        if (rc != CVK_OK) return rc;
+        ++launches;
+        return prec_apply_dev(M, tmp, outv, ptmp, &nl);
+    };
+    auto hist = [&](double v) {
+        if (o->record_history && rep->history && rep->history_len < rep->history_cap) rep->history[rep->history_len] = v;
+        if (o->record_history) rep->history_len++;
+    };
+    rep->converged = 0, rep->breakdown = CVK_BRK_NONE, rep->iterations = 0, rep->final_relres = 0.0;
+    rep->true_relres = 0.0, rep->history_len = 0;
+    CK(cudaEventRecord(c->e0, st));
+    CK(cudaMemsetAsync(x, 0, sizeof(double2) * nv, st));
+    if ((e = prec_apply_dev(M, b, r, ptmp, &nl)) != CVK_OK) return e;
+    CK(dot(r, nullptr, 0));
+    double2 h[2];
+    CK(fetch(h, 1));
+    const double bnorm = std::sqrt(h[0].x);
+    bool have_true = true;
+    if (bnorm == 0.0) {
+        rep->converged = 1;
+        have_true = false;
+    } else {
+        const double brk = 1e-30 * bnorm * bnorm;
+        CK(cudaMemcpyAsync(sh, r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+        double2 rho = make_double2(1.0, 0.0), alpha = rho, omega = rho;
+        for (long long it = 1; it <= o->max_iter; ++it) {
+            CK(dot(sh, r, 0));
+            CK(fetch(h, 1));
+            const double2 rho_new = h[0];
+            if (std::hypot(rho_new.x, rho_new.y) < brk) { rep->breakdown = CVK_BRK_RHO; rep->iterations = it - 1; break; }
+            if (it == 1) {
+                CK(cudaMemcpyAsync(p, r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+            } else {
+                const double2 beta = cvk_mul(cvk_cdiv(rho_new, rho), cvk_cdiv(alpha, omega));
+                CK(cvk::launch_axpy(n, make_double2(-omega.x, -omega.y), v, p, st));
+                CK(cvk::launch_xpay(n, beta, p, r, st));
+                launches += 2;
+            }
+            rho = rho_new;
+            if ((e = op(p, v)) != CVK_OK) return e;
+            CK(dot(sh, v, 0));
+            CK(fetch(h, 1));
+            const double2 gamma = h[0];
+            if (std::hypot(gamma.x, gamma.y) < brk) { rep->breakdown = CVK_BRK_SHADOW_V; rep->iterations = it - 1; break; }
+            alpha = cvk_cdiv(rho, gamma);
+            CK(cudaMemcpyAsync(s, r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+            CK(cvk::launch_axpy(n, make_double2(-alpha.x, -alpha.y), v, s, st));
+            CK(cvk::launch_axpy(n, alpha, p, x, st));
+            launches += 2;
+            CK(dot(s, nullptr, 0));
+            CK(fetch(h, 1));
+            double relres = std::sqrt(h[0].x) / bnorm;
+            if (relres <= o->tol) {
+                rep->converged = 1, rep->iterations = it, rep->final_relres = relres;
+                hist(relres);
+                break;
+            }
+            if ((e = op(s, t)) != CVK_OK) return e;
+            CK(dot(t, nullptr, 0));
+            CK(dot(t, s, 1));
+            CK(fetch(h, 2));
+            const double tt = h[0].x;  // <t, t> is real
+            if (std::fabs(tt) < brk) { rep->breakdown = CVK_BRK_OMEGA; rep->iterations = it; break; }
+            omega = cvk_cdiv(h[1], make_double2(tt, 0.0));
+            CK(cvk::launch_axpy(n, omega, s, x, st));
+            CK(cudaMemcpyAsync(r, s, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+            CK(cvk::launch_axpy(n, make_double2(-omega.x, -omega.y), t, r, st));
+            launches += 2;
+            CK(dot(r, nullptr, 0));
+            CK(fetch(h, 1));
+            relres = std::sqrt(h[0].x) / bnorm;
+            rep->final_relres = relres;
+            rep->iterations = it;
+            hist(relres);
+            if (relres <= o->tol) { rep->converged = 1; break; }
+        }
+    }
+    if (have_true) {  // true_relative_residual (krylov.cpp:17-23)
+        CK(cvk::launch_residual(ref ? 1 : A->group, ref, n, A->rp, A->ci, A->av, b, x, tmp, st));
+        CK(dot(b, nullptr, 0));
+        CK(dot(tmp, nullptr, 1));
+        ++launches;
+        CK(fetch(h, 2));
+        const double bn = std::sqrt(h[0].x), rn = std::sqrt(h[1].x);
+        rep->true_relres = bn > 0 ? rn / bn : rn;
+    }
+    CK(cudaEventRecord(c->e1, st));
+    CK(cudaEventSynchronize(c->e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = launches + nl;
     return CVK_OK;
 }
 
@@ -1100,6 +1380,12 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     if (solver == CVK_GMRES && (o->m < 1 || o->m > cvk::kMaxDots))
         return fail(CVK_EINVAL, "gmres: m must be in [1, 64]");
     if (o->max_iter < 0) return fail(CVK_EINVAL, std::string(nm) + ": negative max_iter");
+    if (M->ilu) {
+        if (solver != CVK_BICGSTAB || c->warm_next)
+            return fail(CVK_EINVAL, std::string(nm) + ": the ILU(0) preconditioner supports bicgstab (cold start) only");
+        CK(cudaSetDevice(c->device));
+        return solve_bicgstab_general(c, A, M, o, b_dev, x_dev, rep);
+    }
     const int n = (int)A->n;
     const int mode = resolve_mode(c, o->mode);
     const bool ref = mode == CVK_MODE_REF;

@@ -86,4 +86,16 @@ cudaError_t launch_xpay(int n, double2 alpha, double2* x, const double2* y, cuda
 cudaError_t launch_residual(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                             const double2* b, const double2* x, double2* r, cudaStream_t st);
 
+// ILU(0) factor on the device (cvk_ilu.cu): strict L and strict U as CSR,
+// d = 1 / u_ii; the apply runs `sweeps` Jacobi sweeps per triangle
+struct IluDev {
+    int n = 0, sweeps = 2;
+    int *lrp = nullptr, *lci = nullptr, *urp = nullptr, *uci = nullptr;
+    double2 *lav = nullptr, *uav = nullptr, *dinv = nullptr;
+    void* blob = nullptr;  // one allocation behind all of the above
+};
+// z = M^-1 r; tmp >= 2 n complex; r, z, tmp disjoint; *nl += launches
+cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, double2* tmp, int* nl,
+                              cudaStream_t st);
+
 }  // namespace cvk
