@@ -695,6 +695,128 @@ int cvk_precond_apply(const cvk_prec* M, const double* r, double* z) {
     return CVK_OK;
 }
 
+// FAST BiCGSTAB + ILU(0): the cvk_ilu.cu phase chain, scalars on the device,
+// kIcPerGraph iterations per CUDA graph, the done flag polled one graph late.
+struct IcSpmv {
+    const cvk_csr* A;
+    double2* out;
+    int optin, nsm, streamed;
+    cudaStream_t st;
+};
+static cudaError_t ic_spmv(void* ctx, const double2* in) {
+    const IcSpmv* q = (const IcSpmv*)ctx;
+    const cvk_csr* A = q->A;
+    if (q->streamed)
+        return cvk::launch_spmv_stream((int)A->n, A->rp, A->ci, A->av, in, q->out, A->capk, q->nsm, q->optin, q->st);
+    return cvk::launch_spmv(A->group, false, (int)A->n, A->rp, A->ci, A->av, in, q->out, 0, q->st);
+}
+
+static int solve_ilu_chain(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
+                           const double2* b, double2* x, cvk_report* rep) {
+    constexpr int kIcPerGraph = 8;
+    const int n = (int)A->n;
+    cudaStream_t st = c->stream;
+    int e;
+    const size_t nv = (size_t)std::max(1, n);
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 10 * nv)) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 4 * 592)) != CVK_OK) return e;
+    double2* w = (double2*)c->work;
+    double2* sh = w + 9 * nv;
+    cvk::IcArgs a;
+    a.n = n, a.x = x, a.r = w, a.p = w + nv, a.v = w + 2 * nv, a.s = w + 3 * nv, a.t = w + 4 * nv;
+    a.tmp = w + 5 * nv, a.ptmp = w + 6 * nv, a.sh = sh, a.part = c->part;
+    const long long hcap = o->record_history && rep->history ? std::max<long long>(0, rep->history_cap) : 0;
+    void* mem = nullptr;
+    CK(cudaMalloc(&mem, sizeof(cvk::IcState) + sizeof(double) * std::max<long long>(1, hcap)));
+    struct Free { void* p; ~Free() { cudaFree(p); } } guard{mem};
+    a.st = (cvk::IcState*)mem;
+    a.hist = (double*)((char*)mem + sizeof(cvk::IcState));
+    cvk::IcState h0 = {};
+    h0.record = o->record_history ? 1 : 0;
+    h0.max_iter = o->max_iter, h0.hist_cap = hcap, h0.tol = o->tol;
+    h0.rho = h0.alpha = h0.omega = make_double2(1.0, 0.0);
+    IcSpmv q{A, a.tmp, 0, c->nsm, 0, st};
+    if (A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && !std::getenv("CVK_NO_STREAM")) {
+        CK(cudaDeviceGetAttribute(&q.optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        q.streamed = 1;
+    }
+    int nl = 0;
+    long long launches = 0;
+    CK(cudaEventRecord(c->e0, st));
+    CK(cudaMemcpyAsync(a.st, &h0, sizeof(h0), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(x, 0, sizeof(double2) * nv, st));
+    CK(cvk::launch_ilu0_apply(*M->ilu, b, a.r, a.ptmp, &nl, st));  // r = M^-1 b
+    CK(cudaMemcpyAsync(sh, a.r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+    CK(cvk::launch_ic_init(a, st));
+    launches += 2;
+    if (q.streamed) {  // first call outside the capture sets the kernel attributes
+        const cudaError_t se = ic_spmv(&q, a.r);
+        if (se == cudaErrorInvalidConfiguration) {
+            (void)cudaGetLastError();
+            q.streamed = 0;
+        } else {
+            CK(se);
+            ++launches;
+        }
+    }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    int nl_graph = 0;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const cudaError_t ce = cvk::launch_ic_iters(a, *M->ilu, kIcPerGraph, ic_spmv, &q, &nl_graph, st);
+    const cudaError_t ee = cudaStreamEndCapture(st, &graph);
+    CK(ce);
+    CK(ee);
+    CK(cudaGraphInstantiate(&gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    struct GFree { cudaGraphExec_t g; ~GFree() { cudaGraphExecDestroy(g); } } gguard{gexec};
+    long long graphs = 0;
+    const long long max_graphs = o->max_iter / kIcPerGraph + 3;
+    while (graphs < max_graphs) {
+        CK(cudaGraphLaunch(gexec, st));
+        const int slot = (int)(graphs & 1);
+        CK(cudaMemcpyAsync(&c->h_done[slot], &a.st->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(c->ev[slot], st));
+        ++graphs;
+        launches += nl_graph;
+        if (graphs >= 2) {
+            const int old = (int)((graphs - 2) & 1);
+            CK(cudaEventSynchronize(c->ev[old]));
+            if (c->h_done[old]) break;
+        }
+    }
+    cvk::IcState hs;
+    CK(cudaMemcpyAsync(&hs, a.st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!hs.done) return fail(CVK_ELOGIC, "bicgstab+ilu0: iteration chain did not finish");
+    rep->converged = hs.conv, rep->breakdown = hs.brk_code, rep->iterations = hs.iterations;
+    rep->final_relres = hs.final_relres, rep->true_relres = 0.0;
+    rep->history_len = o->record_history ? hs.hl : 0;
+    if (!hs.no_true) {  // true_relative_residual (krylov.cpp:17-23)
+        double2* od = w + 7 * nv;
+        CK(cvk::launch_residual(A->group, false, n, A->rp, A->ci, A->av, b, x, a.tmp, st));
+        CK(cvk::launch_dot(false, n, b, nullptr, c->part, od, st));
+        CK(cvk::launch_dot(false, n, a.tmp, nullptr, c->part, od + 1, st));
+        launches += 5;
+        double2 hh[2];
+        CK(cudaMemcpyAsync(hh, od, sizeof(hh), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double bn = std::sqrt(hh[0].x), rn = std::sqrt(hh[1].x);
+        rep->true_relres = bn > 0 ? rn / bn : rn;
+    }
+    if (hcap > 0) {
+        const long long k = std::min<long long>(hs.hl, hcap);
+        if (k > 0) CK(cudaMemcpy(rep->history, a.hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    CK(cudaEventRecord(c->e1, st));
+    CK(cudaEventSynchronize(c->e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+    rep->device_time_s = ms * 1e-3;
+    rep->kernel_launches = launches + nl;
+    return CVK_OK;
+}
+
 // BiCGSTAB with a general preconditioner (ILU(0)): the reference's operation
 // order (krylov.cpp:57-138 = oracle orc_bicgstab) as a host loop of device
 // kernels -- SpMV, preconditioner sweeps, axpys and double-double dots --
@@ -704,6 +826,7 @@ static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* 
                                   const double2* b, double2* x, cvk_report* rep) {
     const int n = (int)A->n;
     const bool ref = resolve_mode(c, o->mode) == CVK_MODE_REF;
+    if (!ref && M->ilu && n > 0 && !std::getenv("CVK_ILU_HOSTLOOP")) return solve_ilu_chain(c, A, M, o, b, x, rep);
     cudaStream_t st = c->stream;
     int e;
     const size_t nv = (size_t)std::max(1, n);

@@ -104,4 +104,182 @@ cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, dou
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// BiCGSTAB with the ILU(0) apply, FAST mode, as a chain of phase kernels with
+// the scalars on the device (no host round trip per reduction), replayed from
+// a CUDA graph.  Operation order = krylov.cpp:57-138 (oracle orc_bicgstab);
+// every reduction is the double-double two-stage sum of cvk_blas.cu.  Per
+// iteration: k_ic_p, SpMV, 2s sweeps, k_ic_dot<1> + k_ic_fold<1>, k_ic_s +
+// k_ic_fold<3>, SpMV, 2s sweeps, k_ic_dot<2> + k_ic_fold<2>, k_ic_xr +
+// k_ic_fold<4> (which also takes <sh, r> for the next iteration's rho).
+namespace {
+
+constexpr int kIcBlocks = 592;  // 4 x 148, fixed so the FAST sum order is fixed
+
+__device__ __forceinline__ double cabs2(double2 a) { return hypot(a.x, a.y); }
+
+__device__ void ic_hist(IcState* st, double* hist, double v) {
+    if (!st->record) return;
+    if (st->hl < st->hist_cap) hist[st->hl] = v;
+    st->hl++;
+}
+
+// rho for iteration it (MODE 0 logic), thread 0 of the fold
+__device__ void ic_rho(IcState* st, double2 rho_new) {
+    const long long it = st->it + 1;
+    if (it > st->max_iter) { st->done = 1; return; }
+    if (cabs2(rho_new) < st->brk) { st->brk_code = 1; st->iterations = it - 1; st->done = 1; return; }
+    if (it > 1) st->beta = cvk_mul(cvk_cdiv(rho_new, st->rho), cvk_cdiv(st->alpha, st->omega));
+    st->rho = rho_new;
+    st->it = it;
+}
+
+// stage 1: MODE 0 init {|r|^2, <r, r>}, 1 <sh, v>, 2 {|t|^2, <t, s>}
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_ic_dot(IcArgs a) {
+    if (a.st->done) return;
+    CAcc acc[2] = {};
+    for_elems(a.n, gridDim.x, blockIdx.x, [&](int i) {
+        if (MODE == 0) {
+            const double2 ri = a.r[i];
+            acc_norm(acc[0], ri);
+            acc_dot(acc[1], ri, ri);
+        } else if (MODE == 1) {
+            acc_dot(acc[0], __ldg(a.sh + i), a.v[i]);
+        } else {
+            const double2 ti = a.t[i];
+            acc_norm(acc[0], ti);
+            acc_dot(acc[1], ti, a.s[i]);
+        }
+    });
+    cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+}
+
+// p = r (it == 1) or p = beta (p - omega v) + r  (axpy then xpay, krylov.cpp:77-80)
+__global__ void __launch_bounds__(kThreads) k_ic_p(IcArgs a) {
+    const IcState* st = a.st;
+    if (st->done) return;
+    const bool first = st->it == 1;
+    const double2 nom = make_double2(-st->omega.x, -st->omega.y), beta = st->beta;
+    for_elems(a.n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 ri = a.r[i];
+        a.p[i] = first ? ri : cvk_add(cvk_mul(beta, cvk_add(a.p[i], cvk_mul(nom, a.v[i]))), ri);
+    });
+}
+
+// s = r - alpha v; x += alpha p; partial |s|^2
+__global__ void __launch_bounds__(kThreads) k_ic_s(IcArgs a) {
+    const IcState* st = a.st;
+    if (st->done) return;
+    const double2 al = st->alpha, nal = make_double2(-al.x, -al.y);
+    CAcc acc[2] = {};
+    for_elems(a.n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 si = cvk_add(a.r[i], cvk_mul(nal, a.v[i]));
+        a.s[i] = si;
+        a.x[i] = cvk_add(a.x[i], cvk_mul(al, a.p[i]));
+        acc_norm(acc[0], si);
+    });
+    cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+}
+
+// x += omega s; r = s - omega t; partials |r|^2 and <sh, r>
+__global__ void __launch_bounds__(kThreads) k_ic_xr(IcArgs a) {
+    const IcState* st = a.st;
+    if (st->done) return;
+    const double2 om = st->omega, nom = make_double2(-om.x, -om.y);
+    CAcc acc[2] = {};
+    for_elems(a.n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 si = a.s[i];
+        a.x[i] = cvk_add(a.x[i], cvk_mul(om, si));
+        const double2 ri = cvk_add(si, cvk_mul(nom, a.t[i]));
+        a.r[i] = ri;
+        acc_norm(acc[0], ri);
+        acc_dot(acc[1], __ldg(a.sh + i), ri);
+    });
+    cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+}
+
+// stage 2 + the scalar step.  MODE 0: bnorm and rho_1; 1: gamma -> alpha;
+// 2: omega; 3: |s| test; 4: |r| test, then rho for the next iteration.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_ic_fold(IcArgs a) {
+    IcState* st = a.st;
+    if (st->done) return;
+    double2 v[2];
+    fold_partials<2>(v, a.part, kIcBlocks);
+    if (threadIdx.x != 0) return;
+    if (MODE == 0) {
+        st->bnorm = sqrt(v[0].x);
+        if (st->bnorm == 0.0) { st->conv = 1; st->no_true = 1; st->done = 1; return; }
+        st->brk = 1e-30 * st->bnorm * st->bnorm;
+        ic_rho(st, v[1]);
+    } else if (MODE == 1) {
+        if (cabs2(v[0]) < st->brk) { st->brk_code = 2; st->iterations = st->it - 1; st->done = 1; return; }
+        st->alpha = cvk_cdiv(st->rho, v[0]);
+    } else if (MODE == 2) {
+        const double2 tt = make_double2(v[0].x, 0.0);
+        if (cabs2(tt) < st->brk) { st->brk_code = 3; st->iterations = st->it; st->done = 1; return; }
+        st->omega = cvk_cdiv(v[1], tt);
+    } else if (MODE == 3) {
+        const double relres = sqrt(v[0].x) / st->bnorm;
+        if (relres <= st->tol) {
+            st->conv = 1, st->iterations = st->it, st->final_relres = relres;
+            ic_hist(st, a.hist, relres);
+            st->done = 1;
+        }
+    } else {
+        const double relres = sqrt(v[0].x) / st->bnorm;
+        st->final_relres = relres;
+        st->iterations = st->it;
+        ic_hist(st, a.hist, relres);
+        if (relres <= st->tol) { st->conv = 1; st->done = 1; return; }
+        ic_rho(st, v[1]);
+    }
+}
+
+int ic_grid(int n) {
+    (void)n;
+    return kIcBlocks;
+}
+
+}  // namespace
+
+cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st) {
+    k_ic_dot<0><<<kIcBlocks, kThreads, 0, st>>>(a);
+    k_ic_fold<0><<<1, kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// one iteration; spmv(in, out) launches A in -> a.tmp; returns launches in *nl
+template <class Spmv>
+static cudaError_t ic_iter(const IcArgs& a, const IluDev& M, Spmv&& spmv, int* nl, cudaStream_t st) {
+    cudaError_t e;
+    const int G = ic_grid(a.n);
+    k_ic_p<<<G, kThreads, 0, st>>>(a);
+    if ((e = spmv(a.p)) != cudaSuccess) return e;
+    if ((e = launch_ilu0_apply(M, a.tmp, a.v, a.ptmp, nl, st)) != cudaSuccess) return e;
+    k_ic_dot<1><<<G, kThreads, 0, st>>>(a);
+    k_ic_fold<1><<<1, kThreads, 0, st>>>(a);
+    k_ic_s<<<G, kThreads, 0, st>>>(a);
+    k_ic_fold<3><<<1, kThreads, 0, st>>>(a);
+    if ((e = spmv(a.s)) != cudaSuccess) return e;
+    if ((e = launch_ilu0_apply(M, a.tmp, a.t, a.ptmp, nl, st)) != cudaSuccess) return e;
+    k_ic_dot<2><<<G, kThreads, 0, st>>>(a);
+    k_ic_fold<2><<<1, kThreads, 0, st>>>(a);
+    k_ic_xr<<<G, kThreads, 0, st>>>(a);
+    k_ic_fold<4><<<1, kThreads, 0, st>>>(a);
+    *nl += 12;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ic_iters(const IcArgs& a, const IluDev& M, int iters,
+                            cudaError_t (*spmv)(void*, const double2*), void* ctx, int* nl, cudaStream_t st) {
+    for (int k = 0; k < iters; ++k) {
+        cudaError_t e = ic_iter(a, M, [&](const double2* in) { return spmv(ctx, in); }, nl, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace cvk

@@ -98,4 +98,24 @@ struct IluDev {
 cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, double2* tmp, int* nl,
                               cudaStream_t st);
 
+// BiCGSTAB + ILU(0) phase chain (cvk_ilu.cu): device-resident scalars
+struct IcState {
+    int done, conv, brk_code, no_true, record, pad;
+    long long it, iterations, max_iter, hl, hist_cap;
+    double bnorm, brk, tol, final_relres;
+    double2 rho, alpha, omega, beta;
+};
+struct IcArgs {
+    int n;
+    double2 *x, *r, *p, *v, *s, *t, *tmp, *ptmp;  // ptmp: 2 n (ILU sweeps)
+    const double2* sh;
+    double2* part;  // >= 4 * 592 double2
+    IcState* st;
+    double* hist;
+};
+cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st);
+// `iters` iterations; spmv(ctx, in) computes A in -> a.tmp on st
+cudaError_t launch_ic_iters(const IcArgs& a, const IluDev& M, int iters,
+                            cudaError_t (*spmv)(void*, const double2*), void* ctx, int* nl, cudaStream_t st);
+
 }  // namespace cvk

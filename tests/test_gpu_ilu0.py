@@ -123,3 +123,38 @@ def test_ilu0_errors(cvk, oracle):
     # zero rhs: converged at once, x = 0
     res = P.solve(P.SolverId.BiCGStab, A, np.zeros(n, complex), M)
     assert res.report.converged and res.report.iterations == 0 and not res.x.any()
+
+
+def test_graph_chain_matches_host_loop(cvk, oracle, monkeypatch):
+    """FAST mode runs the device-scalar phase chain (cvk_ilu.cu, CUDA graph);
+    CVK_ILU_HOSTLOOP=1 forces the host loop of the same kernels' arithmetic.
+    Same reduction kernels' sums, so the same iterations and a matching x."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.008, 250.0)
+    n = len(rp) - 1
+    A = P.CsrMatrix(n, n, rp, ci, v)
+    opts = P.SolverOptions(tol=1e-9, max_iter=100000, record_history=True)
+    for s in (0, 2, 3):
+        M = P.ilu0(A, s)
+        chain = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
+        monkeypatch.setenv("CVK_ILU_HOSTLOOP", "1")
+        host = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
+        monkeypatch.delenv("CVK_ILU_HOSTLOOP")
+        assert chain.report.converged and host.report.converged
+        assert abs(chain.report.iterations - host.report.iterations) <= 1
+        assert len(chain.report.residual_history) == chain.report.iterations
+        assert np.linalg.norm(chain.x - host.x) <= 1e-9 * np.linalg.norm(host.x)
+        assert chain.report.true_relres <= 1e-8
+
+
+def test_chain_max_iter_and_zero_rhs(cvk, oracle):
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.012)
+    n = len(rp) - 1
+    A = P.CsrMatrix(n, n, rp, ci, v)
+    M = P.ilu0(A, 2)
+    for k in (0, 1, 5, 13):
+        r = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-30, max_iter=k)).report
+        assert not r.converged and r.iterations == k
+    r = P.solve(P.SolverId.BiCGStab, A, np.zeros(n, complex), M).report
+    assert r.converged and r.iterations == 0
