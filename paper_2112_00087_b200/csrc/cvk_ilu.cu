@@ -135,6 +135,27 @@ __device__ void ic_rho(IcState* st, double2 rho_new) {
     st->it = it;
 }
 
+template <int MODE>
+__device__ void ic_fold_tail(const IcArgs& a);
+
+// a.fused: the CTA that publishes its partial last folds them and runs the
+// scalar step (no separate 1-CTA k_ic_fold launch)
+template <int MODE>
+__device__ __forceinline__ void ic_finish(const IcArgs& a) {
+    if (!a.fused) return;
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&a.st->counter, 1u) == gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) a.st->counter = 0;
+    ic_fold_tail<MODE>(a);
+}
+
 // stage 1: MODE 0 init {|r|^2, <r, r>}, 1 <sh, v>, 2 {|t|^2, <t, s>}
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_ic_dot(IcArgs a) {
@@ -154,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) k_ic_dot(IcArgs a) {
         }
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+    ic_finish<MODE>(a);
 }
 
 // p = r (it == 1) or p = beta (p - omega v) + r  (axpy then xpay, krylov.cpp:77-80)
@@ -181,6 +203,7 @@ __global__ void __launch_bounds__(kThreads) k_ic_s(IcArgs a) {
         acc_norm(acc[0], si);
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+    ic_finish<3>(a);
 }
 
 // x += omega s; r = s - omega t; partials |r|^2 and <sh, r>
@@ -198,14 +221,14 @@ __global__ void __launch_bounds__(kThreads) k_ic_xr(IcArgs a) {
         acc_dot(acc[1], __ldg(a.sh + i), ri);
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
+    ic_finish<4>(a);
 }
 
 // stage 2 + the scalar step.  MODE 0: bnorm and rho_1; 1: gamma -> alpha;
 // 2: omega; 3: |s| test; 4: |r| test, then rho for the next iteration.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_ic_fold(IcArgs a) {
+__device__ void ic_fold_tail(const IcArgs& a) {
     IcState* st = a.st;
-    if (st->done) return;
     double2 v[2];
     fold_partials<2>(v, a.part, kIcBlocks);
     if (threadIdx.x != 0) return;
@@ -238,6 +261,12 @@ __global__ void __launch_bounds__(kThreads) k_ic_fold(IcArgs a) {
     }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_ic_fold(IcArgs a) {
+    if (a.st->done) return;
+    ic_fold_tail<MODE>(a);
+}
+
 int ic_grid(int n) {
     (void)n;
     return kIcBlocks;
@@ -247,7 +276,7 @@ int ic_grid(int n) {
 
 cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st) {
     k_ic_dot<0><<<kIcBlocks, kThreads, 0, st>>>(a);
-    k_ic_fold<0><<<1, kThreads, 0, st>>>(a);
+    if (!a.fused) k_ic_fold<0><<<1, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -260,16 +289,16 @@ static cudaError_t ic_iter(const IcArgs& a, const IluDev& M, Spmv&& spmv, int* n
     if ((e = spmv(a.p)) != cudaSuccess) return e;
     if ((e = launch_ilu0_apply(M, a.tmp, a.v, a.ptmp, nl, st)) != cudaSuccess) return e;
     k_ic_dot<1><<<G, kThreads, 0, st>>>(a);
-    k_ic_fold<1><<<1, kThreads, 0, st>>>(a);
+    if (!a.fused) k_ic_fold<1><<<1, kThreads, 0, st>>>(a);
     k_ic_s<<<G, kThreads, 0, st>>>(a);
-    k_ic_fold<3><<<1, kThreads, 0, st>>>(a);
+    if (!a.fused) k_ic_fold<3><<<1, kThreads, 0, st>>>(a);
     if ((e = spmv(a.s)) != cudaSuccess) return e;
     if ((e = launch_ilu0_apply(M, a.tmp, a.t, a.ptmp, nl, st)) != cudaSuccess) return e;
     k_ic_dot<2><<<G, kThreads, 0, st>>>(a);
-    k_ic_fold<2><<<1, kThreads, 0, st>>>(a);
+    if (!a.fused) k_ic_fold<2><<<1, kThreads, 0, st>>>(a);
     k_ic_xr<<<G, kThreads, 0, st>>>(a);
-    k_ic_fold<4><<<1, kThreads, 0, st>>>(a);
-    *nl += 12;
+    if (!a.fused) k_ic_fold<4><<<1, kThreads, 0, st>>>(a);
+    *nl += a.fused ? 8 : 12;
     return cudaGetLastError();
 }
 

@@ -104,6 +104,7 @@ struct IcState {
     long long it, iterations, max_iter, hl, hist_cap;
     double bnorm, brk, tol, final_relres;
     double2 rho, alpha, omega, beta;
+    unsigned counter;  // last-arrival counter of the fused folds
 };
 struct IcArgs {
     int n;
@@ -112,6 +113,7 @@ struct IcArgs {
     double2* part;  // >= 4 * 592 double2
     IcState* st;
     double* hist;
+    int fused;  // 1: stage-1 kernels fold in their last CTA; 0: separate k_ic_fold launches
 };
 cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st);
 // `iters` iterations; spmv(ctx, in) computes A in -> a.tmp on st

@@ -158,3 +158,21 @@ def test_chain_max_iter_and_zero_rhs(cvk, oracle):
         assert not r.converged and r.iterations == k
     r = P.solve(P.SolverId.BiCGStab, A, np.zeros(n, complex), M).report
     assert r.converged and r.iterations == 0
+
+
+def test_fused_folds_bitwise_separate_folds(cvk, oracle, monkeypatch):
+    """Separate 1-CTA k_ic_fold launches (default) or the last-arriving CTA
+    folding the partials (CVK_ILU_FUSED_FOLD=1, opt-in): same sums, same bits."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.008, 250.0)
+    n = len(rp) - 1
+    A = P.CsrMatrix(n, n, rp, ci, v)
+    M = P.ilu0(A, 3)
+    opts = P.SolverOptions(tol=1e-9, max_iter=100000)
+    sep = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
+    monkeypatch.setenv("CVK_ILU_FUSED_FOLD", "1")
+    fused = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
+    monkeypatch.delenv("CVK_ILU_FUSED_FOLD")
+    assert fused.report.iterations == sep.report.iterations
+    assert np.array_equal(bits(fused.x), bits(sep.x))
+    assert fused.report.kernel_launches < sep.report.kernel_launches
