@@ -14,9 +14,15 @@ from paper_2112_00087_b200 import helmholtz as Hm  # noqa: E402
 
 
 def run(h, f=100.0, tol=1e-8):
-    g = Hm.build_grid(2.4, 1.2, h, 0.4, 0.65, 0.01)
-    pr = Hm.assemble(g, 2 * math.pi * f, 340.0, np.ones(g.roof_size(), np.complex128))
-    A, b = pr.A, pr.b
+    if str(h).startswith("fem:"):  # 3-D P1 FEM cavity, N cells per edge (fem3d.py)
+        from paper_2112_00087_b200 import fem3d as F
+        cav = F.build_cavity(int(str(h)[4:]))
+        A, b = cav.matrix(2 * math.pi * f), cav.b
+    else:
+        h = float(h)
+        g = Hm.build_grid(2.4, 1.2, h, 0.4, 0.65, 0.01)
+        pr = Hm.assemble(g, 2 * math.pi * f, 340.0, np.ones(g.roof_size(), np.complex128))
+        A, b = pr.A, pr.b
     opts = P.SolverOptions(tol=tol, max_iter=200000)
     out = {"h": h, "dof": A.nrows, "nnz": A.nnz()}
     for name, mk in [("jacobi", lambda: P.jacobi(A))] + [
@@ -33,4 +39,4 @@ def run(h, f=100.0, tol=1e-8):
 
 if __name__ == "__main__":
     for h in (sys.argv[1:] or ["0.008", "0.0017"]):
-        run(float(h))
+        run(h)
