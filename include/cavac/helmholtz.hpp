@@ -65,6 +65,9 @@ struct LineProfile {
     double coordinate;
     std::vector<std::pair<double, double>> samples;
 };
+// Post-processing, off the solve path: declared for the reference's
+// pipeline.cpp, defined by the reference's own helmholtz.cpp (not by
+// libcavac_host.so).
 std::vector<LineProfile> sample_lines(const HelmholtzProblem& problem, const CVector& solution,
                                       const std::vector<LineSpec>& lines);
 void write_profiles_csv(const std::string& path, const std::vector<LineProfile>& profiles);

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CVK_ABI_VERSION 1
+#define CVK_ABI_VERSION 2
 
 /* status codes */
 #define CVK_OK 0
@@ -66,9 +66,14 @@ extern "C" {
 #define CVK_GMRES 3 /* beyond reference: restarted GMRES(m) */
 
 /* arithmetic modes */
-#define CVK_MODE_FAST 0 /* tree reductions, group-per-row SpMV (the product) */
-#define CVK_MODE_REF 1  /* reference order: row-sequential SpMV and sequential
-                           dots; bitwise identical to the reference CPU code */
+#define CVK_MODE_FAST 0     /* double-double reductions, streamed SpMV (the product) */
+#define CVK_MODE_REF 1      /* reference order: row-sequential SpMV and sequential
+                               dots, each dot summed by one thread in element order
+                               (ExecMode::Sequential); bitwise the reference CPU code */
+#define CVK_MODE_REF_PAR 2  /* the same sums in the same order (bitwise CVK_MODE_REF),
+                               with the element terms formed by all threads of a CTA
+                               and one thread running only the dependent adds
+                               (ExecMode::Parallel, numkit.hpp:14-18) */
 
 /* breakdown codes (SolveReport.breakdown strings, krylov.cpp) */
 #define CVK_BRK_NONE 0
@@ -91,7 +96,10 @@ typedef struct {
     int64_t l;             /* BiCGSTAB(l) degree, default 8 */
     int64_t m;             /* GMRES restart, default 30 (beyond reference) */
     int32_t record_history;
-    int32_t mode;          /* CVK_MODE_FAST / CVK_MODE_REF */
+    int32_t mode;          /* CVK_MODE_FAST / CVK_MODE_REF / CVK_MODE_REF_PAR (< 0: ctx ExecMode) */
+    int32_t warm;          /* Schwarz inner BiCGSTAB solves start from the previous sweep's
+                              solution (beyond the reference, cvk_schwarz_solve / cvk_ddm_rank_create) */
+    int32_t reserved;
 } cvk_opts;
 
 /* SolveReport (krylov.hpp:25-33).  history is caller-owned (may be NULL);
@@ -124,9 +132,29 @@ int cvk_ctx_destroy(cvk_ctx *ctx);
 /* the stream all work of this context is issued on (a cudaStream_t) */
 void *cvk_ctx_stream(cvk_ctx *ctx);
 /* ExecMode (numkit.hpp:14-21): 0 Sequential -> CVK_MODE_REF, 1 Parallel ->
- * CVK_MODE_FAST.  Used when cvk_opts.mode < 0 and by the kernel calls. */
+ * CVK_MODE_REF_PAR.  Both give the reference's iterates bit for bit, as the
+ * reference promises for its two modes.  Used when cvk_opts.mode < 0 and by
+ * the kernel calls with mode < 0; FAST is always an explicit choice. */
 int cvk_set_exec_mode(cvk_ctx *ctx, int parallel);
 int cvk_get_exec_mode(cvk_ctx *ctx);
+
+/* Execution-path options of a context (measurement and path-parity tests;
+ * the defaults are the tuned product choices).  Unknown key -> CVK_EINVAL. */
+#define CVK_OPT_PHASED_MIN_N 1     /* rows from which BiCGSTAB / tfQMR / BiCGSTAB(l) run as
+                                      phase kernels instead of one persistent kernel (131072) */
+#define CVK_OPT_MAX_CTAS 2         /* cap on the persistent / thread-per-row grid, 0 = none */
+#define CVK_OPT_STREAM 3           /* 1: TMA-streamed SpMV phases (default), 0: thread-per-row */
+#define CVK_OPT_STREAM_FLAVOR 4    /* 0 auto, 2: 2 x 224-row consumer groups, 4: 4 x 128 */
+#define CVK_OPT_SPMV_GROUP 5       /* lanes per row of the thread-per-row FAST SpMV, 0 auto
+                                      (read at cvk_csr_upload) */
+#define CVK_OPT_GMRES_PERSISTENT 6 /* 1: GMRES in one persistent kernel at any size */
+#define CVK_OPT_BICGL_PERSISTENT 7 /* 1: BiCGSTAB(l) in one persistent kernel at any size */
+#define CVK_OPT_ILU_HOSTLOOP 8     /* 1: ILU(0) BiCGSTAB as a host loop with scalar read-backs */
+#define CVK_OPT_DDM_SEQ_MIN 9      /* strip rows from which Schwarz inner solves run one after
+                                      another on the single-system path (131072) */
+#define CVK_OPT_RB_STREAM_MIN 10   /* own rows from which row-block phases are streamed */
+int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
+int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 
 /* ---- matrix ---- */
 int cvk_csr_upload(cvk_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz,
@@ -278,8 +306,8 @@ int cvk_ddm_rank_solution(cvk_ddm_rank *rank, double *x_cols);
 int cvk_ddm_rank_get_traces(cvk_ddm_rank *rank, double *g_l, double *g_r);
 int cvk_ddm_rank_set_traces(cvk_ddm_rank *rank, const double *g_l, const double *g_r);
 /* warm-started inner solves (beyond the reference; BiCGSTAB inner solver):
- * each strip's solve starts from its previous-sweep solution.  Also set for
- * cvk_schwarz_solve by the environment variable CVK_DDM_WARM=1. */
+ * each strip's solve starts from its previous-sweep solution.  The initial
+ * value is inner->warm of cvk_ddm_rank_create / cvk_schwarz_solve. */
 int cvk_ddm_rank_set_warm(cvk_ddm_rank *rank, int warm);
 int cvk_ddm_rank_destroy(cvk_ddm_rank *rank);
 

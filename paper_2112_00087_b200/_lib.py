@@ -21,7 +21,11 @@ ERRORS = {
     -1: "EINVAL", -2: "ECUDA", -3: "ENOMEM", -4: "EOVERFLOW", -5: "EZERODIAG",
     -6: "ESOLVER", -7: "ELOGIC", -8: "ETIMEOUT",
 }
-MODE_FAST, MODE_REF = 0, 1
+MODE_FAST, MODE_REF, MODE_REF_PAR = 0, 1, 2
+# cvk_ctx_set_option keys (include/cavac_b200.h)
+OPTIONS = {"phased_min_n": 1, "max_ctas": 2, "stream": 3, "stream_flavor": 4, "spmv_group": 5,
+           "gmres_persistent": 6, "bicgl_persistent": 7, "ilu_hostloop": 8, "ddm_seq_min": 9,
+           "rb_stream_min": 10}
 
 
 class CvkOpts(C.Structure):
@@ -32,6 +36,8 @@ class CvkOpts(C.Structure):
         ("m", C.c_int64),
         ("record_history", C.c_int32),
         ("mode", C.c_int32),
+        ("warm", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -104,6 +110,8 @@ def load():
         "cvk_ctx_stream": ([P], P),
         "cvk_set_exec_mode": ([P, i32], i32),
         "cvk_get_exec_mode": ([P], i32),
+        "cvk_ctx_set_option": ([P, i32, i64], i32),
+        "cvk_ctx_get_option": ([P, i32, C.POINTER(i64)], i32),
         "cvk_csr_upload": ([P, i64, i64, i64, P, P, P, C.POINTER(P)], i32),
         "cvk_csr_set_values": ([P, P], i32),
         "cvk_csr_free": ([P], i32),

@@ -14,10 +14,12 @@ behaviour follow the reference headers (paths relative to proj/core/):
 std::invalid_argument -> InvalidArgument (a ValueError), std::logic_error ->
 LogicError, std::runtime_error -> RuntimeError.  Vectors live on the host as
 numpy arrays (the reference's CVector); matrices are uploaded to the device
-once and cached on the CsrMatrix.  ExecMode.Sequential selects the device's
-reference-order arithmetic (bitwise identical to the reference CPU code),
-ExecMode.Parallel the fast reductions -- the GPU analogue of the reference's
-two kernel modes (numkit.hpp:14-18).
+once and cached on the CsrMatrix.  The reference's two kernel modes
+(numkit.hpp:14-18) both give its iterates bit for bit: ExecMode.Sequential
+sums every dot in one device thread, ExecMode.Parallel forms the element terms
+with a whole CTA and keeps one thread on the dependent adds.  ExecMode.Fast
+(beyond the reference, the default of this module) is the product path:
+double-double reductions and the streamed phase kernels.
 """
 from __future__ import annotations
 
@@ -43,6 +45,7 @@ class LogicError(RuntimeError):
 class ExecMode(enum.IntEnum):
     Sequential = 0
     Parallel = 1
+    Fast = 2  # beyond the reference: the B200 product arithmetic
 
 
 class SolverId(enum.IntEnum):
@@ -61,6 +64,17 @@ def solver_name(sid: SolverId) -> str:
 
 
 def solver_from_name(name: str) -> SolverId:
+    """krylov.cpp:377-384: the reference's three names; "gmres" is rejected
+    with the reference's message (test_krylov.cpp:35-46, test_config.cpp:37-46).
+    The B200 extensions are reached through solver_id / gmres()."""
+    for k in (SolverId.BiCGStab, SolverId.BiCGStabL, SolverId.TfQmr):
+        if _NAMES[k] == name:
+            return k
+    raise InvalidArgument(f'unknown solver "{name}" (allowed: bicgstab, bicgstab_l, tfqmr)')
+
+
+def solver_id(name: str) -> SolverId:
+    """solver_from_name plus the B200 extensions ("gmres")."""
     for k, v in _NAMES.items():
         if v == name:
             return k
@@ -93,7 +107,7 @@ class Device:
             self.handle = None
 
 
-_mode = ExecMode.Parallel
+_mode = ExecMode.Fast
 
 
 def set_exec_mode(mode: ExecMode) -> None:
@@ -107,7 +121,35 @@ def exec_mode() -> ExecMode:
 
 def _dev_mode(mode: Optional[ExecMode] = None) -> int:
     m = _mode if mode is None else ExecMode(mode)
-    return _lib.MODE_REF if m == ExecMode.Sequential else _lib.MODE_FAST
+    return {ExecMode.Sequential: _lib.MODE_REF, ExecMode.Parallel: _lib.MODE_REF_PAR}.get(m, _lib.MODE_FAST)
+
+
+class path_options:
+    """Execution-path options of the default device context (cvk_ctx_set_option),
+    restored on exit: ``with path_options(phased_min_n=0, stream=0): ...``.
+    For path-parity tests and measurements; the defaults are the product's."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.saved = {}
+
+    def __enter__(self):
+        L = _lib.load()
+        h = Device.default().handle
+        for k, v in self.kw.items():
+            key = _lib.OPTIONS[k]
+            old = C.c_int64()
+            check(L.cvk_ctx_get_option(h, key, C.byref(old)))
+            self.saved[key] = old.value
+            check(L.cvk_ctx_set_option(h, key, int(v)))
+        return self
+
+    def __exit__(self, *exc):
+        L = _lib.load()
+        h = Device.default().handle
+        for key, v in self.saved.items():
+            L.cvk_ctx_set_option(h, key, v)
+        return False
 
 
 # ------------------------------------------------------------- numkit ----
@@ -417,7 +459,7 @@ _BRK = {0: None, 1: "rho breakdown", 2: "stagnation in <shadow, v>", 3: "omega b
 
 def _opts(o: SolverOptions, mode: Optional[ExecMode]) -> CvkOpts:
     return CvkOpts(float(o.tol), int(o.max_iter), int(o.l), int(o.m),
-                   1 if o.record_history else 0, _dev_mode(mode))
+                   1 if o.record_history else 0, _dev_mode(mode), 0, 0)
 
 
 def _report(r: CvkReport, hist) -> SolveReport:

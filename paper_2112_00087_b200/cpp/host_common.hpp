@@ -13,7 +13,7 @@ namespace cavac::detail {
 // Lazily created context on device $CVK_DEVICE (default 0).
 cvk_ctx* ctx();
 
-// ExecMode -> CVK_MODE_REF / CVK_MODE_FAST
+// ExecMode -> CVK_MODE_REF (Sequential) / CVK_MODE_REF_PAR (Parallel)
 int device_mode();
 
 // Map a C-ABI status onto the reference's exception types.

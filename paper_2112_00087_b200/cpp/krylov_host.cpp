@@ -17,20 +17,28 @@ CVector JacobiApply::operator()(const CVector& v) const {
 
 Preconditioner identity_preconditioner() { return {IdentityApply{}}; }
 
-// krylov.cpp:31-55: the inverse diagonal is computed by the device kernel
-// (first col == i entry, 1.0 / d with __divdc3 rounding) and kept on the host
-// inside the callable so apply() works as in the reference.
+// krylov.cpp:31-55: the first col == i entry of each row, inverted with
+// std::complex division (libgcc __divdc3, the reference's rounding).  This is
+// host setup, one pass over the rows the caller already holds: uploading A
+// only to read n values back would double the transfer of a
+// jacobi + solve pair (pipeline.cpp:196-202).  The callable keeps the inverse
+// diagonal so apply() works as in the reference, and the device solve takes
+// it from there (cvk_precond_jacobi with inv_diag).
 Preconditioner jacobi(const CsrMatrix& A) {
     if (A.nrows != A.ncols) throw std::invalid_argument("jacobi: matrix must be square");
     JacobiApply f;
     f.inv_diag.assign(A.nrows, Complex(0.0));
-    if (A.nrows) {
-        detail::DevCsr d(A);
-        cvk_prec* M = nullptr;
-        detail::check(cvk_precond_jacobi(d.h, nullptr, &M));
-        const int e = cvk_precond_get_diag(M, reinterpret_cast<double*>(f.inv_diag.data()));
-        cvk_precond_free(M);
-        detail::check(e);
+    for (std::size_t i = 0; i < A.nrows; ++i) {
+        bool found = false;
+        for (std::size_t k = A.row_offsets[i]; k < A.row_offsets[i + 1]; ++k)
+            if (A.col_indices[k] == i) {
+                if (A.values[k] != Complex(0.0)) {
+                    f.inv_diag[i] = Complex(1.0) / A.values[k];
+                    found = true;
+                }
+                break;
+            }
+        if (!found) throw std::invalid_argument("jacobi: zero diagonal at row " + std::to_string(i));
     }
     return {f};
 }
@@ -60,7 +68,7 @@ SolveResult device_solve(int solver, const char* name, const CsrMatrix& A, const
                                     ": the device solvers support the jacobi and identity preconditioners");
     }
     cvk_opts o{opts.tol, (int64_t)opts.max_iter, (int64_t)opts.l, (int64_t)opts.m,
-               opts.record_history ? 1 : 0, detail::device_mode()};
+               opts.record_history ? 1 : 0, opts.fast_reductions ? CVK_MODE_FAST : detail::device_mode(), 0, 0};
     cvk_report r{};
     std::vector<double> hist;
     if (opts.record_history) {
@@ -104,8 +112,7 @@ SolverId solver_from_name(const std::string& name) {
     if (name == "bicgstab") return SolverId::BiCGStab;
     if (name == "bicgstab_l") return SolverId::BiCGStabL;
     if (name == "tfqmr") return SolverId::TfQmr;
-    if (name == "gmres") return SolverId::GMRES;
-    throw std::invalid_argument("unknown solver \"" + name + "\" (allowed: bicgstab, bicgstab_l, tfqmr, gmres)");
+    throw std::invalid_argument("unknown solver \"" + name + "\" (allowed: bicgstab, bicgstab_l, tfqmr)");
 }
 
 std::string solver_name(SolverId id) {

@@ -26,7 +26,10 @@ cvk_ctx* ctx() {
     return g_ctx;
 }
 
-int device_mode() { return g_mode.load() == ExecMode::Sequential ? CVK_MODE_REF : CVK_MODE_FAST; }
+// Both ExecModes give the reference's iterates bit for bit, as the reference
+// promises (numkit.hpp:14-18); Parallel forms the reduction terms with whole
+// CTAs (CVK_MODE_REF_PAR).  The FAST arithmetic is SolverOptions::fast_reductions.
+int device_mode() { return g_mode.load() == ExecMode::Sequential ? CVK_MODE_REF : CVK_MODE_REF_PAR; }
 
 }  // namespace detail
 

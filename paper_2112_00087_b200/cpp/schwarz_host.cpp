@@ -27,7 +27,8 @@ DdmResult schwarz_solve(const HelmholtzProblem& problem, const Partition& part, 
     std::vector<int64_t> cb(part.col_begin.begin(), part.col_begin.end());
     const double sl[2] = {tp.s_left.real(), tp.s_left.imag()};
     const double sr[2] = {tp.s_right.real(), tp.s_right.imag()};
-    cvk_opts o{inner.tol, (int64_t)inner.max_iter, (int64_t)inner.l, (int64_t)inner.m, 0, detail::device_mode()};
+    cvk_opts o{inner.tol, (int64_t)inner.max_iter, (int64_t)inner.l, (int64_t)inner.m, 0,
+               inner.fast_reductions ? CVK_MODE_FAST : detail::device_mode(), 0, 0};
     DdmResult res;
     res.x.assign(problem.A.nrows, Complex(0.0));
     std::vector<double> hist(max_outer + 1, 0.0);

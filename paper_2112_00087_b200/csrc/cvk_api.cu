@@ -31,9 +31,8 @@ size_t flavor_stage_bytes(int capk, int nvec, int ngather);
 size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
-                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
-                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
-                      int dyn, int pf_rows, int nband);
+                      const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows);
 }  // namespace cvk_g4
 namespace cvk {
 int flavor_stream_rows();
@@ -42,16 +41,30 @@ size_t flavor_stage_bytes(int capk, int nvec, int ngather);
 size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
-                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
-                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
-                      int dyn, int pf_rows, int nband);
+                      const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows);
 }  // namespace cvk
+
+// execution-path options (cvk_ctx_set_option); defaults are the product's
+struct CvkKnobs {
+    long long phased_min_n = 131072;
+    long long max_ctas = 0;
+    long long stream = 1;
+    long long flavor = 0;
+    long long spmv_group = 0;
+    long long gmres_persistent = 0;
+    long long bicgl_persistent = 0;
+    long long ilu_hostloop = 0;
+    long long ddm_seq_min = 131072;
+    long long rb_stream_min = 65536;
+};
 
 struct cvk_ctx {
     int device = 0;
     int nsm = 0;
     cudaStream_t stream = nullptr;
-    int exec_parallel = 1;
+    int exec_parallel = 0;  // ExecMode::Sequential, the reference's initial mode (numkit.cpp:16)
+    CvkKnobs knob;
     // reusable workspace
     void* work = nullptr;
     size_t work_bytes = 0;
@@ -95,7 +108,6 @@ struct cvk_csr {
     int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
     int capk_g4 = 0;  // the same for the 128-row chunks of the cvk_g4 flavor
     int* cmax = nullptr;  // [nchunks] largest column of each streamed chunk (L2 prefetch)
-    int4* bands = nullptr;  // [nchunks] halo bands {b0, w0, b1, w1} of each streamed chunk
 };
 
 struct cvk_prec {
@@ -125,11 +137,9 @@ int fail(int code, const std::string& msg) {
 
 const char* kSolverNames[] = {"bicgstab", "bicgstab_l", "tfqmr", "gmres"};
 
-int pick_group(double avg_nnz) {
-    if (const char* env = std::getenv("CVK_SPMV_GROUP")) {
-        const int v = std::atoi(env);
-        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return v;
-    }
+int pick_group(const cvk_ctx* c, double avg_nnz) {
+    const long long v = c->knob.spmv_group;
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return (int)v;
     // thread per row with all of a row's loads issued up front wins up to
     // ~16 entries per row (profiles/r01_spmv_lab.txt); lanes per row beyond
     if (avg_nnz <= 16.0) return 1;
@@ -149,8 +159,26 @@ int ensure(cvk_ctx* c, void** p, size_t* have, size_t need) {
 }
 
 int resolve_mode(const cvk_ctx* c, int mode) {
-    if (mode == CVK_MODE_FAST || mode == CVK_MODE_REF) return mode;
-    return c->exec_parallel ? CVK_MODE_FAST : CVK_MODE_REF;
+    if (mode == CVK_MODE_FAST || mode == CVK_MODE_REF || mode == CVK_MODE_REF_PAR) return mode;
+    return c->exec_parallel ? CVK_MODE_REF_PAR : CVK_MODE_REF;
+}
+
+bool is_ref(int mode) { return mode == CVK_MODE_REF || mode == CVK_MODE_REF_PAR; }
+
+long long* knob_slot(cvk_ctx* c, int key) {
+    switch (key) {
+        case CVK_OPT_PHASED_MIN_N: return &c->knob.phased_min_n;
+        case CVK_OPT_MAX_CTAS: return &c->knob.max_ctas;
+        case CVK_OPT_STREAM: return &c->knob.stream;
+        case CVK_OPT_STREAM_FLAVOR: return &c->knob.flavor;
+        case CVK_OPT_SPMV_GROUP: return &c->knob.spmv_group;
+        case CVK_OPT_GMRES_PERSISTENT: return &c->knob.gmres_persistent;
+        case CVK_OPT_BICGL_PERSISTENT: return &c->knob.bicgl_persistent;
+        case CVK_OPT_ILU_HOSTLOOP: return &c->knob.ilu_hostloop;
+        case CVK_OPT_DDM_SEQ_MIN: return &c->knob.ddm_seq_min;
+        case CVK_OPT_RB_STREAM_MIN: return &c->knob.rb_stream_min;
+    }
+    return nullptr;
 }
 
 double now_s() {
@@ -160,6 +188,10 @@ double now_s() {
 }  // namespace
 
 int cvk_fail(int code, const std::string& msg) { return fail(code, msg); }
+long long cvk_ctx_knob(cvk_ctx* c, int key) {
+    const long long* p = knob_slot(c, key);
+    return p ? *p : 0;
+}
 
 extern "C" {
 
@@ -167,7 +199,6 @@ int cvk_abi_version(void) { return CVK_ABI_VERSION; }
 
 // measurement builds only (CVK_TRACE): not part of include/cavac_b200.h
 int cvk_trace_read(void* out, size_t bytes) { return cvk::phased_trace_read(out, bytes); }
-int cvk_streamk_trace_read(unsigned long long* out16) { return cvk::streamk_trace_read(out16); }
 const char* cvk_last_error(void) { return g_err.c_str(); }
 
 const char* cvk_breakdown_name(int code) {
@@ -268,6 +299,22 @@ int cvk_set_exec_mode(cvk_ctx* c, int parallel) {
 }
 int cvk_get_exec_mode(cvk_ctx* c) { return c ? c->exec_parallel : 0; }
 
+int cvk_ctx_set_option(cvk_ctx* c, int key, int64_t value) {
+    if (!c) return fail(CVK_EINVAL, "null ctx");
+    long long* p = knob_slot(c, key);
+    if (!p) return fail(CVK_EINVAL, "cvk_ctx_set_option: unknown option " + std::to_string(key));
+    *p = value;
+    return CVK_OK;
+}
+
+int cvk_ctx_get_option(cvk_ctx* c, int key, int64_t* value) {
+    if (!c || !value) return fail(CVK_EINVAL, "cvk_ctx_get_option: null argument");
+    const long long* p = knob_slot(c, key);
+    if (!p) return fail(CVK_EINVAL, "cvk_ctx_get_option: unknown option " + std::to_string(key));
+    *value = *p;
+    return CVK_OK;
+}
+
 int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const uint64_t* row_offsets,
                    const uint64_t* col_indices, const double* values, cvk_csr** out) {
     if (!c || !out) return fail(CVK_EINVAL, "cvk_csr_upload: null argument");
@@ -295,7 +342,7 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     A->ctx = c;
     A->n = nrows;
     A->nnz = nnz;
-    A->group = pick_group(nrows ? (double)nnz / (double)nrows : 1.0);
+    A->group = pick_group(c, nrows ? (double)nnz / (double)nrows : 1.0);
 
     // one allocation [values | columns | row offsets] so a single L2
     // access-policy window can pin the whole matrix (solve-time persistence)
@@ -336,38 +383,6 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
             cudaMemcpy(A->cmax, cm.data(), sizeof(int) * cm.size(), cudaMemcpyHostToDevice);
         else
             A->cmax = nullptr;
-        // Halo bands: the out-of-chunk columns of each chunk, clustered; the two
-        // most-referenced clusters that fit in kStreamRows rows are staged with
-        // the chunk (cvk_stream.cuh).  For the cavity grid these are the +-nx
-        // neighbour rows; anything else stays a global gather.
-        std::vector<int4> bd((size_t)std::max<int64_t>(1, nch), make_int4(0, 0, 0, 0));
-        bool any = false;
-        std::vector<int> cols;
-        for (int64_t q = 0; q < nch; ++q) {
-            const int64_t r0 = q * cvk::kStreamRows, r1 = std::min<int64_t>(r0 + cvk::kStreamRows, nrows);
-            cols.clear();
-            for (int64_t k = rp[(size_t)r0]; k < rp[(size_t)r1]; ++k)
-                if (ci[(size_t)k] < r0 || ci[(size_t)k] >= r1) cols.push_back(ci[(size_t)k]);
-            if (cols.empty()) continue;
-            std::sort(cols.begin(), cols.end());
-            // clusters: maximal runs whose span fits a band
-            struct Cl { int lo, hi, cnt; };
-            std::vector<Cl> cl;
-            for (int v : cols) {
-                if (!cl.empty() && v - cl.back().lo < cvk::kStreamRows) { cl.back().hi = v; cl.back().cnt++; }
-                else cl.push_back({v, v, 1});
-            }
-            std::sort(cl.begin(), cl.end(), [](const Cl& a, const Cl& b) { return a.cnt > b.cnt; });
-            int4 b = make_int4(0, 0, 0, 0);
-            if (cl.size() >= 1 && cl[0].cnt >= 8) { b.x = cl[0].lo; b.y = cl[0].hi - cl[0].lo + 1; }
-            if (cl.size() >= 2 && cl[1].cnt >= 8) { b.z = cl[1].lo; b.w = cl[1].hi - cl[1].lo + 1; }
-            if (b.y || b.w) any = true;
-            bd[(size_t)q] = b;
-        }
-        if (any && cudaMalloc(&A->bands, sizeof(int4) * bd.size()) == cudaSuccess)
-            cudaMemcpy(A->bands, bd.data(), sizeof(int4) * bd.size(), cudaMemcpyHostToDevice);
-        else
-            A->bands = nullptr;
     }
     *out = A;
     return CVK_OK;
@@ -396,7 +411,6 @@ int cvk_csr_free(cvk_csr* A) {
     cudaStreamSynchronize(A->ctx->stream);
     cudaFree(A->blob);
     if (A->cmax) cudaFree(A->cmax);
-    if (A->bands) cudaFree(A->bands);
     delete A;
     return CVK_OK;
 }
@@ -566,6 +580,14 @@ int cvk_precond_ilu0(cvk_csr* A, int sweeps, cvk_prec** out) {
         CK(cudaMemcpyAsync(f.data(), A->av, sizeof(double2) * nnz, cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
+    // the IKJ factor below walks each row in column order (L part, then U from
+    // the diagonal on): a row with unsorted or repeated columns would get a
+    // silently wrong factor, so reject it (csr_from_triplets sorts,
+    // numkit.cpp:41-75; a hand-built CsrMatrix need not)
+    for (int64_t i = 0; i < n; ++i)
+        for (int p = rp[i] + 1; p < rp[i + 1]; ++p)
+            if (ci[p] <= ci[p - 1])
+                return fail(CVK_EINVAL, "ilu0: columns of row " + std::to_string(i) + " are not strictly increasing");
     std::vector<int64_t> pos(std::max<int64_t>(1, n), -1), dg(std::max<int64_t>(1, n), -1);
     for (int64_t i = 0; i < n; ++i) {
         for (int p = rp[i]; p < rp[i + 1]; ++p) {
@@ -702,12 +724,14 @@ struct IcSpmv {
     double2* out;
     int optin, nsm, streamed;
     cudaStream_t st;
+    const int* skip;  // the chain's done flag
 };
 static cudaError_t ic_spmv(void* ctx, const double2* in) {
     const IcSpmv* q = (const IcSpmv*)ctx;
     const cvk_csr* A = q->A;
     if (q->streamed)
-        return cvk::launch_spmv_stream((int)A->n, A->rp, A->ci, A->av, in, q->out, A->capk, q->nsm, q->optin, q->st);
+        return cvk::launch_spmv_stream((int)A->n, A->rp, A->ci, A->av, in, q->out, A->capk, q->nsm, q->optin, q->st,
+                                       q->skip);
     return cvk::launch_spmv(A->group, false, (int)A->n, A->rp, A->ci, A->av, in, q->out, 0, q->st);
 }
 
@@ -725,7 +749,6 @@ static int solve_ilu_chain(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, cons
     cvk::IcArgs a;
     a.n = n, a.x = x, a.r = w, a.p = w + nv, a.v = w + 2 * nv, a.s = w + 3 * nv, a.t = w + 4 * nv;
     a.tmp = w + 5 * nv, a.ptmp = w + 6 * nv, a.sh = sh, a.part = c->part;
-    a.fused = std::getenv("CVK_ILU_FUSED_FOLD") && std::atoi(std::getenv("CVK_ILU_FUSED_FOLD")) == 1;  // opt-in: 0.401 vs 0.397 s at 1M
     const long long hcap = o->record_history && rep->history ? std::max<long long>(0, rep->history_cap) : 0;
     void* mem = nullptr;
     CK(cudaMalloc(&mem, sizeof(cvk::IcState) + sizeof(double) * std::max<long long>(1, hcap)));
@@ -736,8 +759,8 @@ static int solve_ilu_chain(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, cons
     h0.record = o->record_history ? 1 : 0;
     h0.max_iter = o->max_iter, h0.hist_cap = hcap, h0.tol = o->tol;
     h0.rho = h0.alpha = h0.omega = make_double2(1.0, 0.0);
-    IcSpmv q{A, a.tmp, 0, c->nsm, 0, st};
-    if (A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && !std::getenv("CVK_NO_STREAM")) {
+    IcSpmv q{A, a.tmp, 0, c->nsm, 0, st, &a.st->done};
+    if (A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && c->knob.stream) {
         CK(cudaDeviceGetAttribute(&q.optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
         q.streamed = 1;
     }
@@ -749,7 +772,7 @@ static int solve_ilu_chain(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, cons
     CK(cvk::launch_ilu0_apply(*M->ilu, b, a.r, a.ptmp, &nl, st));  // r = M^-1 b
     CK(cudaMemcpyAsync(sh, a.r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
     CK(cvk::launch_ic_init(a, st));
-    launches += a.fused ? 1 : 2;
+    launches += 2;
     if (q.streamed) {  // first call outside the capture sets the kernel attributes
         const cudaError_t se = ic_spmv(&q, a.r);
         if (se == cudaErrorInvalidConfiguration) {
@@ -826,8 +849,8 @@ static int solve_ilu_chain(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, cons
 static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                                   const double2* b, double2* x, cvk_report* rep) {
     const int n = (int)A->n;
-    const bool ref = resolve_mode(c, o->mode) == CVK_MODE_REF;
-    if (!ref && M->ilu && n > 0 && !std::getenv("CVK_ILU_HOSTLOOP")) return solve_ilu_chain(c, A, M, o, b, x, rep);
+    const bool ref = is_ref(resolve_mode(c, o->mode));
+    if (!ref && M->ilu && n > 0 && !c->knob.ilu_hostloop) return solve_ilu_chain(c, A, M, o, b, x, rep);
     cudaStream_t st = c->stream;
     int e;
     const size_t nv = (size_t)std::max(1, n);
@@ -949,40 +972,6 @@ static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* 
 // lazily polled device `done` flag -> (tfQMR x fix-up) -> true residual.
 static constexpr int kIterPerGraph = 8;
 
-static long long phased_min_n() {
-    if (const char* env = std::getenv("CVK_PHASED_MIN_N")) return std::atoll(env);
-    return 131072;
-}
-
-// Optional (CVK_L2_PERSIST=1): pin the matrix in L2 for the duration of a
-// solve.  Measured on the 1M-DOF cavity it is SLOWER (201 vs 177 us per
-// BiCGSTAB iteration): the persisting carve-out starves the eight streamed
-// work vectors, so it is off by default.  Returns true if a window was set.
-static bool l2_pin(cvk_ctx* c, const cvk_csr* A) {
-    const char* env = std::getenv("CVK_L2_PERSIST");
-    if (!env || std::atoi(env) == 0) return false;
-    int maxwin = 0, maxpers = 0;
-    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c->device);
-    if (maxwin <= 0 || maxpers <= 0) return false;
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxpers) != cudaSuccess) return false;
-    const size_t win = std::min<size_t>(A->blob_bytes, (size_t)maxwin);
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.base_ptr = A->blob;
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxpers / (double)win);
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    return cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
-}
-
-static void l2_unpin(cvk_ctx* c) {
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
-    cudaCtxResetPersistingL2Cache();
-}
-
 // cudaLaunchKernel with the programmatic-stream-serialization attribute (PDL)
 static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
@@ -992,21 +981,21 @@ static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args,
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("CVK_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelExC(&cfg, f, args);
 }
 
 static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
-                        const double2* b_dev, double2* x_dev, cvk_report* rep, bool pinned) {
+                        const double2* b_dev, double2* x_dev, cvk_report* rep) {
     const int n = (int)A->n;
     const int S = A->group;
     // consumer shape of the streamed phases: 4 x 128 rows for matrices with
     // many out-of-chunk gathers per row (FEM-3D), 2 x 224 for the 5-point
-    // cavity (cvk_phased_g4.cu); CVK_STREAM_FLAVOR=g2|g4 forces one
+    // cavity (cvk_phased_g4.cu); CVK_OPT_STREAM_FLAVOR forces one
     bool g4 = A->n > 0 && (double)A->nnz / (double)A->n > 8.0;
-    if (const char* env = std::getenv("CVK_STREAM_FLAVOR")) g4 = std::strcmp(env, "g4") == 0;
+    if (c->knob.flavor == 2 || c->knob.flavor == 4) g4 = c->knob.flavor == 4;
     cvk::PhasedKernels K;
     if (g4) cvk_g4::flavor_kernels(&K);
     else cvk::flavor_kernels(&K);
@@ -1023,10 +1012,8 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     // one 256-row chunk per CTA up to kChunkCtasCap CTAs (hardware scheduling
     // keeps the memory pipes full), grid-stride beyond that
-    long long cap = 32LL * per_sm * c->nsm;
-    if (const char* env = std::getenv("CVK_PHASED_GRID")) cap = std::max(1LL, std::atoll(env)) * per_sm * c->nsm;
-    long long G = std::min<long long>(cap, chunks);
-    if (const char* env = std::getenv("CVK_MAX_CTAS")) G = std::min<long long>(G, std::max(1, std::atoi(env)));
+    long long G = std::min<long long>(32LL * per_sm * c->nsm, chunks);
+    if (c->knob.max_ctas > 0) G = std::min<long long>(G, c->knob.max_ctas);
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 8 * (size_t)std::max(1, n))) != CVK_OK) return e;
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
@@ -1050,59 +1037,40 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    // per kernel: staged vectors, gathered vectors
-    // (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_bm_a_s, k_bm_b_s)
-    const int kvec[6] = {5, 5, 7, 8, 7, 6}, kgat[6] = {3, 2, 2, 2, 4, 2};
-    // halo-band staging: measured no faster on the 1M cavity (consumer latency is
-    // not dominated by the out-of-chunk gathers), so opt-in (CVK_BANDS=1)
-    // band staging is per 224-row chunk: the 2 x 224 flavor only
-    const int nband = (!g4 && A->bands && std::getenv("CVK_BANDS") && std::atoi(std::getenv("CVK_BANDS"))) ? 1 : 0;
+    // per kernel: staged vectors, gathered vectors (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s)
+    const int kvec[4] = {5, 5, 7, 8}, kgat[4] = {3, 2, 2, 2};
     auto layout_for = [&](int k, int stg) {
         cvk::StreamLayout L{A->capk, kvec[k], stg};
         L.ngather = kgat[k];
-        L.nband = nband;
         return L;
     };
     auto stage_bytes_k = [&](int k) { return g4 ? stage_bytes(kvec[k], kgat[k]) : layout_for(k, 1).stage_bytes(); };
-    int stg[6];
-    for (int k = 0; k < 6; ++k) {
+    int stg[4];
+    for (int k = 0; k < 4; ++k) {
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
-        long long cap = nband ? 3 : 4;  // measured best ring depths
-        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
-        stg[k] = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));
+        stg[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));  // 4: measured best
     }
-    const bool streamed = !std::getenv("CVK_NO_STREAM") && A->nnz > 0 &&
+    const bool streamed = c->knob.stream && A->nnz > 0 &&
                           (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2 : std::min(stg[2], stg[3]) >= 2);
-    // BiCGSTAB in two streamed kernels per iteration (k_bm_*): opt-in
-    // (CVK_BICG_MERGED=1).  Measured 152 vs 142 us per iteration at 1M DOF:
-    // one launch fewer and 16 n fewer bytes, but the merged SpMV phase (7
-    // staged, 4 gathered vectors) is consumer-bound.
-    const bool merged = streamed && solver == CVK_BICGSTAB && std::min(stg[4], stg[5]) >= 2 && !hs.warm &&
-                        std::getenv("CVK_BICG_MERGED") && std::atoi(std::getenv("CVK_BICG_MERGED")) == 1;
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
-    const void* sk[6] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.bm_a_s, K.bm_b_s};
+    const void* sk[4] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // elementwise phases: grid-stride, 4 elements per thread per trip
     long long Ge = std::min<long long>(2LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
-    if (const char* env = std::getenv("CVK_ELEM_CTAS")) Ge = std::max(1, std::atoi(env));
     if (!streamed) Ge = G;
     const long long Gmax = std::max<long long>(std::max<long long>(G, Ge), c->nsm);
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
         return e;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     {
-        const int contig = std::getenv("CVK_STREAM_CONTIG") ? std::atoi(std::getenv("CVK_STREAM_CONTIG")) : 0;
-        const int dyn = std::getenv("CVK_STREAM_DYN") ? std::atoi(std::getenv("CVK_STREAM_DYN")) : 0;
         // the L2 prefetch window reads A->cmax, which is per 224-row chunk
-        const int pf = g4 ? 0
-                          : (std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF"))
-                                                          : (nband ? 0 : 2 * cvk::kStreamRows));
+        const int pf = g4 ? 0 : 2 * cvk::kStreamRows;
         (g4 ? cvk_g4::flavor_pack_args : cvk::flavor_pack_args)(
-            blob.data(), n, A->rp, A->ci, A->av, g4 ? nullptr : A->cmax, g4 ? nullptr : A->bands, M->dinv, b_dev,
-            x_dev, (double2*)c->work, c->part, c->st, c->hist, c->rep, scapk, stg, contig, dyn, pf, nband);
+            blob.data(), n, A->rp, A->ci, A->av, g4 ? nullptr : A->cmax, M->dinv, b_dev, x_dev, (double2*)c->work,
+            c->part, c->st, c->hist, c->rep, scapk, stg, pf);
     }
     void* args[] = {blob.data()};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
@@ -1112,11 +1080,9 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     std::vector<unsigned char> key(blob);
     key.push_back((unsigned char)solver);
     key.push_back((unsigned char)S);
-    key.push_back((unsigned char)(pinned ? 1 : 0));  // captured nodes carry the L2 window
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
     key.push_back((unsigned char)(streamed ? 1 : 0));
-    key.push_back((unsigned char)(merged ? 1 : 0));
     key.push_back((unsigned char)(g4 ? 1 : 0));
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
@@ -1126,10 +1092,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const dim3 sgrid((unsigned)c->nsm), sblock((unsigned)sthreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
-            if (merged) {
-                launch_pdl(K.bm_a_s, sgrid, sblock, args, smem_for(4), c->stream);
-                launch_pdl(K.bm_b_s, sgrid, sblock, args, smem_for(5), c->stream);
-            } else if (solver == CVK_BICGSTAB) {
+            if (solver == CVK_BICGSTAB) {
                 if (streamed) {
                     launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(0), c->stream);
                     launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(1), c->stream);
@@ -1159,7 +1122,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     CK(cudaEventRecord(c->e0, c->stream));
     long long launches = 0;
     if (solver == CVK_BICGSTAB) {
-        CK(launch_pdl(merged ? K.bm_init : K.bi_init, grid, block, args, 0, c->stream));
+        CK(launch_pdl(K.bi_init, grid, block, args, 0, c->stream));
         launches += 1;
     } else {
         CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
@@ -1175,7 +1138,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaMemcpyAsync(&c->h_done[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += (merged ? 2 : 3) * kIterPerGraph;
+        launches += 3 * kIterPerGraph;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));
@@ -1209,74 +1172,6 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     return CVK_OK;
 }
 
-// Persistent TMA-streamed BiCGSTAB (cvk_streamk.cu): one cooperative launch per
-// solve, one CTA per SM.  Returns CVK_OK, an error, or 1 if the matrix does
-// not fit the ring (caller falls back to the phase kernels).
-static int solve_streamk(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o, const double2* b_dev,
-                         double2* x_dev, cvk_report* rep) {
-    const int n = (int)A->n;
-    int optin = 0;
-    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    cvk::StreamLayout L{A->capk, 5, 1};
-    L.ngather = 3;
-    {
-        const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
-        long long cap = 4;
-        if (const char* env = std::getenv("CVK_STREAM_STAGES")) cap = std::max(2, std::min(cvk::kStreamMaxStages, std::atoi(env)));
-        L.stages = (int)std::min<long long>(cap, std::max<long long>(0, avail / (long long)L.stage_bytes()));
-    }
-    if (L.stages < 2 || A->nnz == 0) return 1;
-    const void* kern = cvk::streamk_bicgstab_kernel();
-    const size_t smem = L.smem_bytes();
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cvk::kStreamThreads, smem));
-    if (per_sm < 1) return 1;
-    const int G = c->nsm;
-    int e;
-    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * 8 * (size_t)std::max(1, n))) != CVK_OK) return e;
-    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)G)) != CVK_OK)
-        return e;
-    const long long hcap = o->record_history ? std::max<long long>(2 * o->max_iter + 8, 16) : 0;
-    if (hcap > 0 && (size_t)hcap > c->hist_cap) {
-        cudaFree(c->hist);
-        c->hist = nullptr;
-        c->hist_cap = 0;
-        CK(cudaMalloc(&c->hist, sizeof(double) * hcap));
-        c->hist_cap = (size_t)hcap;
-    }
-    CK(cudaMemsetAsync(c->bar, 0, 2 * sizeof(unsigned long long), c->stream));
-    std::vector<unsigned char> blob(cvk::streamk_args_size());
-    cvk::streamk_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, A->bands}, M->dinv, b_dev, x_dev,
-                           (double2*)c->work, c->part, c->bar, c->rep, c->hist, hcap, o->tol,
-                           o->max_iter < 1 ? 0 : o->max_iter, o->record_history ? 1 : 0, L);
-    void* args[] = {blob.data()};
-    CK(cudaEventRecord(c->e0, c->stream));
-    CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kStreamThreads), args, smem, c->stream));
-    CK(cudaEventRecord(c->e1, c->stream));
-    DevReport dr;
-    CK(cudaMemcpyAsync(&dr, c->rep, sizeof(dr), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
-    if (dr.error) return fail(CVK_ETIMEOUT, "bicgstab: device grid barrier aborted");
-    rep->converged = dr.converged;
-    rep->breakdown = dr.breakdown;
-    rep->iterations = dr.iterations;
-    rep->final_relres = dr.final_relres;
-    rep->true_relres = dr.true_relres;
-    rep->history_len = o->record_history ? dr.history_len : 0;
-    rep->device_time_s = ms * 1e-3;
-    rep->kernel_launches = 1;
-    if (o->record_history && rep->history && rep->history_cap > 0) {
-        const long long k = std::min<long long>(std::min<long long>(rep->history_len, rep->history_cap), hcap);
-        if (k > 0) CK(cudaMemcpy(rep->history, c->hist, sizeof(double) * k, cudaMemcpyDeviceToHost));
-    }
-    return CVK_OK;
-}
-
-// Phase-kernel GMRES(m) (cvk_gmres.cu): slots of [x-update, SpMV, dots,
-// update+dots, update+norm+Givens] replayed from a CUDA graph.
 static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                               const double2* b_dev, double2* x_dev, cvk_report* rep) {
     const int n = (int)A->n;
@@ -1286,7 +1181,6 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.dots, cvk::kThreads, 0));
     const long long blocks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, blocks);
-    if (const char* env = std::getenv("CVK_GMRES_CTAS")) G = std::max(1, std::atoi(env));
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(m + 4) * std::max(1, n))) != CVK_OK) return e;
     // partials of the G-CTA kernels and of the one-CTA-per-SM streamed ones
@@ -1312,18 +1206,18 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     SL.ngather = 1;
     const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
     int nst = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)SL.stage_bytes()));
-    if (nst < 2 || A->nnz == 0 || std::getenv("CVK_NO_STREAM")) nst = 0;
+    if (nst < 2 || A->nnz == 0 || !c->knob.stream) nst = 0;
     SL.stages = std::max(1, nst);
     if (nst) CK(cudaFuncSetAttribute(K.spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // second CGS pass from shared-memory tiles (k_g_ud_s): needs 2 stages of
     // (m + 2) 128-row vectors
     int ud_smem = optin - 8192 - 4096;
-    const bool ud = nst && m <= 32 && (long long)ud_smem >= 2LL * (m + 2) * 128 * 16 + 256 && !std::getenv("CVK_GMRES_NO_TILES");
+    const bool ud = nst && m <= 32 && (long long)ud_smem >= 2LL * (m + 2) * 128 * 16 + 256;
     if (ud) CK(cudaFuncSetAttribute(K.upd1_s, cudaFuncAttributeMaxDynamicSharedMemorySize, ud_smem));
     void* uargs[2] = {nullptr, &ud_smem};
-    const int pf = std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows;
+    const int pf = 2 * cvk::kStreamRows;
     std::vector<unsigned char> blob(cvk::gmres_args_size());
-    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, nullptr}, M->dinv, b_dev, x_dev,
+    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
                          (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf);
     void* args[] = {blob.data()};
     uargs[0] = blob.data();
@@ -1408,7 +1302,6 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.step, cvk::kThreads, 0));
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, chunks);
-    if (const char* env = std::getenv("CVK_BICGL_CTAS")) G = std::max(1, std::atoi(env));
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(2 * L + 6) * std::max(1, n))) != CVK_OK)
         return e;
@@ -1512,43 +1405,29 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     }
     const int n = (int)A->n;
     const int mode = resolve_mode(c, o->mode);
-    const bool ref = mode == CVK_MODE_REF;
+    const bool ref = is_ref(mode);
     CK(cudaSetDevice(c->device));
-    // persistent streamed BiCGSTAB: opt-in (CVK_STREAMK=1).  Measured 218-293 vs
-    // 134-143 us per iteration for the phase kernels at 1M DOF: with ~200 KB
-    // of shared memory resident for the whole solve the L1 left for global
-    // loads is too small for the element phase's memory-level parallelism
-    // (40 vs 14 us), and the merged phases spill (tools/trace_streamk.py).
-    if (!ref && solver == CVK_BICGSTAB && (long long)n >= phased_min_n() && !c->warm_next &&
-        std::getenv("CVK_STREAMK") && std::atoi(std::getenv("CVK_STREAMK")) == 1 && !std::getenv("CVK_NO_STREAM")) {
-        const int rc = solve_streamk(c, A, M, o, b_dev, x_dev, rep);
-        if (rc != 1) return rc;
-    }
+    const long long pmin = c->knob.phased_min_n;
     // GMRES phase kernels from 32k rows (50k DOF: 58 vs 63 us per step; BiCGSTAB keeps the persistent kernel there)
-    if (!ref && solver == CVK_GMRES && (long long)n >= std::min(phased_min_n(), 32768LL) && !std::getenv("CVK_GMRES_PERSISTENT"))
+    if (!ref && solver == CVK_GMRES && (long long)n >= std::min(pmin, 32768LL) && !c->knob.gmres_persistent)
         return solve_gmres_phased(c, A, M, o, b_dev, x_dev, rep);
     // BiCGSTAB(l) step kernel from 131072 rows (1M DOF, l = 8: 2293 vs 2380 us
-    // per cycle on the cavity, 3007 vs 3085 on 3-D FEM; CVK_BICGL_PERSISTENT=1
-    // keeps the persistent kernel)
-    if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= phased_min_n() && !std::getenv("CVK_BICGL_PERSISTENT"))
+    // per cycle on the cavity, 3007 vs 3085 on 3-D FEM)
+    if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= pmin && !c->knob.bicgl_persistent)
         return solve_bicgl_phased(c, A, M, o, b_dev, x_dev, rep);
-    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= phased_min_n()) {
-        const bool pinned = l2_pin(c, A);
-        const int rc = solve_phased(c, solver, A, M, o, b_dev, x_dev, rep, pinned);
-        if (pinned) l2_unpin(c);
-        return rc;
-    }
+    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= pmin)
+        return solve_phased(c, solver, A, M, o, b_dev, x_dev, rep);
     const int S = ref ? 1 : A->group;
     const void* kern = cvk::solver_kernel(solver, S, ref);
     if (!kern) return fail(CVK_ELOGIC, "no kernel for this configuration");
     const size_t smem = cvk::solver_smem(solver, (int)o->m);
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 0) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cvk::kThreads, smem));
     if (per_sm < 1) return fail(CVK_ECUDA, "solver kernel does not fit on an SM");
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>((long long)per_sm * c->nsm, chunks);
-    if (const char* env = std::getenv("CVK_MAX_CTAS")) G = std::min<long long>(G, std::max(1, std::atoi(env)));
+    if (c->knob.max_ctas > 0) G = std::min<long long>(G, c->knob.max_ctas);
     const int nwork = cvk::solver_nwork(solver, (int)o->l, (int)o->m);
     CK(cudaSetDevice(c->device));
     int e;
@@ -1584,6 +1463,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     a.G = (int)G;
     a.cta_base = 0;
     a.warm = (solver == CVK_BICGSTAB && c->warm_next) ? 1 : 0;
+    a.refpar = mode == CVK_MODE_REF_PAR ? 1 : 0;
     void* args[] = {&a};
     CK(cudaEventRecord(c->e0, c->stream));
     CK(cudaLaunchCooperativeKernel(kern, dim3((unsigned)G), dim3(cvk::kThreads), args, smem, c->stream));
@@ -1660,9 +1540,9 @@ static int stage(cvk_ctx* c, size_t n2) {
 int cvk_spmv_device(const cvk_csr* A, const double* x_dev, double* y_dev, int mode) {
     if (!A) return fail(CVK_EINVAL, "spmv: null matrix");
     cvk_ctx* c = A->ctx;
-    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    const bool ref = is_ref(resolve_mode(c, mode));
     CK(cudaSetDevice(c->device));
-    if (!ref && A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && !std::getenv("CVK_NO_STREAM")) {
+    if (!ref && A->n >= 4 * cvk::kStreamRows && A->nnz > 0 && c->knob.stream) {
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
         const cudaError_t e = cvk::launch_spmv_stream((int)A->n, A->rp, A->ci, A->av, (const double2*)x_dev,
@@ -1712,7 +1592,7 @@ int cvk_spmv_bench(const cvk_csr* A, const double* x_dev, double* y_dev, int mod
 static int dot_impl(cvk_ctx* c, int64_t n, const double* x, const double* y, double* out, int mode) {
     if (!c || !x || !out || n < 0) return fail(CVK_EINVAL, "dot: bad argument");
     CK(cudaSetDevice(c->device));
-    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    const bool ref = is_ref(resolve_mode(c, mode));
     const size_t nn = (size_t)n;
     int e;
     if ((e = stage(c, 2 * nn + 2)) != CVK_OK) return e;
@@ -1800,7 +1680,7 @@ int cvk_true_relres(const cvk_csr* A, const double* b, const double* x, double* 
     double2* xd = c->bx + n;
     double2* rd = c->bx + 2 * n;
     double2* od = c->bx + 3 * n;
-    const bool ref = resolve_mode(c, mode) == CVK_MODE_REF;
+    const bool ref = is_ref(resolve_mode(c, mode));
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
     CK(cudaMemcpyAsync(bd, b, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(xd, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1822,10 +1702,10 @@ int cvk_true_relres(const cvk_csr* A, const double* b, const double* x, double* 
 extern "C" void* cvk_ddm_stream(cvk_ctx* c) { return c->stream; }
 
 extern "C" int cvk_ddm_ctas(cvk_ctx* c, int solver, int mode, size_t smem, int* total) {
-    const void* k = cvk::solver_kernel(solver, 1, mode == CVK_MODE_REF, true);
+    const void* k = cvk::solver_kernel(solver, 1, is_ref(mode), true);
     if (!k) return fail(CVK_ELOGIC, "no batched kernel");
     CK(cudaSetDevice(c->device));
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 0) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, cvk::kThreads, smem));
     *total = per_sm * c->nsm;
@@ -1834,7 +1714,7 @@ extern "C" int cvk_ddm_ctas(cvk_ctx* c, int solver, int mode, size_t smem, int* 
 
 extern "C" int cvk_ddm_launch_batched(cvk_ctx* c, int solver, int mode, const void* segs, int nseg,
                                       int total_ctas, size_t smem, float* ms) {
-    const void* k = cvk::solver_kernel(solver, 1, mode == CVK_MODE_REF, true);
+    const void* k = cvk::solver_kernel(solver, 1, is_ref(mode), true);
     void* args[] = {(void*)&segs, &nseg};
     CK(cudaLaunchCooperativeKernel(k, dim3((unsigned)total_ctas), dim3(cvk::kThreads), args, smem, c->stream));
     (void)ms;

@@ -34,8 +34,9 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Csr A, const double2* __restr
 // FAST standalone SpMV on the TMA ring (cvk_stream.cuh): x staged per chunk,
 // out-of-chunk columns gathered through L1/L2; per-row order as k_spmv.
 __global__ void __launch_bounds__(kStreamThreads, 1) k_spmv_s(Csr A, StreamLayout L, const double2* __restrict__ x,
-                                                              double2* __restrict__ y) {
+                                                              double2* __restrict__ y, const int* skip) {
     extern __shared__ __align__(128) unsigned char smem[];
+    if (skip && *(volatile const int*)skip) return;  // the solve already stopped (graph tail)
     const double2* vecs[1] = {x};
     stream_rows(A, L, vecs, smem, [&](int t, const Chunk& ch) {
         const double2 acc = chunk_row_sum<CVK_SPMV_BATCH>(ch, t, [&](int l) { return ch.v(0, l); },
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_spmv_s(Csr A, StreamLayou
 }
 
 cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
-                               double2* y, int capk, int nsm, int optin, cudaStream_t st) {
+                               double2* y, int capk, int nsm, int optin, cudaStream_t st, const int* skip) {
     StreamLayout L{capk, 1, 1};
     const long long avail = (long long)optin - 8192 - 2 * kStreamMaxStages * 8;
     L.stages = (int)std::min<long long>(kStreamMaxStages, avail / (long long)L.stage_bytes());
@@ -53,7 +54,7 @@ cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double
     const size_t smem = L.smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k_spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_spmv_s<<<nsm, kStreamThreads, smem, st>>>(Csr{n, rp, ci, av}, L, x, y);
+    k_spmv_s<<<nsm, kStreamThreads, smem, st>>>(Csr{n, rp, ci, av}, L, x, y, skip);
     return cudaGetLastError();
 }
 

@@ -359,7 +359,11 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
     DK(cudaMemcpyAsync(R->d_wlr, h_wlr.data(), sizeof(double2) * 2 * ns, cudaMemcpyHostToDevice, st));
 
     // local CSRs + Jacobi, one batched-solve segment per strip
-    R->mode = inner->mode == CVK_MODE_REF ? CVK_MODE_REF : CVK_MODE_FAST;
+    {
+        int m = inner->mode;
+        if (m < 0) m = cvk_get_exec_mode(ctx) ? CVK_MODE_REF_PAR : CVK_MODE_REF;
+        R->mode = (m == CVK_MODE_REF || m == CVK_MODE_REF_PAR) ? m : CVK_MODE_FAST;
+    }
     R->smem = solver_smem(inner_solver, (int)inner->m);
     int e = cvk_ddm_ctas(ctx, inner_solver, R->mode, R->smem, &R->total_ctas);
     if (e != CVK_OK) return e;
@@ -421,11 +425,12 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
         a.record = 0;
         a.G = gs[j];
         a.cta_base = cta_base;
+        a.refpar = R->mode == CVK_MODE_REF_PAR ? 1 : 0;
         cta_base += gs[j];
     }
     R->total_ctas = cta_base;
     R->off.assign(h_off.begin(), h_off.end());
-    R->warm = inner_solver == CVK_BICGSTAB && std::getenv("CVK_DDM_WARM") && std::atoi(std::getenv("CVK_DDM_WARM")) == 1;
+    R->warm = inner_solver == CVK_BICGSTAB && inner->warm != 0;
     for (int64_t j = 0; j < ns; ++j) segs[j].warm = R->warm ? 1 : 0;
     R->inner_opts = *inner;
     R->inner_opts.record_history = 0;
@@ -434,8 +439,7 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
         // a strip this large fills the device on its own: the batched launch
         // gives each strip ~1/ns of the SMs on the latency-bound persistent
         // kernel (5M DOF, 8 strips: ~490 us per inner iteration)
-        long long thr = 131072;
-        if (const char* env = std::getenv("CVK_DDM_SEQ_MIN")) thr = std::atoll(env);
+        const long long thr = cvk_ctx_knob(ctx, CVK_OPT_DDM_SEQ_MIN);
         int64_t nmin = INT64_MAX;
         for (const Strip& S : strips) nmin = std::min<int64_t>(nmin, S.n);
         R->seq = R->mode == CVK_MODE_FAST && nmin >= thr;

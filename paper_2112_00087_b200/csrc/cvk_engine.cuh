@@ -49,7 +49,6 @@ struct Csr {
     const int* __restrict__ ci;
     const double2* __restrict__ av;
     const int* cmax = nullptr;  // per streamed chunk: largest column index (L2 prefetch window), optional
-    const int4* bands = nullptr;  // per streamed chunk: halo bands {b0, w0, b1, w1} (cvk_stream.cuh), optional
 };
 
 // Kernel arguments (passed by value to cudaLaunchCooperativeKernel).
@@ -72,6 +71,7 @@ struct KArgs {
     int G;
     int cta_base;  // first CTA of this solve in a batched launch
     int warm;      // BiCGSTAB only: x holds x0 (r0 = M^-1 (b - A x0)); 0 = the reference's x0 = 0
+    int refpar;    // REF reductions with parallel term formation (CVK_MODE_REF_PAR)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -93,6 +93,7 @@ struct GridBar {
     unsigned G;
 
     int cta;  // CTA index within this grid (or within a batched segment)
+    int refpar = 0;  // REF reductions: CTA 0 sums with all its threads forming the terms
 
     __device__ GridBar(unsigned long long* b, int g, int cta_ = -1)
         : bar(b), target(0), G((unsigned)g), cta(cta_ < 0 ? (int)blockIdx.x : cta_) {}
@@ -397,11 +398,95 @@ __device__ __forceinline__ void seq_sums(double2 (&out)[K], int n, C&& contrib) 
     for (int k = 0; k < K; ++k) out[k] = res[k];
 }
 
+// REF_PAR: the same sequential sums, bit for bit, at the speed of the
+// dependent adds.  Warps 1..7 form the element terms contrib(i, 0) -- exactly
+// the reference's rounded products conj(x_i) y_i / std::norm(x_i) (0 + t == t,
+// and the sign of a zero term cannot change a sum that starts at +0) -- into
+// an NB-deep ring of shared-memory blocks; lane 0 of warp 0 adds them left to
+// right, loads of a batch of 8 issued before its adds.  Named barriers
+// 1..NB (full) and NB+1..2NB (empty) hand the blocks over.
+__device__ __forceinline__ void named_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
+
+constexpr int kRefParTerms = 2016;  // one shared-memory ring for every K (32 KB)
+__device__ __forceinline__ double2* refpar_ring() {
+    __shared__ double2 ring[kRefParTerms];
+    return ring;
+}
+
+template <int K, class C>
+__device__ __forceinline__ void seq_sums_par(double2* out, int n, C&& contrib) {
+    constexpr int P = kThreads - 32;  // producer threads
+    constexpr int NB = kRefParTerms / (K * P) < 4 ? kRefParTerms / (K * P) : 4;
+    static_assert(NB >= 2, "REF_PAR ring too small for K");
+    double2 (*buf)[K][P] = reinterpret_cast<double2 (*)[K][P]>(refpar_ring());
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (n + P - 1) / P;
+    if (warp == 0) {
+        double2 acc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+        for (int b = 0; b < nblk; ++b) {
+            const int s = b % NB;
+            named_sync(1 + s);
+            if (lane == 0) {
+                const int cnt = min(P, n - b * P);
+                for (int e0 = 0; e0 < cnt; e0 += 8) {
+                    double2 v[8][K];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+#pragma unroll
+                        for (int k = 0; k < K; ++k) v[u][k] = buf[s][k][min(e0 + u, P - 1)];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (e0 + u < cnt)
+#pragma unroll
+                            for (int k = 0; k < K; ++k) acc[k] = cvk_add(acc[k], v[u][k]);
+                }
+            }
+            __syncwarp();
+            named_arrive(1 + NB + s);
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < K; ++k) out[k] = acc[k];
+    } else {
+        const int t = threadIdx.x - 32;
+        for (int b = 0; b < nblk; ++b) {
+            const int s = b % NB;
+            if (b >= NB) named_sync(1 + NB + s);
+            double2 q[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) q[k] = make_double2(0.0, 0.0);
+            const int i = b * P + t;
+            if (i < n) contrib(i, q);
+#pragma unroll
+            for (int k = 0; k < K; ++k) buf[s][k][t] = q[k];
+            named_arrive(1 + s);
+        }
+        // match the consumer's releases of the last blocks
+        for (int b = max(nblk, NB); b < nblk + NB; ++b) named_sync(1 + NB + b % NB);
+    }
+    __syncthreads();
+}
+
 // One reduction phase end: partials/sequential sums + grid barrier.
 template <bool REF, int K, class C>
 __device__ __forceinline__ bool reduce(GridBar& g, const CAcc (&acc)[K], double2 (&out)[K],
                                        double2* part, int n, C&& contrib) {
-    if (REF) {
+    if (REF && g.refpar) {
+        // CTA 0 sums, publishes the K results in part[0..K); the second
+        // barrier also keeps fast CTAs from rewriting the vectors meanwhile
+        if (!g.sync()) return false;
+        if (g.cta == 0) seq_sums_par<K>(part, n, contrib);
+        if (!g.sync()) return false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] = __ldcg(part + k);
+    } else if (REF) {
         // thread 0 of every CTA re-reads whole vectors after the barrier; the
         // second barrier keeps fast CTAs from rewriting them meanwhile
         if (!g.sync()) return false;

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_g_spmv_s(GArgs a) {
     double2* vj = Vq(a, j);
     const double sc = st->scale;
     const double2* vecs[2] = {src, a.dinv};
-    StreamLayout L{a.capk, 2, a.nst, 0};
+    StreamLayout L{a.capk, 2, a.nst};
     L.ngather = 1;
     L.pf_rows = a.pf_rows;
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_g_spmv_s(GArgs a) {
         const int row = ch.r0 + t;
         vj[row] = xs(t);
         w[row] = a.dinv ? cvk_mul(ch.v(1, t), y) : y;
-    }, nullptr, nullptr, [&](int t, const Chunk& ch) { ch.set(0, t, cvk_divr(ch.v(0, t), sc)); });
+    }, nullptr, [&](int t, const Chunk& ch) { ch.set(0, t, cvk_divr(ch.v(0, t), sc)); });
 }
 
 // h = V^H w over q <= j (UPDATE: first w -= V h1 per row).  Basis vectors are

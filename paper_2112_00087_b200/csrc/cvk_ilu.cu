@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(kIluThreads) k_ilu_sweep(int n, const int* __r
                                                            const double2* __restrict__ xin,
                                                            const double2* __restrict__ xs,
                                                            const double2* __restrict__ os,
-                                                           double2* __restrict__ out) {
+                                                           double2* __restrict__ out, const int* skip) {
+    if (skip && *(volatile const int*)skip) return;  // the solve already stopped (graph tail)
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int p0 = __ldg(rp + i), p1 = __ldg(rp + i + 1);
@@ -55,7 +56,8 @@ __global__ void __launch_bounds__(kIluThreads) k_ilu_sweep(int n, const int* __r
 
 __global__ void __launch_bounds__(kIluThreads) k_ilu_scale(int n, const double2* __restrict__ d,
                                                            const double2* __restrict__ y,
-                                                           double2* __restrict__ z) {
+                                                           double2* __restrict__ z, const int* skip) {
+    if (skip && *(volatile const int*)skip) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) z[i] = cvk_mul(__ldg(d + i), __ldg(y + i));
 }
@@ -67,13 +69,13 @@ int ilu_grid(int n) { return (n + kIluThreads - 1) / kIluThreads; }
 // z = M^-1 r for the ILU(0) factor (see the header comment).  tmp holds 2 n
 // complex.  r and z must not alias.  Returns the number of launches in *nl.
 cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, double2* tmp, int* nl,
-                              cudaStream_t st) {
+                              cudaStream_t st, const int* skip) {
     const int n = M.n;
     if (n <= 0) return cudaSuccess;
     const int G = ilu_grid(n);
     int launches = 0;
     if (M.sweeps <= 0) {
-        k_ilu_scale<<<G, kIluThreads, 0, st>>>(n, M.dinv, r, z);
+        k_ilu_scale<<<G, kIluThreads, 0, st>>>(n, M.dinv, r, z, skip);
         if (nl) *nl += 1;
         return cudaGetLastError();
     }
@@ -82,7 +84,7 @@ cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, dou
     const double2* y = r;
     for (int k = 0; k < M.sweeps; ++k) {
         double2* o = buf[k & 1];
-        k_ilu_sweep<false, false><<<G, kIluThreads, 0, st>>>(n, M.lrp, M.lci, M.lav, r, y, nullptr, nullptr, o);
+        k_ilu_sweep<false, false><<<G, kIluThreads, 0, st>>>(n, M.lrp, M.lci, M.lav, r, y, nullptr, nullptr, o, skip);
         ++launches;
         y = o;
     }
@@ -94,9 +96,9 @@ cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, dou
     for (int k = 0; k < M.sweeps; ++k) {
         double2* o = zb[k & 1];
         if (k == 0)
-            k_ilu_sweep<true, true><<<G, kIluThreads, 0, st>>>(n, M.urp, M.uci, M.uav, y, zin, M.dinv, M.dinv, o);
+            k_ilu_sweep<true, true><<<G, kIluThreads, 0, st>>>(n, M.urp, M.uci, M.uav, y, zin, M.dinv, M.dinv, o, skip);
         else
-            k_ilu_sweep<false, true><<<G, kIluThreads, 0, st>>>(n, M.urp, M.uci, M.uav, y, zin, nullptr, M.dinv, o);
+            k_ilu_sweep<false, true><<<G, kIluThreads, 0, st>>>(n, M.urp, M.uci, M.uav, y, zin, nullptr, M.dinv, o, skip);
         ++launches;
         zin = o;
     }
@@ -138,24 +140,6 @@ __device__ void ic_rho(IcState* st, double2 rho_new) {
 template <int MODE>
 __device__ void ic_fold_tail(const IcArgs& a);
 
-// a.fused: the CTA that publishes its partial last folds them and runs the
-// scalar step (no separate 1-CTA k_ic_fold launch)
-template <int MODE>
-__device__ __forceinline__ void ic_finish(const IcArgs& a) {
-    if (!a.fused) return;
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&a.st->counter, 1u) == gridDim.x - 1u;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) a.st->counter = 0;
-    ic_fold_tail<MODE>(a);
-}
-
 // stage 1: MODE 0 init {|r|^2, <r, r>}, 1 <sh, v>, 2 {|t|^2, <t, s>}
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_ic_dot(IcArgs a) {
@@ -175,7 +159,6 @@ __global__ void __launch_bounds__(kThreads) k_ic_dot(IcArgs a) {
         }
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
-    ic_finish<MODE>(a);
 }
 
 // p = r (it == 1) or p = beta (p - omega v) + r  (axpy then xpay, krylov.cpp:77-80)
@@ -203,7 +186,6 @@ __global__ void __launch_bounds__(kThreads) k_ic_s(IcArgs a) {
         acc_norm(acc[0], si);
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
-    ic_finish<3>(a);
 }
 
 // x += omega s; r = s - omega t; partials |r|^2 and <sh, r>
@@ -221,7 +203,6 @@ __global__ void __launch_bounds__(kThreads) k_ic_xr(IcArgs a) {
         acc_dot(acc[1], __ldg(a.sh + i), ri);
     });
     cta_partial<2>(acc, a.part, gridDim.x, blockIdx.x);
-    ic_finish<4>(a);
 }
 
 // stage 2 + the scalar step.  MODE 0: bnorm and rho_1; 1: gamma -> alpha;
@@ -276,7 +257,7 @@ int ic_grid(int n) {
 
 cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st) {
     k_ic_dot<0><<<kIcBlocks, kThreads, 0, st>>>(a);
-    if (!a.fused) k_ic_fold<0><<<1, kThreads, 0, st>>>(a);
+    k_ic_fold<0><<<1, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -287,18 +268,18 @@ static cudaError_t ic_iter(const IcArgs& a, const IluDev& M, Spmv&& spmv, int* n
     const int G = ic_grid(a.n);
     k_ic_p<<<G, kThreads, 0, st>>>(a);
     if ((e = spmv(a.p)) != cudaSuccess) return e;
-    if ((e = launch_ilu0_apply(M, a.tmp, a.v, a.ptmp, nl, st)) != cudaSuccess) return e;
+    if ((e = launch_ilu0_apply(M, a.tmp, a.v, a.ptmp, nl, st, &a.st->done)) != cudaSuccess) return e;
     k_ic_dot<1><<<G, kThreads, 0, st>>>(a);
-    if (!a.fused) k_ic_fold<1><<<1, kThreads, 0, st>>>(a);
+    k_ic_fold<1><<<1, kThreads, 0, st>>>(a);
     k_ic_s<<<G, kThreads, 0, st>>>(a);
-    if (!a.fused) k_ic_fold<3><<<1, kThreads, 0, st>>>(a);
+    k_ic_fold<3><<<1, kThreads, 0, st>>>(a);
     if ((e = spmv(a.s)) != cudaSuccess) return e;
-    if ((e = launch_ilu0_apply(M, a.tmp, a.t, a.ptmp, nl, st)) != cudaSuccess) return e;
+    if ((e = launch_ilu0_apply(M, a.tmp, a.t, a.ptmp, nl, st, &a.st->done)) != cudaSuccess) return e;
     k_ic_dot<2><<<G, kThreads, 0, st>>>(a);
-    if (!a.fused) k_ic_fold<2><<<1, kThreads, 0, st>>>(a);
+    k_ic_fold<2><<<1, kThreads, 0, st>>>(a);
     k_ic_xr<<<G, kThreads, 0, st>>>(a);
-    if (!a.fused) k_ic_fold<4><<<1, kThreads, 0, st>>>(a);
-    *nl += a.fused ? 8 : 12;
+    k_ic_fold<4><<<1, kThreads, 0, st>>>(a);
+    *nl += 12;
     return cudaGetLastError();
 }
 

@@ -11,6 +11,9 @@
 
 // shared error channel of the C ABI (cvk_last_error); returns code
 int cvk_fail(int code, const std::string& msg);
+// a context's execution-path option (CVK_OPT_*, cvk_ctx_set_option)
+struct cvk_ctx;
+long long cvk_ctx_knob(cvk_ctx* c, int key);
 
 namespace cvk {
 
@@ -24,16 +27,6 @@ struct DevReport;
 const void* solver_kernel(int solver, int S, bool ref, bool batched = false);
 int solver_nwork(int solver, int l, int m);
 size_t solver_smem(int solver, int m);
-
-// persistent TMA-streamed BiCGSTAB (cvk_streamk.cu): cooperative, one CTA per
-// SM, kStreamThreads threads, dynamic smem = L.smem_bytes()
-struct StreamLayout;
-const void* streamk_bicgstab_kernel();
-int streamk_trace_read(unsigned long long* out16);  // CVK_TRACE builds
-size_t streamk_args_size();
-void streamk_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
-                       double2* part, unsigned long long* bar, DevReport* rep, double* hist, long long hist_cap,
-                       double tol, long long max_iter, int record, const StreamLayout& L);
 
 // phase-kernel GMRES(m) (cvk_gmres.cu), kThreads threads per CTA
 struct GmresKernels {
@@ -67,7 +60,7 @@ cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, co
                         const double2* x, double2* y, int tile, cudaStream_t st);
 // FAST SpMV on the TMA ring; cudaErrorInvalidConfiguration if a chunk does not fit
 cudaError_t launch_spmv_stream(int n, const int* rp, const int* ci, const double2* av, const double2* x,
-                               double2* y, int capk, int nsm, int optin, cudaStream_t st);
+                               double2* y, int capk, int nsm, int optin, cudaStream_t st, const int* skip = nullptr);
 // cavity operator values at omega on the cavity's 5-point pattern (cvk_assemble.cu);
 // *bad receives the first row whose pattern does not match (INT32_MAX if none)
 cudaError_t launch_cavity_values(int nx, int ny, int roof_begin, int roof_end, double k2, double om2,
@@ -95,8 +88,9 @@ struct IluDev {
     void* blob = nullptr;  // one allocation behind all of the above
 };
 // z = M^-1 r; tmp >= 2 n complex; r, z, tmp disjoint; *nl += launches
+// skip (optional, device): a stop flag; the launches return at once when it is set
 cudaError_t launch_ilu0_apply(const IluDev& M, const double2* r, double2* z, double2* tmp, int* nl,
-                              cudaStream_t st);
+                              cudaStream_t st, const int* skip = nullptr);
 
 // BiCGSTAB + ILU(0) phase chain (cvk_ilu.cu): device-resident scalars
 struct IcState {
@@ -113,7 +107,6 @@ struct IcArgs {
     double2* part;  // >= 4 * 592 double2
     IcState* st;
     double* hist;
-    int fused;  // 1: stage-1 kernels fold in their last CTA; 0: separate k_ic_fold launches
 };
 cudaError_t launch_ic_init(const IcArgs& a, cudaStream_t st);
 // `iters` iterations; spmv(ctx, in) computes A in -> a.tmp on st

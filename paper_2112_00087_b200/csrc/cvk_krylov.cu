@@ -944,6 +944,7 @@ __device__ __forceinline__ void run_body(const KArgs& a, GridBar& g) {
 template <int S, bool REF, int SOLVER>
 __global__ void __launch_bounds__(kThreads, kMinCtas) k_solve(KArgs a) {
     GridBar g(a.bar, a.G);
+    g.refpar = REF ? a.refpar : 0;
     run_body<S, REF, SOLVER>(a, g);
 }
 
@@ -961,6 +962,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) k_solve_batched(const KArg
     }
     __syncthreads();
     GridBar g(sa.bar, sa.G, (int)blockIdx.x - sa.cta_base);
+    g.refpar = REF ? sa.refpar : 0;
     run_body<S, REF, SOLVER>(sa, g);
 }
 

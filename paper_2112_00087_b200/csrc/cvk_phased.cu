@@ -46,11 +46,8 @@ struct PArgs {
     double* hist;
     DevReport* rep;
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
-    int nst[6];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_bm_a_s, k_bm_b_s
-    int contig;         // streamed chunk assignment (StreamLayout::contig)
-    int dyn;            // 1: dynamic chunk assignment (stream_rows, PState::chunk_ctr)
+    int nst[4];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s
     int pf_rows;        // StreamLayout::pf_rows (L2 prefetch of the forward gather band)
-    int nband;          // StreamLayout::nband (stage the halo bands of the gathered vectors)
 };
 
 // ------------------------------------------------------------ tracing --
@@ -595,10 +592,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
     double2* __restrict__ pn = cur ? V.p0 : V.p1;
     double2* __restrict__ vn = cur ? V.v0 : V.v1;
     const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
-    StreamLayout L{a.capk, 5, a.nst[0], a.contig};
+    StreamLayout L{a.capk, 5, a.nst[0]};
     L.ngather = 3;
     L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         // slot 0 of the chunk rows holds p_new (pre); band slots hold raw r, p, v
@@ -618,14 +614,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_a_s(PArgs a) {
         pn[row] = xs(t);
         vn[row] = vi;
         acc_dot(acc[0], ch.v(3, t), vi);
-    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1), PreIf<kPreHook>([&](int t, const Chunk& ch) {
+    }, SPROF(1), PreIf<kPreHook>([&](int t, const Chunk& ch) {
         if (!first)
             ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
     }));
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
     if (threadIdx.x != 0) return;
-    st->chunk_ctr[0] = 0u;
     if (cvk_abs(tot[0]) < st->brk) {
         st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
         return;
@@ -650,10 +645,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     double2* __restrict__ t_ = V.t;
     double2* __restrict__ x = a.x;
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
-    StreamLayout L{a.capk, 5, a.nst[1], a.contig};
+    StreamLayout L{a.capk, 5, a.nst[1]};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
     CAcc acc[3] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds s (pre)
@@ -670,13 +664,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
         acc_norm(acc[0], si);
         acc_dot(acc[1], ti, ti);
         acc_dot(acc[2], ti, si);
-    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
+    }, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
     }));
     double2 tot[3];
     if (!partial_last<3, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
     if (threadIdx.x != 0) return;
-    st->chunk_ctr[1] = 0u;
     const double relres = sqrt(tot[0].x) / st->bnorm;
     if (relres <= st->tol) {
         st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
@@ -705,10 +698,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ vv = V.v;
     const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
-    StreamLayout L{a.capk, 7, a.nst[2], a.contig};
+    StreamLayout L{a.capk, 7, a.nst[2]};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
     CAcc acc[2] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds u - alpha v (pre)
@@ -728,13 +720,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
         V.d[row] = cvk_add(cvk_mul(coef, di), ui);
         acc_norm(acc[0], wi);
         acc_dot(acc[1], ch.v(6, t), wi);
-    }, a.dyn ? &st->chunk_ctr[2] : nullptr, SPROF(3), [&](int t, const Chunk& ch) {
+    }, SPROF(3), [&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
     });
     double2 tot[2];
     if (!partial_last<2, kStreamThreads>(acc, partv(a, 0), &st->counter[0], tot)) return;
     if (threadIdx.x != 0) return;
-    st->chunk_ctr[2] = 0u;
     st->cur ^= 1;
     st->theta = sqrt(tot[0].x) / st->tau;
     const double c = 1.0 / sqrt(1.0 + st->theta * st->theta);
@@ -765,10 +756,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     double2* __restrict__ un = st->cur ? V.u0 : V.u1;
     const double2* __restrict__ w = V.w;
     const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
-    StreamLayout L{a.capk, 8, a.nst[3], a.contig};
+    StreamLayout L{a.capk, 8, a.nst[3]};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
     CAcc acc[1] = {};
     stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
         auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds w + beta u (pre)
@@ -786,205 +776,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
         V.au[row] = an;
         a.x[row] = cvk_add(ch.v(5, t), cvk_mul(eta_o, ch.v(6, t)));
         acc_dot(acc[0], ch.v(7, t), vi);
-    }, a.dyn ? &st->chunk_ctr[3] : nullptr, SPROF(3), [&](int t, const Chunk& ch) {
+    }, SPROF(3), [&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(beta, ch.v(1, t))));
     });
     double2 tot[1];
     if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
     if (threadIdx.x != 0) return;
-    st->chunk_ctr[3] = 0u;
     st->pending_x = 0;
     st->cur ^= 1;
     st->it++;
     tf_even_head(st, tot[0]);
-}
-
-// ------------------------------------ BiCGSTAB in two streamed kernels ----
-// The update x += omega s, r = s - omega t (krylov.cpp:124-127) is folded
-// into the next iteration's SpMV phase, which forms r on the fly from s and
-// t exactly as the 3-kernel path does.  That needs rho_new = <shadow, r>
-// before the phase starts: it is taken from B's reductions as
-// <shadow, s> - omega <shadow, t> (two more dots in B), the only arithmetic
-// that differs from the 3-kernel path.  ||r|| (the convergence test) is still
-// summed from the formed r, one phase later, with the reference's check order
-// (relres, then max_iter, then rho breakdown, krylov.cpp:81-87,128-132).
-// Per iteration: 40 nnz + 328 n bytes in 2 launches (vs 344 n in 3).
-
-__global__ void __launch_bounds__(kThreads) k_bm_init(PArgs a) {
-    pdl_enter();
-    const int n = a.A.n;
-    BiVecs V(a.work, (size_t)n);
-    CAcc acc[2] = {};
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        const double2 ri = prec_apply(a.dinv, i, __ldg(a.b + i));
-        V.s[i] = ri;  // r0 lives in s with t = 0: r = s - omega t is then r0 exactly
-        V.t[i] = make_double2(0.0, 0.0);
-        V.sh[i] = ri;
-        a.x[i] = make_double2(0.0, 0.0);
-        acc_norm(acc[0], ri);
-        acc_dot(acc[1], ri, ri);
-    });
-    double2 tot[2];
-    if (!partial_last<2>(acc, partv(a, 0), &a.st->counter[0], tot)) return;
-    if (threadIdx.x != 0) return;
-    PState* st = a.st;
-    st->bnorm = sqrt(tot[0].x);
-    if (st->bnorm == 0.0) {  // krylov.cpp:70-74
-        st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1;
-        return;
-    }
-    st->brk = 1e-30 * st->bnorm * st->bnorm;
-    st->rho_new = tot[1];
-    st->rho = st->alpha = st->omega = make_double2(1.0, 0.0);
-    st->it = 1;
-    st->first = 1;
-    st->cur = 0;
-    bi_top(st);
-}
-
-// r = s - omega t, x += omega s (previous iteration), p = r + beta (p - omega v),
-// v = M^-1 A p; ||r||^2, <shadow, v>
-__global__ void __launch_bounds__(kStreamThreads, 1) k_bm_a_s(PArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    pdl_enter();
-    PState* st = a.st;
-    if (st->done) return;
-    TR(1, st->it, 0);
-    const int n = a.A.n;
-    BiVecs V(a.work, (size_t)n);
-    const int cur = st->cur;
-    const bool first = st->first != 0;
-    const double2 beta = st->beta, omega = st->omega, nom = cvk_neg(st->omega);
-    const double2* __restrict__ sv = V.s;
-    const double2* __restrict__ tv = V.t;
-    const double2* __restrict__ pc = cur ? V.p1 : V.p0;
-    const double2* __restrict__ vc = cur ? V.v1 : V.v0;
-    double2* __restrict__ pn = cur ? V.p0 : V.p1;
-    double2* __restrict__ vn = cur ? V.v0 : V.v1;
-    double2* __restrict__ r = V.r;
-    double2* __restrict__ x = a.x;
-    const double2* vecs[7] = {sv, tv, pc, vc, V.sh, a.dinv, x};
-    StreamLayout L{a.capk, 7, a.nst[4], a.contig};
-    L.ngather = 4;
-    L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
-    auto rval = [&](double2 s_, double2 t_) { return first ? s_ : cvk_add(s_, cvk_mul(nom, t_)); };
-    auto pval = [&](double2 r_, double2 p_, double2 v_) {
-        return first ? r_ : cvk_add(cvk_mul(beta, cvk_add(p_, cvk_mul(nom, v_))), r_);
-    };
-    CAcc acc[2] = {};
-    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        // slots after pre: 0 p_new, 1 r, 6 x_new (chunk rows); band slots raw
-        auto xs = [&](int l) -> double2 {
-            if (l < kStreamRows) return ch.v(0, l);
-            return pval(rval(ch.v(0, l), ch.v(1, l)), ch.v(2, l), ch.v(3, l));
-        };
-        auto xg = [&](int c) -> double2 { return pval(rval(sv[c], tv[c]), pc[c], vc[c]); };
-        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
-        const double2 vi = prec_staged(a, ch, 5, t, y);
-        const int row = ch.r0 + t;
-        const double2 ri = ch.v(1, t);
-        r[row] = ri;
-        if (!first) x[row] = ch.v(6, t);
-        pn[row] = ch.v(0, t);
-        vn[row] = vi;
-        acc_norm(acc[0], ri);
-        acc_dot(acc[1], ch.v(4, t), vi);
-    }, a.dyn ? &st->chunk_ctr[0] : nullptr, SPROF(1), [&](int t, const Chunk& ch) {
-        const double2 s_ = ch.v(0, t), t_ = ch.v(1, t);
-        const double2 ri = rval(s_, t_);
-        if (!first) ch.set(6, t, cvk_add(ch.v(6, t), cvk_mul(omega, s_)));
-        ch.set(1, t, ri);
-        ch.set(0, t, pval(ri, ch.v(2, t), ch.v(3, t)));
-    });
-    double2 tot[2];
-    if (!partial_last<2, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot, 1, st->it)) return;
-    if (threadIdx.x != 0) return;
-    st->chunk_ctr[0] = 0u;
-    if (!first) {
-        // end of iteration it-1 (krylov.cpp:128-132) ...
-        const double relres = sqrt(tot[0].x) / st->bnorm;
-        st->final_relres = relres;
-        st->iters = st->it - 1;
-        st_hist(a, st, relres);
-        if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
-        // ... and the top of iteration it (krylov.cpp:81-87); beta, rho were set by B
-        if (st->it > st->max_iter) { st->done = 1; return; }
-        if (cvk_abs(st->rho) < st->brk) { st->done = 1; st->brk_code = 1; st->iters = st->it - 1; return; }
-    }
-    if (cvk_abs(tot[1]) < st->brk) {
-        st->done = 1; st->brk_code = 2; st->iters = st->it - 1;
-        return;
-    }
-    st->alpha = cvk_cdiv(st->rho, tot[1]);
-}
-
-// s = r - alpha v, t = M^-1 A s, x += alpha p; ||s||^2, <t,t>, <t,s>, <shadow,s>, <shadow,t>
-__global__ void __launch_bounds__(kStreamThreads, 1) k_bm_b_s(PArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    pdl_enter();
-    PState* st = a.st;
-    if (st->done) return;
-    TR(2, st->it, 0);
-    const int n = a.A.n;
-    BiVecs V(a.work, (size_t)n);
-    const int cur = st->cur;
-    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
-    const double2* __restrict__ r = V.r;
-    const double2* __restrict__ pn = cur ? V.p0 : V.p1;
-    const double2* __restrict__ vn = cur ? V.v0 : V.v1;
-    double2* __restrict__ s = V.s;
-    double2* __restrict__ t_ = V.t;
-    double2* __restrict__ x = a.x;
-    const double2* vecs[6] = {r, vn, a.dinv, pn, x, V.sh};
-    StreamLayout L{a.capk, 6, a.nst[5], a.contig};
-    L.ngather = 2;
-    L.pf_rows = a.pf_rows;
-    L.nband = a.nband;
-    CAcc acc[5] = {};
-    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
-        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds s (pre)
-            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
-        };
-        auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
-        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
-        const double2 ti = prec_staged(a, ch, 2, t, y);
-        const double2 si = xs(t);
-        const double2 shi = ch.v(5, t);
-        const int row = ch.r0 + t;
-        s[row] = si;
-        t_[row] = ti;
-        x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
-        acc_norm(acc[0], si);
-        acc_dot(acc[1], ti, ti);
-        acc_dot(acc[2], ti, si);
-        acc_dot(acc[3], shi, si);
-        acc_dot(acc[4], shi, ti);
-    }, a.dyn ? &st->chunk_ctr[1] : nullptr, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
-        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
-    }));
-    double2 tot[5];
-    if (!partial_last<5, kStreamThreads>(acc, partv(a, 2), &st->counter[2], tot, 2, st->it)) return;
-    if (threadIdx.x != 0) return;
-    st->chunk_ctr[1] = 0u;
-    const double relres = sqrt(tot[0].x) / st->bnorm;
-    if (relres <= st->tol) {  // half-step exit (krylov.cpp:107-114)
-        st->done = 1; st->conv = 1; st->iters = st->it; st->final_relres = relres;
-        st_hist(a, st, relres);
-        return;
-    }
-    if (cvk_abs(tot[1]) < st->brk) {
-        st->done = 1; st->brk_code = 3; st->iters = st->it;
-        return;
-    }
-    st->omega = cvk_cdiv(tot[2], tot[1]);
-    // next iteration's scalars (its checks run in k_bm_a_s)
-    st->rho_new = cvk_sub(tot[3], cvk_mul(st->omega, tot[4]));
-    st->it++;
-    st->first = 0;
-    st->cur ^= 1;
-    st->beta = cvk_mul(cvk_cdiv(st->rho_new, st->rho), cvk_cdiv(st->alpha, st->omega));
-    st->rho = st->rho_new;
 }
 
 // ------------------------------------------------- true residual + report
@@ -1041,9 +842,6 @@ PhasedKernels kernels_all() {
     k.bi_b_s = (const void*)k_bi_b_s;
     k.tf_e_s = (const void*)k_tf_e_s;
     k.tf_o_s = (const void*)k_tf_o_s;
-    k.bm_init = (const void*)k_bm_init;
-    k.bm_a_s = (const void*)k_bm_a_s;
-    k.bm_b_s = (const void*)k_bm_b_s;
     return k;
 }
 
@@ -1089,23 +887,19 @@ void flavor_kernels(void* out) {
     memcpy(out, &k, sizeof(k));
 }
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
-                      const int4* bands, const double2* dinv, const double2* b, double2* x, double2* work,
-                      double2* part, void* st, double* hist, void* rep, int capk, const int* nst, int contig,
-                      int dyn, int pf_rows, int nband) {
-    phased_pack_args(out, Csr{n, rp, ci, av, cmax, bands}, dinv, b, x, work, part, (PState*)st, hist,
-                     (DevReport*)rep, capk, nst, contig, dyn, pf_rows, nband);
+                      const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows) {
+    phased_pack_args(out, Csr{n, rp, ci, av, cmax}, dinv, b, x, work, part, (PState*)st, hist, (DevReport*)rep,
+                     capk, nst, pf_rows);
 }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, const int* nst, int contig, int dyn, int pf_rows, int nband) {
+                      int capk, const int* nst, int pf_rows) {
     PArgs* p = (PArgs*)out;
-    p->nband = nband;
     p->pf_rows = pf_rows;
-    p->contig = contig;
-    p->dyn = dyn;
     p->capk = capk;
-    for (int i = 0; i < 6; ++i) p->nst[i] = nst[i];
+    for (int i = 0; i < 4; ++i) p->nst[i] = nst[i];
     p->A = A;
     p->dinv = dinv;
     p->b = b;

@@ -20,7 +20,6 @@ struct PState {
     int done, conv, brk_code, first, pending_x, cur, record, skip_true;
     int warm;  // BiCGSTAB: start from the x passed in (k_bi_init)
     unsigned counter[4];
-    unsigned chunk_ctr[4];  // dynamic chunk counters of the streamed kernels (reset by their last CTA)
 };
 
 struct PhasedKernels {
@@ -29,8 +28,6 @@ struct PhasedKernels {
     const void* true_res;  // (PArgs, double2* scratch)
     // streamed SpMV phases (cvk_stream.cuh): kStreamThreads threads, dynamic smem
     const void *bi_a_s, *bi_b_s, *tf_e_s, *tf_o_s;
-    // BiCGSTAB in two streamed kernels per iteration (x/r update merged into A)
-    const void *bm_init, *bm_a_s, *bm_b_s;
 };
 
 PhasedKernels phased_kernels();
@@ -39,6 +36,6 @@ int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, const int* nst, int contig, int dyn, int pf_rows, int nband);
+                      int capk, const int* nst, int pf_rows);
 
 }  // namespace cvk

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_rb_a_s(RBArgs a) {
     double2* __restrict__ pn = vec(a, cur ? VP0 : VP1);
     double2* __restrict__ vn = vec(a, cur ? VV0 : VV1);
     const double2* vecs[5] = {r, pc, vc, vec(a, VSH), a.dinv};
-    StreamLayout L{a.capk, 5, a.nst[0], 0};
+    StreamLayout L{a.capk, 5, a.nst[0]};
     L.ngather = 3;
     L.pf_rows = a.pf_rows;
     CAcc acc[1] = {};
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_rb_a_s(RBArgs a) {
         pn[row] = xs(t);
         vn[row] = vi;
         acc_dot(acc[0], ch.v(3, t), vi);
-    }, nullptr, nullptr, [&](int t, const Chunk& ch) {
+    }, nullptr, [&](int t, const Chunk& ch) {
         if (!first)
             ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
     });
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_rb_b_s(RBArgs a) {
     double2* __restrict__ t_ = vec(a, VT);
     double2* __restrict__ x = vec(a, VX);
     const double2* vecs[5] = {r, vn, a.dinv, pn, x};
-    StreamLayout L{a.capk, 5, a.nst[1], 0};
+    StreamLayout L{a.capk, 5, a.nst[1]};
     L.ngather = 2;
     L.pf_rows = a.pf_rows;
     CAcc acc[3] = {};
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_rb_b_s(RBArgs a) {
         acc_norm(acc[0], si);
         acc_dot(acc[1], ti, ti);
         acc_dot(acc[2], ti, si);
-    }, nullptr, nullptr, [&](int t, const Chunk& ch) {
+    }, nullptr, [&](int t, const Chunk& ch) {
         ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
     });
     rank_total<3, kStreamThreads>(acc, a, &st->counter[2]);
@@ -765,9 +765,8 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
         nst[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)L1.stage_bytes()));
     }
-    long long smin = 65536;
-    if (const char* env = std::getenv("CVK_RB_STREAM_MIN")) smin = std::atoll(env);
-    R->streamed = d->nnz > 0 && d->n_own >= smin && std::min(nst[0], nst[1]) >= 2 && !std::getenv("CVK_NO_STREAM");
+    const long long smin = cvk_ctx_knob(ctx, CVK_OPT_RB_STREAM_MIN);
+    R->streamed = d->nnz > 0 && d->n_own >= smin && std::min(nst[0], nst[1]) >= 2 && cvk_ctx_knob(ctx, CVK_OPT_STREAM);
     if (R->streamed) {
         for (int k = 0; k < 2; ++k) {
             cvk::StreamLayout L{capk, kv[k], nst[k]};
@@ -842,7 +841,7 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
     a.capk = capk;
     a.nst[0] = nst[0];
     a.nst[1] = nst[1];
-    a.pf_rows = std::getenv("CVK_STREAM_PF") ? std::atoi(std::getenv("CVK_STREAM_PF")) : 2 * cvk::kStreamRows;
+    a.pf_rows = 2 * cvk::kStreamRows;
     a.nv = R->nv;
     a.dinv = d_dinv;
     a.b = d_b;

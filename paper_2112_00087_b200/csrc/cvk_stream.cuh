@@ -88,19 +88,13 @@ struct StreamLayout {
     int capk;    // nnz capacity of a chunk (multiple of 4)
     int nvec;    // staged row-local vectors
     int stages;  // ring depth
-    int contig = 0;  // 1: each CTA takes a contiguous block of chunks; 0: grid-stride
     int ngather = 0;  // vecs[0..ngather) are also gathered at neighbour columns
     int pf_rows = 0;  // L2-prefetch window (rows) below the chunk's largest column, 0 = off
-    int nband = 0;    // 1: stage the chunk's halo bands of the gathered vectors (A.bands)
     __host__ __device__ size_t rp_bytes() const { return (size_t)(kStreamRows + 4) * 4; }
     __host__ __device__ size_t ci_bytes() const { return (size_t)(capk + 8) * 4; }
     __host__ __device__ size_t av_bytes() const { return (size_t)capk * 16; }
     __host__ __device__ size_t vec_bytes() const { return (size_t)kStreamRows * 16; }
-    // gathered vectors get 3 R slots when banded: [chunk rows | band 0 | band 1]
-    __host__ __device__ int gslots() const { return nband ? 3 : 1; }
-    __host__ __device__ size_t stage_bytes() const {
-        return rp_bytes() + ci_bytes() + av_bytes() + (size_t)(nvec + (gslots() - 1) * ngather) * vec_bytes();
-    }
+    __host__ __device__ size_t stage_bytes() const { return rp_bytes() + ci_bytes() + av_bytes() + (size_t)nvec * vec_bytes(); }
     // stages, then full / empty barriers, then the per-stage header (8 ints)
     __host__ __device__ size_t smem_bytes() const {
         return (size_t)stages * stage_bytes() + 2 * kStreamMaxStages * 8 + kStreamMaxStages * 32;
@@ -112,31 +106,22 @@ struct Chunk {
     const int* rp;      // global row offsets of rows r0 .. r0+rows
     const int* ci;      // columns, index k - k0 + cio
     const double2* av;  // values, index k - k0
-    const double2* vec; // staged vectors (voff)
+    const double2* vec; // staged vectors, R rows each
     int k0, cio, r0, rows;
-    int ng, gs;         // gathered vectors, their slot count (1, or 3 when banded)
-    int b0, w0, b1, w1; // halo bands [b, b + w) (w = 0: none)
-    __device__ __forceinline__ int voff(int j) const {
-        return (j < ng ? j * gs : ng * gs + (j - ng)) * kStreamRows;
-    }
-    __device__ __forceinline__ double2 v(int j, int l) const { return vec[voff(j) + l]; }
-    __device__ __forceinline__ void set(int j, int l, double2 x) const { const_cast<double2*>(vec)[voff(j) + l] = x; }
-    // slot of column c in a gathered vector's staged data, or -1 (global)
+    __device__ __forceinline__ double2 v(int j, int l) const { return vec[j * kStreamRows + l]; }
+    __device__ __forceinline__ void set(int j, int l, double2 x) const { const_cast<double2*>(vec)[j * kStreamRows + l] = x; }
+    // slot of column c in the chunk's staged rows, or -1 (global gather)
     __device__ __forceinline__ int stage_index(int c) const {
         const int l = c - r0;
-        if ((unsigned)l < (unsigned)rows) return l;
-        const int l0 = c - b0, l1 = c - b1;
-        if ((unsigned)l0 < (unsigned)w0) return kStreamRows + l0;
-        if ((unsigned)l1 < (unsigned)w1) return 2 * kStreamRows + l1;
-        return -1;
+        return (unsigned)l < (unsigned)rows ? l : -1;
     }
 };
 
 // Row sum for row t of the chunk: y = sum_k A[k] * x(col_k), left to right,
 // with x read through xs(l) for columns staged in shared memory (the chunk's
-// rows and its halo bands; l = Chunk::stage_index) and xg(c) otherwise.  The
-// (value, column) pairs of a batch come from shared memory; the global
-// gathers of a batch are all issued before the first product.
+// own rows; l = Chunk::stage_index) and xg(c) otherwise.  The (value, column)
+// pairs of a batch come from shared memory; the global gathers of a batch are
+// all issued before the first product.
 template <int BATCH, class XS, class XG>
 __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs, XG&& xg) {
     const int b = ch.rp[t] - ch.k0, e = ch.rp[t + 1] - ch.k0;
@@ -166,22 +151,11 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
 // The producer/consumer ring.  `vecs` lists the row-local vectors to stage
 // (nullptr entries are skipped but keep their slot).  body(t, chunk) runs for
 // every row t < rows of every chunk in consumer threads.  Must be called by
-// all kStreamThreads threads of the CTA; returns when the CTA's chunks are done.
-//
-// Chunk assignment: with dyn == nullptr, static (grid-stride, or contiguous
-// blocks with L.contig).  With dyn pointing at a zeroed global counter,
-// dynamic: the producer takes kDynBatch chunks at a time with one atomicAdd,
-// so slower SMs simply stream fewer chunks (the static grid-stride split left
-// the p90 CTA of the BiCGSTAB s/t phase 25% behind the median,
-// profiles/r01_phase_timeline.txt).  The chunk index travels to the consumers
-// in a per-stage header; -1 ends a consumer group.  FAST reductions are
-// double-double, so the run-to-run varying chunk-to-CTA map does not change
-// any result bit.  The caller resets *dyn after the kernel (last CTA).
-constexpr int kDynBatch = 2;
-
+// all kStreamThreads threads of the CTA; returns when the CTA's chunks are
+// done.  Chunks are assigned grid-stride (chunk = cta + i * G).
 __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L, const double2* const* vecs,
                                              unsigned char* sp, uint64_t* bar, int chunk, int k0, int k1,
-                                             int cmax, int4 band) {
+                                             int cmax) {
     const int n = A.n;
     const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
     const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
@@ -189,11 +163,9 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
     const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
     const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
     const uint32_t b_v = (uint32_t)(rows * 16);
-    const bool banded = L.nband != 0;
-    const uint32_t b_h0 = banded ? (uint32_t)(band.y * 16) : 0u, b_h1 = banded ? (uint32_t)(band.w * 16) : 0u;
     uint32_t tx = b_rp + b_ci + b_av;
     for (int j2 = 0; j2 < L.nvec; ++j2)
-        if (vecs[j2]) tx += b_v + (j2 < L.ngather ? b_h0 + b_h1 : 0u);
+        if (vecs[j2]) tx += b_v;
     mbar_expect_tx(bar, tx);
     bulk_g2s(sp, A.rp + r0, b_rp, bar);
     unsigned char* q = sp + L.rp_bytes();
@@ -202,14 +174,8 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
     if (b_av) bulk_g2s(q, A.av + k0, b_av, bar);
     q += L.av_bytes();
     for (int j2 = 0; j2 < L.nvec; ++j2) {
-        if (vecs[j2]) {
-            bulk_g2s(q, vecs[j2] + r0, b_v, bar);
-            if (j2 < L.ngather && banded) {
-                if (b_h0) bulk_g2s(q + L.vec_bytes(), vecs[j2] + band.x, b_h0, bar);
-                if (b_h1) bulk_g2s(q + 2 * L.vec_bytes(), vecs[j2] + band.z, b_h1, bar);
-            }
-        }
-        q += (j2 < L.ngather ? L.gslots() : 1) * L.vec_bytes();
+        if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, bar);
+        q += L.vec_bytes();
     }
     // forward band of the gathered vectors (e.g. the +nx neighbours of the
     // cavity grid): not yet streamed by any CTA, so the consumers' gathers
@@ -234,149 +200,67 @@ struct NoPre {
 // between): a phase computes each row's gathered combination once -- e.g.
 // p = r + beta (p - omega v) -- into the staged slot of vector 0, so the
 // in-chunk gathers read one value instead of recomputing it per entry.
-// Persistent use (one ring across many phases of one kernel): call
-// stream_init once, then stream_rows with init = false and base = the ring
-// position where this phase starts (phases so far x chunks per CTA); static
-// chunk assignment only.
-__device__ __forceinline__ void stream_init(unsigned char* smem, const StreamLayout& L) {
+template <class Body, class Pre = NoPre>
+__device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L, const double2* const* vecs,
+                                            unsigned char* smem, Body&& body, unsigned long long* prof = nullptr,
+                                            Pre&& pre = Pre()) {
+    constexpr bool kPre = !std::is_same<typename std::decay<Pre>::type, NoPre>::value;
+    unsigned long long pw = 0, cw = 0, cb = 0, cn = 0;
     uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
     uint64_t* empty = full + kStreamMaxStages;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < L.stages; ++s) {
+    const int n = A.n;
+    const int nchunks = (n + kStreamRows - 1) / kStreamRows;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x;
+    const int ST = L.stages;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, kStreamRows);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-}
-
-// chunks per CTA under the static split
-__device__ __forceinline__ int stream_chunks_per_cta(int n, const StreamLayout& L) {
-    const int nchunks = (n + kStreamRows - 1) / kStreamRows, G = gridDim.x;
-    const int cpc = (nchunks + G - 1) / G;
-    if (L.contig) return max(0, min(nchunks, (int)blockIdx.x * cpc + cpc) - (int)blockIdx.x * cpc);
-    return (int)blockIdx.x < nchunks ? (nchunks - 1 - (int)blockIdx.x) / G + 1 : 0;
-}
-
-template <class Body, class Pre = NoPre>
-__device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L, const double2* const* vecs,
-                                            unsigned char* smem, Body&& body, unsigned* dyn = nullptr,
-                                            unsigned long long* prof = nullptr, Pre&& pre = Pre(), int base = 0,
-                                            bool init = true) {
-    constexpr bool kPre = !std::is_same<typename std::decay<Pre>::type, NoPre>::value;
-    unsigned long long pw = 0, cw = 0, cb = 0, cn = 0;
-    uint64_t* full = (uint64_t*)(smem + (size_t)L.stages * L.stage_bytes());
-    uint64_t* empty = full + kStreamMaxStages;
-    int* hdr = (int*)(empty + kStreamMaxStages);
-    const int n = A.n;
-    const int nchunks = (n + kStreamRows - 1) / kStreamRows;
-    const int G = gridDim.x;
-    const int tid = threadIdx.x;
-    const int ST = L.stages;
-    if (init) stream_init(smem, L);
-    // static split: this CTA's chunks first + i * step, i < cnt
-    const int cpc = (nchunks + G - 1) / G;
-    const int first = L.contig ? blockIdx.x * cpc : blockIdx.x;
-    const int cnt = L.contig ? max(0, min(nchunks, first + cpc) - first)
-                             : (blockIdx.x < nchunks ? (nchunks - 1 - blockIdx.x) / G + 1 : 0);
-    const int step = L.contig ? 1 : G;
+    const int first = blockIdx.x;
+    const int cnt = first < nchunks ? (nchunks - 1 - first) / G + 1 : 0;
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
-        int it = base;
-        const bool banded = L.nband != 0 && A.bands != nullptr;
-        auto put = [&](int chunk, int k0, int k1, int cm, int4 band) {  // lane 0
-            const int s = it % ST;
-            const long long t0 = prof ? clock64() : 0;
-            mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
-            if (prof) pw += clock64() - t0;
-            hdr[8 * s] = chunk;
-            hdr[8 * s + 1] = band.x;
-            hdr[8 * s + 2] = band.y;
-            hdr[8 * s + 3] = band.z;
-            hdr[8 * s + 4] = band.w;
-            stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, chunk, k0, k1, cm, band);
-            ++it;
-        };
         const bool pf = L.pf_rows > 0 && A.cmax != nullptr;
-        if (dyn) {
-            int base = 0;
-            if (lane == 0) base = (int)atomicAdd(dyn, (unsigned)kDynBatch);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            while (base < nchunks) {
-                int k0j = 0, k1j = 0, cmj = -1;
-                int4 bj = make_int4(0, 0, 0, 0);
-                if (lane < kDynBatch && base + lane < nchunks) {
-                    const int cj = base + lane;
-                    k0j = __ldg(A.rp + cj * kStreamRows);
-                    k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
-                    if (pf) cmj = __ldg(A.cmax + cj);
-                    if (banded) bj = __ldg(A.bands + cj);
-                }
-                int nb = 0;
-                if (lane == 0) nb = (int)atomicAdd(dyn, (unsigned)kDynBatch);  // next batch, in flight
-#pragma unroll
-                for (int j = 0; j < kDynBatch; ++j) {
-                    const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
-                    const int cm = __shfl_sync(0xffffffffu, cmj, j);
-                    const int4 bd = make_int4(__shfl_sync(0xffffffffu, bj.x, j), __shfl_sync(0xffffffffu, bj.y, j),
-                                              __shfl_sync(0xffffffffu, bj.z, j), __shfl_sync(0xffffffffu, bj.w, j));
-                    if (lane == 0 && base + j < nchunks) put(base + j, k0, k1, cm, bd);
-                }
-                base = __shfl_sync(0xffffffffu, nb, 0);
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int cj = first + (i0 + lane) * G;
+            int k0j = 0, k1j = 0, cmj = -1;
+            if (i0 + lane < cnt) {
+                k0j = __ldg(A.rp + cj * kStreamRows);
+                k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
+                if (pf) cmj = __ldg(A.cmax + cj);
             }
-            if (lane == 0) {
-                for (int g = 0; g < kStreamGroups; ++g) {  // one end marker per consumer group
-                    const int s = it % ST;
+            for (int j = 0; j < 32; ++j) {
+                if (i0 + j >= cnt) break;
+                const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
+                const int cm = __shfl_sync(0xffffffffu, cmj, j);
+                if (lane == 0) {
+                    const int it = i0 + j, s = it % ST;
+                    const long long t0 = prof ? clock64() : 0;
                     mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
-                    hdr[8 * s] = -1;
-                    mbar_arrive(full + s);
-                    ++it;
-                }
-            }
-        } else {
-            for (int i0 = 0; i0 < cnt; i0 += 32) {
-                const int cj = first + (i0 + lane) * step;
-                int k0j = 0, k1j = 0, cmj = -1;
-                int4 bj = make_int4(0, 0, 0, 0);
-                if (i0 + lane < cnt) {
-                    k0j = __ldg(A.rp + cj * kStreamRows);
-                    k1j = __ldg(A.rp + min(cj * kStreamRows + kStreamRows, n));
-                    if (pf) cmj = __ldg(A.cmax + cj);
-                    if (banded) bj = __ldg(A.bands + cj);
-                }
-                for (int j = 0; j < 32; ++j) {
-                    if (i0 + j >= cnt) break;
-                    const int k0 = __shfl_sync(0xffffffffu, k0j, j), k1 = __shfl_sync(0xffffffffu, k1j, j);
-                    const int cm = __shfl_sync(0xffffffffu, cmj, j);
-                    const int4 bd = make_int4(__shfl_sync(0xffffffffu, bj.x, j), __shfl_sync(0xffffffffu, bj.y, j),
-                                              __shfl_sync(0xffffffffu, bj.z, j), __shfl_sync(0xffffffffu, bj.w, j));
-                    if (lane == 0) put(first + (i0 + j) * step, k0, k1, cm, bd);
+                    if (prof) pw += clock64() - t0;
+                    stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, first + it * G, k0, k1, cm);
                 }
             }
         }
     } else {
         const int g = tid / kStreamRows, t = tid % kStreamRows;
-        for (int i = g; dyn || i < cnt; i += kStreamGroups) {
-            const int it = base + i;
-            const int s = it % ST;
+        for (int i = g; i < cnt; i += kStreamGroups) {
+            const int s = i % ST;
             const long long t0 = prof ? clock64() : 0;
-            mbar_wait(full + s, (uint32_t)(it / ST) & 1u);
+            mbar_wait(full + s, (uint32_t)(i / ST) & 1u);
             const long long t1 = prof ? clock64() : 0;
-            const int chunk = hdr[8 * s];
-            if (chunk < 0) break;
+            const int chunk = first + i * G;
             const unsigned char* sp = smem + (size_t)s * L.stage_bytes();
             Chunk ch;
             ch.rp = (const int*)sp;
             ch.ci = (const int*)(sp + L.rp_bytes());
             ch.av = (const double2*)(sp + L.rp_bytes() + L.ci_bytes());
             ch.vec = (const double2*)(sp + L.rp_bytes() + L.ci_bytes() + L.av_bytes());
-            ch.ng = L.ngather;
-            ch.gs = L.gslots();
-            ch.b0 = hdr[8 * s + 1];
-            ch.w0 = L.nband ? hdr[8 * s + 2] : 0;
-            ch.b1 = hdr[8 * s + 3];
-            ch.w1 = L.nband ? hdr[8 * s + 4] : 0;
             ch.r0 = chunk * kStreamRows;
             ch.rows = min(kStreamRows, n - ch.r0);
             ch.k0 = ch.rp[0];

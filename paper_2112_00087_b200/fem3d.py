@@ -236,7 +236,7 @@ class FemOperator:
 
 def fem_frequency_sweep(cav: FemCavity, freqs_hz, solver="bicgstab", opts=None, mode=None, keep_solutions=False):
     """The sweep driver of sweep.py on the FEM operator (K, M, C resident)."""
-    from .cavac import SolverOptions, _dev_mode, solver_from_name
+    from .cavac import SolverOptions, _dev_mode, solver_id
     from .sweep import SweepRow, SweepTable
     import time
     op = FemOperator(cav)
@@ -251,7 +251,7 @@ def fem_frequency_sweep(cav: FemCavity, freqs_hz, solver="bicgstab", opts=None, 
             op.set_omega(omega)
             o = _lib.CvkOpts(opts.tol, opts.max_iter, opts.l, opts.m, 0, _dev_mode(mode))
             rep = _lib.CvkReport()
-            _lib.check(op.L.cvk_solve(Device.default().handle, int(solver_from_name(solver)), op.hA, op.hM,
+            _lib.check(op.L.cvk_solve(Device.default().handle, int(solver_id(solver)), op.hA, op.hM,
                                       C.byref(o), b.ctypes.data_as(P), x.ctypes.data_as(P), C.byref(rep)))
             table.rows.append(SweepRow(solver, float(f), omega, cav.n, int(rep.iterations), bool(rep.converged),
                                        rep.final_relres, rep.true_relres,

@@ -101,19 +101,8 @@ def schwarz_solve(problem: HelmholtzProblem, part: Partition, tp: TransmissionPa
     """schwarz_solve (schwarz.cpp:111-238).  warm_start (beyond the reference,
     BiCGSTAB inner solver): each strip's inner solve starts from its
     previous-sweep solution instead of 0."""
-    if warm_start:
-        if SolverId(inner_solver) != SolverId.BiCGStab:
-            raise InvalidArgument("schwarz_solve: warm_start needs the bicgstab inner solver")
-        import os
-        old = os.environ.get("CVK_DDM_WARM")
-        os.environ["CVK_DDM_WARM"] = "1"
-        try:
-            return schwarz_solve(problem, part, tp, inner, ddm_tol, max_outer, inner_solver, mode)
-        finally:
-            if old is None:
-                os.environ.pop("CVK_DDM_WARM", None)
-            else:
-                os.environ["CVK_DDM_WARM"] = old
+    if warm_start and SolverId(inner_solver) != SolverId.BiCGStab:
+        raise InvalidArgument("schwarz_solve: warm_start needs the bicgstab inner solver")
     L = _setup_lib()
     A = problem.A
     n = A.nrows
@@ -129,7 +118,8 @@ def schwarz_solve(problem: HelmholtzProblem, part: Partition, tp: TransmissionPa
     cb = np.asarray(part.col_begin, np.int64)
     sl = np.array([complex(tp.s_left).real, complex(tp.s_left).imag])
     sr = np.array([complex(tp.s_right).real, complex(tp.s_right).imag])
-    o = _lib.CvkOpts(float(inner.tol), int(inner.max_iter), int(inner.l), int(inner.m), 0, _dev_mode(mode))
+    o = _lib.CvkOpts(float(inner.tol), int(inner.max_iter), int(inner.l), int(inner.m), 0, _dev_mode(mode),
+                     1 if warm_start else 0, 0)
     g = _grid(problem.grid)
     p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
     code = L.cvk_schwarz_solve(Device.default().handle, C.byref(g), float(problem.c), n, A.nnz(),

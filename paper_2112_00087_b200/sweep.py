@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _lib
 from .cavac import (CsrMatrix, Device, InvalidArgument, SolverId, SolverOptions, _dev_mode,
-                    solver_from_name, solver_name)
+                    solver_id, solver_name)
 from .helmholtz import CavityGrid, pattern, rhs
 from .schwarz import CvkGrid, _grid  # noqa: F401
 
@@ -114,7 +114,7 @@ class CavitySweep:
 
     def solve(self, solver=SolverId.BiCGStab, opts: Optional[SolverOptions] = None, mode=None):
         opts = opts or SolverOptions()
-        sid = solver_from_name(solver) if isinstance(solver, str) else SolverId(solver)
+        sid = solver_id(solver) if isinstance(solver, str) else SolverId(solver)
         o = _lib.CvkOpts(opts.tol, opts.max_iter, opts.l, opts.m, 0, _dev_mode(mode))
         rep = _lib.CvkReport()
         L = _lib.load()

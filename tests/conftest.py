@@ -46,3 +46,19 @@ def cvk():
     from paper_2112_00087_b200 import build
     build.build()
     return P
+
+
+@pytest.fixture
+def knobs(cvk):
+    """knobs(phased_min_n=0, stream=0, ...): execution-path options of the
+    default device context (cvk_ctx_set_option), restored after the test."""
+    entered = []
+
+    def set_(**kw):
+        cm = cvk.path_options(**kw)
+        cm.__enter__()
+        entered.append(cm)
+
+    yield set_
+    for cm in reversed(entered):
+        cm.__exit__(None, None, None)

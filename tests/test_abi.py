@@ -34,12 +34,27 @@ def test_sm100a_cubin_and_no_fma(lib):
 
 def test_names_and_codes(lib):
     L = lib.load()
-    assert L.cvk_abi_version() == 1
+    assert L.cvk_abi_version() == 2
     assert L.cvk_solver_name(2) == b"tfqmr"
     assert L.cvk_solver_from_name(b"bicgstab_l") == 1
     assert L.cvk_solver_from_name(b"gmres2") == -6
     assert b"allowed" in L.cvk_last_error()
     assert L.cvk_breakdown_name(3) == b"omega breakdown"
+
+
+def test_cvk_opts_layout(lib):
+    """cvk_opts as declared in include/cavac_b200.h (ABI 2 adds warm)."""
+    import ctypes as C
+    assert C.sizeof(lib.CvkOpts) == 48
+    assert lib.CvkOpts.warm.offset == 40
+    assert set(lib.OPTIONS.values()) == set(range(1, 11))
+
+
+def test_no_environment_switches_in_native_code():
+    """Execution paths are chosen by cvk_ctx_set_option, never by getenv."""
+    src = os.path.join(ROOT, "paper_2112_00087_b200", "csrc")
+    for f in os.listdir(src):
+        assert "getenv" not in open(os.path.join(src, f)).read(), f
 
 
 @pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure path")

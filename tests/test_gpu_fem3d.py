@@ -46,17 +46,17 @@ def test_fem_sweep_matches_dense(cvk, oracle, solver):
         assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-9, row
 
 
-def test_fem_streamed_path_matches_oracle(cvk, oracle, monkeypatch):
+def test_fem_streamed_path_matches_oracle(cvk, oracle, knobs):
     """A 14-entries-per-row operator on the phase-kernel (TMA-streamed) path,
     against the oracle's BiCGSTAB on the same CSR at tight tolerance."""
     import paper_2112_00087_b200 as P
     from paper_2112_00087_b200 import fem3d as F
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    knobs(phased_min_n=0)
     cav = F.build_cavity(9)          # 19 x 10 x 10 = 1900 DOF, several 224-row chunks
     om = 2 * math.pi * 140.0
     A = cav.matrix(om)
     for s in ("bicgstab", "tfqmr"):
-        r = P.solve(P.solver_from_name(s), A, cav.b, P.jacobi(A), P.SolverOptions(tol=1e-12, max_iter=20000))
+        r = P.solve(P.solver_id(s), A, cav.b, P.jacobi(A), P.SolverOptions(tol=1e-12, max_iter=20000))
         x_o, rep = oracle.solve(s, cav.rp, cav.ci, cav.values(om), cav.b, tol=1e-12, max_iter=20000)
         assert r.report.converged and rep.converged
         assert np.linalg.norm(r.x - x_o) / np.linalg.norm(x_o) <= 1e-9

@@ -27,17 +27,15 @@ ACCEPT = os.path.join(ROOT, "dropin", "_bin", "acceptance_b200")
 
 @pytest.mark.skipif(not os.path.exists(ACCEPT), reason="drop-in acceptance binary not built here")
 def test_reference_acceptance_gate_on_b200(cvk):
-    """proj/tests/acceptance.cpp with the B200 numkit/krylov/schwarz.  Criteria
-    4-6 (manufactured O(h^2), solver suite, DDM + tuning) and 8 (determinism +
-    byte comparison with every golden artifact) must pass.  Criterion 7
-    requires equal iteration counts in both ExecModes; on the device
-    Sequential is the bitwise reference arithmetic and Parallel the tree
-    reductions, whose counts differ, so it is reported, not
-    required."""
+    """proj/tests/acceptance.cpp with the B200 numkit/krylov/schwarz: every
+    criterion must pass, including 7 (bench_solvers, pipeline.cpp:227-293),
+    which throws unless both ExecModes give identical iteration counts and
+    asserts Parallel >= Sequential speed at the finest ladder point.  On the
+    device both modes give the reference's iterates bit for bit (Sequential:
+    one thread per reduction; Parallel: the terms formed by a whole CTA)."""
     r = subprocess.run([ACCEPT], cwd=ROOT, capture_output=True, text=True, timeout=1500)
     out = r.stdout
     status = dict((m.group(2), m.group(1)) for m in re.finditer(r"\[(PASS|FAIL)\] (.+?) \(", out))
-    for name in ("manufactured-solution grid convergence", "iterative solver suite",
-                 "domain decomposition vs monodomain and tuning", "determinism and recorded reference run",
-                 "face interpolation formulas and limiter", "transform identities and peak detection"):
-        assert status.get(name) == "PASS", out
+    assert len(status) == 8, out
+    assert all(v == "PASS" for v in status.values()), out
+    assert r.returncode == 0, out + r.stderr

@@ -125,9 +125,9 @@ def test_ilu0_errors(cvk, oracle):
     assert res.report.converged and res.report.iterations == 0 and not res.x.any()
 
 
-def test_graph_chain_matches_host_loop(cvk, oracle, monkeypatch):
+def test_graph_chain_matches_host_loop(cvk, oracle, knobs):
     """FAST mode runs the device-scalar phase chain (cvk_ilu.cu, CUDA graph);
-    CVK_ILU_HOSTLOOP=1 forces the host loop of the same kernels' arithmetic.
+    CVK_OPT_ILU_HOSTLOOP forces the host loop of the same kernels' arithmetic.
     Same reduction kernels' sums, so the same iterations and a matching x."""
     P = cvk
     rp, ci, v, b = cavity(oracle, 0.008, 250.0)
@@ -137,9 +137,9 @@ def test_graph_chain_matches_host_loop(cvk, oracle, monkeypatch):
     for s in (0, 2, 3):
         M = P.ilu0(A, s)
         chain = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
-        monkeypatch.setenv("CVK_ILU_HOSTLOOP", "1")
+        knobs(ilu_hostloop=1)
         host = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
-        monkeypatch.delenv("CVK_ILU_HOSTLOOP")
+        knobs(ilu_hostloop=0)
         assert chain.report.converged and host.report.converged
         assert abs(chain.report.iterations - host.report.iterations) <= 1
         assert len(chain.report.residual_history) == chain.report.iterations
@@ -158,21 +158,3 @@ def test_chain_max_iter_and_zero_rhs(cvk, oracle):
         assert not r.converged and r.iterations == k
     r = P.solve(P.SolverId.BiCGStab, A, np.zeros(n, complex), M).report
     assert r.converged and r.iterations == 0
-
-
-def test_fused_folds_bitwise_separate_folds(cvk, oracle, monkeypatch):
-    """Separate 1-CTA k_ic_fold launches (default) or the last-arriving CTA
-    folding the partials (CVK_ILU_FUSED_FOLD=1, opt-in): same sums, same bits."""
-    P = cvk
-    rp, ci, v, b = cavity(oracle, 0.008, 250.0)
-    n = len(rp) - 1
-    A = P.CsrMatrix(n, n, rp, ci, v)
-    M = P.ilu0(A, 3)
-    opts = P.SolverOptions(tol=1e-9, max_iter=100000)
-    sep = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
-    monkeypatch.setenv("CVK_ILU_FUSED_FOLD", "1")
-    fused = P.solve(P.SolverId.BiCGStab, A, b, M, opts)
-    monkeypatch.delenv("CVK_ILU_FUSED_FOLD")
-    assert fused.report.iterations == sep.report.iterations
-    assert np.array_equal(bits(fused.x), bits(sep.x))
-    assert fused.report.kernel_launches < sep.report.kernel_launches

@@ -55,13 +55,14 @@ def test_spmv_ref_bitwise_and_fast_close(cvk, oracle, golden):
         A = mat(P, rp, ci, v)
         got_ref = P.spmv(A, x, mode=P.ExecMode.Sequential)
         assert np.array_equal(bits(got_ref), bits(want))
-        got = P.spmv(A, x, mode=P.ExecMode.Parallel)
+        assert np.array_equal(bits(P.spmv(A, x, mode=P.ExecMode.Parallel)), bits(want))
+        got = P.spmv(A, x, mode=P.ExecMode.Fast)
         assert np.all(np.abs(got - want) <= 1e-13 * (1.0 + np.abs(want)))
 
 
 @pytest.mark.parametrize("group", [1, 2, 4, 8, 16])
-def test_spmv_every_group_width(cvk, oracle, monkeypatch, group):
-    monkeypatch.setenv("CVK_SPMV_GROUP", str(group))
+def test_spmv_every_group_width(cvk, oracle, knobs, group):
+    knobs(spmv_group=group)
     P = cvk
     rng = np.random.default_rng(group)
     rp, ci, v = rand_csr(oracle, 3001, 3001 * 14, rng)
@@ -80,7 +81,8 @@ def test_dot_norm_axpy(cvk, oracle):
         y = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
         want = oracle.dot(x, y)
         assert P.dot_hermitian(x, y, mode=P.ExecMode.Sequential) == want
-        got = P.dot_hermitian(x, y, mode=P.ExecMode.Parallel)
+        assert P.dot_hermitian(x, y, mode=P.ExecMode.Parallel) == want
+        got = P.dot_hermitian(x, y, mode=P.ExecMode.Fast)
         assert abs(got - want) <= 1e-13 * max(1.0, np.abs(x).dot(np.abs(y)))
         assert P.norm2(x, mode=P.ExecMode.Sequential) == oracle.norm2(x)
         assert abs(P.norm2(x) - oracle.norm2(x)) <= 1e-14 * max(1.0, oracle.norm2(x))
@@ -104,23 +106,26 @@ def test_jacobi_device_bitwise(cvk, oracle, golden):
         P.jacobi(sing)
 
 
-def test_golden_ref_mode_reproduces_reference(cvk, oracle, golden):
-    """The reference's recorded run, bit for bit, on the device."""
+@pytest.mark.parametrize("mode", ["Sequential", "Parallel"])
+def test_golden_ref_mode_reproduces_reference(cvk, oracle, golden, mode):
+    """The reference's recorded run, bit for bit, on the device -- in both of
+    the reference's ExecModes, which promise identical iterates (numkit.hpp:14-18)."""
     P = cvk
     A = mat(P, golden["rp"], golden["ci"], golden["v"])
-    r = P.bicgstab(A, golden["b"], P.jacobi(A), P.SolverOptions(), mode=P.ExecMode.Sequential)
+    r = P.bicgstab(A, golden["b"], P.jacobi(A), P.SolverOptions(), mode=P.ExecMode[mode])
     assert r.report.converged and r.report.iterations == 246
     assert "%.17g" % r.report.final_relres == "8.9265369265007959e-10"
     assert "%.17g" % r.report.true_relres == "8.5608367217167752e-10"
     assert oracle.format_vector_csv(r.x) == golden["solution_csv"]
 
 
+@pytest.mark.parametrize("mode", ["Sequential", "Parallel"])
 @pytest.mark.parametrize("solver", SOLVERS)
-def test_ref_mode_bitwise_all_solvers(cvk, oracle, golden, solver):
+def test_ref_mode_bitwise_all_solvers(cvk, oracle, golden, solver, mode):
     P = cvk
     A = mat(P, golden["rp"], golden["ci"], golden["v"])
     opts = P.SolverOptions(record_history=True, max_iter=400 if solver == "gmres" else 10000)
-    r = P.solve(P.solver_from_name(solver), A, golden["b"], P.jacobi(A), opts, mode=P.ExecMode.Sequential)
+    r = P.solve(P.solver_id(solver), A, golden["b"], P.jacobi(A), opts, mode=P.ExecMode[mode])
     xo, ro = oracle.solve(solver, golden["rp"], golden["ci"], golden["v"], golden["b"],
                           record_history=True, max_iter=opts.max_iter)
     assert (r.report.iterations, r.report.converged) == (ro.iterations, ro.converged)
@@ -138,11 +143,11 @@ def test_fast_mode_matches_reference_solution(cvk, oracle, golden, solver):
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     x_tight, _ = oracle.solve(solver, rp, ci, v, b, tol=1e-12)
-    r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-12))
+    r = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-12))
     assert r.report.converged and r.report.final_relres <= 1e-12
     assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
     _, ro = oracle.solve(solver, rp, ci, v, b, tol=1e-9)
-    r9 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    r9 = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-9))
     # reduction order alone moves the counts: SURVEY.md 7 measured -14% / +8%
     # for BiCGSTAB; on this device tfQMR gives 187 vs 207 (-10%)
     band = 0.15
@@ -168,7 +173,7 @@ def test_ref_mode_bitwise_larger_and_damped(cvk, oracle):
         A = mat(P, rp, ci, v)
         M = P.jacobi(A)
         for s in ("bicgstab", "tfqmr", "bicgstab_l"):
-            r = P.solve(P.solver_from_name(s), A, b, M, P.SolverOptions(), mode=P.ExecMode.Sequential)
+            r = P.solve(P.solver_id(s), A, b, M, P.SolverOptions(), mode=P.ExecMode.Sequential)
             xo, ro = oracle.solve(s, rp, ci, v, b)
             assert r.report.iterations == ro.iterations
             assert np.array_equal(bits(r.x), bits(xo))
@@ -181,15 +186,15 @@ def test_kats(cvk):
     I = P.csr_identity(10)
     b = rng.uniform(-1, 1, 10) + 1j * rng.uniform(-1, 1, 10)
     for s in SOLVERS:
-        r = P.solve(P.solver_from_name(s), I, b, P.identity_preconditioner())
+        r = P.solve(P.solver_id(s), I, b, P.identity_preconditioner())
         assert r.report.converged and r.report.iterations <= 1
         assert np.abs(r.x - b).max() <= 1e-12
     n = 12
     D = P.csr_from_triplets(np.arange(n), np.arange(n), [complex(1 + i, 0.5 * i) for i in range(n)], n, n)
     b = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
     for s in SOLVERS:
-        for mode in (P.ExecMode.Sequential, P.ExecMode.Parallel):
-            r = P.solve(P.solver_from_name(s), D, b, P.jacobi(D), mode=mode)
+        for mode in (P.ExecMode.Sequential, P.ExecMode.Parallel, P.ExecMode.Fast):
+            r = P.solve(P.solver_id(s), D, b, P.jacobi(D), mode=mode)
             assert r.report.converged and r.report.iterations == 1 and r.report.true_relres <= 1e-12
     A2 = P.csr_from_triplets([0, 1], [0, 1], [1 + 1j, 2 - 1j], 2, 2)
     r = P.bicgstab(A2, [1 + 1j, 2 - 1j], P.jacobi(A2))
@@ -209,7 +214,7 @@ def test_errors_and_exhaustion(cvk, oracle):
     with pytest.raises(P.InvalidArgument, match="dimension mismatch"):
         P.bicgstab(A, b[:-1], P.jacobi(A))
     with pytest.raises(P.InvalidArgument, match="allowed"):
-        P.solver_from_name("gmres2")
+        P.solver_id("gmres2")
 
 
 def test_fast_mode_deterministic(cvk, oracle):
@@ -243,17 +248,17 @@ def test_ladder_iterations_grow(cvk, oracle):
         for h in (0.133425, 0.066604, 0.033289, 0.016643):
             rp, ci, v, b = cavity(oracle, h)
             A = mat(P, rp, ci, v)
-            r = P.solve(P.solver_from_name(s), A, b, P.jacobi(A))
+            r = P.solve(P.solver_id(s), A, b, P.jacobi(A))
             assert r.report.converged and r.report.true_relres <= 1e-8
             assert r.report.iterations >= prev
             prev = r.report.iterations
 
 
 @pytest.fixture(params=["persistent", "phased"])
-def fast_path(request, monkeypatch):
+def fast_path(request, knobs):
     """Run a FAST-mode test on both device paths: the persistent cooperative
     kernel (small systems) and the phase-kernel graph path (large systems)."""
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0" if request.param == "phased" else "1000000000")
+    knobs(phased_min_n=0 if request.param == "phased" else 1000000000)
     return request.param
 
 
@@ -264,21 +269,21 @@ def test_fast_paths_agree_with_reference(cvk, oracle, golden, fast_path, solver)
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     x_tight, _ = oracle.solve(solver, rp, ci, v, b, tol=1e-12)
-    r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-12, record_history=True))
+    r = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-12, record_history=True))
     assert r.report.converged and r.report.final_relres <= 1e-12
     assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
     assert len(r.report.residual_history) >= r.report.iterations - 1
     assert abs(r.report.true_relres - oracle.true_relres(rp, ci, v, b, r.x)) <= 1e-3 * r.report.true_relres + 1e-15
     _, ro = oracle.solve(solver, rp, ci, v, b, tol=1e-9)
-    r9 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    r9 = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-9))
     assert r9.report.converged
     assert abs(r9.report.iterations - ro.iterations) <= max(2, 0.15 * ro.iterations)
     # exhaustion, zero rhs, determinism
-    e = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(max_iter=3))
+    e = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(max_iter=3))
     assert not e.report.converged and e.report.iterations <= 3
-    z = P.solve(P.solver_from_name(solver), A, np.zeros_like(b), M)
+    z = P.solve(P.solver_id(solver), A, np.zeros_like(b), M)
     assert z.report.converged and z.report.iterations == 0 and z.report.true_relres == 0.0
-    r2 = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-9))
+    r2 = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-9))
     assert np.array_equal(bits(r2.x), bits(r9.x))
 
 
@@ -289,7 +294,7 @@ def test_fast_paths_diagonal_kat(cvk, fast_path):
     D = P.csr_from_triplets(np.arange(n), np.arange(n), [complex(1 + i, 0.5 * i) for i in range(n)], n, n)
     b = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
     for s in ("bicgstab", "tfqmr"):
-        r = P.solve(P.solver_from_name(s), D, b, P.jacobi(D))
+        r = P.solve(P.solver_id(s), D, b, P.jacobi(D))
         assert r.report.converged and r.report.iterations == 1 and r.report.true_relres <= 1e-12
 
 
@@ -311,14 +316,12 @@ def irregular_csr(O, n, rng, max_row=40):
 
 
 @pytest.mark.parametrize("stream", ["streamed", "thread-per-row"])
-def test_phased_irregular_rows(cvk, oracle, monkeypatch, stream):
+def test_phased_irregular_rows(cvk, oracle, knobs, stream):
     """The phase-kernel path (TMA-streamed SpMV phases and the fallback) on a
     ragged matrix: chunk edges, rows longer than a batch, empty off-diagonal
     rows, a partial last chunk, Jacobi and identity preconditioners."""
     P = cvk
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
-    if stream != "streamed":
-        monkeypatch.setenv("CVK_NO_STREAM", "1")
+    knobs(phased_min_n=0, stream=1 if stream == "streamed" else 0)
     rng = np.random.default_rng(7)
     n = 256 * 11 + 77
     rp, ci, v = irregular_csr(oracle, n, rng)
@@ -329,7 +332,7 @@ def test_phased_irregular_rows(cvk, oracle, monkeypatch, stream):
             M = P.jacobi(A) if prec == "jacobi" else P.identity_preconditioner()
             x_ref, _ = oracle.solve(s, rp, ci, v, b, dinv=None if prec == "jacobi" else "identity",
                                     tol=1e-13)
-            r = P.solve(P.solver_from_name(s), A, b, M, P.SolverOptions(tol=1e-12))
+            r = P.solve(P.solver_id(s), A, b, M, P.SolverOptions(tol=1e-12))
             assert r.report.converged, (s, prec, r.report)
             err = np.linalg.norm(r.x - x_ref) / np.linalg.norm(x_ref)
             assert err <= 1e-10, (s, prec, err)
@@ -337,7 +340,7 @@ def test_phased_irregular_rows(cvk, oracle, monkeypatch, stream):
 
 
 @pytest.mark.parametrize("solver", ["bicgstab", "tfqmr"])
-def test_fast_paths_bitwise_identical(cvk, golden, monkeypatch, solver):
+def test_fast_paths_bitwise_identical(cvk, golden, knobs, solver):
     """FAST reductions are double-double (cvk_engine.cuh): the reduced scalars
     do not depend on grid size or row-to-CTA mapping, so the persistent
     kernel, the thread-per-row phase kernels and the TMA-streamed phase
@@ -347,18 +350,12 @@ def test_fast_paths_bitwise_identical(cvk, golden, monkeypatch, solver):
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     out = {}
-    for path, env in (("persistent", {"CVK_PHASED_MIN_N": "1000000000"}),
-                      ("phased", {"CVK_PHASED_MIN_N": "0", "CVK_NO_STREAM": "1"}),
-                      ("streamed", {"CVK_PHASED_MIN_N": "0"}),
-                      ("persistent-small-grid", {"CVK_PHASED_MIN_N": "1000000000", "CVK_MAX_CTAS": "3"}),
-                      ("streamed-persistent", {"CVK_PHASED_MIN_N": "0", "CVK_STREAMK": "1"})):
-        if path == "streamed-persistent" and solver != "bicgstab":
-            continue
-        for k in ("CVK_PHASED_MIN_N", "CVK_NO_STREAM", "CVK_MAX_CTAS", "CVK_STREAMK"):
-            monkeypatch.delenv(k, raising=False)
-        for k, val in env.items():
-            monkeypatch.setenv(k, val)
-        r = P.solve(P.solver_from_name(solver), A, b, M, P.SolverOptions(tol=1e-10))
+    for path, kw in (("persistent", dict(phased_min_n=1000000000)),
+                     ("phased", dict(phased_min_n=0, stream=0)),
+                     ("streamed", dict(phased_min_n=0)),
+                     ("persistent-small-grid", dict(phased_min_n=1000000000, max_ctas=3))):
+        knobs(**{"phased_min_n": 131072, "stream": 1, "max_ctas": 0, **kw})
+        r = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-10))
         out[path] = (r.report.iterations, bits(r.x))
     it0, x0 = out["persistent"]
     for path, (it, x) in out.items():
@@ -366,32 +363,8 @@ def test_fast_paths_bitwise_identical(cvk, golden, monkeypatch, solver):
         assert np.array_equal(x, x0), path
 
 
-def test_merged_bicgstab_matches_reference(cvk, oracle, golden, monkeypatch):
-    """The opt-in two-kernel BiCGSTAB (rho_new from <shadow,s> - omega <shadow,t>,
-    x/r update merged into the next SpMV phase): same solution as the
-    reference at tol 1e-12, iteration count in the BiCGSTAB band."""
-    P = cvk
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
-    monkeypatch.setenv("CVK_BICG_MERGED", "1")
-    rp, ci, v, b = golden["rp"], golden["ci"], golden["v"], golden["b"]
-    A = mat(P, rp, ci, v)
-    M = P.jacobi(A)
-    x_tight, _ = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-12)
-    r = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-12, record_history=True))
-    assert r.report.converged and r.report.final_relres <= 1e-12
-    assert np.linalg.norm(r.x - x_tight) / np.linalg.norm(x_tight) <= 1e-10
-    assert len(r.report.residual_history) >= r.report.iterations - 1
-    _, ro = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-9)
-    r9 = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(tol=1e-9))
-    assert r9.report.converged and abs(r9.report.iterations - ro.iterations) <= max(2, 0.15 * ro.iterations)
-    e = P.solve(P.SolverId.BiCGStab, A, b, M, P.SolverOptions(max_iter=3))
-    assert not e.report.converged and e.report.iterations == 3
-    z = P.solve(P.SolverId.BiCGStab, A, np.zeros_like(b), M)
-    assert z.report.converged and z.report.iterations == 0
-
-
 @pytest.mark.parametrize("m", [30, 7])
-def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, monkeypatch, m):
+def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, knobs, m):
     """GMRES(m) as phase kernels (cvk_gmres.cu) = the persistent kernel, bit
     for bit (same operation order, double-double dots), across restarts; and
     pinned to the reference solution at tight tolerance."""
@@ -402,7 +375,7 @@ def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, monkeypatch, m):
     M = P.jacobi(A)
     out = {}
     for path, min_n in (("persistent", "1000000000"), ("phased", "0")):
-        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+        knobs(phased_min_n=int(min_n))
         r = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(tol=1e-11, m=m, max_iter=5000, record_history=True))
         out[path] = r
     a_, b_ = out["persistent"], out["phased"]
@@ -417,7 +390,7 @@ def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, monkeypatch, m):
 
 
 @pytest.mark.parametrize("l", [8, 2, 1])
-def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypatch, l):
+def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, knobs, l):
     """BiCGSTAB(l) as the uniform phase-step kernel (cvk_bicgl.cu) = the
     persistent kernel bit for bit (double-double reductions), and the
     reference's iteration count within the +-5% band of SURVEY.md 8(c)."""
@@ -426,12 +399,9 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     out = {}
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    knobs(phased_min_n=0)
     for path in ("persistent", "phased"):
-        if path == "persistent":
-            monkeypatch.setenv("CVK_BICGL_PERSISTENT", "1")
-        else:
-            monkeypatch.delenv("CVK_BICGL_PERSISTENT", raising=False)
+        knobs(bicgl_persistent=1 if path == "persistent" else 0)
         out[path] = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(tol=1e-10, l=l, record_history=True))
     a_, b_ = out["persistent"], out["phased"]
     assert a_.report.converged and b_.report.converged
@@ -450,7 +420,7 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, monkeypa
 
 
 @pytest.mark.parametrize("solver", ["bicgstab", "tfqmr"])
-def test_stream_flavors_bitwise(cvk, oracle, monkeypatch, solver):
+def test_stream_flavors_bitwise(cvk, oracle, knobs, solver):
     """The two consumer shapes of the streamed phase kernels (2 x 224 rows,
     cvk_phased.cu; 4 x 128 rows, cvk_phased_g4.cu) give the same bits on a
     cavity and an FEM-3D system -- only the row-to-thread mapping differs."""
@@ -459,14 +429,14 @@ def test_stream_flavors_bitwise(cvk, oracle, monkeypatch, solver):
     cav = F.build_cavity(12)
     systems = [cavity(oracle, 0.0075, f=60.0, adm=0.01),
                (cav.rp, cav.ci, cav.values(2 * np.pi * 80.0), np.asarray(cav.b, np.complex128))]
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    knobs(phased_min_n=0)
     for rp, ci, v, b in systems:
         A = mat(P, rp, ci, v)
         M = P.jacobi(A)
         out = {}
         for fl in ("g2", "g4"):
-            monkeypatch.setenv("CVK_STREAM_FLAVOR", fl)
-            out[fl] = P.solve(P.solver_from_name(solver), A, b, M,
+            knobs(stream_flavor=2 if fl == "g2" else 4)
+            out[fl] = P.solve(P.solver_id(solver), A, b, M,
                               P.SolverOptions(tol=1e-10, max_iter=5000, record_history=True))
         a_, b_ = out["g2"], out["g4"]
         assert a_.report.converged and a_.report.iterations == b_.report.iterations

@@ -105,7 +105,7 @@ def test_single_subdomain_is_plain_solve(cvk, ddm):
     H, S = ddm
     P = cvk
     p = cavity_problem(H, 0.1)
-    for mode in (P.ExecMode.Sequential, P.ExecMode.Parallel):
+    for mode in (P.ExecMode.Sequential, P.ExecMode.Parallel, P.ExecMode.Fast):
         r = S.schwarz_solve(p, S.partition(p.grid, 1), S.TransmissionParams(1j, 1j), P.SolverOptions(), 1e-8, 50,
                             mode=mode)
         d = P.bicgstab(p.A, p.b, P.jacobi(p.A), P.SolverOptions(), mode=mode)
@@ -164,9 +164,9 @@ def test_tune_parameters(cvk, ddm):
 
 
 @pytest.mark.parametrize("solver", ["bicgstab", "tfqmr", "gmres"])
-def test_sequential_strip_solves_bitwise_batched(cvk, ddm, monkeypatch, solver):
+def test_sequential_strip_solves_bitwise_batched(cvk, ddm, knobs, solver):
     """FAST DDM with the strips' inner solves run one after another on the
-    single-system path (used when every strip has >= CVK_DDM_SEQ_MIN rows;
+    single-system path (used when every strip has >= CVK_OPT_DDM_SEQ_MIN rows;
     forced here) = the batched persistent launch, bit for bit: the inner
     reductions are double-double on both paths."""
     H, S = ddm
@@ -175,11 +175,10 @@ def test_sequential_strip_solves_bitwise_batched(cvk, ddm, monkeypatch, solver):
     k = p.omega / p.c
     part = S.partition(p.grid, 3)
     tp = S.TransmissionParams(complex(2.0, k), complex(2.0, k))
-    sid = P.solver_from_name(solver)
+    sid = P.solver_id(solver)
     out = {}
     for path, thr in (("batched", "1000000000"), ("sequential", "0")):
-        monkeypatch.setenv("CVK_DDM_SEQ_MIN", thr)
-        monkeypatch.setenv("CVK_PHASED_MIN_N", "0" if path == "sequential" else "1000000000")
+        knobs(ddm_seq_min=int(thr), phased_min_n=0 if path == "sequential" else 1000000000)
         out[path] = S.schwarz_solve(p, part, tp, P.SolverOptions(tol=1e-10, m=20), 1e-8, 40, inner_solver=sid)
     a, b = out["batched"], out["sequential"]
     assert a.report.outer_iterations == b.report.outer_iterations
@@ -211,7 +210,7 @@ def test_krylov_interface_iteration(cvk, ddm, ns):
     assert kr.report.residual_history[-1] <= 1e-9
 
 
-def test_warm_started_inner_solves(cvk, ddm, monkeypatch):
+def test_warm_started_inner_solves(cvk, ddm, knobs):
     """Warm-started inner BiCGSTAB (beyond the reference): the same DDM
     solution as the reference's cold starts (monodomain tolerance) with fewer
     inner iterations, bitwise the same on the batched persistent and the
@@ -233,8 +232,7 @@ def test_warm_started_inner_solves(cvk, ddm, monkeypatch):
     tot = lambda r: sum(s.iterations for s in r.report.per_subdomain_solves)  # noqa: E731
     assert tot(warm) < tot(cold), (tot(warm), tot(cold))
     assert np.linalg.norm(warm.x - mono.x) <= 1e-6 * np.linalg.norm(mono.x)
-    monkeypatch.setenv("CVK_DDM_SEQ_MIN", "0")
-    monkeypatch.setenv("CVK_PHASED_MIN_N", "0")
+    knobs(ddm_seq_min=0, phased_min_n=0)
     seq = S.schwarz_solve(p, part, tp, inner, 1e-8, 300, warm_start=True)
     assert seq.report.outer_iterations == warm.report.outer_iterations
     assert np.array_equal(bits(seq.x), bits(warm.x))
@@ -246,7 +244,7 @@ def test_warm_started_inner_solves(cvk, ddm, monkeypatch):
     M = P.jacobi(A)
     dev = P.Device.default()
     for min_n in ("1000000000", "0"):
-        monkeypatch.setenv("CVK_PHASED_MIN_N", min_n)
+        knobs(phased_min_n=int(min_n))
         r = P.solve(P.SolverId.BiCGStab, A, p.b, M, P.SolverOptions(tol=1e-10))
         bd = torch.from_numpy(np.asarray(p.b, np.complex128).view(np.float64).copy()).cuda()
         xd = torch.zeros_like(bd)

@@ -20,5 +20,5 @@ for ctas in ("1", "2", "0"):
         t_orc = O.true_relres(rp, ci, v, b, r.x)
         print(ctas, mode.name, r.report.iterations, "%.17g %.17g %.17g" % (r.report.true_relres, t_api, t_orc), flush=True)
     for s in ("tfqmr", "bicgstab_l", "gmres"):
-        r = P.solve(P.solver_from_name(s), A, b, M, P.SolverOptions(max_iter=300), mode=P.ExecMode.Sequential)
+        r = P.solve(P.solver_id(s), A, b, M, P.SolverOptions(max_iter=300), mode=P.ExecMode.Sequential)
         print(ctas, s, r.report.iterations, "%.17g %.17g" % (r.report.true_relres, O.true_relres(rp, ci, v, b, r.x)), flush=True)

@@ -36,7 +36,7 @@ for S in (int(s) for s in os.environ.get("PROBE_SOLVE_S", "4").split(",")):
     A = P.CsrMatrix(prob.A.nrows, prob.A.ncols, prob.A.row_offsets, prob.A.col_indices, prob.A.values)
     M = P.jacobi(A)
     for solver in os.environ.get("PROBE_SOLVERS", "bicgstab").split(","):
-        r = P.solve(P.solver_from_name(solver), A, prob.b, M, P.SolverOptions(tol=1e-8, max_iter=int(os.environ.get("PROBE_MAXIT", "3000"))))
+        r = P.solve(P.solver_id(solver), A, prob.b, M, P.SolverOptions(tol=1e-8, max_iter=int(os.environ.get("PROBE_MAXIT", "3000"))))
         rep = r.report
         it = max(rep.iterations, 1)
         print(f"S={S} {solver}: it={rep.iterations} conv={rep.converged} relres={rep.final_relres:.2e} true={rep.true_relres:.2e} "

@@ -33,8 +33,8 @@ for case in cases:
     n, nnz = A.nrows, A.nnz()
     for s in solvers:
         opts = P.SolverOptions(tol=1e-30, max_iter=maxit)
-        P.solve(P.solver_from_name(s), A, b, M, opts)
-        r = P.solve(P.solver_from_name(s), A, b, M, opts)
+        P.solve(P.solver_id(s), A, b, M, opts)
+        r = P.solve(P.solver_id(s), A, b, M, opts)
         it = max(1, r.report.iterations)
         per = r.report.device_time / it
         spmv_b = 20 * nnz + 4 * (n + 1) + 32 * n

@@ -10,5 +10,5 @@ prob = H.assemble(g, 2 * math.pi * 100.0, 340.0, np.ones(g.roof_size(), np.compl
 A = prob.A
 M = P.jacobi(A)
 for solver in os.environ.get("PROBE_SOLVERS", "bicgstab").split(","):
-    r = P.solve(P.solver_from_name(solver), A, prob.b, M, P.SolverOptions(tol=1e-8, max_iter=int(os.environ.get("PROBE_MAXIT", "20"))))
+    r = P.solve(P.solver_id(solver), A, prob.b, M, P.SolverOptions(tol=1e-8, max_iter=int(os.environ.get("PROBE_MAXIT", "20"))))
     print(solver, r.report.iterations, r.report.device_time)

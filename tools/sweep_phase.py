@@ -26,7 +26,7 @@ for solver in os.environ.get("PROBE_SOLVERS", "bicgstab").split(","):
             for kv in cfg.split(","):
                 k, v = kv.split("=")
                 os.environ[k] = v
-        sid = P.solver_from_name(solver)
+        sid = P.solver_id(solver)
         opts = P.SolverOptions(tol=1e-30, max_iter=maxit)
         P.solve(sid, A, prob.b, M, opts)  # warm (graph capture)
         ts = []
