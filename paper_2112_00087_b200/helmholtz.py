@@ -105,14 +105,23 @@ def wall_weight(grid: CavityGrid, omega: float) -> complex:
     return cdiv(complex(1.0, 0.0), complex(1.0, 0.0) + cmul(complex(0.0, omega * grid.h), grid.wall_admittance))
 
 
-def pattern(grid: CavityGrid):
+def _nodes(grid: CavityGrid, rows):
+    """(node, ix, iy) of the grid rows [r0, r1) (all rows when rows is None)."""
+    r0, r1 = (0, grid.size()) if rows is None else (int(rows[0]), int(rows[1]))
+    if not 0 <= r0 <= r1 <= grid.size():
+        raise InvalidArgument("rows must satisfy 0 <= r0 <= r1 <= grid size")
+    node = np.arange(r0, r1, dtype=np.int64)
+    return node, node % grid.nx, node // grid.nx
+
+
+def pattern(grid: CavityGrid, rows=None):
     """CSR pattern of the 5-point operator: per row below, left, diag, right,
     above (the stable (row, col) order csr_from_triplets produces).  Returns
-    (row_offsets, col_indices, slot) with slot = 0..4 naming each entry."""
+    (row_offsets, col_indices, slot) with slot = 0..4 naming each entry.
+    rows = (r0, r1): only those rows (row offsets from 0, global columns) --
+    a rank's block of a distributed solve, assembled without the rest."""
     nx, ny = grid.nx, grid.ny
-    ix = np.tile(np.arange(nx, dtype=np.int64), ny)
-    iy = np.repeat(np.arange(ny, dtype=np.int64), nx)
-    node = iy * nx + ix
+    node, ix, iy = _nodes(grid, rows)
     has = np.stack([iy > 0, ix > 0, np.ones_like(ix, bool), ix + 1 < nx, iy + 1 < ny], axis=1)
     off = np.array([-nx, -1, 0, 1, nx], dtype=np.int64)
     cols = node[:, None] + off[None, :]
@@ -124,20 +133,20 @@ def pattern(grid: CavityGrid):
     return rp, ci, slot, has
 
 
-def values(grid: CavityGrid, omega: float, c: float, pat=None) -> np.ndarray:
+def values(grid: CavityGrid, omega: float, c: float, pat=None, rows=None) -> np.ndarray:
     """helmholtz.cpp:78-113 values on the fixed pattern (diag 4k^2 - omega^2,
     minus k^2 w per missing wall neighbour in the order left, right, below,
-    above; off-diagonals -k^2)."""
-    rp, ci, slot, has = pat if pat is not None else pattern(grid)
+    above; off-diagonals -k^2).  Each row's values depend only on its grid
+    position, so rows=(r0, r1) gives bitwise those rows of the global values."""
+    rp, ci, slot, has = pat if pat is not None else pattern(grid, rows)
     nx, ny = grid.nx, grid.ny
     k2 = c * c / (grid.h * grid.h)
     ww = wall_weight(grid, omega)
     kw_re, kw_im = k2 * ww.real, k2 * ww.imag
-    ix = np.tile(np.arange(nx), ny)
-    iy = np.repeat(np.arange(ny), nx)
+    _, ix, iy = _nodes(grid, rows)
     roof = (iy + 1 == ny) & (ix >= grid.roof_begin) & (ix < grid.roof_end)
-    dre = np.full(nx * ny, 4.0 * k2 - omega * omega)
-    dim = np.zeros(nx * ny)
+    dre = np.full(len(ix), 4.0 * k2 - omega * omega)
+    dim = np.zeros(len(ix))
     for cond in (ix == 0, ix + 1 == nx, iy == 0, (iy + 1 == ny) & ~roof):
         dre = np.where(cond, dre - kw_re, dre)
         dim = np.where(cond, dim - kw_im, dim)
@@ -150,14 +159,16 @@ def values(grid: CavityGrid, omega: float, c: float, pat=None) -> np.ndarray:
     return v
 
 
-def rhs(grid: CavityGrid, c: float, dirichlet) -> np.ndarray:
+def rhs(grid: CavityGrid, c: float, dirichlet, rows=None) -> np.ndarray:
     """b: k^2 * dirichlet on the top row under the roof span (helmholtz.cpp:104-107)."""
     k2 = c * c / (grid.h * grid.h)
     d = np.asarray(dirichlet, np.complex128)
-    b = np.zeros(grid.size(), np.complex128)
+    r0, r1 = (0, grid.size()) if rows is None else (int(rows[0]), int(rows[1]))
+    b = np.zeros(r1 - r0, np.complex128)
     nodes = (grid.ny - 1) * grid.nx + np.arange(grid.roof_begin, grid.roof_end)
-    b.real[nodes] = 0.0 + k2 * d.real
-    b.imag[nodes] = 0.0 + k2 * d.imag
+    keep = (nodes >= r0) & (nodes < r1)
+    b.real[nodes[keep] - r0] = 0.0 + k2 * d.real[keep]
+    b.imag[nodes[keep] - r0] = 0.0 + k2 * d.imag[keep]
     return b
 
 
@@ -170,6 +181,17 @@ def assemble(grid: CavityGrid, omega: float, c: float, dirichlet) -> HelmholtzPr
     v = values(grid, omega, c, pat)
     A = CsrMatrix(grid.size(), grid.size(), pat[0], pat[1], v)
     return HelmholtzProblem(grid, omega, c, dirichlet, A, rhs(grid, c, dirichlet))
+
+
+def assemble_rows(grid: CavityGrid, omega: float, c: float, dirichlet, r0: int, r1: int):
+    """Rows [r0, r1) of assemble(): (row_offsets from 0, global columns,
+    values, rhs), bitwise the same rows of the global system, built without
+    the other rows (a rank's share of a distributed solve)."""
+    dirichlet = np.asarray(dirichlet, np.complex128)
+    if len(dirichlet) != grid.roof_size():
+        raise InvalidArgument("assemble: dirichlet length does not match roof span")
+    pat = pattern(grid, (r0, r1))
+    return pat[0], pat[1], values(grid, omega, c, pat, (r0, r1)), rhs(grid, c, dirichlet, (r0, r1))
 
 
 @dataclass

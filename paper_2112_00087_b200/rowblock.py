@@ -156,6 +156,67 @@ def plan_row_blocks(A: CsrMatrix, n_ranks: int, bounds: Optional[np.ndarray] = N
     return plans
 
 
+def plan_local_block(rank: int, bounds, row_offsets, cols_global, values,
+                     gather: Callable[[object], list]) -> RowBlockPlan:
+    """This rank's plan from its own rows only (the distributed setup: no rank
+    holds the global matrix).  Each rank derives its halo from its rows'
+    columns; one all-gather of the halo lists (gather(obj) -> every rank's
+    obj, e.g. torch.distributed.all_gather_object) tells every rank which of
+    its rows the others read, and every owner's send list.  Bitwise the plan
+    plan_row_blocks computes from the global pattern."""
+    bounds = np.asarray(bounds, np.int64)
+    n_ranks = len(bounds) - 1
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    c = np.asarray(cols_global, np.int64)
+    ext = (c < r0) | (c >= r1)
+    halo = np.unique(c[ext])
+    loc = c - r0
+    loc[ext] = (r1 - r0) + np.searchsorted(halo, c[ext])
+    halos = gather(halo)
+    owner_of = lambda g: np.searchsorted(bounds, g, side="right") - 1  # noqa: E731
+    needed = [[] for _ in range(n_ranks)]
+    for q in range(n_ranks):
+        own = owner_of(halos[q])
+        for o in np.unique(own):
+            needed[int(o)].append(halos[q][own == o])
+    sends = [np.unique(np.concatenate(v)) - bounds[o] if v else np.zeros(0, np.int64)
+             for o, v in enumerate(needed)]
+    max_send = max([len(x) for x in sends] + [0])
+    own = owner_of(halo)
+    src = np.zeros(len(halo), np.int64)
+    for o in np.unique(own):
+        m = own == o
+        src[m] = int(o) * max_send + np.searchsorted(sends[int(o)], halo[m] - bounds[o])
+    return RowBlockPlan(rank, n_ranks, r0, r1, np.asarray(row_offsets, np.int64), loc,
+                        np.asarray(values, np.complex128), halo, sends[rank].astype(np.int64), max_send, src)
+
+
+def local_jacobi(r0: int, row_offsets, cols_global, values) -> np.ndarray:
+    """Inverse diagonal of a rank's own rows (jacobi, krylov.cpp:31-55: the
+    first stored entry with col == row, inverted on the device with the
+    reference's __divdc3 rounding); zero or missing -> InvalidArgument naming
+    the global row, as the reference does."""
+    rp = np.asarray(row_offsets, np.int64)
+    c = np.asarray(cols_global, np.int64)
+    v = np.asarray(values, np.complex128)
+    n = len(rp) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    hit = np.nonzero(c == rows + r0)[0]
+    first = np.full(n, -1, np.int64)
+    first[rows[hit][::-1]] = hit[::-1]  # first col == row entry of each row
+    d = np.zeros(n, np.complex128)
+    ok = first >= 0
+    d[ok] = v[first[ok]]
+    ar = np.arange(n, dtype=np.uint64)
+    D = CsrMatrix(n, n, np.arange(n + 1, dtype=np.uint64), ar, d)
+    from .cavac import jacobi
+    try:
+        return jacobi(D).inv_diag
+    except InvalidArgument as e:
+        row = int(str(e).rsplit(" ", 1)[-1])
+        raise InvalidArgument(f"jacobi: zero diagonal at row {row + r0}") from None
+
+
 # ------------------------------------------------ geometric partitioning --
 
 def rcb_partition(coords, n_parts: int) -> np.ndarray:

@@ -7,7 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-GOLDEN = os.path.join(ROOT, "tests", "golden")
+GOLDEN = os.path.join(ROOT, "tests", "golden")  # the reference's own fixtures, byte for byte
+FIXTURES = os.path.join(ROOT, "tests", "fixtures")  # fixtures made here from the reference (tools/)
 
 
 def pytest_configure(config):

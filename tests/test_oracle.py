@@ -7,7 +7,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
+from conftest import FIXTURES, GOLDEN
 
 H_GOLDEN = 0.05
 OMEGA_GOLDEN = 2.0 * math.pi * 74.21875  # proj/tests/golden/dominant.csv:2
@@ -122,3 +122,25 @@ def test_restatement_equals_reference_bitwise(oracle, golden):
         xo, ro = oracle.solve(s, rp, ci, v, b)
         xr, rr = oracle.ref_solve(s, rp, ci, v, b)
         assert np.array_equal(xo.view(np.uint64), xr.view(np.uint64))
+
+
+def test_breakdown_fixture_pinned(oracle):
+    """tests/golden/breakdowns.json: the C restatement (and, where it is
+    built, the reference itself) reproduces every recorded breakdown."""
+    import hashlib
+    import json
+    cases = json.load(open(os.path.join(FIXTURES, "breakdowns.json")))
+    assert {c["breakdown"] for c in cases.values()} == {
+        "rho breakdown", "stagnation in <shadow, v>", "omega breakdown", "stagnation in <shadow, u>",
+        "degenerate least-squares in MR step", "sigma breakdown"}
+    for c in cases.values():
+        v = np.array([complex(a, b) for a, b in c["v"]])
+        b = np.array([complex(a, b_) for a, b_ in c["b"]])
+        runs = [oracle.solve(c["solver"], c["rp"], c["ci"], v, b, tol=c["tol"], max_iter=c["max_iter"], l=c["l"])]
+        if oracle.ref_available():
+            runs.append(oracle.ref_solve(c["solver"], c["rp"], c["ci"], v, b, tol=c["tol"],
+                                         max_iter=c["max_iter"], l=c["l"]))
+        for x, rep in runs:
+            assert rep.breakdown == c["breakdown"] and rep.iterations == c["iterations"]
+            assert rep.final_relres.hex() == c["final_relres"]
+            assert hashlib.sha256(np.ascontiguousarray(x).view(np.uint8)).hexdigest() == c["x_sha256"]

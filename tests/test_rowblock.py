@@ -194,3 +194,58 @@ def test_permute_system_is_similarity():
         assert np.all(np.diff(c) > 0)
         Dp[i, c] = v2[rp2[i]:rp2[i + 1]]
     assert np.array_equal(Dp, D[np.ix_(perm, perm)])
+
+
+def _local_plan_worker(rank, world, port, h, out_dir):
+    """One rank of the bench's rank-local setup (bench.py run_rowblock): its
+    own rows of the cavity, its plan from one gloo all-gather of halo lists."""
+    import pickle
+
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    from paper_2112_00087_b200 import helmholtz as H
+    from paper_2112_00087_b200.rowblock import plan_local_block
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = H.build_grid(2.4, 1.2, h, 0.4, 0.65, 0.01)
+    n = g.size()
+    bounds = np.array([(q * n) // world for q in range(world + 1)], np.int64)
+    d = np.ones(g.roof_size(), np.complex128)
+    rp, cols, vals, b = H.assemble_rows(g, 2 * np.pi * 100.0, 340.0, d, int(bounds[rank]), int(bounds[rank + 1]))
+
+    def gather(obj):
+        res = [None] * world
+        dist.all_gather_object(res, obj)
+        return res
+
+    plan = plan_local_block(rank, bounds, rp, cols, vals, gather)
+    with open(os.path.join(out_dir, f"plan{rank}.pkl"), "wb") as f:
+        pickle.dump((plan, b), f)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_local_setup_matches_global_plan(tmp_path, world):
+    """bench.py's N > 1 setup on gloo ranks: every rank assembles only its own
+    rows and plans its halo from an all-gather of halo lists; the plans and
+    right-hand sides equal the global assemble + plan_row_blocks bit for bit."""
+    import pickle
+
+    import torch.multiprocessing as mp
+    from paper_2112_00087_b200 import helmholtz as H
+    from paper_2112_00087_b200.rowblock import plan_row_blocks
+    h = 0.05
+    mp.spawn(_local_plan_worker, args=(world, _free_port(), h, str(tmp_path)), nprocs=world, join=True)
+    g = H.build_grid(2.4, 1.2, h, 0.4, 0.65, 0.01)
+    p = H.assemble(g, 2 * np.pi * 100.0, 340.0, np.ones(g.roof_size(), np.complex128))
+    n = g.size()
+    bounds = np.array([(q * n) // world for q in range(world + 1)], np.int64)
+    ref = plan_row_blocks(p.A, world, bounds)
+    for q in range(world):
+        plan, b = pickle.load(open(tmp_path / f"plan{q}.pkl", "rb"))
+        r = ref[q]
+        assert (plan.r0, plan.r1, plan.max_send) == (r.r0, r.r1, r.max_send)
+        for f in ("row_offsets", "col_local", "halo_cols", "send_rows", "halo_src"):
+            assert np.array_equal(getattr(plan, f), getattr(r, f)), f
+        assert np.array_equal(plan.values.view(np.uint64), r.values.view(np.uint64))
+        assert np.array_equal(b.view(np.uint64), np.asarray(p.b[r.r0:r.r1]).view(np.uint64))

@@ -21,7 +21,7 @@ import numpy as np  # noqa: E402
 import paper_2112_00087_b200 as P  # noqa: E402
 from paper_2112_00087_b200 import helmholtz as H  # noqa: E402
 
-PIN = json.load(open(os.path.join(ROOT, "tests", "golden", "configs_ref.json")))
+PIN = json.load(open(os.path.join(ROOT, "tests", "fixtures", "configs_ref.json")))
 
 
 def system(name):

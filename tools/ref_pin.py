@@ -30,7 +30,7 @@ import numpy as np  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "configs_ref.json")
+OUT = os.path.join(ROOT, "tests", "fixtures", "configs_ref.json")
 BIG = os.path.join(ROOT, "tests", "_big")
 
 SYSTEMS = {
@@ -53,6 +53,7 @@ def cases():
             out[f"c1_{solver}_{tol:.0e}"] = ("c1", solver, tol, 40000)
     out["c2_bicgstab_1e-08"] = ("c2", "bicgstab", 1e-8, 20000)
     out["c2_bicgstab_1e-12"] = ("c2", "bicgstab", 1e-12, 40000)
+    out["c2_tfqmr_1e-12"] = ("c2", "tfqmr", 1e-12, 40000)
     return out
 
 
