@@ -59,11 +59,13 @@ extern "C" {
 #define CVK_ELOGIC -7      /* std::logic_error in the reference */
 #define CVK_ETIMEOUT -8    /* device grid barrier timed out (never expected) */
 
-/* solver ids: the reference's SolverId order (krylov.hpp:63) + GMRES */
+/* solver ids: the reference's SolverId order (krylov.hpp:63) + GMRES, COCG */
 #define CVK_BICGSTAB 0
 #define CVK_BICGSTAB_L 1
 #define CVK_TFQMR 2
 #define CVK_GMRES 3 /* beyond reference: restarted GMRES(m) */
+#define CVK_COCG 4  /* beyond reference: conjugate orthogonal CG for the
+                       complex-symmetric operator (oracle orc_cocg) */
 
 /* arithmetic modes */
 #define CVK_MODE_FAST 0     /* double-double reductions, streamed SpMV (the product) */
@@ -84,6 +86,7 @@ extern "C" {
 #define CVK_BRK_MR 5         /* "degenerate least-squares in MR step" */
 #define CVK_BRK_SIGMA 6      /* "sigma breakdown" */
 #define CVK_BRK_ARNOLDI 7    /* "arnoldi breakdown" (GMRES) */
+#define CVK_BRK_PAP 8        /* "stagnation in <p, A p>" (COCG) */
 
 typedef struct cvk_ctx cvk_ctx;
 typedef struct cvk_csr cvk_csr;

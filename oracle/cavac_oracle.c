@@ -17,9 +17,10 @@
  * (ac-bd, ad+bc) and complex division through libgcc __divdc3 -- the same
  * helper std::complex<double> uses.  C99 `double complex` reaches both.
  *
- * GMRES(m) is NOT in the reference (krylov.cpp:377-384 rejects "gmres"); the
- * restatement here is the beyond-reference oracle for the device GMRES and is
- * parity-unpinned except through the solution of the same system.
+ * GMRES(m) and COCG are NOT in the reference (krylov.cpp:377-384 rejects
+ * "gmres"); the restatements here are the beyond-reference oracles for the
+ * device GMRES / COCG and are parity-unpinned except through the solution of
+ * the same system.
  */
 #define _POSIX_C_SOURCE 200809L
 #include <complex.h>
@@ -40,7 +41,8 @@ enum {
     ORC_BRK_SHADOW_U = 4,   /* "stagnation in <shadow, u>" */
     ORC_BRK_MR = 5,         /* "degenerate least-squares in MR step" */
     ORC_BRK_SIGMA = 6,      /* "sigma breakdown" */
-    ORC_BRK_ARNOLDI = 7     /* "arnoldi breakdown" (gmres, beyond reference) */
+    ORC_BRK_ARNOLDI = 7,    /* "arnoldi breakdown" (gmres, beyond reference) */
+    ORC_BRK_PAP = 8         /* "stagnation in <p, A p>" (cocg, beyond reference) */
 };
 
 typedef struct {
@@ -153,8 +155,32 @@ void orc_spmv(const orc_csr *A, const cplx *x, cplx *y) {
     }
 }
 
+/* Summation mode of the reductions below: 0 = the reference's sequential
+ * sums (default); 1 = double-double (TwoSum per term), the FAST device
+ * arithmetic's near-exact sums -- used only by tools/find_breakdowns.py to
+ * keep the breakdown fixtures whose cancellation is exact in both. */
+static int g_sum_dd = 0;
+void orc_set_sum_mode(int dd) { g_sum_dd = dd; }
+
+static void dd_add(double *hi, double *lo, double x) {
+    double s = *hi + x, bb = s - *hi;
+    double e = (*hi - (s - bb)) + (x - bb);
+    e += *lo;
+    *hi = s + e;
+    *lo = e - (*hi - s);
+}
+
 /* dot_hermitian numkit.cpp:113-119: sum conj(x_i) y_i, sequential. */
 cplx orc_dot(int64_t n, const cplx *x, const cplx *y) {
+    if (g_sum_dd) {
+        double rh = 0, rl = 0, ih = 0, il = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            cplx t = conj(x[i]) * y[i];
+            dd_add(&rh, &rl, creal(t));
+            dd_add(&ih, &il, cimag(t));
+        }
+        return CMPLX(rh, ih);
+    }
     cplx acc = 0.0;
     for (int64_t i = 0; i < n; ++i) acc += conj(x[i]) * y[i];
     return acc;
@@ -167,6 +193,14 @@ void orc_dot_out(int64_t n, const cplx *x, const cplx *y, double *out) {
 
 /* norm2 numkit.cpp:121-125: sqrt(sum re^2 + im^2), sequential. */
 double orc_norm2(int64_t n, const cplx *x) {
+    if (g_sum_dd) {
+        double h = 0, l = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            double a = creal(x[i]), b = cimag(x[i]);
+            dd_add(&h, &l, a * a + b * b);
+        }
+        return sqrt(h);
+    }
     double acc = 0.0;
     for (int64_t i = 0; i < n; ++i) {
         double a = creal(x[i]), b = cimag(x[i]);
@@ -560,6 +594,73 @@ done_notrue:
 
 /* solve krylov.cpp:395-403 dispatch; solver ids shared with the C-ABI:
  * 0 bicgstab, 1 bicgstab_l, 2 tfqmr, 3 gmres (beyond reference). */
+/* udot: sum x_i y_i, unconjugated, sequential (the bilinear form of COCG). */
+static cplx orc_udot(int64_t n, const cplx *x, const cplx *y) {
+    if (g_sum_dd) {
+        double rh = 0, rl = 0, ih = 0, il = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            cplx t = x[i] * y[i];
+            dd_add(&rh, &rl, creal(t));
+            dd_add(&ih, &il, cimag(t));
+        }
+        return CMPLX(rh, ih);
+    }
+    cplx acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += x[i] * y[i];
+    return acc;
+}
+
+/* COCG (conjugate orthogonal CG, van der Vorst & Melissen 1990) for the
+ * complex-symmetric Helmholtz operator A = A^T -- NOT in the reference; the
+ * beyond-reference oracle of the device COCG, parity-unpinned except through
+ * the solution.  Written in the reference's conventions (krylov.cpp:57-138):
+ * x0 = 0, Jacobi M (symmetric), relres = ||M^-1 r|| / ||M^-1 b||, breakdown
+ * threshold 1e-30 ||M^-1 b||^2.
+ *   r = b, z = M^-1 r, p = z, rho = r^T z
+ *   per iteration: q = A p; mu = p^T q; alpha = rho / mu; x += alpha p;
+ *                  r -= alpha q; z = M^-1 r; relres test;
+ *                  rho' = r^T z; beta = rho' / rho; p = z + beta p */
+void orc_cocg(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o, cplx *x,
+              orc_report *rep) {
+    double t0 = now_s();
+    int64_t n = A->n;
+    orc_op op = {A, dinv};
+    memset(x, 0, (size_t)n * sizeof(cplx));
+    cplx *r = cvec(n), *z = cvec(n), *p = cvec(n), *q = cvec(n);
+    memcpy(r, b, (size_t)n * sizeof(cplx));
+    prec_apply(&op, r, z);
+    double bnorm = orc_norm2(n, z);
+    if (bnorm == 0.0) { rep->converged = 1; goto done_notrue; }
+    double brk = 1e-30 * bnorm * bnorm;
+    cplx rho = orc_udot(n, r, z);
+    for (int64_t it = 1; it <= o->max_iter; ++it) {
+        if (cabs(rho) < brk) { rep->breakdown = ORC_BRK_RHO; rep->iterations = it - 1; break; }
+        if (it == 1) {
+            memcpy(p, z, (size_t)n * sizeof(cplx));
+        }
+        orc_spmv(A, p, q);
+        cplx mu = orc_udot(n, p, q);
+        if (cabs(mu) < brk) { rep->breakdown = ORC_BRK_PAP; rep->iterations = it - 1; break; }
+        cplx alpha = rho / mu;
+        orc_axpy(n, alpha, p, x);
+        orc_axpy(n, -alpha, q, r);
+        prec_apply(&op, r, z);
+        double relres = orc_norm2(n, z) / bnorm;
+        rep->final_relres = relres;
+        rep->iterations = it;
+        hist_push(rep, o, relres);
+        if (relres <= o->tol) { rep->converged = 1; break; }
+        cplx rho_new = orc_udot(n, r, z);
+        cplx beta = rho_new / rho;
+        rho = rho_new;
+        orc_xpay(n, beta, p, z); /* p = beta p + z */
+    }
+    rep->true_relres = orc_true_relres(A, b, x);
+done_notrue:
+    rep->wall_time_s = now_s() - t0;
+    free(r); free(z); free(p); free(q);
+}
+
 int orc_solve(int solver, int64_t n, const int64_t *rp, const int64_t *ci, const cplx *v,
               const cplx *dinv, const cplx *b, const orc_opts *o, cplx *x, orc_report *rep) {
     orc_csr A = {n, rp, ci, v};
@@ -570,6 +671,7 @@ int orc_solve(int solver, int64_t n, const int64_t *rp, const int64_t *ci, const
         case 1: if (o->l < 1) return -2; orc_bicgstab_l(&A, dinv, b, o, x, rep); return 0;
         case 2: orc_tfqmr(&A, dinv, b, o, x, rep); return 0;
         case 3: orc_gmres(&A, dinv, b, o, x, rep); return 0;
+        case 4: orc_cocg(&A, dinv, b, o, x, rep); return 0;
     }
     return -1;
 }

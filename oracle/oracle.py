@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 REF_PATH = os.path.join(HERE, "_ref", "libcavac_ref.so")
 
-SOLVERS = {"bicgstab": 0, "bicgstab_l": 1, "tfqmr": 2, "gmres": 3}
+SOLVERS = {"bicgstab": 0, "bicgstab_l": 1, "tfqmr": 2, "gmres": 3, "cocg": 4}
 BREAKDOWN = {
     0: None,
     1: "rho breakdown",
@@ -28,6 +28,7 @@ BREAKDOWN = {
     5: "degenerate least-squares in MR step",
     6: "sigma breakdown",
     7: "arnoldi breakdown",
+    8: "stagnation in <p, A p>",
 }
 
 
@@ -110,6 +111,7 @@ def lib():
         L = _lib
         P = C.c_void_p
         L.orc_solve.argtypes = [C.c_int, C.c_int64, P, P, P, P, P, C.POINTER(_Opts), P, C.POINTER(_Report)]
+        L.orc_set_sum_mode.argtypes = [C.c_int]
         L.orc_solve.restype = C.c_int
         L.orc_jacobi_arrays.argtypes = [C.c_int64, P, P, P, P]
         L.orc_jacobi_arrays.restype = C.c_int64

@@ -6,7 +6,7 @@ CUDA behind the C ABI in include/cavac_b200.h).
 """
 from .cavac import (  # noqa: F401
     CsrMatrix, Device, ExecMode, InvalidArgument, LogicError, Preconditioner, SolveReport,
-    SolveResult, SolverId, SolverOptions, axpy, axpy_inplace, bicgstab, bicgstab_l,
+    SolveResult, SolverId, SolverOptions, axpy, axpy_inplace, bicgstab, bicgstab_l, cocg,
     csr_from_triplets, csr_identity, dot_hermitian, exec_mode, gmres, identity_preconditioner, ilu0,
     ilu0_factor,
     jacobi, norm2, path_options, scale_inplace, set_exec_mode, solve, solver_from_name, solver_id,

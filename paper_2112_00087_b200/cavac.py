@@ -53,10 +53,11 @@ class SolverId(enum.IntEnum):
     BiCGStabL = 1
     TfQmr = 2
     GMRES = 3  # beyond the reference
+    COCG = 4  # beyond the reference: conjugate orthogonal CG (complex-symmetric A)
 
 
 _NAMES = {SolverId.BiCGStab: "bicgstab", SolverId.BiCGStabL: "bicgstab_l",
-          SolverId.TfQmr: "tfqmr", SolverId.GMRES: "gmres"}
+          SolverId.TfQmr: "tfqmr", SolverId.GMRES: "gmres", SolverId.COCG: "cocg"}
 
 
 def solver_name(sid: SolverId) -> str:
@@ -74,11 +75,11 @@ def solver_from_name(name: str) -> SolverId:
 
 
 def solver_id(name: str) -> SolverId:
-    """solver_from_name plus the B200 extensions ("gmres")."""
+    """solver_from_name plus the B200 extensions ("gmres", "cocg")."""
     for k, v in _NAMES.items():
         if v == name:
             return k
-    raise InvalidArgument(f'unknown solver "{name}" (allowed: bicgstab, bicgstab_l, tfqmr, gmres)')
+    raise InvalidArgument(f'unknown solver "{name}" (allowed: bicgstab, bicgstab_l, tfqmr, gmres, cocg)')
 
 
 # ------------------------------------------------------------- device ----
@@ -454,7 +455,7 @@ def ilu0_factor(M: Preconditioner) -> np.ndarray:
 
 _BRK = {0: None, 1: "rho breakdown", 2: "stagnation in <shadow, v>", 3: "omega breakdown",
         4: "stagnation in <shadow, u>", 5: "degenerate least-squares in MR step",
-        6: "sigma breakdown", 7: "arnoldi breakdown"}
+        6: "sigma breakdown", 7: "arnoldi breakdown", 8: "stagnation in <p, A p>"}
 
 
 def _opts(o: SolverOptions, mode: Optional[ExecMode]) -> CvkOpts:
@@ -512,6 +513,13 @@ def tfqmr(A, b, M, opts=None, mode=None):
 
 def gmres(A, b, M, opts=None, mode=None):
     return solve(SolverId.GMRES, A, b, M, opts, mode)
+
+
+def cocg(A, b, M, opts=None, mode=None):
+    """Conjugate orthogonal CG (beyond the reference; north_star's CG for the
+    complex-symmetric Helmholtz operator A = A^T): one SpMV per iteration,
+    the reference's conventions (x0 = 0, Jacobi, relres = ||M^-1 r|| / ||M^-1 b||)."""
+    return solve(SolverId.COCG, A, b, M, opts, mode)
 
 
 def true_relative_residual(A: CsrMatrix, b, x, mode: Optional[ExecMode] = None) -> float:

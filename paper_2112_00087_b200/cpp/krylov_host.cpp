@@ -47,7 +47,7 @@ namespace {
 
 const char* kBreak[] = {"", "rho breakdown", "stagnation in <shadow, v>", "omega breakdown",
                         "stagnation in <shadow, u>", "degenerate least-squares in MR step", "sigma breakdown",
-                        "arnoldi breakdown"};
+                        "arnoldi breakdown", "stagnation in <p, A p>"};
 
 SolveResult device_solve(int solver, const char* name, const CsrMatrix& A, const CVector& b,
                          const Preconditioner& M, const SolverOptions& opts) {
@@ -88,7 +88,7 @@ SolveResult device_solve(int solver, const char* name, const CsrMatrix& A, const
     rep.device_time = r.device_time_s;
     if (opts.record_history)
         rep.residual_history.assign(hist.begin(), hist.begin() + std::min<int64_t>(r.history_len, r.history_cap));
-    if (r.breakdown > 0 && r.breakdown < 8) rep.breakdown = kBreak[r.breakdown];
+    if (r.breakdown > 0 && r.breakdown < 9) rep.breakdown = kBreak[r.breakdown];
     rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return res;
 }
@@ -107,6 +107,9 @@ SolveResult tfqmr(const CsrMatrix& A, const CVector& b, const Preconditioner& M,
 SolveResult gmres(const CsrMatrix& A, const CVector& b, const Preconditioner& M, const SolverOptions& o) {
     return device_solve(CVK_GMRES, "gmres", A, b, M, o);
 }
+SolveResult cocg(const CsrMatrix& A, const CVector& b, const Preconditioner& M, const SolverOptions& o) {
+    return device_solve(CVK_COCG, "cocg", A, b, M, o);
+}
 
 SolverId solver_from_name(const std::string& name) {
     if (name == "bicgstab") return SolverId::BiCGStab;
@@ -121,6 +124,7 @@ std::string solver_name(SolverId id) {
         case SolverId::BiCGStabL: return "bicgstab_l";
         case SolverId::TfQmr: return "tfqmr";
         case SolverId::GMRES: return "gmres";
+        case SolverId::COCG: return "cocg";
     }
     return "?";
 }
@@ -132,6 +136,7 @@ SolveResult solve(SolverId id, const CsrMatrix& A, const CVector& b, const Preco
         case SolverId::BiCGStabL: return bicgstab_l(A, b, M, opts);
         case SolverId::TfQmr: return tfqmr(A, b, M, opts);
         case SolverId::GMRES: return gmres(A, b, M, opts);
+        case SolverId::COCG: return cocg(A, b, M, opts);
     }
     throw std::logic_error("solve: unreachable");
 }

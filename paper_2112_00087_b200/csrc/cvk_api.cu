@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cavac_b200.h"
@@ -94,7 +95,45 @@ struct cvk_ctx {
     int warm_next = 0;
     cudaGraphExec_t bl_exec = nullptr;
     std::vector<unsigned char> bl_key;
+    // device blocks released by cvk_csr_free / cvk_precond_free, reused by
+    // the next upload of a similar size: a reference caller runs jacobi +
+    // solve per call (pipeline.cpp:196-202), i.e. uploads and frees A each
+    // time, and cudaMalloc / cudaFree of ~100 MB cost milliseconds each
+    std::vector<std::pair<void*, size_t>> spare;
+    size_t spare_bytes = 0;
 };
+
+static constexpr size_t kSpareCap = size_t(4) << 30;
+
+static cudaError_t ctx_alloc(cvk_ctx* c, void** p, size_t bytes) {
+    int best = -1;
+    for (int i = 0; i < (int)c->spare.size(); ++i) {
+        const size_t b = c->spare[i].second;
+        if (b >= bytes && b - bytes <= bytes / 4 + (size_t(1) << 20) &&
+            (best < 0 || b < c->spare[best].second))
+            best = i;
+    }
+    if (best >= 0) {
+        *p = c->spare[best].first;
+        c->spare_bytes -= c->spare[best].second;
+        c->spare.erase(c->spare.begin() + best);
+        return cudaSuccess;
+    }
+    return cudaMalloc(p, bytes);
+}
+
+// returns the block's real size through *bytes_out when it came from the cache
+static void ctx_release(cvk_ctx* c, void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes > kSpareCap) { cudaFree(p); return; }
+    c->spare.emplace_back(p, bytes);
+    c->spare_bytes += bytes;
+    while (c->spare_bytes > kSpareCap && !c->spare.empty()) {
+        cudaFree(c->spare.front().first);
+        c->spare_bytes -= c->spare.front().second;
+        c->spare.erase(c->spare.begin());
+    }
+}
 
 struct cvk_csr {
     cvk_ctx* ctx = nullptr;
@@ -135,7 +174,7 @@ int fail(int code, const std::string& msg) {
                         std::string(#call) + ": " + cudaGetErrorString(e_));         \
     } while (0)
 
-const char* kSolverNames[] = {"bicgstab", "bicgstab_l", "tfqmr", "gmres"};
+const char* kSolverNames[] = {"bicgstab", "bicgstab_l", "tfqmr", "gmres", "cocg"};
 
 int pick_group(const cvk_ctx* c, double avg_nnz) {
     const long long v = c->knob.spmv_group;
@@ -211,21 +250,22 @@ const char* cvk_breakdown_name(int code) {
         case CVK_BRK_MR: return "degenerate least-squares in MR step";
         case CVK_BRK_SIGMA: return "sigma breakdown";
         case CVK_BRK_ARNOLDI: return "arnoldi breakdown";
+        case CVK_BRK_PAP: return "stagnation in <p, A p>";
     }
     return "unknown breakdown";
 }
 
 const char* cvk_solver_name(int solver) {
-    if (solver < 0 || solver > 3) return "?";
+    if (solver < 0 || solver > 4) return "?";
     return kSolverNames[solver];
 }
 
 int cvk_solver_from_name(const char* name) {
     if (name)
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 5; ++i)
             if (std::strcmp(name, kSolverNames[i]) == 0) return i;
     return fail(CVK_ESOLVER, std::string("unknown solver \"") + (name ? name : "") +
-                                 "\" (allowed: bicgstab, bicgstab_l, tfqmr, gmres)");
+                                 "\" (allowed: bicgstab, bicgstab_l, tfqmr, gmres, cocg)");
 }
 
 int cvk_ctx_create(int device, cvk_ctx** out) {
@@ -284,6 +324,7 @@ int cvk_ctx_destroy(cvk_ctx* c) {
     if (c->gm_exec) cudaGraphExecDestroy(c->gm_exec);
     cudaFree(c->gst);
     if (c->bl_exec) cudaGraphExecDestroy(c->bl_exec);
+    for (auto& sp : c->spare) cudaFree(sp.first);
     cudaFree(c->bst);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -332,10 +373,22 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
         rp[(size_t)i] = (int)row_offsets[i];
     }
     if (row_offsets[nrows] != (uint64_t)nnz) return fail(CVK_EINVAL, "cvk_csr_upload: row_offsets[n] != nnz");
-    for (int64_t k = 0; k < nnz; ++k) {
-        if (col_indices[k] >= (uint64_t)ncols)
-            return fail(CVK_EINVAL, "cvk_csr_upload: column index out of range at " + std::to_string(k));
-        ci[(size_t)k] = (int)col_indices[k];
+    {
+        // narrow the columns on all host cores (5M entries per 1M DOF)
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(16, nnz / (1 << 18)));
+        std::vector<int64_t> bad((size_t)nt, -1);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                const int64_t k0 = nnz * t / nt, k1 = nnz * (t + 1) / nt;
+                for (int64_t k = k0; k < k1; ++k) {
+                    if (col_indices[k] >= (uint64_t)ncols) { bad[(size_t)t] = k; return; }
+                    ci[(size_t)k] = (int)col_indices[k];
+                }
+            });
+        for (auto& t : th) t.join();
+        for (int64_t k : bad)
+            if (k >= 0) return fail(CVK_EINVAL, "cvk_csr_upload: column index out of range at " + std::to_string(k));
     }
     CK(cudaSetDevice(c->device));
     cvk_csr* A = new cvk_csr();
@@ -350,7 +403,7 @@ int cvk_csr_upload(cvk_ctx* c, int64_t nrows, int64_t ncols, int64_t nnz, const 
     const size_t cb = (sizeof(int) * (size_t)std::max<int64_t>(1, nnz) + 255) & ~(size_t)255;
     // 16 bytes of padding: the streamed kernels copy row offsets in 16-byte units
     const size_t rb = sizeof(int) * rp.size() + 16;
-    CK(cudaMalloc(&A->blob, vb + cb + rb));
+    CK(ctx_alloc(c, &A->blob, vb + cb + rb));
     A->blob_bytes = vb + cb + rb;
     A->av = (double2*)A->blob;
     A->ci = (int*)((char*)A->blob + vb);
@@ -409,7 +462,7 @@ int cvk_csr_free(cvk_csr* A) {
     if (!A) return CVK_OK;
     cudaSetDevice(A->ctx->device);
     cudaStreamSynchronize(A->ctx->stream);
-    cudaFree(A->blob);
+    ctx_release(A->ctx, A->blob, A->blob_bytes);
     if (A->cmax) cudaFree(A->cmax);
     delete A;
     return CVK_OK;
@@ -425,7 +478,7 @@ int cvk_precond_jacobi(cvk_csr* A, const double* inv_diag, cvk_prec** out) {
     cvk_prec* M = new cvk_prec();
     M->ctx = c;
     M->n = A->n;
-    CK(cudaMalloc(&M->dinv, sizeof(double2) * std::max<int64_t>(1, A->n)));
+    CK(ctx_alloc(c, (void**)&M->dinv, sizeof(double2) * std::max<int64_t>(1, A->n)));
     if (inv_diag) {
         CK(cudaMemcpyAsync(M->dinv, inv_diag, sizeof(double2) * A->n, cudaMemcpyHostToDevice, c->stream));
     } else {
@@ -542,7 +595,8 @@ int cvk_precond_free(cvk_prec* M) {
     if (!M) return CVK_OK;
     if (M->dinv) {
         cudaSetDevice(M->ctx->device);
-        cudaFree(M->dinv);
+        cudaStreamSynchronize(M->ctx->stream);
+        ctx_release(M->ctx, M->dinv, sizeof(double2) * std::max<int64_t>(1, M->n));
     }
     if (M->ilu) {
         cudaSetDevice(M->ctx->device);
@@ -972,6 +1026,27 @@ static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* 
 // lazily polled device `done` flag -> (tfQMR x fix-up) -> true residual.
 static constexpr int kIterPerGraph = 8;
 
+// Install a freshly captured graph as *exec: update the cached executable in
+// place when only kernel parameters changed (new matrix / vector pointers of
+// the same shapes -- every jacobi + solve of a reference caller uploads A
+// anew), instantiate otherwise.  Consumes `graph`.
+static cudaError_t install_graph(cudaGraphExec_t* exec, cudaGraph_t graph) {
+    cudaError_t e = cudaSuccess;
+    if (*exec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(*exec, graph, &info) == cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return cudaSuccess;
+        }
+        (void)cudaGetLastError();
+        cudaGraphExecDestroy(*exec);
+        *exec = nullptr;
+    }
+    e = cudaGraphInstantiate(exec, graph, 0);
+    cudaGraphDestroy(graph);
+    return e;
+}
+
 // cudaLaunchKernel with the programmatic-stream-serialization attribute (PDL)
 static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
@@ -1037,25 +1112,27 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // streamed (TMA ring) SpMV phases when a 256-row chunk fits >= 2 stages
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    // per kernel: staged vectors, gathered vectors (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s)
-    const int kvec[4] = {5, 5, 7, 8}, kgat[4] = {3, 2, 2, 2};
+    // per kernel: staged vectors, gathered vectors (k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_cg_a_s)
+    const int kvec[5] = {5, 5, 7, 8, 2}, kgat[5] = {3, 2, 2, 2, 2};
     auto layout_for = [&](int k, int stg) {
         cvk::StreamLayout L{A->capk, kvec[k], stg};
         L.ngather = kgat[k];
         return L;
     };
     auto stage_bytes_k = [&](int k) { return g4 ? stage_bytes(kvec[k], kgat[k]) : layout_for(k, 1).stage_bytes(); };
-    int stg[4];
-    for (int k = 0; k < 4; ++k) {
+    int stg[5];
+    for (int k = 0; k < 5; ++k) {
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
         stg[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));  // 4: measured best
     }
     const bool streamed = c->knob.stream && A->nnz > 0 &&
-                          (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2 : std::min(stg[2], stg[3]) >= 2);
+                          (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2
+                           : solver == CVK_COCG   ? stg[4] >= 2
+                                                  : std::min(stg[2], stg[3]) >= 2);
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
-    const void* sk[4] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s};
+    const void* sk[5] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // elementwise phases: grid-stride, 4 elements per thread per trip
@@ -1087,12 +1164,15 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
-        if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const dim3 sgrid((unsigned)c->nsm), sblock((unsigned)sthreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
-            if (solver == CVK_BICGSTAB) {
+            if (solver == CVK_COCG) {
+                if (streamed) launch_pdl(K.cg_a_s, sgrid, sblock, args, smem_for(4), c->stream);
+                else launch_pdl(K.cg_a, grid, block, args, smem, c->stream);
+                launch_pdl(K.cg_b, egrid, block, args, 0, c->stream);
+            } else if (solver == CVK_BICGSTAB) {
                 if (streamed) {
                     launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(0), c->stream);
                     launch_pdl(K.bi_b_s, sgrid, sblock, args, smem_for(1), c->stream);
@@ -1114,15 +1194,14 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         }
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
-        CK(cudaGraphInstantiate(&c->gexec, graph, 0));
-        cudaGraphDestroy(graph);
+        CK(install_graph(&c->gexec, graph));
         c->gkey = key;
     }
     CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->e0, c->stream));
     long long launches = 0;
-    if (solver == CVK_BICGSTAB) {
-        CK(launch_pdl(K.bi_init, grid, block, args, 0, c->stream));
+    if (solver == CVK_BICGSTAB || solver == CVK_COCG) {
+        CK(launch_pdl(solver == CVK_COCG ? K.cg_init : K.bi_init, grid, block, args, 0, c->stream));
         launches += 1;
     } else {
         CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
@@ -1138,7 +1217,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaMemcpyAsync(&c->h_done[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += 3 * kIterPerGraph;
+        launches += (solver == CVK_COCG ? 2 : 3) * kIterPerGraph;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));
@@ -1227,7 +1306,6 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     key.insert(key.end(), gp, gp + sizeof(G));
     key.push_back((unsigned char)(ud ? 1 : 0));
     if (!c->gm_exec || c->gm_key != key) {
-        if (c->gm_exec) { cudaGraphExecDestroy(c->gm_exec); c->gm_exec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < kIterPerGraph; ++it) {
@@ -1243,8 +1321,7 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
         }
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
-        CK(cudaGraphInstantiate(&c->gm_exec, graph, 0));
-        cudaGraphDestroy(graph);
+        CK(install_graph(&c->gm_exec, graph));
         c->gm_key = key;
     }
     CK(cudaMemcpyAsync(c->gst, hs.data(), hs.size(), cudaMemcpyHostToDevice, c->stream));
@@ -1328,14 +1405,12 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
     if (!c->bl_exec || c->bl_key != key) {
-        if (c->bl_exec) { cudaGraphExecDestroy(c->bl_exec); c->bl_exec = nullptr; }
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         for (int it = 0; it < kStepsPerGraph; ++it) launch_pdl(K.step, grid, block, args, 0, c->stream);
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
-        CK(cudaGraphInstantiate(&c->bl_exec, graph, 0));
-        cudaGraphDestroy(graph);
+        CK(install_graph(&c->bl_exec, graph));
         c->bl_key = key;
     }
     CK(cudaMemcpyAsync(c->bst, hs.data(), hs.size(), cudaMemcpyHostToDevice, c->stream));
@@ -1385,9 +1460,9 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
 
 static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* M, const cvk_opts* o,
                       const double2* b_dev, double2* x_dev, cvk_report* rep) {
-    if (solver < 0 || solver > 3)
+    if (solver < 0 || solver > 4)
         return fail(CVK_ESOLVER, "unknown solver id " + std::to_string(solver) +
-                                     " (allowed: bicgstab, bicgstab_l, tfqmr, gmres)");
+                                     " (allowed: bicgstab, bicgstab_l, tfqmr, gmres, cocg)");
     const char* nm = kSolverNames[solver];
     if (!A || !M || !o || !rep) return fail(CVK_EINVAL, std::string(nm) + ": null argument");
     if (M->n != A->n) return fail(CVK_EINVAL, std::string(nm) + ": dimension mismatch");
@@ -1415,7 +1490,7 @@ static int solve_impl(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec* 
     // per cycle on the cavity, 3007 vs 3085 on 3-D FEM)
     if (!ref && solver == CVK_BICGSTAB_L && (long long)n >= pmin && !c->knob.bicgl_persistent)
         return solve_bicgl_phased(c, A, M, o, b_dev, x_dev, rep);
-    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR) && (long long)n >= pmin)
+    if (!ref && (solver == CVK_BICGSTAB || solver == CVK_TFQMR || solver == CVK_COCG) && (long long)n >= pmin)
         return solve_phased(c, solver, A, M, o, b_dev, x_dev, rep);
     const int S = ref ? 1 : A->group;
     const void* kern = cvk::solver_kernel(solver, S, ref);

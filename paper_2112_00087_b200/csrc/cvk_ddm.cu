@@ -287,7 +287,7 @@ extern "C" int cvk_ddm_rank_create(cvk_ctx* ctx, const cvk_grid* grid, double c,
     if (!ctx || !grid || !row_offsets || !b || !col_begin || !s_left || !s_right || !inner || !out)
         return dfail(CVK_EINVAL, "schwarz_solve: null argument");
     if (grid->nx * grid->ny != n) return dfail(CVK_EINVAL, "schwarz_solve: grid does not match the system");
-    if (inner_solver < 0 || inner_solver > 3) return dfail(CVK_ESOLVER, "schwarz_solve: unknown inner solver");
+    if (inner_solver < 0 || inner_solver > 4) return dfail(CVK_ESOLVER, "schwarz_solve: unknown inner solver");
     if (n_sub < 2 || n_sub > 4096) return dfail(CVK_EINVAL, "schwarz_solve: n_sub out of range");
     if (s_begin < 0 || s_end > n_sub || s_begin >= s_end) return dfail(CVK_EINVAL, "ddm rank: bad strip range");
     (void)nnz;
@@ -620,7 +620,7 @@ extern "C" int cvk_schwarz_solve(cvk_ctx* ctx, const cvk_grid* grid, double c, i
     if (!ctx || !grid || !row_offsets || !b || !col_begin || !s_left || !s_right || !inner || !x || !rep)
         return dfail(CVK_EINVAL, "schwarz_solve: null argument");
     if (grid->nx * grid->ny != n) return dfail(CVK_EINVAL, "schwarz_solve: grid does not match the system");
-    if (inner_solver < 0 || inner_solver > 3) return dfail(CVK_ESOLVER, "schwarz_solve: unknown inner solver");
+    if (inner_solver < 0 || inner_solver > 4) return dfail(CVK_ESOLVER, "schwarz_solve: unknown inner solver");
     rep->outer_iterations = 0;
     rep->converged = 0;
     rep->inner_breakdown = 0;

@@ -519,6 +519,14 @@ __device__ __forceinline__ void acc_dot(CAcc& a, double2 x, double2 y) {
     dd_add1(a.hi.y, a.lo.y, t.y);
 }
 
+// unconjugated x^T y terms (COCG's bilinear form)
+__device__ __forceinline__ void acc_udot(double2& a, double2 x, double2 y) { a = cvk_add(a, cvk_mul(x, y)); }
+__device__ __forceinline__ void acc_udot(CAcc& a, double2 x, double2 y) {
+    const double2 t = cvk_mul(x, y);
+    dd_add1(a.hi.x, a.lo.x, t.x);
+    dd_add1(a.hi.y, a.lo.y, t.y);
+}
+
 __device__ __forceinline__ double2 prec_apply(const double2* dinv, int i, double2 y) {
     return dinv ? cvk_mul(__ldg(dinv + i), y) : y;
 }

@@ -22,6 +22,10 @@
 
 namespace cvk {
 
+// breakdown codes (include/cavac_b200.h CVK_BRK_*)
+constexpr int CVK_BRK_RHO_ = 1;
+constexpr int CVK_BRK_PAP_ = 8;
+
 namespace {
 
 __device__ __forceinline__ void write_report(const KArgs& a, int cta, int conv, int brk, long long it,
@@ -227,6 +231,110 @@ __device__ __forceinline__ void bicgstab_body(const KArgs& a, GridBar& g) {
     }
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, s, part[1], trr);
+    write_report(a, g.cta, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
+}
+
+// ==================================================================== COCG
+// Beyond the reference (oracle/cavac_oracle.c orc_cocg): conjugate orthogonal
+// CG for the complex-symmetric operator, in the reference's conventions (x0 =
+// 0, Jacobi, relres = ||M^-1 r|| / ||M^-1 b||, breakdown 1e-30 ||M^-1 b||^2).
+// One SpMV per iteration: phase A forms p = z + beta p inside the SpMV
+// gathers and takes mu = p^T A p; phase B updates x, r, z and takes ||z||^2,
+// r^T z.  work: r, z, q, p[2]
+template <int S, bool REF>
+__device__ __forceinline__ void cocg_body(const KArgs& a, GridBar& g) {
+    const int n = a.A.n, G = a.G;
+    const double2* __restrict__ dinv = a.dinv;
+    const double2* __restrict__ b = a.b;
+    double2* x = a.x;
+    double2* r = a.work;
+    double2* z = a.work + (size_t)n;
+    double2* q = a.work + 2 * (size_t)n;
+    double2* pv[2] = {a.work + 3 * (size_t)n, a.work + 4 * (size_t)n};
+    double2* part[kRegions];
+    for (int k = 0; k < kRegions; ++k) part[k] = a.part + (size_t)k * kMaxSlots * G;
+    long long hl = 0;
+
+    CAcc acc0[2] = {};
+    for_elems(n, G, g.cta, [&](int i) {
+        const double2 ri = __ldg(b + i);
+        const double2 zi = prec_apply(dinv, i, ri);
+        r[i] = ri;
+        z[i] = zi;
+        x[i] = make_double2(0.0, 0.0);
+        if (!REF) { acc_norm(acc0[0], zi); acc_udot(acc0[1], ri, zi); }
+    });
+    double2 t0[2];
+    if (!reduce<REF, 2>(g, acc0, t0, part[0], n, [&](int i, double2* qq) {
+            acc_norm(qq[0], z[i]);
+            acc_udot(qq[1], r[i], z[i]);
+        })) {
+        write_report(a, g.cta, 0, 0, 0, 0, 0, 0, 1);
+        return;
+    }
+    const double bnorm = sqrt(t0[0].x);
+    if (bnorm == 0.0) {
+        write_report(a, g.cta, 1, 0, 0, 0.0, 0.0, 0, 0);
+        return;
+    }
+    const double brk = 1e-30 * bnorm * bnorm;
+    double2 rho = t0[1], beta = make_double2(0, 0);
+    int conv = 0, brkc = 0, cur = 0;
+    long long iters = 0;
+    double final_relres = 0.0;
+    bool ok = true;
+    for (long long it = 1; it <= a.max_iter; ++it) {
+        if (cvk_abs(rho) < brk) { brkc = CVK_BRK_RHO_; iters = it - 1; break; }
+        const bool first = (it == 1);
+        const double2* pc = pv[cur];
+        double2* pn = pv[cur ^ 1];
+        auto pnew = [&](int c) -> double2 {
+            const double2 zc = z[c];
+            return first ? zc : cvk_add(cvk_mul(beta, pc[c]), zc);
+        };
+        // phase A: p = z + beta p, q = A p; mu = p^T q
+        CAcc accA[1] = {};
+        for_rows<S>(n, G, g.cta, [&](int row, int lane, bool valid) {
+            const double2 y = row_sum<S>(a.A, row, lane, valid, pnew);
+            if (valid && lane == 0) {
+                const double2 pi = pnew(row);
+                pn[row] = pi;
+                q[row] = y;
+                if (!REF) acc_udot(accA[0], pi, y);
+            }
+        });
+        double2 mu[1];
+        ok = reduce<REF, 1>(g, accA, mu, part[1], n, [&](int i, double2* qq) { acc_udot(qq[0], pn[i], q[i]); });
+        if (!ok) break;
+        if (cvk_abs(mu[0]) < brk) { brkc = CVK_BRK_PAP_; iters = it - 1; break; }
+        const double2 alpha = cvk_cdiv(rho, mu[0]), nal = cvk_neg(alpha);
+        // phase B: x += alpha p; r -= alpha q; z = M^-1 r; ||z||^2, r^T z
+        CAcc accB[2] = {};
+        for_elems(n, G, g.cta, [&](int i) {
+            x[i] = cvk_add(x[i], cvk_mul(alpha, pn[i]));
+            const double2 ri = cvk_add(r[i], cvk_mul(nal, q[i]));
+            const double2 zi = prec_apply(dinv, i, ri);
+            r[i] = ri;
+            z[i] = zi;
+            if (!REF) { acc_norm(accB[0], zi); acc_udot(accB[1], ri, zi); }
+        });
+        double2 tB[2];
+        ok = reduce<REF, 2>(g, accB, tB, part[2], n, [&](int i, double2* qq) {
+            acc_norm(qq[0], z[i]);
+            acc_udot(qq[1], r[i], z[i]);
+        });
+        if (!ok) break;
+        const double relres = sqrt(tB[0].x) / bnorm;
+        final_relres = relres;
+        iters = it;
+        hist_push(a, g.cta, hl, relres);
+        if (relres <= a.tol) { conv = 1; break; }
+        beta = cvk_cdiv(tB[1], rho);
+        rho = tB[1];
+        cur ^= 1;
+    }
+    double trr = 0.0;
+    if (ok) ok = true_relres<S, REF>(g, a, q, part[1], trr);
     write_report(a, g.cta, conv, brkc, iters, final_relres, trr, hl, ok ? 0 : 1);
 }
 
@@ -937,7 +1045,8 @@ __device__ __forceinline__ void run_body(const KArgs& a, GridBar& g) {
     if (SOLVER == 0) bicgstab_body<S, REF>(a, g);
     else if (SOLVER == 1) bicgstab_l_body<S, REF>(a, g);
     else if (SOLVER == 2) tfqmr_body<S, REF>(a, g);
-    else gmres_body<S, REF>(a, g);
+    else if (SOLVER == 3) gmres_body<S, REF>(a, g);
+    else cocg_body<S, REF>(a, g);
 }
 
 // one solve per cooperative launch
@@ -975,6 +1084,7 @@ static const void* pick(int solver, bool batched) {
         case 1: return batched ? (const void*)k_solve_batched<S, REF, 1> : (const void*)k_solve<S, REF, 1>;
         case 2: return batched ? (const void*)k_solve_batched<S, REF, 2> : (const void*)k_solve<S, REF, 2>;
         case 3: return batched ? (const void*)k_solve_batched<S, REF, 3> : (const void*)k_solve<S, REF, 3>;
+        case 4: return batched ? (const void*)k_solve_batched<S, REF, 4> : (const void*)k_solve<S, REF, 4>;
     }
     return nullptr;
 }
@@ -997,6 +1107,7 @@ int solver_nwork(int solver, int l, int m) {
         case 1: return 2 * l + 6;
         case 2: return 8;
         case 3: return m + 4;
+        case 4: return 5;
     }
     return 0;
 }

@@ -46,7 +46,7 @@ struct PArgs {
     double* hist;
     DevReport* rep;
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
-    int nst[4];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s
+    int nst[5];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_cg_a_s
     int pf_rows;        // StreamLayout::pf_rows (L2 prefetch of the forward gather band)
 };
 
@@ -347,6 +347,136 @@ __global__ void __launch_bounds__(kThreads) k_bi_c(PArgs a) {
     st->first = 0;
     st->it++;
     bi_top(st);
+}
+
+// ---------------------------------------------------------------- COCG --
+// Beyond the reference (cvk_krylov.cu cocg_body, oracle orc_cocg).  Two
+// launches per iteration: the SpMV phase (p = z + beta p formed in the
+// gathers, q = A p, mu = p^T q) and the elementwise phase (x, r, z updates,
+// ||z||^2 and r^T z).  work: r, z, q, p[2]
+struct CgVecs {
+    double2 *r, *z, *q, *p0, *p1;
+    __device__ CgVecs(double2* w, size_t n) : r(w), z(w + n), q(w + 2 * n), p0(w + 3 * n), p1(w + 4 * n) {}
+};
+
+// top of iteration st->it: max_iter, rho breakdown, beta (orc_cocg order)
+__device__ void cg_top(PState* st) {
+    if (st->it > st->max_iter) { st->done = 1; return; }
+    if (cvk_abs(st->rho_new) < st->brk) {
+        st->done = 1; st->brk_code = 1; st->iters = st->it - 1;
+        return;
+    }
+    if (!st->first) st->beta = cvk_cdiv(st->rho_new, st->rho);
+    st->rho = st->rho_new;
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_init(PArgs a) {
+    pdl_enter();
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    CAcc acc[2] = {};
+    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
+        const double2 ri = __ldg(a.b + i);
+        const double2 zi = prec_apply(a.dinv, i, ri);
+        V.r[i] = ri;
+        V.z[i] = zi;
+        a.x[i] = make_double2(0.0, 0.0);
+        acc_norm(acc[0], zi);
+        acc_udot(acc[1], ri, zi);
+    });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 0), &a.st->counter[0], tot)) return;
+    if (threadIdx.x != 0) return;
+    PState* st = a.st;
+    st->bnorm = sqrt(tot[0].x);
+    if (st->bnorm == 0.0) {
+        st->done = 1; st->conv = 1; st->iters = 0; st->skip_true = 1;
+        return;
+    }
+    st->brk = 1e-30 * st->bnorm * st->bnorm;
+    st->rho_new = tot[1];
+    st->it = 1;
+    st->first = 1;
+    st->cur = 0;
+    cg_top(st);
+}
+
+// mu breakdown / alpha, last CTA of the SpMV phase
+__device__ __forceinline__ void cg_alpha(PState* st, double2 mu) {
+    if (cvk_abs(mu) < st->brk) {
+        st->done = 1; st->brk_code = 8; st->iters = st->it - 1;
+        return;
+    }
+    st->alpha = cvk_cdiv(st->rho, mu);
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_a(PArgs a) {
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    const bool first = st->first != 0;
+    const double2 beta = st->beta;
+    const double2* __restrict__ z = V.z;
+    const double2* __restrict__ pc = st->cur ? V.p1 : V.p0;
+    double2* __restrict__ pn = st->cur ? V.p0 : V.p1;
+    auto pnew = [&](int c) -> double2 { return first ? z[c] : cvk_add(cvk_mul(beta, pc[c]), z[c]); };
+    CAcc acc[1] = {};
+    for_rows<1>(n, gridDim.x, blockIdx.x, [&](int row, int, bool valid) {
+        const double2 y = row_sum<1, decltype(pnew)&, kBatch>(a.A, row, 0, valid, pnew);
+        if (valid) {
+            const double2 pi = pnew(row);
+            pn[row] = pi;
+            V.q[row] = y;
+            acc_udot(acc[0], pi, y);
+        }
+    });
+    double2 tot[1];
+    if (!partial_last<1>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    cg_alpha(st, tot[0]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_b(PArgs a) {
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
+    const double2* __restrict__ pn = st->cur ? V.p0 : V.p1;
+    const double2* __restrict__ q = V.q;
+    double2* __restrict__ r = V.r;
+    double2* __restrict__ z = V.z;
+    double2* __restrict__ x = a.x;
+    const double2* __restrict__ dinv = a.dinv;
+    struct L5 { double2 x, p, r, q, d; };
+    CAcc acc[2] = {};
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L5{x[i], pn[i], r[i], q[i], dinv ? __ldg(dinv + i) : make_double2(1.0, 0.0)}; },
+        [&](int i, const L5& v) {
+            x[i] = cvk_add(v.x, cvk_mul(alpha, v.p));
+            const double2 ri = cvk_add(v.r, cvk_mul(nal, v.q));
+            const double2 zi = dinv ? cvk_mul(v.d, ri) : ri;
+            r[i] = ri;
+            z[i] = zi;
+            acc_norm(acc[0], zi);
+            acc_udot(acc[1], ri, zi);
+        });
+    double2 tot[2];
+    if (!partial_last<2>(acc, partv(a, 2), &st->counter[2], tot)) return;
+    if (threadIdx.x != 0) return;
+    const double relres = sqrt(tot[0].x) / st->bnorm;
+    st->final_relres = relres;
+    st->iters = st->it;
+    st_hist(a, st, relres);
+    if (relres <= st->tol) { st->done = 1; st->conv = 1; return; }
+    st->rho_new = tot[1];
+    st->cur ^= 1;
+    st->first = 0;
+    st->it++;
+    cg_top(st);
 }
 
 // --------------------------------------------------------------- tfQMR --
@@ -683,6 +813,44 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bi_b_s(PArgs a) {
     st->omega = cvk_cdiv(tot[2], tot[1]);
 }
 
+// COCG SpMV phase (k_cg_a) on the ring: p = z + beta p formed once per chunk
+// row in the pre-hook, q = A p, mu = p^T q
+__global__ void __launch_bounds__(kStreamThreads, 1) k_cg_a_s(PArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    const bool first = st->first != 0;
+    const double2 beta = st->beta;
+    const double2* __restrict__ z = V.z;
+    const double2* __restrict__ pc = st->cur ? V.p1 : V.p0;
+    double2* __restrict__ pn = st->cur ? V.p0 : V.p1;
+    double2* __restrict__ q = V.q;
+    const double2* vecs[2] = {z, first ? nullptr : pc};
+    StreamLayout L{a.capk, 2, a.nst[4]};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[1] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return ch.v(0, l); };  // p (pre)
+        auto xg = [&](int c) -> double2 { return first ? z[c] : cvk_add(cvk_mul(beta, pc[c]), z[c]); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 pi = ch.v(0, t);
+        const int row = ch.r0 + t;
+        pn[row] = pi;
+        q[row] = y;
+        acc_udot(acc[0], pi, y);
+    }, SPROF(1), [&](int t, const Chunk& ch) {
+        if (!first) ch.set(0, t, cvk_add(cvk_mul(beta, ch.v(1, t)), ch.v(0, t)));
+    });
+    double2 tot[1];
+    if (!partial_last<1, kStreamThreads>(acc, partv(a, 1), &st->counter[1], tot)) return;
+    if (threadIdx.x != 0) return;
+    cg_alpha(st, tot[0]);
+}
+
 // even tail + odd head of tfQMR (k_tf_e) on the ring
 __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_e_s(PArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -842,6 +1010,10 @@ PhasedKernels kernels_all() {
     k.bi_b_s = (const void*)k_bi_b_s;
     k.tf_e_s = (const void*)k_tf_e_s;
     k.tf_o_s = (const void*)k_tf_o_s;
+    k.cg_init = (const void*)k_cg_init;
+    k.cg_a = (const void*)k_cg_a;
+    k.cg_b = (const void*)k_cg_b;
+    k.cg_a_s = (const void*)k_cg_a_s;
     return k;
 }
 
@@ -899,7 +1071,7 @@ void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double
     PArgs* p = (PArgs*)out;
     p->pf_rows = pf_rows;
     p->capk = capk;
-    for (int i = 0; i < 4; ++i) p->nst[i] = nst[i];
+    for (int i = 0; i < 5; ++i) p->nst[i] = nst[i];
     p->A = A;
     p->dinv = dinv;
     p->b = b;

@@ -28,6 +28,9 @@ struct PhasedKernels {
     const void* true_res;  // (PArgs, double2* scratch)
     // streamed SpMV phases (cvk_stream.cuh): kStreamThreads threads, dynamic smem
     const void *bi_a_s, *bi_b_s, *tf_e_s, *tf_o_s;
+    // COCG (beyond the reference): init, thread-per-row SpMV phase, elementwise
+    // phase, streamed SpMV phase
+    const void *cg_init, *cg_a, *cg_b, *cg_a_s;
 };
 
 PhasedKernels phased_kernels();

@@ -15,7 +15,7 @@ from oracle import oracle as O
 from paper_2112_00087_b200.ddm_dist import SweepOut
 from paper_2112_00087_b200.helmholtz import cdiv, cmul
 
-SOLVERS = {0: "bicgstab", 1: "bicgstab_l", 2: "tfqmr", 3: "gmres"}
+SOLVERS = {0: "bicgstab", 1: "bicgstab_l", 2: "tfqmr", 3: "gmres", 4: "cocg"}
 
 
 def _local_system(problem, c0, c1, hl, hr, tp):

@@ -13,7 +13,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-SOLVERS = ("bicgstab", "bicgstab_l", "tfqmr", "gmres")
+SOLVERS = ("bicgstab", "bicgstab_l", "tfqmr", "gmres", "cocg")
 
 
 def bits(a):

@@ -73,7 +73,13 @@ def main():
         for solver, l in (("bicgstab", 8), ("bicgstab_l", 2), ("bicgstab_l", 1), ("tfqmr", 8)):
             x, rep = O.solve(solver, rp, ci, v, b, tol=1e-12, max_iter=50, l=l)
             key = (solver, rep.breakdown)
-            if key in todo and rep.iterations < best.get(key, 1 << 30):
+            if key in todo and rep.iterations < best.get(key, 1 << 30) and np.all(np.isfinite(x)):
+                # the same breakdown, at the same step, with near-exact sums
+                O.lib().orc_set_sum_mode(1)
+                _, rd = O.solve(solver, rp, ci, v, b, tol=1e-12, max_iter=50, l=l)
+                O.lib().orc_set_sum_mode(0)
+                if (rd.breakdown, rd.iterations, rd.converged) != (rep.breakdown, rep.iterations, rep.converged):
+                    continue
                 # the reference itself must agree (Sequential mode, Jacobi)
                 xr, rr = O.ref_solve(solver, rp, ci, v, b, tol=1e-12, max_iter=50, l=l)
                 if (rr.breakdown, rr.iterations, rr.converged) != (rep.breakdown, rep.iterations, rep.converged) \
