@@ -314,6 +314,35 @@ int cvk_ddm_rank_set_traces(cvk_ddm_rank *rank, const double *g_l, const double 
 int cvk_ddm_rank_set_warm(cvk_ddm_rank *rank, int warm);
 int cvk_ddm_rank_destroy(cvk_ddm_rank *rank);
 
+/* ---- Schwarz DDM on algebraic subdomains (FEM meshes, METIS-style / RCB
+ * partitions; beyond the reference, whose schwarz_solve knows only the FD
+ * cavity's strips, schwarz.cpp:29-89) ----
+ *
+ * part_of_row[i] in [0, n_parts) assigns row i to a subdomain; each
+ * subdomain works on its rows grown by `overlap` layers of A's graph, with
+ * every coupling that leaves that set folded into the diagonal by the
+ * reference's Robin factor (1/h - s/2) / (1/h + s/2) (schwarz.cpp:43-50,
+ * s = s_robin complex, h the mesh size).  The preconditioner is restricted
+ * additive Schwarz: each subdomain solves its local system (inner solver and
+ * options as the reference's inner solves, schwarz.cpp:177) and writes back
+ * its owned rows.  cvk_asm_solve: m = 0 iterates the fixed point
+ * u <- u + M^-1 (b - A u) (the reference's additive sweep); m > 0 runs
+ * FGMRES(m) right-preconditioned by M^-1.  Both stop at ||b - A u|| <= tol
+ * ||b||, whose solution is the monodomain one.  Report: outer_iterations =
+ * subdomain sweeps, jump_history = relative residuals, total_inner_iterations
+ * = the last sweep's inner iterations. */
+typedef struct cvk_asm cvk_asm;
+int cvk_asm_create(cvk_ctx *ctx, int64_t n, int64_t nnz, const uint64_t *row_offsets,
+                   const uint64_t *col_indices, const double *values, int64_t n_parts,
+                   const int64_t *part_of_row, int64_t overlap, const double *s_robin, double h,
+                   const cvk_opts *inner, int inner_solver, cvk_asm **out);
+/* z = M^-1 r, device vectors of length n on ctx's device */
+int cvk_asm_apply_device(cvk_asm *S, const double *r_dev, double *z_dev);
+int cvk_asm_solve(cvk_asm *S, const double *b, double *x, double tol, int64_t max_outer, int64_t m,
+                  cvk_ddm_report *rep);
+int64_t cvk_asm_n_parts(const cvk_asm *S);
+int cvk_asm_destroy(cvk_asm *S);
+
 /* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */
 
 /* Overwrite A's values with the cavity operator at `omega` (assemble,

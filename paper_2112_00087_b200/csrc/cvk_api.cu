@@ -909,7 +909,7 @@ static int solve_bicgstab_general(cvk_ctx* c, const cvk_csr* A, const cvk_prec* 
     int e;
     const size_t nv = (size_t)std::max(1, n);
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (9 * nv + 8))) != CVK_OK) return e;
-    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 2048)) != CVK_OK) return e;
     double2* w = (double2*)c->work;
     double2 *r = w, *sh = w + nv, *p = w + 2 * nv, *v = w + 3 * nv, *s = w + 4 * nv, *t = w + 5 * nv,
             *tmp = w + 6 * nv, *ptmp = w + 7 * nv, *od = w + 9 * nv;
@@ -1674,7 +1674,7 @@ static int dot_impl(cvk_ctx* c, int64_t n, const double* x, const double* y, dou
     double2* xd = c->bx;
     double2* yd = y ? c->bx + nn : nullptr;
     double2* od = c->bx + 2 * nn;
-    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 2048)) != CVK_OK) return e;
     if (nn) CK(cudaMemcpyAsync(xd, x, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
     if (y && nn) CK(cudaMemcpyAsync(yd, y, sizeof(double2) * nn, cudaMemcpyHostToDevice, c->stream));
     CK(cvk::launch_dot(ref, (int)n, xd, yd, c->part, od, c->stream));
@@ -1756,7 +1756,7 @@ int cvk_true_relres(const cvk_csr* A, const double* b, const double* x, double* 
     double2* rd = c->bx + 2 * n;
     double2* od = c->bx + 3 * n;
     const bool ref = is_ref(resolve_mode(c, mode));
-    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 1024)) != CVK_OK) return e;
+    if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * 2048)) != CVK_OK) return e;
     CK(cudaMemcpyAsync(bd, b, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(xd, x, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cvk::launch_residual(ref ? 1 : A->group, ref, (int)n, A->rp, A->ci, A->av, bd, xd, rd, c->stream));

@@ -71,7 +71,8 @@ cudaError_t launch_fem_values(long long nnz, const double* K, const double* M, c
                               double2* av, int nsm, cudaStream_t st);
 cudaError_t launch_inv_diag(int n, const int* rp, const int* ci, const double2* av, double2* out,
                             int* bad_row, cudaStream_t st);
-// out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 1024 double2
+// out[0] = sum conj(x) y (mode dot) or sum |x|^2 (norm, y == nullptr); part >= 2048 double2
+// (hi and lo partials of 592 CTAs)
 cudaError_t launch_dot(bool ref, int n, const double2* x, const double2* y, double2* part,
                        double2* out, cudaStream_t st);
 cudaError_t launch_axpy(int n, double2 alpha, const double2* x, double2* y, cudaStream_t st);

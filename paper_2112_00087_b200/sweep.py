@@ -115,7 +115,7 @@ class CavitySweep:
     def solve(self, solver=SolverId.BiCGStab, opts: Optional[SolverOptions] = None, mode=None):
         opts = opts or SolverOptions()
         sid = solver_id(solver) if isinstance(solver, str) else SolverId(solver)
-        o = _lib.CvkOpts(opts.tol, opts.max_iter, opts.l, opts.m, 0, _dev_mode(mode))
+        o = _lib.CvkOpts(opts.tol, opts.max_iter, opts.l, opts.m, 0, _dev_mode(mode), 0, 0)
         rep = _lib.CvkReport()
         L = _lib.load()
         # host b / x: 16 n bytes each way per point, ~1e-3 of a point's solve time

@@ -8,7 +8,8 @@ name=$1; shift
 out=_variants/$name
 mkdir -p $out
 objs=()
-for f in cvk_api cvk_blas cvk_krylov cvk_phased cvk_ddm cvk_assemble cvk_gmres cvk_bicgl cvk_rowblock cvk_mmio cvk_phased_g4; do
+for src in paper_2112_00087_b200/csrc/*.cu; do
+  f=$(basename $src .cu)
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
     -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude "$@" -c paper_2112_00087_b200/csrc/$f.cu -o $out/$f.o &
   objs+=($out/$f.o)
