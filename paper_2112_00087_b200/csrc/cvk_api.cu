@@ -1375,10 +1375,16 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     const int n = (int)A->n;
     const int L = (int)o->l;
     const cvk::BiclKernels K = cvk::bicgl_kernels();
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.step, cvk::kThreads, 0));
+    // grid per kernel: its resident CTAs (the phases are grid-stride)
     const long long chunks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
-    long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, chunks);
+    auto grid_of = [&](const void* f) -> long long {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, cvk::kThreads, 0);
+        return std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, chunks);
+    };
+    const long long Gu = grid_of(K.u), Gr = grid_of(K.r), Gm = grid_of(K.mgs), Gq = grid_of(K.mgsr),
+                    Gp = grid_of(K.upd), Gx = grid_of(K.exit);
+    const long long G = std::max(std::max(std::max(Gu, Gr), std::max(Gm, Gp)), std::max(Gx, Gq));
     int e;
     if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(2 * L + 6) * std::max(1, n))) != CVK_OK)
         return e;
@@ -1400,14 +1406,27 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
                          c->part, c->bst, c->hist, c->rep);
     void* args[] = {blob.data()};
     const dim3 grid((unsigned)G), block(cvk::kThreads);
-    constexpr int kStepsPerGraph = 32;
+    // one graph = one cycle's static phase sequence (cvk_bicgl.cu)
+    const long long per_cycle = 2LL * L + (L <= cvk::kBiclMgsrL ? L : (long long)L * (L + 1) / 2) + 2;
     std::vector<unsigned char> key(blob);
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
+    key.push_back((unsigned char)L);
     if (!c->bl_exec || c->bl_key != key) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        for (int it = 0; it < kStepsPerGraph; ++it) launch_pdl(K.step, grid, block, args, 0, c->stream);
+        for (int j = 0; j < L; ++j) {
+            launch_pdl(K.u, dim3((unsigned)Gu), block, args, 0, c->stream);
+            launch_pdl(K.r, dim3((unsigned)Gr), block, args, 0, c->stream);
+        }
+        if (L <= cvk::kBiclMgsrL)
+            for (int q = 0; q < L; ++q)  // slices of kBiclMgsrW columns (cvk_bicgl.cu k_bl_mgsr)
+                launch_pdl(K.mgsr, dim3((unsigned)Gq, (unsigned)((L - q + cvk::kBiclMgsrW - 1) / cvk::kBiclMgsrW)), block,
+                           args, 0, c->stream);
+        else
+            for (int q = 0; q < L * (L + 1) / 2; ++q) launch_pdl(K.mgs, dim3((unsigned)Gm), block, args, 0, c->stream);
+        launch_pdl(K.upd, dim3((unsigned)Gp), block, args, 0, c->stream);
+        launch_pdl(K.exit, dim3((unsigned)Gx), block, args, 0, c->stream);
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
         CK(install_graph(&c->bl_exec, graph));
@@ -1418,8 +1437,7 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     CK(launch_pdl(K.init, grid, block, args, 0, c->stream));
     long long launches = 1;
     const int* done_ptr = (const int*)((const char*)c->bst + cvk::bicgl_state_done_offset());
-    const long long per_cycle = 2LL * L + (long long)L * (L + 1) / 2 + 2;
-    const long long max_graphs = (std::max<long long>(1, o->max_iter) * per_cycle) / kStepsPerGraph + 3;
+    const long long max_graphs = std::max<long long>(1, o->max_iter) + 3;
     long long graphs = 0;
     for (;;) {
         if (graphs >= max_graphs) break;
@@ -1428,7 +1446,7 @@ static int solve_bicgl_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
         CK(cudaMemcpyAsync(&c->h_done[slot], done_ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += kStepsPerGraph;
+        launches += per_cycle;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));

@@ -280,7 +280,7 @@ int cvk_asm_solve(cvk_asm* S, const double* b_host, double* x_host, double tol, 
     const double t0 = now_s();
     const int n = (int)S->n;
     const size_t nb = sizeof(double2) * (size_t)n;
-    const int nvec = m > 0 ? (int)(2 * m + 4) : 4;
+    const int nvec = m > 0 ? (int)(2 * m + 5) : 4;  // b, x, r, t, V (m + 1), Z (m)
     double2* W = nullptr;
     AK(cudaMalloc(&W, nb * (size_t)nvec));
     struct Free { void* p; ~Free() { cudaFree(p); } } guard{W};

@@ -3,12 +3,15 @@
 //
 // A BiCGSTAB(l) cycle is 2l + l(l+1)/2 + 1 reduction phases (l u-steps and
 // l r-steps with an SpMV each, the l(l+1)/2 modified-Gram-Schmidt steps of
-// the minimal-residual part, the polynomial update).  Each launch of
-// k_bl_step runs the phase named by the device state; the CTA that arrives
+// the minimal-residual part, the polynomial update).  The graph is one
+// cycle's phase sequence -- U0 R0 ... U(l-1) R(l-1), the MGS steps, the
+// update, an exit node -- each node a kernel specialised to its phase type
+// (k_bl_u / k_bl_r / k_bl_mgs / k_bl_upd / k_bl_exit).  The CTA that arrives
 // last folds the double-double partials and runs the reference's scalar
 // logic (breakdown tests, tau / sigma / gamma', the gamma recurrences,
-// convergence), then names the next phase.  The graph is just N identical
-// launches; the host polls `done` between graphs.  The persistent kernel
+// convergence), then names the next phase; a node whose phase is not the
+// state's returns at once, so an early exit skips to the exit node.  The host
+// polls `done` between graphs.  The persistent kernel
 // runs these phases with one CTA-wide element per thread and grid barriers
 // at 3 CTAs/SM (2.4 ms per l=8 cycle at 1M DOF); here every phase is a
 // full-occupancy kernel.
@@ -28,7 +31,10 @@ namespace cvk {
 
 namespace {
 
-enum { P_U = 0, P_R = 1, P_MGS = 2, P_UPD = 3, P_EXIT = 4 };
+enum { P_U = 0, P_R = 1, P_MGS = 2, P_UPD = 3, P_EXIT = 4, P_MGSR = 5 };
+
+// right-looking MGS passes for l <= kMgsrL (accumulators per pass: l + 1)
+constexpr int kMgsrL = 8;
 
 struct BLState {
     int done, conv, brk_code, phase, j, i, exit_mr, skip_true;
@@ -126,6 +132,24 @@ __device__ void to_exit(BLState* st, int mr) {
     st->phase = P_EXIT;
 }
 
+// gamma, gamma', gamma'' (krylov.cpp:251-262), then the update phase
+__device__ void finish_mr(BLState* st, int L) {
+    // gamma, gamma', gamma'' (krylov.cpp:251-262)
+    st->gam[L - 1] = st->gp[L - 1];
+    for (int jj = L - 1; jj-- > 0;) {
+        double2 gj = st->gp[jj];
+        for (int q = jj + 1; q < L; ++q) gj = cvk_sub(gj, cvk_mul(st->tau[jj * L + q], st->gam[q]));
+        st->gam[jj] = gj;
+    }
+    for (int jj = 0; jj + 1 < L; ++jj) {
+        double2 gj = st->gam[jj + 1];
+        for (int q = jj + 1; q + 1 < L; ++q) gj = cvk_add(gj, cvk_mul(st->tau[jj * L + q], st->gam[q + 1]));
+        st->gpp[jj] = gj;
+    }
+    st->omega = st->gam[L - 1];
+    st->phase = P_UPD;
+}
+
 // top of BiCG step j (krylov.cpp:175-186)
 __device__ void prep_u(BLState* st) {
     const double2 rho = st->rho_next;
@@ -183,13 +207,19 @@ __global__ void __launch_bounds__(kThreads) k_bl_init(BLArgs a) {
 #define CVK_BL_SPMV_BATCH 5  // gathers in flight per row in the u/r SpMV phases
 #endif
 #ifndef CVK_BL_BATCH
-#define CVK_BL_BATCH 2  // measured at 1M DOF: 1 -> 2343, 2 -> 2293, 4 -> 2382 us per l=8 cycle
+#define CVK_BL_BATCH 4  // elements in flight per thread in the MGS phases
 #endif
-__global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
+// One phase of the cycle; PH is the phase this launch implements: a launch
+// whose phase is not the state's current one returns at once (the graph is
+// one cycle's static phase sequence, and an early exit skips ahead to the
+// cycle's P_EXIT node).
+template <int PH>
+__device__ __forceinline__ void bl_phase(const BLArgs& a) {
     pdl_enter_b();
     BLState* st = a.st;
-    if (st->done) return;
-    const int n = a.A.n, L = st->L, phase = st->phase, j = st->j;
+    if (st->done || st->phase != PH) return;
+    constexpr int phase = PH;
+    const int n = a.A.n, L = st->L, j = st->j;
     __shared__ int ri[kMaxL + 2], ui[kMaxL + 2];
     if (threadIdx.x <= L + 1) { ri[threadIdx.x] = st->ri[threadIdx.x]; ui[threadIdx.x] = st->ui[threadIdx.x]; }
     __syncthreads();
@@ -199,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
     const double2* dinv = a.dinv;
     const int G = gridDim.x, cta = blockIdx.x;
 
-    if (phase == P_U) {
+    if constexpr (phase == P_U) {
         // u_i = r_i - beta u_i (i <= j, u_j formed in the gathers); u_{j+1} = M^-1 A u_j; <shadow, u_{j+1}>
         const double2 nbeta = cvk_neg(st->beta);
         const double2* uj_old = U(j);
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
         st->phase = P_R;
         return;
     }
-    if (phase == P_R) {
+    if constexpr (phase == P_R) {
         // r_i -= alpha u_{i+1} (i <= j, r_j formed in the gathers); r_{j+1} = M^-1 A r_j; x += alpha u_0
         const double2 alpha = st->alpha, nal = cvk_neg(st->alpha);
         const double2* rj_old = R(j);
@@ -285,13 +315,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
             st->j = j + 1;
             prep_u(st);
         } else {
-            st->phase = P_MGS;
+            st->phase = L <= kMgsrL ? P_MGSR : P_MGS;
             st->j = 0;
             st->i = 0;
         }
         return;
     }
-    if (phase == P_MGS) {
+    if constexpr (phase == P_MGS) {
         // pending update r_{j+1} -= tau_{i-1,j} r_i, then <r_{i+1}, r_{j+1}> (i < j)
         // or sigma_j = <r_{j+1}, r_{j+1}>, <r_{j+1}, r_0> (i == j)   (krylov.cpp:224-238)
         const int i = st->i;
@@ -330,23 +360,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
             st->i = 0;
             return;
         }
-        // gamma, gamma', gamma'' (krylov.cpp:251-262)
-        st->gam[L - 1] = st->gp[L - 1];
-        for (int jj = L - 1; jj-- > 0;) {
-            double2 gj = st->gp[jj];
-            for (int q = jj + 1; q < L; ++q) gj = cvk_sub(gj, cvk_mul(st->tau[jj * L + q], st->gam[q]));
-            st->gam[jj] = gj;
-        }
-        for (int jj = 0; jj + 1 < L; ++jj) {
-            double2 gj = st->gam[jj + 1];
-            for (int q = jj + 1; q + 1 < L; ++q) gj = cvk_add(gj, cvk_mul(st->tau[jj * L + q], st->gam[q + 1]));
-            st->gpp[jj] = gj;
-        }
-        st->omega = st->gam[L - 1];
-        st->phase = P_UPD;
+        finish_mr(st, L);
         return;
     }
-    if (phase == P_UPD) {
+    if constexpr (phase == P_UPD) {
         // updates (krylov.cpp:264-271), per element in the reference's order
         __shared__ double2 gam[kMaxL], gp[kMaxL], gpp[kMaxL];
         if (threadIdx.x < L) { gam[threadIdx.x] = st->gam[threadIdx.x]; gp[threadIdx.x] = st->gp[threadIdx.x]; gpp[threadIdx.x] = st->gpp[threadIdx.x]; }
@@ -383,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
         start_cycle(st);
         return;
     }
+    if constexpr (phase != P_EXIT) return;
     // P_EXIT: ||r_0|| after a break (krylov.cpp:208-222, 239-249)
     const double2* r0 = R(0);
     CAcc acc[1] = {};
@@ -404,6 +422,171 @@ __global__ void __launch_bounds__(kThreads, 3) k_bl_step(BLArgs a) {
     }
     st->done = 1;
 }
+
+// Right-looking MGS (l <= kMgsrL): pass q makes r_{q+1} the pivot.  It first
+// applies the pending update of every later column, r_{jj+1} -= tau_{q-1,jj}
+// r_q (jj >= q), then takes sigma_q = <r_{q+1}, r_{q+1}>, <r_{q+1}, r_0> and
+// <r_{q+1}, r_{jj+1}> (jj > q) in the same pass.  Every r_{jj+1} receives
+// the same updates in the same order as in the reference's column loop
+// (krylov.cpp:224-238), and every inner product sees the same operands, so
+// tau, sigma and gamma' are those of the left-looking phases; l passes
+// replace l(l+1)/2.
+//
+// The columns of a pass are split over blockIdx.y slices of kMgsrW: slice y
+// updates and writes its own columns (the pivot is column 0 of slice 0) and
+// takes their inner products with the pivot, which it updates itself (every
+// slice re-reads the pivot and r_q), so a thread carries at most kMgsrW + 1
+// double-double accumulators.  All slices arrive on one counter; the last
+// CTA folds every accumulator from the x-partials of its slice.
+constexpr int kMgsrW = 4;
+#ifndef CVK_MGSR_U
+#define CVK_MGSR_U 2
+#endif
+constexpr int kMgsrU = CVK_MGSR_U;
+__global__ void __launch_bounds__(kThreads, kMgsrU > 1 ? 2 : 3) k_bl_mgsr(BLArgs a) {
+    pdl_enter_b();
+    BLState* st = a.st;
+    if (st->done || st->phase != P_MGSR) return;
+    constexpr int KA = kMgsrW + 1;  // slice 0: sigma, gamma', W - 1 dots; slice y > 0: W dots
+    const int n = a.A.n, L = st->L, q = st->i;
+    const int nc = L - q;  // columns left (pivot included)
+    const int y = blockIdx.y, c0 = y * kMgsrW;
+    if (c0 >= nc && y > 0) {  // idle slice: still arrives on the counter
+        CAcc acc[1] = {};
+        double2 tot[1];
+        (void)tot;
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&st->counter[0], 1u) == gridDim.x * gridDim.y - 1u;
+        }
+        __syncthreads();
+        (void)acc;
+        if (!s_last) return;
+        __threadfence();
+        // fall through as the last CTA: nothing of its own to contribute
+        goto fold;
+    }
+    {
+        __shared__ const double2* cols[kMgsrW];
+        __shared__ double2 ntau[kMgsrW];
+        __shared__ double2 ntp;  // pivot's pending factor
+        __shared__ const double2 *piv, *rq, *r0;
+        if (threadIdx.x < kMgsrW) {
+            const int jj = q + c0 + (int)threadIdx.x;
+            cols[threadIdx.x] = jj < L ? slot(a, st->ri[jj + 1]) : nullptr;
+            ntau[threadIdx.x] = (q > 0 && jj < L) ? cvk_neg(st->tau[(q - 1) * L + jj]) : make_double2(0, 0);
+        }
+        if (threadIdx.x == 0) {
+            piv = slot(a, st->ri[q + 1]);
+            ntp = q > 0 ? cvk_neg(st->tau[(q - 1) * L + q]) : make_double2(0, 0);
+            rq = q > 0 ? slot(a, st->ri[q]) : nullptr;
+            r0 = slot(a, st->ri[0]);
+        }
+        __syncthreads();
+        const int ncol = min(kMgsrW, nc - c0);  // this slice's columns
+        CAcc acc[KA] = {};
+        // kMgsrU elements per thread per trip, every load of a trip issued
+        // before its first update (the pass is latency-bound otherwise)
+        const long long stride = (long long)gridDim.x * kThreads;
+        for (long long i0 = (long long)blockIdx.x * kThreads + threadIdx.x; i0 < n; i0 += stride * kMgsrU) {
+            double2 v[kMgsrU][kMgsrW], pv[kMgsrU], o[kMgsrU], p[kMgsrU];
+#pragma unroll
+            for (int u = 0; u < kMgsrU; ++u) {
+                const long long i = i0 + u * stride;
+                if (i >= n) continue;
+#pragma unroll
+                for (int c = 0; c < kMgsrW; ++c)
+                    if (c < ncol) v[u][c] = cols[c][i];
+                pv[u] = y == 0 ? make_double2(0, 0) : piv[i];
+                o[u] = y == 0 ? r0[i] : make_double2(0, 0);
+                p[u] = q > 0 ? rq[i] : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kMgsrU; ++u) {
+                const long long i = i0 + u * stride;
+                if (i >= n) continue;
+                if (q > 0) {
+#pragma unroll
+                    for (int c = 0; c < kMgsrW; ++c)
+                        if (c < ncol) {
+                            v[u][c] = cvk_add(v[u][c], cvk_mul(ntau[c], p[u]));
+                            const_cast<double2*>(cols[c])[i] = v[u][c];
+                        }
+                    if (y != 0) pv[u] = cvk_add(pv[u], cvk_mul(ntp, p[u]));
+                }
+                if (y == 0) {
+                    const double2 pw = v[u][0];
+                    acc_dot(acc[0], pw, pw);
+                    acc_dot(acc[1], pw, o[u]);
+#pragma unroll
+                    for (int c = 1; c < kMgsrW; ++c)
+                        if (c < ncol) acc_dot(acc[1 + c], pw, v[u][c]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kMgsrW; ++c)
+                        if (c < ncol) acc_dot(acc[c], pv[u], v[u][c]);
+                }
+            }
+        }
+        // partial slots: 0 sigma, 1 gamma', 1 + c for global column c (pivot = 0)
+        __shared__ CAcc sm[KA][32];
+        cta_sum_k<KA, kThreads>(acc, sm);
+        const int Gx = gridDim.x;
+        if (threadIdx.x == 0) {
+            if (y == 0) {
+                cacc_store(a.part, 0, Gx, blockIdx.x, acc[0]);
+                cacc_store(a.part, 1, Gx, blockIdx.x, acc[1]);
+                for (int c = 1; c < ncol; ++c) cacc_store(a.part, 1 + c, Gx, blockIdx.x, acc[1 + c]);
+            } else {
+                for (int c = 0; c < ncol; ++c) cacc_store(a.part, 1 + c0 + c, Gx, blockIdx.x, acc[c]);
+            }
+        }
+        __shared__ int s_last2;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last2 = atomicAdd(&st->counter[0], 1u) == gridDim.x * gridDim.y - 1u;
+        }
+        __syncthreads();
+        if (!s_last2) return;
+        __threadfence();
+    }
+fold:
+    {
+        // the last CTA: fold sigma, gamma' and the nc - 1 pivot dots (one warp each)
+        __shared__ double2 res[kMgsrL + 1];
+        const int Gx = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int k = warp; k < 1 + nc; k += kThreads / 32) {
+            const double2 t = fold_one(a.part, k, Gx, lane);
+            if (lane == 0) res[k] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        st->counter[0] = 0;
+        const double2 sig = res[0];
+        if (cvk_abs(sig) < st->brk) { st->brk_code = 5; to_exit(st, 1); return; }  // krylov.cpp:231-236
+        st->sig[q] = sig;
+        st->gp[q] = cvk_cdiv(res[1], sig);
+        for (int c = 1; c < nc; ++c) st->tau[q * L + q + c] = cvk_cdiv(res[1 + c], sig);
+        if (q + 1 < L) {
+            st->i = q + 1;
+            return;
+        }
+        finish_mr(st, L);
+    }
+}
+
+// The phase kernels.  Each carries only its own phase's registers: the MGS
+// and update phases are plain element streams and run at full occupancy with
+// four elements' loads in flight per thread; the u / r phases keep the
+// thread-per-row SpMV.
+__global__ void __launch_bounds__(kThreads, 3) k_bl_u(BLArgs a) { bl_phase<P_U>(a); }
+__global__ void __launch_bounds__(kThreads, 3) k_bl_r(BLArgs a) { bl_phase<P_R>(a); }
+__global__ void __launch_bounds__(kThreads, 2) k_bl_mgs(BLArgs a) { bl_phase<P_MGS>(a); }
+__global__ void __launch_bounds__(kThreads, 3) k_bl_upd(BLArgs a) { bl_phase<P_UPD>(a); }
+__global__ void __launch_bounds__(kThreads, 4) k_bl_exit(BLArgs a) { bl_phase<P_EXIT>(a); }
 
 __global__ void __launch_bounds__(kThreads) k_bl_true(BLArgs a) {
     pdl_enter_b();
@@ -445,7 +628,12 @@ __global__ void __launch_bounds__(kThreads) k_bl_true(BLArgs a) {
 BiclKernels bicgl_kernels() {
     BiclKernels k;
     k.init = (const void*)k_bl_init;
-    k.step = (const void*)k_bl_step;
+    k.u = (const void*)k_bl_u;
+    k.r = (const void*)k_bl_r;
+    k.mgs = (const void*)k_bl_mgs;
+    k.mgsr = (const void*)k_bl_mgsr;
+    k.upd = (const void*)k_bl_upd;
+    k.exit = (const void*)k_bl_exit;
     k.true_res = (const void*)k_bl_true;
     return k;
 }

@@ -43,9 +43,13 @@ int gmres_state_done_offset();
 void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
                      double2* part, void* st, double* hist, DevReport* rep, int capk, int nst, int pf_rows);
 
-// phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): one uniform step kernel
+// phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): one kernel per phase type; the
+// right-looking MGS kernel (mgsr) serves l <= kBiclMgsrL, the left-looking
+// per-(i, j) kernel larger l
+constexpr int kBiclMgsrL = 8;
+constexpr int kBiclMgsrW = 4;  // columns per blockIdx.y slice of k_bl_mgsr
 struct BiclKernels {
-    const void *init, *step, *true_res;
+    const void *init, *u, *r, *mgs, *mgsr, *upd, *exit, *true_res;
 };
 BiclKernels bicgl_kernels();
 size_t bicgl_state_size();

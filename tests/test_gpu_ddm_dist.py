@@ -81,3 +81,51 @@ def test_device_ranks_match_single_device(cvk, oracle, world, n_sub, mode):
                                           complex(2.0, k), complex(2.0, k), tol=1e-10, ddm_tol=1e-8,
                                           max_outer=300)
         assert np.array_equal(outs[0][1].view(np.uint64), x_o.view(np.uint64))
+
+
+def _tune_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2112_00087_b200 as P
+        from paper_2112_00087_b200.ddm_dist import tune_parameters_distributed
+        from paper_2112_00087_b200.schwarz import default_candidate_grid, partition
+        prob = _problem()
+        part = partition(prob.grid, 2)
+        k = prob.omega / prob.c
+        cands = default_candidate_grid(k)
+        t = tune_parameters_distributed(prob, part, cands, P.SolverOptions(tol=1e-10), 300,
+                                        mode=P.ExecMode.Fast)
+        q.put((rank, t.best, [(e.outer_iterations, e.total_inner_iterations, e.converged) for e in t.table]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_tuner_on_device(cvk):
+    """tune_parameters (schwarz.cpp:240-301) with the 36 candidates split over
+    2 ranks sharing cuda:0, every candidate a device schwarz_solve: the same
+    table and minimiser as the single-process device tuner."""
+    import torch.multiprocessing as mp
+    from paper_2112_00087_b200.schwarz import default_candidate_grid, partition, tune_parameters
+    P = cvk
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tune_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = [q.get(timeout=900) for _ in procs]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    prob = _problem()
+    part = partition(prob.grid, 2)
+    k = prob.omega / prob.c
+    t = tune_parameters(prob, part, default_candidate_grid(k), P.SolverOptions(tol=1e-10), 300,
+                        mode=P.ExecMode.Fast)
+    want = [(e.outer_iterations, e.total_inner_iterations, e.converged) for e in t.table]
+    for rank, best, table in got:
+        assert best == t.best
+        assert table == want
