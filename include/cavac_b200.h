@@ -156,6 +156,8 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
 #define CVK_OPT_DDM_SEQ_MIN 9      /* strip rows from which Schwarz inner solves run one after
                                       another on the single-system path (131072) */
 #define CVK_OPT_RB_STREAM_MIN 10   /* own rows from which row-block phases are streamed */
+#define CVK_OPT_BICG_FOLD 11       /* 1: streamed BiCGSTAB folds each reduction in the consuming
+                                      kernel (default); 0: in the producer's last CTA */
 int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
 int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 
@@ -342,6 +344,22 @@ int cvk_asm_solve(cvk_asm *S, const double *b, double *x, double tol, int64_t ma
                   cvk_ddm_report *rep);
 int64_t cvk_asm_n_parts(const cvk_asm *S);
 int cvk_asm_destroy(cvk_asm *S);
+/* Several ranks (one device each, north_star's "one or more subdomains per
+ * GPU"): rank r of n_ranks builds and solves the subdomains q with
+ * q % n_ranks == r; the outer loop runs on every rank.  After its local
+ * solves a rank holds M^-1 r on its subdomains' owned rows and zero
+ * elsewhere; the reducer must sum z_dev (n complex, device memory of the
+ * rank's device; with buf_dev non-null the library stages z through that
+ * caller-owned buffer, e.g. a framework tensor) over all ranks, complete
+ * before it returns, and sum meta[0] (inner iterations) and max meta[1]
+ * (breakdown flag) -- an all-reduce.  Returns 0 on success.  The sum has one nonzero term per entry,
+ * so results are bitwise those of one rank. */
+typedef int (*cvk_asm_reduce_fn)(void *user, double *z_dev, int64_t n, int64_t *meta);
+int cvk_asm_create_rank(cvk_ctx *ctx, int64_t n, int64_t nnz, const uint64_t *row_offsets,
+                        const uint64_t *col_indices, const double *values, int64_t n_parts,
+                        const int64_t *part_of_row, int64_t overlap, const double *s_robin, double h,
+                        const cvk_opts *inner, int inner_solver, int rank, int n_ranks, cvk_asm **out);
+int cvk_asm_set_reducer(cvk_asm *S, cvk_asm_reduce_fn fn, void *user, double *buf_dev);
 
 /* ---- frequency sweeps (beyond the reference's single-omega assemble) ---- */
 

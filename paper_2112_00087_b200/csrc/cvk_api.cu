@@ -33,7 +33,7 @@ size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows);
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod);
 }  // namespace cvk_g4
 namespace cvk {
 int flavor_stream_rows();
@@ -43,7 +43,7 @@ size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows);
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod);
 }  // namespace cvk
 
 // execution-path options (cvk_ctx_set_option); defaults are the product's
@@ -58,6 +58,7 @@ struct CvkKnobs {
     long long ilu_hostloop = 0;
     long long ddm_seq_min = 131072;
     long long rb_stream_min = 65536;
+    long long bicg_fold = 1;
 };
 
 struct cvk_ctx {
@@ -216,6 +217,7 @@ long long* knob_slot(cvk_ctx* c, int key) {
         case CVK_OPT_ILU_HOSTLOOP: return &c->knob.ilu_hostloop;
         case CVK_OPT_DDM_SEQ_MIN: return &c->knob.ddm_seq_min;
         case CVK_OPT_RB_STREAM_MIN: return &c->knob.rb_stream_min;
+        case CVK_OPT_BICG_FOLD: return &c->knob.bicg_fold;
     }
     return nullptr;
 }
@@ -1132,9 +1134,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
-    const void* sk[5] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s};
+    const void* sk[7] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s, K.bf_a_s, K.bf_b_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
+    // BiCGSTAB with the reductions folded by the consuming kernel (k_bf_*)
+    const bool fold = streamed && solver == CVK_BICGSTAB && c->knob.bicg_fold;
     // elementwise phases: grid-stride, 4 elements per thread per trip
     long long Ge = std::min<long long>(2LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
     if (!streamed) Ge = G;
@@ -1145,11 +1149,15 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     {
         // the L2 prefetch window reads A->cmax, which is per 224-row chunk
         const int pf = g4 ? 0 : 2 * cvk::kStreamRows;
+        // producers of the partial regions of k_bf_*: 0 = k_bf_c, 1 = k_bf_a_s, 2 = k_bf_b_s
+        const int gprod[3] = {(int)Ge, c->nsm, c->nsm};
         (g4 ? cvk_g4::flavor_pack_args : cvk::flavor_pack_args)(
             blob.data(), n, A->rp, A->ci, A->av, g4 ? nullptr : A->cmax, M->dinv, b_dev, x_dev, (double2*)c->work,
-            c->part, c->st, c->hist, c->rep, scapk, stg, pf);
+            c->part, c->st, c->hist, c->rep, scapk, stg, pf, gprod);
     }
     void* args[] = {blob.data()};
+    int parity[2] = {0, 1};
+    void* pargs[2][2] = {{blob.data(), &parity[0]}, {blob.data(), &parity[1]}};
     double2* scratch = (double2*)c->work;  // r / first work vector, dead after the loop
     void* targs[] = {blob.data(), &scratch};
     const dim3 grid((unsigned)G), block(cvk::kThreads);
@@ -1161,6 +1169,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     key.insert(key.end(), gp, gp + sizeof(G));
     key.push_back((unsigned char)(streamed ? 1 : 0));
     key.push_back((unsigned char)(g4 ? 1 : 0));
+    key.push_back((unsigned char)(fold ? 1 : 0));
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
@@ -1172,6 +1181,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
                 if (streamed) launch_pdl(K.cg_a_s, sgrid, sblock, args, smem_for(4), c->stream);
                 else launch_pdl(K.cg_a, grid, block, args, smem, c->stream);
                 launch_pdl(K.cg_b, egrid, block, args, 0, c->stream);
+            } else if (fold) {  // 3 launches per iteration, parity 0 1 0 | 1 0 1 | ...
+                const int p0 = (3 * it) & 1;
+                launch_pdl(K.bf_a_s, sgrid, sblock, pargs[p0], smem_for(0), c->stream);
+                launch_pdl(K.bf_b_s, sgrid, sblock, pargs[p0 ^ 1], smem_for(1), c->stream);
+                launch_pdl(K.bf_c, egrid, block, pargs[p0], 0, c->stream);
             } else if (solver == CVK_BICGSTAB) {
                 if (streamed) {
                     launch_pdl(K.bi_a_s, sgrid, sblock, args, smem_for(0), c->stream);
@@ -1203,6 +1217,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     if (solver == CVK_BICGSTAB || solver == CVK_COCG) {
         CK(launch_pdl(solver == CVK_COCG ? K.cg_init : K.bi_init, grid, block, args, 0, c->stream));
         launches += 1;
+        if (fold) {
+            CK(launch_pdl(K.bf_init, dim3(1), dim3(1), args, 0, c->stream));
+            launches += 1;
+        }
     } else {
         CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
         CK(launch_pdl(K.tf_init2, grid, block, args, smem, c->stream));

@@ -29,6 +29,15 @@
 // Vector algebra of the outer loop runs on this file's kernels and the
 // library's double-double dot (cvk_blas.cu); one scalar read-back per
 // Arnoldi dot.
+//
+// Several ranks (one GPU each): rank r builds and solves only the subdomains
+// q with q % n_ranks == r; every other operation of the outer loop runs
+// redundantly on every rank on full-length vectors.  After the local solves
+// each rank holds M^-1 r on its own subdomains' owned rows and zero
+// elsewhere, and a caller-supplied sum over ranks (cvk_asm_set_reducer:
+// NCCL / gloo all-reduce of n complex values) completes it -- every entry has
+// one nonzero contributor, so the sum is exact and the iterates are bitwise
+// those of one rank.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -94,6 +103,7 @@ __global__ void k_sub(int n, const double2* __restrict__ b, const double2* __res
 }
 
 struct Sub {
+    int q = 0;  // global subdomain id
     cvk_csr* A = nullptr;
     cvk_prec* M = nullptr;
     int n_ext = 0, n_own = 0;
@@ -121,6 +131,10 @@ struct cvk_asm {
     int64_t last_inner = 0;                    // inner iterations of the last application
     int last_brk = 0;
     double inner_device_s = 0.0;
+    int rank = 0, n_ranks = 1;
+    cvk_asm_reduce_fn reduce = nullptr;        // sum over ranks of the owned-row results
+    void* reduce_user = nullptr;
+    double* reduce_buf = nullptr;              // caller's device buffer (n complex) or null
 };
 
 // ||x||^2 or <x, y> (double-double sums, cvk_blas.cu)
@@ -133,14 +147,15 @@ static int dev_dot(cvk_asm* S, int n, const double2* x, const double2* y, double
 
 extern "C" {
 
-int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, const uint64_t* ci, const double* v,
-                   int64_t n_parts, const int64_t* part_of_row, int64_t overlap, const double* s_robin, double h,
-                   const cvk_opts* inner, int inner_solver, cvk_asm** out) {
+int cvk_asm_create_rank(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, const uint64_t* ci, const double* v,
+                        int64_t n_parts, const int64_t* part_of_row, int64_t overlap, const double* s_robin, double h,
+                        const cvk_opts* inner, int inner_solver, int rank, int n_ranks, cvk_asm** out) {
     if (!ctx || !rp || !part_of_row || !inner || !out || !s_robin)
         return afail(CVK_EINVAL, "cvk_asm_create: null argument");
     if (n < 1 || n_parts < 1 || overlap < 0 || !(h > 0))
         return afail(CVK_EINVAL, "cvk_asm_create: need n >= 1, n_parts >= 1, overlap >= 0, h > 0");
     if (inner_solver < 0 || inner_solver > 4) return afail(CVK_ESOLVER, "cvk_asm_create: unknown inner solver");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return afail(CVK_EINVAL, "cvk_asm_create: bad rank / n_ranks");
     std::vector<std::vector<int64_t>> own((size_t)n_parts);
     for (int64_t i = 0; i < n; ++i) {
         const int64_t q = part_of_row[i];
@@ -156,6 +171,8 @@ int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, con
     S->inner = *inner;
     S->inner.record_history = 0;
     S->inner_solver = inner_solver;
+    S->rank = rank;
+    S->n_ranks = n_ranks;
     AC(cvk_csr_upload(ctx, n, n, nnz, rp, ci, v, &S->A));
     const Cx s(s_robin[0], s_robin[1]);
     const Cx theta = (Cx(1.0 / h) - 0.5 * s) / (Cx(1.0 / h) + 0.5 * s);  // schwarz.cpp:43-50
@@ -164,6 +181,7 @@ int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, con
     std::vector<char> mark((size_t)n, 0);
     size_t max_ext = 1;
     for (int64_t q = 0; q < n_parts; ++q) {
+        if (q % n_ranks != rank) continue;  // another rank's subdomain
         // E_q: the owned rows grown by `overlap` graph layers
         std::vector<int64_t> ext = own[(size_t)q];
         for (int64_t i : ext) mark[(size_t)i] = 1;
@@ -205,6 +223,7 @@ int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, con
             lrp[(size_t)k + 1] = lci.size();
         }
         Sub sb;
+        sb.q = (int)q;
         sb.n_ext = (int)m;
         sb.n_own = (int)own_pos.size();
         AC(cvk_csr_upload(ctx, m, m, (int64_t)lci.size(), lrp.data(), lci.data(),
@@ -224,6 +243,21 @@ int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, con
     AK(cudaMalloc(&S->d_part, sizeof(double2) * 2048));
     AK(cudaMalloc(&S->d_dot, sizeof(double2)));
     *out = S.release();
+    return CVK_OK;
+}
+
+int cvk_asm_create(cvk_ctx* ctx, int64_t n, int64_t nnz, const uint64_t* rp, const uint64_t* ci, const double* v,
+                   int64_t n_parts, const int64_t* part_of_row, int64_t overlap, const double* s_robin, double h,
+                   const cvk_opts* inner, int inner_solver, cvk_asm** out) {
+    return cvk_asm_create_rank(ctx, n, nnz, rp, ci, v, n_parts, part_of_row, overlap, s_robin, h, inner, inner_solver,
+                               0, 1, out);
+}
+
+int cvk_asm_set_reducer(cvk_asm* S, cvk_asm_reduce_fn fn, void* user, double* buf_dev) {
+    if (!S) return afail(CVK_EINVAL, "cvk_asm_set_reducer: null argument");
+    S->reduce = fn;
+    S->reduce_user = user;
+    S->reduce_buf = buf_dev;
     return CVK_OK;
 }
 
@@ -253,6 +287,7 @@ int cvk_asm_apply_device(cvk_asm* S, const double* r_dev, double* z_dev) {
     double2* z = (double2*)z_dev;
     S->last_inner = 0;
     S->last_brk = 0;
+    if (S->n_ranks > 1) AK(cudaMemsetAsync(z, 0, sizeof(double2) * (size_t)S->n, S->st));
     for (Sub& sb : S->subs) {
         k_gather<<<grid_for(sb.n_ext), kThreads, 0, S->st>>>(sb.n_ext, sb.d_idx, r, S->d_rl);
         AK(cudaGetLastError());
@@ -264,6 +299,19 @@ int cvk_asm_apply_device(cvk_asm* S, const double* r_dev, double* z_dev) {
         if (rep.breakdown) S->last_brk = 1;
         k_scatter_own<<<grid_for(sb.n_own), kThreads, 0, S->st>>>(sb.n_own, sb.d_own, sb.d_idx, S->d_xl, z);
         AK(cudaGetLastError());
+    }
+    if (S->n_ranks > 1) {
+        if (!S->reduce) return afail(CVK_EINVAL, "cvk_asm_apply: several ranks need cvk_asm_set_reducer");
+        const size_t nb = sizeof(double2) * (size_t)S->n;
+        double* zb = S->reduce_buf ? S->reduce_buf : (double*)z;
+        if (S->reduce_buf) AK(cudaMemcpyAsync(zb, z, nb, cudaMemcpyDeviceToDevice, S->st));
+        AK(cudaStreamSynchronize(S->st));
+        int64_t meta[2] = {S->last_inner, S->last_brk};
+        const int rc = S->reduce(S->reduce_user, zb, S->n, meta);
+        if (rc != 0) return afail(CVK_ECUDA, "cvk_asm_apply: reducer failed");
+        if (S->reduce_buf) AK(cudaMemcpyAsync(z, zb, nb, cudaMemcpyDeviceToDevice, S->st));
+        S->last_inner = meta[0];
+        S->last_brk = (int)meta[1];
     }
     return CVK_OK;
 }

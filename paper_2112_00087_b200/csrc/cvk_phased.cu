@@ -48,6 +48,8 @@ struct PArgs {
     int capk;           // nnz capacity of a 256-row chunk (streamed kernels)
     int nst[5];         // ring depths of k_bi_a_s, k_bi_b_s, k_tf_e_s, k_tf_o_s, k_cg_a_s
     int pf_rows;        // StreamLayout::pf_rows (L2 prefetch of the forward gather band)
+    int gprod[3];       // k_bf_*: grids of the producers of partial regions 0 (C / init), 1 (A), 2 (B)
+    int gstride;        // k_bf_*: partial region stride = max grid
 };
 
 // ------------------------------------------------------------ tracing --
@@ -956,6 +958,248 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_tf_o_s(PArgs a) {
     tf_even_head(st, tot[0]);
 }
 
+// ------------------------------- BiCGSTAB with consumer-folded reductions --
+// The three streamed BiCGSTAB phases without a last-CTA fold: every CTA
+// publishes its double-double partials and exits; the NEXT kernel's CTAs each
+// fold them (one warp per reduction, fold_one) and run the scalar recurrence
+// redundantly -- the same bits in every CTA, the same order of checks as the
+// last-CTA kernels above -- so the fold leaves the critical path of the
+// phase boundary, and the consumer's producer warp starts the ring while its
+// consumer warps fold.  Scalars are double-buffered by launch parity
+// (PState::scal[par] read, scal[par ^ 1] written by CTA 0); `done`,
+// the report fields and the history are written by CTA 0 only, and a kernel
+// that sets `done` processes no rows in any CTA.
+
+__device__ __forceinline__ double2* bf_part(const PArgs& a, int region) {
+    return a.part + (size_t)region * kPhSlots * a.gstride;
+}
+
+// CTA partials of K reductions into region (no arrival counting)
+template <int K, int NT>
+__device__ __forceinline__ void bf_publish(const CAcc (&acc)[K], const PArgs& a, int region) {
+    __shared__ CAcc sm[K][32];
+    CAcc v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = acc[k];
+    cta_sum_k<K, NT>(v, sm);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) cacc_store(bf_part(a, region), k, a.gstride, blockIdx.x, v[k]);
+}
+
+// every CTA: fold K reductions of region (producer grid g) -> tot (all threads)
+template <int K>
+__device__ __forceinline__ void bf_fold(const PArgs& a, int region, double2 (&tot)[K]) {
+    __shared__ double2 res[K];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = a.gprod[region];
+    for (int k = warp; k < K; k += (int)(blockDim.x >> 5)) {
+        const double2 t = fold_one(bf_part(a, region), k, a.gstride, lane);
+        if (lane == 0) res[k] = t;
+    }
+    (void)g;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = res[k];
+}
+
+__device__ __forceinline__ void bf_hist(const PArgs& a, PState* st, double v) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st_hist(a, st, v);
+}
+
+// A: evaluate the previous C (end of iteration it - 1) and the top of
+// iteration it; then p = r + beta (p - omega v), v = M^-1 A p, <shadow, v>
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bf_a_s(PArgs a, int par) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    BiScal S = st->scal[par];
+    TR(1, S.it + (S.first ? 0 : 1), 0);
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!S.first) {
+        double2 tot[2];
+        bf_fold<2>(a, 0, tot);
+        const double relres = sqrt(tot[0].x) / st->bnorm;  // krylov.cpp:124-132
+        if (lead) { st->final_relres = relres; st->iters = S.it; }
+        bf_hist(a, st, relres);
+        if (relres <= st->tol) { if (lead) { st->done = 1; st->conv = 1; } return; }
+        S.it++;
+        S.cur ^= 1;
+        // top of iteration S.it (krylov.cpp:81-96)
+        if (S.it > st->max_iter) { if (lead) st->done = 1; return; }
+        if (cvk_abs(tot[1]) < st->brk) {
+            if (lead) { st->done = 1; st->brk_code = 1; st->iters = S.it - 1; }
+            return;
+        }
+        S.beta = cvk_mul(cvk_cdiv(tot[1], S.rho), cvk_cdiv(S.alpha, S.omega));
+        S.rho = tot[1];
+    }
+    const bool first = S.first != 0;
+    if (lead) { BiScal W = S; W.first = 0; st->scal[par ^ 1] = W; }
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = S.cur;
+    const double2 beta = S.beta, nom = cvk_neg(S.omega);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pc = cur ? V.p1 : V.p0;
+    const double2* __restrict__ vc = cur ? V.v1 : V.v0;
+    double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    const double2* vecs[5] = {r, pc, vc, V.sh, a.dinv};
+    StreamLayout L{a.capk, 5, a.nst[0]};
+    L.ngather = 3;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[1] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {
+            const double2 rc = ch.v(0, l);
+            if (first || (kPreHook && l < kStreamRows)) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(ch.v(1, l), cvk_mul(nom, ch.v(2, l)))), rc);
+        };
+        auto xg = [&](int c) -> double2 {
+            const double2 rc = r[c];
+            if (first) return rc;
+            return cvk_add(cvk_mul(beta, cvk_add(pc[c], cvk_mul(nom, vc[c]))), rc);
+        };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 vi = prec_staged(a, ch, 4, t, y);
+        const int row = ch.r0 + t;
+        pn[row] = xs(t);
+        vn[row] = vi;
+        acc_dot(acc[0], ch.v(3, t), vi);
+    }, SPROF(1), PreIf<kPreHook>([&](int t, const Chunk& ch) {
+        if (!first)
+            ch.set(0, t, cvk_add(cvk_mul(beta, cvk_add(ch.v(1, t), cvk_mul(nom, ch.v(2, t)))), ch.v(0, t)));
+    }));
+    TR(1, S.it, 1);
+    bf_publish<1, kStreamThreads>(acc, a, 1);
+    TR(1, S.it, 2);
+}
+
+// B: alpha = rho / <shadow, v>; s = r - alpha v, t = M^-1 A s, x += alpha p;
+// ||s||^2, <t,t>, <t,s>
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bf_b_s(PArgs a, int par) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    BiScal S = st->scal[par];
+    TR(2, S.it, 0);
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    {
+        double2 tot[1];
+        bf_fold<1>(a, 1, tot);
+        if (cvk_abs(tot[0]) < st->brk) {  // krylov.cpp:99-103
+            if (lead) { st->done = 1; st->brk_code = 2; st->iters = S.it - 1; }
+            return;
+        }
+        S.alpha = cvk_cdiv(S.rho, tot[0]);
+    }
+    if (lead) st->scal[par ^ 1] = S;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const int cur = S.cur;
+    const double2 alpha = S.alpha, nal = cvk_neg(S.alpha);
+    const double2* __restrict__ r = V.r;
+    const double2* __restrict__ pn = cur ? V.p0 : V.p1;
+    const double2* __restrict__ vn = cur ? V.v0 : V.v1;
+    double2* __restrict__ s = V.s;
+    double2* __restrict__ t_ = V.t;
+    double2* __restrict__ x = a.x;
+    const double2* vecs[5] = {r, vn, a.dinv, pn, x};
+    StreamLayout L{a.capk, 5, a.nst[1]};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[3] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {
+            return (kPreHook && l < kStreamRows) ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+        };
+        auto xg = [&](int c) -> double2 { return cvk_add(r[c], cvk_mul(nal, vn[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 ti = prec_staged(a, ch, 2, t, y);
+        const double2 si = xs(t);
+        const int row = ch.r0 + t;
+        s[row] = si;
+        t_[row] = ti;
+        x[row] = cvk_add(ch.v(4, t), cvk_mul(alpha, ch.v(3, t)));
+        acc_norm(acc[0], si);
+        acc_dot(acc[1], ti, ti);
+        acc_dot(acc[2], ti, si);
+    }, SPROF(2), PreIf<kPreHook>([&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
+    }));
+    TR(2, S.it, 1);
+    bf_publish<3, kStreamThreads>(acc, a, 2);
+    TR(2, S.it, 2);
+}
+
+// C: half-step exit / omega breakdown / omega; x += omega s, r = s - omega t;
+// ||r||^2, <shadow, r>
+__global__ void __launch_bounds__(kThreads) k_bf_c(PArgs a, int par) {
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    BiScal S = st->scal[par];
+    TR(0, S.it, 0);
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    {
+        double2 tot[3];
+        bf_fold<3>(a, 2, tot);
+        const double relres = sqrt(tot[0].x) / st->bnorm;
+        if (relres <= st->tol) {  // half-step exit (krylov.cpp:107-114)
+            if (lead) { st->done = 1; st->conv = 1; st->iters = S.it; st->final_relres = relres; }
+            bf_hist(a, st, relres);
+            return;
+        }
+        if (cvk_abs(tot[1]) < st->brk) {  // krylov.cpp:117-121
+            if (lead) { st->done = 1; st->brk_code = 3; st->iters = S.it; }
+            return;
+        }
+        S.omega = cvk_cdiv(tot[2], tot[1]);
+    }
+    if (lead) st->scal[par ^ 1] = S;
+    const int n = a.A.n;
+    BiVecs V(a.work, (size_t)n);
+    const double2 omega = S.omega, nom = cvk_neg(S.omega);
+    CAcc acc[2] = {};
+    const double2* __restrict__ s = V.s;
+    const double2* __restrict__ t = V.t;
+    const double2* __restrict__ sh = V.sh;
+    double2* __restrict__ r = V.r;
+    double2* __restrict__ x = a.x;
+    struct L4 { double2 s, t, sh, x; };
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L4{s[i], t[i], sh[i], x[i]}; },
+        [&](int i, const L4& v) {
+            x[i] = cvk_add(v.x, cvk_mul(omega, v.s));
+            const double2 ri = cvk_add(v.s, cvk_mul(nom, v.t));
+            r[i] = ri;
+            acc_norm(acc[0], ri);
+            acc_dot(acc[1], v.sh, ri);
+        });
+    TR(0, S.it, 1);
+    bf_publish<2, kThreads>(acc, a, 0);
+    TR(0, S.it, 2);
+}
+
+// after k_bi_init (r0, shadow, x0, ||r0||, <r0, r0>, top of iteration 1):
+// its scalars into scal[0] for the first k_bf_a_s
+__global__ void k_bf_init(PArgs a) {
+    pdl_enter();
+    PState* st = a.st;
+    BiScal S;
+    S.rho = st->rho;
+    S.alpha = st->alpha;
+    S.omega = st->omega;
+    S.beta = st->beta;
+    S.it = st->it;
+    S.first = st->first;
+    S.cur = st->cur;
+    st->scal[0] = S;
+}
+
 // ------------------------------------------------- true residual + report
 __global__ void __launch_bounds__(kThreads) k_true(PArgs a, double2* scratch) {
     pdl_enter();
@@ -1014,6 +1258,10 @@ PhasedKernels kernels_all() {
     k.cg_a = (const void*)k_cg_a;
     k.cg_b = (const void*)k_cg_b;
     k.cg_a_s = (const void*)k_cg_a_s;
+    k.bf_a_s = (const void*)k_bf_a_s;
+    k.bf_b_s = (const void*)k_bf_b_s;
+    k.bf_c = (const void*)k_bf_c;
+    k.bf_init = (const void*)k_bf_init;
     return k;
 }
 
@@ -1060,16 +1308,21 @@ void flavor_kernels(void* out) {
 }
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows) {
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod) {
     phased_pack_args(out, Csr{n, rp, ci, av, cmax}, dinv, b, x, work, part, (PState*)st, hist, (DevReport*)rep,
-                     capk, nst, pf_rows);
+                     capk, nst, pf_rows, gprod);
 }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, const int* nst, int pf_rows) {
+                      int capk, const int* nst, int pf_rows, const int* gprod) {
     PArgs* p = (PArgs*)out;
     p->pf_rows = pf_rows;
+    p->gstride = 0;
+    for (int i = 0; i < 3; ++i) {
+        p->gprod[i] = gprod ? gprod[i] : 0;
+        p->gstride = p->gprod[i] > p->gstride ? p->gprod[i] : p->gstride;
+    }
     p->capk = capk;
     for (int i = 0; i < 5; ++i) p->nst[i] = nst[i];
     p->A = A;

@@ -11,8 +11,17 @@ namespace cvk {
 struct Csr;
 struct DevReport;
 
+// BiCGSTAB scalars of the consumer-fold kernels (k_bf_*), double-buffered by
+// launch parity: a kernel reads scal[par] and its CTA 0 writes scal[par ^ 1].
+struct BiScal {
+    double2 rho, alpha, omega, beta;
+    long long it;
+    int cur, first;
+};
+
 // Solver state carried between phase kernels (device memory).  Written only
-// by the last-arriving CTA of each phase kernel; read by the next kernel.
+// by the last-arriving CTA of each phase kernel (CTA 0 for k_bf_*); read by
+// the next kernel.
 struct PState {
     double2 rho, rho_new, alpha, omega, beta, eta;
     double bnorm, brk, tol, final_relres, tau, theta;
@@ -20,6 +29,7 @@ struct PState {
     int done, conv, brk_code, first, pending_x, cur, record, skip_true;
     int warm;  // BiCGSTAB: start from the x passed in (k_bi_init)
     unsigned counter[4];
+    BiScal scal[2];
 };
 
 struct PhasedKernels {
@@ -31,6 +41,9 @@ struct PhasedKernels {
     // COCG (beyond the reference): init, thread-per-row SpMV phase, elementwise
     // phase, streamed SpMV phase
     const void *cg_init, *cg_a, *cg_b, *cg_a_s;
+    // BiCGSTAB with the reductions folded by the consuming kernel (every CTA,
+    // redundantly): (PArgs, int parity)
+    const void *bf_a_s, *bf_b_s, *bf_c, *bf_init;
 };
 
 PhasedKernels phased_kernels();
@@ -39,6 +52,6 @@ int phased_trace_read(void* out, size_t bytes);
 size_t phased_args_size();
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,
                       double2* work, double2* part, PState* st, double* hist, DevReport* rep,
-                      int capk, const int* nst, int pf_rows);
+                      int capk, const int* nst, int pf_rows, const int* gprod = nullptr);
 
 }  // namespace cvk

@@ -37,7 +37,16 @@ def _bind(L):
     L.cvk_asm_destroy.argtypes = [P]
     L.cvk_asm_n_parts.argtypes = [P]
     L.cvk_asm_n_parts.restype = i64
+    L.cvk_asm_create_rank.argtypes = [P, i64, i64, P, P, P, i64, P, i64, P, C.c_double, C.POINTER(_lib.CvkOpts),
+                                      C.c_int, C.c_int, C.c_int, C.POINTER(P)]
+    L.cvk_asm_set_reducer.argtypes = [P, REDUCE_FN, P, P]
+    for f in ("create", "create_rank", "solve", "apply_device", "destroy", "set_reducer"):
+        getattr(L, "cvk_asm_" + f).restype = C.c_int
     L._asm_bound = True
+
+
+# int (*)(void* user, double* z_dev, int64 n, int64* meta)
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64))
 
 
 class SubdomainSchwarz:
@@ -45,7 +54,11 @@ class SubdomainSchwarz:
     device (cvk_asm_create); solve() runs the outer DDM iteration."""
 
     def __init__(self, A: CsrMatrix, part_of_row, s_robin: complex, h: float, inner: SolverOptions = None,
-                 overlap: int = 1, inner_solver: SolverId = SolverId.BiCGStab, mode: Optional[ExecMode] = None):
+                 overlap: int = 1, inner_solver: SolverId = SolverId.BiCGStab, mode: Optional[ExecMode] = None,
+                 group=None):
+        """group: a torch.distributed group (one rank per GPU): rank r solves
+        the subdomains q with q % world == r, one all-reduce per sweep
+        completes the preconditioner (cvk_asm_create_rank)."""
         L = _lib.load()
         _bind(L)
         self.L = L
@@ -61,13 +74,47 @@ class SubdomainSchwarz:
         o = _lib.CvkOpts(float(inner.tol), int(inner.max_iter), int(inner.l), int(inner.m), 0, _dev_mode(mode), 0, 0)
         h_ = P()
         p = lambda a: a.ctypes.data_as(P)  # noqa: E731
-        code = L.cvk_asm_create(Device.default().handle, A.nrows, len(v), p(rp), p(ci), p(v), self.n_parts, p(part),
-                                int(overlap), p(s), float(h), C.byref(o), int(inner_solver), C.byref(h_))
+        rank, world = 0, 1
+        if group is not None or _dist_initialized():
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        code = L.cvk_asm_create_rank(Device.default().handle, A.nrows, len(v), p(rp), p(ci), p(v), self.n_parts,
+                                     p(part), int(overlap), p(s), float(h), C.byref(o), int(inner_solver), rank, world,
+                                     C.byref(h_))
         if code in (-1, -6):
             raise InvalidArgument(_lib.last_error())
         _lib.check(code)
         self.h = h_
         self.n = A.nrows
+        self.rank, self.world = rank, world
+        if world > 1:
+            self._install_reducer(group)
+
+    def _install_reducer(self, group):
+        """Sum over ranks of each sweep's owned-row results (an all-reduce of
+        n complex values on the rank's device, plus the sweep's counters)."""
+        import torch
+        import torch.distributed as dist
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._buf = torch.zeros(2 * self.n, dtype=torch.float64, device=dev)
+        meta_t = torch.zeros(2, dtype=torch.int64)
+
+        def reduce(user, z_dev, n, meta):
+            try:
+                dist.all_reduce(self._buf, group=group)
+                meta_t[0], meta_t[1] = meta[0], meta[1]
+                m0 = meta_t[:1].clone()
+                m1 = meta_t[1:].clone()
+                dist.all_reduce(m0, group=group)
+                dist.all_reduce(m1, op=dist.ReduceOp.MAX, group=group)
+                torch.cuda.synchronize(dev)
+                meta[0], meta[1] = int(m0[0]), int(m1[0])
+                return 0
+            except Exception:  # the C side reports CVK_ECUDA
+                return 1
+
+        self._reduce_cb = REDUCE_FN(reduce)  # keep alive
+        _lib.check(self.L.cvk_asm_set_reducer(self.h, self._reduce_cb, None, C.c_void_p(self._buf.data_ptr())))
 
     def solve(self, b, tol: float = 1e-8, max_outer: int = 300, m: int = 30) -> DdmResult:
         b = np.ascontiguousarray(b, np.complex128)
@@ -96,12 +143,22 @@ class SubdomainSchwarz:
             pass
 
 
+def _dist_initialized() -> bool:
+    try:
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    except Exception:
+        return False
+
+
 def schwarz_solve_subdomains(A: CsrMatrix, b, part_of_row, s_robin: complex, h: float,
                              inner: SolverOptions = None, ddm_tol: float = 1e-8, max_outer: int = 300,
                              m: int = 30, overlap: int = 1, inner_solver: SolverId = SolverId.BiCGStab,
-                             mode: Optional[ExecMode] = None) -> DdmResult:
-    """One call: build the subdomain systems, run the outer iteration, free."""
-    S = SubdomainSchwarz(A, part_of_row, s_robin, h, inner, overlap, inner_solver, mode)
+                             mode: Optional[ExecMode] = None, group=None) -> DdmResult:
+    """One call: build the subdomain systems, run the outer iteration, free.
+    Under torch.distributed (or with `group`) the subdomains are split over
+    the ranks, one GPU each."""
+    S = SubdomainSchwarz(A, part_of_row, s_robin, h, inner, overlap, inner_solver, mode, group)
     try:
         return S.solve(b, ddm_tol, max_outer, m)
     finally:

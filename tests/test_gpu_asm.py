@@ -7,11 +7,13 @@ DDM == monodomain.  The reference monodomain solve (oracle/_ref when built,
 else the bitwise C restatement) of the same FEM system at tol 1e-12 is the
 target; the DDM must land within its own tolerance of it."""
 import math
+import os
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -99,3 +101,57 @@ def test_fd_cavity_strips_as_algebraic_subdomains(cvk, oracle):
                                  ddm_tol=1e-10, max_outer=200, m=30)
     assert r.report.converged
     assert np.linalg.norm(r.x - x_ref) / np.linalg.norm(x_ref) <= 1e-8
+
+
+def _rank_worker(rank, world, port, q):
+    import os
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2112_00087_b200 as P
+        from paper_2112_00087_b200 import fem3d as F
+        from paper_2112_00087_b200.ddm_fem import schwarz_solve_subdomains
+        from paper_2112_00087_b200.rowblock import rcb_partition
+        cav = F.build_cavity(10)
+        om = 2 * math.pi * 100.0
+        r = schwarz_solve_subdomains(cav.matrix(om), cav.b, rcb_partition(cav.coords(), 4), complex(2.0, om / 340.0),
+                                     cav.lx / cav.nx, P.SolverOptions(tol=1e-11), ddm_tol=1e-9, max_outer=200, m=40)
+        q.put((rank, r.x, r.report.outer_iterations, r.report.total_inner_iterations,
+               list(r.report.interface_residual_history)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_subdomains_split_over_ranks_bitwise(cvk, fem):
+    """One subdomain set split over 2 ranks (sharing cuda:0 over gloo): each
+    rank solves its own subdomains, one all-reduce per sweep -- bitwise the
+    single-rank DDM (north_star: subdomains partitioned across GPUs)."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2112_00087_b200.ddm_fem import schwarz_solve_subdomains
+    from paper_2112_00087_b200.rowblock import rcb_partition
+    P = cvk
+    cav, om, _ = fem
+    one = schwarz_solve_subdomains(cav.matrix(om), cav.b, rcb_partition(cav.coords(), 4), complex(2.0, om / 340.0),
+                                   cav.lx / cav.nx, P.SolverOptions(tol=1e-11), ddm_tol=1e-9, max_outer=200, m=40)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = [q.get(timeout=600) for _ in procs]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for rank, x, outer, inner, hist in got:
+        assert outer == one.report.outer_iterations
+        assert inner == one.report.total_inner_iterations
+        assert hist == one.report.interface_residual_history
+        assert np.array_equal(np.ascontiguousarray(x).view(np.uint64), np.ascontiguousarray(one.x).view(np.uint64))

@@ -442,3 +442,31 @@ def test_stream_flavors_bitwise(cvk, oracle, knobs, solver):
         assert a_.report.converged and a_.report.iterations == b_.report.iterations
         assert np.array_equal(bits(a_.x), bits(b_.x))
         assert a_.report.residual_history == b_.report.residual_history
+
+
+def test_consumer_folded_bicgstab_bitwise(cvk, oracle, knobs):
+    """The streamed BiCGSTAB with every reduction folded by the consuming
+    kernel (k_bf_*, default) = the last-CTA-fold kernels, bit for bit, on a
+    system large enough to stream (several graphs of 8 iterations, history,
+    max_iter exhaustion and the zero rhs)."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.0075, f=60.0, adm=0.01)
+    A = mat(P, rp, ci, v)
+    M = P.jacobi(A)
+    knobs(phased_min_n=0)
+    out = {}
+    for fold in (1, 0):
+        knobs(bicg_fold=fold)
+        r = P.bicgstab(A, b, M, P.SolverOptions(tol=1e-10, max_iter=5000, record_history=True))
+        e = P.bicgstab(A, b, M, P.SolverOptions(tol=1e-30, max_iter=13))
+        z = P.bicgstab(A, np.zeros_like(b), M)
+        out[fold] = (r, e, z)
+    (a1, e1, z1), (a0, e0, z0) = out[1], out[0]
+    assert a1.report.converged and a1.report.iterations == a0.report.iterations
+    assert np.array_equal(bits(a1.x), bits(a0.x))
+    assert a1.report.residual_history == a0.report.residual_history
+    assert a1.report.final_relres == a0.report.final_relres and a1.report.true_relres == a0.report.true_relres
+    assert (e1.report.iterations, e1.report.converged) == (e0.report.iterations, e0.report.converged) == (13, False)
+    assert np.array_equal(bits(e1.x), bits(e0.x))
+    assert z1.report.converged and z1.report.iterations == 0
+
