@@ -987,17 +987,28 @@ __device__ __forceinline__ void bf_publish(const CAcc (&acc)[K], const PArgs& a,
         for (int k = 0; k < K; ++k) cacc_store(bf_part(a, region), k, a.gstride, blockIdx.x, v[k]);
 }
 
-// every CTA: fold K reductions of region (producer grid g) -> tot (all threads)
+// every CTA: fold K reductions of region -> tot (all threads).  The region's
+// slots are laid out with stride gstride, and only its producer's gprod CTAs
+// wrote partials: fold exactly those (the loads of four partials issued
+// before their adds, then the fixed xor tree -- fold_one's order).
 template <int K>
 __device__ __forceinline__ void bf_fold(const PArgs& a, int region, double2 (&tot)[K]) {
     __shared__ double2 res[K];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = a.gprod[region];
+    const int g = a.gprod[region], stride = a.gstride;
+    const double2* part = bf_part(a, region);
     for (int k = warp; k < K; k += (int)(blockDim.x >> 5)) {
-        const double2 t = fold_one(bf_part(a, region), k, a.gstride, lane);
-        if (lane == 0) res[k] = t;
+        CAcc sacc = {};
+        for (int b0 = lane; b0 < g; b0 += 128) {
+            CAcc v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = b0 + 32 * u < g ? cacc_load(part, k, stride, b0 + 32 * u) : CAcc{};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cacc_add(sacc, v[u]);
+        }
+        sacc = warp_sum(sacc);
+        if (lane == 0) res[k] = sacc.hi;
     }
-    (void)g;
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) tot[k] = res[k];

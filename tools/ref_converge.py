@@ -1,17 +1,36 @@
-"""Run the unmodified reference (oracle/_ref, ExecMode::Parallel) to convergence
-on the bench system (h=0.0017, 994,755 DOF, admittance 0.01, 100 Hz, BiCGSTAB +
-Jacobi, tol 1e-8).  Measured here (8-core Xeon): 6952 iterations, final relres
-1.0609e-9, true relres 1.0604e-9, 688 s.  bench.py uses the iteration count
-to extrapolate its bounded CPU sample (REF_ITERS)."""
-import sys, math, time
+"""Run the unmodified reference (oracle/_ref, ExecMode::Parallel, all host
+cores) to convergence on the bench system (h=0.0017, 994,755 DOF, admittance
+0.01, 100 Hz, BiCGSTAB + Jacobi, tol 1e-8), the system built by the oracle's
+restatement of build_grid/assemble (bitwise the reference's).  Validates the
+bench's bounded CPU sample x iteration count (REF_ITERS) on the host it runs
+on.  This container (8 threads): 6952 iterations, 524.5 s.  Writes
+profiles/r02_ref_full_solve.json."""
+import json
+import math
 import os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
-from oracle import oracle as O
-from paper_2112_00087_b200 import helmholtz as Hm
-g = Hm.build_grid(2.4, 1.2, 0.0017, 0.4, 0.65, 0.01)
-prob = Hm.assemble(g, 2 * math.pi * 100.0, 340.0, np.ones(g.roof_size(), np.complex128))
-A = prob.A
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+
+g = O.build_grid(2.4, 1.2, 0.0017, 0.4, 0.65, 0.01)
+rp, ci, v, b = O.assemble(g, 2 * math.pi * 100.0, 340.0, np.ones(g.roof_size, np.complex128))
 t = time.time()
-x, rep = O.ref_solve("bicgstab", A.row_offsets.astype(np.int64), A.col_indices.astype(np.int64), A.values, prob.b, tol=1e-8, max_iter=20000, parallel=True)
-print("iters", rep.iterations, "conv", rep.converged, "final", rep.final_relres, "true", rep.true_relres, "wall", time.time() - t, flush=True)
+sample = int(os.environ.get("REF_SAMPLE_ITERS", "40"))
+_, rs = O.ref_solve("bicgstab", rp, ci, v, b, tol=1e-8, max_iter=sample, parallel=True)
+t_sample = time.time() - t
+t = time.time()
+x, rep = O.ref_solve("bicgstab", rp, ci, v, b, tol=1e-8, max_iter=20000, parallel=True)
+wall = time.time() - t
+out = {"iterations": rep.iterations, "converged": rep.converged, "final_relres": rep.final_relres,
+       "true_relres": rep.true_relres, "wall_s": wall, "threads": int(O.ref().ref_omp_threads()),
+       "sample_iterations": sample, "sample_wall_s": t_sample,
+       "extrapolated_s": t_sample / sample * rep.iterations,
+       "host": os.uname().nodename}
+print(json.dumps(out), flush=True)
+os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+json.dump(out, open(os.path.join(ROOT, "profiles", "r02_ref_full_solve.json"), "w"), indent=1)
