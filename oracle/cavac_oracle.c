@@ -496,12 +496,54 @@ done_notrue:
  * krylov.cpp; conventions follow krylov.hpp:46-49: convergence on the
  * preconditioned relative residual |g_{j+1}| / ||M^{-1} b||, true relres
  * recomputed after the loop, breakdown threshold 1e-30 ||M^{-1}b||^2).
- * Arnoldi with classical Gram-Schmidt plus one reorthogonalisation (CGS2),
- * Givens rotations with real cosine (moduli as sqrt(re^2+im^2), never
- * hypot, so host and device round identically), back substitution at every
- * restart.
- * iterations counts Arnoldi steps.  The device solver follows exactly this
- * order of operations. */
+ *
+ * Arnoldi with classical Gram-Schmidt and DELAYED reorthogonalisation
+ * (DCGS2: Swirydowicz, Langou, Ananthan, Yang, Thomas, "Low synchronization
+ * Gram-Schmidt and GMRES algorithms", NLAA 2021; Bielich et al., "Low-synch
+ * Gram-Schmidt with delayed reorthogonalization for Krylov solvers",
+ * Parallel Computing 2022).  Every basis vector still gets two CGS passes,
+ * but the second pass of u_j is merged into the first pass of w = M^-1 A u_j,
+ * so a step reads the basis twice (one dot pass, one update pass) instead of
+ * three times.  Step j, with Q = [q_0 .. q_{j-1}] final and u_j the
+ * once-orthogonalised unit candidate (V[j]):
+ *   w = M^-1 A u_j
+ *   a_q = <q_q, u_j>, b_q = <q_q, w> (q < j);  a_j = <u_j, u_j>, b_j = <u_j, w>
+ *   nu = sqrt(a_j - sum |a_q|^2)               (Pythagoras: ||u_j - Q a||)
+ *   c  = (b_j - sum conj(a_q) b_q) / nu        (= <q_j, w>)
+ *   column j-1 corrected for u_j = nu q_j + Q a:
+ *     Hu[q][j-1] += Hu[j][j-1] a_q,  Hu[j][j-1] *= nu,  its rotation redone
+ *   column j: Hu[k][j] = (hf_k - sum_i Hu[k][i] a_i) / nu, hf = (b_0..b_{j-1}, c)
+ *   q_j = (u_j - Q a) / nu                     (stored over u_j)
+ *   u'  = w - Q e - gamma u_j, gamma = c / nu, e_q = b_q - a_q gamma
+ *   hn = ||u'||, Hu[j+1][j] = hn / nu (provisional until step j + 1),
+ *   u_{j+1} = u' / hn.
+ * The residual estimate at step j uses the provisional column j (rotated
+ * copy R); a restart or stop back-substitutes with it.  Givens rotations
+ * with real cosine (moduli as sqrt(re^2+im^2), never hypot, so host and
+ * device round identically).  iterations counts Arnoldi steps.  The device
+ * solvers (cvk_krylov.cu gmres_body, cvk_gmres.cu) follow exactly this order
+ * of operations. */
+static void gm_rotate(int64_t m, int64_t col, double hsub, const cplx *Hu, cplx *R, double *cs, cplx *sn,
+                      cplx *g, cplx gp) {
+    for (int64_t i = 0; i <= col; ++i) R[i * m + col] = Hu[i * m + col];
+    for (int64_t i = 0; i < col; ++i) {
+        cplx a = R[i * m + col], c2 = R[(i + 1) * m + col];
+        R[i * m + col] = cs[i] * a + sn[i] * c2;
+        R[(i + 1) * m + col] = -conj(sn[i]) * a + cs[i] * c2;
+    }
+    cplx a = R[col * m + col];
+    double aa = sqrt(creal(a) * creal(a) + cimag(a) * cimag(a));
+    double nu = sqrt(aa * aa + hsub * hsub);
+    if (aa == 0.0) { cs[col] = 0.0; sn[col] = 1.0; R[col * m + col] = hsub; }
+    else {
+        cs[col] = aa / nu;
+        sn[col] = (a / aa) * (hsub / nu);
+        R[col * m + col] = (a / aa) * nu;
+    }
+    g[col + 1] = -conj(sn[col]) * gp;
+    g[col] = cs[col] * gp;
+}
+
 void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts *o,
                cplx *x, orc_report *rep) {
     double t0 = now_s();
@@ -510,8 +552,8 @@ void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts
     memset(x, 0, (size_t)n * sizeof(cplx));
     cplx *r = cvec(n), *w = cvec(n), *tmp = cvec(n);
     cplx *V = cvec((m + 1) * n);
-    cplx *H = cvec((m + 1) * m), *g = cvec(m + 1), *sn = cvec(m), *h1 = cvec(m + 1),
-         *h2 = cvec(m + 1), *y = cvec(m);
+    cplx *Hu = cvec((m + 1) * m), *R = cvec((m + 1) * m), *g = cvec(m + 1), *gpre = cvec(m + 1), *sn = cvec(m),
+         *av = cvec(m + 1), *bv = cvec(m + 1), *ev = cvec(m + 1), *y = cvec(m);
     double *cs = calloc((size_t)m, sizeof(double));
     prec_apply(&op, b, r);
     double bnorm = orc_norm2(n, r);
@@ -532,34 +574,50 @@ void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts
         int stop = 0;
         for (int64_t j = 0; j < m; ++j) {
             total++;
-            op_apply(&op, V + j * n, w, tmp);
-            for (int64_t i = 0; i <= j; ++i) h1[i] = orc_dot(n, V + i * n, w);
-            for (int64_t i = 0; i <= j; ++i) orc_axpy(n, -h1[i], V + i * n, w);
-            for (int64_t i = 0; i <= j; ++i) h2[i] = orc_dot(n, V + i * n, w);
-            for (int64_t i = 0; i <= j; ++i) orc_axpy(n, -h2[i], V + i * n, w);
+            cplx *uj = V + j * n;
+            op_apply(&op, uj, w, tmp);
+            /* one dot pass: a_q = <V_q, u_j>, b_q = <V_q, w>, q <= j */
+            for (int64_t q = 0; q <= j; ++q) { av[q] = orc_dot(n, V + q * n, uj); bv[q] = orc_dot(n, V + q * n, w); }
+            double ss = 0.0;
+            for (int64_t q = 0; q < j; ++q) ss = ss + (creal(av[q]) * creal(av[q]) + cimag(av[q]) * cimag(av[q]));
+            double nu2 = creal(av[j]) - ss;
+            cplx cc = bv[j];
+            for (int64_t q = 0; q < j; ++q) cc = cc - conj(av[q]) * bv[q];
+            rep->iterations = total;
+            if (!(nu2 > 0.0)) { rep->breakdown = ORC_BRK_ARNOLDI; k = j; stop = 1; break; }
+            double nu = sqrt(nu2);
+            cplx c = cc / nu, gam = c / nu;
+            if (j > 0) {   /* the delayed correction of column j-1, then its rotation again */
+                cplx hjj = Hu[j * m + j - 1];
+                for (int64_t q = 0; q < j; ++q) Hu[q * m + j - 1] = Hu[q * m + j - 1] + hjj * av[q];
+                Hu[j * m + j - 1] = hjj * nu;
+                gm_rotate(m, j - 1, creal(Hu[j * m + j - 1]), Hu, R, cs, sn, g, gpre[j - 1]);
+            }
+            for (int64_t kk = 0; kk <= j; ++kk) {
+                cplx acc = kk < j ? bv[kk] : c;
+                for (int64_t i = kk > 0 ? kk - 1 : 0; i < j; ++i) acc = acc - Hu[kk * m + i] * av[i];
+                Hu[kk * m + j] = acc / nu;
+            }
+            for (int64_t q = 0; q < j; ++q) ev[q] = bv[q] - av[q] * gam;
+            /* one update pass: q_j = (u_j - Q a) / nu, u' = w - Q e - gamma u_j */
+            for (int64_t i = 0; i < n; ++i) {
+                cplx u = uj[i], qv = u, up = w[i];
+                for (int64_t q = 0; q < j; ++q) {
+                    cplx vq = V[q * n + i];
+                    qv = qv - av[q] * vq;
+                    up = up - ev[q] * vq;
+                }
+                up = up - gam * u;
+                uj[i] = qv / nu;
+                w[i] = up;
+            }
             double hn = orc_norm2(n, w);
-            for (int64_t i = 0; i <= j; ++i) H[i * m + j] = h1[i] + h2[i];
-            /* apply the previous rotations to column j */
-            for (int64_t i = 0; i < j; ++i) {
-                cplx a = H[i * m + j], c2 = H[(i + 1) * m + j];
-                H[i * m + j] = cs[i] * a + sn[i] * c2;
-                H[(i + 1) * m + j] = -conj(sn[i]) * a + cs[i] * c2;
-            }
-            cplx a = H[j * m + j];
-            double aa = sqrt(creal(a) * creal(a) + cimag(a) * cimag(a));
-            double nu = sqrt(aa * aa + hn * hn);
-            if (aa == 0.0) { cs[j] = 0.0; sn[j] = 1.0; H[j * m + j] = hn; }
-            else {
-                cs[j] = aa / nu;
-                sn[j] = (a / aa) * (hn / nu);
-                H[j * m + j] = (a / aa) * nu;
-            }
-            g[j + 1] = -conj(sn[j]) * g[j];
-            g[j] = cs[j] * g[j];
+            Hu[(j + 1) * m + j] = hn / nu;
+            gpre[j] = g[j];
+            gm_rotate(m, j, hn / nu, Hu, R, cs, sn, g, gpre[j]);
             double gabs = sqrt(creal(g[j + 1]) * creal(g[j + 1]) + cimag(g[j + 1]) * cimag(g[j + 1]));
             double relres = gabs / bnorm;
             rep->final_relres = relres;
-            rep->iterations = total;
             hist_push(rep, o, relres);
             k = j + 1;
             if (relres <= o->tol) { rep->converged = 1; stop = 1; break; }
@@ -567,11 +625,11 @@ void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts
             if (total >= o->max_iter) { stop = 1; break; }
             for (int64_t i = 0; i < n; ++i) V[(j + 1) * n + i] = w[i] / hn;
         }
-        /* back substitution H(0:k,0:k) y = g(0:k), then x += V y */
+        /* back substitution R(0:k,0:k) y = g(0:k), then x += V y */
         for (int64_t i = k; i-- > 0;) {
             cplx s = g[i];
-            for (int64_t q = i + 1; q < k; ++q) s -= H[i * m + q] * y[q];
-            y[i] = s / H[i * m + i];
+            for (int64_t q = i + 1; q < k; ++q) s -= R[i * m + q] * y[q];
+            y[i] = s / R[i * m + i];
         }
         for (int64_t q = 0; q < k; ++q) orc_axpy(n, y[q], V + q * n, x);
         if (rep->breakdown == ORC_BRK_ARNOLDI && rep->final_relres <= o->tol) {
@@ -588,8 +646,8 @@ void orc_gmres(const orc_csr *A, const cplx *dinv, const cplx *b, const orc_opts
     rep->true_relres = orc_true_relres(A, b, x);
 done_notrue:
     rep->wall_time_s = now_s() - t0;
-    free(r); free(w); free(tmp); free(V); free(H); free(g); free(sn); free(h1); free(h2);
-    free(y); free(cs);
+    free(r); free(w); free(tmp); free(V); free(Hu); free(R); free(g); free(gpre); free(sn); free(av); free(bv);
+    free(ev); free(y); free(cs);
 }
 
 /* solve krylov.cpp:395-403 dispatch; solver ids shared with the C-ABI:

@@ -1275,7 +1275,7 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     const int m = (int)o->m;
     const cvk::GmresKernels K = cvk::gmres_kernels();
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.dots, cvk::kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.dd, cvk::kThreads, 0));
     const long long blocks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, blocks);
     int e;
@@ -1306,23 +1306,15 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     if (nst < 2 || A->nnz == 0 || !c->knob.stream) nst = 0;
     SL.stages = std::max(1, nst);
     if (nst) CK(cudaFuncSetAttribute(K.spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
-    // second CGS pass from shared-memory tiles (k_g_ud_s): needs 2 stages of
-    // (m + 2) 128-row vectors
-    int ud_smem = optin - 8192 - 4096;
-    const bool ud = nst && m <= 32 && (long long)ud_smem >= 2LL * (m + 2) * 128 * 16 + 256;
-    if (ud) CK(cudaFuncSetAttribute(K.upd1_s, cudaFuncAttributeMaxDynamicSharedMemorySize, ud_smem));
-    void* uargs[2] = {nullptr, &ud_smem};
     const int pf = 2 * cvk::kStreamRows;
     std::vector<unsigned char> blob(cvk::gmres_args_size());
     cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
                          (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf);
     void* args[] = {blob.data()};
-    uargs[0] = blob.data();
     const dim3 grid((unsigned)G), block(cvk::kThreads);
     std::vector<unsigned char> key(blob);
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
-    key.push_back((unsigned char)(ud ? 1 : 0));
     if (!c->gm_exec || c->gm_key != key) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1330,12 +1322,8 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
             launch_pdl(K.x, grid, block, args, 0, c->stream);
             launch_pdl(K.spmv, grid, block, args, 0, c->stream);
             if (nst) launch_pdl(K.spmv_s, dim3((unsigned)c->nsm), dim3(cvk::kStreamThreads), args, SL.smem_bytes(), c->stream);
-            launch_pdl(K.dots, grid, block, args, 0, c->stream);
-            if (ud)
-                launch_pdl(K.upd1_s, dim3((unsigned)c->nsm), dim3(cvk::kGmresTileThreads), uargs, (size_t)ud_smem, c->stream);
-            else
-                launch_pdl(K.upd1, grid, block, args, 0, c->stream);
-            launch_pdl(K.upd2, grid, block, args, 0, c->stream);
+            launch_pdl(K.dd, grid, block, args, 0, c->stream);
+            launch_pdl(K.up, grid, block, args, 0, c->stream);
         }
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));
@@ -1357,7 +1345,7 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
         CK(cudaMemcpyAsync(&c->h_done[slot], done_ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(c->ev[slot], c->stream));
         ++graphs;
-        launches += (nst ? 6 : 5) * kIterPerGraph;
+        launches += (nst ? 5 : 4) * kIterPerGraph;
         if (graphs >= 2) {
             const int old = (int)((graphs - 2) & 1);
             CK(cudaEventSynchronize(c->ev[old]));

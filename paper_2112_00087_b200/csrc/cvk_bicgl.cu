@@ -470,12 +470,16 @@ __global__ void __launch_bounds__(kThreads, kMgsrU > 1 ? 2 : 3) k_bl_mgsr(BLArgs
     }
     {
         __shared__ const double2* cols[kMgsrW];
+        __shared__ double2* outs[kMgsrW];
         __shared__ double2 ntau[kMgsrW];
         __shared__ double2 ntp;  // pivot's pending factor
         __shared__ const double2 *piv, *rq, *r0;
         if (threadIdx.x < kMgsrW) {
             const int jj = q + c0 + (int)threadIdx.x;
             cols[threadIdx.x] = jj < L ? slot(a, st->ri[jj + 1]) : nullptr;
+            // the updated pivot goes to the spare slot: the other slices
+            // read the pivot as it was before this pass (swapped in by the fold)
+            outs[threadIdx.x] = jj < L ? slot(a, st->ri[jj == q ? L + 1 : jj + 1]) : nullptr;
             ntau[threadIdx.x] = (q > 0 && jj < L) ? cvk_neg(st->tau[(q - 1) * L + jj]) : make_double2(0, 0);
         }
         if (threadIdx.x == 0) {
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, kMgsrU > 1 ? 2 : 3) k_bl_mgsr(BLArgs
                     for (int c = 0; c < kMgsrW; ++c)
                         if (c < ncol) {
                             v[u][c] = cvk_add(v[u][c], cvk_mul(ntau[c], p[u]));
-                            const_cast<double2*>(cols[c])[i] = v[u][c];
+                            outs[c][i] = v[u][c];
                         }
                     if (y != 0) pv[u] = cvk_add(pv[u], cvk_mul(ntp, p[u]));
                 }
@@ -565,6 +569,7 @@ fold:
         __syncthreads();
         if (threadIdx.x != 0) return;
         st->counter[0] = 0;
+        if (q > 0) { const int tmp = st->ri[q + 1]; st->ri[q + 1] = st->ri[L + 1]; st->ri[L + 1] = tmp; }
         const double2 sig = res[0];
         if (cvk_abs(sig) < st->brk) { st->brk_code = 5; to_exit(st, 1); return; }  // krylov.cpp:231-236
         st->sig[q] = sig;

@@ -1,23 +1,27 @@
 // cvk_gmres.cu -- FAST-mode restarted GMRES(m) for large systems as a chain
 // of phase kernels replayed from a CUDA graph (beyond the reference, which
 // has no GMRES; operation order = the persistent kernel's gmres_body =
-// oracle/cavac_oracle.c orc_gmres: CGS2 Arnoldi, complex Givens).
+// oracle/cavac_oracle.c orc_gmres: DCGS2 Arnoldi, complex Givens).
 //
-// The persistent kernel keeps every CTA busy with one element at a time and
-// folds each of the up-to-2m inner products with its own block reduction;
-// at 1M DOF it ran at ~20% of the HBM roofline (450-500 us per Arnoldi
-// step).  Here each Arnoldi step is four kernels:
-//   k_g_spmv   V_j = src / scale (formed in the gathers), w = M^-1 A V_j
-//   k_g_dots   h1 = V^H w               -- warps own basis vectors q, lanes rows
-//   k_g_dots   w -= V h1; h2 = V^H w    -- update pass, then dot pass per block
-//   k_g_upd2   w -= V h2; ||w||; Hessenberg column, rotations, residual
-//              estimate, restart decision (last CTA)
-// and a restart is k_g_x (x += V y) + k_g_spmv in residual mode.  Every
-// reduction is double-double, so the scalars equal the persistent FAST path's.
+// Each Arnoldi step reads the basis twice (delayed reorthogonalisation,
+// cvk_dcgs2.cuh), in three kernels:
+//   k_g_spmv_s  u_j = V_j = src / scale (formed in the gathers), w = M^-1 A u_j
+//   k_g_dd      a = V^H u_j, b = V^H w in one pass (u_j, w staged per block in
+//               shared memory); last CTA: nu, the delayed correction of
+//               column j-1, column j, the update coefficients
+//   k_g_up      q_j = (u_j - V a) / nu over V_j, u' = w - V e - gamma u_j,
+//               ||u'||; last CTA: provisional rotation, residual estimate,
+//               restart decision.  Rows are walked top-down, the reverse of
+//               k_g_dd, so the tail k_g_dd left in L2 is read first.
+// The CGS2 version read the basis three times (dots; update + dots; update):
+// 307 us per step at 1M DOF (profiles/r01_gmres_5m.txt).  A restart is
+// k_g_x (x += V y) + k_g_spmv in residual mode.  Every reduction is
+// double-double, so the scalars equal the persistent FAST path's.
 #include <cuda_runtime.h>
 
 #include <cstddef>
 
+#include "cvk_dcgs2.cuh"
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 #include "cvk_stream.cuh"
@@ -38,12 +42,29 @@ struct GState {
     int done, conv, brk_code, mode, stop, j, k, wcur, skip_true, pad;
     long long total, hl, hist_cap, max_iter;
     int record, m;
-    double bnorm, brk, beta, scale, final_relres, tol, hn;
+    double bnorm, brk, beta, scale, final_relres, tol, nu;
     unsigned counter[4];
-    double2 h1[kMaxDots], h2[kMaxDots], sn[kMaxDots], gv[kMaxDots + 1], yv[kMaxDots];
+    double2 sn[kMaxDots], gv[kMaxDots + 1], gpre[kMaxDots + 1], yv[kMaxDots + 1];
+    double2 av[kMaxDots + 1], bv[kMaxDots + 1], ev[kMaxDots + 1];
     double cs[kMaxDots];
-    double2 H[(kMaxDots + 1) * kMaxDots];
+    double2 Hu[(kMaxDots + 1) * kMaxDots], R[(kMaxDots + 1) * kMaxDots];
 };
+
+__device__ __forceinline__ GmView gview(GState* st) {
+    GmView v;
+    v.Hu = st->Hu;
+    v.R = st->R;
+    v.cs = st->cs;
+    v.sn = st->sn;
+    v.g = st->gv;
+    v.gpre = st->gpre;
+    v.av = st->av;
+    v.bv = st->bv;
+    v.ev = st->ev;
+    v.nu = &st->nu;
+    v.M = st->m;
+    return v;
+}
 
 struct GArgs {
     Csr A;
@@ -83,16 +104,6 @@ __device__ __forceinline__ void ghist(const GArgs& a, GState* st, double v) {
     if (!st->record) return;
     if (st->hl < st->hist_cap) a.hist[st->hl] = v;
     st->hl++;
-}
-
-// back substitution H y = g (thread 0), then the x update is k_g_x
-__device__ void back_subst(GState* st) {
-    const int k = st->k, M = st->m;
-    for (int i = k; i-- > 0;) {
-        double2 s = st->gv[i];
-        for (int q = i + 1; q < k; ++q) s = cvk_sub(s, cvk_mul(st->H[i * M + q], st->yv[q]));
-        st->yv[i] = cvk_cdiv(s, st->H[i * M + i]);
-    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_g_init(GArgs a) {
@@ -252,239 +263,140 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_g_spmv_s(GArgs a) {
     }, nullptr, [&](int t, const Chunk& ch) { ch.set(0, t, cvk_divr(ch.v(0, t), sc)); });
 }
 
-// h = V^H w over q <= j (UPDATE: first w -= V h1 per row).  Basis vectors are
-// owned by warps (q = warp + 8 u), lanes stride the rows of a 256-row block.
-template <bool UPDATE>
-__global__ void __launch_bounds__(kThreads) k_g_dots(GArgs a) {
+// a_q = <V_q, u_j>, b_q = <V_q, w> for q <= j in one pass over the basis.
+// Blocks of kGB rows of u_j and w are staged in shared memory; warps own
+// basis vectors (q = q0 + warp + kWarps u), lanes stride the block's rows.
+constexpr int kDdQ = 4;  // basis vectors per warp and round: 32 per round
+
+__global__ void __launch_bounds__(kThreads) k_g_dd(GArgs a) {
     pdl_enter_g();
     GState* st = a.st;
     if (st->done || st->mode != G_ARN) return;
-    const int n = a.A.n, j = st->j, cnt = j + 1;
-    double2* w = vec(a, 1 + st->wcur);
+    const int n = a.A.n, j = st->j, cnt = j + 1, G = gridDim.x;
+    const double2* uj = Vq(a, j);
+    const double2* w = vec(a, 1 + st->wcur);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ double2 hs[kMaxDots];
-    if (UPDATE)
-        for (int q = threadIdx.x; q < cnt; q += blockDim.x) hs[q] = st->h1[q];
-    __syncthreads();
+    __shared__ double2 su[kGB], sw[kGB];
     const int nblk = (n + kGB - 1) / kGB;
     double2* pr = a.part;
-    auto update_block = [&](int blk) {  // w -= V h1 on one block (thread per row, 4 basis loads in flight)
-        const int i = blk * kGB + threadIdx.x;
-        if (i < n) {
-            double2 wi = w[i];
-            for (int q0 = 0; q0 < cnt; q0 += 4) {
-                double2 vq4[4];
+    for (int q0 = 0; q0 < cnt; q0 += kWarps * kDdQ) {
+        CAcc acc[kDdQ][2];
 #pragma unroll
-                for (int u4 = 0; u4 < 4; ++u4)
-                    if (q0 + u4 < cnt) vq4[u4] = Vq(a, q0 + u4)[i];
-#pragma unroll
-                for (int u4 = 0; u4 < 4; ++u4)
-                    if (q0 + u4 < cnt) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q0 + u4]), vq4[u4]));
+        for (int u = 0; u < kDdQ; ++u) acc[u][0] = acc[u][1] = CAcc{};
+        for (int blk = blockIdx.x; blk < nblk; blk += G) {
+            const int r0 = blk * kGB, rows = min(kGB, n - r0);
+            __syncthreads();
+            if ((int)threadIdx.x < rows) {
+                su[threadIdx.x] = uj[r0 + threadIdx.x];
+                sw[threadIdx.x] = w[r0 + threadIdx.x];
             }
-            w[i] = wi;
-        }
-    };
-    auto dot_block = [&](CAcc& sq, const double2* vq, int blk) {  // one basis vector, one block
-        const int r0 = blk * kGB;
+            __syncthreads();
 #pragma unroll
-        for (int e0 = 0; e0 < kGB / 32; e0 += 4) {
-            double2 vv[4], wv[4];
+            for (int u = 0; u < kDdQ; ++u) {
+                const int q = q0 + warp + kWarps * u;
+                if (q >= cnt) break;
+                const double2* vq = Vq(a, q) + r0;
+                double2 vv[kGB / 32];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int i = r0 + lane + 32 * (e0 + e);
-                if (i < n) { vv[e] = vq[i]; wv[e] = w[i]; }
-            }
+                for (int e = 0; e < kGB / 32; ++e) {
+                    const int row = lane + 32 * e;
+                    if (row < rows) vv[e] = vq[row];
+                }
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (r0 + lane + 32 * (e0 + e) < n) acc_dot(sq, vv[e], wv[e]);
-        }
-    };
-    {
-        // update every block of this CTA first, then the dots with one
-        // accumulator live at a time (measured faster than block-interleaved
-        // update+dots, whose 122 registers halve the occupancy)
-        if (UPDATE) {
-            for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) update_block(blk);
-            __syncthreads();  // the dots below read only this CTA's rows
-        }
-        for (int q = warp; q < cnt; q += kWarps) {
-            CAcc sq = {};
-            for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) dot_block(sq, Vq(a, q), blk);
-            const CAcc t = warp_sum(sq);
-            if (lane == 0) {
-                cacc_store(pr, q, gridDim.x, blockIdx.x, t);
-                __threadfence();
-            }
-        }
-    }
-    if (!arrive_last(&st->counter[UPDATE ? 1 : 0])) return;
-    double2* out = UPDATE ? st->h2 : st->h1;
-    for (int q = warp; q < cnt; q += kWarps) {
-        const double2 v = fold_one(pr, q, gridDim.x, lane);
-        if (lane == 0) out[q] = v;
-    }
-    if (threadIdx.x == 0) st->counter[UPDATE ? 1 : 0] = 0;
-}
-
-// Second CGS pass in ONE read of the basis: w -= V h1, then h2 = V^H w, on
-// row tiles of [w | V_0 .. V_j] streamed into shared memory by TMA (a ring of
-// as many stages as fit).  k_g_dots<true> reads V twice (its update pass,
-// then its dot pass); at 5M DOF that pass was ~30% of an Arnoldi step.
-// Per-row update order is that of k_g_dots<true>; h2 is double-double, so
-// the scalars equal it.
-constexpr int kTileRows = 128;                          // rows per tile = threads per consumer group
-constexpr int kTileGroups = 3;                          // consumer groups
-constexpr int kTileThreads = kTileRows * kTileGroups + 32;  // + producer warp
-constexpr int kTileWarps = kTileRows / 32;              // warps per group
-constexpr int kTileQ = 8;                               // basis vectors per warp: cnt <= 32 (m <= 32)
-
-__global__ void __launch_bounds__(kTileThreads, 1) k_g_ud_s(GArgs a, int smem_bytes) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    pdl_enter_g();
-    GState* st = a.st;
-    if (st->done || st->mode != G_ARN) return;
-    const int n = a.A.n, cnt = st->j + 1;
-    double2* w = vec(a, 1 + st->wcur);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    __shared__ double2 hs[kMaxDots];
-    __shared__ CAcc red[kTileGroups][kMaxDots];
-    for (int q = tid; q < cnt; q += blockDim.x) hs[q] = st->h1[q];
-    const size_t vb = (size_t)kTileRows * 16, sb = (size_t)(cnt + 1) * vb;
-    const int ST = (int)min((size_t)kStreamMaxStages, ((size_t)smem_bytes - 2 * kStreamMaxStages * 8) / sb);
-    uint64_t* full = (uint64_t*)(smem + (size_t)ST * sb);  // sb is a multiple of 2 KB
-    uint64_t* empty = full + kStreamMaxStages;
-    if (tid == 0) {
-        for (int q = 0; q < ST; ++q) {
-            mbar_init(full + q, 1);
-            mbar_init(empty + q, kTileRows);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int ntiles = (n + kTileRows - 1) / kTileRows, G = gridDim.x;
-    const int mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
-    if (tid >= kTileGroups * kTileRows) {  // producer warp (lane 0 issues; the loop is warp-uniform)
-        for (int i = 0; i < mine; ++i) {
-            const int s = i % ST, r0 = (blockIdx.x + i * G) * kTileRows;
-            const uint32_t bytes = (uint32_t)(min(kTileRows, n - r0) * 16);
-            if (lane == 0) {
-                mbar_wait(empty + s, ((uint32_t)(i / ST) & 1u) ^ 1u);
-                mbar_expect_tx(full + s, bytes * (uint32_t)(cnt + 1));
-                unsigned char* sp = smem + (size_t)s * sb;
-                bulk_g2s(sp, w + r0, bytes, full + s);
-                for (int q = 0; q < cnt; ++q) bulk_g2s(sp + (size_t)(q + 1) * vb, Vq(a, q) + r0, bytes, full + s);
-            }
-            __syncwarp();
-        }
-    } else {
-        const int g = tid / kTileRows, t = tid % kTileRows, wq = (tid % kTileRows) >> 5;
-        CAcc acc[kTileQ];
-#pragma unroll
-        for (int u = 0; u < kTileQ; ++u) acc[u] = CAcc{};
-        for (int i = g; i < mine; i += kTileGroups) {
-            const int s = i % ST, r0 = (blockIdx.x + i * G) * kTileRows, rows = min(kTileRows, n - r0);
-            mbar_wait(full + s, (uint32_t)(i / ST) & 1u);
-            double2* W = (double2*)(smem + (size_t)s * sb);
-            const double2* V = W + kTileRows;
-            if (t < rows) {
-                double2 wi = W[t];
-                for (int q = 0; q < cnt; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q]), V[(size_t)q * kTileRows + t]));
-                W[t] = wi;
-                w[r0 + t] = wi;
-            }
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kTileRows) : "memory");
-#pragma unroll
-            for (int u = 0; u < kTileQ; ++u) {
-                const int q = wq + kTileWarps * u;
-                if (q < cnt) {
-                    const double2* vq = V + (size_t)q * kTileRows;
-#pragma unroll
-                    for (int e = 0; e < kTileRows / 32; ++e) {
-                        const int row = lane + 32 * e;
-                        if (row < rows) acc_dot(acc[u], vq[row], W[row]);
+                for (int e = 0; e < kGB / 32; ++e) {
+                    const int row = lane + 32 * e;
+                    if (row < rows) {
+                        acc_dot(acc[u][0], vv[e], su[row]);
+                        acc_dot(acc[u][1], vv[e], sw[row]);
                     }
                 }
             }
-            mbar_arrive(empty + s);
         }
 #pragma unroll
-        for (int u = 0; u < kTileQ; ++u) {
-            const int q = wq + kTileWarps * u;
-            const CAcc tq = warp_sum(acc[u]);
-            if (q < cnt && lane == 0) red[g][q] = tq;
+        for (int u = 0; u < kDdQ; ++u) {
+            const int q = q0 + warp + kWarps * u;
+            const CAcc t0 = warp_sum(acc[u][0]), t1 = warp_sum(acc[u][1]);
+            if (q < cnt && lane == 0) {
+                cacc_store(pr, 2 * q, G, blockIdx.x, t0);
+                cacc_store(pr, 2 * q + 1, G, blockIdx.x, t1);
+            }
         }
     }
+    if (!arrive_last(&st->counter[0])) return;
+    for (int k = warp; k < 2 * cnt; k += kWarps) {
+        const double2 v = fold_one(pr, k, G, lane);
+        if (lane == 0) (k & 1 ? st->bv : st->av)[k >> 1] = v;
+    }
+    if (threadIdx.x == 0) st->counter[0] = 0;
     __syncthreads();
-    double2* pr = a.part;
-    if (tid < cnt) {
-        CAcc sq = red[0][tid];
-        for (int g = 1; g < kTileGroups; ++g) cacc_add(sq, red[g][tid]);
-        cacc_store(pr, tid, G, blockIdx.x, sq);
-        __threadfence();
-    }
-    if (!arrive_last(&st->counter[1])) return;
-    for (int q = warp; q < cnt; q += kTileThreads / 32) {
-        const double2 v = fold_one(pr, q, G, lane);
-        if (lane == 0) st->h2[q] = v;
-    }
-    if (tid == 0) st->counter[1] = 0;
+    const GmView gv = gview(st);
+    const double nu = gm_dcgs2_scalars(gv, j, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+    if (nu > 0.0 || threadIdx.x != 0) return;
+    // u_j lies in span(V_0 .. V_{j-1}): stop with the j columns built
+    st->brk_code = 7;
+    st->k = j;
+    st->stop = 1;
+    gm_back_subst(gv, j, st->yv);
+    st->mode = G_RX;
 }
 
-// w -= V h2, ||w||; then (last CTA) the Givens step of the persistent kernel
-__global__ void __launch_bounds__(kThreads) k_g_upd2(GArgs a) {
+// q_j = (u_j - V a) / nu over V_j; u' = w - V e - gamma u_j over w; ||u'||.
+// Then (last CTA) Hu[j+1][j], the provisional rotation of column j, the
+// residual estimate and the restart decision.
+__global__ void __launch_bounds__(kThreads) k_g_up(GArgs a) {
     pdl_enter_g();
     GState* st = a.st;
     if (st->done || st->mode != G_ARN) return;
-    const int n = a.A.n, j = st->j, cnt = j + 1;
+    const int n = a.A.n, j = st->j, G = gridDim.x;
+    const double nu = st->nu;
     double2* w = vec(a, 1 + st->wcur);
-    __shared__ double2 hs[kMaxDots];
-    for (int q = threadIdx.x; q < cnt; q += blockDim.x) hs[q] = st->h2[q];
+    double2* uj = Vq(a, j);
+    __shared__ double2 sa[kMaxDots + 1], se[kMaxDots + 1];
+    for (int q = threadIdx.x; q <= j; q += blockDim.x) {
+        sa[q] = st->av[q];
+        se[q] = st->ev[q];
+    }
     __syncthreads();
     CAcc acc = {};
-    for_elems(n, gridDim.x, blockIdx.x, [&](int i) {
-        double2 wi = w[i];
-        for (int q0 = 0; q0 < cnt; q0 += 4) {
-            double2 vq4[4];
+    const int nblk = (n + kGB - 1) / kGB;
+    const int last = blockIdx.x < nblk ? blockIdx.x + ((nblk - 1 - blockIdx.x) / G) * G : -1;
+    for (int blk = last; blk >= 0; blk -= G) {
+        const int i = blk * kGB + threadIdx.x;
+        if (i >= n) continue;
+        const double2 u = uj[i];
+        double2 qv = u, up = w[i];
+        constexpr int B = 8;
+        for (int q0 = 0; q0 < j; q0 += B) {
+            double2 vq[B];
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4)
-                if (q0 + u4 < cnt) vq4[u4] = Vq(a, q0 + u4)[i];
+            for (int t = 0; t < B; ++t)
+                if (q0 + t < j) vq[t] = Vq(a, q0 + t)[i];
 #pragma unroll
-            for (int u4 = 0; u4 < 4; ++u4)
-                if (q0 + u4 < cnt) wi = cvk_add(wi, cvk_mul(cvk_neg(hs[q0 + u4]), vq4[u4]));
+            for (int t = 0; t < B; ++t)
+                if (q0 + t < j) {
+                    qv = cvk_sub(qv, cvk_mul(sa[q0 + t], vq[t]));
+                    up = cvk_sub(up, cvk_mul(se[q0 + t], vq[t]));
+                }
         }
-        w[i] = wi;
-        acc_norm(acc, wi);
-    });
+        up = cvk_sub(up, cvk_mul(se[j], u));
+        uj[i] = cvk_divr(qv, nu);
+        w[i] = up;
+        acc_norm(acc, up);
+    }
     CAcc v[1] = {acc};
     __shared__ CAcc sm[1][32];
     cta_sum_k<1, kThreads>(v, sm);
-    if (threadIdx.x == 0) cacc_store(a.part + (size_t)4 * kMaxDots * gridDim.x, 0, gridDim.x, blockIdx.x, v[0]);
+    double2* pr = a.part + (size_t)4 * kMaxDots * G;
+    if (threadIdx.x == 0) cacc_store(pr, 0, G, blockIdx.x, v[0]);
     if (!arrive_last(&st->counter[3])) return;
-    const double2 tot = fold_one(a.part + (size_t)4 * kMaxDots * gridDim.x, 0, gridDim.x, threadIdx.x & 31);
+    const double2 tot = fold_one(pr, 0, G, threadIdx.x & 31);
     if (threadIdx.x != 0) return;
     st->counter[3] = 0;
     const int M = st->m;
     const double hn = sqrt(tot.x);
     st->total++;
-    double2* H = st->H;
-    for (int i = 0; i <= j; ++i) H[i * M + j] = cvk_add(st->h1[i], st->h2[i]);
-    for (int i = 0; i < j; ++i) {
-        const double2 a0 = H[i * M + j], c2 = H[(i + 1) * M + j];
-        H[i * M + j] = cvk_add(cvk_scale(st->cs[i], a0), cvk_mul(st->sn[i], c2));
-        H[(i + 1) * M + j] = cvk_add(cvk_mul(cvk_neg(cvk_conj(st->sn[i])), a0), cvk_scale(st->cs[i], c2));
-    }
-    const double2 aj = H[j * M + j];
-    const double aa = sqrt(aj.x * aj.x + aj.y * aj.y);
-    const double nu = sqrt(aa * aa + hn * hn);
-    if (aa == 0.0) {
-        st->cs[j] = 0.0; st->sn[j] = make_double2(1.0, 0.0); H[j * M + j] = make_double2(hn, 0.0);
-    } else {
-        st->cs[j] = aa / nu;
-        st->sn[j] = cvk_scale(hn / nu, cvk_divr(aj, aa));
-        H[j * M + j] = cvk_scale(nu, cvk_divr(aj, aa));
-    }
-    st->gv[j + 1] = cvk_mul(cvk_neg(cvk_conj(st->sn[j])), st->gv[j]);
-    st->gv[j] = cvk_scale(st->cs[j], st->gv[j]);
+    const GmView gv = gview(st);
+    gm_provisional(gv, j, hn, nu);
     const double2 gj1 = st->gv[j + 1];
     const double relres = sqrt(gj1.x * gj1.x + gj1.y * gj1.y) / st->bnorm;
     st->final_relres = relres;
@@ -496,7 +408,7 @@ __global__ void __launch_bounds__(kThreads) k_g_upd2(GArgs a) {
     else if (st->total >= st->max_iter) { stop = true; }
     if (stop || j + 1 == M) {
         st->stop = stop ? 1 : 0;
-        back_subst(st);
+        gm_back_subst(gv, j + 1, st->yv);
         st->mode = G_RX;
         return;
     }
@@ -555,10 +467,8 @@ GmresKernels gmres_kernels() {
     k.x = (const void*)k_g_x;
     k.spmv = (const void*)k_g_spmv;
     k.spmv_s = (const void*)k_g_spmv_s;
-    k.upd1_s = (const void*)k_g_ud_s;
-    k.dots = (const void*)k_g_dots<false>;
-    k.upd1 = (const void*)k_g_dots<true>;
-    k.upd2 = (const void*)k_g_upd2;
+    k.dd = (const void*)k_g_dd;
+    k.up = (const void*)k_g_up;
     k.true_res = (const void*)k_g_true;
     return k;
 }

@@ -30,11 +30,9 @@ size_t solver_smem(int solver, int m);
 
 // phase-kernel GMRES(m) (cvk_gmres.cu), kThreads threads per CTA
 struct GmresKernels {
-    const void *init, *x, *spmv, *dots, *upd1, *upd2, *true_res;
+    const void *init, *x, *spmv, *dd, *up, *true_res;
     const void* spmv_s;  // streamed Arnoldi SpMV: kStreamThreads threads, dynamic smem
-    const void* upd1_s;  // (GArgs, int smem_bytes): w -= V h1 and h2 = V^H w in one TMA-fed pass
 };
-constexpr int kGmresTileThreads = 3 * 128 + 32;
 GmresKernels gmres_kernels();
 size_t gmres_state_size();
 size_t gmres_args_size();

@@ -17,6 +17,7 @@
 // owner's write never races a neighbour's read.  Per element the arithmetic
 // is exactly the reference's sequence of roundings, so in REF mode (S = 1,
 // sequential sums) the iterates are bitwise those of the reference.
+#include "cvk_dcgs2.cuh"
 #include "cvk_engine.cuh"
 #include "cvk_kernels.h"
 
@@ -794,10 +795,13 @@ __device__ __forceinline__ void bicgstab_l_body(const KArgs& a, GridBar& g) {
 }
 
 // ================================================================ GMRES(m)
-// Beyond reference: left-preconditioned restarted GMRES with CGS2 Arnoldi
-// and complex Givens rotations, order of operations = orc_gmres.
+// Beyond reference: left-preconditioned restarted GMRES, Arnoldi with
+// delayed reorthogonalisation (DCGS2: one dot pass and one update pass over
+// the basis per step) and complex Givens rotations; order of operations =
+// orc_gmres, scalar side shared with the phase kernels (cvk_dcgs2.cuh).
 // work: r, W[2], V[0..m]   (m + 4 vectors)
-// dynamic shared: H[(m+1) m], sn[m], g[m+1], y[m], h1[m+1], h2[m+1] (double2), cs[m] (double)
+// dynamic shared (gmres_smem_layout): Hu, R [(m+1) m], sn[m], g, gpre, y,
+// av, bv, ev [m+1] (double2), cs[m], nu (double)
 template <int S, bool REF>
 __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     const int n = a.A.n, G = a.G, M = a.m;
@@ -808,15 +812,20 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     double2* Wb[2] = {a.work + (size_t)n, a.work + 2 * (size_t)n};
     double2* V = a.work + 3 * (size_t)n;
     extern __shared__ double2 dsm[];
-    double2* H = dsm;
-    double2* sn = H + (size_t)(M + 1) * M;
-    double2* gv = sn + M;
-    double2* yv = gv + M + 1;
-    double2* h1 = yv + M;
-    double2* h2 = h1 + M + 1;
-    double* cs = (double*)(h2 + M + 1);
-    __shared__ double2 wsum[kWarps];
-    __shared__ CAcc hsm[kMaxDots][kWarps];
+    GmView gv;
+    gv.M = M;
+    gv.Hu = dsm;
+    gv.R = gv.Hu + (size_t)(M + 1) * M;
+    gv.sn = gv.R + (size_t)(M + 1) * M;
+    gv.g = gv.sn + M;
+    gv.gpre = gv.g + M + 1;
+    double2* yv = gv.gpre + M + 1;
+    gv.av = yv + M + 1;
+    gv.bv = gv.av + M + 1;
+    gv.ev = gv.bv + M + 1;
+    gv.cs = (double*)(gv.ev + M + 1);
+    gv.nu = gv.cs + M;
+    __shared__ CAcc hsm[2 * kMaxDots + 2][kWarps];
     double2* part[kRegions];
     for (int q = 0; q < kRegions; ++q) part[q] = a.part + (size_t)q * kMaxSlots * G;
     int region = 0;
@@ -824,37 +833,48 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     long long hl = 0;
     const double tol = a.tol;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto bar = [] { __syncthreads(); };
 
-    // FAST: cnt dots <V_k, w> for k < cnt over the CTA's rows -> partials
-    auto multi_dot = [&](const double2* wv, int cnt, double2* pr) {
-        for (int k = 0; k < cnt; ++k) {
-            const double2* vk = V + (size_t)k * n;
-            CAcc s = {};
-            for_elems(n, G, g.cta, [&](int i) { acc_dot(s, vk[i], wv[i]); });
-            s = warp_sum(s);
-            if (lane == 0) hsm[k][warp] = s;
+    // FAST: <V_q, u_j> and <V_q, w> for q < cnt over the CTA's rows -> partial slots 2q, 2q+1
+    auto dual_dot = [&](const double2* uj, const double2* wv, int cnt, double2* pr) {
+        for (int q = 0; q < cnt; ++q) {
+            const double2* vq = V + (size_t)q * n;
+            CAcc s[2] = {};
+            for_elems(n, G, g.cta, [&](int i) {
+                const double2 v = vq[i];
+                acc_dot(s[0], v, uj[i]);
+                acc_dot(s[1], v, wv[i]);
+            });
+            s[0] = warp_sum(s[0]);
+            s[1] = warp_sum(s[1]);
+            if (lane == 0) {
+                hsm[2 * q][warp] = s[0];
+                hsm[2 * q + 1][warp] = s[1];
+            }
         }
         __syncthreads();
-        if (threadIdx.x < cnt) {
-            CAcc s = hsm[threadIdx.x][0];
-            for (int w2 = 1; w2 < kWarps; ++w2) cacc_add(s, hsm[threadIdx.x][w2]);
-            cacc_store(pr, threadIdx.x, G, g.cta, s);
+        for (int k = threadIdx.x; k < 2 * cnt; k += blockDim.x) {
+            CAcc s = hsm[k][0];
+            for (int w2 = 1; w2 < kWarps; ++w2) cacc_add(s, hsm[k][w2]);
+            cacc_store(pr, k, G, g.cta, s);
         }
     };
-    auto fold_multi = [&](const double2* pr, int cnt, double2* out) {
-        for (int k = warp; k < cnt; k += kWarps) {  // one warp per dot product
+    auto fold_dual = [&](const double2* pr, int cnt) {
+        for (int k = warp; k < 2 * cnt; k += kWarps) {  // one warp per dot product
             const double2 s = fold_one(pr, k, G, lane);
-            if (lane == 0) out[k] = s;
+            if (lane == 0) (k & 1 ? gv.bv : gv.av)[k >> 1] = s;
         }
         __syncthreads();
     };
-    auto seq_multi = [&](const double2* wv, int cnt, double2* out) {
+    auto seq_dual = [&](const double2* uj, const double2* wv, int cnt) {
         if (threadIdx.x == 0) {
-            for (int k = 0; k < cnt; ++k) {
-                const double2* vk = V + (size_t)k * n;
-                double2 s = make_double2(0, 0);
-                for (int i = 0; i < n; ++i) acc_dot(s, vk[i], wv[i]);
-                out[k] = s;
+            for (int q = 0; q < cnt; ++q) {
+                const double2* vq = V + (size_t)q * n;
+                double2 sa = make_double2(0, 0), sb = make_double2(0, 0);
+                for (int i = 0; i < n; ++i) acc_dot(sa, vq[i], uj[i]);
+                for (int i = 0; i < n; ++i) acc_dot(sb, vq[i], wv[i]);
+                gv.av[q] = sa;
+                gv.bv[q] = sb;
             }
         }
         __syncthreads();
@@ -889,8 +909,8 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
             if (final_relres <= tol) { conv = 1; break; }
         }
         if (threadIdx.x == 0) {
-            for (int i = 0; i <= M; ++i) gv[i] = make_double2(0, 0);
-            gv[0] = make_double2(beta, 0.0);
+            for (int i = 0; i <= M; ++i) gv.g[i] = make_double2(0, 0);
+            gv.g[0] = make_double2(beta, 0.0);
         }
         __syncthreads();
         const double2* src = r;
@@ -899,7 +919,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
         bool stop = false;
         for (int j = 0; j < M; ++j) {
             ++total;
-            // ---- S: V_j = src / scale; w = M^{-1} A V_j; h1 = V^H w
+            // ---- S: u_j = V_j = src / scale; w = M^{-1} A u_j
             double2* Vj = V + (size_t)j * n;
             double2* w = Wb[wcur];
             {
@@ -914,79 +934,46 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
                     }
                 });
                 __syncthreads();
-                double2* pr = next_part();
-                if (REF) {
-                    ok = g.sync();
-                    if (!ok) break;
-                    seq_multi(w, j + 1, h1);
-                    ok = g.sync();
-                    if (!ok) break;
-                } else {
-                    multi_dot(w, j + 1, pr);
-                    ok = g.sync();
-                    if (!ok) break;
-                    fold_multi(pr, j + 1, h1);
-                }
             }
-            // ---- R1: w -= V h1; h2 = V^H w
-            {
-                for_elems(n, G, g.cta, [&](int i) {
-                    double2 wi = w[i];
-                    for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h1[q]), V[(size_t)q * n + i]));
-                    w[i] = wi;
-                });
+            // ---- D: a = V^H u_j, b = V^H w (one pass)
+            if (REF) {
+                ok = g.sync();
+                if (!ok) break;
+                seq_dual(Vj, w, j + 1);
+                ok = g.sync();
+                if (!ok) break;
+            } else {
                 double2* pr = next_part();
-                if (REF) {
-                    ok = g.sync();
-                    if (!ok) break;
-                    seq_multi(w, j + 1, h2);
-                    ok = g.sync();
-                    if (!ok) break;
-                } else {
-                    multi_dot(w, j + 1, pr);
-                    ok = g.sync();
-                    if (!ok) break;
-                    fold_multi(pr, j + 1, h2);
-                }
+                dual_dot(Vj, w, j + 1, pr);
+                ok = g.sync();
+                if (!ok) break;
+                fold_dual(pr, j + 1);
             }
-            // ---- R2: w -= V h2; ||w||
+            const double nu = gm_dcgs2_scalars(gv, j, threadIdx.x, blockDim.x, bar);
+            if (!(nu > 0.0)) {
+                brkc = 7;
+                k = j;
+                stop = true;
+                break;
+            }
+            // ---- U: q_j = (u_j - Q a) / nu, u' = w - Q e - gamma u_j; ||u'||
             double hn;
             {
                 CAcc acc[1] = {};
                 for_elems(n, G, g.cta, [&](int i) {
-                    double2 wi = w[i];
-                    for (int q = 0; q <= j; ++q) wi = cvk_add(wi, cvk_mul(cvk_neg(h2[q]), V[(size_t)q * n + i]));
-                    w[i] = wi;
-                    if (!REF) acc_norm(acc[0], wi);
+                    const double2 up = gm_update_row(gv.av, gv.ev, j, nu, Vj[i], w[i],
+                                                     [&](int q) { return V[(size_t)q * n + i]; });
+                    w[i] = up;
+                    if (!REF) acc_norm(acc[0], up);
                 });
                 double2 tn[1];
                 ok = reduce<REF, 1>(g, acc, tn, next_part(), n, [&](int i, double2* q) { acc_norm(q[0], w[i]); });
                 if (!ok) break;
                 hn = sqrt(tn[0].x);
             }
-            // ---- Hessenberg column, rotations, residual estimate (thread 0)
-            if (threadIdx.x == 0) {
-                for (int i = 0; i <= j; ++i) H[i * M + j] = cvk_add(h1[i], h2[i]);
-                for (int i = 0; i < j; ++i) {
-                    const double2 a0 = H[i * M + j], c2 = H[(i + 1) * M + j];
-                    H[i * M + j] = cvk_add(cvk_scale(cs[i], a0), cvk_mul(sn[i], c2));
-                    H[(i + 1) * M + j] = cvk_add(cvk_mul(cvk_neg(cvk_conj(sn[i])), a0), cvk_scale(cs[i], c2));
-                }
-                const double2 aj = H[j * M + j];
-                const double aa = sqrt(aj.x * aj.x + aj.y * aj.y);
-                const double nu = sqrt(aa * aa + hn * hn);
-                if (aa == 0.0) {
-                    cs[j] = 0.0; sn[j] = make_double2(1.0, 0.0); H[j * M + j] = make_double2(hn, 0.0);
-                } else {
-                    cs[j] = aa / nu;
-                    sn[j] = cvk_scale(hn / nu, cvk_divr(aj, aa));
-                    H[j * M + j] = cvk_scale(nu, cvk_divr(aj, aa));
-                }
-                gv[j + 1] = cvk_mul(cvk_neg(cvk_conj(sn[j])), gv[j]);
-                gv[j] = cvk_scale(cs[j], gv[j]);
-            }
+            if (threadIdx.x == 0) gm_provisional(gv, j, hn, nu);
             __syncthreads();
-            const double2 gj1 = gv[j + 1];
+            const double2 gj1 = gv.g[j + 1];
             const double relres = sqrt(gj1.x * gj1.x + gj1.y * gj1.y) / bnorm;
             final_relres = relres;
             hist_push(a, g.cta, hl, relres);
@@ -1000,13 +987,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
         }
         if (!ok) break;
         // back substitution (thread 0), then x += V y
-        if (threadIdx.x == 0) {
-            for (int i = k; i-- > 0;) {
-                double2 s = gv[i];
-                for (int q = i + 1; q < k; ++q) s = cvk_sub(s, cvk_mul(H[i * M + q], yv[q]));
-                yv[i] = cvk_cdiv(s, H[i * M + i]);
-            }
-        }
+        if (threadIdx.x == 0) gm_back_subst(gv, k, yv);
         __syncthreads();
         for_elems(n, G, g.cta, [&](int i) {
             double2 xi = x[i];
@@ -1032,7 +1013,6 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
         beta = sqrt(tn[0].x);
         if (beta == 0.0) { conv = 1; final_relres = 0.0; break; }
     }
-    (void)wsum;
     double trr = 0.0;
     if (ok) ok = true_relres<S, REF>(g, a, Wb[0], next_part(), trr);
     write_report(a, g.cta, conv, brkc, total, final_relres, trr, hl, ok ? 0 : 1);
@@ -1114,7 +1094,7 @@ int solver_nwork(int solver, int l, int m) {
 
 size_t solver_smem(int solver, int m) {
     if (solver != 3) return 0;
-    return sizeof(double2) * ((size_t)(m + 1) * m + m + (m + 1) + m + 2 * (m + 1)) + sizeof(double) * m;
+    return sizeof(double2) * (2 * (size_t)(m + 1) * m + m + 6 * (size_t)(m + 1)) + sizeof(double) * (m + 1);
 }
 
 }  // namespace cvk

@@ -408,6 +408,12 @@ def test_bicgstab_l_step_kernel_bitwise_persistent(cvk, oracle, golden, knobs, l
     assert a_.report.iterations == b_.report.iterations
     assert np.array_equal(bits(a_.x), bits(b_.x))
     assert a_.report.residual_history == b_.report.residual_history
+    # repeated runs: the column slices of one right-looking MGS pass run
+    # concurrently, and none may see another's writes (a once-intermittent
+    # race on the pivot column)
+    for _ in range(4):
+        r = P.solve(P.SolverId.BiCGStabL, A, b, M, P.SolverOptions(tol=1e-10, l=l, record_history=True))
+        assert np.array_equal(bits(r.x), bits(b_.x))
     _, ro = oracle.solve("bicgstab_l", rp, ci, v, b, tol=1e-10, l=l)
     # BiCGSTAB(1) is BiCGSTAB, whose count moves with reduction order alone
     # (hard part 1): the persistent path gives the same count
