@@ -158,6 +158,8 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
 #define CVK_OPT_RB_STREAM_MIN 10   /* own rows from which row-block phases are streamed */
 #define CVK_OPT_BICG_FOLD 11       /* 1: streamed BiCGSTAB folds each reduction in the consuming
                                       kernel (default); 0: in the producer's last CTA */
+#define CVK_OPT_GMRES_TILES 12     /* 1: GMRES basis passes on bulk-copied row tiles (default,
+                                      m <= 32); 0: element-loop kernels */
 int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
 int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 

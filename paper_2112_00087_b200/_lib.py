@@ -25,7 +25,8 @@ MODE_FAST, MODE_REF, MODE_REF_PAR = 0, 1, 2
 # cvk_ctx_set_option keys (include/cavac_b200.h)
 OPTIONS = {"phased_min_n": 1, "max_ctas": 2, "stream": 3, "stream_flavor": 4, "spmv_group": 5,
            "gmres_persistent": 6, "bicgl_persistent": 7, "ilu_hostloop": 8, "ddm_seq_min": 9,
-           "rb_stream_min": 10, "bicg_fold": 11}
+           "rb_stream_min": 10, "bicg_fold": 11,
+           "gmres_tiles": 12}
 
 
 class CvkOpts(C.Structure):

@@ -59,6 +59,7 @@ struct CvkKnobs {
     long long ddm_seq_min = 131072;
     long long rb_stream_min = 65536;
     long long bicg_fold = 1;
+    long long gmres_tiles = 1;
 };
 
 struct cvk_ctx {
@@ -218,6 +219,7 @@ long long* knob_slot(cvk_ctx* c, int key) {
         case CVK_OPT_DDM_SEQ_MIN: return &c->knob.ddm_seq_min;
         case CVK_OPT_RB_STREAM_MIN: return &c->knob.rb_stream_min;
         case CVK_OPT_BICG_FOLD: return &c->knob.bicg_fold;
+        case CVK_OPT_GMRES_TILES: return &c->knob.gmres_tiles;
     }
     return nullptr;
 }
@@ -1060,7 +1062,11 @@ static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
+#ifdef CVK_NO_PDL  // measurement / debugging builds (tools/variant_build.sh)
+    cfg.numAttrs = 0;
+#else
     cfg.numAttrs = 1;
+#endif
     return cudaLaunchKernelExC(&cfg, f, args);
 }
 
@@ -1279,7 +1285,8 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     const long long blocks = std::max<long long>(1, ((long long)n + cvk::kThreads - 1) / cvk::kThreads);
     long long G = std::min<long long>(std::max(1, per_sm) * (long long)c->nsm, blocks);
     int e;
-    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(m + 4) * std::max(1, n))) != CVK_OK) return e;
+    const size_t npad = (size_t)cvk::gmres_padded_rows(std::max(1, n));
+    if ((e = ensure(c, &c->work, &c->work_bytes, sizeof(double2) * (size_t)(m + 4) * npad)) != CVK_OK) return e;
     // partials of the G-CTA kernels and of the one-CTA-per-SM streamed ones
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes,
                     sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)std::max<long long>(G, c->nsm))) != CVK_OK)
@@ -1306,15 +1313,27 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     if (nst < 2 || A->nnz == 0 || !c->knob.stream) nst = 0;
     SL.stages = std::max(1, nst);
     if (nst) CK(cudaFuncSetAttribute(K.spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
+    // the basis passes on bulk-copied tiles of the m + 1 vectors (k_g_dd_s /
+    // k_g_up_s): at least 2 stages of (m + 1) 128-row vectors
+    int tile_smem = optin - 8192 - 4096;
+    const int stage_max = cvk::gmres_tile_stage_max(m);
+    const bool tiles = nst && m <= 32 && (long long)tile_smem >= 2LL * stage_max + 256 &&
+                       c->knob.gmres_tiles;
+    if (tiles) {
+        CK(cudaFuncSetAttribute(K.dd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+        CK(cudaFuncSetAttribute(K.up_s, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));
+    }
     const int pf = 2 * cvk::kStreamRows;
     std::vector<unsigned char> blob(cvk::gmres_args_size());
     cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
-                         (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf);
+                         (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf, m);
     void* args[] = {blob.data()};
+    void* targs[] = {blob.data(), &tile_smem};
     const dim3 grid((unsigned)G), block(cvk::kThreads);
     std::vector<unsigned char> key(blob);
     const unsigned char* gp = (const unsigned char*)&G;
     key.insert(key.end(), gp, gp + sizeof(G));
+    key.push_back((unsigned char)(tiles ? 1 : 0));
     if (!c->gm_exec || c->gm_key != key) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1322,8 +1341,14 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
             launch_pdl(K.x, grid, block, args, 0, c->stream);
             launch_pdl(K.spmv, grid, block, args, 0, c->stream);
             if (nst) launch_pdl(K.spmv_s, dim3((unsigned)c->nsm), dim3(cvk::kStreamThreads), args, SL.smem_bytes(), c->stream);
-            launch_pdl(K.dd, grid, block, args, 0, c->stream);
-            launch_pdl(K.up, grid, block, args, 0, c->stream);
+            if (tiles) {
+                const dim3 tg((unsigned)c->nsm);
+                launch_pdl(K.dd_s, tg, dim3(cvk::kGmresDdsThreads), targs, (size_t)tile_smem, c->stream);
+                launch_pdl(K.up_s, tg, dim3(cvk::kGmresUpsThreads), targs, (size_t)tile_smem, c->stream);
+            } else {
+                launch_pdl(K.dd, grid, block, args, 0, c->stream);
+                launch_pdl(K.up, grid, block, args, 0, c->stream);
+            }
         }
         CK(cudaGetLastError());
         CK(cudaStreamEndCapture(c->stream, &graph));

@@ -16,6 +16,7 @@
 #pragma once
 
 #include "cvk_complex.h"
+#include "cvk_engine.cuh"
 
 namespace cvk {
 
@@ -29,21 +30,28 @@ struct GmView {
     double2* av;    // M + 1: a_q
     double2* bv;    // M + 1: b_q (bv[j] becomes c)
     double2* ev;    // M + 1: update coefficients
+    double2* yv;    // M + 1: least-squares solution of the cycle
     double* nu;     // 1
     int M;
 };
 
 // Givens rotation of column col: R[.][col] = Hu[.][col] rotated by 0..col-1,
 // then the rotation that annihilates the subdiagonal hsub; g from gp.
+// The running entry a0 is carried in registers (through memory every
+// iteration paid a store-to-load round trip: the dependent chain of the
+// last-CTA scalar step was ~15 us at j = 14 on the B200).
 __device__ __forceinline__ void gm_rotate(const GmView& v, int col, double hsub, double2 gp) {
     const int M = v.M;
-    for (int i = 0; i <= col; ++i) v.R[i * M + col] = v.Hu[i * M + col];
+    double2 a0 = v.Hu[col];
     for (int i = 0; i < col; ++i) {
-        const double2 a0 = v.R[i * M + col], c2 = v.R[(i + 1) * M + col];
-        v.R[i * M + col] = cvk_add(cvk_scale(v.cs[i], a0), cvk_mul(v.sn[i], c2));
-        v.R[(i + 1) * M + col] = cvk_add(cvk_mul(cvk_neg(cvk_conj(v.sn[i])), a0), cvk_scale(v.cs[i], c2));
+        const double2 c2 = v.Hu[(i + 1) * M + col];
+        const double ci = v.cs[i];
+        const double2 si = v.sn[i];
+        v.R[i * M + col] = cvk_add(cvk_scale(ci, a0), cvk_mul(si, c2));
+        a0 = cvk_add(cvk_mul(cvk_neg(cvk_conj(si)), a0), cvk_scale(ci, c2));
     }
-    const double2 aj = v.R[col * M + col];
+    v.R[col * M + col] = a0;
+    const double2 aj = a0;
     const double aa = sqrt(aj.x * aj.x + aj.y * aj.y);
     const double nr = sqrt(aa * aa + hsub * hsub);
     if (aa == 0.0) {
@@ -132,6 +140,62 @@ __device__ __forceinline__ double2 gm_update_row(const double2* av, const double
     up = cvk_sub(up, cvk_mul(ev[j], u));
     uj = cvk_divr(qv, nu);
     return up;
+}
+
+// FAST dot passes form canonical groups: the rows r0 + l + 32 e (e = 0..3)
+// of every 128-row-aligned sub-block [r0, r0 + 128), l = 0..31.  A group's
+// terms (zero past n) are summed in plain FP64 as (t0 + t1) + (t2 + t3) and
+// only the group sums enter the double-double accumulators: a quarter of the
+// double-double work per row and short dependency chains (the row-by-row
+// double-double pass was FP64-latency-bound at 2.2 TB/s).  Every GMRES FAST
+// path forms the same groups, so their scalars agree bit for bit whatever
+// the CTA count or the tiling.
+__device__ __forceinline__ double2 gm_tree4(const double2 (&t)[4]) {
+    return cvk_add(cvk_add(t[0], t[1]), cvk_add(t[2], t[3]));
+}
+
+// one group: <v, u> and <v, w> terms of the lane's four rows (nr valid)
+__device__ __forceinline__ void gm_group4(const double2 (&v)[4], const double2 (&u)[4], const double2 (&w)[4],
+                                          int nr, CAcc (&acc)[2]) {
+    double2 ta[4], tb[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        ta[e] = e < nr ? cvk_cmul(v[e], u[e]) : make_double2(0.0, 0.0);
+        tb[e] = e < nr ? cvk_cmul(v[e], w[e]) : make_double2(0.0, 0.0);
+    }
+    const double2 pa = gm_tree4(ta), pb = gm_tree4(tb);
+    dd_add1(acc[0].hi.x, acc[0].lo.x, pa.x);
+    dd_add1(acc[0].hi.y, acc[0].lo.y, pa.y);
+    dd_add1(acc[1].hi.x, acc[1].lo.x, pb.x);
+    dd_add1(acc[1].hi.y, acc[1].lo.y, pb.y);
+}
+
+// rows of the lane's group in a sub-block with `rows` rows: e < nr valid
+__device__ __forceinline__ int gm_group_rows(int rows, int lane) {
+    return rows > lane ? min(4, (rows - lane + 31) / 32) : 0;
+}
+
+// one 128-row sub-block (its first `rows` rows valid) from pointers to its
+// first row; NQ basis vectors at a time (the first nq valid), their loads
+// issued together
+template <int NQ>
+__device__ __forceinline__ void gm_group_dots(const double2* const (&vq)[NQ], int nq, const double2* u,
+                                              const double2* w, int rows, int lane, CAcc (&acc)[NQ][2]) {
+    const int nr = gm_group_rows(rows, lane);
+    double2 vv[NQ][4], uu[4], ww[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        if (e < nr) {
+            const int row = lane + 32 * e;
+            uu[e] = u[row];
+            ww[e] = w[row];
+#pragma unroll
+            for (int k = 0; k < NQ; ++k)
+                if (k < nq) vv[k][e] = vq[k][row];
+        }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k)
+        if (k < nq) gm_group4(vv[k], uu, ww, nr, acc[k]);
 }
 
 }  // namespace cvk

@@ -32,14 +32,21 @@ size_t solver_smem(int solver, int m);
 struct GmresKernels {
     const void *init, *x, *spmv, *dd, *up, *true_res;
     const void* spmv_s;  // streamed Arnoldi SpMV: kStreamThreads threads, dynamic smem
+    // the basis passes on bulk-copied row tiles, (GArgs, int smem_bytes), m <= 32
+    const void *dd_s, *up_s;
 };
+constexpr int kGmresDdsThreads = 512 + 32, kGmresUpsThreads = 128 + 32;
+constexpr int kGmresTileRows = 128;
 GmresKernels gmres_kernels();
 size_t gmres_state_size();
 size_t gmres_args_size();
 void gmres_init_state(void* host_state, double tol, long long max_iter, int m, int record, long long hist_cap);
 int gmres_state_done_offset();
 void gmres_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x, double2* work,
-                     double2* part, void* st, double* hist, DevReport* rep, int capk, int nst, int pf_rows);
+                     double2* part, void* st, double* hist, DevReport* rep, int capk, int nst, int pf_rows, int m);
+// work vectors of the phase kernels are padded to whole 128-row basis blocks
+long long gmres_padded_rows(long long n);
+int gmres_tile_stage_max(int m);  // bytes of the largest tile stage, j < m
 
 // phase-kernel BiCGSTAB(l) (cvk_bicgl.cu): one kernel per phase type; the
 // right-looking MGS kernel (mgsr) serves l <= kBiclMgsrL, the left-looking

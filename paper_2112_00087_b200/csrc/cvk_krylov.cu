@@ -820,6 +820,7 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     gv.g = gv.sn + M;
     gv.gpre = gv.g + M + 1;
     double2* yv = gv.gpre + M + 1;
+    gv.yv = yv;
     gv.av = yv + M + 1;
     gv.bv = gv.av + M + 1;
     gv.ev = gv.bv + M + 1;
@@ -835,21 +836,25 @@ __device__ __forceinline__ void gmres_body(const KArgs& a, GridBar& g) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto bar = [] { __syncthreads(); };
 
-    // FAST: <V_q, u_j> and <V_q, w> for q < cnt over the CTA's rows -> partial slots 2q, 2q+1
+    // FAST: <V_q, u_j> and <V_q, w> for q < cnt over the CTA's own 256-row
+    // chunks (one warp per chunk), in the canonical row groups of
+    // gm_group_dots -> partial slots 2q, 2q+1
+    const int nchunk = (n + kThreads - 1) / kThreads;
     auto dual_dot = [&](const double2* uj, const double2* wv, int cnt, double2* pr) {
         for (int q = 0; q < cnt; ++q) {
             const double2* vq = V + (size_t)q * n;
-            CAcc s[2] = {};
-            for_elems(n, G, g.cta, [&](int i) {
-                const double2 v = vq[i];
-                acc_dot(s[0], v, uj[i]);
-                acc_dot(s[1], v, wv[i]);
-            });
-            s[0] = warp_sum(s[0]);
-            s[1] = warp_sum(s[1]);
+            CAcc s[1][2] = {};
+            for (int c = g.cta + warp * G; c < nchunk; c += kWarps * G)
+                for (int h = 0; h < 2; ++h) {
+                    const int r0 = c * kThreads + 128 * h;
+                    const double2* const vb[1] = {vq + r0};
+                    if (r0 < n) gm_group_dots<1>(vb, 1, uj + r0, wv + r0, min(128, n - r0), lane, s);
+                }
+            s[0][0] = warp_sum(s[0][0]);
+            s[0][1] = warp_sum(s[0][1]);
             if (lane == 0) {
-                hsm[2 * q][warp] = s[0];
-                hsm[2 * q + 1][warp] = s[1];
+                hsm[2 * q][warp] = s[0][0];
+                hsm[2 * q + 1][warp] = s[0][1];
             }
         }
         __syncthreads();

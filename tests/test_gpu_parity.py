@@ -363,7 +363,7 @@ def test_fast_paths_bitwise_identical(cvk, golden, knobs, solver):
         assert np.array_equal(x, x0), path
 
 
-@pytest.mark.parametrize("m", [30, 7])
+@pytest.mark.parametrize("m", [30, 7, 40])
 def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, knobs, m):
     """GMRES(m) as phase kernels (cvk_gmres.cu) = the persistent kernel, bit
     for bit (same operation order, double-double dots), across restarts; and
@@ -374,15 +374,18 @@ def test_gmres_phase_kernels_bitwise_persistent(cvk, oracle, knobs, m):
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
     out = {}
-    for path, min_n in (("persistent", "1000000000"), ("phased", "0")):
-        knobs(phased_min_n=int(min_n))
+    for path, min_n, tiles in (("persistent", 1000000000, 1), ("phased", 0, 1), ("phased_loops", 0, 0)):
+        knobs(phased_min_n=min_n, gmres_tiles=tiles)
         r = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(tol=1e-11, m=m, max_iter=5000, record_history=True))
         out[path] = r
     a_, b_ = out["persistent"], out["phased"]
     assert a_.report.converged and b_.report.converged
-    assert a_.report.iterations == b_.report.iterations
-    assert np.array_equal(bits(a_.x), bits(b_.x))
-    assert a_.report.residual_history == b_.report.residual_history
+    for other in ("phased", "phased_loops"):
+        # the canonical row groups of the dot pass make every FAST path agree
+        o = out[other]
+        assert a_.report.iterations == o.report.iterations, other
+        assert np.array_equal(bits(a_.x), bits(o.x)), other
+        assert a_.report.residual_history == o.report.residual_history, other
     x_tight, _ = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-13)
     assert np.linalg.norm(b_.x - x_tight) / np.linalg.norm(x_tight) <= 1e-9
     e = P.solve(P.SolverId.GMRES, A, b, M, P.SolverOptions(m=m, max_iter=5))

@@ -16,4 +16,5 @@ for src in paper_2112_00087_b200/csrc/*.cu; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libcavac_b200.so "${objs[@]}" -lcudart -ldl
+rm -f "${objs[@]}"
 echo $out/libcavac_b200.so
