@@ -160,6 +160,9 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
                                       kernel (default); 0: in the producer's last CTA */
 #define CVK_OPT_GMRES_TILES 12     /* 1: GMRES basis passes on bulk-copied row tiles (default,
                                       m <= 32); 0: element-loop kernels */
+#define CVK_OPT_UNIFORM_OFFDIAG 13 /* 1: streamed SpMVs check each solve's matrix for off-diagonal
+                                      values that are all bitwise equal (constant-coefficient
+                                      stencils) and then stream only the diagonal (default); 0: off */
 int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
 int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 

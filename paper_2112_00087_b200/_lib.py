@@ -26,7 +26,7 @@ MODE_FAST, MODE_REF, MODE_REF_PAR = 0, 1, 2
 OPTIONS = {"phased_min_n": 1, "max_ctas": 2, "stream": 3, "stream_flavor": 4, "spmv_group": 5,
            "gmres_persistent": 6, "bicgl_persistent": 7, "ilu_hostloop": 8, "ddm_seq_min": 9,
            "rb_stream_min": 10, "bicg_fold": 11,
-           "gmres_tiles": 12}
+           "gmres_tiles": 12, "uniform_offdiag": 13}
 
 
 class CvkOpts(C.Structure):

@@ -33,7 +33,8 @@ size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod);
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod,
+                      const double2* udg);
 }  // namespace cvk_g4
 namespace cvk {
 int flavor_stream_rows();
@@ -43,7 +44,8 @@ size_t flavor_smem_bytes(int capk, int nvec, int ngather, int stages);
 void flavor_kernels(void* out);
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod);
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod,
+                      const double2* udg);
 }  // namespace cvk
 
 // execution-path options (cvk_ctx_set_option); defaults are the product's
@@ -60,6 +62,7 @@ struct CvkKnobs {
     long long rb_stream_min = 65536;
     long long bicg_fold = 1;
     long long gmres_tiles = 1;
+    long long uniform = 1;
 };
 
 struct cvk_ctx {
@@ -149,7 +152,22 @@ struct cvk_csr {
     int capk = 0;   // max nnz of a kStreamRows-row chunk, rounded up to 4 (streamed kernels)
     int capk_g4 = 0;  // the same for the 128-row chunks of the cvk_g4 flavor
     int* cmax = nullptr;  // [nchunks] largest column of each streamed chunk (L2 prefetch)
+    double2* dg = nullptr;   // [n] diagonal + [2] uniform flag / value (Csr::dg, Csr::uni), allocated at
+                             // the first streamed solve, refreshed at every streamed solve
 };
+
+// The streamed solves check the matrix for uniform off-diagonal values at the
+// start of every solve (the values change between solves: sweeps,
+// set_values): uniform_dg allocates (nullptr: the general path), the check
+// is enqueued inside the solve's timed region.
+static double2* uniform_dg(cvk_ctx* c, cvk_csr* A) {
+    if (!c->knob.uniform) return nullptr;
+    if (!A->dg && cudaMalloc(&A->dg, sizeof(double2) * ((size_t)std::max<int64_t>(1, A->n) + 2)) != cudaSuccess) {
+        A->dg = nullptr;
+        cudaGetLastError();
+    }
+    return A->dg;
+}
 
 struct cvk_prec {
     cvk_ctx* ctx = nullptr;
@@ -220,6 +238,7 @@ long long* knob_slot(cvk_ctx* c, int key) {
         case CVK_OPT_RB_STREAM_MIN: return &c->knob.rb_stream_min;
         case CVK_OPT_BICG_FOLD: return &c->knob.bicg_fold;
         case CVK_OPT_GMRES_TILES: return &c->knob.gmres_tiles;
+        case CVK_OPT_UNIFORM_OFFDIAG: return &c->knob.uniform;
     }
     return nullptr;
 }
@@ -468,6 +487,7 @@ int cvk_csr_free(cvk_csr* A) {
     cudaStreamSynchronize(A->ctx->stream);
     ctx_release(A->ctx, A->blob, A->blob_bytes);
     if (A->cmax) cudaFree(A->cmax);
+    if (A->dg) cudaFree(A->dg);
     delete A;
     return CVK_OK;
 }
@@ -1151,6 +1171,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const long long Gmax = std::max<long long>(std::max<long long>(G, Ge), c->nsm);
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)
         return e;
+    double2* udg = streamed ? uniform_dg(c, const_cast<cvk_csr*>(A)) : nullptr;
     std::vector<unsigned char> blob(cvk::phased_args_size());
     {
         // the L2 prefetch window reads A->cmax, which is per 224-row chunk
@@ -1159,7 +1180,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         const int gprod[3] = {(int)Ge, c->nsm, c->nsm};
         (g4 ? cvk_g4::flavor_pack_args : cvk::flavor_pack_args)(
             blob.data(), n, A->rp, A->ci, A->av, g4 ? nullptr : A->cmax, M->dinv, b_dev, x_dev, (double2*)c->work,
-            c->part, c->st, c->hist, c->rep, scapk, stg, pf, gprod);
+            c->part, c->st, c->hist, c->rep, scapk, stg, pf, gprod, udg);
     }
     void* args[] = {blob.data()};
     int parity[2] = {0, 1};
@@ -1219,6 +1240,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     }
     CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->e0, c->stream));
+    if (udg) CK(cvk::launch_uniform_check(n, A->rp, A->ci, A->av, udg, udg + n, c->stream));
     long long launches = 0;
     if (solver == CVK_BICGSTAB || solver == CVK_COCG) {
         CK(launch_pdl(solver == CVK_COCG ? K.cg_init : K.bi_init, grid, block, args, 0, c->stream));
@@ -1325,7 +1347,8 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     }
     const int pf = 2 * cvk::kStreamRows;
     std::vector<unsigned char> blob(cvk::gmres_args_size());
-    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax}, M->dinv, b_dev, x_dev,
+    double2* udg = nst ? uniform_dg(c, const_cast<cvk_csr*>(A)) : nullptr;
+    cvk::gmres_pack_args(blob.data(), cvk::Csr{n, A->rp, A->ci, A->av, A->cmax, udg, udg ? udg + n : nullptr}, M->dinv, b_dev, x_dev,
                          (double2*)c->work, c->part, c->gst, c->hist, c->rep, A->capk, nst, pf, m);
     void* args[] = {blob.data()};
     void* targs[] = {blob.data(), &tile_smem};
@@ -1357,6 +1380,7 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     }
     CK(cudaMemcpyAsync(c->gst, hs.data(), hs.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaEventRecord(c->e0, c->stream));
+    if (udg) CK(cvk::launch_uniform_check(n, A->rp, A->ci, A->av, udg, udg + n, c->stream));
     CK(launch_pdl(K.init, grid, block, args, 0, c->stream));
     long long launches = 1;
     const int* done_ptr = (const int*)((const char*)c->gst + cvk::gmres_state_done_offset());

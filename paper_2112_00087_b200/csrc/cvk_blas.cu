@@ -209,4 +209,45 @@ cudaError_t launch_xpay(int n, double2 alpha, double2* x, const double2* y, cuda
     return cudaGetLastError();
 }
 
+// Uniform off-diagonal check (Csr::dg / Csr::uni): uni[1] = the first
+// off-diagonal value among the first rows, uni[0].x = 1 if found; then every
+// off-diagonal value is compared with it bit for bit (a mismatch clears the
+// flag: every writer stores the same 0) and dg[row] = the row's diagonal.
+__global__ void k_uniform_ref(int n, const int* rp, const int* ci, const double2* av, double2* uni) {
+    if (threadIdx.x != 0) return;
+    uni[0] = make_double2(0.0, 0.0);
+    const int rows = min(n, 1024);
+    for (int r = 0; r < rows; ++r)
+        for (int k = rp[r]; k < rp[r + 1]; ++k)
+            if (ci[k] != r) {
+                uni[1] = av[k];
+                uni[0] = make_double2(1.0, 0.0);
+                return;
+            }
+}
+
+__global__ void k_uniform_check(int n, const int* rp, const int* ci, const double2* av, double2* dg, double2* uni) {
+    const double2 ref = uni[1];
+    const unsigned long long rx = __double_as_longlong(ref.x), ry = __double_as_longlong(ref.y);
+    bool ok = true;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        double2 d = make_double2(0.0, 0.0);
+        for (int k = rp[r]; k < rp[r + 1]; ++k) {
+            const double2 v = av[k];
+            if (ci[k] == r) d = v;
+            else ok = ok && (unsigned long long)__double_as_longlong(v.x) == rx &&
+                      (unsigned long long)__double_as_longlong(v.y) == ry;
+        }
+        dg[r] = d;
+    }
+    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) uni[0] = make_double2(0.0, 0.0);
+}
+
+cudaError_t launch_uniform_check(int n, const int* rp, const int* ci, const double2* av, double2* dg, double2* uni,
+                                 cudaStream_t st) {
+    k_uniform_ref<<<1, 32, 0, st>>>(n, rp, ci, av, uni);
+    if (n > 0) k_uniform_check<<<grid_for(n), kThreads, 0, st>>>(n, rp, ci, av, dg, uni);
+    return cudaGetLastError();
+}
+
 }  // namespace cvk

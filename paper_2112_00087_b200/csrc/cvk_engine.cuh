@@ -49,6 +49,12 @@ struct Csr {
     const int* __restrict__ ci;
     const double2* __restrict__ av;
     const int* cmax = nullptr;  // per streamed chunk: largest column index (L2 prefetch window), optional
+    // Uniform off-diagonal values (streamed SpMV only, optional): when uni[0].x
+    // != 0 every off-diagonal entry equals uni[1] bit for bit and dg holds the
+    // diagonal, so a chunk streams 16 B of values per row instead of per
+    // entry.  Checked on the device at the start of every solve (k_uniform_*).
+    const double2* dg = nullptr;
+    const double2* uni = nullptr;
 };
 
 // Kernel arguments (passed by value to cudaLaunchCooperativeKernel).

@@ -65,6 +65,9 @@ void bicgl_pack_args(void* out, const Csr& A, const double2* dinv, const double2
                      double2* part, void* st, double* hist, DevReport* rep);
 
 // standalone kernels (cvk_blas.cu); all enqueue on `st`
+// uniform off-diagonal values (Csr::dg / Csr::uni), checked per solve
+cudaError_t launch_uniform_check(int n, const int* rp, const int* ci, const double2* av, double2* dg, double2* uni,
+                                 cudaStream_t st);
 cudaError_t launch_spmv(int S, bool ref, int n, const int* rp, const int* ci, const double2* av,
                         const double2* x, double2* y, int tile, cudaStream_t st);
 // FAST SpMV on the TMA ring; cudaErrorInvalidConfiguration if a chunk does not fit

@@ -1319,9 +1319,10 @@ void flavor_kernels(void* out) {
 }
 void flavor_pack_args(void* out, int n, const int* rp, const int* ci, const double2* av, const int* cmax,
                       const double2* dinv, const double2* b, double2* x, double2* work, double2* part, void* st,
-                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod) {
-    phased_pack_args(out, Csr{n, rp, ci, av, cmax}, dinv, b, x, work, part, (PState*)st, hist, (DevReport*)rep,
-                     capk, nst, pf_rows, gprod);
+                      double* hist, void* rep, int capk, const int* nst, int pf_rows, const int* gprod,
+                      const double2* udg) {
+    phased_pack_args(out, Csr{n, rp, ci, av, cmax, udg, udg ? udg + n : nullptr}, dinv, b, x, work, part,
+                     (PState*)st, hist, (DevReport*)rep, capk, nst, pf_rows, gprod);
 }
 
 void phased_pack_args(void* out, const Csr& A, const double2* dinv, const double2* b, double2* x,

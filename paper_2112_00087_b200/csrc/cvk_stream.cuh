@@ -108,6 +108,8 @@ struct Chunk {
     const double2* av;  // values, index k - k0
     const double2* vec; // staged vectors, R rows each
     int k0, cio, r0, rows;
+    int uni;            // uniform off-diagonal: av holds the rows' diagonal, coff the rest
+    double2 coff;
     __device__ __forceinline__ double2 v(int j, int l) const { return vec[j * kStreamRows + l]; }
     __device__ __forceinline__ void set(int j, int l, double2 x) const { const_cast<double2*>(vec)[j * kStreamRows + l] = x; }
     // slot of column c in the chunk's staged rows, or -1 (global gather)
@@ -132,8 +134,8 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
 #pragma unroll
         for (int u = 0; u < BATCH; ++u)
             if (k + u < e) {
-                a[u] = ch.av[k + u];
                 c[u] = ch.ci[k + u + ch.cio];
+                a[u] = ch.uni ? (c[u] == ch.r0 + t ? ch.av[t] : ch.coff) : ch.av[k + u];
             }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u)
@@ -155,13 +157,13 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
 // done.  Chunks are assigned grid-stride (chunk = cta + i * G).
 __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L, const double2* const* vecs,
                                              unsigned char* sp, uint64_t* bar, int chunk, int k0, int k1,
-                                             int cmax) {
+                                             int cmax, bool uni) {
     const int n = A.n;
     const int r0 = chunk * kStreamRows, rows = min(kStreamRows, n - r0);
     const int a0 = k0 & ~3, a1 = (k1 + 3) & ~3;
     const uint32_t b_rp = (uint32_t)(((rows + 1 + 3) & ~3) * 4);
     const uint32_t b_ci = (uint32_t)((a1 - a0) * 4);
-    const uint32_t b_av = (uint32_t)((k1 - k0) * 16);
+    const uint32_t b_av = (uint32_t)((uni ? rows : k1 - k0) * 16);
     const uint32_t b_v = (uint32_t)(rows * 16);
     uint32_t tx = b_rp + b_ci + b_av;
     for (int j2 = 0; j2 < L.nvec; ++j2)
@@ -171,7 +173,7 @@ __device__ __forceinline__ void stream_issue(const Csr& A, const StreamLayout& L
     unsigned char* q = sp + L.rp_bytes();
     if (b_ci) bulk_g2s(q, A.ci + a0, b_ci, bar);
     q += L.ci_bytes();
-    if (b_av) bulk_g2s(q, A.av + k0, b_av, bar);
+    if (b_av) bulk_g2s(q, uni ? A.dg + r0 : A.av + k0, b_av, bar);
     q += L.av_bytes();
     for (int j2 = 0; j2 < L.nvec; ++j2) {
         if (vecs[j2]) bulk_g2s(q, vecs[j2] + r0, b_v, bar);
@@ -223,6 +225,8 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     __syncthreads();
     const int first = blockIdx.x;
     const int cnt = first < nchunks ? (nchunks - 1 - first) / G + 1 : 0;
+    const bool uni = A.dg != nullptr && __ldcg(&A.uni[0].x) != 0.0;
+    const double2 coff = uni ? __ldcg(A.uni + 1) : make_double2(0.0, 0.0);
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
         const bool pf = L.pf_rows > 0 && A.cmax != nullptr;
@@ -243,7 +247,8 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
                     const long long t0 = prof ? clock64() : 0;
                     mbar_wait(empty + s, ((uint32_t)(it / ST) & 1u) ^ 1u);
                     if (prof) pw += clock64() - t0;
-                    stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, first + it * G, k0, k1, cm);
+                    stream_issue(A, L, vecs, smem + (size_t)s * L.stage_bytes(), full + s, first + it * G, k0, k1, cm,
+                                 uni);
                 }
             }
         }
@@ -265,6 +270,8 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
             ch.rows = min(kStreamRows, n - ch.r0);
             ch.k0 = ch.rp[0];
             ch.cio = ch.k0 & 3;
+            ch.uni = uni;
+            ch.coff = coff;
             if (kPre) {
                 if (t < ch.rows) pre(t, ch);
                 asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kStreamRows) : "memory");

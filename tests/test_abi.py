@@ -47,7 +47,7 @@ def test_cvk_opts_layout(lib):
     import ctypes as C
     assert C.sizeof(lib.CvkOpts) == 48
     assert lib.CvkOpts.warm.offset == 40
-    assert set(lib.OPTIONS.values()) == set(range(1, 13))
+    assert set(lib.OPTIONS.values()) == set(range(1, 14))
 
 
 def test_no_environment_switches_in_native_code():

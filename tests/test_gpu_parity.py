@@ -479,3 +479,28 @@ def test_consumer_folded_bicgstab_bitwise(cvk, oracle, knobs):
     assert np.array_equal(bits(e1.x), bits(e0.x))
     assert z1.report.converged and z1.report.iterations == 0
 
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "tfqmr", "cocg", "gmres"])
+def test_uniform_offdiag_stream_bitwise(cvk, oracle, knobs, solver):
+    """The streamed SpMV's uniform off-diagonal format (CVK_OPT_UNIFORM_OFFDIAG,
+    checked on the device at every solve): the cavity's off-diagonal values
+    are all -c^2/h^2, so the streamed phases read the diagonal only.  On and
+    off give the same bits; with one off-diagonal value perturbed in its last
+    bit the check falls back to the general format, again the same bits."""
+    P = cvk
+    rp, ci, v, b = cavity(oracle, 0.01, f=100.0, adm=0.01)
+    rp, ci = np.asarray(rp), np.asarray(ci)
+    v2 = np.array(v, dtype=np.complex128)
+    row = (len(rp) - 1) // 2
+    k = next(k for k in range(rp[row], rp[row + 1]) if ci[k] != row)
+    v2[k] = complex(np.nextafter(v2[k].real, 0.0), v2[k].imag)
+    for vals in (v, v2):
+        A = mat(P, rp, ci, vals)
+        M = P.jacobi(A)
+        out = {}
+        for uni in (1, 0):
+            knobs(phased_min_n=0, uniform_offdiag=uni)
+            out[uni] = P.solve(P.solver_id(solver), A, b, M, P.SolverOptions(tol=1e-10, max_iter=3000))
+        assert out[1].report.iterations == out[0].report.iterations
+        assert np.array_equal(bits(out[1].x), bits(out[0].x))
