@@ -340,7 +340,7 @@ def main():
     # the streamed SpMV phases read 16 B of values per ROW when every
     # off-diagonal value is the same constant (CVK_OPT_UNIFORM_OFFDIAG, checked
     # on the device at each solve): the reference cavity's -c^2/h^2
-    uniform = uniform_offdiag(A)
+    uniform = uniform_offdiag(A) and P.option("uniform_offdiag") != 0
     if uniform:
         iter_bytes = 8 * nnz + 376 * n  # 2 SpMVs of 4 nnz + 20 n instead of 20 nnz + 4 n
         setup_bytes = (16 * n * 4) + (20 * nnz + 4 * n + 48 * n) + (20 * nnz + 4 * n + 16 * n)  # + the check

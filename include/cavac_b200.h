@@ -162,7 +162,8 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
                                       m <= 32); 0: element-loop kernels */
 #define CVK_OPT_UNIFORM_OFFDIAG 13 /* 1: streamed SpMVs check each solve's matrix for off-diagonal
                                       values that are all bitwise equal (constant-coefficient
-                                      stencils) and then stream only the diagonal (default); 0: off */
+                                      stencils) and then stream only the diagonal; 0: off (default:
+                                      the phases are consumer-bound, the bytes saved buy ~2.5%) */
 int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
 int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 

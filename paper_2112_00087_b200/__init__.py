@@ -9,7 +9,7 @@ from .cavac import (  # noqa: F401
     SolveResult, SolverId, SolverOptions, axpy, axpy_inplace, bicgstab, bicgstab_l, cocg,
     csr_from_triplets, csr_identity, dot_hermitian, exec_mode, gmres, identity_preconditioner, ilu0,
     ilu0_factor,
-    jacobi, norm2, path_options, scale_inplace, set_exec_mode, solve, solver_from_name, solver_id,
+    jacobi, norm2, option, path_options, scale_inplace, set_exec_mode, solve, solver_from_name, solver_id,
     solver_name, spmv,
     tfqmr, true_relative_residual, xpay_inplace,
 )

@@ -153,6 +153,14 @@ class path_options:
         return False
 
 
+def option(name: str) -> int:
+    """Current value of an execution-path option of the default context."""
+    L = _lib.load()
+    v = C.c_int64()
+    check(L.cvk_ctx_get_option(Device.default().handle, _lib.OPTIONS[name], C.byref(v)))
+    return int(v.value)
+
+
 # ------------------------------------------------------------- numkit ----
 
 def _cvec(x) -> np.ndarray:

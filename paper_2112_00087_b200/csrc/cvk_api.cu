@@ -62,7 +62,7 @@ struct CvkKnobs {
     long long rb_stream_min = 65536;
     long long bicg_fold = 1;
     long long gmres_tiles = 1;
-    long long uniform = 1;
+    long long uniform = 0;  // measured: 24% fewer bytes per BiCGSTAB iteration, 2.5% less time
 };
 
 struct cvk_ctx {
