@@ -307,6 +307,11 @@ def main():
     # every timed launch
     spmv_s = spmv_time(L, dev, hA, b_dev, reps=20)
     spmv_bytes = 20 * nnz + 4 * (n + 1) + 32 * n
+    spmv_traffic = None  # ncu DRAM bytes of one k_spmv_s launch (profiles/r02_traffic.json)
+    try:
+        spmv_traffic = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json"))).get("spmv_dram_bytes")
+    except Exception:
+        pass
 
     # beyond the reference: the same system with ILU(0) (3 sweeps per triangle)
     # instead of Jacobi -- a side number, not the headline (the reference has
@@ -372,7 +377,8 @@ def main():
         "seconds_per_iteration": t_solve / max(iters, 1),
         "spmv": {"gbs": spmv_bytes / spmv_s / 1e9, "seconds": spmv_s,
                  "frac": spmv_bytes / spmv_s / 1e9 / peak, "bytes": spmv_bytes,
-                 "timing": "CUDA events per launch on the library stream, L2 flushed before each of 20 launches"},
+                 "timing": "CUDA events per launch on the library stream, L2 evicted by a 256 MB read before "
+                           "each of 20 launches", "traffic": spmv_traffic},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "BiCGSTAB iteration: TMA-streamed SpMV phases k_bf_a_s + k_bf_b_s, "
@@ -429,11 +435,14 @@ def spmv_time(L, dev, hA, x_dev, reps=20):
     import torch
     st = torch.cuda.ExternalStream(L.cvk_ctx_stream(dev.handle))
     y = torch.empty_like(x_dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=x_dev.device)
+    # L2 (126 MB) evicted before every launch by READING a 256 MB buffer: a
+    # write flush (round 2's first version) leaves L2 full of dirty lines whose
+    # write-back then competes with the SpMV (34.8 vs 25.4 us in ncu)
+    flush = torch.ones(32 << 20, dtype=torch.int64, device=x_dev.device)
     times = []
     with torch.cuda.stream(st):
         for k in range(reps + 2):
-            flush.fill_(k & 0xFF)
+            flush.sum()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             from paper_2112_00087_b200 import _lib
