@@ -1166,7 +1166,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // BiCGSTAB with the reductions folded by the consuming kernel (k_bf_*)
     const bool fold = streamed && solver == CVK_BICGSTAB && c->knob.bicg_fold;
     // elementwise phases: grid-stride, 4 elements per thread per trip
-    long long Ge = std::min<long long>(2LL * c->nsm, std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
+#ifndef CVK_EGRID_MUL
+#define CVK_EGRID_MUL 2
+#endif
+    long long Ge = std::min<long long>((long long)CVK_EGRID_MUL * c->nsm,
+                                       std::max<long long>(1, (n + 4LL * cvk::kThreads - 1) / (4LL * cvk::kThreads)));
     if (!streamed) Ge = G;
     const long long Gmax = std::max<long long>(std::max<long long>(G, Ge), c->nsm);
     if ((e = ensure(c, (void**)&c->part, &c->part_bytes, sizeof(double2) * cvk::kRegions * cvk::kMaxSlots * (size_t)Gmax)) != CVK_OK)

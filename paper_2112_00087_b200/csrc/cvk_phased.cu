@@ -126,7 +126,10 @@ __device__ bool partial_last(const CAcc (&acc)[K], double2* part, unsigned* coun
 // latency-bound with one 16-byte load per vector in flight; tools/bicg_lab.cu
 // phase C: 3.5 vs 2.0 TB/s at 1M DOF).  Launched on a grid of
 // kElemCtasPerSm CTAs per SM.
-constexpr int kElemBatch = 4;
+#ifndef CVK_ELEM_BATCH
+#define CVK_ELEM_BATCH 4
+#endif
+constexpr int kElemBatch = CVK_ELEM_BATCH;
 template <int U, class LD, class STF>
 __device__ __forceinline__ void for_elems_batched(int n, LD&& ld, STF&& stf) {
     using T = decltype(ld(0));
@@ -1148,7 +1151,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bf_b_s(PArgs a, int par) 
 
 // C: half-step exit / omega breakdown / omega; x += omega s, r = s - omega t;
 // ||r||^2, <shadow, r>
-__global__ void __launch_bounds__(kThreads) k_bf_c(PArgs a, int par) {
+#ifndef CVK_BFC_MINB
+#define CVK_BFC_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, CVK_BFC_MINB) k_bf_c(PArgs a, int par) {
     pdl_enter();
     PState* st = a.st;
     if (st->done) return;
