@@ -144,3 +144,19 @@ def test_breakdown_fixture_pinned(oracle):
             assert rep.breakdown == c["breakdown"] and rep.iterations == c["iterations"]
             assert rep.final_relres.hex() == c["final_relres"]
             assert hashlib.sha256(np.ascontiguousarray(x).view(np.uint8)).hexdigest() == c["x_sha256"]
+
+
+@pytest.mark.parametrize("m", [30, 7])
+def test_gmres_dcgs2_solution(oracle, m):
+    """GMRES(m) with delayed reorthogonalisation (orc_gmres, beyond the
+    reference): on a damped cavity it converges to the reference's BiCGSTAB
+    solution at tight tolerance, and its relative residual estimate tracks the
+    true residual (the basis stays orthonormal to working accuracy)."""
+    _, rp, ci, v, b = cavity(oracle, 0.05, adm=0.02)
+    xt, rt = oracle.solve("bicgstab", rp, ci, v, b, tol=1e-13, max_iter=100000)
+    x, r = oracle.solve("gmres", rp, ci, v, b, tol=1e-11, m=m, max_iter=20000)
+    assert r.converged and r.breakdown is None
+    assert np.linalg.norm(x - xt) / np.linalg.norm(xt) <= 1e-9
+    # final_relres is GMRES's estimate (left-preconditioned); true_relres is
+    # recomputed from x: they agree to the conditioning of the preconditioner
+    assert r.true_relres <= 10 * r.final_relres
