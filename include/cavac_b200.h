@@ -156,7 +156,7 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
 #define CVK_OPT_DDM_SEQ_MIN 9      /* strip rows from which Schwarz inner solves run one after
                                       another on the single-system path (131072) */
 #define CVK_OPT_RB_STREAM_MIN 10   /* own rows from which row-block phases are streamed */
-#define CVK_OPT_BICG_FOLD 11       /* 1: streamed BiCGSTAB folds each reduction in the consuming
+#define CVK_OPT_BICG_FOLD 11       /* 1: streamed BiCGSTAB and COCG fold each reduction in the consuming
                                       kernel (default); 0: in the producer's last CTA */
 #define CVK_OPT_GMRES_TILES 12     /* 1: GMRES basis passes on bulk-copied row tiles (default,
                                       m <= 32); 0: element-loop kernels */

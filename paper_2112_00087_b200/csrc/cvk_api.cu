@@ -1151,7 +1151,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     int stg[5];
     for (int k = 0; k < 5; ++k) {
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
-        stg[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));  // 4: measured best
+#ifndef CVK_STAGES_MAX
+#define CVK_STAGES_MAX 4
+#endif
+        stg[k] = (int)std::min<long long>(CVK_STAGES_MAX, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));  // 4: measured best
     }
     const bool streamed = c->knob.stream && A->nnz > 0 &&
                           (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2
@@ -1160,11 +1163,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
-    const void* sk[7] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s, K.bf_a_s, K.bf_b_s};
+    const void* sk[8] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s, K.bf_a_s, K.bf_b_s, K.cf_a_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // BiCGSTAB with the reductions folded by the consuming kernel (k_bf_*)
-    const bool fold = streamed && solver == CVK_BICGSTAB && c->knob.bicg_fold;
+    const bool fold = streamed && (solver == CVK_BICGSTAB || solver == CVK_COCG) && c->knob.bicg_fold;
     // elementwise phases: grid-stride, 4 elements per thread per trip
 #ifndef CVK_EGRID_MUL
 #define CVK_EGRID_MUL 2
@@ -1208,7 +1211,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const dim3 sgrid((unsigned)c->nsm), sblock((unsigned)sthreads), egrid((unsigned)Ge);
         for (int it = 0; it < kIterPerGraph; ++it) {
-            if (solver == CVK_COCG) {
+            if (solver == CVK_COCG && fold) {  // 2 launches per iteration: A parity 0, B parity 1
+                launch_pdl(K.cf_a_s, sgrid, sblock, pargs[0], smem_for(4), c->stream);
+                launch_pdl(K.cf_b, egrid, block, pargs[1], 0, c->stream);
+            } else if (solver == CVK_COCG) {
                 if (streamed) launch_pdl(K.cg_a_s, sgrid, sblock, args, smem_for(4), c->stream);
                 else launch_pdl(K.cg_a, grid, block, args, smem, c->stream);
                 launch_pdl(K.cg_b, egrid, block, args, 0, c->stream);

@@ -1201,6 +1201,113 @@ __global__ void __launch_bounds__(kThreads, CVK_BFC_MINB) k_bf_c(PArgs a, int pa
     TR(0, S.it, 2);
 }
 
+// ------------------------------------ COCG with consumer-folded reductions --
+// The k_bf_* pattern for COCG (two kernels per iteration, so A always runs
+// with parity 0 and B with parity 1): B's partials (||z||^2, r^T z) go to
+// region 0 and are folded by the next A, A's (p^T q) to region 1, folded by
+// B.  The checks run in the last-CTA kernels' order (k_cg_b's tail then
+// cg_top at A, cg_alpha at B); k_bf_init seeds scal[0] from k_cg_init.
+
+// A: evaluate the previous B and the top of iteration it (cg_top); then
+// p = z + beta p, q = M^-1... (COCG: q = A p), mu = p^T q
+__global__ void __launch_bounds__(kStreamThreads, 1) k_cf_a_s(PArgs a, int par) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    BiScal S = st->scal[par];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!S.first) {
+        double2 tot[2];
+        bf_fold<2>(a, 0, tot);
+        const double relres = sqrt(tot[0].x) / st->bnorm;
+        if (lead) { st->final_relres = relres; st->iters = S.it; }
+        bf_hist(a, st, relres);
+        if (relres <= st->tol) { if (lead) { st->done = 1; st->conv = 1; } return; }
+        S.cur ^= 1;
+        S.it++;
+        // cg_top
+        if (S.it > st->max_iter) { if (lead) st->done = 1; return; }
+        if (cvk_abs(tot[1]) < st->brk) {
+            if (lead) { st->done = 1; st->brk_code = 1; st->iters = S.it - 1; }
+            return;
+        }
+        S.beta = cvk_cdiv(tot[1], S.rho);
+        S.rho = tot[1];
+    }
+    const bool first = S.first != 0;
+    if (lead) { BiScal W = S; W.first = 0; st->scal[par ^ 1] = W; }
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    const double2 beta = S.beta;
+    const double2* __restrict__ z = V.z;
+    const double2* __restrict__ pc = S.cur ? V.p1 : V.p0;
+    double2* __restrict__ pn = S.cur ? V.p0 : V.p1;
+    double2* __restrict__ q = V.q;
+    const double2* vecs[2] = {z, first ? nullptr : pc};
+    StreamLayout L{a.capk, 2, a.nst[4]};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[1] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 { return ch.v(0, l); };  // p (pre)
+        auto xg = [&](int c) -> double2 { return first ? z[c] : cvk_add(cvk_mul(beta, pc[c]), z[c]); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const double2 pi = ch.v(0, t);
+        const int row = ch.r0 + t;
+        pn[row] = pi;
+        q[row] = y;
+        acc_udot(acc[0], pi, y);
+    }, SPROF(1), [&](int t, const Chunk& ch) {
+        if (!first) ch.set(0, t, cvk_add(cvk_mul(beta, ch.v(1, t)), ch.v(0, t)));
+    });
+    bf_publish<1, kStreamThreads>(acc, a, 1);
+}
+
+// B: alpha = rho / mu (cg_alpha); x += alpha p, r -= alpha q, z = M^-1 r;
+// ||z||^2, r^T z
+__global__ void __launch_bounds__(kThreads) k_cf_b(PArgs a, int par) {
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    BiScal S = st->scal[par];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    {
+        double2 tot[1];
+        bf_fold<1>(a, 1, tot);
+        if (cvk_abs(tot[0]) < st->brk) {
+            if (lead) { st->done = 1; st->brk_code = 8; st->iters = S.it - 1; }
+            return;
+        }
+        S.alpha = cvk_cdiv(S.rho, tot[0]);
+    }
+    if (lead) st->scal[par ^ 1] = S;
+    const int n = a.A.n;
+    CgVecs V(a.work, (size_t)n);
+    const double2 alpha = S.alpha, nal = cvk_neg(S.alpha);
+    // S.cur is A's (A flipped it before its SpMV): A wrote the new p into pn
+    const double2* __restrict__ pn = S.cur ? V.p0 : V.p1;
+    const double2* __restrict__ q = V.q;
+    double2* __restrict__ r = V.r;
+    double2* __restrict__ z = V.z;
+    double2* __restrict__ x = a.x;
+    const double2* __restrict__ dinv = a.dinv;
+    struct L5 { double2 x, p, r, q, d; };
+    CAcc acc[2] = {};
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L5{x[i], pn[i], r[i], q[i], dinv ? __ldg(dinv + i) : make_double2(1.0, 0.0)}; },
+        [&](int i, const L5& v) {
+            x[i] = cvk_add(v.x, cvk_mul(alpha, v.p));
+            const double2 ri = cvk_add(v.r, cvk_mul(nal, v.q));
+            const double2 zi = dinv ? cvk_mul(v.d, ri) : ri;
+            r[i] = ri;
+            z[i] = zi;
+            acc_norm(acc[0], zi);
+            acc_udot(acc[1], ri, zi);
+        });
+    bf_publish<2, kThreads>(acc, a, 0);
+}
+
 // after k_bi_init (r0, shadow, x0, ||r0||, <r0, r0>, top of iteration 1):
 // its scalars into scal[0] for the first k_bf_a_s
 __global__ void k_bf_init(PArgs a) {
@@ -1279,6 +1386,8 @@ PhasedKernels kernels_all() {
     k.bf_b_s = (const void*)k_bf_b_s;
     k.bf_c = (const void*)k_bf_c;
     k.bf_init = (const void*)k_bf_init;
+    k.cf_a_s = (const void*)k_cf_a_s;
+    k.cf_b = (const void*)k_cf_b;
     return k;
 }
 

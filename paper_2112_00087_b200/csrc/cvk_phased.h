@@ -44,6 +44,8 @@ struct PhasedKernels {
     // BiCGSTAB with the reductions folded by the consuming kernel (every CTA,
     // redundantly): (PArgs, int parity)
     const void *bf_a_s, *bf_b_s, *bf_c, *bf_init;
+    // COCG with consumer-folded reductions (k_cf_*): (PArgs, int parity)
+    const void *cf_a_s, *cf_b;
 };
 
 PhasedKernels phased_kernels();

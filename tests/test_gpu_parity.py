@@ -453,22 +453,24 @@ def test_stream_flavors_bitwise(cvk, oracle, knobs, solver):
         assert a_.report.residual_history == b_.report.residual_history
 
 
-def test_consumer_folded_bicgstab_bitwise(cvk, oracle, knobs):
-    """The streamed BiCGSTAB with every reduction folded by the consuming
-    kernel (k_bf_*, default) = the last-CTA-fold kernels, bit for bit, on a
-    system large enough to stream (several graphs of 8 iterations, history,
-    max_iter exhaustion and the zero rhs)."""
+@pytest.mark.parametrize("solver", ["bicgstab", "cocg"])
+def test_consumer_folded_bitwise(cvk, oracle, knobs, solver):
+    """The streamed BiCGSTAB / COCG with every reduction folded by the
+    consuming kernel (k_bf_* / k_cf_*, default) = the last-CTA-fold kernels,
+    bit for bit, on a system large enough to stream (several graphs of 8
+    iterations, history, max_iter exhaustion and the zero rhs)."""
     P = cvk
     rp, ci, v, b = cavity(oracle, 0.0075, f=60.0, adm=0.01)
     A = mat(P, rp, ci, v)
     M = P.jacobi(A)
+    sid = P.solver_id(solver)
     knobs(phased_min_n=0)
     out = {}
     for fold in (1, 0):
         knobs(bicg_fold=fold)
-        r = P.bicgstab(A, b, M, P.SolverOptions(tol=1e-10, max_iter=5000, record_history=True))
-        e = P.bicgstab(A, b, M, P.SolverOptions(tol=1e-30, max_iter=13))
-        z = P.bicgstab(A, np.zeros_like(b), M)
+        r = P.solve(sid, A, b, M, P.SolverOptions(tol=1e-10, max_iter=5000, record_history=True))
+        e = P.solve(sid, A, b, M, P.SolverOptions(tol=1e-30, max_iter=13))
+        z = P.solve(sid, A, np.zeros_like(b), M, P.SolverOptions())
         out[fold] = (r, e, z)
     (a1, e1, z1), (a0, e0, z0) = out[1], out[0]
     assert a1.report.converged and a1.report.iterations == a0.report.iterations
