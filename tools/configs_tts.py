@@ -49,6 +49,8 @@ def rep_row(r, extra=None):
 
 
 SOLVERS = [("bicgstab", {}), ("bicgstab_l", {"l": 8}), ("tfqmr", {}), ("gmres", {"m": 30}), ("cocg", {})]
+if os.environ.get("TTS_SOLVERS"):  # re-measure some solvers, keep the other rows
+    SOLVERS = [sv for sv in SOLVERS if sv[0] in os.environ["TTS_SOLVERS"].split(",")]
 
 
 def cavity(h, f, beta):
@@ -82,6 +84,8 @@ def c2():
     freqs = [50.0 * k for k in range(1, 11)]
     out = {"n": g.size(), "tol": 1e-8, "budget": "max_iter 20000 (BiCGSTAB, tfQMR, COCG), 3000 cycles "
            "(BiCGSTAB(8)), 200000 Arnoldi steps (GMRES(30))", "rows": []}
+    keep = {sv[0] for sv in SOLVERS}
+    out["rows"] = [r for r in res.get("c2", {}).get("rows", []) if r["solver"] not in keep]
     budget = {"bicgstab": 20000, "bicgstab_l": 3000, "tfqmr": 20000, "gmres": 200000, "cocg": 40000}
     for s, kw in SOLVERS:
         t = frequency_sweep(g, 340.0, np.ones(g.roof_size(), np.complex128), freqs, solver=s,
