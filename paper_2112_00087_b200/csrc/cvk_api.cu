@@ -1163,11 +1163,12 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
-    const void* sk[8] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s, K.bf_a_s, K.bf_b_s, K.cf_a_s};
+    const void* sk[10] = {K.bi_a_s, K.bi_b_s, K.tf_e_s, K.tf_o_s, K.cg_a_s, K.bf_a_s, K.bf_b_s, K.cf_a_s,
+                          K.tq_e_s, K.tq_o_s};
     if (streamed)
         for (const void* f : sk) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // BiCGSTAB with the reductions folded by the consuming kernel (k_bf_*)
-    const bool fold = streamed && (solver == CVK_BICGSTAB || solver == CVK_COCG) && c->knob.bicg_fold;
+    const bool fold = streamed && c->knob.bicg_fold;  // BiCGSTAB, COCG, tfQMR
     // elementwise phases: grid-stride, 4 elements per thread per trip
 #ifndef CVK_EGRID_MUL
 #define CVK_EGRID_MUL 2
@@ -1218,7 +1219,7 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
                 if (streamed) launch_pdl(K.cg_a_s, sgrid, sblock, args, smem_for(4), c->stream);
                 else launch_pdl(K.cg_a, grid, block, args, smem, c->stream);
                 launch_pdl(K.cg_b, egrid, block, args, 0, c->stream);
-            } else if (fold) {  // 3 launches per iteration, parity 0 1 0 | 1 0 1 | ...
+            } else if (solver == CVK_BICGSTAB && fold) {  // 3 launches per iteration, parity 0 1 0 | 1 0 1 | ...
                 const int p0 = (3 * it) & 1;
                 launch_pdl(K.bf_a_s, sgrid, sblock, pargs[p0], smem_for(0), c->stream);
                 launch_pdl(K.bf_b_s, sgrid, sblock, pargs[p0 ^ 1], smem_for(1), c->stream);
@@ -1232,6 +1233,11 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
                     launch_pdl(K.bi_b, grid, block, args, smem, c->stream);
                 }
                 launch_pdl(K.bi_c, egrid, block, args, 0, c->stream);
+            } else if (fold) {  // tfQMR, 3 launches per iteration as k_bf_*
+                const int p0 = (3 * it) & 1;
+                launch_pdl(K.tq_w, egrid, block, pargs[p0], 0, c->stream);
+                launch_pdl(K.tq_e_s, sgrid, sblock, pargs[p0 ^ 1], smem_for(2), c->stream);
+                launch_pdl(K.tq_o_s, sgrid, sblock, pargs[p0], smem_for(3), c->stream);
             } else {
                 launch_pdl(K.tf_w, egrid, block, args, 0, c->stream);
                 if (streamed) {
@@ -1262,6 +1268,10 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     } else {
         CK(launch_pdl(K.tf_init, grid, block, args, 0, c->stream));
         CK(launch_pdl(K.tf_init2, grid, block, args, smem, c->stream));
+        if (fold) {
+            CK(launch_pdl(K.tq_seed, dim3(1), dim3(1), args, 0, c->stream));
+            launches += 1;
+        }
         launches += 2;
     }
     long long graphs = 0;

@@ -1308,6 +1308,186 @@ __global__ void __launch_bounds__(kThreads) k_cf_b(PArgs a, int par) {
     bf_publish<2, kThreads>(acc, a, 0);
 }
 
+// ----------------------------------- tfQMR with consumer-folded reductions --
+// The k_bf_* pattern for tfQMR (three launches per iteration: W elementwise,
+// E and O on the ring).  W's partial (||w||^2) goes to region 0 and is
+// folded by E, E's (||w||^2, <shadow, w>) to region 1 for O, O's (sigma) to
+// region 2 for the next W; each consumer runs its producer's tail in the
+// last-CTA kernels' order, and CTA 0 keeps pending_x / eta in the state for
+// k_tf_fix.  k_tq_seed copies k_tf_init2's scalars into tscal[0].
+
+__device__ __forceinline__ void tq_theta(TfScal& S, double ww) {
+    S.theta = sqrt(ww) / S.tau;
+    const double c = 1.0 / sqrt(1.0 + S.theta * S.theta);
+    S.tau = S.tau * S.theta * c;
+    S.eta = cvk_scale(c * c, S.alpha);
+}
+
+// W: the previous O's tail (cur, it, tf_even_head); w -= alpha au, d = coef d + u; ||w||^2
+__global__ void __launch_bounds__(kThreads) k_tq_w(PArgs a, int par) {
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    TfScal S = st->tscal[par];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!S.first) {
+        double2 tot[1];
+        bf_fold<1>(a, 2, tot);
+        if (lead) st->pending_x = 0;
+        S.cur ^= 1;
+        S.it++;
+        if (S.it > st->max_iter) { if (lead) st->done = 1; return; }
+        if (cvk_abs(tot[0]) < st->brk) { if (lead) { st->done = 1; st->brk_code = 6; } return; }
+        S.alpha = cvk_cdiv(S.rho, tot[0]);
+    }
+    if (lead) { TfScal W = S; W.first = 0; st->tscal[par ^ 1] = W; }
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 nal = cvk_neg(S.alpha);
+    const double2 coef = cvk_cdiv(cvk_scale(S.theta * S.theta, S.eta), S.alpha);
+    const double2* __restrict__ uc = S.cur ? V.u1 : V.u0;
+    CAcc acc[1] = {};
+    struct L4 { double2 w, au, d, u; };
+    for_elems_batched<kElemBatch>(
+        n, [&](int i) { return L4{V.w[i], V.au[i], V.d[i], uc[i]}; },
+        [&](int i, const L4& v) {
+            const double2 wi = cvk_add(v.w, cvk_mul(nal, v.au));
+            V.w[i] = wi;
+            V.d[i] = cvk_add(cvk_mul(coef, v.d), v.u);
+            acc_norm(acc[0], wi);
+        });
+    bf_publish<1, kThreads>(acc, a, 0);
+}
+
+// E: W's tail (theta, tau, eta, the even residual estimate); then the even
+// tail + odd head of k_tf_e_s
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tq_e_s(PArgs a, int par) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    TfScal S = st->tscal[par];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    {
+        double2 tot[1];
+        bf_fold<1>(a, 0, tot);
+        tq_theta(S, tot[0].x);
+        const long long hs = 2 * (S.it - 1);
+        const double relres = S.tau * sqrt((double)(hs + 2)) / st->bnorm;
+        if (lead) { st->pending_x = 1; st->eta = S.eta; st->final_relres = relres; st->iters = hs / 2 + 1; }
+        if (relres <= st->tol) { if (lead) { st->done = 1; st->conv = 1; } return; }
+    }
+    if (lead) st->tscal[par ^ 1] = S;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 nal = cvk_neg(S.alpha);
+    const double2 eta_e = S.eta;
+    const double2 coef = cvk_cdiv(cvk_scale(S.theta * S.theta, S.eta), S.alpha);
+    const double2* __restrict__ uc = S.cur ? V.u1 : V.u0;
+    double2* __restrict__ un = S.cur ? V.u0 : V.u1;
+    const double2* __restrict__ vv = V.v;
+    const double2* vecs[7] = {uc, vv, a.dinv, V.d, a.x, V.w, V.sh};
+    StreamLayout L{a.capk, 7, a.nst[2]};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[2] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds u - alpha v (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(nal, ch.v(1, l)));
+        };
+        auto xg = [&](int c) -> double2 { return cvk_add(uc[c], cvk_mul(nal, vv[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const int row = ch.r0 + t;
+        const double2 ui = xs(t);
+        const double2 ai = prec_staged(a, ch, 2, t, y);
+        un[row] = ui;
+        V.au[row] = ai;
+        const double2 di = ch.v(3, t);
+        a.x[row] = cvk_add(ch.v(4, t), cvk_mul(eta_e, di));
+        const double2 wi = cvk_add(ch.v(5, t), cvk_mul(nal, ai));
+        V.w[row] = wi;
+        V.d[row] = cvk_add(cvk_mul(coef, di), ui);
+        acc_norm(acc[0], wi);
+        acc_dot(acc[1], ch.v(6, t), wi);
+    }, SPROF(3), [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(nal, ch.v(1, t))));
+    });
+    bf_publish<2, kStreamThreads>(acc, a, 1);
+}
+
+// O: E's tail (cur, theta, tau, eta, the odd residual estimate, rho, beta);
+// then the odd tail of k_tf_o_s
+__global__ void __launch_bounds__(kStreamThreads, 1) k_tq_o_s(PArgs a, int par) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+    PState* st = a.st;
+    if (st->done) return;
+    TfScal S = st->tscal[par];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    {
+        double2 tot[2];
+        bf_fold<2>(a, 1, tot);
+        S.cur ^= 1;
+        tq_theta(S, tot[0].x);
+        const long long hs = 2 * (S.it - 1) + 1;
+        const double relres = S.tau * sqrt((double)(hs + 2)) / st->bnorm;
+        if (lead) { st->pending_x = 1; st->eta = S.eta; st->final_relres = relres; st->iters = hs / 2 + 1; }
+        bf_hist(a, st, relres);
+        if (relres <= st->tol) { if (lead) { st->done = 1; st->conv = 1; } return; }
+        if (cvk_abs(S.rho) < st->brk) { if (lead) { st->done = 1; st->brk_code = 1; } return; }
+        S.beta = cvk_cdiv(tot[1], S.rho);
+        S.rho = tot[1];
+    }
+    if (lead) st->tscal[par ^ 1] = S;
+    const int n = a.A.n;
+    TfVecs V(a.work, (size_t)n);
+    const double2 beta = S.beta, eta_o = S.eta;
+    const double2* __restrict__ uc = S.cur ? V.u1 : V.u0;
+    double2* __restrict__ un = S.cur ? V.u0 : V.u1;
+    const double2* __restrict__ w = V.w;
+    const double2* vecs[8] = {w, uc, a.dinv, V.v, V.au, a.x, V.d, V.sh};
+    StreamLayout L{a.capk, 8, a.nst[3]};
+    L.ngather = 2;
+    L.pf_rows = a.pf_rows;
+    CAcc acc[1] = {};
+    stream_rows(a.A, L, vecs, smem, [&](int t, const Chunk& ch) {
+        auto xs = [&](int l) -> double2 {  // slot 0 of the chunk rows holds w + beta u (pre)
+            return l < kStreamRows ? ch.v(0, l) : cvk_add(ch.v(0, l), cvk_mul(beta, ch.v(1, l)));
+        };
+        auto xg = [&](int c) -> double2 { return cvk_add(w[c], cvk_mul(beta, uc[c])); };
+        const double2 y = chunk_row_sum<kBatch>(ch, t, xs, xg);
+        const int row = ch.r0 + t;
+        const double2 un_i = xs(t);
+        const double2 an = prec_staged(a, ch, 2, t, y);
+        un[row] = un_i;
+        double2 vi = cvk_add(cvk_mul(beta, ch.v(3, t)), ch.v(4, t));
+        vi = cvk_add(cvk_mul(beta, vi), an);
+        V.v[row] = vi;
+        V.au[row] = an;
+        a.x[row] = cvk_add(ch.v(5, t), cvk_mul(eta_o, ch.v(6, t)));
+        acc_dot(acc[0], ch.v(7, t), vi);
+    }, SPROF(3), [&](int t, const Chunk& ch) {
+        ch.set(0, t, cvk_add(ch.v(0, t), cvk_mul(beta, ch.v(1, t))));
+    });
+    bf_publish<1, kStreamThreads>(acc, a, 2);
+}
+
+__global__ void k_tq_seed(PArgs a) {
+    pdl_enter();
+    PState* st = a.st;
+    TfScal S;
+    S.rho = st->rho;
+    S.alpha = st->alpha;
+    S.beta = st->beta;
+    S.eta = st->eta;
+    S.theta = st->theta;
+    S.tau = st->tau;
+    S.it = st->it;
+    S.cur = st->cur;
+    S.first = 1;
+    st->tscal[0] = S;
+}
+
 // after k_bi_init (r0, shadow, x0, ||r0||, <r0, r0>, top of iteration 1):
 // its scalars into scal[0] for the first k_bf_a_s
 __global__ void k_bf_init(PArgs a) {
@@ -1388,6 +1568,10 @@ PhasedKernels kernels_all() {
     k.bf_init = (const void*)k_bf_init;
     k.cf_a_s = (const void*)k_cf_a_s;
     k.cf_b = (const void*)k_cf_b;
+    k.tq_w = (const void*)k_tq_w;
+    k.tq_e_s = (const void*)k_tq_e_s;
+    k.tq_o_s = (const void*)k_tq_o_s;
+    k.tq_seed = (const void*)k_tq_seed;
     return k;
 }
 

@@ -19,6 +19,15 @@ struct BiScal {
     int cur, first;
 };
 
+// tfQMR scalars of the consumer-fold kernels (k_tq_*), double-buffered the
+// same way.
+struct TfScal {
+    double2 rho, alpha, beta, eta;
+    double theta, tau;
+    long long it;
+    int cur, first;
+};
+
 // Solver state carried between phase kernels (device memory).  Written only
 // by the last-arriving CTA of each phase kernel (CTA 0 for k_bf_*); read by
 // the next kernel.
@@ -30,6 +39,7 @@ struct PState {
     int warm;  // BiCGSTAB: start from the x passed in (k_bi_init)
     unsigned counter[4];
     BiScal scal[2];
+    TfScal tscal[2];
 };
 
 struct PhasedKernels {
@@ -46,6 +56,8 @@ struct PhasedKernels {
     const void *bf_a_s, *bf_b_s, *bf_c, *bf_init;
     // COCG with consumer-folded reductions (k_cf_*): (PArgs, int parity)
     const void *cf_a_s, *cf_b;
+    // tfQMR with consumer-folded reductions (k_tq_*): (PArgs, int parity); seed (PArgs)
+    const void *tq_w, *tq_e_s, *tq_o_s, *tq_seed;
 };
 
 PhasedKernels phased_kernels();

@@ -453,10 +453,10 @@ def test_stream_flavors_bitwise(cvk, oracle, knobs, solver):
         assert a_.report.residual_history == b_.report.residual_history
 
 
-@pytest.mark.parametrize("solver", ["bicgstab", "cocg"])
+@pytest.mark.parametrize("solver", ["bicgstab", "cocg", "tfqmr"])
 def test_consumer_folded_bitwise(cvk, oracle, knobs, solver):
-    """The streamed BiCGSTAB / COCG with every reduction folded by the
-    consuming kernel (k_bf_* / k_cf_*, default) = the last-CTA-fold kernels,
+    """The streamed BiCGSTAB / COCG / tfQMR with every reduction folded by the
+    consuming kernel (k_bf_* / k_cf_* / k_tq_*, default) = the last-CTA-fold kernels,
     bit for bit, on a system large enough to stream (several graphs of 8
     iterations, history, max_iter exhaustion and the zero rhs)."""
     P = cvk
