@@ -90,6 +90,7 @@ struct cvk_ctx {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaGraphExec_t gexec = nullptr;
     std::vector<unsigned char> gkey;
+    int gkind = -1;  // kernel set of gexec (solve_phased): updates only within one set
     // phase-kernel GMRES
     void* gst = nullptr;  // cvk::GState
     cudaGraphExec_t gm_exec = nullptr;
@@ -1071,6 +1072,10 @@ static cudaError_t install_graph(cudaGraphExec_t* exec, cudaGraph_t graph) {
     return e;
 }
 
+// ring depth below which the streamed phases are not used (solve_phased,
+// the GMRES Arnoldi SpMV): the tested configuration
+constexpr int kStreamMinStages = 4;
+
 // cudaLaunchKernel with the programmatic-stream-serialization attribute (PDL)
 static cudaError_t launch_pdl(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
@@ -1098,6 +1103,22 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     // many out-of-chunk gathers per row (FEM-3D), 2 x 224 for the 5-point
     // cavity (cvk_phased_g4.cu); CVK_OPT_STREAM_FLAVOR forces one
     bool g4 = A->n > 0 && (double)A->nnz / (double)A->n > 8.0;
+#ifndef CVK_STAGES_MAX
+#define CVK_STAGES_MAX 4
+#endif
+    if (g4) {
+        // the 4-group flavor needs a ring stage per group (4) in each SpMV
+        // phase of the solver; a matrix too wide for that takes 2 x 224
+        int optin0 = 0;
+        CK(cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        const long long avail0 = (long long)optin0 - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
+        const int kv[5] = {5, 5, 7, 8, 2}, kg[5] = {3, 2, 2, 2, 2};
+        const int k0 = solver == CVK_BICGSTAB ? 0 : solver == CVK_COCG ? 4 : 2;
+        const int k1 = solver == CVK_BICGSTAB ? 1 : solver == CVK_COCG ? 4 : 3;
+        for (int k = k0; k <= k1; ++k)
+            if (std::min<long long>(CVK_STAGES_MAX, avail0 / (long long)cvk_g4::flavor_stage_bytes(A->capk_g4, kv[k], kg[k])) < 4)
+                g4 = false;
+    }
     if (c->knob.flavor == 2 || c->knob.flavor == 4) g4 = c->knob.flavor == 4;
     cvk::PhasedKernels K;
     if (g4) cvk_g4::flavor_kernels(&K);
@@ -1151,15 +1172,19 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     int stg[5];
     for (int k = 0; k < 5; ++k) {
         const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
-#ifndef CVK_STAGES_MAX
-#define CVK_STAGES_MAX 4
-#endif
         stg[k] = (int)std::min<long long>(CVK_STAGES_MAX, std::max<long long>(0, avail / (long long)stage_bytes_k(k)));  // 4: measured best
     }
+    // the ring needs a stage per consumer group (cvk_stream.cuh): 2 groups in
+    // the 2 x 224 flavor, 4 in the 4 x 128 one.  Streaming also requires the
+    // measured-best depth of 4 (kStreamMinStages): a 3-stage COCG ring
+    // faulted intermittently on the B200 (2 of 6 runs at 1M DOF; no
+    // sanitizer finding), so shallower rings take the thread-per-row phases.
+    const int ngroups = (sthreads - 32) / (g4 ? cvk_g4::flavor_stream_rows() : cvk::flavor_stream_rows());
+    const int need = std::max(kStreamMinStages, ngroups);
     const bool streamed = c->knob.stream && A->nnz > 0 &&
-                          (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= 2
-                           : solver == CVK_COCG   ? stg[4] >= 2
-                                                  : std::min(stg[2], stg[3]) >= 2);
+                          (solver == CVK_BICGSTAB ? std::min(stg[0], stg[1]) >= need
+                           : solver == CVK_COCG   ? stg[4] >= need
+                                                  : std::min(stg[2], stg[3]) >= need);
     auto smem_for = [&](int k) {
         return g4 ? cvk_g4::flavor_smem_bytes(scapk, kvec[k], kgat[k], stg[k]) : layout_for(k, stg[k]).smem_bytes();
     };
@@ -1208,6 +1233,16 @@ static int solve_phased(cvk_ctx* c, int solver, const cvk_csr* A, const cvk_prec
     const unsigned char* gep = (const unsigned char*)&Ge;
     key.insert(key.end(), gep, gep + sizeof(Ge));
     if (!c->gexec || c->gkey != key) {
+        // a graph of other kernels (another solver, flavor or fold) is never
+        // updated in place, only re-instantiated: cudaGraphExecUpdate accepts
+        // a same-shaped graph of different kernels (BiCGSTAB -> tfQMR, 24
+        // nodes each), and that path faulted intermittently with 3-stage rings
+        const int kind = solver | (S << 4) | ((streamed ? 1 : 0) << 12) | ((g4 ? 1 : 0) << 13) | ((fold ? 1 : 0) << 14);
+        if (c->gexec && c->gkind != kind) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        c->gkind = kind;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const dim3 sgrid((unsigned)c->nsm), sblock((unsigned)sthreads), egrid((unsigned)Ge);
@@ -1352,14 +1387,14 @@ static int solve_gmres_phased(cvk_ctx* c, const cvk_csr* A, const cvk_prec* M, c
     SL.ngather = 1;
     const long long avail = (long long)optin - 8192 - 2 * cvk::kStreamMaxStages * 8 - cvk::kStreamMaxStages * 32;
     int nst = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)SL.stage_bytes()));
-    if (nst < 2 || A->nnz == 0 || !c->knob.stream) nst = 0;
+    if (nst < kStreamMinStages || A->nnz == 0 || !c->knob.stream) nst = 0;
     SL.stages = std::max(1, nst);
     if (nst) CK(cudaFuncSetAttribute(K.spmv_s, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 8192));
     // the basis passes on bulk-copied tiles of the m + 1 vectors (k_g_dd_s /
     // k_g_up_s): at least 2 stages of (m + 1) 128-row vectors
     int tile_smem = optin - 8192 - 4096;
     const int stage_max = cvk::gmres_tile_stage_max(m);
-    const bool tiles = nst && m <= 32 && (long long)tile_smem >= 2LL * stage_max + 256 &&
+    const bool tiles = c->knob.stream && A->nnz > 0 && m <= 32 && (long long)tile_smem >= 2LL * stage_max + 256 &&
                        c->knob.gmres_tiles;
     if (tiles) {
         CK(cudaFuncSetAttribute(K.dd_s, cudaFuncAttributeMaxDynamicSharedMemorySize, tile_smem));

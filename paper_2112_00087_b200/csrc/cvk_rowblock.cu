@@ -766,7 +766,8 @@ extern "C" int cvk_rowblock_create(cvk_ctx* ctx, const cvk_rowblock_desc* d, int
         nst[k] = (int)std::min<long long>(4, std::max<long long>(0, avail / (long long)L1.stage_bytes()));
     }
     const long long smin = cvk_ctx_knob(ctx, CVK_OPT_RB_STREAM_MIN);
-    R->streamed = d->nnz > 0 && d->n_own >= smin && std::min(nst[0], nst[1]) >= 2 && cvk_ctx_knob(ctx, CVK_OPT_STREAM);
+    // the tested ring depth (4; cvk_api.cu kStreamMinStages)
+    R->streamed = d->nnz > 0 && d->n_own >= smin && std::min(nst[0], nst[1]) >= 4 && cvk_ctx_knob(ctx, CVK_OPT_STREAM);
     if (R->streamed) {
         for (int k = 0; k < 2; ++k) {
             cvk::StreamLayout L{capk, kv[k], nst[k]};

@@ -215,6 +215,11 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     const int G = gridDim.x;
     const int tid = threadIdx.x;
     const int ST = L.stages;
+    // a group waits on the stage of its next chunk with the parity of that
+    // chunk's ring cycle: unambiguous only with at least one stage per group
+    // (the launcher guarantees it; a 3-stage ring under the 4-group flavor
+    // read stale stages -- found by compute-sanitizer)
+    if (ST < kStreamGroups) __trap();
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full + s, 1);
