@@ -163,7 +163,8 @@ int cvk_get_exec_mode(cvk_ctx *ctx);
 #define CVK_OPT_UNIFORM_OFFDIAG 13 /* 1: streamed SpMVs check each solve's matrix for off-diagonal
                                       values that are all bitwise equal (constant-coefficient
                                       stencils) and then stream only the diagonal; 0: off (default:
-                                      the phases are consumer-bound, the bytes saved buy ~2.5%) */
+                                      the phases are consumer-bound, the bytes saved buy ~2.5%).
+                                      Takes effect in builds with -DCVK_UNIFORM_OFFDIAG only */
 int cvk_ctx_set_option(cvk_ctx *ctx, int key, int64_t value);
 int cvk_ctx_get_option(cvk_ctx *ctx, int key, int64_t *value);
 

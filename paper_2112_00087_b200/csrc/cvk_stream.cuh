@@ -124,8 +124,8 @@ struct Chunk {
 // own rows; l = Chunk::stage_index) and xg(c) otherwise.  The (value, column)
 // pairs of a batch come from shared memory; the global gathers of a batch are
 // all issued before the first product.
-template <int BATCH, class XS, class XG>
-__device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs, XG&& xg) {
+template <int BATCH, bool UNI, class XS, class XG>
+__device__ __forceinline__ double2 chunk_row_sum_t(const Chunk& ch, int t, XS&& xs, XG&& xg) {
     const int b = ch.rp[t] - ch.k0, e = ch.rp[t + 1] - ch.k0;
     double2 acc = make_double2(0.0, 0.0);
     for (int k = b; k < e; k += BATCH) {
@@ -135,8 +135,13 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
         for (int u = 0; u < BATCH; ++u)
             if (k + u < e) {
                 c[u] = ch.ci[k + u + ch.cio];
-                a[u] = ch.uni ? (c[u] == ch.r0 + t ? ch.av[t] : ch.coff) : ch.av[k + u];
+                if (!UNI) a[u] = ch.av[k + u];
             }
+        if (UNI) {
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                if (k + u < e) a[u] = c[u] == ch.r0 + t ? ch.av[t] : ch.coff;
+        }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u)
             if (k + u < e) {
@@ -148,6 +153,16 @@ __device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs
             if (k + u < e) acc = cvk_add(acc, cvk_mul(a[u], xv[u]));
     }
     return acc;
+}
+
+// uniform off-diagonal chunks (Chunk::uni) take their own loop: the general
+// one keeps its (value, column) loads independent
+template <int BATCH, class XS, class XG>
+__device__ __forceinline__ double2 chunk_row_sum(const Chunk& ch, int t, XS&& xs, XG&& xg) {
+#ifdef CVK_UNIFORM_OFFDIAG
+    if (ch.uni) return chunk_row_sum_t<BATCH, true>(ch, t, xs, xg);
+#endif
+    return chunk_row_sum_t<BATCH, false>(ch, t, xs, xg);
 }
 
 // The producer/consumer ring.  `vecs` lists the row-local vectors to stage
@@ -230,7 +245,14 @@ __device__ __forceinline__ void stream_rows(const Csr& A, const StreamLayout& L,
     __syncthreads();
     const int first = blockIdx.x;
     const int cnt = first < nchunks ? (nchunks - 1 - first) / G + 1 : 0;
+    // uniform off-diagonal values (CVK_OPT_UNIFORM_OFFDIAG) only in builds
+    // with -DCVK_UNIFORM_OFFDIAG: the second row-sum loop alone cost the
+    // default build 2.5 us per BiCGSTAB iteration, and the format bought 2.5%
+#ifdef CVK_UNIFORM_OFFDIAG
     const bool uni = A.dg != nullptr && __ldcg(&A.uni[0].x) != 0.0;
+#else
+    const bool uni = false;
+#endif
     const double2 coff = uni ? __ldcg(A.uni + 1) : make_double2(0.0, 0.0);
     if (tid >= kStreamGroups * kStreamRows) {
         const int lane = tid & 31;
