@@ -27,7 +27,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 CU_SOURCES = ["cvk_api.cu", "cvk_blas.cu", "cvk_krylov.cu", "cvk_phased.cu", "cvk_ddm.cu", "cvk_assemble.cu", "cvk_gmres.cu", "cvk_bicgl.cu", "cvk_rowblock.cu", "cvk_mmio.cu", "cvk_phased_g4.cu", "cvk_ilu.cu", "cvk_asm.cu"]
-HEADERS = ["cvk_phased.cu", "cvk_complex.h", "cvk_engine.cuh", "cvk_kernels.h", "cvk_phased.h", "cvk_stream.cuh"]
+HEADERS = ["cvk_phased.cu", "cvk_complex.h", "cvk_engine.cuh", "cvk_kernels.h", "cvk_phased.h", "cvk_stream.cuh",
+           "cvk_dcgs2.cuh", "cvk_tiles.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
